@@ -1,0 +1,141 @@
+/*
+ * rmx.h -- C ABI of librmx.so, the B200 (sm_100a) max-null engine.
+ *
+ * The reference (rapidmaxnull 0.1.0, pure Python) has no FFI; its boundary is
+ * the Python module API.  Each entry point below replaces the numerical work
+ * behind one reference function and is bound by
+ * paper_1703_01506_b200/_native.py (ctypes).  INTEGRATION.md shows the
+ * binding a reference maintainer would add.
+ *
+ * Conventions
+ *   - Every array pointer is a DEVICE pointer owned by the caller (allocated
+ *     e.g. as a torch tensor on the current device).  Host pointers are only
+ *     the rmx_status out-parameter and scalar arguments.
+ *   - `stream` is a cudaStream_t (passed as void*); all work is stream-
+ *     ordered.  Entry points that must decide on device results (fallback
+ *     paths, error detection) synchronise that stream before returning.
+ *   - Layouts follow the reference: x is the DataMatrix.values layout
+ *     (v x n row-major float64, reference model.py:27-34); orders[p] is
+ *     PermutationPlan.shuffle(p) as int16 (reference model.py:100-105);
+ *     T is StatMatrix.values (v x L row-major, reference naive.py:25-34).
+ *   - Return value = rmx_status.code.  Error codes map onto the reference
+ *     exception hierarchy (reference errors.py:8-43):
+ *        RMX_OK 0, RMX_E_USAGE 1 -> UsageError,
+ *        RMX_E_DEGENERATE 2 -> DegenerateVoxelError(voxel, value = mean_diff),
+ *        RMX_E_ILLCOND 3 -> IllConditionedBasisError(value = cond),
+ *        RMX_E_CUDA 4 / RMX_E_NUMERIC 5 -> NumericalError.
+ */
+#ifndef RMX_H_
+#define RMX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMX_OK 0
+#define RMX_E_USAGE 1
+#define RMX_E_DEGENERATE 2
+#define RMX_E_ILLCOND 3
+#define RMX_E_CUDA 4
+#define RMX_E_NUMERIC 5
+
+#define RMX_ABI_VERSION 1
+
+typedef struct rmx_status {
+  int32_t code;
+  int32_t _pad;
+  int64_t perm;  /* permutation index of the failure (global), or -1 */
+  int64_t voxel; /* voxel index of the failure, or -1 */
+  double value;  /* mean_diff (DEGENERATE) / condition number (ILLCOND) */
+  char msg[256];
+} rmx_status;
+
+/* Diagnostics / counters for the last naive call (host struct). */
+typedef struct rmx_naive_stats {
+  int64_t suspects;        /* near-zero-variance entries re-evaluated exactly */
+  int64_t band_candidates; /* fp64 refinements performed */
+  int64_t overflow_perms;  /* permutations re-run by the exhaustive fp64 path */
+  int32_t chunks;          /* voxel chunks per permutation tile */
+  int32_t grid;            /* persistent CTAs of the tensor-core kernel */
+  int32_t stages;          /* smem pipeline depth */
+  int32_t bk;              /* K elements per stage */
+} rmx_naive_stats;
+
+int rmx_abi_version(void);
+
+/* Device capability probe: returns RMX_OK on an sm_100 device, fills SM count. */
+int rmx_device_check(int device, int32_t *sm_count, rmx_status *st);
+
+/* ---------------------------------------------------------------- NaivePT
+ * Replaces reference naive.py:60-109 run_naive (the _max_block loop 49-57:
+ * group_blocks model.py:65-69 + _welch_rows teststat.py:28-50 + column_max
+ * teststat.py:88-90) for permutations [0, L) of `orders`.
+ *
+ * max_out[p]    = max_j t_pj (or max_j |t_pj| when two_sided), float64,
+ *                 bit-identical to the reference (fp64 refinement of the
+ *                 tensor-core candidates);
+ * argmax_out[p] = the voxel attaining it (lowest index on exact ties).
+ * Degenerate voxel (zero pooled variance, unequal means) in any permutation:
+ *   returns RMX_E_DEGENERATE with the first (perm, voxel) in permutation order.
+ */
+size_t rmx_naive_workspace_bytes(int64_t v, int32_t n, int64_t L);
+
+int rmx_naive_maxnull(const double *x, int64_t v, int32_t n, int32_t n1,
+                      const int16_t *orders, int64_t L, int32_t two_sided,
+                      double *max_out, int32_t *argmax_out, void *workspace,
+                      size_t workspace_bytes, void *stream, rmx_status *st,
+                      rmx_naive_stats *stats);
+
+/* The same call split in its three stream-ordered phases so a caller can
+ * time the tensor-core contraction alone (bench.py):
+ *   prepare: K0 -- standardise each voxel in fp64, split Z and Z^2 into
+ *            fp16 hi/lo planes (4 x v x kpad), exact constant-voxel handling;
+ *   tfill:   K1 -- tcgen05 contraction G.[Z|Z^2] with the fused t / top-2
+ *            epilogue (T never leaves TMEM/registers);
+ *   finish:  K2 -- fp64 refinement of the band candidates, suspects and
+ *            fallbacks; synchronises `stream`.  */
+int rmx_naive_prepare(const double *x, int64_t v, int32_t n, int32_t n1, int64_t L,
+                      void *workspace, size_t workspace_bytes, void *stream,
+                      rmx_status *st);
+int rmx_naive_tfill(int64_t v, int32_t n, int32_t n1, const int16_t *orders, int64_t L,
+                    int32_t two_sided, void *workspace, size_t workspace_bytes,
+                    void *stream, rmx_status *st, rmx_naive_stats *stats);
+int rmx_naive_finish(const double *x, int64_t v, int32_t n, int32_t n1,
+                     const int16_t *orders, int64_t L, int32_t two_sided,
+                     double *max_out, int32_t *argmax_out, void *workspace,
+                     size_t workspace_bytes, void *stream, rmx_status *st,
+                     rmx_naive_stats *stats);
+
+/* Debug/validation: the tensor-core statistic t~ for every entry, written
+ * as t_dbg[p * v + j] (float32).  Same kernel as tfill with the epilogue's
+ * store path enabled; used by the parity tests to bound |t~ - t|. */
+int rmx_naive_tfill_debug(int64_t v, int32_t n, int32_t n1, const int16_t *orders,
+                          int64_t L, int32_t two_sided, float *t_dbg, void *workspace,
+                          size_t workspace_bytes, void *stream, rmx_status *st);
+
+/* ---------------------------------------------------------------- exact fp64
+ * Bit-exact statistic matrix (reference _welch_rows arithmetic):
+ *   t_out[p * ld + j] = t(perm p, voxel j), p < L, j < v  (perm-major; the
+ *   caller transposes into StatMatrix's v x L layout).
+ * Replaces the `store[:, i] = col` path (naive.py:55-56) and RapidPT's
+ * training columns (rapid.py:64-69).  Degenerate -> RMX_E_DEGENERATE. */
+int rmx_tstat_exact(const double *x, int64_t v, int32_t n, int32_t n1,
+                    const int16_t *orders, int64_t L, double *t_out, int64_t ld,
+                    void *stream, rmx_status *st);
+
+/* Exact statistic at explicit (perm, voxel) pairs: pairs[2i] = perm row of
+ * `orders`, pairs[2i+1] = voxel.  Outputs t, mean difference and a
+ * degenerate flag per pair.  Replaces tstat_subset (teststat.py:64-77). */
+int rmx_tstat_pairs(const double *x, int64_t v, int32_t n, int32_t n1,
+                    const int16_t *orders, const int32_t *pairs, int64_t npairs,
+                    double *t_out, double *num_out, int32_t *deg_out, void *stream,
+                    rmx_status *st);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RMX_H_ */

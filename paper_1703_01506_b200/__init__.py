@@ -1,0 +1,50 @@
+"""B200-native max-null permutation testing (NaivePT / RapidPT hot path).
+
+Drop-in for the reference package ``rapidmaxnull`` 0.1.0's engine entry
+points: same names, signatures, return types and error contract, computed by
+hand-written sm_100a CUDA kernels (librmx.so, include/rmx.h) instead of numpy.
+PyTorch is used only for device memory and streams; there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .domain import (  # noqa: F401
+    Basis,
+    DataMatrix,
+    MaxNull,
+    ObservedColumn,
+    PermutationPlan,
+    RunConfig,
+    StatMatrix,
+    SubspaceModel,
+    min_sample_rate,
+    permute_columns,
+    relabel,
+)
+from .exceptions import (  # noqa: F401
+    DataFormatError,
+    DegenerateVoxelError,
+    EngineUnavailableError,
+    IllConditionedBasisError,
+    NumericalError,
+    UsageError,
+)
+from .naive_engine import NaiveJob, NaiveResult, run_naive, run_naive_ex  # noqa: F401
+from .stats import (  # noqa: F401
+    column_max,
+    pvalue,
+    reject_set,
+    stat_map,
+    threshold_at,
+    tstat_full,
+    tstat_subset,
+)
+
+__all__ = [
+    "__version__", "Basis", "DataMatrix", "MaxNull", "ObservedColumn", "PermutationPlan",
+    "RunConfig", "StatMatrix", "SubspaceModel", "min_sample_rate", "permute_columns", "relabel",
+    "DataFormatError", "DegenerateVoxelError", "EngineUnavailableError",
+    "IllConditionedBasisError", "NumericalError", "UsageError", "NaiveJob", "NaiveResult",
+    "run_naive", "run_naive_ex", "column_max", "pvalue", "reject_set", "stat_map",
+    "threshold_at", "tstat_full", "tstat_subset",
+]

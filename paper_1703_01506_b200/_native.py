@@ -1,0 +1,150 @@
+"""ctypes binding of librmx.so (include/rmx.h).
+
+This module is the only door into the CUDA engine.  There is no CPU
+fallback: if the library or a B200 device is missing, every call raises
+``EngineUnavailableError``.  Status codes are mapped onto the reference's
+exception hierarchy (see exceptions.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+from .exceptions import (
+    DegenerateVoxelError,
+    EngineUnavailableError,
+    IllConditionedBasisError,
+    NumericalError,
+    UsageError,
+)
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librmx.so")
+CSRC = os.path.join(_PKG, "csrc")
+
+RMX_OK, RMX_E_USAGE, RMX_E_DEGENERATE, RMX_E_ILLCOND, RMX_E_CUDA, RMX_E_NUMERIC = range(6)
+
+
+class Status(ctypes.Structure):
+    _fields_ = [
+        ("code", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("perm", ctypes.c_int64),
+        ("voxel", ctypes.c_int64),
+        ("value", ctypes.c_double),
+        ("msg", ctypes.c_char * 256),
+    ]
+
+
+class NaiveStats(ctypes.Structure):
+    _fields_ = [
+        ("suspects", ctypes.c_int64),
+        ("band_candidates", ctypes.c_int64),
+        ("overflow_perms", ctypes.c_int64),
+        ("chunks", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("stages", ctypes.c_int32),
+        ("bk", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+# Every symbol include/rmx.h declares (tests check the library exports them).
+EXPORTS = (
+    "rmx_abi_version",
+    "rmx_device_check",
+    "rmx_naive_workspace_bytes",
+    "rmx_naive_maxnull",
+    "rmx_naive_prepare",
+    "rmx_naive_tfill",
+    "rmx_naive_finish",
+    "rmx_naive_tfill_debug",
+    "rmx_tstat_exact",
+    "rmx_tstat_pairs",
+)
+
+_lib = None
+
+_i64, _i32, _vp, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
+_SP = ctypes.POINTER(Status)
+_NP = ctypes.POINTER(NaiveStats)
+
+_SIGS = {
+    "rmx_abi_version": ([], ctypes.c_int),
+    "rmx_device_check": ([ctypes.c_int, ctypes.POINTER(_i32), _SP], ctypes.c_int),
+    "rmx_naive_workspace_bytes": ([_i64, _i32, _i64], _sz),
+    "rmx_naive_maxnull": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
+                          ctypes.c_int),
+    "rmx_naive_prepare": ([_vp, _i64, _i32, _i32, _i64, _vp, _sz, _vp, _SP], ctypes.c_int),
+    "rmx_naive_tfill": ([_i64, _i32, _i32, _vp, _i64, _i32, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_naive_finish": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
+                         ctypes.c_int),
+    "rmx_naive_tfill_debug": ([_i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _sz, _vp, _SP],
+                              ctypes.c_int),
+    "rmx_tstat_exact": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _SP], ctypes.c_int),
+    "rmx_tstat_pairs": ([_vp, _i64, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _SP],
+                        ctypes.c_int),
+}
+
+
+def build(force: bool = False) -> str:
+    """Compile librmx.so in-tree (nvcc, sm_100a)."""
+    cmd = ["make", "-s", "-C", CSRC]
+    if force:
+        subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load librmx.so; raises EngineUnavailableError (never falls back)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise EngineUnavailableError(
+            f"{LIB_PATH} is missing: build it with `make -C {CSRC}` (nvcc, sm_100a); "
+            "there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def raise_for(rc: int, st: Status) -> None:
+    if rc == RMX_OK:
+        return
+    msg = st.msg.decode(errors="replace")
+    if rc == RMX_E_USAGE:
+        raise UsageError(msg)
+    if rc == RMX_E_DEGENERATE:
+        raise DegenerateVoxelError(int(st.voxel), float(st.value))
+    if rc == RMX_E_ILLCOND:
+        raise IllConditionedBasisError(float(st.value))
+    raise NumericalError(f"librmx error {rc}: {msg}")
+
+
+def ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream) -> int:
+    return int(stream.cuda_stream)
+
+
+def device_check(device: int = 0) -> int:
+    lib = load()
+    st = Status()
+    sms = _i32(0)
+    rc = lib.rmx_device_check(device, ctypes.byref(sms), ctypes.byref(st))
+    if rc != RMX_OK:
+        raise EngineUnavailableError(st.msg.decode(errors="replace"))
+    return int(sms.value)

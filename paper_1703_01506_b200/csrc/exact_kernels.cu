@@ -1,0 +1,417 @@
+// exact_kernels.cu -- the fp64 side of the NaivePT path (compiled with
+// -fmad=false: every double op is an individually rounded IEEE op, so the
+// statistic reproduces the reference's numpy bits, see np_exact.cuh).
+//
+//   k_prep          K0: per-voxel standardisation, fp16 hi/lo split planes
+//   k_const_reduce  voxels constant over all subjects (exact, perm-invariant)
+//   k_refine        K2: fp64 refinement of the tensor-core top-2 candidates
+//   k_transpose     X (v x n) -> X^T (n x v) for the coalesced exact kernels
+//   k_exact_rows    exhaustive exact statistic (materialised T / fallback)
+//   k_exact_reduce  per-permutation max/argmax of k_exact_rows' partials
+//   k_pairs         exact statistic at explicit (perm, voxel) pairs
+#include <cfloat>
+#include <cmath>
+
+#include "np_exact.cuh"
+#include "rmx_internal.cuh"
+
+namespace rmx {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// (value, index) max with the lowest index on ties (np.argmax semantics)
+__device__ __forceinline__ void warp_argmax(double& v, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (ov > v || (ov == v && oj >= 0 && (j < 0 || oj < j))) {
+      v = ov;
+      j = oj;
+    }
+  }
+}
+__device__ __forceinline__ void warp_argmax_f(float& v, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (ov > v || (ov == v && oj >= 0 && (j < 0 || oj < j))) {
+      v = ov;
+      j = oj;
+    }
+  }
+}
+
+__device__ __forceinline__ void note_degenerate(NaiveCounters* c, int64_t perm, int64_t voxel) {
+  unsigned long long key = ((unsigned long long)perm << 32) | (unsigned long long)voxel;
+  atomicMin(&c->deg_key, key);
+}
+
+// ---------------------------------------------------------------- K0
+// One warp per voxel row: fp64 mean / sd, z = (x - mean) / sd, q = z^2,
+// each split into fp16 hi + lo.  Rows constant across all subjects get z = 0
+// (tensor-core t~ = 0) and, if numpy's rounding makes their exact statistic
+// non-zero, are listed for k_const_reduce.
+__global__ void k_prep(PrepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  const int64_t plane = a.v * (int64_t)a.kpad;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < a.v;
+       j += warps) {
+    const double* row = a.x + j * a.n;
+    double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+    for (int k = lane; k < a.n; k += 32) {
+      const double xv = row[k];
+      s += xv;
+      mn = fmin(mn, xv);
+      mx = fmax(mx, xv);
+    }
+    s = warp_sum_d(s);
+    mn = warp_min_d(mn);
+    mx = warp_max_d(mx);
+    const double mean = s / a.n;
+    double ss = 0.0;
+    for (int k = lane; k < a.n; k += 32) {
+      const double d = row[k] - mean;
+      ss += d * d;
+    }
+    ss = warp_sum_d(ss);
+    const bool constant = (mn == mx);
+    const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
+    __half* zh = a.planes + j * a.kpad;
+    for (int k = lane; k < a.kpad; k += 32) {
+      double z = 0.0;
+      if (k < a.n && !constant) z = (row[k] - mean) * inv;
+      const double q = z * z;
+      const __half h_z = __double2half(z);
+      const __half h_q = __double2half(q);
+      zh[k] = h_z;
+      zh[plane + k] = h_q;
+      zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
+      zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
+    }
+    if (constant && lane == 0) {
+      const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
+      if (w.t != 0.0 || w.degenerate) {
+        unsigned slot = atomicAdd(&a.counters->cvox_count, 1u);
+        a.cvox[slot] = (int32_t)j;
+      }
+    }
+  }
+}
+
+__global__ void k_const_reduce(const double* x, int n, int n1, const int32_t* cvox,
+                               NaiveCounters* counters, ConstInfo* out) {
+  __shared__ double sv[32], sa[32];
+  __shared__ int sj[32], sja[32], sd[32];
+  const int count = (int)counters->cvox_count;
+  double best = -DBL_MAX, best_abs = -DBL_MAX;
+  int bj = -1, bja = -1, dj = -1;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int j = cvox[i];
+    const WelchExact w = welch_exact_const(x[(int64_t)j * n], n1, n - n1);
+    if (w.degenerate) {
+      if (dj < 0 || j < dj) dj = j;
+      continue;
+    }
+    if (w.t > best || (w.t == best && j < bj)) best = w.t, bj = j;
+    const double at = fabs(w.t);
+    if (at > best_abs || (at == best_abs && j < bja)) best_abs = at, bja = j;
+  }
+  warp_argmax(best, bj);
+  warp_argmax(best_abs, bja);
+  for (int o = 16; o > 0; o >>= 1) {
+    int od = __shfl_xor_sync(0xffffffffu, dj, o);
+    if (od >= 0 && (dj < 0 || od < dj)) dj = od;
+  }
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (lane == 0) sv[w] = best, sj[w] = bj, sa[w] = best_abs, sja[w] = bja, sd[w] = dj;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    best = lane < nw ? sv[lane] : -DBL_MAX;
+    bj = lane < nw ? sj[lane] : -1;
+    best_abs = lane < nw ? sa[lane] : -DBL_MAX;
+    bja = lane < nw ? sja[lane] : -1;
+    dj = lane < nw ? sd[lane] : -1;
+    warp_argmax(best, bj);
+    warp_argmax(best_abs, bja);
+    for (int o = 16; o > 0; o >>= 1) {
+      int od = __shfl_xor_sync(0xffffffffu, dj, o);
+      if (od >= 0 && (dj < 0 || od < dj)) dj = od;
+    }
+    if (lane == 0) {
+      out->best_t = best;
+      out->best_t_voxel = bj;
+      out->best_abs = best_abs;
+      out->best_abs_voxel = bja;
+      out->deg_voxel = dj;
+      out->count = count;
+      out->deg_num = 0.0;
+      if (dj >= 0) {
+        const WelchExact wd = welch_exact_const(x[(int64_t)dj * n], n1, n - n1);
+        out->deg_num = wd.num;
+        note_degenerate(counters, 0, dj);  // every labelling: first perm of the call
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2
+// One warp per permutation: gather the (perm, chunk) top-2 candidates, keep
+// every voxel whose t~ lies in the band below the best, evaluate those
+// exactly in fp64 (reference arithmetic) and take the max.  A chunk whose
+// runner-up is inside the band might hide a third in-band voxel: the
+// permutation is then queued for the exhaustive exact path.
+constexpr int kRefineWarps = 8;
+
+__global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
+  extern __shared__ int16_t ord_s[];
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * kRefineWarps + w;
+  if (p >= a.L) return;
+  int16_t* ord = ord_s + w * a.n;
+  for (int i = lane; i < a.n; i += 32) ord[i] = a.orders[p * a.n + i];
+  __syncwarp();
+  const int n2 = a.n - a.n1;
+  const int4* cp = a.cand + p * a.slots;
+
+  float tmax = -FLT_MAX;
+  for (int c = lane; c < a.slots; c += 32) {
+    const int4 e = cp[c];
+    if (e.y >= 0) tmax = fmaxf(tmax, __int_as_float(e.x));
+  }
+  for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+  const float band = kBandRel * fmaxf(fabsf(tmax), 1.0f);
+  const float lo = tmax - band;
+
+  double best = -DBL_MAX;
+  int bj = -1;
+  bool overflow = false;
+  unsigned nref = 0;
+  auto consider = [&](int j) {
+    const WelchExact r = welch_exact(a.x + (int64_t)j * a.n, 1, ord, a.n1, n2);
+    ++nref;
+    if (r.degenerate) {
+      note_degenerate(a.counters, p, j);
+      return;
+    }
+    const double key = a.two_sided ? fabs(r.t) : r.t;
+    if (key > best || (key == best && (bj < 0 || j < bj))) {
+      best = key;
+      bj = j;
+    }
+  };
+  if (tmax > -FLT_MAX) {
+    for (int c = lane; c < a.slots; c += 32) {
+      const int4 e = cp[c];
+      if (e.y >= 0 && __int_as_float(e.x) >= lo) consider(e.y);
+      if (e.w >= 0 && __int_as_float(e.z) >= lo) {
+        consider(e.w);
+        overflow = true;
+      }
+    }
+  }
+  const unsigned scount = a.counters->susp_count;
+  if (scount > 0 && scount <= (unsigned)kSuspectCap) {
+    for (unsigned i = lane; i < scount; i += 32)
+      if (a.susp[2 * i] == (int)p) consider(a.susp[2 * i + 1]);
+  }
+  warp_argmax(best, bj);
+  const unsigned any_over = __ballot_sync(0xffffffffu, overflow);
+  for (int o = 16; o > 0; o >>= 1) nref += __shfl_xor_sync(0xffffffffu, nref, o);
+  if (lane == 0) {
+    // constant voxels: the same exact statistic under every labelling
+    const ConstInfo ci = *a.cinfo;
+    const double cb = a.two_sided ? ci.best_abs : ci.best_t;
+    const int cj = a.two_sided ? ci.best_abs_voxel : ci.best_t_voxel;
+    if (cj >= 0 && (cb > best || (cb == best && (bj < 0 || cj < bj)))) {
+      best = cb;
+      bj = cj;
+    }
+    a.max_out[p] = best;
+    a.argmax_out[p] = bj;
+    atomicAdd(&a.counters->band_candidates, nref);
+    if (any_over || bj < 0) {
+      unsigned slot = atomicAdd(&a.counters->overflow_count, 1u);
+      a.overflow[slot] = (int32_t)p;
+    }
+  }
+}
+
+__global__ void k_transpose(const double* __restrict__ x, int64_t v, int n, double* __restrict__ xt) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + r;
+    const int k = k0 + threadIdx.x;
+    if (j < v && k < n) tile[r][threadIdx.x] = x[j * n + k];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r;
+    const int64_t j = j0 + threadIdx.x;
+    if (j < v && k < n) xt[(int64_t)k * v + j] = tile[threadIdx.x][r];
+  }
+}
+
+// grid (nvb, nperm): block (vb, i) evaluates perm list[i] over its voxel
+// stripe using X^T (coalesced across voxels).
+__global__ void k_exact_rows(const double* __restrict__ xt, int64_t v, int n, int n1,
+                             const int16_t* __restrict__ orders, const int32_t* perm_list,
+                             int64_t perm_offset, int two_sided, double* t_out, int64_t ld,
+                             double* part_val, int32_t* part_idx, NaiveCounters* counters) {
+  extern __shared__ int16_t ord[];
+  const int64_t i = blockIdx.y;
+  const int64_t p = perm_list ? perm_list[i] : perm_offset + i;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) ord[k] = orders[p * n + k];
+  __syncthreads();
+  const int64_t per = (v + gridDim.x - 1) / gridDim.x;
+  const int64_t jlo = blockIdx.x * per, jhi = min(v, jlo + per);
+  double best = -DBL_MAX;
+  int bj = -1;
+  for (int64_t j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
+    const WelchExact r = welch_exact(xt + j, v, ord, n1, n - n1);
+    if (r.degenerate) {
+      if (counters) note_degenerate(counters, p, j);
+      continue;
+    }
+    if (t_out) t_out[i * ld + j] = r.t;
+    const double key = two_sided ? fabs(r.t) : r.t;
+    if (key > best || (key == best && (bj < 0 || j < bj))) best = key, bj = (int)j;
+  }
+  if (!part_val) return;
+  __shared__ double sv[32];
+  __shared__ int sj[32];
+  warp_argmax(best, bj);
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (lane == 0) sv[w] = best, sj[w] = bj;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    best = lane < nw ? sv[lane] : -DBL_MAX;
+    bj = lane < nw ? sj[lane] : -1;
+    warp_argmax(best, bj);
+    if (lane == 0) {
+      part_val[i * gridDim.x + blockIdx.x] = best;
+      part_idx[i * gridDim.x + blockIdx.x] = bj;
+    }
+  }
+}
+
+__global__ void k_exact_reduce(const double* part_val, const int32_t* part_idx, int nvb,
+                               const int32_t* perm_list, int64_t nperm, double* max_out,
+                               int32_t* argmax_out) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (i >= nperm) return;
+  double best = -DBL_MAX;
+  int bj = -1;
+  for (int b = lane; b < nvb; b += 32) {
+    const double val = part_val[i * nvb + b];
+    const int j = part_idx[i * nvb + b];
+    if (j >= 0 && (val > best || (val == best && (bj < 0 || j < bj)))) best = val, bj = j;
+  }
+  warp_argmax(best, bj);
+  if (lane == 0) {
+    const int64_t p = perm_list ? perm_list[i] : i;
+    max_out[p] = best;
+    argmax_out[p] = bj;
+  }
+}
+
+__global__ void k_pairs(const double* x, int64_t v, int n, int n1, const int16_t* orders,
+                        const int32_t* pairs, int64_t npairs, double* t_out, double* num_out,
+                        int32_t* deg_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npairs) return;
+  const int64_t p = pairs[2 * i];
+  const int64_t j = pairs[2 * i + 1];
+  const WelchExact r = welch_exact(x + j * n, 1, orders + p * n, n1, n - n1);
+  t_out[i] = r.t;
+  if (num_out) num_out[i] = r.num;
+  if (deg_out) deg_out[i] = r.degenerate ? 1 : 0;
+}
+
+}  // namespace
+
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t s) {
+  const int wpb = 8;
+  int64_t blocks = (a.v + wpb - 1) / wpb;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  k_prep<<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_const_reduce(const double* x, int64_t, int n, int n1, const int32_t* cvox,
+                                NaiveCounters* counters, ConstInfo* out, cudaStream_t s) {
+  k_const_reduce<<<1, 256, 0, s>>>(x, n, n1, cvox, counters, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t s) {
+  const int64_t blocks = (a.L + kRefineWarps - 1) / kRefineWarps;
+  const size_t smem = (size_t)kRefineWarps * a.n * sizeof(int16_t);
+  k_refine<<<(unsigned)blocks, 32 * kRefineWarps, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double* x, int64_t v, int n, double* xt, cudaStream_t s) {
+  dim3 grid((unsigned)((v + 31) / 32), (unsigned)((n + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(x, v, n, xt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1, const int16_t* orders,
+                             const int32_t* perm_list, int64_t nperm, int two_sided,
+                             double* t_out, int64_t ld, double* part_val, int32_t* part_idx,
+                             int nvb, NaiveCounters* counters, cudaStream_t s) {
+  if (nperm <= 0) return cudaSuccess;
+  for (int64_t base = 0; base < nperm; base += 65535) {
+    const int64_t cnt = nperm - base < 65535 ? nperm - base : 65535;
+    dim3 grid((unsigned)nvb, (unsigned)cnt);
+    k_exact_rows<<<grid, 256, n * sizeof(int16_t), s>>>(
+        xt, v, n, n1, orders, perm_list ? perm_list + base : nullptr, base, two_sided,
+        t_out ? t_out + base * ld : nullptr, ld, part_val ? part_val + base * nvb : nullptr,
+        part_idx ? part_idx + base * nvb : nullptr, counters);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_reduce(const double* part_val, const int32_t* part_idx, int nvb,
+                                const int32_t* perm_list, int64_t nperm, double* max_out,
+                                int32_t* argmax_out, cudaStream_t s) {
+  if (nperm <= 0) return cudaSuccess;
+  const int wpb = 8;
+  k_exact_reduce<<<(unsigned)((nperm + wpb - 1) / wpb), 32 * wpb, 0, s>>>(
+      part_val, part_idx, nvb, perm_list, nperm, max_out, argmax_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pairs(const double* x, int64_t v, int n, int n1, const int16_t* orders,
+                         const int32_t* pairs, int64_t npairs, double* t_out, double* num_out,
+                         int32_t* deg_out, cudaStream_t s) {
+  if (npairs <= 0) return cudaSuccess;
+  k_pairs<<<(unsigned)((npairs + 127) / 128), 128, 0, s>>>(x, v, n, n1, orders, pairs, npairs,
+                                                          t_out, num_out, deg_out);
+  return cudaGetLastError();
+}
+
+}  // namespace rmx

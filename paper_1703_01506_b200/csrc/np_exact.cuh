@@ -1,0 +1,153 @@
+// np_exact.cuh -- float64 two-sample statistic, bit-identical to the
+// reference's numpy arithmetic.
+//
+// The reference evaluates (teststat.py:28-50)
+//     m_g  = x_g.mean(axis=-1)             -> add.reduce / n_g
+//     s2_g = x_g.var(axis=-1, ddof=1)      -> add.reduce((x - mean)^2) / (n_g - 1)
+//     t    = (m1 - m2) / sqrt(s2_1/n1 + s2_2/n2)
+// on the fancy-indexed blocks values[:, order[:n1]] / values[:, order[n1:]]
+// (model.py:65-69).  numpy's float64 add.reduce over a contiguous axis is the
+// pairwise sum of loops_utils.h.src: < 8 terms sequential from 0.0; <= 128
+// terms with 8 interleaved accumulators combined as ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) plus a sequential tail; otherwise split at
+// n/2 - (n/2)%8 and recurse.  Reproducing that order with explicitly rounded
+// IEEE ops (no FMA contraction) gives the reference's bits exactly.
+#pragma once
+#include <cstdint>
+
+namespace rmx {
+
+// Subject s of the voxel lives at row[s * stride]: stride 1 for the
+// DataMatrix layout (v x n row-major), stride v for the transposed copy.
+struct GroupVals {  // a[i] = row[ord[i]]
+  const double* row;
+  const int16_t* ord;
+  int64_t stride;
+  __device__ __forceinline__ double operator()(int i) const { return row[ord[i] * stride]; }
+};
+
+struct GroupSqDev {  // a[i] = (row[ord[i]] - mean)^2
+  const double* row;
+  const int16_t* ord;
+  int64_t stride;
+  double mean;
+  __device__ __forceinline__ double operator()(int i) const {
+    double d = __dsub_rn(row[ord[i] * stride], mean);
+    return __dmul_rn(d, d);
+  }
+};
+
+template <class G>
+__device__ __forceinline__ double np_pw_leaf(const G& g, int lo, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, g(lo + i));
+    return res;
+  }
+  double r0 = g(lo + 0), r1 = g(lo + 1), r2 = g(lo + 2), r3 = g(lo + 3);
+  double r4 = g(lo + 4), r5 = g(lo + 5), r6 = g(lo + 6), r7 = g(lo + 7);
+  int i = 8;
+  const int stop = n - (n % 8);
+  for (; i < stop; i += 8) {
+    r0 = __dadd_rn(r0, g(lo + i + 0));
+    r1 = __dadd_rn(r1, g(lo + i + 1));
+    r2 = __dadd_rn(r2, g(lo + i + 2));
+    r3 = __dadd_rn(r3, g(lo + i + 3));
+    r4 = __dadd_rn(r4, g(lo + i + 4));
+    r5 = __dadd_rn(r5, g(lo + i + 5));
+    r6 = __dadd_rn(r6, g(lo + i + 6));
+    r7 = __dadd_rn(r7, g(lo + i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) res = __dadd_rn(res, g(lo + i));
+  return res;
+}
+
+// Depth-bounded recursion (D levels of halving => n <= 128 * 2^D).
+template <int D>
+struct NpPairwise {
+  template <class G>
+  __device__ __noinline__ static double sum(const G& g, int lo, int n) {
+    if (n <= 128) return np_pw_leaf(g, lo, n);
+    int h = n / 2;
+    h -= h % 8;
+    return __dadd_rn(NpPairwise<D - 1>::sum(g, lo, h), NpPairwise<D - 1>::sum(g, lo + h, n - h));
+  }
+};
+template <>
+struct NpPairwise<0> {
+  template <class G>
+  __device__ __noinline__ static double sum(const G& g, int lo, int n) {
+    return np_pw_leaf(g, lo, n);
+  }
+};
+
+template <class G>
+__device__ __forceinline__ double np_pw_sum(const G& g, int n) {
+  return NpPairwise<8>::sum(g, 0, n);  // n <= 32768 (labels are int16: n <= 32767)
+}
+
+struct WelchExact {
+  double t;
+  double num;       // m1 - m2
+  bool degenerate;  // var_term == 0 and num != 0
+};
+
+// Statistic of one voxel row (n doubles) under the labelling `ord`
+// (ord[0..n1) = group 1 in permutation order, ord[n1..n) = group 2).
+__device__ __forceinline__ WelchExact welch_exact(const double* row, int64_t stride,
+                                                  const int16_t* ord, int n1, int n2) {
+  GroupVals a{row, ord, stride}, b{row, ord + n1, stride};
+  const double m1 = __ddiv_rn(np_pw_sum(a, n1), (double)n1);
+  const double m2 = __ddiv_rn(np_pw_sum(b, n2), (double)n2);
+  GroupSqDev da{row, ord, stride, m1}, db{row, ord + n1, stride, m2};
+  const double v1 = __ddiv_rn(np_pw_sum(da, n1), (double)(n1 - 1));
+  const double v2 = __ddiv_rn(np_pw_sum(db, n2), (double)(n2 - 1));
+  const double var_term = __dadd_rn(__ddiv_rn(v1, (double)n1), __ddiv_rn(v2, (double)n2));
+  WelchExact r;
+  r.num = __dsub_rn(m1, m2);
+  if (var_term == 0.0) {
+    r.t = 0.0;
+    r.degenerate = (r.num != 0.0);
+  } else {
+    r.t = __ddiv_rn(r.num, __dsqrt_rn(var_term));
+    r.degenerate = false;
+  }
+  return r;
+}
+
+struct ConstVals {
+  double c;
+  __device__ __forceinline__ double operator()(int) const { return c; }
+};
+struct ConstSqDev {
+  double c, mean;
+  __device__ __forceinline__ double operator()(int) const {
+    double d = __dsub_rn(c, mean);
+    return __dmul_rn(d, d);
+  }
+};
+
+// A voxel whose n values are all equal to c has the same statistic under
+// every labelling; numpy's rounding of the group means can still make it
+// non-zero (e.g. c = 0.1, n1 = 3, n2 = 4), so it is evaluated exactly once.
+__device__ __forceinline__ WelchExact welch_exact_const(double c, int n1, int n2) {
+  const double m1 = __ddiv_rn(np_pw_sum(ConstVals{c}, n1), (double)n1);
+  const double m2 = __ddiv_rn(np_pw_sum(ConstVals{c}, n2), (double)n2);
+  const double v1 = __ddiv_rn(np_pw_sum(ConstSqDev{c, m1}, n1), (double)(n1 - 1));
+  const double v2 = __ddiv_rn(np_pw_sum(ConstSqDev{c, m2}, n2), (double)(n2 - 1));
+  const double var_term = __dadd_rn(__ddiv_rn(v1, (double)n1), __ddiv_rn(v2, (double)n2));
+  WelchExact r;
+  r.num = __dsub_rn(m1, m2);
+  if (var_term == 0.0) {
+    r.t = 0.0;
+    r.degenerate = (r.num != 0.0);
+  } else {
+    r.t = __ddiv_rn(r.num, __dsqrt_rn(var_term));
+    r.degenerate = false;
+  }
+  return r;
+}
+
+}  // namespace rmx

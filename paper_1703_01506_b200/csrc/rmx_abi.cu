@@ -1,0 +1,453 @@
+// rmx_abi.cu -- extern "C" entry points of librmx.so (declared in include/rmx.h)
+// and the host-side driver logic of the NaivePT path: workspace layout,
+// persistent-grid / chunk scheduling, and the decisions that need device
+// results (suspect overflow, exhaustive fallback, degenerate reporting).
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/rmx.h"
+#include "rmx_internal.cuh"
+
+namespace rmx {
+
+size_t tfill_smem_bytes(int bk, int stages, int kpad);
+
+namespace {
+
+constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic smem per CTA on sm_100
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int set_status(rmx_status* st, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+int set_status(rmx_status* st, int code, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(st->msg, sizeof(st->msg), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+void clear_status(rmx_status* st) {
+  if (!st) return;
+  memset(st, 0, sizeof(*st));
+  st->perm = -1;
+  st->voxel = -1;
+}
+
+#define RMX_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return set_status(st, RMX_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+int check_dims(int64_t v, int32_t n, int32_t n1, int64_t L, rmx_status* st) {
+  if (v < 1) return set_status(st, RMX_E_USAGE, "need at least one voxel, got v=%lld", (long long)v);
+  if (n1 < 2 || n - n1 < 2)
+    return set_status(st, RMX_E_USAGE,
+                      "need at least two subjects per group, got n1=%d, n2=%d", n1, n - n1);
+  if (n > 32767) return set_status(st, RMX_E_USAGE, "subject count %d exceeds 32767", n);
+  if (L < 1) return set_status(st, RMX_E_USAGE, "permutation count must be >= 1");
+  if (v > 0x7fffffffLL) return set_status(st, RMX_E_USAGE, "voxel count exceeds int32 range");
+  return RMX_OK;
+}
+
+// Stage/BK choice for the tensor-core kernel; returns false when the A tile
+// does not fit next to a 2-stage ring (n > ~640).
+bool pick_pipeline(int kpad, int* bk, int* stages) {
+  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024;
+  if (a_bytes >= kMaxSmem) return false;
+  const size_t avail = kMaxSmem - a_bytes;
+  int b = kpad <= 32 ? 32 : 64;
+  int s = (int)(avail / ((size_t)2 * 2 * kTileV * b * 2));
+  if (b == 64 && s < 3) {
+    b = 32;
+    s = (int)(avail / ((size_t)2 * 2 * kTileV * b * 2));
+  }
+  s = std::min(s, b == 64 ? 3 : 4);
+  if (s < 2) return false;
+  *bk = b;
+  *stages = s;
+  return true;
+}
+
+}  // namespace
+
+int device_sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
+  NaiveLayout lay{};
+  lay.kpad = (n + 15) / 16 * 16;
+  lay.n_vtiles = (int)((v + kTileV - 1) / kTileV);
+  lay.n_mtiles = (int)((L + kTileM - 1) / kTileM);
+  if (!pick_pipeline(lay.kpad, &lay.bk, &lay.stages)) {
+    lay.bk = 0;
+    lay.stages = 0;
+  }
+  // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
+  lay.groups = lay.kpad <= 128 ? 2 : 1;
+  // Voxel chunks per permutation tile: minimise the static round-robin
+  // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
+  // one chunk of voxel tiles; A-tile rebuild counted as ~1/4 tile).
+  double best_cost = 1e300;
+  int best_c = 1;
+  const int cmax = std::min(lay.n_vtiles, 64);
+  for (int c = 1; c <= cmax; ++c) {
+    const int tpc = (lay.n_vtiles + c - 1) / c;
+    const int nc = (lay.n_vtiles + tpc - 1) / tpc;
+    if (nc != c) continue;
+    const int64_t units = (int64_t)lay.n_mtiles * nc;
+    const int grid = (int)std::min<int64_t>(sm_count, units);
+    double worst = 0;
+    for (int b = 0; b < std::min(grid, 8); ++b) {  // CTA 0.. carry the most units
+      double w = 0;
+      for (int64_t u = b; u < units; u += grid) {
+        const int chunk = (int)(u / lay.n_mtiles);
+        const int tiles = std::min(tpc, lay.n_vtiles - chunk * tpc);
+        w += tiles + 0.25;
+      }
+      worst = std::max(worst, w);
+    }
+    const double cost = worst * (1.0 + 0.001 * c);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_c = c;
+    }
+  }
+  lay.tiles_per_chunk = (lay.n_vtiles + best_c - 1) / best_c;
+  lay.n_chunks = (lay.n_vtiles + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
+  lay.grid = (int)std::min<int64_t>(sm_count, (int64_t)lay.n_mtiles * lay.n_chunks);
+
+  size_t off = 0;
+  lay.off_planes = off;
+  off = align_up(off + (size_t)4 * v * lay.kpad * 2, 1024);
+  lay.off_cand = off;
+  off = align_up(off + (size_t)L * lay.n_chunks * lay.groups * 16, 256);
+  lay.off_susp = off;
+  off = align_up(off + (size_t)kSuspectCap * 8, 256);
+  lay.off_cvox = off;
+  off = align_up(off + (size_t)v * 4, 256);
+  lay.off_overflow = off;
+  off = align_up(off + (size_t)L * 4, 256);
+  lay.off_const = off;
+  off = align_up(off + sizeof(ConstInfo), 256);
+  lay.off_counters = off;
+  off = align_up(off + sizeof(NaiveCounters), 256);
+  lay.total = off;
+  return lay;
+}
+
+namespace {
+
+struct Ws {
+  NaiveLayout lay;
+  uint8_t* base;
+  __half* planes() const { return reinterpret_cast<__half*>(base + lay.off_planes); }
+  int4* cand() const { return reinterpret_cast<int4*>(base + lay.off_cand); }
+  int32_t* susp() const { return reinterpret_cast<int32_t*>(base + lay.off_susp); }
+  int32_t* cvox() const { return reinterpret_cast<int32_t*>(base + lay.off_cvox); }
+  int32_t* overflow() const { return reinterpret_cast<int32_t*>(base + lay.off_overflow); }
+  ConstInfo* cinfo() const { return reinterpret_cast<ConstInfo*>(base + lay.off_const); }
+  NaiveCounters* counters() const { return reinterpret_cast<NaiveCounters*>(base + lay.off_counters); }
+};
+
+int get_ws(int64_t v, int32_t n, int64_t L, void* workspace, size_t bytes, Ws* ws, rmx_status* st) {
+  ws->lay = naive_layout(v, n, L, device_sm_count());
+  ws->base = static_cast<uint8_t*>(workspace);
+  if (!workspace || bytes < ws->lay.total)
+    return set_status(st, RMX_E_USAGE, "workspace of %zu bytes is smaller than the %zu required",
+                      bytes, ws->lay.total);
+  return RMX_OK;
+}
+
+// exhaustive exact fp64 evaluation of `nperm` perms (list or all) -> max/argmax
+int run_exhaustive(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                   const int32_t* perm_list, int64_t nperm, int two_sided, double* max_out,
+                   int32_t* argmax_out, NaiveCounters* counters, cudaStream_t s, rmx_status* st) {
+  if (nperm <= 0) return RMX_OK;
+  double* xt = nullptr;
+  double* pv = nullptr;
+  int32_t* pi = nullptr;
+  const int nvb = (int)std::min<int64_t>(std::max<int64_t>(1, (v + 4095) / 4096), 64);
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xt), (size_t)v * n * sizeof(double), s));
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pv), (size_t)nperm * nvb * sizeof(double), s));
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pi), (size_t)nperm * nvb * sizeof(int32_t), s));
+  RMX_CUDA(launch_transpose(x, v, n, xt, s));
+  RMX_CUDA(launch_exact_rows(xt, v, n, n1, orders, perm_list, nperm, two_sided, nullptr, 0, pv, pi,
+                             nvb, counters, s));
+  RMX_CUDA(launch_exact_reduce(pv, pi, nvb, perm_list, nperm, max_out, argmax_out, s));
+  RMX_CUDA(cudaFreeAsync(xt, s));
+  RMX_CUDA(cudaFreeAsync(pv, s));
+  RMX_CUDA(cudaFreeAsync(pi, s));
+  return RMX_OK;
+}
+
+// Report the first degenerate (perm, voxel) if any; fills mean_diff.
+int report_degenerate(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                      unsigned long long key, cudaStream_t s, rmx_status* st) {
+  if (key == ~0ull) return RMX_OK;
+  const int32_t perm = (int32_t)(key >> 32), voxel = (int32_t)(key & 0xffffffffu);
+  int32_t* dpair = nullptr;
+  double* dt = nullptr;
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dpair), 8, s));
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dt), 16, s));
+  const int32_t hp[2] = {perm, voxel};
+  RMX_CUDA(cudaMemcpyAsync(dpair, hp, 8, cudaMemcpyHostToDevice, s));
+  RMX_CUDA(launch_pairs(x, v, n, n1, orders, dpair, 1, dt, dt + 1, nullptr, s));
+  double h[2] = {0, 0};
+  RMX_CUDA(cudaMemcpyAsync(h, dt, 16, cudaMemcpyDeviceToHost, s));
+  RMX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(dpair, s);
+  cudaFreeAsync(dt, s);
+  st->perm = perm;
+  st->voxel = voxel;
+  st->value = h[1];
+  return set_status(st, RMX_E_DEGENERATE,
+                    "voxel %d: zero pooled variance with group mean difference %.6g "
+                    "(permutation %d); statistic would be infinite",
+                    voxel, h[1], perm);
+}
+
+}  // namespace
+}  // namespace rmx
+
+using namespace rmx;
+
+extern "C" {
+
+int rmx_abi_version(void) { return RMX_ABI_VERSION; }
+
+int rmx_device_check(int device, int32_t* sm_count, rmx_status* st) {
+  clear_status(st);
+  int ndev = 0;
+  RMX_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return set_status(st, RMX_E_USAGE, "device %d not present (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  RMX_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (prop.major != 10)
+    return set_status(st, RMX_E_USAGE, "librmx is built for sm_100a; device %d is sm_%d%d (%s)",
+                      device, prop.major, prop.minor, prop.name);
+  return RMX_OK;
+}
+
+size_t rmx_naive_workspace_bytes(int64_t v, int32_t n, int64_t L) {
+  return naive_layout(v, n, L, device_sm_count()).total;
+}
+
+int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t L,
+                      void* workspace, size_t workspace_bytes, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  Ws ws;
+  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RMX_CUDA(cudaMemsetAsync(ws.counters(), 0, sizeof(NaiveCounters), s));
+  RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
+  PrepArgs pa{x, v, n, n1, ws.lay.kpad, ws.planes(), ws.cvox(), ws.counters()};
+  RMX_CUDA(launch_prep(pa, s));
+  RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
+  return RMX_OK;
+}
+
+static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
+                      int32_t two_sided, float* dbg, void* workspace, size_t workspace_bytes,
+                      void* stream, rmx_status* st, rmx_naive_stats* stats) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  Ws ws;
+  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  if (ws.lay.stages == 0)
+    return set_status(st, RMX_E_USAGE,
+                      "n=%d subjects exceed the tensor-core tile (A tile > smem); "
+                      "use the exact path",
+                      n);
+  const double dn = n, d1 = n1, d2 = n - n1;
+  const double c = (d1 * d2 / dn) * (d1 * d2 / dn);
+  const double T = dn - 1.0;  // sum of z^2 over all subjects
+  const double alpha = c * (1.0 / (d1 * (d1 - 1.0)) - 1.0 / (d2 * (d2 - 1.0)));
+  const double beta = -c * (1.0 / (d1 * d1 * (d1 - 1.0)) + 1.0 / (d2 * d2 * (d2 - 1.0)));
+  const double gamma = c * T / (d2 * (d2 - 1.0));
+  const double bmax = std::fabs(alpha) * T + std::fabs(beta) * d1 * T + gamma;
+  TfillArgs a{};
+  a.orders = orders;
+  a.L = L;
+  a.v = v;
+  a.n = n;
+  a.n1 = n1;
+  a.kpad = ws.lay.kpad;
+  a.nk16 = ws.lay.kpad / 16;
+  a.n_vtiles = ws.lay.n_vtiles;
+  a.n_mtiles = ws.lay.n_mtiles;
+  a.n_chunks = ws.lay.n_chunks;
+  a.tiles_per_chunk = ws.lay.tiles_per_chunk;
+  a.alpha = (float)alpha;
+  a.beta = (float)beta;
+  a.gamma = (float)gamma;
+  a.dthr = (float)(1e-4 * bmax);
+  a.cand = ws.cand();
+  a.susp = ws.susp();
+  a.counters = ws.counters();
+  a.dbg_t = dbg;
+  RMX_CUDA(launch_tfill_tc(ws.lay, a, ws.planes(), two_sided, static_cast<cudaStream_t>(stream)));
+  if (stats) {
+    stats->chunks = ws.lay.n_chunks;
+    stats->grid = ws.lay.grid;
+    stats->stages = ws.lay.stages;
+    stats->bk = ws.lay.bk;
+  }
+  return RMX_OK;
+}
+
+int rmx_naive_tfill(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
+                    int32_t two_sided, void* workspace, size_t workspace_bytes, void* stream,
+                    rmx_status* st, rmx_naive_stats* stats) {
+  return tfill_impl(v, n, n1, orders, L, two_sided, nullptr, workspace, workspace_bytes, stream,
+                    st, stats);
+}
+
+int rmx_naive_tfill_debug(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
+                          int32_t two_sided, float* t_dbg, void* workspace,
+                          size_t workspace_bytes, void* stream, rmx_status* st) {
+  if (!t_dbg) return set_status(st, RMX_E_USAGE, "t_dbg must not be null");
+  return tfill_impl(v, n, n1, orders, L, two_sided, t_dbg, workspace, workspace_bytes, stream, st,
+                    nullptr);
+}
+
+int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                     int64_t L, int32_t two_sided, double* max_out, int32_t* argmax_out,
+                     void* workspace, size_t workspace_bytes, void* stream, rmx_status* st,
+                     rmx_naive_stats* stats) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  Ws ws;
+  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RefineArgs ra{};
+  ra.x = x;
+  ra.orders = orders;
+  ra.L = L;
+  ra.v = v;
+  ra.n = n;
+  ra.n1 = n1;
+  ra.slots = ws.lay.n_chunks * ws.lay.groups;
+  ra.two_sided = two_sided;
+  ra.cand = ws.cand();
+  ra.susp = ws.susp();
+  ra.cinfo = ws.cinfo();
+  ra.counters = ws.counters();
+  ra.overflow = ws.overflow();
+  ra.max_out = max_out;
+  ra.argmax_out = argmax_out;
+  RMX_CUDA(launch_refine(ra, s));
+  NaiveCounters hc;
+  RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+  RMX_CUDA(cudaStreamSynchronize(s));
+  int64_t overflow_perms = 0;
+  if (hc.susp_count > (unsigned)kSuspectCap) {
+    // too many near-degenerate entries to list: exact fp64 evaluation of everything
+    if (int rc = run_exhaustive(x, v, n, n1, orders, nullptr, L, two_sided, max_out, argmax_out,
+                                ws.counters(), s, st))
+      return rc;
+    overflow_perms = L;
+  } else if (hc.overflow_count > 0) {
+    if (int rc = run_exhaustive(x, v, n, n1, orders, ws.overflow(), hc.overflow_count, two_sided,
+                                max_out, argmax_out, ws.counters(), s, st))
+      return rc;
+    overflow_perms = hc.overflow_count;
+  }
+  if (overflow_perms > 0) {
+    RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+    RMX_CUDA(cudaStreamSynchronize(s));
+  }
+  if (stats) {
+    stats->suspects = hc.susp_count;
+    stats->band_candidates = hc.band_candidates;
+    stats->overflow_perms = overflow_perms;
+    stats->chunks = ws.lay.n_chunks;
+    stats->grid = ws.lay.grid;
+    stats->stages = ws.lay.stages;
+    stats->bk = ws.lay.bk;
+  }
+  return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);
+}
+
+int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                      int64_t L, int32_t two_sided, double* max_out, int32_t* argmax_out,
+                      void* workspace, size_t workspace_bytes, void* stream, rmx_status* st,
+                      rmx_naive_stats* stats) {
+  if (int rc = rmx_naive_prepare(x, v, n, n1, L, workspace, workspace_bytes, stream, st)) return rc;
+  Ws ws;
+  ws.lay = naive_layout(v, n, L, device_sm_count());
+  if (ws.lay.stages == 0) {
+    // subject count beyond the tensor-core A tile: exhaustive exact path
+    // (still on the GPU; fp64 CUDA cores)
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ws.base = static_cast<uint8_t*>(workspace);
+    if (int rc = run_exhaustive(x, v, n, n1, orders, nullptr, L, two_sided, max_out, argmax_out,
+                                ws.counters(), s, st))
+      return rc;
+    NaiveCounters hc;
+    RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+    RMX_CUDA(cudaStreamSynchronize(s));
+    if (stats) {
+      memset(stats, 0, sizeof(*stats));
+      stats->overflow_perms = L;
+    }
+    return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);
+  }
+  if (int rc = rmx_naive_tfill(v, n, n1, orders, L, two_sided, workspace, workspace_bytes, stream,
+                               st, stats))
+    return rc;
+  return rmx_naive_finish(x, v, n, n1, orders, L, two_sided, max_out, argmax_out, workspace,
+                          workspace_bytes, stream, st, stats);
+}
+
+int rmx_tstat_exact(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                    int64_t L, double* t_out, int64_t ld, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  if (!t_out || ld < v) return set_status(st, RMX_E_USAGE, "t_out must hold L rows of ld >= v");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* xt = nullptr;
+  NaiveCounters* c = nullptr;
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xt), (size_t)v * n * sizeof(double), s));
+  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(NaiveCounters), s));
+  RMX_CUDA(cudaMemsetAsync(c, 0, sizeof(NaiveCounters), s));
+  RMX_CUDA(cudaMemsetAsync(&c->deg_key, 0xff, sizeof(unsigned long long), s));
+  RMX_CUDA(launch_transpose(x, v, n, xt, s));
+  const int nvb = (int)std::max<int64_t>(1, std::min<int64_t>((v + 1023) / 1024, 1024));
+  RMX_CUDA(launch_exact_rows(xt, v, n, n1, orders, nullptr, L, 0, t_out, ld, nullptr, nullptr, nvb,
+                             c, s));
+  NaiveCounters hc;
+  RMX_CUDA(cudaMemcpyAsync(&hc, c, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  RMX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(xt, s);
+  cudaFreeAsync(c, s);
+  return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);
+}
+
+int rmx_tstat_pairs(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                    const int32_t* pairs, int64_t npairs, double* t_out, double* num_out,
+                    int32_t* deg_out, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, 1, st)) return rc;
+  RMX_CUDA(launch_pairs(x, v, n, n1, orders, pairs, npairs, t_out, num_out, deg_out,
+                        static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,380 @@
+// tfill_tc.cu -- K1: the NaivePT permutation-matrix fill on tcgen05 tensor cores.
+//
+// Replaces the reference's per-permutation loop (naive.py:49-57):
+//     x1, x2 = x.group_blocks(plan.shuffle(i))      # model.py:65-69
+//     col    = tstat_full(x1, x2)                   # teststat.py:28-61
+//     out[i] = column_max(col, two_sided)           # teststat.py:88-90
+// for all permutations at once.  With per-voxel standardisation z (K0, fp64;
+// t is invariant to a per-voxel affine map) the statistic only needs
+//     S1 = sum_{j in G1} z_j,   Q1 = sum_{j in G1} z_j^2
+// and for all (perm, voxel) pairs that is the contraction
+//     [S1 | Q1] (L x 2v) = G (L x n, 0/1 indicator) . [Z | Z^2] (n x 2v).
+// Z and Z^2 are split into fp16 hi + lo planes (residual <= 2^-22 |z|), G is
+// exact in fp16, and D += G.B_hi + G.B_lo accumulates in fp32 TMEM.
+//
+// Tile: M = 128 permutations (TMEM lanes), N = 256 = 128 voxels x {S, Q},
+// K = subjects.  Persistent CTAs, one per SM, warp-specialised:
+//   warp 0     TMA producer: B tiles (hi and lo boxes) into a STAGES-deep ring
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..  epilogue: tcgen05.ld S,Q -> t~ (division-free compare) ->
+//              per-permutation top-2 over the unit's voxel chunk; also build
+//              the A tile (G, fp16 0/1) in smem once per unit.
+// Two TMEM accumulators (2 x 256 columns) let the epilogue of tile t overlap
+// the MMAs of tile t+1.  T never leaves the chip; the only outputs are the
+// per-(perm, chunk) top-2 candidates refined in fp64 by K2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+
+#include "rmx_internal.cuh"
+#include "sm100.cuh"
+
+namespace rmx {
+
+namespace {
+
+constexpr int kNumAcc = 2;
+constexpr int kTileN = 2 * kTileV;
+
+template <bool TWO_SIDED, bool MASKED, bool DEBUG>
+__device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uint32_t (&q)[32],
+                                              int jbase, int valid, float alpha, float beta,
+                                              float gamma, float dthr, float& K1, int& j1,
+                                              float& K2, int& j2, int64_t p, bool prow,
+                                              const TfillArgs& a) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const float S = __uint_as_float(s[c]);
+    const float Q = __uint_as_float(q[c]);
+    // u = sign(t) t^2 * d  (two-sided: t^2 * d); d = var_term * (n1 n2 / n)^2
+    const float u = TWO_SIDED ? S * S : S * fabsf(S);
+    const float d = fmaf(beta, fabsf(u), fmaf(alpha, Q, gamma));
+    bool hit = (u > K2 * d) | (d < dthr);
+    if (MASKED) hit = hit & (c < valid);
+    if (DEBUG) {
+      if (prow && (!MASKED || c < valid)) {
+        float t = (d < dthr) ? __int_as_float(0x7fc00000) : copysignf(sqrtf(fabsf(u) / d), u);
+        a.dbg_t[p * a.v + jbase + c] = t;
+      }
+    }
+    if (hit) {
+      const int j = jbase + c;
+      if (d < dthr) {
+        // near-zero pooled variance: exact fp64 re-evaluation in K2
+        if (prow) {
+          unsigned slot = atomicAdd(&a.counters->susp_count, 1u);
+          if (slot < (unsigned)kSuspectCap) {
+            a.susp[2 * slot] = (int)p;
+            a.susp[2 * slot + 1] = j;
+          }
+        }
+      } else {
+        const float key = u / d;
+        if (key > K1) {
+          K2 = K1;
+          j2 = j1;
+          K1 = key;
+          j1 = j;
+        } else if (key > K2) {
+          K2 = key;
+          j2 = j;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
+
+template <int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool DEBUG>
+__global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
+    k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
+  constexpr int HALF_BYTES = kTileN * BK * 2;  // one plane pair box (hi or lo)
+  constexpr int STAGE_BYTES = 2 * HALF_BYTES;
+  constexpr int KSTEPS = BK / 16;
+  constexpr uint32_t B_LAYOUT = (BK == 64) ? 2u : 4u;  // 128B : 64B swizzle
+  constexpr uint32_t B_SBO = (BK == 64) ? 1024u : 512u;
+  constexpr int GROUPS = EPI_WARPS / 4;  // epilogue warps sharing a TMEM lane quadrant
+  constexpr int COLGROUPS = kTileV / 32 / GROUPS;
+  constexpr uint32_t IDESC = idesc_f16_f32(kTileM, kTileN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_mem = smem;
+  uint8_t* a_mem = smem + STAGES * STAGE_BYTES;
+  const int a_bytes = kTileM * a.kpad * 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a_mem + a_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + kNumAcc;
+  uint64_t* afull = tempty + kNumAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
+
+  const int warp = (int)warp_id();
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < kNumAcc; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS);
+    }
+    mbar_init(afull, kTileM);
+    fence_mbar_init();
+    tma_prefetch(&pmap);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int n_units = a.n_mtiles * a.n_chunks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int chunk = u / a.n_mtiles;
+        const int t0 = chunk * a.tiles_per_chunk;
+        const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < a.kpad; kb += BK) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            uint8_t* dst = stage_mem + stage * STAGE_BYTES;
+            tma_load_3d(dst, &pmap, &full[stage], kb, t * kTileV, 0);               // z_hi, q_hi
+            tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV, 2);  // z_lo, q_lo
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t a_base = smem_u32(a_mem);
+    const uint32_t a_sbo = (uint32_t)a.kpad * 16u;
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0, a_phase = 0;
+    int acc = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int chunk = u / a.n_mtiles;
+      const int t0 = chunk * a.tiles_per_chunk;
+      const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+      mbar_wait(afull, a_phase);
+      a_phase ^= 1;
+      tc_fence_after();
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * kTileN);
+        for (int kb = 0; kb < a.kpad; kb += BK) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sb = smem_u32(stage_mem + stage * STAGE_BYTES);
+#pragma unroll
+            for (int s = 0; s < KSTEPS; ++s) {
+              const int ks = kb / 16 + s;
+              if (ks < a.nk16) {
+                const uint64_t adesc = smem_desc(a_base + (uint32_t)ks * 256u, 128u, a_sbo, 0u);
+                const uint64_t bh = smem_desc(sb + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
+                const uint64_t bl =
+                    smem_desc(sb + (uint32_t)HALF_BYTES + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
+                mma_f16_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
+                mma_f16_ss(d_tmem, adesc, bl, IDESC, 1u);
+              }
+            }
+            mma_commit(&empty[stage]);                        // smem slot reusable
+            if (kb + BK >= a.kpad) mma_commit(&tfull[acc]);   // accumulator ready
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++acc == kNumAcc) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad + 32) are ours
+    const int grp = ew / 4;
+    const int row = quad * 32 + lane;
+    const float alpha = a.alpha, beta = a.beta, gamma = a.gamma, dthr = a.dthr;
+    const int slots = a.n_chunks * GROUPS;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int mtile = u % a.n_mtiles;
+      const int chunk = u / a.n_mtiles;
+      const int t0 = chunk * a.tiles_per_chunk;
+      const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+      const int64_t p = (int64_t)mtile * kTileM + row;
+      const bool prow = p < a.L;
+      if (grp == 0) {
+        // A row `row`: G[p, k] = 1 for k in orders[p, :n1] (canonical K-major
+        // no-swizzle layout: 8x8 core matrices, LBO = 128 B, SBO = kpad*16 B)
+        uint8_t* rbase = a_mem + (row >> 3) * (a.kpad * 16) + (row & 7) * 16;
+        for (int kc = 0; kc < a.kpad / 8; ++kc)
+          *reinterpret_cast<uint4*>(rbase + kc * 128) = make_uint4(0, 0, 0, 0);
+        if (prow) {
+          const int16_t* ord = a.orders + p * a.n;
+          for (int i = 0; i < a.n1; ++i) {
+            const int k = ord[i];
+            *reinterpret_cast<uint16_t*>(rbase + (k >> 3) * 128 + (k & 7) * 2) = 0x3C00u;  // 1.0
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(afull);
+      }
+      float K1 = -FLT_MAX, K2 = -FLT_MAX;
+      int j1 = -1, j2 = -1;
+      for (int t = t0; t < t1; ++t) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const int64_t vleft = a.v - (int64_t)t * kTileV;
+        const int valid = vleft < kTileV ? (int)vleft : kTileV;
+#pragma unroll 1
+        for (int g = grp * COLGROUPS; g < (grp + 1) * COLGROUPS; ++g) {
+          uint32_t sv[32], qv[32];
+          const uint32_t taddr =
+              tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTileN + g * 32);
+          tmem_ld32(taddr, sv);
+          tmem_ld32(taddr + kTileV, qv);
+          tmem_ld_wait();
+          const int jbase = t * kTileV + g * 32;
+          const int gvalid = valid - g * 32;
+          if (gvalid >= 32)
+            epilogue_cols<TWO_SIDED, false, DEBUG>(sv, qv, jbase, 32, alpha, beta, gamma, dthr, K1,
+                                                   j1, K2, j2, p, prow, a);
+          else if (gvalid > 0)
+            epilogue_cols<TWO_SIDED, true, DEBUG>(sv, qv, jbase, gvalid, alpha, beta, gamma, dthr,
+                                                  K1, j1, K2, j2, p, prow, a);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == kNumAcc) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if (prow) {
+        const float tt1 = (j1 >= 0) ? key_to_t(K1) : -FLT_MAX;
+        const float tt2 = (j2 >= 0) ? key_to_t(K2) : -FLT_MAX;
+        a.cand[p * slots + chunk * GROUPS + grp] =
+            make_int4(__float_as_int(tt1), j1, __float_as_int(tt2), j2);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// -------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+size_t smem_bytes_for(int bk, int stages, int kpad) {
+  const size_t stage = (size_t)2 * kTileN * bk * 2;
+  size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024;
+  // one CTA per SM: TMEM (512 columns) is allocated whole by each CTA
+  return bytes < 120 * 1024 ? 120 * 1024 : bytes;
+}
+
+template <int BK, int STAGES, int EPI, bool TS, bool DBG>
+cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                       cudaStream_t s) {
+  auto kern = k_tfill_tc<BK, STAGES, EPI, TS, DBG>;
+  const size_t smem = smem_bytes_for(BK, STAGES, lay.kpad);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<lay.grid, 64 + 32 * EPI, smem, s>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <bool TS, bool DBG>
+cudaError_t dispatch(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                     cudaStream_t s) {
+  // epilogue width: 8 warps when the K loop is short (epilogue-bound), else 4
+  const bool wide = lay.groups == 2;
+  if (lay.bk == 64) {
+    if (lay.stages >= 3)
+      return wide ? launch_cfg<64, 3, 8, TS, DBG>(lay, a, map, s)
+                  : launch_cfg<64, 3, 4, TS, DBG>(lay, a, map, s);
+    return wide ? launch_cfg<64, 2, 8, TS, DBG>(lay, a, map, s)
+                : launch_cfg<64, 2, 4, TS, DBG>(lay, a, map, s);
+  }
+  if (lay.stages >= 4)
+    return wide ? launch_cfg<32, 4, 8, TS, DBG>(lay, a, map, s)
+                : launch_cfg<32, 4, 4, TS, DBG>(lay, a, map, s);
+  if (lay.stages == 3)
+    return wide ? launch_cfg<32, 3, 8, TS, DBG>(lay, a, map, s)
+                : launch_cfg<32, 3, 4, TS, DBG>(lay, a, map, s);
+  return wide ? launch_cfg<32, 2, 8, TS, DBG>(lay, a, map, s)
+              : launch_cfg<32, 2, 4, TS, DBG>(lay, a, map, s);
+}
+
+}  // namespace
+
+bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad, int bk) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)v, 4};
+  cuuint64_t strides[2] = {(cuuint64_t)kpad * 2, (cuuint64_t)v * kpad * 2};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)kTileV, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(planes), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
+                            int two_sided, cudaStream_t s) {
+  CUtensorMap map;
+  if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk)) return cudaErrorInvalidValue;
+  const bool dbg = a.dbg_t != nullptr;
+  if (two_sided)
+    return dbg ? dispatch<true, true>(lay, a, map, s) : dispatch<true, false>(lay, a, map, s);
+  return dbg ? dispatch<false, true>(lay, a, map, s) : dispatch<false, false>(lay, a, map, s);
+}
+
+size_t tfill_smem_bytes(int bk, int stages, int kpad) { return smem_bytes_for(bk, stages, kpad); }
+
+}  // namespace rmx

@@ -1,0 +1,86 @@
+"""Permutation label matrices: PermutationPlan -> L x n subject orders.
+
+The engine consumes the plan as a dense int16 matrix ``orders[p, :]`` =
+``plan.shuffle(p)`` (group 1 = the first n1 entries, in shuffle order -- the
+order matters for the bit-exact refinement, which sums in that order, as the
+reference's fancy-indexed blocks do; reference model.py:65-69).
+
+Generating a shuffle costs ~26-30 us of host time per permutation (numpy
+SeedSequence + SFC64), i.e. ~3 s for L = 1e5 on one core, so the
+matrix is generated once per plan with a process pool and cached in host
+memory.  bench.py reports this cost separately from the device clock.
+"""
+
+from __future__ import annotations
+
+import multiprocessing as mp
+import os
+import threading
+from collections import OrderedDict
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+from .exceptions import UsageError
+from .rng import shuffle_order
+
+_CACHE: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
+_CACHE_BYTES = 0
+_CACHE_LIMIT = int(os.environ.get("RMX_LABEL_CACHE_BYTES", str(2 << 30)))
+_LOCK = threading.Lock()
+
+
+def _orders_block(args) -> np.ndarray:
+    seed, lo, hi, n = args
+    out = np.empty((hi - lo, n), dtype=np.int16)
+    for i in range(lo, hi):
+        out[i - lo] = shuffle_order(seed, i, n)
+    return out
+
+
+def generate_orders(seed: int, lo: int, hi: int, n: int, workers: int | None = None) -> np.ndarray:
+    """Rows [lo, hi) of the plan's order matrix (uncached)."""
+    if n > 32767:
+        raise UsageError(f"subject count {n} exceeds the int16 label format")
+    count = hi - lo
+    if workers is None:
+        workers = min(os.cpu_count() or 1, 32)
+    if workers <= 1 or count < 4096:
+        return _orders_block((seed, lo, hi, n))
+    bounds = np.linspace(lo, hi, workers * 4 + 1).astype(np.int64)
+    jobs = [(seed, int(a), int(b), n) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    ctx = mp.get_context("fork")
+    with ProcessPoolExecutor(max_workers=workers, mp_context=ctx) as pool:
+        parts = list(pool.map(_orders_block, jobs))
+    return np.concatenate(parts, axis=0)
+
+
+def plan_orders(plan, lo: int = 0, hi: int | None = None) -> np.ndarray:
+    """Cached order matrix for ``plan`` rows [lo, hi) (int16, read-only)."""
+    global _CACHE_BYTES
+    hi = plan.count if hi is None else hi
+    key = (int(plan.master_seed), int(plan.count), int(plan.subjects))
+    with _LOCK:
+        full = _CACHE.get(key)
+        if full is not None:
+            _CACHE.move_to_end(key)
+            return full[lo:hi]
+    if (hi - lo) != plan.count:
+        # a shard: generate only the requested rows, do not cache
+        return generate_orders(key[0], lo, hi, key[2])
+    full = generate_orders(key[0], 0, plan.count, key[2])
+    full.setflags(write=False)
+    with _LOCK:
+        _CACHE[key] = full
+        _CACHE_BYTES += full.nbytes
+        while _CACHE_BYTES > _CACHE_LIMIT and len(_CACHE) > 1:
+            _, old = _CACHE.popitem(last=False)
+            _CACHE_BYTES -= old.nbytes
+    return full[lo:hi]
+
+
+def clear_cache() -> None:
+    global _CACHE_BYTES
+    with _LOCK:
+        _CACHE.clear()
+        _CACHE_BYTES = 0

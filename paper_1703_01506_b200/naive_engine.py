@@ -1,0 +1,224 @@
+"""NaivePT on the B200: drop-in ``run_naive``.
+
+Reference: naive.py:60-109 ``run_naive(x, plan, materialize, two_sided,
+threads, mem_cap_bytes) -> (MaxNull, StatMatrix | None, counters)``.
+
+Device pipeline (one stream, librmx.so):
+  K0 prepare  fp64 standardisation + fp16 hi/lo split planes of Z and Z^2
+  K1 tfill    tcgen05 contraction G.[Z|Z^2] + fused t / top-2 epilogue
+  K2 finish   fp64 refinement of the band candidates -> maxima bit-identical
+              to the reference (numpy arithmetic restated, np_exact.cuh)
+``materialize=True`` additionally fills the dense statistic matrix with the
+exact fp64 kernel (bit-identical to the reference's ``store[:, i] = col``).
+
+Threads: the reference parallelises over permutation blocks on a thread pool
+and guarantees thread-count-independent results (naive.py:86-101).  Here the
+parallelism is the GPU's; ``threads`` is validated for API parity and has no
+effect on the (deterministic) result.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as nat
+from .domain import MaxNull, StatMatrix, as_data_matrix, as_plan
+from .exceptions import EngineUnavailableError, UsageError
+from .labels import plan_orders
+
+DEFAULT_MEM_CAP_BYTES = 2 << 30
+
+_CHECKED_DEVICES: set = set()
+
+
+def resolve_threads(threads: Optional[int]) -> int:
+    """Same precedence as the reference (naive.py:37-46): argument, then
+    RAPIDMAXNULL_THREADS, then os.cpu_count()."""
+    if threads is None:
+        env = os.environ.get("RAPIDMAXNULL_THREADS")
+        if env:
+            threads = int(env)
+    if threads is None:
+        threads = os.cpu_count() or 1
+    if threads < 1:
+        raise UsageError(f"thread count must be >= 1, got {threads}")
+    return threads
+
+
+def cuda_device():
+    """The current CUDA device, checked to be sm_100 (B200).  Raises
+    EngineUnavailableError otherwise -- there is no CPU path."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise EngineUnavailableError("no CUDA device visible; the engine has no CPU fallback")
+    dev = torch.cuda.current_device()
+    if dev not in _CHECKED_DEVICES:
+        nat.device_check(dev)
+        _CHECKED_DEVICES.add(dev)
+    return torch.device("cuda", dev)
+
+
+@dataclass
+class NaiveResult:
+    maxima: np.ndarray
+    argmax: np.ndarray
+    stats: dict = field(default_factory=dict)
+    T: Optional[np.ndarray] = None
+
+
+class NaiveJob:
+    """A NaivePT evaluation over device-resident inputs.
+
+    x:      (v, n) float64 CUDA tensor (DataMatrix.values layout)
+    orders: (L, n) int16 CUDA tensor (row p = plan.shuffle(p))
+    The three phases are exposed separately so callers can time the
+    tensor-core contraction alone (bench.py); ``run`` chains them.
+    """
+
+    def __init__(self, x, n1: int, orders, two_sided: bool, stream=None):
+        import torch
+
+        if x.dtype != torch.float64 or x.dim() != 2 or not x.is_contiguous():
+            raise UsageError("x must be a contiguous (v, n) float64 CUDA tensor")
+        if orders.dtype != torch.int16 or orders.dim() != 2 or not orders.is_contiguous():
+            raise UsageError("orders must be a contiguous (L, n) int16 CUDA tensor")
+        if orders.shape[1] != x.shape[1]:
+            raise UsageError("orders and x disagree on the subject count")
+        self.lib = nat.load()
+        self.x, self.orders = x, orders
+        self.v, self.n = int(x.shape[0]), int(x.shape[1])
+        self.L = int(orders.shape[0])
+        self.n1 = int(n1)
+        self.two_sided = int(bool(two_sided))
+        self.stream = stream if stream is not None else torch.cuda.current_stream(x.device)
+        self.ws_bytes = int(self.lib.rmx_naive_workspace_bytes(self.v, self.n, self.L))
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=x.device)
+        self.max_out = torch.empty(self.L, dtype=torch.float64, device=x.device)
+        self.argmax_out = torch.empty(self.L, dtype=torch.int32, device=x.device)
+        self._st = nat.Status()
+        self.stats = nat.NaiveStats()
+
+    def _s(self):
+        return nat.stream_handle(self.stream)
+
+    def prepare(self) -> None:
+        rc = self.lib.rmx_naive_prepare(
+            nat.ptr(self.x), self.v, self.n, self.n1, self.L, nat.ptr(self.workspace),
+            self.ws_bytes, self._s(), ctypes.byref(self._st))
+        nat.raise_for(rc, self._st)
+
+    def tfill(self) -> None:
+        rc = self.lib.rmx_naive_tfill(
+            self.v, self.n, self.n1, nat.ptr(self.orders), self.L, self.two_sided,
+            nat.ptr(self.workspace), self.ws_bytes, self._s(), ctypes.byref(self._st),
+            ctypes.byref(self.stats))
+        nat.raise_for(rc, self._st)
+
+    def finish(self) -> None:
+        rc = self.lib.rmx_naive_finish(
+            nat.ptr(self.x), self.v, self.n, self.n1, nat.ptr(self.orders), self.L,
+            self.two_sided, nat.ptr(self.max_out), nat.ptr(self.argmax_out),
+            nat.ptr(self.workspace), self.ws_bytes, self._s(), ctypes.byref(self._st),
+            ctypes.byref(self.stats))
+        nat.raise_for(rc, self._st)
+
+    def run(self):
+        """All phases in one ABI call (rmx_naive_maxnull)."""
+        rc = self.lib.rmx_naive_maxnull(
+            nat.ptr(self.x), self.v, self.n, self.n1, nat.ptr(self.orders), self.L,
+            self.two_sided, nat.ptr(self.max_out), nat.ptr(self.argmax_out),
+            nat.ptr(self.workspace), self.ws_bytes, self._s(), ctypes.byref(self._st),
+            ctypes.byref(self.stats))
+        nat.raise_for(rc, self._st)
+        return self.max_out, self.argmax_out
+
+    def tfill_debug(self):
+        """t~ for every (perm, voxel) from the tensor-core epilogue (float32,
+        (L, v)); validation only."""
+        import torch
+
+        t = torch.full((self.L, self.v), float("nan"), dtype=torch.float32, device=self.x.device)
+        self.prepare()
+        rc = self.lib.rmx_naive_tfill_debug(
+            self.v, self.n, self.n1, nat.ptr(self.orders), self.L, self.two_sided, nat.ptr(t),
+            nat.ptr(self.workspace), self.ws_bytes, self._s(), ctypes.byref(self._st))
+        nat.raise_for(rc, self._st)
+        return t
+
+
+def tstat_exact_device(x, n1: int, orders, stream=None):
+    """(L, v) float64 statistics, bit-identical to the reference, on device."""
+    import torch
+
+    lib = nat.load()
+    v, n = int(x.shape[0]), int(x.shape[1])
+    L = int(orders.shape[0])
+    out = torch.empty((L, v), dtype=torch.float64, device=x.device)
+    stream = stream if stream is not None else torch.cuda.current_stream(x.device)
+    st = nat.Status()
+    rc = lib.rmx_tstat_exact(nat.ptr(x), v, n, int(n1), nat.ptr(orders), L, nat.ptr(out), v,
+                             nat.stream_handle(stream), ctypes.byref(st))
+    nat.raise_for(rc, st)
+    return out
+
+
+def upload(x_values: np.ndarray, orders: np.ndarray, device):
+    """Host -> device copies through pinned staging buffers."""
+    import torch
+
+    xh = torch.from_numpy(np.ascontiguousarray(x_values, dtype=np.float64))
+    oh = torch.from_numpy(np.ascontiguousarray(orders, dtype=np.int16))
+    xd = xh.pin_memory().to(device, non_blocking=True)
+    od = oh.pin_memory().to(device, non_blocking=True)
+    return xd, od
+
+
+def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
+                 threads: Optional[int] = None,
+                 mem_cap_bytes: int = DEFAULT_MEM_CAP_BYTES) -> NaiveResult:
+    """``run_naive`` with the argmax voxel and engine diagnostics."""
+    x = as_data_matrix(x)
+    plan = as_plan(plan)
+    if plan.subjects != x.subjects:
+        raise UsageError("plan and data matrix disagree on subject count")
+    v, L = x.voxels, plan.count
+    if materialize:
+        needed = v * L * 8
+        if needed > mem_cap_bytes:
+            raise UsageError(
+                f"materializing the statistic matrix needs {needed} bytes "
+                f"({v} voxels x {L} permutations x 8), above the cap {mem_cap_bytes}; "
+                f"raise the cap or drop --dump-T"
+            )
+    resolve_threads(threads)
+    device = cuda_device()
+    orders = plan_orders(plan)
+    xd, od = upload(x.values, orders, device)
+    job = NaiveJob(xd, x.n1, od, two_sided)
+    mx, am = job.run()
+    T = None
+    if materialize:
+        T = tstat_exact_device(xd, x.n1, od).t().contiguous().cpu().numpy()
+    return NaiveResult(mx.cpu().numpy(), am.cpu().numpy().astype(np.int64),
+                       job.stats.as_dict(), T)
+
+
+def run_naive(x, plan, materialize: bool = False, two_sided: bool = False,
+              threads: Optional[int] = None, mem_cap_bytes: int = DEFAULT_MEM_CAP_BYTES):
+    """Drop-in for the reference ``run_naive`` (naive.py:60-109)."""
+    res = run_naive_ex(x, plan, materialize, two_sided, threads, mem_cap_bytes)
+    plan = as_plan(plan)
+    v, L = as_data_matrix(x).voxels, plan.count
+    counters = {
+        "full_statistic_evaluations": v * L,
+        "subsampled_statistic_evaluations": 0,
+        "statistic_evaluations": v * L,
+    }
+    mat = StatMatrix(res.T, plan) if res.T is not None else None
+    return MaxNull(res.maxima), mat, counters

@@ -1,0 +1,139 @@
+"""NaivePT parity on the GPU: librmx (through the C ABI) vs the CPU oracle.
+
+The oracle is the bit-exact C restatement of the reference statistic path
+(oracle/rmx_oracle.c, pinned to the reference by tests/test_oracle_golden.py).
+The bar: maxima bit-identical, argmax identical (lowest index on exact ties).
+"""
+import numpy as np
+import pytest
+
+import paper_1703_01506_b200 as rmx
+from paper_1703_01506_b200.labels import plan_orders
+
+pytestmark = pytest.mark.gpu
+
+
+def _data(v, n1, n2, seed, scale=1.0):
+    g = np.random.default_rng(seed)
+    vals = (g.standard_normal((v, n1 + n2)) * scale).astype(np.float32).astype(np.float64)
+    return rmx.DataMatrix(vals, n1, n2)
+
+
+CASES = [
+    # v, n1, n2, L, two_sided, seed
+    (20, 2, 2, 50, False, 42),
+    (1, 3, 3, 30, False, 1),
+    (300, 10, 10, 200, True, 3),
+    (1000, 10, 10, 300, False, 4),
+    (777, 3, 9, 129, False, 5),
+    (2500, 50, 50, 257, False, 6),
+    (1300, 120, 280, 140, False, 7),
+    (4099, 200, 200, 130, True, 8),
+]
+
+
+@pytest.mark.parametrize("v,n1,n2,L,two_sided,seed", CASES)
+def test_maxima_bit_exact_vs_oracle(oracle_mod, v, n1, n2, L, two_sided, seed):
+    x = _data(v, n1, n2, seed)
+    plan = rmx.PermutationPlan(seed + 100, L, n1 + n2)
+    res = rmx.run_naive_ex(x, plan, two_sided=two_sided)
+    orders = plan_orders(plan).astype(np.int64)
+    mx, am, _ = oracle_mod.naive_maxnull(x.values, n1, orders, two_sided, threads=8)
+    assert np.array_equal(res.maxima, mx), np.abs(res.maxima - mx).max()
+    assert np.array_equal(res.argmax, am)
+
+
+def test_tensor_core_error_bound(oracle_mod):
+    """|t~ - t| of the fused tcgen05 epilogue, before fp64 refinement."""
+    import torch
+
+    from paper_1703_01506_b200.naive_engine import NaiveJob, cuda_device, upload
+
+    for (v, n1, n2, L, seed) in [(3000, 10, 10, 256, 11), (2000, 50, 50, 200, 12),
+                                 (1500, 200, 200, 130, 13), (1200, 120, 280, 128, 14)]:
+        x = _data(v, n1, n2, seed, scale=3.0)
+        plan = rmx.PermutationPlan(seed, L, n1 + n2)
+        orders = plan_orders(plan)
+        xd, od = upload(x.values, orders, cuda_device())
+        job = NaiveJob(xd, n1, od, False)
+        t_dbg = job.tfill_debug().cpu().numpy().astype(np.float64)
+        _, _, T = oracle_mod.naive_maxnull(x.values, n1, orders.astype(np.int64), False,
+                                           materialize=True)
+        err = np.abs(t_dbg - T.T) / np.maximum(np.abs(T.T), 1.0)
+        assert np.isfinite(t_dbg).all()
+        assert err.max() < 1e-5, (v, n1, n2, err.max())
+        torch.cuda.synchronize()
+
+
+def test_materialized_matrix_bit_exact(oracle_mod):
+    x = _data(120, 3, 4, 21)
+    plan = rmx.PermutationPlan(13, 40, 7)
+    null, mat, counters = rmx.run_naive(x, plan, materialize=True)
+    _, _, T = oracle_mod.naive_maxnull(x.values, 3, plan_orders(plan).astype(np.int64), False,
+                                       materialize=True)
+    assert mat.values.shape == (120, 40)
+    assert np.array_equal(mat.values, T)
+    assert np.array_equal(null.maxima, T.max(axis=0))
+    assert counters["statistic_evaluations"] == 120 * 40
+
+
+def test_constant_matrix_gives_all_zero_null():
+    x = rmx.DataMatrix(np.full((10, 6), 3.5), 3, 3)
+    null, _, _ = rmx.run_naive(x, rmx.PermutationPlan(5, 20, 6))
+    assert np.all(null.maxima == 0.0)
+
+
+def test_constant_voxel_with_inexact_means_matches_reference(oracle_mod):
+    # 0.1 repeated: numpy's rounding of the group means gives t != 0
+    vals = np.random.default_rng(3).standard_normal((50, 7)) * 1e-3
+    vals[17] = 0.1
+    x = rmx.DataMatrix(vals, 3, 4)
+    plan = rmx.PermutationPlan(9, 33, 7)
+    res = rmx.run_naive_ex(x, plan)
+    mx, am, _ = oracle_mod.naive_maxnull(x.values, 3, plan_orders(plan).astype(np.int64), False)
+    assert np.array_equal(res.maxima, mx)
+    assert np.array_equal(res.argmax, am)
+
+
+def test_degenerate_voxel_raises_first_in_permutation_order(oracle_mod):
+    g = np.random.default_rng(4)
+    vals = g.standard_normal((40, 6))
+    vals[23] = [1.0, 1.0, 1.0, 2.0, 2.0, 2.0]      # degenerate under the identity
+    vals[31] = [5.0, 5.0, 5.0, 7.0, 7.0, 7.0]
+    x = rmx.DataMatrix(vals, 3, 3)
+    plan = rmx.PermutationPlan(2, 10, 6)
+    with pytest.raises(rmx.DegenerateVoxelError) as err:
+        rmx.run_naive(x, plan)
+    with pytest.raises(oracle_mod.OracleDegenerate) as ref:
+        oracle_mod.naive_maxnull(x.values, 3, plan_orders(plan).astype(np.int64), False)
+    assert err.value.voxel == ref.value.voxel == 23
+    assert err.value.mean_diff == ref.value.mean_diff
+
+
+def test_column_zero_is_the_true_labelling(oracle_mod):
+    x = _data(500, 4, 4, 2)
+    plan = rmx.PermutationPlan(9, 10, 8)
+    null, _, _ = rmx.run_naive(x, plan)
+    t0 = rmx.tstat_full(x.values[:, :4], x.values[:, 4:])
+    assert null.maxima[0] == t0.max()
+
+
+def test_two_sided_dominates_signed():
+    x = _data(300, 3, 3, 7)
+    plan = rmx.PermutationPlan(3, 25, 6)
+    signed, _, _ = rmx.run_naive(x, plan)
+    absolute, _, _ = rmx.run_naive(x, plan, two_sided=True)
+    assert np.all(absolute.maxima >= signed.maxima)
+
+
+def test_c1_full_config_bit_exact(oracle_mod):
+    from paper_1703_01506_b200.datagen import CONFIGS, make_data_numpy
+
+    cfg = CONFIGS["c1"]
+    x = rmx.DataMatrix(make_data_numpy(cfg), cfg.n1, cfg.n2)
+    plan = rmx.PermutationPlan(cfg.plan_seed, cfg.permutations, cfg.subjects)
+    res = rmx.run_naive_ex(x, plan, two_sided=cfg.two_sided)
+    mx, am, _ = oracle_mod.naive_maxnull(x.values, cfg.n1, plan_orders(plan).astype(np.int64),
+                                         cfg.two_sided, threads=8)
+    assert np.array_equal(res.maxima, mx)
+    assert np.array_equal(res.argmax, am)
