@@ -169,13 +169,12 @@ def tstat_exact_device(x, n1: int, orders, stream=None):
 
 
 def upload(x_values: np.ndarray, orders: np.ndarray, device):
-    """Host -> device copies through pinned staging buffers."""
-    import torch
+    """Host -> device copies of the data matrix and the label matrix
+    (page-locked in place, see hostmem.py)."""
+    from .hostmem import to_device
 
-    xh = torch.from_numpy(np.ascontiguousarray(x_values, dtype=np.float64))
-    oh = torch.from_numpy(np.ascontiguousarray(orders, dtype=np.int16))
-    xd = xh.pin_memory().to(device, non_blocking=True)
-    od = oh.pin_memory().to(device, non_blocking=True)
+    xd = to_device(np.ascontiguousarray(x_values, dtype=np.float64), device)
+    od = to_device(np.ascontiguousarray(orders, dtype=np.int16), device)
     return xd, od
 
 
