@@ -4,7 +4,7 @@
 //
 //   k_prep          K0: per-voxel standardisation, fp16 hi/lo split planes
 //   k_const_reduce  voxels constant over all subjects (exact, perm-invariant)
-//   k_refine        K2: fp64 refinement of the tensor-core top-2 candidates
+//   k_refine        K2: fp64 refinement of the tensor-core top-4 candidates
 //   k_transpose     X (v x n) -> X^T (n x v) for the coalesced exact kernels
 //   k_exact_rows    exhaustive exact statistic (materialised T / fallback)
 //   k_exact_reduce  per-permutation max/argmax of k_exact_rows' partials
@@ -46,18 +46,6 @@ __device__ __forceinline__ void warp_argmax(double& v, int& j) {
     }
   }
 }
-__device__ __forceinline__ void warp_argmax_f(float& v, int& j) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    float ov = __shfl_xor_sync(0xffffffffu, v, o);
-    int oj = __shfl_xor_sync(0xffffffffu, j, o);
-    if (ov > v || (ov == v && oj >= 0 && (j < 0 || oj < j))) {
-      v = ov;
-      j = oj;
-    }
-  }
-}
-
 __device__ __forceinline__ void note_degenerate(NaiveCounters* c, int64_t perm, int64_t voxel) {
   unsigned long long key = ((unsigned long long)perm << 32) | (unsigned long long)voxel;
   atomicMin(&c->deg_key, key);
@@ -174,10 +162,10 @@ __global__ void k_const_reduce(const double* x, int n, int n1, const int32_t* cv
 }
 
 // ---------------------------------------------------------------- K2
-// One warp per permutation: gather the (perm, chunk) top-2 candidates, keep
+// One warp per permutation: gather the (perm, chunk) top-4 candidates, keep
 // every voxel whose t~ lies in the band below the best, evaluate those
 // exactly in fp64 (reference arithmetic) and take the max.  A chunk whose
-// runner-up is inside the band might hide a third in-band voxel: the
+// 4th-best is inside the band might hide a fifth in-band voxel: the
 // permutation is then queued for the exhaustive exact path.
 constexpr int kRefineWarps = 8;
 
@@ -190,11 +178,11 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
   for (int i = lane; i < a.n; i += 32) ord[i] = a.orders[p * a.n + i];
   __syncwarp();
   const int n2 = a.n - a.n1;
-  const int4* cp = a.cand + p * a.slots;
+  const int4* cp = a.cand + 2 * p * a.slots;
 
   float tmax = -FLT_MAX;
   for (int c = lane; c < a.slots; c += 32) {
-    const int4 e = cp[c];
+    const int4 e = cp[2 * c];
     if (e.y >= 0) tmax = fmaxf(tmax, __int_as_float(e.x));
   }
   for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
@@ -220,11 +208,13 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
   };
   if (tmax > -FLT_MAX) {
     for (int c = lane; c < a.slots; c += 32) {
-      const int4 e = cp[c];
-      if (e.y >= 0 && __int_as_float(e.x) >= lo) consider(e.y);
-      if (e.w >= 0 && __int_as_float(e.z) >= lo) {
-        consider(e.w);
-        overflow = true;
+      const int4 e0 = cp[2 * c], e1 = cp[2 * c + 1];
+      if (e0.y >= 0 && __int_as_float(e0.x) >= lo) consider(e0.y);
+      if (e0.w >= 0 && __int_as_float(e0.z) >= lo) consider(e0.w);
+      if (e1.y >= 0 && __int_as_float(e1.x) >= lo) consider(e1.y);
+      if (e1.w >= 0 && __int_as_float(e1.z) >= lo) {
+        consider(e1.w);
+        overflow = true;  // a 5th in-band voxel of this chunk could be hiding
       }
     }
   }

@@ -134,7 +134,7 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
   lay.off_planes = off;
   off = align_up(off + (size_t)4 * v * lay.kpad * 2, 1024);
   lay.off_cand = off;
-  off = align_up(off + (size_t)L * lay.n_chunks * lay.groups * 16, 256);
+  off = align_up(off + (size_t)L * lay.n_chunks * lay.groups * 32, 256);
   lay.off_susp = off;
   off = align_up(off + (size_t)kSuspectCap * 8, 256);
   lay.off_cvox = off;

@@ -59,7 +59,7 @@ struct TfillArgs {
   int n, n1, kpad, nk16;
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
   float alpha, beta, gamma, dthr;
-  int4* cand;  // [L][n_chunks * groups]: (t~1, j1, t~2, j2)
+  int4* cand;  // [L][n_chunks * groups][2]: top-4 (t~, voxel) pairs
   int32_t* susp;
   NaiveCounters* counters;
   float* dbg_t;  // [L][v] when debugging

@@ -17,11 +17,11 @@
 //   warp 0     TMA producer: B tiles (hi and lo boxes) into a STAGES-deep ring
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..  epilogue: tcgen05.ld S,Q -> t~ (division-free compare) ->
-//              per-permutation top-2 over the unit's voxel chunk; also build
+//              per-permutation top-4 over the unit's voxel chunk; also build
 //              the A tile (G, fp16 0/1) in smem once per unit.
 // Two TMEM accumulators (2 x 256 columns) let the epilogue of tile t overlap
 // the MMAs of tile t+1.  T never leaves the chip; the only outputs are the
-// per-(perm, chunk) top-2 candidates refined in fp64 by K2.
+// per-(perm, chunk) top-4 candidates refined in fp64 by K2.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,12 +38,41 @@ namespace {
 constexpr int kNumAcc = 2;
 constexpr int kTileN = 2 * kTileV;
 
+// Running top-4 (key, voxel) per permutation row; keys are sign(t) t^2
+// (two-sided: t^2).  The common path is one compare against the 4th best
+// (u > K3 * d, division-free); only entries entering the top-4 divide.
+struct Top4 {
+  float k0, k1, k2, k3;
+  int j0, j1, j2, j3;
+  __device__ __forceinline__ void reset() {
+    k0 = k1 = k2 = k3 = -FLT_MAX;
+    j0 = j1 = j2 = j3 = -1;
+  }
+  __device__ __forceinline__ void insert(float key, int j) {
+    if (!(key > k3)) return;
+    if (key > k1) {
+      k3 = k2; j3 = j2;
+      k2 = k1; j2 = j1;
+      if (key > k0) {
+        k1 = k0; j1 = j0;
+        k0 = key; j0 = j;
+      } else {
+        k1 = key; j1 = j;
+      }
+    } else if (key > k2) {
+      k3 = k2; j3 = j2;
+      k2 = key; j2 = j;
+    } else {
+      k3 = key; j3 = j;
+    }
+  }
+};
+
 template <bool TWO_SIDED, bool MASKED, bool DEBUG>
 __device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uint32_t (&q)[32],
                                               int jbase, int valid, float alpha, float beta,
-                                              float gamma, float dthr, float& K1, int& j1,
-                                              float& K2, int& j2, int64_t p, bool prow,
-                                              const TfillArgs& a) {
+                                              float gamma, float dthr, Top4& top, int64_t p,
+                                              bool prow, const TfillArgs& a) {
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const float S = __uint_as_float(s[c]);
@@ -51,7 +80,7 @@ __device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uin
     // u = sign(t) t^2 * d  (two-sided: t^2 * d); d = var_term * (n1 n2 / n)^2
     const float u = TWO_SIDED ? S * S : S * fabsf(S);
     const float d = fmaf(beta, fabsf(u), fmaf(alpha, Q, gamma));
-    bool hit = (u > K2 * d) | (d < dthr);
+    bool hit = (u > top.k3 * d) | (d < dthr);
     if (MASKED) hit = hit & (c < valid);
     if (DEBUG) {
       if (prow && (!MASKED || c < valid)) {
@@ -71,16 +100,7 @@ __device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uin
           }
         }
       } else {
-        const float key = u / d;
-        if (key > K1) {
-          K2 = K1;
-          j2 = j1;
-          K1 = key;
-          j1 = j;
-        } else if (key > K2) {
-          K2 = key;
-          j2 = j;
-        }
+        top.insert(u / d, j);
       }
     }
   }
@@ -246,8 +266,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         fence_proxy_async_smem();
         mbar_arrive(afull);
       }
-      float K1 = -FLT_MAX, K2 = -FLT_MAX;
-      int j1 = -1, j2 = -1;
+      Top4 top;
+      top.reset();
       for (int t = t0; t < t1; ++t) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -264,11 +284,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           const int jbase = t * kTileV + g * 32;
           const int gvalid = valid - g * 32;
           if (gvalid >= 32)
-            epilogue_cols<TWO_SIDED, false, DEBUG>(sv, qv, jbase, 32, alpha, beta, gamma, dthr, K1,
-                                                   j1, K2, j2, p, prow, a);
+            epilogue_cols<TWO_SIDED, false, DEBUG>(sv, qv, jbase, 32, alpha, beta, gamma, dthr,
+                                                   top, p, prow, a);
           else if (gvalid > 0)
-            epilogue_cols<TWO_SIDED, true, DEBUG>(sv, qv, jbase, gvalid, alpha, beta, gamma, dthr,
-                                                  K1, j1, K2, j2, p, prow, a);
+            epilogue_cols<TWO_SIDED, true, DEBUG>(sv, qv, jbase, gvalid, alpha, beta, gamma,
+                                                  dthr, top, p, prow, a);
         }
         tc_fence_before();
         __syncwarp();
@@ -279,10 +299,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         }
       }
       if (prow) {
-        const float tt1 = (j1 >= 0) ? key_to_t(K1) : -FLT_MAX;
-        const float tt2 = (j2 >= 0) ? key_to_t(K2) : -FLT_MAX;
-        a.cand[p * slots + chunk * GROUPS + grp] =
-            make_int4(__float_as_int(tt1), j1, __float_as_int(tt2), j2);
+        int4* dst = a.cand + 2 * (p * slots + chunk * GROUPS + grp);
+        dst[0] = make_int4(__float_as_int(top.j0 >= 0 ? key_to_t(top.k0) : -FLT_MAX), top.j0,
+                           __float_as_int(top.j1 >= 0 ? key_to_t(top.k1) : -FLT_MAX), top.j1);
+        dst[1] = make_int4(__float_as_int(top.j2 >= 0 ? key_to_t(top.k2) : -FLT_MAX), top.j2,
+                           __float_as_int(top.j3 >= 0 ? key_to_t(top.k3) : -FLT_MAX), top.j3);
       }
     }
   }
