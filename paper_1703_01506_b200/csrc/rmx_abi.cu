@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -98,6 +99,7 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
   }
   // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
   lay.groups = lay.kpad <= 128 ? 2 : 1;
+  if (const char* g = getenv("RMX_EPI_GROUPS")) lay.groups = atoi(g) == 2 ? 2 : 1;
   // Voxel chunks per permutation tile: minimise the static round-robin
   // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
   // one chunk of voxel tiles; A-tile rebuild counted as ~1/4 tile).

@@ -68,39 +68,61 @@ struct Top4 {
   }
 };
 
+template <bool TWO_SIDED>
+__device__ __forceinline__ void stat_ud(uint32_t sbits, uint32_t qbits, float alpha, float beta,
+                                        float gamma, float& u, float& d) {
+  const float S = __uint_as_float(sbits);
+  const float Q = __uint_as_float(qbits);
+  // u = sign(t) t^2 d (two-sided: t^2 d); d = var_term * (n1 n2 / n)^2
+  u = TWO_SIDED ? S * S : S * fabsf(S);
+  d = fmaf(beta, fabsf(u), fmaf(alpha, Q, gamma));
+}
+
+// 32 columns (voxels jbase..jbase+31) of one accumulator row.  Pass 1 is
+// branch-free: every column's (u, d) and its "may enter the top-4 or is a
+// near-zero-variance suspect" bit, 32 independent dependency chains.  Pass 2
+// (rare) walks the set bits.  Using the group's entry threshold k3 for the
+// whole group is conservative: k3 only grows, insert() re-checks.
 template <bool TWO_SIDED, bool MASKED, bool DEBUG>
 __device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uint32_t (&q)[32],
                                               int jbase, int valid, float alpha, float beta,
                                               float gamma, float dthr, Top4& top, int64_t p,
                                               bool prow, const TfillArgs& a) {
+  const float k3 = top.k3;
+  uint32_t mask = 0;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
-    const float S = __uint_as_float(s[c]);
-    const float Q = __uint_as_float(q[c]);
-    // u = sign(t) t^2 * d  (two-sided: t^2 * d); d = var_term * (n1 n2 / n)^2
-    const float u = TWO_SIDED ? S * S : S * fabsf(S);
-    const float d = fmaf(beta, fabsf(u), fmaf(alpha, Q, gamma));
-    bool hit = (u > top.k3 * d) | (d < dthr);
-    if (MASKED) hit = hit & (c < valid);
+    float u, d;
+    stat_ud<TWO_SIDED>(s[c], q[c], alpha, beta, gamma, u, d);
+    const bool hit = (u > k3 * d) | (d < dthr);
+    mask |= (hit ? 1u : 0u) << c;
     if (DEBUG) {
       if (prow && (!MASKED || c < valid)) {
         float t = (d < dthr) ? __int_as_float(0x7fc00000) : copysignf(sqrtf(fabsf(u) / d), u);
         a.dbg_t[p * a.v + jbase + c] = t;
       }
     }
-    if (hit) {
-      const int j = jbase + c;
-      if (d < dthr) {
-        // near-zero pooled variance: exact fp64 re-evaluation in K2
-        if (prow) {
-          unsigned slot = atomicAdd(&a.counters->susp_count, 1u);
-          if (slot < (unsigned)kSuspectCap) {
-            a.susp[2 * slot] = (int)p;
-            a.susp[2 * slot + 1] = j;
+  }
+  if (MASKED) mask &= (valid >= 32) ? 0xffffffffu : ((1u << valid) - 1u);
+  if (__builtin_expect(mask != 0u, 0)) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (mask & (1u << c)) {
+        float u, d;
+        stat_ud<TWO_SIDED>(s[c], q[c], alpha, beta, gamma, u, d);
+        const int j = jbase + c;
+        if (d < dthr) {
+          // near-zero pooled variance: exact fp64 re-evaluation in K2
+          if (prow) {
+            unsigned slot = atomicAdd(&a.counters->susp_count, 1u);
+            if (slot < (unsigned)kSuspectCap) {
+              a.susp[2 * slot] = (int)p;
+              a.susp[2 * slot + 1] = j;
+            }
           }
+        } else {
+          top.insert(u / d, j);
         }
-      } else {
-        top.insert(u / d, j);
       }
     }
   }
