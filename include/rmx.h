@@ -62,6 +62,8 @@ typedef struct rmx_naive_stats {
   int32_t grid;            /* persistent CTAs of the tensor-core kernel */
   int32_t stages;          /* smem pipeline depth */
   int32_t bk;              /* K elements per stage */
+  int64_t rare_groups;     /* epilogue: 32-column groups that took the exact path */
+  int64_t all_groups;      /* epilogue: all 32-column groups (per warp) */
 } rmx_naive_stats;
 
 int rmx_abi_version(void);

@@ -47,6 +47,8 @@ class NaiveStats(ctypes.Structure):
         ("grid", ctypes.c_int32),
         ("stages", ctypes.c_int32),
         ("bk", ctypes.c_int32),
+        ("rare_groups", ctypes.c_int64),
+        ("all_groups", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

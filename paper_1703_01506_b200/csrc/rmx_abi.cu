@@ -73,6 +73,7 @@ bool pick_pipeline(int kpad, int* bk, int* stages) {
     s = (int)(avail / ((size_t)2 * 2 * kTileV * b * 2));
   }
   s = std::min(s, b == 64 ? 3 : 4);
+  if (b == 64 && s < 3) return false;
   if (s < 2) return false;
   *bk = b;
   *stages = s;
@@ -98,8 +99,7 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
     lay.stages = 0;
   }
   // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
-  lay.groups = lay.kpad <= 128 ? 2 : 1;
-  if (const char* g = getenv("RMX_EPI_GROUPS")) lay.groups = atoi(g) == 2 ? 2 : 1;
+  lay.groups = 2;  // 8 epilogue warps: two per TMEM lane quadrant
   // Voxel chunks per permutation tile: minimise the static round-robin
   // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
   // one chunk of voxel tiles; A-tile rebuild counted as ~1/4 tile).
@@ -152,6 +152,23 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
 }
 
 namespace {
+
+int gcd_i(int x, int y) {
+  while (y) {
+    const int r = x % y;
+    x = y;
+    y = r;
+  }
+  return x;
+}
+
+// largest stride <= 0.618 T coprime with T (golden-ratio sweep order)
+int golden_stride(int T) {
+  if (T <= 2) return 1;
+  for (int s = (int)(0.6180339887 * T); s > 1; --s)
+    if (gcd_i(s, T) == 1) return s;
+  return 1;
+}
 
 struct Ws {
   NaiveLayout lay;
@@ -296,6 +313,8 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   a.n_mtiles = ws.lay.n_mtiles;
   a.n_chunks = ws.lay.n_chunks;
   a.tiles_per_chunk = ws.lay.tiles_per_chunk;
+  a.stride_full = golden_stride(ws.lay.tiles_per_chunk);
+  a.stride_last = golden_stride(ws.lay.n_vtiles - (ws.lay.n_chunks - 1) * ws.lay.tiles_per_chunk);
   a.alpha = (float)alpha;
   a.beta = (float)beta;
   a.gamma = (float)gamma;
@@ -378,6 +397,8 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
   if (stats) {
     stats->suspects = hc.susp_count;
     stats->band_candidates = hc.band_candidates;
+    stats->rare_groups = (int64_t)hc.rare_groups;
+    stats->all_groups = (int64_t)hc.all_groups;
     stats->overflow_perms = overflow_perms;
     stats->chunks = ws.lay.n_chunks;
     stats->grid = ws.lay.grid;

@@ -32,6 +32,8 @@ struct NaiveCounters {
   unsigned int band_candidates;
   unsigned int cvox_count;
   unsigned int pad[2];
+  unsigned long long rare_groups;  // epilogue diagnostics (lane max per warp)
+  unsigned long long all_groups;
 };
 
 // Workspace carve-up for one naive call.
@@ -58,6 +60,7 @@ struct TfillArgs {
   int64_t L, v;
   int n, n1, kpad, nk16;
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
+  int stride_full, stride_last;  // tile visiting strides (coprime with the chunk length)
   float alpha, beta, gamma, dthr;
   int4* cand;  // [L][n_chunks * groups][2]: top-4 (t~, voxel) pairs
   int32_t* susp;

@@ -78,59 +78,120 @@ __device__ __forceinline__ void stat_ud(uint32_t sbits, uint32_t qbits, float al
   d = fmaf(beta, fabsf(u), fmaf(alpha, Q, gamma));
 }
 
-// 32 columns (voxels jbase..jbase+31) of one accumulator row.  Pass 1 is
-// branch-free: every column's (u, d) and its "may enter the top-4 or is a
-// near-zero-variance suspect" bit, 32 independent dependency chains.  Pass 2
-// (rare) walks the set bits.  Using the group's entry threshold k3 for the
-// whole group is conservative: k3 only grows, insert() re-checks.
-template <bool TWO_SIDED, bool MASKED, bool DEBUG>
-__device__ __forceinline__ void epilogue_cols(const uint32_t (&s)[32], const uint32_t (&q)[32],
-                                              int jbase, int valid, float alpha, float beta,
-                                              float gamma, float dthr, Top4& top, int64_t p,
-                                              bool prow, const TfillArgs& a) {
-  const float k3 = top.k3;
-  uint32_t mask = 0;
+__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+struct EpiConst {
+  uint64_t alpha2, beta2, gamma2;  // packed (x, x)
+  float alpha, beta, gamma, dthr;
+};
+
+// Common path over 32 columns (voxels jbase..jbase+31) of one accumulator
+// row, packed f32x2 over column pairs, branch-free:
+//     m = S^2 - k3 * d      (d = alpha Q + beta S^2 + gamma)
+// m > 0 <=> |t| beats the row's 4th-best key k3 (two-sided exactly; signed:
+// a superset, negative t included).  A degenerate voxel (d ~ 0) has S^2 at
+// its maximum, so m > 0 there too.  Returns the per-column hit mask, built by
+// funnel-shifting the sign bits of m (one SHF per column).
+template <bool ALPHA0>
+__device__ __forceinline__ uint32_t group_hits(const uint32_t (&s)[32], const uint32_t (&q)[32],
+                                               const EpiConst& ec, float k3) {
+  const uint64_t nk3 = pack2(__float_as_uint(-k3), __float_as_uint(-k3));
+  uint32_t neg = 0;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    float u, d;
-    stat_ud<TWO_SIDED>(s[c], q[c], alpha, beta, gamma, u, d);
-    const bool hit = (u > k3 * d) | (d < dthr);
-    mask |= (hit ? 1u : 0u) << c;
-    if (DEBUG) {
-      if (prow && (!MASKED || c < valid)) {
-        float t = (d < dthr) ? __int_as_float(0x7fc00000) : copysignf(sqrtf(fabsf(u) / d), u);
-        a.dbg_t[p * a.v + jbase + c] = t;
-      }
+  for (int c = 30; c >= 0; c -= 2) {
+    const uint64_t S2 = pack2(s[c], s[c + 1]);
+    const uint64_t sq = mul2(S2, S2);
+    uint64_t d;
+    if (ALPHA0) {
+      d = fma2(ec.beta2, sq, ec.gamma2);
+    } else {
+      d = fma2(ec.alpha2, pack2(q[c], q[c + 1]), ec.gamma2);
+      d = fma2(ec.beta2, sq, d);
     }
+    const uint64_t m = fma2(nk3, d, sq);
+    neg = __funnelshift_l((uint32_t)(m >> 32), neg, 1);  // column c+1
+    neg = __funnelshift_l((uint32_t)m, neg, 1);          // column c
   }
-  if (MASKED) mask &= (valid >= 32) ? 0xffffffffu : ((1u << valid) - 1u);
-  if (__builtin_expect(mask != 0u, 0)) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      if (mask & (1u << c)) {
-        float u, d;
-        stat_ud<TWO_SIDED>(s[c], q[c], alpha, beta, gamma, u, d);
-        const int j = jbase + c;
-        if (d < dthr) {
-          // near-zero pooled variance: exact fp64 re-evaluation in K2
-          if (prow) {
-            unsigned slot = atomicAdd(&a.counters->susp_count, 1u);
-            if (slot < (unsigned)kSuspectCap) {
-              a.susp[2 * slot] = (int)p;
-              a.susp[2 * slot + 1] = j;
-            }
+  return ~neg;
+}
+
+// Rare path: the warp walks the union of its lanes' hit columns (uniform
+// loop); each column is re-read from TMEM (dynamic column = address, so no
+// register-array indexing) and every lane that flagged it re-tests exactly:
+// suspect listing for near-zero variance, else top-4 insertion.
+template <bool TWO_SIDED>
+__device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int jbase,
+                                           const EpiConst& ec, Top4& top, int64_t p, bool prow,
+                                           const TfillArgs& a) {
+  uint32_t uni = __reduce_or_sync(0xffffffffu, hits);
+  while (uni) {
+    const int c = __ffs(uni) - 1;
+    uni &= uni - 1;
+    uint32_t sb, qb;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(sb) : "r"(taddr_s + c));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                 : "=r"(qb)
+                 : "r"(taddr_s + kTileV + c));
+    tmem_ld_wait();
+    if ((hits >> c) & 1u) {
+      float u, d;
+      stat_ud<TWO_SIDED>(sb, qb, ec.alpha, ec.beta, ec.gamma, u, d);
+      const int j = jbase + c;
+      if (d < ec.dthr) {
+        // near-zero pooled variance: exact fp64 re-evaluation in K2
+        if (prow) {
+          unsigned slot = atomicAdd(&a.counters->susp_count, 1u);
+          if (slot < (unsigned)kSuspectCap) {
+            a.susp[2 * slot] = (int)p;
+            a.susp[2 * slot + 1] = j;
           }
-        } else {
-          top.insert(u / d, j);
         }
+      } else if (u > top.k3 * d) {
+        top.insert(u / d, j);
       }
     }
   }
 }
 
+template <bool TWO_SIDED>
+__device__ __forceinline__ void group_debug(const uint32_t (&s)[32], const uint32_t (&q)[32],
+                                            int jbase, int valid, const EpiConst& ec, int64_t p,
+                                            bool prow, const TfillArgs& a) {
+  if (!prow) return;
+  for (int c = 0; c < 32 && c < valid; ++c) {
+    float u, d;
+    stat_ud<TWO_SIDED>(s[c], q[c], ec.alpha, ec.beta, ec.gamma, u, d);
+    a.dbg_t[p * a.v + jbase + c] =
+        (d < ec.dthr) ? __int_as_float(0x7fc00000) : copysignf(sqrtf(fabsf(u) / d), u);
+  }
+}
+
+// i-th tile of a unit's chunk in a low-discrepancy (golden-ratio stride)
+// order: every permutation's top-4 threshold is close to final after the
+// first few percent of the sweep, which keeps the epilogue's rare path rare.
+__device__ __forceinline__ int chunk_tile(const TfillArgs& a, int t0, int t1, int i) {
+  const int T = t1 - t0;
+  const int stride = (T == a.tiles_per_chunk) ? a.stride_full : a.stride_last;
+  return t0 + (int)(((int64_t)i * stride) % T);
+}
+
 __device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
 
-template <int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool DEBUG>
+template <int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG>
 __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
   constexpr int HALF_BYTES = kTileN * BK * 2;  // one plane pair box (hi or lo)
@@ -189,7 +250,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         const int chunk = u / a.n_mtiles;
         const int t0 = chunk * a.tiles_per_chunk;
         const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
-        for (int t = t0; t < t1; ++t) {
+        for (int i = 0; i < t1 - t0; ++i) {
+          const int t = chunk_tile(a, t0, t1, i);
           for (int kb = 0; kb < a.kpad; kb += BK) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], STAGE_BYTES);
@@ -261,7 +323,14 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad + 32) are ours
     const int grp = ew / 4;
     const int row = quad * 32 + lane;
-    const float alpha = a.alpha, beta = a.beta, gamma = a.gamma, dthr = a.dthr;
+    EpiConst ec;
+    ec.alpha = a.alpha;
+    ec.beta = a.beta;
+    ec.gamma = a.gamma;
+    ec.dthr = a.dthr;
+    ec.alpha2 = pack2(__float_as_uint(a.alpha), __float_as_uint(a.alpha));
+    ec.beta2 = pack2(__float_as_uint(a.beta), __float_as_uint(a.beta));
+    ec.gamma2 = pack2(__float_as_uint(a.gamma), __float_as_uint(a.gamma));
     const int slots = a.n_chunks * GROUPS;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -290,34 +359,46 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       }
       Top4 top;
       top.reset();
-      for (int t = t0; t < t1; ++t) {
+      unsigned rare_groups = 0;
+      for (int i = 0; i < t1 - t0; ++i) {
+        const int t = chunk_tile(a, t0, t1, i);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const int64_t vleft = a.v - (int64_t)t * kTileV;
         const int valid = vleft < kTileV ? (int)vleft : kTileV;
 #pragma unroll 1
-        for (int g = grp * COLGROUPS; g < (grp + 1) * COLGROUPS; ++g) {
-          uint32_t sv[32], qv[32];
+        for (int g = 0; g < COLGROUPS; ++g) {
+          const int gc = (grp * COLGROUPS + g) * 32;
           const uint32_t taddr =
-              tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTileN + g * 32);
+              tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTileN + gc);
+          uint32_t sv[32], qv[32];
           tmem_ld32(taddr, sv);
           tmem_ld32(taddr + kTileV, qv);
           tmem_ld_wait();
-          const int jbase = t * kTileV + g * 32;
-          const int gvalid = valid - g * 32;
-          if (gvalid >= 32)
-            epilogue_cols<TWO_SIDED, false, DEBUG>(sv, qv, jbase, 32, alpha, beta, gamma, dthr,
-                                                   top, p, prow, a);
-          else if (gvalid > 0)
-            epilogue_cols<TWO_SIDED, true, DEBUG>(sv, qv, jbase, gvalid, alpha, beta, gamma,
-                                                  dthr, top, p, prow, a);
+          const int jbase = t * kTileV + gc;
+          const int gvalid = valid - gc;
+          if (DEBUG) group_debug<TWO_SIDED>(sv, qv, jbase, gvalid, ec, p, prow, a);
+          if (gvalid <= 0) continue;
+          uint32_t hits = group_hits<ALPHA0>(sv, qv, ec, top.k3);
+          if (gvalid < 32) hits &= (1u << gvalid) - 1u;
+          if (__any_sync(0xffffffffu, hits != 0u)) {
+            ++rare_groups;
+            group_rare<TWO_SIDED>(hits, taddr, jbase, ec, top, p, prow, a);
+          }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained
         if (++acc == kNumAcc) {
           acc = 0;
           acc_phase ^= 1;
+        }
+      }
+      {
+        // diagnostics: warp-groups that entered the rare path / all warp-groups
+        if (lane == 0) {
+          atomicAdd(&a.counters->rare_groups, (unsigned long long)rare_groups);
+          atomicAdd(&a.counters->all_groups, (unsigned long long)((t1 - t0) * COLGROUPS));
         }
       }
       if (prow) {
@@ -359,10 +440,11 @@ size_t smem_bytes_for(int bk, int stages, int kpad) {
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
 
-template <int BK, int STAGES, int EPI, bool TS, bool DBG>
+template <int BK, int STAGES, bool TS, bool A0, bool DBG>
 cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                        cudaStream_t s) {
-  auto kern = k_tfill_tc<BK, STAGES, EPI, TS, DBG>;
+  constexpr int EPI = 8;
+  auto kern = k_tfill_tc<BK, STAGES, EPI, TS, A0, DBG>;
   const size_t smem = smem_bytes_for(BK, STAGES, lay.kpad);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -370,26 +452,21 @@ cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtenso
   return cudaGetLastError();
 }
 
-template <bool TS, bool DBG>
+template <bool TS, bool A0, bool DBG>
 cudaError_t dispatch(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                      cudaStream_t s) {
-  // epilogue width: 8 warps when the K loop is short (epilogue-bound), else 4
-  const bool wide = lay.groups == 2;
-  if (lay.bk == 64) {
-    if (lay.stages >= 3)
-      return wide ? launch_cfg<64, 3, 8, TS, DBG>(lay, a, map, s)
-                  : launch_cfg<64, 3, 4, TS, DBG>(lay, a, map, s);
-    return wide ? launch_cfg<64, 2, 8, TS, DBG>(lay, a, map, s)
-                : launch_cfg<64, 2, 4, TS, DBG>(lay, a, map, s);
-  }
-  if (lay.stages >= 4)
-    return wide ? launch_cfg<32, 4, 8, TS, DBG>(lay, a, map, s)
-                : launch_cfg<32, 4, 4, TS, DBG>(lay, a, map, s);
-  if (lay.stages == 3)
-    return wide ? launch_cfg<32, 3, 8, TS, DBG>(lay, a, map, s)
-                : launch_cfg<32, 3, 4, TS, DBG>(lay, a, map, s);
-  return wide ? launch_cfg<32, 2, 8, TS, DBG>(lay, a, map, s)
-              : launch_cfg<32, 2, 4, TS, DBG>(lay, a, map, s);
+  if (lay.bk == 64) return launch_cfg<64, 3, TS, A0, DBG>(lay, a, map, s);
+  if (lay.stages >= 4) return launch_cfg<32, 4, TS, A0, DBG>(lay, a, map, s);
+  return launch_cfg<32, 3, TS, A0, DBG>(lay, a, map, s);
+}
+
+template <bool TS>
+cudaError_t dispatch_a(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                       cudaStream_t s) {
+  const bool a0 = a.alpha == 0.0f;
+  if (a.dbg_t) return a0 ? dispatch<TS, true, true>(lay, a, map, s)
+                         : dispatch<TS, false, true>(lay, a, map, s);
+  return a0 ? dispatch<TS, true, false>(lay, a, map, s) : dispatch<TS, false, false>(lay, a, map, s);
 }
 
 }  // namespace
@@ -412,10 +489,7 @@ cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __
                             int two_sided, cudaStream_t s) {
   CUtensorMap map;
   if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk)) return cudaErrorInvalidValue;
-  const bool dbg = a.dbg_t != nullptr;
-  if (two_sided)
-    return dbg ? dispatch<true, true>(lay, a, map, s) : dispatch<true, false>(lay, a, map, s);
-  return dbg ? dispatch<false, true>(lay, a, map, s) : dispatch<false, false>(lay, a, map, s);
+  return two_sided ? dispatch_a<true>(lay, a, map, s) : dispatch_a<false>(lay, a, map, s);
 }
 
 size_t tfill_smem_bytes(int bk, int stages, int kpad) { return smem_bytes_for(bk, stages, kpad); }
