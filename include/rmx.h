@@ -64,6 +64,8 @@ typedef struct rmx_naive_stats {
   int32_t bk;              /* K elements per stage */
   int64_t rare_groups;     /* epilogue: 32-column groups that took the exact path */
   int64_t all_groups;      /* epilogue: all 32-column groups (per warp) */
+  int32_t cg;              /* CTAs per MMA tile (tcgen05 cta_group 1 or 2) */
+  int32_t _pad;
 } rmx_naive_stats;
 
 int rmx_abi_version(void);

@@ -49,6 +49,8 @@ class NaiveStats(ctypes.Structure):
         ("bk", ctypes.c_int32),
         ("rare_groups", ctypes.c_int64),
         ("all_groups", ctypes.c_int64),
+        ("cg", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

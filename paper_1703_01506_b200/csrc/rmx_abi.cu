@@ -15,7 +15,7 @@
 
 namespace rmx {
 
-size_t tfill_smem_bytes(int bk, int stages, int kpad);
+size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad);
 
 namespace {
 
@@ -61,23 +61,47 @@ int check_dims(int64_t v, int32_t n, int32_t n1, int64_t L, rmx_status* st) {
 }
 
 // Stage/BK choice for the tensor-core kernel; returns false when the A tile
-// does not fit next to a 2-stage ring (n > ~640).
-bool pick_pipeline(int kpad, int* bk, int* stages) {
+// does not fit next to a minimal ring (n > ~640).  Instantiated configs
+// (tfill_tc.cu): cg=1 (64,3) (32,4) (32,3); cg=2 (64,6) (64,4) (32,7) (32,4).
+bool pick_pipeline(int cg, int kpad, int* bk, int* stages) {
   const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024;
   if (a_bytes >= kMaxSmem) return false;
   const size_t avail = kMaxSmem - a_bytes;
-  int b = kpad <= 32 ? 32 : 64;
-  int s = (int)(avail / ((size_t)2 * 2 * kTileV * b * 2));
-  if (b == 64 && s < 3) {
-    b = 32;
-    s = (int)(avail / ((size_t)2 * 2 * kTileV * b * 2));
+  auto fit = [&](int b) { return (int)(avail / ((size_t)2 * (2 * kTileV / cg) * b * 2)); };
+  if (cg == 1) {
+    if (kpad > 32 && fit(64) >= 3) {
+      *bk = 64;
+      *stages = 3;
+      return true;
+    }
+    const int s = std::min(fit(32), 4);
+    if (s < 3) return false;
+    *bk = 32;
+    *stages = s;
+    return true;
   }
-  s = std::min(s, b == 64 ? 3 : 4);
-  if (b == 64 && s < 3) return false;
-  if (s < 2) return false;
-  *bk = b;
-  *stages = s;
-  return true;
+  if (kpad > 32 && fit(64) >= 6) {
+    *bk = 64;
+    *stages = 6;
+    return true;
+  }
+  const int s32 = fit(32);
+  if (s32 >= 7) {
+    *bk = 32;
+    *stages = 7;
+    return true;
+  }
+  if (kpad > 32 && fit(64) >= 4) {
+    *bk = 64;
+    *stages = 4;
+    return true;
+  }
+  if (s32 >= 4) {
+    *bk = 32;
+    *stages = 4;
+    return true;
+  }
+  return false;
 }
 
 }  // namespace
@@ -93,11 +117,21 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
   NaiveLayout lay{};
   lay.kpad = (n + 15) / 16 * 16;
   lay.n_vtiles = (int)((v + kTileV - 1) / kTileV);
-  lay.n_mtiles = (int)((L + kTileM - 1) / kTileM);
-  if (!pick_pipeline(lay.kpad, &lay.bk, &lay.stages)) {
-    lay.bk = 0;
-    lay.stages = 0;
+  // CTA pairs (cta_group::2) by default; RMX_CG=1 forces single-CTA tiles
+  // (pairs halve B traffic per SM and deepen the ring; short-K tiles are
+  // epilogue-bound and run better as single CTAs)
+  lay.cg = lay.kpad >= 192 ? 2 : 1;
+  if (const char* e = getenv("RMX_CG")) lay.cg = atoi(e) == 1 ? 1 : 2;
+  if (!pick_pipeline(lay.cg, lay.kpad, &lay.bk, &lay.stages)) {
+    lay.cg = 1;
+    if (!pick_pipeline(1, lay.kpad, &lay.bk, &lay.stages)) {
+      lay.bk = 0;
+      lay.stages = 0;
+    }
   }
+  const int tile_perms = kTileM * lay.cg;
+  lay.n_mtiles = (int)((L + tile_perms - 1) / tile_perms);
+  const int n_clusters = std::max(1, sm_count / lay.cg);
   // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
   lay.groups = 2;  // 8 epilogue warps: two per TMEM lane quadrant
   // Voxel chunks per permutation tile: minimise the static round-robin
@@ -111,7 +145,7 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
     const int nc = (lay.n_vtiles + tpc - 1) / tpc;
     if (nc != c) continue;
     const int64_t units = (int64_t)lay.n_mtiles * nc;
-    const int grid = (int)std::min<int64_t>(sm_count, units);
+    const int grid = (int)std::min<int64_t>(n_clusters, units);
     double worst = 0;
     for (int b = 0; b < std::min(grid, 8); ++b) {  // CTA 0.. carry the most units
       double w = 0;
@@ -130,13 +164,13 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
   }
   lay.tiles_per_chunk = (lay.n_vtiles + best_c - 1) / best_c;
   lay.n_chunks = (lay.n_vtiles + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
-  lay.grid = (int)std::min<int64_t>(sm_count, (int64_t)lay.n_mtiles * lay.n_chunks);
+  lay.grid = lay.cg * (int)std::min<int64_t>(n_clusters, (int64_t)lay.n_mtiles * lay.n_chunks);
 
   size_t off = 0;
   lay.off_planes = off;
   off = align_up(off + (size_t)4 * v * lay.kpad * 2, 1024);
   lay.off_cand = off;
-  off = align_up(off + (size_t)L * lay.n_chunks * lay.groups * 32, 256);
+  off = align_up(off + (size_t)lay.n_mtiles * tile_perms * lay.n_chunks * lay.groups * 32, 256);
   lay.off_susp = off;
   off = align_up(off + (size_t)kSuspectCap * 8, 256);
   lay.off_cvox = off;
@@ -329,6 +363,7 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
     stats->grid = ws.lay.grid;
     stats->stages = ws.lay.stages;
     stats->bk = ws.lay.bk;
+    stats->cg = ws.lay.cg;
   }
   return RMX_OK;
 }
@@ -404,6 +439,7 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
     stats->grid = ws.lay.grid;
     stats->stages = ws.lay.stages;
     stats->bk = ws.lay.bk;
+    stats->cg = ws.lay.cg;
   }
   return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);
 }

@@ -40,6 +40,7 @@ struct NaiveCounters {
 struct NaiveLayout {
   int kpad;           // n rounded up to 16 (MMA K granularity)
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk, groups, grid, bk, stages;
+  int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
   size_t off_planes, off_cand, off_susp, off_cvox, off_overflow, off_const, off_counters;
   size_t total;
 };

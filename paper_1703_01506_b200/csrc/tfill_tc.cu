@@ -191,17 +191,24 @@ __device__ __forceinline__ int chunk_tile(const TfillArgs& a, int t0, int t1, in
 
 __device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
 
-template <int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG>
+// CG = 1: one CTA computes a 128-permutation x 128-voxel tile (M = 128).
+// CG = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a
+//   256 x 128 tile with M = 256 MMAs issued by the leader CTA: each CTA holds
+//   its own 128-permutation A tile and loads HALF of every B tile (rank 0 the
+//   Z planes, rank 1 the Z^2 planes), so per-SM B traffic halves and the
+//   smem ring gets ~2x deeper.  Each CTA's TMEM receives its own 128 rows x
+//   256 columns, so the epilogue is identical.
+template <int CG, int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG>
 __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
-  constexpr int HALF_BYTES = kTileN * BK * 2;  // one plane pair box (hi or lo)
+  constexpr int HALF_BYTES = (kTileN / CG) * BK * 2;  // this CTA's hi (or lo) box
   constexpr int STAGE_BYTES = 2 * HALF_BYTES;
   constexpr int KSTEPS = BK / 16;
   constexpr uint32_t B_LAYOUT = (BK == 64) ? 2u : 4u;  // 128B : 64B swizzle
   constexpr uint32_t B_SBO = (BK == 64) ? 1024u : 512u;
   constexpr int GROUPS = EPI_WARPS / 4;  // epilogue warps sharing a TMEM lane quadrant
   constexpr int COLGROUPS = kTileV / 32 / GROUPS;
-  constexpr uint32_t IDESC = idesc_f16_f32(kTileM, kTileN);
+  constexpr uint32_t IDESC = idesc_f16_f32(kTileM * CG, kTileN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -219,6 +226,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
 
   const int warp = (int)warp_id();
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -227,37 +236,50 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     }
     for (int i = 0; i < kNumAcc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS);
+      mbar_init(&tempty[i], EPI_WARPS * CG);
     }
-    mbar_init(afull, kTileM);
+    mbar_init(afull, kTileM * CG);
     fence_mbar_init();
     tma_prefetch(&pmap);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if (CG == 2) tmem_alloc_2sm(tmem_slot, 512);
+    else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   const int n_units = a.n_mtiles * a.n_chunks;
+  const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = unit0; u < n_units; u += unit_step) {
         const int chunk = u / a.n_mtiles;
         const int t0 = chunk * a.tiles_per_chunk;
         const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
         for (int i = 0; i < t1 - t0; ++i) {
           const int t = chunk_tile(a, t0, t1, i);
           for (int kb = 0; kb < a.kpad; kb += BK) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], STAGE_BYTES);
             uint8_t* dst = stage_mem + stage * STAGE_BYTES;
-            tma_load_3d(dst, &pmap, &full[stage], kb, t * kTileV, 0);               // z_hi, q_hi
-            tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV, 2);  // z_lo, q_lo
+            if (CG == 2) {
+              mbar_wait_cluster(&empty[stage], phase ^ 1);
+              if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+              tma_load_3d_2sm(dst, &pmap, &full[stage], kb, t * kTileV, (int)rank);  // z_hi | q_hi
+              tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV,
+                              2 + (int)rank);  // z_lo | q_lo
+            } else {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_expect_tx(&full[stage], STAGE_BYTES);
+              tma_load_3d(dst, &pmap, &full[stage], kb, t * kTileV, 0);               // z_hi, q_hi
+              tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV, 2);  // z_lo, q_lo
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -269,51 +291,65 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t a_base = smem_u32(a_mem);
-    const uint32_t a_sbo = (uint32_t)a.kpad * 16u;
-    int stage = 0;
-    uint32_t phase = 0, acc_phase = 0, a_phase = 0;
-    int acc = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int chunk = u / a.n_mtiles;
-      const int t0 = chunk * a.tiles_per_chunk;
-      const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
-      mbar_wait(afull, a_phase);
-      a_phase ^= 1;
-      tc_fence_after();
-      for (int t = t0; t < t1; ++t) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    if (leader) {
+      const uint32_t a_base = smem_u32(a_mem);
+      const uint32_t a_sbo = (uint32_t)a.kpad * 16u;
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0, a_phase = 0;
+      int acc = 0;
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const int chunk = u / a.n_mtiles;
+        const int t0 = chunk * a.tiles_per_chunk;
+        const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+        if (CG == 2) mbar_wait_cluster(afull, a_phase);
+        else mbar_wait(afull, a_phase);
+        a_phase ^= 1;
         tc_fence_after();
-        const uint32_t d_tmem = tmem + (uint32_t)(acc * kTileN);
-        for (int kb = 0; kb < a.kpad; kb += BK) {
-          mbar_wait(&full[stage], phase);
+        for (int t = t0; t < t1; ++t) {
+          if (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+          else mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
-          if (elect_one()) {
-            const uint32_t sb = smem_u32(stage_mem + stage * STAGE_BYTES);
+          const uint32_t d_tmem = tmem + (uint32_t)(acc * kTileN);
+          for (int kb = 0; kb < a.kpad; kb += BK) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t sb = smem_u32(stage_mem + stage * STAGE_BYTES);
 #pragma unroll
-            for (int s = 0; s < KSTEPS; ++s) {
-              const int ks = kb / 16 + s;
-              if (ks < a.nk16) {
-                const uint64_t adesc = smem_desc(a_base + (uint32_t)ks * 256u, 128u, a_sbo, 0u);
-                const uint64_t bh = smem_desc(sb + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
-                const uint64_t bl =
-                    smem_desc(sb + (uint32_t)HALF_BYTES + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
-                mma_f16_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
-                mma_f16_ss(d_tmem, adesc, bl, IDESC, 1u);
+              for (int s = 0; s < KSTEPS; ++s) {
+                const int ks = kb / 16 + s;
+                if (ks < a.nk16) {
+                  const uint64_t adesc = smem_desc(a_base + (uint32_t)ks * 256u, 128u, a_sbo, 0u);
+                  const uint64_t bh = smem_desc(sb + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
+                  const uint64_t bl = smem_desc(sb + (uint32_t)HALF_BYTES + (uint32_t)s * 32u, 16u,
+                                                B_SBO, B_LAYOUT);
+                  if (CG == 2) {
+                    mma_f16_ss_2sm(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
+                    mma_f16_ss_2sm(d_tmem, adesc, bl, IDESC, 1u);
+                  } else {
+                    mma_f16_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
+                    mma_f16_ss(d_tmem, adesc, bl, IDESC, 1u);
+                  }
+                }
+              }
+              if (CG == 2) {
+                mma_commit_2sm(&empty[stage], 0x3);                       // both smem slots free
+                if (kb + BK >= a.kpad) mma_commit_2sm(&tfull[acc], 0x3);  // both accumulators
+              } else {
+                mma_commit(&empty[stage]);
+                if (kb + BK >= a.kpad) mma_commit(&tfull[acc]);
               }
             }
-            mma_commit(&empty[stage]);                        // smem slot reusable
-            if (kb + BK >= a.kpad) mma_commit(&tfull[acc]);   // accumulator ready
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          __syncwarp();
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+          if (++acc == kNumAcc) {
+            acc = 0;
+            acc_phase ^= 1;
           }
-        }
-        if (++acc == kNumAcc) {
-          acc = 0;
-          acc_phase ^= 1;
         }
       }
     }
@@ -334,12 +370,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     const int slots = a.n_chunks * GROUPS;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = unit0; u < n_units; u += unit_step) {
       const int mtile = u % a.n_mtiles;
       const int chunk = u / a.n_mtiles;
       const int t0 = chunk * a.tiles_per_chunk;
       const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
-      const int64_t p = (int64_t)mtile * kTileM + row;
+      const int64_t p = ((int64_t)mtile * CG + rank) * kTileM + row;
       const bool prow = p < a.L;
       if (grp == 0) {
         // A row `row`: G[p, k] = 1 for k in orders[p, :n1] (canonical K-major
@@ -355,14 +391,16 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           }
         }
         fence_proxy_async_smem();
-        mbar_arrive(afull);
+        if (CG == 2) mbar_arrive_cluster(afull, 0);
+        else mbar_arrive(afull);
       }
       Top4 top;
       top.reset();
       unsigned rare_groups = 0;
       for (int i = 0; i < t1 - t0; ++i) {
         const int t = chunk_tile(a, t0, t1, i);
-        mbar_wait(&tfull[acc], acc_phase);
+        if (CG == 2) mbar_wait_cluster(&tfull[acc], acc_phase);
+        else mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const int64_t vleft = a.v - (int64_t)t * kTileV;
         const int valid = vleft < kTileV ? (int)vleft : kTileV;
@@ -388,18 +426,18 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained
+        if (lane == 0) {  // accumulator drained
+          if (CG == 2) mbar_arrive_cluster(&tempty[acc], 0);
+          else mbar_arrive(&tempty[acc]);
+        }
         if (++acc == kNumAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      {
-        // diagnostics: warp-groups that entered the rare path / all warp-groups
-        if (lane == 0) {
-          atomicAdd(&a.counters->rare_groups, (unsigned long long)rare_groups);
-          atomicAdd(&a.counters->all_groups, (unsigned long long)((t1 - t0) * COLGROUPS));
-        }
+      if (lane == 0) {  // diagnostics: warp-groups that took the rare path / all
+        atomicAdd(&a.counters->rare_groups, (unsigned long long)rare_groups);
+        atomicAdd(&a.counters->all_groups, (unsigned long long)((t1 - t0) * COLGROUPS));
       }
       if (prow) {
         int4* dst = a.cand + 2 * (p * slots + chunk * GROUPS + grp);
@@ -411,10 +449,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if (CG == 2) tmem_dealloc_2sm(tmem, 512);
+    else tmem_dealloc(tmem, 512);
   }
 }
 
@@ -433,31 +473,50 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-size_t smem_bytes_for(int bk, int stages, int kpad) {
-  const size_t stage = (size_t)2 * kTileN * bk * 2;
+size_t smem_bytes_for(int cg, int bk, int stages, int kpad) {
+  const size_t stage = (size_t)2 * (kTileN / cg) * bk * 2;
   size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024;
   // one CTA per SM: TMEM (512 columns) is allocated whole by each CTA
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
 
-template <int BK, int STAGES, bool TS, bool A0, bool DBG>
+template <int CG, int BK, int STAGES, bool TS, bool A0, bool DBG>
 cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                        cudaStream_t s) {
   constexpr int EPI = 8;
-  auto kern = k_tfill_tc<BK, STAGES, EPI, TS, A0, DBG>;
-  const size_t smem = smem_bytes_for(BK, STAGES, lay.kpad);
+  auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG>;
+  const size_t smem = smem_bytes_for(CG, BK, STAGES, lay.kpad);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<lay.grid, 64 + 32 * EPI, smem, s>>>(map, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)lay.grid);
+  cfg.blockDim = dim3(64 + 32 * EPI);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, map, a);
 }
 
 template <bool TS, bool A0, bool DBG>
 cudaError_t dispatch(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                      cudaStream_t s) {
-  if (lay.bk == 64) return launch_cfg<64, 3, TS, A0, DBG>(lay, a, map, s);
-  if (lay.stages >= 4) return launch_cfg<32, 4, TS, A0, DBG>(lay, a, map, s);
-  return launch_cfg<32, 3, TS, A0, DBG>(lay, a, map, s);
+  if (lay.cg == 2) {
+    if (lay.bk == 64) {
+      if (lay.stages >= 6) return launch_cfg<2, 64, 6, TS, A0, DBG>(lay, a, map, s);
+      return launch_cfg<2, 64, 4, TS, A0, DBG>(lay, a, map, s);
+    }
+    if (lay.stages >= 7) return launch_cfg<2, 32, 7, TS, A0, DBG>(lay, a, map, s);
+    return launch_cfg<2, 32, 4, TS, A0, DBG>(lay, a, map, s);
+  }
+  if (lay.bk == 64) return launch_cfg<1, 64, 3, TS, A0, DBG>(lay, a, map, s);
+  if (lay.stages >= 4) return launch_cfg<1, 32, 4, TS, A0, DBG>(lay, a, map, s);
+  return launch_cfg<1, 32, 3, TS, A0, DBG>(lay, a, map, s);
 }
 
 template <bool TS>
@@ -471,12 +530,13 @@ cudaError_t dispatch_a(const NaiveLayout& lay, const TfillArgs& a, const CUtenso
 
 }  // namespace
 
-bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad, int bk) {
+bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad, int bk,
+                     int planes_per_box) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)v, 4};
   cuuint64_t strides[2] = {(cuuint64_t)kpad * 2, (cuuint64_t)v * kpad * 2};
-  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)kTileV, 2};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)kTileV, (cuuint32_t)planes_per_box};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(planes), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -488,10 +548,13 @@ bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s) {
   CUtensorMap map;
-  if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk)) return cudaErrorInvalidValue;
+  if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk, 2 / lay.cg))
+    return cudaErrorInvalidValue;
   return two_sided ? dispatch_a<true>(lay, a, map, s) : dispatch_a<false>(lay, a, map, s);
 }
 
-size_t tfill_smem_bytes(int bk, int stages, int kpad) { return smem_bytes_for(bk, stages, kpad); }
+size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad) {
+  return smem_bytes_for(cg, bk, stages, kpad);
+}
 
 }  // namespace rmx
