@@ -177,6 +177,8 @@ NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
   off = align_up(off + (size_t)v * 4, 256);
   lay.off_overflow = off;
   off = align_up(off + (size_t)L * 4, 256);
+  lay.off_best = off;
+  off = align_up(off + (size_t)L * 4, 256);
   lay.off_const = off;
   off = align_up(off + sizeof(ConstInfo), 256);
   lay.off_counters = off;
@@ -212,6 +214,7 @@ struct Ws {
   int32_t* susp() const { return reinterpret_cast<int32_t*>(base + lay.off_susp); }
   int32_t* cvox() const { return reinterpret_cast<int32_t*>(base + lay.off_cvox); }
   int32_t* overflow() const { return reinterpret_cast<int32_t*>(base + lay.off_overflow); }
+  uint32_t* best() const { return reinterpret_cast<uint32_t*>(base + lay.off_best); }
   ConstInfo* cinfo() const { return reinterpret_cast<ConstInfo*>(base + lay.off_const); }
   NaiveCounters* counters() const { return reinterpret_cast<NaiveCounters*>(base + lay.off_counters); }
 };
@@ -310,6 +313,7 @@ int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   RMX_CUDA(cudaMemsetAsync(ws.counters(), 0, sizeof(NaiveCounters), s));
   RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
+  RMX_CUDA(cudaMemsetAsync(ws.best(), 0, (size_t)L * 4, s));
   PrepArgs pa{x, v, n, n1, ws.lay.kpad, ws.planes(), ws.cvox(), ws.counters()};
   RMX_CUDA(launch_prep(pa, s));
   RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
@@ -355,6 +359,7 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   a.dthr = (float)(1e-4 * bmax);
   a.cand = ws.cand();
   a.susp = ws.susp();
+  a.best_t = ws.best();
   a.counters = ws.counters();
   a.dbg_t = dbg;
   RMX_CUDA(launch_tfill_tc(ws.lay, a, ws.planes(), two_sided, static_cast<cudaStream_t>(stream)));

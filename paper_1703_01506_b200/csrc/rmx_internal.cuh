@@ -41,7 +41,8 @@ struct NaiveLayout {
   int kpad;           // n rounded up to 16 (MMA K granularity)
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk, groups, grid, bk, stages;
   int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
-  size_t off_planes, off_cand, off_susp, off_cvox, off_overflow, off_const, off_counters;
+  size_t off_planes, off_cand, off_susp, off_cvox, off_overflow, off_best, off_const,
+      off_counters;
   size_t total;
 };
 
@@ -65,6 +66,7 @@ struct TfillArgs {
   float alpha, beta, gamma, dthr;
   int4* cand;  // [L][n_chunks * groups][2]: top-4 (t~, voxel) pairs
   int32_t* susp;
+  uint32_t* best_t;  // [L] running best t~ per permutation (order-encoded, 0 = none)
   NaiveCounters* counters;
   float* dbg_t;  // [L][v] when debugging
 };

@@ -44,8 +44,10 @@ constexpr int kTileN = 2 * kTileV;
 struct Top4 {
   float k0, k1, k2, k3;
   int j0, j1, j2, j3;
-  __device__ __forceinline__ void reset() {
-    k0 = k1 = k2 = k3 = -FLT_MAX;
+  // Entries below `floor` can never be refinement candidates (see seed_key),
+  // so the threshold starts there; unfilled slots keep voxel -1.
+  __device__ __forceinline__ void reset(float floor) {
+    k0 = k1 = k2 = k3 = floor;
     j0 = j1 = j2 = j3 = -1;
   }
   __device__ __forceinline__ void insert(float key, int j) {
@@ -190,6 +192,31 @@ __device__ __forceinline__ int chunk_tile(const TfillArgs& a, int t0, int t1, in
 }
 
 __device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
+
+// Order-preserving float <-> uint32 map for atomicMax; 0 = "no value yet".
+__device__ __forceinline__ uint32_t ord_enc(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord_dec(uint32_t e) {
+  return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
+}
+
+// Threshold seed from the permutation's best t~ over chunks finished so far
+// (best_t, written by earlier units).  K2 refines exactly the voxels with
+// t~ >= t~max - band(t~max), and t~max >= seed, so nothing below
+// seed - 2 band(seed) can matter: starting the top-4 there is exact and
+// keeps the epilogue's rare path rare.
+template <bool TWO_SIDED>
+__device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, bool prow) {
+  if (!prow) return -FLT_MAX;
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(best_t + p);
+  if (e == 0u) return -FLT_MAX;
+  const float t = ord_dec(e);
+  const float lo = t - 2.0f * kBandRel * fmaxf(fabsf(t), 1.0f);
+  if (TWO_SIDED) return lo > 0.0f ? lo * lo : 0.0f;
+  return lo * fabsf(lo);
+}
 
 // CG = 1: one CTA computes a 128-permutation x 128-voxel tile (M = 128).
 // CG = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a
@@ -395,7 +422,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         else mbar_arrive(afull);
       }
       Top4 top;
-      top.reset();
+      top.reset(seed_key<TWO_SIDED>(a.best_t, p, prow));
       unsigned rare_groups = 0;
       for (int i = 0; i < t1 - t0; ++i) {
         const int t = chunk_tile(a, t0, t1, i);
@@ -439,6 +466,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         atomicAdd(&a.counters->rare_groups, (unsigned long long)rare_groups);
         atomicAdd(&a.counters->all_groups, (unsigned long long)((t1 - t0) * COLGROUPS));
       }
+      if (prow && top.j0 >= 0) atomicMax(a.best_t + p, ord_enc(key_to_t(top.k0)));
       if (prow) {
         int4* dst = a.cand + 2 * (p * slots + chunk * GROUPS + grp);
         dst[0] = make_int4(__float_as_int(top.j0 >= 0 ? key_to_t(top.k0) : -FLT_MAX), top.j0,
