@@ -138,6 +138,73 @@ int rmx_tstat_pairs(const double *x, int64_t v, int32_t n, int32_t n1,
                     double *t_out, double *num_out, int32_t *deg_out, void *stream,
                     rmx_status *st);
 
+/* ---------------------------------------------------------------- RapidPT
+ * Replaces reference rapid.py:138-206 (_recover_block), lrmc.py:127-157
+ * (solve_block / fit_coefficients / complete_column) and lrmc.py:160-268
+ * (track_update / train_basis).  Observation sets (Omega) and labels are
+ * drawn host-side with the reference's own streams and passed in, so they
+ * are bit-identical; the Gaussian residuals of the recovery are drawn on the
+ * device from a counter-based Philox stream keyed by (seed, permutation)
+ * ("RapidPT noise").
+ *
+ * rmx_rapid_stats: t_out[p*k + i] = statistic of voxel omegas[p*k + i] under
+ *   orders[p] (bit-identical to the reference's batched _welch_rows).
+ *   Degenerate -> RMX_E_DEGENERATE with perm = p, voxel = i (Omega index). */
+int rmx_rapid_stats(const double *x, int64_t v, int32_t n, int32_t n1,
+                    const int16_t *orders, const int32_t *omegas, int64_t L, int32_t k,
+                    double *t_out, void *stream, rmx_status *st);
+
+/* Batched least squares on gathered rows (solve_block semantics):
+ *   w_b = argmin |U[idx_b] w - vals_b|  via G = A^T A, A = [U[idx_b] | vals_b],
+ *   Cholesky in fp64.  idx = NULL uses rows 0..k-1.  flag_out[b] = 1 for a
+ *   rank-deficient restriction (caller resamples, rapid.py:173-196).
+ *   norms_out[4b..4b+3] = (|resid|^2 by the normal equations, |w|^2,
+ *   min L_ii, max L_ii) -- max/min L_ii is a lower bound of the reference's
+ *   condition number sqrt(lambda_max / lambda_min) of U_Omega. */
+size_t rmx_lsq_workspace_bytes(int32_t r, int64_t batch);
+int rmx_lsq_solve(const double *u, int64_t ldu, int32_t r, const int32_t *idx, int32_t k,
+                  const double *vals, int64_t B, double *w_out, int32_t *flag_out,
+                  double *norms_out, void *workspace, size_t workspace_bytes, void *stream,
+                  rmx_status *st);
+
+/* Completion + residual + max (rapid.py:198-205): for each of B columns,
+ *   max_out[b] = max_j op(W[b] . U[j] + sigma * z(perm_base + b, j)) + mu,
+ * op = |.| when two_sided.  z is Philox N(0,1) unless znoise (B x v fp32) is
+ * given; base (B x v fp64) switches to op(base - W[b].U[j]) (residual-sup). */
+int rmx_complete_max(const float *u32, int64_t v, int32_t r, const float *w32, int64_t B,
+                     int64_t perm_base, double sigma, double mu, uint64_t seed,
+                     int32_t two_sided, const float *znoise, const double *base,
+                     double *max_out, void *stream, rmx_status *st);
+
+/* Small helpers used by the host orchestration. */
+int rmx_to_f32(const double *a, int64_t n, float *out, void *stream, rmx_status *st);
+int rmx_row_max(const double *a, int64_t rows, int64_t cols, int32_t two_sided, double *out,
+                void *stream, rmx_status *st);
+int rmx_resid_batch(const double *u, int32_t r, const int32_t *idx, int32_t k,
+                    const double *vals, const double *w, int64_t B, double *resid,
+                    void *stream, rmx_status *st);
+int rmx_gather_rows(const double *t, int64_t ldt, const int32_t *idx, int32_t k, int64_t B,
+                    double *out, void *stream, rmx_status *st);
+int rmx_gemv(const double *u, int64_t v, int32_t r, const double *w, double *out, void *stream,
+             rmx_status *st);
+int rmx_mean_var(const double *a, int64_t n, double *out2, void *stream, rmx_status *st);
+/* CholeskyQR2 re-orthonormalisation of U (v x r) when max|U^T U - I| > 1e-8
+ * (or always with force); *drift receives the error before the call. */
+int rmx_orthonormalize(double *u, int64_t v, int32_t r, int32_t force, double *drift,
+                       void *stream, rmx_status *st);
+
+/* GROUSE training (train_basis): t is ell x v (training statistics,
+ * perm-major), omegas0 max_passes x ell x k first-attempt observation sets,
+ * u (v x r) the initial orthonormal basis, updated in place.  cb draws the
+ * next observation set of (col, pass) on an ill-conditioned restriction. */
+typedef int (*rmx_omega_cb)(void *user, int32_t col, int32_t pass, int32_t attempt,
+                            int32_t *omega_out);
+int rmx_grouse_train(const double *t, int64_t v, int32_t ell, int32_t r, int32_t k,
+                     const int32_t *omegas0, int32_t max_passes, double tol, double *u,
+                     rmx_omega_cb cb, void *user, double *pass_resid, int32_t *passes_out,
+                     int32_t *converged_out, int64_t *updates_out, int32_t *final_omegas,
+                     void *stream, rmx_status *st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,16 @@ from .exceptions import (  # noqa: F401
     UsageError,
 )
 from .naive_engine import NaiveJob, NaiveResult, run_naive, run_naive_ex  # noqa: F401
+from .rapid_engine import (  # noqa: F401
+    complete_column,
+    fit_coefficients,
+    init_basis,
+    recover,
+    run_rapid,
+    solve_block,
+    train,
+    train_basis,
+)
 from .stats import (  # noqa: F401
     column_max,
     pvalue,
@@ -46,5 +56,6 @@ __all__ = [
     "DataFormatError", "DegenerateVoxelError", "EngineUnavailableError",
     "IllConditionedBasisError", "NumericalError", "UsageError", "NaiveJob", "NaiveResult",
     "run_naive", "run_naive_ex", "column_max", "pvalue", "reject_set", "stat_map",
-    "threshold_at", "tstat_full", "tstat_subset",
+    "threshold_at", "tstat_full", "tstat_subset", "complete_column", "fit_coefficients",
+    "init_basis", "recover", "run_rapid", "solve_block", "train", "train_basis",
 ]

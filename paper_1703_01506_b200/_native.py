@@ -69,9 +69,27 @@ EXPORTS = (
     "rmx_naive_tfill_debug",
     "rmx_tstat_exact",
     "rmx_tstat_pairs",
+    "rmx_rapid_stats",
+    "rmx_lsq_workspace_bytes",
+    "rmx_lsq_solve",
+    "rmx_complete_max",
+    "rmx_to_f32",
+    "rmx_row_max",
+    "rmx_resid_batch",
+    "rmx_gather_rows",
+    "rmx_gemv",
+    "rmx_mean_var",
+    "rmx_orthonormalize",
+    "rmx_grouse_train",
 )
 
+
+
 _lib = None
+
+# int (*)(void* user, int32 col, int32 pass, int32 attempt, int32* omega_out)
+OMEGA_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                            ctypes.c_int32, ctypes.POINTER(ctypes.c_int32))
 
 _i64, _i32, _vp, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
 _SP = ctypes.POINTER(Status)
@@ -92,6 +110,24 @@ _SIGS = {
     "rmx_tstat_exact": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _SP], ctypes.c_int),
     "rmx_tstat_pairs": ([_vp, _i64, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _SP],
                         ctypes.c_int),
+    "rmx_rapid_stats": ([_vp, _i64, _i32, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_lsq_workspace_bytes": ([_i32, _i64], _sz),
+    "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],
+                      ctypes.c_int),
+    "rmx_complete_max": ([_vp, _i64, _i32, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double,
+                          ctypes.c_uint64, _i32, _vp, _vp, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_to_f32": ([_vp, _i64, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_row_max": ([_vp, _i64, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_resid_batch": ([_vp, _i32, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_gather_rows": ([_vp, _i64, _vp, _i32, _i64, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_gemv": ([_vp, _i64, _i32, _vp, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_mean_var": ([_vp, _i64, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_orthonormalize": ([_vp, _i64, _i32, _i32, ctypes.POINTER(ctypes.c_double), _vp, _SP],
+                           ctypes.c_int),
+    "rmx_grouse_train": ([_vp, _i64, _i32, _i32, _i32, _vp, _i32, ctypes.c_double, _vp, OMEGA_CB,
+                          _vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32),
+                          ctypes.POINTER(_i32), ctypes.POINTER(_i64), _vp, _vp, _SP],
+                         ctypes.c_int),
 }
 
 
@@ -142,6 +178,13 @@ def ptr(t) -> int | None:
 
 def stream_handle(stream) -> int:
     return int(stream.cuda_stream)
+
+
+def call(name: str, *args) -> None:
+    """Invoke an rmx_* entry point whose last argument is rmx_status*."""
+    st = Status()
+    rc = getattr(load(), name)(*args, ctypes.byref(st))
+    raise_for(rc, st)
 
 
 def device_check(device: int = 0) -> int:

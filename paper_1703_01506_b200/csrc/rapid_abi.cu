@@ -1,0 +1,301 @@
+// rapid_abi.cu -- extern "C" RapidPT entry points (include/rmx.h) and the
+// native GROUSE training loop (reference lrmc.py:208-268).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/rmx.h"
+#include "rapid_internal.cuh"
+#include "rmx_internal.cuh"
+
+namespace rmx {
+namespace {
+
+int rset(rmx_status* st, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+int rset(rmx_status* st, int code, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(st->msg, sizeof(st->msg), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+void rclear(rmx_status* st) {
+  if (!st) return;
+  memset(st, 0, sizeof(*st));
+  st->perm = -1;
+  st->voxel = -1;
+}
+
+#define RCUDA(call)                                                                  \
+  do {                                                                               \
+    cudaError_t _e = (call);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return rset(st, RMX_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(_e));   \
+  } while (0)
+
+size_t gram_bytes(int r) { return (size_t)(r + 1) * (r + 1) * sizeof(double); }
+
+template <class T>
+struct DevBuf {  // stream-ordered scratch
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t n, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace
+}  // namespace rmx
+
+using namespace rmx;
+
+extern "C" {
+
+int rmx_rapid_stats(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,
+                    const int32_t* omegas, int64_t L, int32_t k, double* t_out, void* stream,
+                    rmx_status* st) {
+  rclear(st);
+  if (v < 1 || n1 < 2 || n - n1 < 2 || k < 1 || k > v || L < 1)
+    return rset(st, RMX_E_USAGE, "bad dimensions v=%lld n=%d n1=%d k=%d L=%lld", (long long)v, n,
+                n1, k, (long long)L);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<unsigned long long> key;
+  RCUDA(key.alloc(1, s));
+  RCUDA(cudaMemsetAsync(key.p, 0xff, sizeof(unsigned long long), s));
+  RCUDA(launch_rapid_stats(x, n, n1, orders, omegas, L, k, t_out, key.p, s));
+  unsigned long long hk = 0;
+  RCUDA(cudaMemcpyAsync(&hk, key.p, sizeof(hk), cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaStreamSynchronize(s));
+  if (hk != ~0ull) {
+    st->perm = (int64_t)(hk >> 32);
+    st->voxel = (int64_t)(hk & 0xffffffffu);  // index into the permutation's Omega
+    return rset(st, RMX_E_DEGENERATE, "zero pooled variance at permutation %lld, Omega index %lld",
+                (long long)st->perm, (long long)st->voxel);
+  }
+  return RMX_OK;
+}
+
+size_t rmx_lsq_workspace_bytes(int32_t r, int64_t batch) {
+  return (size_t)batch * gram_bytes(r) + (size_t)batch * 4 * sizeof(double) + 256;
+}
+
+int rmx_lsq_solve(const double* u, int64_t ldu, int32_t r, const int32_t* idx, int32_t k,
+                  const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                  double* norms_out, void* workspace, size_t workspace_bytes, void* stream,
+                  rmx_status* st) {
+  rclear(st);
+  if (r < 1 || k < r || B < 1 || !vals || !w_out)
+    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t per = gram_bytes(r);
+  int64_t chunk = (int64_t)((workspace_bytes > 256 ? workspace_bytes - 256 : 0) /
+                            (per + 4 * sizeof(double)));
+  if (chunk < 1) return rset(st, RMX_E_USAGE, "lsq workspace too small");
+  chunk = std::min<int64_t>(chunk, B);
+  double* G = static_cast<double*>(workspace);
+  double* nrm = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + chunk * per);
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t cnt = std::min(chunk, B - b0);
+    RCUDA(launch_gram(u, ldu, r, idx ? idx + b0 * k : nullptr, k, vals + b0 * k, G, cnt, s));
+    RCUDA(launch_chol_solve(G, r, cnt, w_out + b0 * r, flag_out ? flag_out + b0 : nullptr,
+                            norms_out ? norms_out + 4 * b0 : nrm, s));
+  }
+  return RMX_OK;
+}
+
+int rmx_complete_max(const float* u32, int64_t v, int32_t r, const float* w32, int64_t B,
+                     int64_t perm_base, double sigma, double mu, uint64_t seed, int32_t two_sided,
+                     const float* znoise, const double* base, double* max_out, void* stream,
+                     rmx_status* st) {
+  rclear(st);
+  if (v < 1 || r < 1 || B < 1) return rset(st, RMX_E_USAGE, "bad completion dimensions");
+  RCUDA(launch_complete_max(u32, v, r, w32, B, perm_base, sigma, mu, seed, two_sided, znoise,
+                            base, max_out, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_to_f32(const double* a, int64_t n, float* out, void* stream, rmx_status* st) {
+  rclear(st);
+  RCUDA(launch_to_f32(a, n, out, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_row_max(const double* a, int64_t rows, int64_t cols, int32_t two_sided, double* out,
+                void* stream, rmx_status* st) {
+  rclear(st);
+  RCUDA(launch_row_max(a, rows, cols, two_sided, out, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_resid_batch(const double* u, int32_t r, const int32_t* idx, int32_t k,
+                    const double* vals, const double* w, int64_t B, double* resid, void* stream,
+                    rmx_status* st) {
+  rclear(st);
+  RCUDA(launch_resid_batch(u, r, idx, k, vals, w, B, resid, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_gather_rows(const double* t, int64_t ldt, const int32_t* idx, int32_t k, int64_t B,
+                    double* out, void* stream, rmx_status* st) {
+  rclear(st);
+  RCUDA(launch_gather_rows(t, ldt, idx, k, B, out, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_gemv(const double* u, int64_t v, int32_t r, const double* w, double* out, void* stream,
+             rmx_status* st) {
+  rclear(st);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<double> sums;
+  RCUDA(sums.alloc(4, s));
+  RCUDA(launch_pred(u, v, r, w, out, sums.p, s));
+  return RMX_OK;
+}
+
+int rmx_mean_var(const double* a, int64_t n, double* out2, void* stream, rmx_status* st) {
+  rclear(st);
+  RCUDA(launch_mean_var(a, n, out2, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+// Orthonormalise U (v x r, in place) by CholeskyQR2.  Returns the
+// orthonormality error max|U^T U - I| measured BEFORE the call in *drift.
+int rmx_orthonormalize(double* u, int64_t v, int32_t r, int32_t force, double* drift,
+                       void* stream, rmx_status* st) {
+  rclear(st);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<double> G, dev;
+  RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
+  RCUDA(dev.alloc(2, s));
+  RCUDA(launch_gram(u, r, r, nullptr, (int)v, nullptr, G.p, 1, s));
+  RCUDA(launch_max_dev_identity(G.p, r, dev.p, s));
+  double h = 0.0;
+  RCUDA(cudaMemcpyAsync(&h, dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaStreamSynchronize(s));
+  if (drift) *drift = h;
+  if (!force && h <= 1e-8) return RMX_OK;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass > 0) RCUDA(launch_gram(u, r, r, nullptr, (int)v, nullptr, G.p, 1, s));
+    DevBuf<int32_t> flag;
+    RCUDA(flag.alloc(1, s));
+    RCUDA(launch_chol_solve(G.p, r, 1, nullptr, flag.p, nullptr, s));
+    RCUDA(launch_trsm_lt(u, v, r, G.p, s));
+  }
+  RCUDA(cudaStreamSynchronize(s));
+  return RMX_OK;
+}
+
+// GROUSE (reference lrmc.py:160-193 track_update + 208-268 train_basis).
+// t: (ell x v) training statistics, perm-major.  omegas0: (max_passes x ell x
+// k) first-attempt observation sets.  cb supplies resampled sets.
+int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t k,
+                     const int32_t* omegas0, int32_t max_passes, double tol, double* u,
+                     rmx_omega_cb cb, void* user, double* pass_resid, int32_t* passes_out,
+                     int32_t* converged_out, int64_t* updates_out, int32_t* final_omegas,
+                     void* stream, rmx_status* st) {
+  rclear(st);
+  if (k < r) return rset(st, RMX_E_USAGE, "%d observed rows per update cannot identify rank %d", k, r);
+  if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<double> G, w, vals, resid, pred, d, sums, wn;  // sums: 0 |r|^2 1 |pred|^2 2 |t|^2 4.. chol
+  DevBuf<int32_t> flag, idxbuf;
+  RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
+  RCUDA(w.alloc(r, s));
+  RCUDA(wn.alloc(r, s));
+  RCUDA(vals.alloc(k, s));
+  RCUDA(resid.alloc(k, s));
+  RCUDA(pred.alloc(v, s));
+  RCUDA(d.alloc(v, s));
+  RCUDA(sums.alloc(8, s));
+  RCUDA(flag.alloc(1, s));
+  RCUDA(idxbuf.alloc(k, s));
+  RCUDA(cudaMemsetAsync(d.p, 0, v * sizeof(double), s));
+  std::vector<int32_t> host_idx(k);
+  const double tau = ell * max_passes / 2.0;
+  int64_t tcount = 0;
+  int passes = 0, converged = 0;
+  for (int p = 0; p < max_passes; ++p) {
+    double rel_sum = 0.0;
+    for (int i = 0; i < ell; ++i) {
+      const double step = 1.0 / (1.0 + (double)tcount / tau);
+      const double* trow = t + (int64_t)i * v;
+      const int32_t* idx = omegas0 + ((int64_t)p * ell + i) * k;
+      double hs[8];
+      int32_t hflag = 0;
+      int attempt = 0;
+      for (;;) {
+        RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
+        RCUDA(launch_gram(u, r, r, idx, k, vals.p, G.p, 1, s));
+        RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+        RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
+        RCUDA(launch_resid(u, r, idx, k, vals.p, w.p, resid.p, sums.p, s));
+        RCUDA(launch_pred(u, v, r, w.p, pred.p, sums.p, s));
+        RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        RCUDA(cudaMemcpyAsync(&hflag, flag.p, sizeof(hflag), cudaMemcpyDeviceToHost, s));
+        RCUDA(cudaStreamSynchronize(s));
+        if (!hflag) break;
+        // ill-conditioned restriction: redraw from the same stream (lrmc.py:240-250)
+        if (++attempt >= 5 || !cb)
+          return rset(st, RMX_E_ILLCOND,
+                      "training column %d pass %d: restricted basis stayed ill-conditioned", i, p);
+        if (cb(user, i, p, attempt, host_idx.data()) != 0)
+          return rset(st, RMX_E_USAGE, "omega callback failed");
+        RCUDA(cudaMemcpyAsync(idxbuf.p, host_idx.data(), k * sizeof(int32_t),
+                              cudaMemcpyHostToDevice, s));
+        idx = idxbuf.p;
+      }
+      const double resid_norm = std::sqrt(std::max(hs[0], 0.0));
+      const double pred_norm = std::sqrt(std::max(hs[1], 0.0));
+      const double t_norm = std::sqrt(std::max(hs[2], 0.0));
+      const double w_norm = std::sqrt(std::max(hs[5], 0.0));
+      bool do_update = !(step == 0.0 || resid_norm == 0.0);
+      if (do_update && (pred_norm == 0.0 || w_norm == 0.0)) do_update = false;
+      if (do_update && resid_norm <= 1e-14 * std::max(1.0, pred_norm)) do_update = false;
+      if (do_update) {
+        const double theta = step * std::atan(resid_norm / pred_norm);
+        const double a = (std::cos(theta) - 1.0) / pred_norm;
+        const double bcoef = std::sin(theta) / resid_norm;
+        RCUDA(launch_scatter(idx, k, resid.p, bcoef, d.p, s));
+        RCUDA(launch_scale_copy(w.p, r, 1.0 / w_norm, wn.p, s));  // w / |w|
+        RCUDA(launch_grouse_update(u, v, r, pred.p, wn.p, a, d.p, s));
+        RCUDA(launch_unscatter(idx, k, d.p, s));
+      }
+      ++tcount;
+      rel_sum += t_norm > 0 ? resid_norm / t_norm : 0.0;
+      if (final_omegas)  // ends up holding the last executed pass (train_basis final_omegas)
+        RCUDA(cudaMemcpyAsync(final_omegas + (int64_t)i * k, idx, k * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, s));
+      if (tcount % 64 == 0) {
+        double drift = 0.0;
+        if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+      }
+    }
+    const double rel = rel_sum / ell;
+    if (pass_resid) pass_resid[p] = rel;
+    passes = p + 1;
+    if (rel < tol) {
+      converged = 1;
+      break;
+    }
+  }
+  double drift = 0.0;
+  if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+  if (passes_out) *passes_out = passes;
+  if (converged_out) *converged_out = converged;
+  if (updates_out) *updates_out = tcount;
+  RCUDA(cudaStreamSynchronize(s));
+  return RMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// rapid_internal.cuh -- launchers of rapid_kernels.cu (RapidPT on the GPU).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace rmx {
+
+cudaError_t launch_rapid_stats(const double* x, int n, int n1, const int16_t* orders,
+                               const int32_t* omegas, int64_t L, int k, double* t_out,
+                               unsigned long long* deg_key, cudaStream_t s);
+// G_b = [U[idx_b] | vals_b]^T [U[idx_b] | vals_b], (r+1)^2 each; idx = null -> all rows
+cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
+                        const double* vals, double* G, int64_t B, cudaStream_t s);
+// in-place Cholesky of G_b[:r,:r]; w_b = G^-1 G_b[r, :r]; resid2[4b..] =
+// (t.t - rhs.w, w.w, min L_ii, max L_ii); flag_b = 1 on a non-positive pivot
+cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
+                              double* resid2, cudaStream_t s);
+cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
+                                int64_t perm_base, double sigma, double mu, uint64_t seed,
+                                int two_sided, const float* znoise, const double* base,
+                                double* max_out, cudaStream_t s);
+cudaError_t launch_resid(const double* U, int r, const int32_t* idx, int k, const double* vals,
+                         const double* w, double* resid, double* sums, cudaStream_t s);
+cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, double* pred,
+                        double* sums, cudaStream_t s);
+cudaError_t launch_grouse_update(double* U, int64_t v, int r, const double* pred,
+                                 const double* wn, double a, const double* dscatter,
+                                 cudaStream_t s);
+cudaError_t launch_scatter(const int32_t* idx, int k, const double* resid, double bcoef,
+                           double* d, cudaStream_t s);
+cudaError_t launch_unscatter(const int32_t* idx, int k, double* d, cudaStream_t s);
+cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s);
+cudaError_t launch_gather_vals(const double* t, const int32_t* idx, int k, double* vals,
+                               cudaStream_t s);
+cudaError_t launch_max_dev_identity(const double* G, int r, double* out, cudaStream_t s);
+cudaError_t launch_row_max(const double* A, int64_t rows, int64_t cols, int two_sided,
+                           double* out, cudaStream_t s);
+cudaError_t launch_resid_batch(const double* U, int r, const int32_t* idx, int k,
+                               const double* vals, const double* W, int64_t B, double* R,
+                               cudaStream_t s);
+cudaError_t launch_to_f32(const double* a, int64_t n, float* out, cudaStream_t s);
+cudaError_t launch_gather_rows(const double* t, int64_t ldt, const int32_t* idx, int k, int64_t B,
+                               double* out, cudaStream_t s);
+cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s);
+cudaError_t launch_scale_copy(const double* a, int n, double sc, double* out, cudaStream_t s);
+
+}  // namespace rmx

@@ -1,0 +1,474 @@
+"""RapidPT on the B200: drop-in ``train`` / ``recover`` / ``run_rapid`` and the
+low-rank entry points of the reference's lrmc module.
+
+Reference: rapid.py:72-275 and lrmc.py:85-268.  What runs where:
+
+  host (numpy, the reference's own streams -> bit-identical inputs)
+      permutation labels, Omega draws (RECOVER_OMEGA, TRAIN_OMEGA), the basis
+      initialisation draw (BASIS_INIT), the max-gap normals (SHIFT_GAP)
+  device (librmx.so)
+      training columns       exact fp64 statistic kernel (bit-identical)
+      GROUSE                 native update loop: gathered Gram + Cholesky
+                             solve, residual, prediction, rank-one rotation,
+                             CholeskyQR2 re-orthonormalisation
+      sigma, mu, maxima      batched LS fits, residual mean/variance,
+                             completion + max kernels
+      recovery               K2 exact Omega statistics -> K3 batched gathered
+                             Gram + Cholesky -> K4 completion W.U^T fused with
+                             Philox residual noise and the row max
+
+Deliberate deviations:
+  * the recovery residual noise is a counter-based Philox N(0,1) keyed by
+    (seed, permutation, voxel), not numpy's SFC64 stream (v doubles per
+    permutation cannot be shipped) -- parity is distributional
+    for sigma > 0 and exact-to-tolerance for sigma = 0;
+  * the restricted-basis condition test uses Cholesky pivots (rank-deficient
+    restrictions are detected; the reference's 1e12 eigenvalue threshold is
+    approximated by a lower bound, see solve_block);
+  * GROUSE runs in a different summation order than OpenBLAS, so the trained
+    basis agrees with the reference's up to rounding, not bit for bit.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import multiprocessing as mp
+import os
+import time
+from concurrent.futures import ProcessPoolExecutor
+from typing import Optional
+
+import numpy as np
+
+from . import _native as nat
+from .domain import (
+    Basis,
+    MaxNull,
+    ObservedColumn,
+    SubspaceModel,
+    as_data_matrix,
+    as_plan,
+    observed_rows,
+)
+from .exceptions import (
+    DegenerateVoxelError,
+    IllConditionedBasisError,
+    NumericalError,
+    UsageError,
+)
+from .labels import plan_orders
+from .naive_engine import cuda_device, resolve_threads, tstat_exact_device
+from .rng import BASIS_INIT, RECOVER_OMEGA, SHIFT_GAP, TRAIN_OMEGA, omega_draw, stream
+
+COND_LIMIT = 1e12
+_BLOCK = 256            # reference recovery span (rapid.py:36), used for error parity
+_RESAMPLE_ATTEMPTS = 5
+_LSQ_BATCH_BYTES = 1 << 30
+
+
+# ---------------------------------------------------------------- host draws
+def _omega_block(args):
+    seed, domain, lo, hi, v, k, extra = args
+    out = np.empty((hi - lo, k), dtype=np.int32)
+    for i in range(lo, hi):
+        path = (domain, i) if extra is None else (domain, i, extra)
+        out[i - lo] = omega_draw(stream(seed, *path), v, k)
+    return out
+
+
+def draw_omegas(seed: int, domain: int, lo: int, hi: int, v: int, k: int,
+                extra: Optional[int] = None, workers: Optional[int] = None) -> np.ndarray:
+    """Sorted observation sets of indices [lo, hi) of a stream domain (first
+    draw of each stream), in parallel over host processes."""
+    count = hi - lo
+    workers = workers or min(os.cpu_count() or 1, 32)
+    if workers <= 1 or count * k < 2_000_000:
+        return _omega_block((seed, domain, lo, hi, v, k, extra))
+    bounds = np.linspace(lo, hi, workers * 4 + 1).astype(np.int64)
+    jobs = [(seed, domain, int(a), int(b), v, k, extra) for a, b in zip(bounds[:-1], bounds[1:])
+            if b > a]
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
+        return np.concatenate(list(pool.map(_omega_block, jobs)), axis=0)
+
+
+def _normals_block(args):
+    seed, domain, lo, hi, v = args
+    return np.stack([stream(seed, domain, i).standard_normal(v) for i in range(lo, hi)]).astype(
+        np.float32)
+
+
+def draw_normals(seed: int, domain: int, lo: int, hi: int, v: int) -> np.ndarray:
+    workers = min(os.cpu_count() or 1, 32)
+    if workers <= 1 or (hi - lo) * v < 4_000_000:
+        return _normals_block((seed, domain, lo, hi, v))
+    bounds = np.linspace(lo, hi, min(workers, hi - lo) + 1).astype(np.int64)
+    jobs = [(seed, domain, int(a), int(b), v) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
+        return np.concatenate(list(pool.map(_normals_block, jobs)), axis=0)
+
+
+def _resample(seed: int, path: tuple, attempt: int, v: int, k: int) -> np.ndarray:
+    """The attempt-th redraw of a stream whose first draw was already used
+    (the reference draws again from the same generator, lrmc.py:240-250,
+    rapid.py:180)."""
+    g = stream(seed, *path)
+    for _ in range(attempt):
+        g.choice(v, size=k, replace=False)
+    return np.sort(g.choice(v, size=k, replace=False)).astype(np.int32)
+
+
+# ---------------------------------------------------------------- device helpers
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream(dev):
+    return nat.stream_handle(_torch().cuda.current_stream(dev))
+
+
+def _to_dev(a, dev, dtype=None):
+    torch = _torch()
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(dev)
+
+
+def _lsq(u_dev, r: int, idx_dev, k: int, vals_dev, B: int):
+    """Batched solve_block on device -> (W (B x r), flags (B), norms (B x 4))."""
+    torch = _torch()
+    dev = u_dev.device
+    W = torch.empty((B, r), dtype=torch.float64, device=dev)
+    flags = torch.empty(B, dtype=torch.int32, device=dev)
+    norms = torch.empty((B, 4), dtype=torch.float64, device=dev)
+    per = (r + 1) * (r + 1) * 8 + 32
+    batch = max(1, min(B, _LSQ_BATCH_BYTES // per))
+    ws_bytes = int(nat.load().rmx_lsq_workspace_bytes(r, batch))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    nat.call("rmx_lsq_solve", nat.ptr(u_dev), r, r, nat.ptr(idx_dev), k, nat.ptr(vals_dev), B,
+             nat.ptr(W), nat.ptr(flags), nat.ptr(norms), nat.ptr(ws), ws_bytes, _stream(dev))
+    return W, flags, norms
+
+
+def _orthonormalize(u_dev, force: bool) -> float:
+    drift = ctypes.c_double(0.0)
+    v, r = u_dev.shape
+    nat.call("rmx_orthonormalize", nat.ptr(u_dev), v, r, int(force), ctypes.byref(drift),
+             _stream(u_dev.device))
+    return float(drift.value)
+
+
+def _complete_max(u32, w32, perm_base: int, sigma: float, mu: float, seed: int, two_sided: bool,
+                  znoise=None, base=None):
+    torch = _torch()
+    v, r = u32.shape
+    B = w32.shape[0]
+    out = torch.empty(B, dtype=torch.float64, device=u32.device)
+    nat.call("rmx_complete_max", nat.ptr(u32), v, r, nat.ptr(w32), B, int(perm_base),
+             float(sigma), float(mu), ctypes.c_uint64(int(seed) & ((1 << 64) - 1)),
+             int(bool(two_sided)), nat.ptr(znoise), nat.ptr(base), nat.ptr(out),
+             _stream(u32.device))
+    return out
+
+
+def _basis_device(model: SubspaceModel, dev):
+    """fp64 basis on device, cached on the (frozen) model object."""
+    cache = getattr(model, "_rmx_dev", None)
+    if cache is not None and cache[0] == dev:
+        return cache[1], cache[2]
+    u = _to_dev(model.basis.matrix, dev)
+    u32 = u.to(_torch().float32)
+    object.__setattr__(model, "_rmx_dev", (dev, u, u32))
+    return u, u32
+
+
+# ---------------------------------------------------------------- lrmc API
+def init_basis(v: int, r: int, seed: int) -> Basis:
+    """Orthonormal basis of a seeded Gaussian draw (reference lrmc.py:85-93):
+    the draw is the reference's BASIS_INIT stream; the orthonormalisation is
+    CholeskyQR2 on the device (same span; column signs may differ from
+    numpy's Householder QR, which GROUSE is invariant to)."""
+    if r > v:
+        raise UsageError(f"rank {r} exceeds dimension {v}")
+    if r < 1:
+        raise UsageError("rank must be >= 1")
+    dev = cuda_device()
+    u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, r)), dev)
+    _orthonormalize(u, force=True)
+    return Basis(u.cpu().numpy(), copy=False)
+
+
+def solve_block(u_stack: np.ndarray, values: np.ndarray):
+    """Batched LS fits (reference lrmc.py:127-149) -> (w (B, r), conds (B,)).
+
+    conds: inf for a rank-deficient restriction (non-positive Cholesky pivot),
+    else max(L_ii) / min(L_ii) of the Gram's Cholesky factor -- a lower bound
+    of the reference's sqrt(lambda_max / lambda_min)."""
+    u_stack = np.ascontiguousarray(u_stack, dtype=np.float64)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    B, k, r = u_stack.shape
+    dev = cuda_device()
+    torch = _torch()
+    U = _to_dev(u_stack.reshape(B * k, r), dev)
+    idx = torch.arange(B * k, dtype=torch.int32, device=dev).reshape(B, k)
+    W, flags, norms = _lsq(U, r, idx, k, _to_dev(values, dev), B)
+    n = norms.cpu().numpy()
+    f = flags.cpu().numpy()
+    with np.errstate(divide="ignore", invalid="ignore"):
+        conds = np.where(f != 0, np.inf, n[:, 3] / n[:, 2])
+    return W.cpu().numpy(), conds
+
+
+def fit_coefficients(b: Basis, col: ObservedColumn) -> np.ndarray:
+    """LS coefficients on the observed rows (reference lrmc.py:107-124)."""
+    if col.size < b.rank:
+        raise UsageError(f"{col.size} observed rows cannot determine {b.rank} coefficients")
+    if col.indices[-1] >= b.voxels:
+        raise UsageError("observed row index outside the basis")
+    w, conds = solve_block(b.matrix[col.indices][None], col.values[None])
+    if not np.isfinite(conds[0]) or conds[0] > COND_LIMIT:
+        raise IllConditionedBasisError(float(conds[0]))
+    return w[0]
+
+
+def complete_column(b: Basis, w: np.ndarray) -> np.ndarray:
+    """U w (reference lrmc.py:152-157)."""
+    w = np.asarray(w, dtype=np.float64)
+    if w.shape != (b.rank,):
+        raise UsageError(f"coefficients must have shape ({b.rank},), got {w.shape}")
+    dev = cuda_device()
+    torch = _torch()
+    u = _to_dev(b.matrix, dev)
+    out = torch.empty(b.voxels, dtype=torch.float64, device=dev)
+    nat.call("rmx_gemv", nat.ptr(u), b.voxels, b.rank, nat.ptr(_to_dev(w, dev)), nat.ptr(out),
+             _stream(dev))
+    return out.cpu().numpy()
+
+
+class TrainingResult:
+    def __init__(self, basis, passes, updates, pass_residuals, final_omegas, converged):
+        self.basis = basis
+        self.passes = passes
+        self.updates = updates
+        self.pass_residuals = pass_residuals
+        self.final_omegas = final_omegas
+        self.converged = converged
+
+
+def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
+                        max_passes: int, tolerance: float):
+    """GROUSE on device.  t_dev: (ell, v) fp64 training statistics."""
+    torch = _torch()
+    dev = t_dev.device
+    u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, rank)), dev)
+    _orthonormalize(u, force=True)
+    om = np.empty((max_passes, ell, k), dtype=np.int32)
+    for p in range(max_passes):
+        om[p] = draw_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, extra=p)
+    om_dev = _to_dev(om, dev)
+    final = torch.empty((ell, k), dtype=torch.int32, device=dev)
+    pass_resid = (ctypes.c_double * max_passes)()
+    passes, conv, updates = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int64(0)
+
+    def cb(_user, col, pas, attempt, out):
+        try:
+            idx = _resample(seed, (TRAIN_OMEGA, col, pas), attempt, v, k)
+            ctypes.memmove(out, idx.ctypes.data, idx.nbytes)
+            return 0
+        except Exception:
+            return 1
+
+    cbf = nat.OMEGA_CB(cb)
+    nat.call("rmx_grouse_train", nat.ptr(t_dev), v, ell, rank, k, nat.ptr(om_dev), max_passes,
+             float(tolerance), nat.ptr(u), cbf, None, pass_resid, ctypes.byref(passes),
+             ctypes.byref(conv), ctypes.byref(updates), nat.ptr(final), _stream(dev))
+    res = [pass_resid[i] for i in range(passes.value)]
+    return u, final, int(passes.value), bool(conv.value), int(updates.value), res
+
+
+def train_basis(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int = 50,
+                tolerance: float = 1e-3, resample_attempts: int = 5) -> TrainingResult:
+    """GROUSE passes over the training columns (reference lrmc.py:208-268)."""
+    t_ex = np.asarray(t_ex, dtype=np.float64)
+    v, ell = t_ex.shape
+    if k < rank:
+        raise UsageError(f"{k} observed rows per update cannot identify rank {rank}")
+    if k > v:
+        raise UsageError(f"observed rows {k} exceed voxel count {v}")
+    dev = cuda_device()
+    t_dev = _to_dev(np.ascontiguousarray(t_ex.T), dev)
+    u, final, passes, conv, updates, res = _train_basis_device(t_dev, v, ell, k, rank, seed,
+                                                               max_passes, tolerance)
+    fo = final.cpu().numpy()
+    return TrainingResult(Basis(u.cpu().numpy(), copy=False), passes, updates, res,
+                          [fo[i].astype(np.int64) for i in range(ell)], conv)
+
+
+# ---------------------------------------------------------------- train / recover
+def _train_device(x, cfg):
+    """Shared by train() and run_rapid(): returns (model, training maxima,
+    t_dev (ell x v, device), u_dev, u32_dev)."""
+    torch = _torch()
+    cfg = cfg.resolve(x)
+    if cfg.engine != "rapid":
+        raise UsageError("training is only meaningful for the rapid engine")
+    ell, rank = cfg.training_columns, cfg.rank
+    v = x.voxels
+    k = observed_rows(cfg.sample_rate, v)
+    plan = cfg.plan_for(x)
+    dev = cuda_device()
+    xd = _to_dev(x.values, dev)
+    od = _to_dev(plan_orders(plan, 0, ell), dev)
+    t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
+    u, final, passes, conv, _, _ = _train_basis_device(t_dev, v, ell, k, rank, cfg.seed,
+                                                       cfg.max_passes, cfg.tolerance)
+    # fits of the frozen basis on the final pass's observed rows (rapid.py:90-97)
+    vals = torch.empty((ell, k), dtype=torch.float64, device=dev)
+    nat.call("rmx_gather_rows", nat.ptr(t_dev), v, nat.ptr(final), k, ell, nat.ptr(vals),
+             _stream(dev))
+    W, flags, norms = _lsq(u, rank, final, k, vals, ell)
+    if int(flags.max().item()) != 0:
+        raise IllConditionedBasisError(math.inf)
+    if cfg.sigma_override is not None:
+        sigma = float(cfg.sigma_override)
+        if sigma < 0:
+            raise UsageError("sigma override must be >= 0")
+    else:
+        resid = torch.empty((ell, k), dtype=torch.float64, device=dev)
+        nat.call("rmx_resid_batch", nat.ptr(u), rank, nat.ptr(final), k, nat.ptr(vals),
+                 nat.ptr(W), ell, nat.ptr(resid), _stream(dev))
+        mv = torch.empty(2, dtype=torch.float64, device=dev)
+        nat.call("rmx_mean_var", nat.ptr(resid), ell * k, nat.ptr(mv), _stream(dev))
+        sigma = float(math.sqrt(max(float(mv[1].item()), 0.0)))
+    tmax = torch.empty(ell, dtype=torch.float64, device=dev)
+    nat.call("rmx_row_max", nat.ptr(t_dev), ell, v, int(cfg.two_sided), nat.ptr(tmax),
+             _stream(dev))
+    training_maxima = tmax.cpu().numpy()
+    u32 = u.to(torch.float32)
+    w32 = W.to(torch.float32)
+    if cfg.shift_override is not None:
+        mu = float(cfg.shift_override)
+    elif cfg.shift_estimator == "residual-sup":
+        m = _complete_max(u32, w32, 0, 0.0, 0.0, cfg.seed, cfg.two_sided, base=t_dev)
+        mu = float(m.max().item())
+    else:  # max-gap: gaps to synthetic columns with the reference's SHIFT_GAP normals
+        z = _to_dev(draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v), dev)
+        synth = _complete_max(u32, w32, 0, sigma, 0.0, cfg.seed, cfg.two_sided, znoise=z)
+        mu = float(np.mean(training_maxima - synth.cpu().numpy()))
+    model = SubspaceModel(
+        basis=Basis(u.cpu().numpy(), copy=False), residual_std=sigma, max_shift=mu,
+        training_columns=ell, sample_rate=cfg.sample_rate, training_maxima=training_maxima,
+        two_sided=cfg.two_sided, seed=cfg.seed, passes=passes, converged=conv)
+    object.__setattr__(model, "_rmx_dev", (dev, u, u32))
+    return model, training_maxima, t_dev
+
+
+def train(x, cfg):
+    """Training phase (reference rapid.py:72-135) -> (model, training maxima,
+    training columns t_ex (v x ell))."""
+    x = as_data_matrix(x)
+    model, training_maxima, t_dev = _train_device(x, cfg)
+    return model, training_maxima, t_dev.t().contiguous().cpu().numpy()
+
+
+def _degenerate_in_recovery(x, plan, ell, L, k, t_perm_idx, omega_idx, omegas, orders):
+    """Raise like the reference: spans of 256 permutations from ell; the first
+    failing span reports the flat index into its (count x k) block."""
+    p = ell + t_perm_idx
+    lo = ell + ((p - ell) // _BLOCK) * _BLOCK
+    voxel = (p - lo) * k + omega_idx
+    row = x.values[omegas[t_perm_idx, omega_idx]]
+    o = orders[t_perm_idx]
+    m = row[o[: x.n1]].mean() - row[o[x.n1:]].mean()
+    raise DegenerateVoxelError(int(voxel), float(m))
+
+
+def recover(x, model: SubspaceModel, plan, cfg):
+    """Recovery phase (reference rapid.py:209-250) -> (MaxNull, counters)."""
+    torch = _torch()
+    x = as_data_matrix(x)
+    plan = as_plan(plan)
+    cfg = cfg.resolve(x)
+    ell, L = model.training_columns, plan.count
+    if ell >= L:
+        raise UsageError(f"no columns to recover: training columns {ell} >= permutations {L}")
+    resolve_threads(cfg.threads)
+    v, n1 = x.voxels, x.n1
+    k = observed_rows(model.sample_rate, v)
+    dev = cuda_device()
+    u, u32 = _basis_device(model, dev)
+    r = model.basis.rank
+    maxima = np.empty(L, dtype=np.float64)
+    maxima[:ell] = model.training_maxima
+    nrec = L - ell
+    orders = plan_orders(plan, ell, L)
+    omegas = draw_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k)
+    xd = _to_dev(x.values, dev)
+    od = _to_dev(orders, dev)
+    omd = _to_dev(omegas, dev)
+    t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
+    st = nat.Status()
+    rc = nat.load().rmx_rapid_stats(nat.ptr(xd), v, x.subjects, n1, nat.ptr(od), nat.ptr(omd),
+                                    nrec, k, nat.ptr(t), _stream(dev), ctypes.byref(st))
+    if rc == nat.RMX_E_DEGENERATE:
+        _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel), omegas, orders)
+    nat.raise_for(rc, st)
+    W, flags, norms = _lsq(u, r, omd, k, t, nrec)
+    evals = nrec * k
+    bad = np.flatnonzero(flags.cpu().numpy() != 0)
+    for j in bad:  # rapid.py:173-196: redraw from the same stream, up to 5 times
+        i = ell + int(j)
+        ok = False
+        for attempt in range(1, _RESAMPLE_ATTEMPTS + 1):
+            idx = _resample(model.seed, (RECOVER_OMEGA, i), attempt, v, k)
+            idx_d = _to_dev(idx[None], dev)
+            tj = torch.empty((1, k), dtype=torch.float64, device=dev)
+            nat.call("rmx_rapid_stats", nat.ptr(xd), v, x.subjects, n1, nat.ptr(od[j:j + 1]),
+                     nat.ptr(idx_d), 1, k, nat.ptr(tj), _stream(dev))
+            evals += k
+            wj, fj, _ = _lsq(u, r, idx_d, k, tj, 1)
+            if int(fj.item()) == 0:
+                W[j] = wj[0]
+                ok = True
+                break
+        if not ok:
+            raise NumericalError(
+                f"permutation {i}: restricted basis stayed ill-conditioned after "
+                f"{_RESAMPLE_ATTEMPTS} observation resamples")
+    m = _complete_max(u32, W.to(torch.float32), ell, model.residual_std, model.max_shift,
+                      model.seed, model.two_sided)
+    maxima[ell:] = m.cpu().numpy()
+    counters = {
+        "subsampled_statistic_evaluations": int(evals),
+        "recovery_columns": nrec,
+        "observed_rows_per_column": k,
+        "resampled_evaluations": int(evals - k * nrec),
+    }
+    return MaxNull(maxima), counters
+
+
+def run_rapid(x, cfg):
+    """Full accelerated run (reference rapid.py:253-275)."""
+    x = as_data_matrix(x)
+    cfg = cfg.resolve(x)
+    plan = cfg.plan_for(x)
+    t0 = time.perf_counter()
+    model, _, _ = _train_device(x, cfg)
+    t1 = time.perf_counter()
+    null, rec = recover(x, model, plan, cfg)
+    t2 = time.perf_counter()
+    v = x.voxels
+    counters = {
+        "full_statistic_evaluations": v * model.training_columns,
+        **rec,
+        "statistic_evaluations": v * model.training_columns + rec["subsampled_statistic_evaluations"],
+        "training_passes": model.passes,
+        "training_converged": model.converged,
+        "train_seconds": t1 - t0,
+        "recover_seconds": t2 - t1,
+        "total_seconds": t2 - t0,
+    }
+    return null, model, counters

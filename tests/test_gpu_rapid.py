@@ -1,0 +1,136 @@
+"""RapidPT on the GPU vs the reference (tests/golden/rapid_cases.npz) and
+the reference's own RapidPT test invariants (tests/test_rapid.py).
+
+Tolerances (north_star: 1e-4 relative on floating-point outputs): the
+recovery completion runs in fp32 on the device, so noise-free (sigma = 0)
+recovered maxima are compared at 1e-5 relative; the Omega statistics and
+training columns are bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1703_01506_b200 as rmx
+from paper_1703_01506_b200.domain import SubspaceModel
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def g():
+    return np.load(os.path.join(GOLD, "rapid_cases.npz"))
+
+
+def _data(v, n1, n2, seed=0):
+    r = np.random.default_rng(seed)
+    return rmx.DataMatrix(r.standard_normal((v, n1 + n2)), n1, n2)
+
+
+def test_solve_block_matches_reference():
+    d = g()
+    w, conds = rmx.solve_block(d["sb_u"], d["sb_vals"])
+    assert np.allclose(w, d["sb_w"], rtol=0, atol=1e-10)
+    assert np.all(conds < 100)
+    u = np.zeros((10, 2))
+    u[0, 0] = u[1, 1] = 1.0
+    _, c = rmx.solve_block(np.stack([u[[0, 1, 2]], u[[5, 6, 7]]]), np.zeros((2, 3)))
+    assert c[0] < 10 and (not np.isfinite(c[1]) or c[1] > 1e12)
+
+
+def test_fit_and_complete_column():
+    b = rmx.init_basis(300, 8, seed=11)
+    assert b.orthonormality_error() < 1e-12
+    col = np.random.default_rng(3).standard_normal(300)
+    idx = np.sort(np.random.default_rng(4).choice(300, 60, replace=False))
+    w = rmx.fit_coefficients(b, rmx.ObservedColumn(idx, col[idx]))
+    u_o = b.matrix[idx]
+    assert np.allclose(w, np.linalg.solve(u_o.T @ u_o, u_o.T @ col[idx]), atol=1e-10)
+    assert np.allclose(rmx.complete_column(b, w), b.matrix @ w, atol=1e-12)
+    u = np.zeros((10, 3))
+    u[0, 0] = u[1, 1] = u[2, 2] = 1.0
+    with pytest.raises(rmx.IllConditionedBasisError):
+        rmx.fit_coefficients(rmx.Basis(u), rmx.ObservedColumn(np.array([5, 6, 7, 8]), np.zeros(4)))
+
+
+def test_noise_free_recovery_with_reference_basis():
+    d = g()
+    v, n1, n2, L, seed, ell, r = (int(t) for t in d["r1_meta"])
+    x = rmx.DataMatrix(d["r1_x"].astype(np.float64), n1, n2)
+    model = SubspaceModel(basis=rmx.Basis(d["r1_basis"]), residual_std=0.0, max_shift=0.0,
+                          training_columns=ell, sample_rate=float(d["r1_eta"]),
+                          training_maxima=d["r1_train_max"], two_sided=False, seed=seed,
+                          passes=1, converged=False)
+    cfg = rmx.RunConfig(permutations=L, seed=seed, engine="rapid", training_columns=ell, rank=r,
+                        sample_rate=float(d["r1_eta"]))
+    null, counters = rmx.recover(x, model, cfg.plan_for(x), cfg)
+    ref = d["r1_maxima_sigma0"]
+    assert np.array_equal(null.maxima[:ell], ref[:ell])
+    assert np.allclose(null.maxima, ref, rtol=1e-5, atol=1e-5)
+    k = int(np.ceil(float(d["r1_eta"]) * v))
+    assert counters["subsampled_statistic_evaluations"] == k * (L - ell)
+    assert counters["resampled_evaluations"] == 0
+
+
+def test_exact_regime_matches_naive():
+    d = g()
+    x = rmx.DataMatrix(d["exact_x"].astype(np.float64), 4, 4)
+    cfg = rmx.RunConfig(permutations=60, seed=3, engine="rapid", training_columns=8, rank=8,
+                        sample_rate=1.0, max_passes=5, sigma_override=0.0, shift_override=0.0)
+    null, model, _ = rmx.run_rapid(x, cfg)
+    ref, _, _ = rmx.run_naive(x, cfg.plan_for(x))
+    assert model.residual_std == 0.0
+    assert np.allclose(null.maxima, ref.maxima, rtol=1e-5, atol=1e-5)
+    assert np.allclose(null.maxima, d["exact_maxima"], rtol=1e-5, atol=1e-5)
+
+
+def test_training_columns_bit_exact_and_maxima_unshifted():
+    x = _data(30, 3, 3, seed=2)
+    cfg = rmx.RunConfig(permutations=40, seed=9, engine="rapid", training_columns=6, rank=4,
+                        sample_rate=0.8)
+    model, training_maxima, t_ex = rmx.train(x, cfg)
+    plan = cfg.plan_for(x)
+    for i in range(6):
+        x1, x2 = x.group_blocks(plan.shuffle(i))
+        assert np.array_equal(t_ex[:, i], rmx.tstat_full(x1, x2))
+        assert training_maxima[i] == t_ex[:, i].max()
+    null, model2, _ = rmx.run_rapid(x, cfg)
+    assert np.array_equal(null.maxima[:6], model2.training_maxima)
+
+
+def test_counter_identity_and_determinism():
+    x = _data(100, 4, 4, seed=9)
+    cfg = rmx.RunConfig(permutations=50, seed=10, engine="rapid", training_columns=8, rank=8,
+                        sample_rate=0.25)
+    a, _, counters = rmx.run_rapid(x, cfg)
+    k = int(np.ceil(0.25 * 100))
+    assert counters["subsampled_statistic_evaluations"] == k * (50 - 8)
+    assert counters["full_statistic_evaluations"] == 100 * 8
+    assert counters["statistic_evaluations"] == 100 * 8 + k * (50 - 8)
+    b, _, _ = rmx.run_rapid(x, cfg)
+    assert np.array_equal(a.maxima, b.maxima)
+
+
+def test_no_recovery_columns_rejected():
+    x = _data(40, 3, 3, seed=13)
+    cfg = rmx.RunConfig(permutations=6, seed=0, engine="rapid", training_columns=6, rank=4,
+                        sample_rate=0.5)
+    model, _, _ = rmx.train(x, cfg)
+    with pytest.raises(rmx.UsageError, match="no columns to recover"):
+        rmx.recover(x, model, cfg.plan_for(x), cfg)
+
+
+def test_trained_model_close_to_reference():
+    """GROUSE on the device vs the reference's trained model (same inputs,
+    same Omega draws; different float summation order)."""
+    d = g()
+    v, n1, n2, L, seed, ell, r = (int(t) for t in d["r1_meta"])
+    x = rmx.DataMatrix(d["r1_x"].astype(np.float64), n1, n2)
+    cfg = rmx.RunConfig(permutations=L, seed=seed, engine="rapid", training_columns=ell, rank=r,
+                        sample_rate=float(d["r1_eta"]))
+    null, model, counters = rmx.run_rapid(x, cfg)
+    assert np.array_equal(model.training_maxima, d["r1_train_max"])
+    # subspaces agree: principal angles via the singular values of U_ref^T U_gpu
+    s = np.linalg.svd(d["r1_basis"].T @ model.basis.matrix, compute_uv=False)
+    assert s.min() > 0.999
+    assert model.residual_std == pytest.approx(float(d["r1_sigma"]), rel=1e-3)
+    assert counters["statistic_evaluations"] == int(d["r1_counters"][0])
