@@ -12,6 +12,7 @@
 //   k_complete_max  K4: max_j (W U^T)[p, j] + sigma z(p, j)  (+ mu), fused
 //                   with a counter-based Philox normal (rapid.py:198-205)
 //   GROUSE helpers  k_resid, k_pred, k_grouse_update (lrmc.py:160-193)
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -56,7 +57,8 @@ __device__ __forceinline__ double a_elem(const double* U, int64_t ldu, int r, co
 
 __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int64_t ldu, int r,
                                               const int32_t* __restrict__ idx, int k,
-                                              const double* __restrict__ vals, double* __restrict__ G) {
+                                              const double* __restrict__ vals, double* __restrict__ G,
+                                              int rows_per_split) {
   __shared__ double As[kGK][kGT + 1];
   __shared__ double Bs[kGK][kGT + 1];
   const int64_t b = blockIdx.y;
@@ -70,11 +72,14 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int6
   const int i0 = ti * kGT, j0 = tj * kGT;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4] = {};
-  for (int k0 = 0; k0 < k; k0 += kGK) {
+  const int kbeg = blockIdx.z * rows_per_split;
+  const int kend = min(k, kbeg + rows_per_split);
+  for (int k0 = kbeg; k0 < kend; k0 += kGK) {
     for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
       const int rr = e / kGT, cc = e % kGT;
-      As[rr][cc] = a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, i0 + cc);
-      Bs[rr][cc] = a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, j0 + cc);
+      const bool in = k0 + rr < kend;
+      As[rr][cc] = in ? a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, i0 + cc) : 0.0;
+      Bs[rr][cc] = in ? a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, j0 + cc) : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
@@ -100,8 +105,13 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int6
     for (int s = 0; s < 4; ++s) {
       const int i = i0 + ty * 4 + q, j = j0 + tx * 4 + s;
       if (i < ld && j < ld && j <= i) {
-        Gb[(int64_t)i * ld + j] = acc[q][s];
-        Gb[(int64_t)j * ld + i] = acc[q][s];
+        if (gridDim.z == 1) {
+          Gb[(int64_t)i * ld + j] = acc[q][s];
+          if (i != j) Gb[(int64_t)j * ld + i] = acc[q][s];
+        } else {  // split-K partial sums (G zeroed by the launcher)
+          atomicAdd(&Gb[(int64_t)i * ld + j], acc[q][s]);
+          if (i != j) atomicAdd(&Gb[(int64_t)j * ld + i], acc[q][s]);
+        }
       }
     }
 }
@@ -125,11 +135,14 @@ __global__ void __launch_bounds__(256) k_chol_solve(double* __restrict__ G, int 
   const int64_t b = blockIdx.x;
   const int ld = r + 1;
   double* Gb = G + b * (int64_t)ld * ld;
-  if (threadIdx.x == 0) {
-    bad = 0;
+  if (threadIdx.x < 32) {
     double m = 0.0;
-    for (int i = 0; i < r; ++i) m = fmax(m, Gb[(int64_t)i * ld + i]);
-    dmax = m;
+    for (int i = threadIdx.x; i < r; i += 32) m = fmax(m, Gb[(int64_t)i * ld + i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) {
+      bad = 0;
+      dmax = m;
+    }
   }
   __syncthreads();
   const double tiny = 1e-24 * dmax;
@@ -171,20 +184,25 @@ __global__ void __launch_bounds__(256) k_chol_solve(double* __restrict__ G, int 
         P[i * kPW + c] = s / D[c * kPW + c];
       }
       for (int c = 0; c < w; ++c) Gb[gi + c] = P[i * kPW + c];
+      for (int c = w; c < kPW; ++c) P[i * kPW + c] = 0.0;  // last (narrow) panel
     }
     __syncthreads();
     // trailing update: G[i, j] -= P_i . P_j for jb+w <= j <= i < r
-    const int64_t npairs = (int64_t)rows * (rows + 1) / 2;
-    for (int64_t e = threadIdx.x; e < npairs; e += blockDim.x) {
-      const int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-      int ii = i;
-      while ((int64_t)(ii + 1) * (ii + 2) / 2 <= e) ++ii;
-      while ((int64_t)ii * (ii + 1) / 2 > e) --ii;
-      const int jj = (int)(e - (int64_t)ii * (ii + 1) / 2);
-      double s = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < w; ++c) s += P[ii * kPW + c] * P[jj * kPW + c];
-      Gb[(int64_t)(jb + w + ii) * ld + jb + w + jj] -= s;
+    // (warp per row i, lanes over j <= i)
+    {
+      const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
+      for (int ii = wid; ii < rows; ii += nw) {
+        double pi[kPW];
+#pragma unroll
+        for (int c = 0; c < kPW; ++c) pi[c] = c < w ? P[ii * kPW + c] : 0.0;
+        double* grow = Gb + (int64_t)(jb + w + ii) * ld + jb + w;
+        for (int jj = lane; jj <= ii; jj += 32) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < kPW; ++c) acc += pi[c] * P[jj * kPW + c];
+          grow[jj] -= acc;
+        }
+      }
     }
     __syncthreads();
   }
@@ -580,11 +598,24 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
                         const double* vals, double* G, int64_t B, cudaStream_t s) {
   const int nt = (r + 1 + kGT - 1) / kGT;
   const int ntiles = nt * (nt + 1) / 2;
+  // split the row (K) dimension when the batch alone cannot fill the GPU
+  int splits = 1;
+  const int64_t blocks = (int64_t)ntiles * B;
+  if (blocks < 2 * 148) {
+    splits = (int)std::min<int64_t>((2 * 148 + blocks - 1) / blocks, std::max(1, k / 64));
+    splits = std::max(1, std::min(splits, 4096));
+  }
+  const int rps = ((k + splits - 1) / splits + kGK - 1) / kGK * kGK;
+  splits = (k + rps - 1) / rps;
+  if (splits > 1) {
+    cudaError_t e = cudaMemsetAsync(G, 0, (size_t)B * (r + 1) * (r + 1) * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+  }
   for (int64_t base = 0; base < B; base += 65535) {
     const int64_t cnt = B - base < 65535 ? B - base : 65535;
-    k_gram<<<dim3(ntiles, (unsigned)cnt), 256, 0, s>>>(
+    k_gram<<<dim3(ntiles, (unsigned)cnt, (unsigned)splits), 256, 0, s>>>(
         U, ldu, r, idx ? idx + base * k : nullptr, k, vals ? vals + base * k : nullptr,
-        G + base * (int64_t)(r + 1) * (r + 1));
+        G + base * (int64_t)(r + 1) * (r + 1), rps);
   }
   return cudaGetLastError();
 }

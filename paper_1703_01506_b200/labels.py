@@ -13,15 +13,14 @@ memory.  bench.py reports this cost separately from the device clock.
 
 from __future__ import annotations
 
-import multiprocessing as mp
 import os
 import threading
 from collections import OrderedDict
-from concurrent.futures import ProcessPoolExecutor
 
 import numpy as np
 
 from .exceptions import UsageError
+from .hostpar import fill_rows
 from .rng import shuffle_order
 
 _CACHE: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
@@ -30,29 +29,14 @@ _CACHE_LIMIT = int(os.environ.get("RMX_LABEL_CACHE_BYTES", str(2 << 30)))
 _LOCK = threading.Lock()
 
 
-def _orders_block(args) -> np.ndarray:
-    seed, lo, hi, n = args
-    out = np.empty((hi - lo, n), dtype=np.int16)
-    for i in range(lo, hi):
-        out[i - lo] = shuffle_order(seed, i, n)
-    return out
-
-
 def generate_orders(seed: int, lo: int, hi: int, n: int, workers: int | None = None) -> np.ndarray:
-    """Rows [lo, hi) of the plan's order matrix (uncached)."""
+    """Rows [lo, hi) of the plan's order matrix (uncached), drawn by forked
+    workers into shared memory (identical to a serial loop)."""
     if n > 32767:
         raise UsageError(f"subject count {n} exceeds the int16 label format")
-    count = hi - lo
-    if workers is None:
-        workers = min(os.cpu_count() or 1, 32)
-    if workers <= 1 or count < 4096:
-        return _orders_block((seed, lo, hi, n))
-    bounds = np.linspace(lo, hi, workers * 4 + 1).astype(np.int64)
-    jobs = [(seed, int(a), int(b), n) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
-    ctx = mp.get_context("fork")
-    with ProcessPoolExecutor(max_workers=workers, mp_context=ctx) as pool:
-        parts = list(pool.map(_orders_block, jobs))
-    return np.concatenate(parts, axis=0)
+    if hi - lo < 4096:
+        workers = 1
+    return fill_rows((n,), np.int16, lambda i: shuffle_order(seed, lo + i, n), hi - lo, workers)
 
 
 def plan_orders(plan, lo: int = 0, hi: int | None = None) -> np.ndarray:

@@ -33,10 +33,8 @@ from __future__ import annotations
 
 import ctypes
 import math
-import multiprocessing as mp
 import os
 import time
-from concurrent.futures import ProcessPoolExecutor
 from typing import Optional
 
 import numpy as np
@@ -51,6 +49,7 @@ from .domain import (
     as_plan,
     observed_rows,
 )
+from .hostpar import fill_rows
 from .exceptions import (
     DegenerateVoxelError,
     IllConditionedBasisError,
@@ -68,44 +67,22 @@ _LSQ_BATCH_BYTES = 1 << 30
 
 
 # ---------------------------------------------------------------- host draws
-def _omega_block(args):
-    seed, domain, lo, hi, v, k, extra = args
-    out = np.empty((hi - lo, k), dtype=np.int32)
-    for i in range(lo, hi):
-        path = (domain, i) if extra is None else (domain, i, extra)
-        out[i - lo] = omega_draw(stream(seed, *path), v, k)
-    return out
-
-
 def draw_omegas(seed: int, domain: int, lo: int, hi: int, v: int, k: int,
                 extra: Optional[int] = None, workers: Optional[int] = None) -> np.ndarray:
     """Sorted observation sets of indices [lo, hi) of a stream domain (first
-    draw of each stream), in parallel over host processes."""
-    count = hi - lo
-    workers = workers or min(os.cpu_count() or 1, 32)
-    if workers <= 1 or count * k < 2_000_000:
-        return _omega_block((seed, domain, lo, hi, v, k, extra))
-    bounds = np.linspace(lo, hi, workers * 4 + 1).astype(np.int64)
-    jobs = [(seed, domain, int(a), int(b), v, k, extra) for a, b in zip(bounds[:-1], bounds[1:])
-            if b > a]
-    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
-        return np.concatenate(list(pool.map(_omega_block, jobs)), axis=0)
+    draw of each stream): rapid.py:158-160 / lrmc.py:237-241."""
 
+    def row(i):
+        path = (domain, lo + i) if extra is None else (domain, lo + i, extra)
+        return omega_draw(stream(seed, *path), v, k)
 
-def _normals_block(args):
-    seed, domain, lo, hi, v = args
-    return np.stack([stream(seed, domain, i).standard_normal(v) for i in range(lo, hi)]).astype(
-        np.float32)
+    return fill_rows((k,), np.int32, row, hi - lo, workers)
 
 
 def draw_normals(seed: int, domain: int, lo: int, hi: int, v: int) -> np.ndarray:
-    workers = min(os.cpu_count() or 1, 32)
-    if workers <= 1 or (hi - lo) * v < 4_000_000:
-        return _normals_block((seed, domain, lo, hi, v))
-    bounds = np.linspace(lo, hi, min(workers, hi - lo) + 1).astype(np.int64)
-    jobs = [(seed, domain, int(a), int(b), v) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
-    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
-        return np.concatenate(list(pool.map(_normals_block, jobs)), axis=0)
+    """stream(seed, domain, i).standard_normal(v) for i in [lo, hi), fp32."""
+    return fill_rows((v,), np.float32,
+                     lambda i: stream(seed, domain, lo + i).standard_normal(v), hi - lo)
 
 
 def _resample(seed: int, path: tuple, attempt: int, v: int, k: int) -> np.ndarray:
