@@ -273,12 +273,21 @@ def main():
     algo_flops = 4.0 * n * v * local_L  # n MACs for S1 + n for Q1 per T entry
     achieved = algo_flops / (tfill_avg / 1e3) / 1e12
     peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")))
+    balanced = 2 * cfg.n1 == n
+    # executed tensor work per T entry: fp16 hi+lo split of Z (and Z^2 when
+    # the groups are unbalanced); balanced designs need S only (Q cancels)
+    exec_flops = (4.0 if balanced else 8.0) * n * v * local_L
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
                 "kernel": "k_tfill_tc (K1)", "algorithmic_flops_per_launch": algo_flops,
+                "algorithmic_unit": "4n flop per T entry (SURVEY 8d: n MACs for S + n for Q)",
                 "kernel_ms": tfill_avg, "peak_kind": f"{pk_kind} bf16 dense sustained",
                 "frac_of_burst": achieved / float(pk.get("bf16_tflops", peak)),
-                "split_factor_executed": 2}
+                "executed_tensor_tflops": exec_flops / (tfill_avg / 1e3) / 1e12,
+                "executed_frac": exec_flops / (tfill_avg / 1e3) / 1e12 / peak,
+                "note": ("n1 == n2: the pooled variance does not depend on Q, so K1 executes "
+                         "S = G.Z only (fp16 hi+lo: 4n flop per entry = the algorithmic count)"
+                         if balanced else "S and Q, fp16 hi+lo split: 8n flop per entry")}
 
     # ---------------- e2e through the public API from host buffers -----------
     e2e = None

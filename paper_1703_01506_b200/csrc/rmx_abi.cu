@@ -113,10 +113,12 @@ int device_sm_count() {
   return sms;
 }
 
-NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count) {
+NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   NaiveLayout lay{};
   lay.kpad = (n + 15) / 16 * 16;
-  lay.n_vtiles = (int)((v + kTileV - 1) / kTileV);
+  // balanced groups: t depends on S only -> 256-voxel S-only tiles
+  lay.vt = (2 * n1 == n) ? 2 * kTileV : kTileV;
+  lay.n_vtiles = (int)((v + lay.vt - 1) / lay.vt);
   // CTA pairs (cta_group::2) by default; RMX_CG=1 forces single-CTA tiles
   // (pairs halve B traffic per SM and deepen the ring; short-K tiles are
   // epilogue-bound and run better as single CTAs)
@@ -219,8 +221,9 @@ struct Ws {
   NaiveCounters* counters() const { return reinterpret_cast<NaiveCounters*>(base + lay.off_counters); }
 };
 
-int get_ws(int64_t v, int32_t n, int64_t L, void* workspace, size_t bytes, Ws* ws, rmx_status* st) {
-  ws->lay = naive_layout(v, n, L, device_sm_count());
+int get_ws(int64_t v, int32_t n, int32_t n1, int64_t L, void* workspace, size_t bytes, Ws* ws,
+           rmx_status* st) {
+  ws->lay = naive_layout(v, n, n1, L, device_sm_count());
   ws->base = static_cast<uint8_t*>(workspace);
   if (!workspace || bytes < ws->lay.total)
     return set_status(st, RMX_E_USAGE, "workspace of %zu bytes is smaller than the %zu required",
@@ -301,7 +304,9 @@ int rmx_device_check(int device, int32_t* sm_count, rmx_status* st) {
 }
 
 size_t rmx_naive_workspace_bytes(int64_t v, int32_t n, int64_t L) {
-  return naive_layout(v, n, L, device_sm_count()).total;
+  // the larger of the balanced (S-only) and general layouts
+  const int sm = device_sm_count();
+  return std::max(naive_layout(v, n, n / 2, L, sm).total, naive_layout(v, n, 2, L, sm).total);
 }
 
 int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t L,
@@ -309,7 +314,7 @@ int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
   Ws ws;
-  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   RMX_CUDA(cudaMemsetAsync(ws.counters(), 0, sizeof(NaiveCounters), s));
   RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
@@ -326,7 +331,7 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
   Ws ws;
-  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
   if (ws.lay.stages == 0)
     return set_status(st, RMX_E_USAGE,
                       "n=%d subjects exceed the tensor-core tile (A tile > smem); "
@@ -395,7 +400,7 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
   Ws ws;
-  if (int rc = get_ws(v, n, L, workspace, workspace_bytes, &ws, st)) return rc;
+  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   RefineArgs ra{};
   ra.x = x;
@@ -455,7 +460,7 @@ int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const i
                       rmx_naive_stats* stats) {
   if (int rc = rmx_naive_prepare(x, v, n, n1, L, workspace, workspace_bytes, stream, st)) return rc;
   Ws ws;
-  ws.lay = naive_layout(v, n, L, device_sm_count());
+  ws.lay = naive_layout(v, n, n1, L, device_sm_count());
   if (ws.lay.stages == 0) {
     // subject count beyond the tensor-core A tile: exhaustive exact path
     // (still on the GPU; fp64 CUDA cores)

@@ -41,12 +41,13 @@ struct NaiveLayout {
   int kpad;           // n rounded up to 16 (MMA K granularity)
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk, groups, grid, bk, stages;
   int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
+  int vt;             // voxels per tile: 256 (S-only, n1 == n2) or 128 (S | Q)
   size_t off_planes, off_cand, off_susp, off_cvox, off_overflow, off_best, off_const,
       off_counters;
   size_t total;
 };
 
-NaiveLayout naive_layout(int64_t v, int n, int64_t L, int sm_count);
+NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count);
 
 struct PrepArgs {
   const double* x;

@@ -135,7 +135,7 @@ __device__ __forceinline__ uint32_t group_hits(const uint32_t (&s)[32], const ui
 // loop); each column is re-read from TMEM (dynamic column = address, so no
 // register-array indexing) and every lane that flagged it re-tests exactly:
 // suspect listing for near-zero variance, else top-4 insertion.
-template <bool TWO_SIDED>
+template <bool TWO_SIDED, bool SONLY>
 __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int jbase,
                                            const EpiConst& ec, Top4& top, int64_t p, bool prow,
                                            const TfillArgs& a) {
@@ -143,11 +143,12 @@ __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int 
   while (uni) {
     const int c = __ffs(uni) - 1;
     uni &= uni - 1;
-    uint32_t sb, qb;
+    uint32_t sb, qb = 0u;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(sb) : "r"(taddr_s + c));
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                 : "=r"(qb)
-                 : "r"(taddr_s + kTileV + c));
+    if (!SONLY)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                   : "=r"(qb)
+                   : "r"(taddr_s + kTileV + c));
     tmem_ld_wait();
     if ((hits >> c) & 1u) {
       float u, d;
@@ -225,16 +226,21 @@ __device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, boo
 //   Z planes, rank 1 the Z^2 planes), so per-SM B traffic halves and the
 //   smem ring gets ~2x deeper.  Each CTA's TMEM receives its own 128 rows x
 //   256 columns, so the epilogue is identical.
+// ALPHA0 (n1 == n2): the pooled variance no longer depends on Q, so the tile
+// holds S only for 256 voxels (N = 256 columns of Z): half the MMA work per
+// T entry of the general (S | Q) tile.
 template <int CG, int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG>
 __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
+  constexpr bool SONLY = ALPHA0;
+  constexpr int TV = SONLY ? 2 * kTileV : kTileV;  // voxels per tile
   constexpr int HALF_BYTES = (kTileN / CG) * BK * 2;  // this CTA's hi (or lo) box
   constexpr int STAGE_BYTES = 2 * HALF_BYTES;
   constexpr int KSTEPS = BK / 16;
   constexpr uint32_t B_LAYOUT = (BK == 64) ? 2u : 4u;  // 128B : 64B swizzle
   constexpr uint32_t B_SBO = (BK == 64) ? 1024u : 512u;
   constexpr int GROUPS = EPI_WARPS / 4;  // epilogue warps sharing a TMEM lane quadrant
-  constexpr int COLGROUPS = kTileV / 32 / GROUPS;
+  constexpr int COLGROUPS = TV / 32 / GROUPS;
   constexpr uint32_t IDESC = idesc_f16_f32(kTileM * CG, kTileN);
 
   extern __shared__ uint8_t smem_raw[];
@@ -298,14 +304,20 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
             if (CG == 2) {
               mbar_wait_cluster(&empty[stage], phase ^ 1);
               if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
-              tma_load_3d_2sm(dst, &pmap, &full[stage], kb, t * kTileV, (int)rank);  // z_hi | q_hi
-              tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV,
-                              2 + (int)rank);  // z_lo | q_lo
+              if (SONLY) {  // this CTA's 128 of the tile's 256 voxels, Z planes only
+                const int v0 = t * TV + (int)rank * kTileV;
+                tma_load_3d_2sm(dst, &pmap, &full[stage], kb, v0, 0);               // z_hi
+                tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, v0, 2);  // z_lo
+              } else {
+                tma_load_3d_2sm(dst, &pmap, &full[stage], kb, t * TV, (int)rank);  // z_hi | q_hi
+                tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, t * TV,
+                                2 + (int)rank);  // z_lo | q_lo
+              }
             } else {
               mbar_wait(&empty[stage], phase ^ 1);
               mbar_expect_tx(&full[stage], STAGE_BYTES);
-              tma_load_3d(dst, &pmap, &full[stage], kb, t * kTileV, 0);               // z_hi, q_hi
-              tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * kTileV, 2);  // z_lo, q_lo
+              tma_load_3d(dst, &pmap, &full[stage], kb, t * TV, 0);               // z_hi(, q_hi)
+              tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * TV, 2);  // z_lo(, q_lo)
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -429,8 +441,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         if (CG == 2) mbar_wait_cluster(&tfull[acc], acc_phase);
         else mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const int64_t vleft = a.v - (int64_t)t * kTileV;
-        const int valid = vleft < kTileV ? (int)vleft : kTileV;
+        const int64_t vleft = a.v - (int64_t)t * TV;
+        const int valid = vleft < TV ? (int)vleft : TV;
 #pragma unroll 1
         for (int g = 0; g < COLGROUPS; ++g) {
           const int gc = (grp * COLGROUPS + g) * 32;
@@ -438,9 +450,14 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
               tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTileN + gc);
           uint32_t sv[32], qv[32];
           tmem_ld32(taddr, sv);
-          tmem_ld32(taddr + kTileV, qv);
+          if (SONLY) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) qv[c] = 0u;
+          } else {
+            tmem_ld32(taddr + kTileV, qv);
+          }
           tmem_ld_wait();
-          const int jbase = t * kTileV + gc;
+          const int jbase = t * TV + gc;
           const int gvalid = valid - gc;
           if (DEBUG) group_debug<TWO_SIDED>(sv, qv, jbase, gvalid, ec, p, prow, a);
           if (gvalid <= 0) continue;
@@ -448,7 +465,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           if (gvalid < 32) hits &= (1u << gvalid) - 1u;
           if (__any_sync(0xffffffffu, hits != 0u)) {
             ++rare_groups;
-            group_rare<TWO_SIDED>(hits, taddr, jbase, ec, top, p, prow, a);
+            group_rare<TWO_SIDED, SONLY>(hits, taddr, jbase, ec, top, p, prow, a);
           }
         }
         tc_fence_before();
@@ -559,12 +576,12 @@ cudaError_t dispatch_a(const NaiveLayout& lay, const TfillArgs& a, const CUtenso
 }  // namespace
 
 bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad, int bk,
-                     int planes_per_box) {
+                     int voxels_per_box, int planes_per_box) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)v, 4};
   cuuint64_t strides[2] = {(cuuint64_t)kpad * 2, (cuuint64_t)v * kpad * 2};
-  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)kTileV, (cuuint32_t)planes_per_box};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)voxels_per_box, (cuuint32_t)planes_per_box};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(planes), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -576,7 +593,12 @@ bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s) {
   CUtensorMap map;
-  if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk, 2 / lay.cg))
+  // box rows per TMA: S-only tiles load 256 (cg 1) or 128 (cg 2) voxels of one
+  // plane; (S | Q) tiles load 128 voxels of 2 (cg 1) or 1 (cg 2) planes
+  const bool sonly = a.alpha == 0.0f;
+  const int vbox = sonly ? 2 * kTileV / lay.cg : kTileV;
+  const int pbox = sonly ? 1 : 2 / lay.cg;
+  if (!make_planes_map(&map, planes, a.v, lay.kpad, lay.bk, vbox, pbox))
     return cudaErrorInvalidValue;
   return two_sided ? dispatch_a<true>(lay, a, map, s) : dispatch_a<false>(lay, a, map, s);
 }
