@@ -135,7 +135,10 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   lay.n_mtiles = (int)((L + tile_perms - 1) / tile_perms);
   const int n_clusters = std::max(1, sm_count / lay.cg);
   // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
-  lay.groups = 2;  // 8 epilogue warps: two per TMEM lane quadrant
+  // epilogue warps per TMEM lane quadrant: 4 for short-K single-CTA tiles
+  // (latency-bound epilogue), else 2
+  lay.groups = (lay.cg == 1 && lay.kpad <= 128 && 2 * n1 == n) ? 4 : 2;
+  if (const char* g = getenv("RMX_EPI_GROUPS")) lay.groups = atoi(g) == 4 ? 4 : 2;
   // Voxel chunks per permutation tile: minimise the static round-robin
   // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
   // one chunk of voxel tiles; A-tile rebuild counted as ~1/4 tile).

@@ -134,7 +134,9 @@ __device__ __forceinline__ uint32_t group_hits(const uint32_t (&s)[32], const ui
 // Rare path: the warp walks the union of its lanes' hit columns (uniform
 // loop); each column is re-read from TMEM (dynamic column = address, so no
 // register-array indexing) and every lane that flagged it re-tests exactly:
-// suspect listing for near-zero variance, else top-4 insertion.
+// suspect listing for near-zero variance, else top-4 insertion.  (Batching
+// all union loads behind one wait measured slower: the typical union is 1-3
+// columns and the unrolled batch costs registers.)
 template <bool TWO_SIDED, bool SONLY>
 __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int jbase,
                                            const EpiConst& ec, Top4& top, int64_t p, bool prow,
@@ -525,10 +527,9 @@ size_t smem_bytes_for(int cg, int bk, int stages, int kpad) {
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
 
-template <int CG, int BK, int STAGES, bool TS, bool A0, bool DBG>
-cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
-                       cudaStream_t s) {
-  constexpr int EPI = 8;
+template <int CG, int BK, int STAGES, int EPI, bool TS, bool A0, bool DBG>
+cudaError_t launch_cfg_e(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                         cudaStream_t s) {
   auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG>;
   const size_t smem = smem_bytes_for(CG, BK, STAGES, lay.kpad);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -546,6 +547,17 @@ cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtenso
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, map, a);
+}
+
+// epilogue warps: 16 (four per TMEM lane quadrant) for short-K single-CTA
+// tiles, where the epilogue is latency-bound; 8 otherwise
+template <int CG, int BK, int STAGES, bool TS, bool A0, bool DBG>
+cudaError_t launch_cfg(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                       cudaStream_t s) {
+  if constexpr (CG == 1 && A0 && !DBG) {
+    if (lay.groups == 4) return launch_cfg_e<CG, BK, STAGES, 16, TS, A0, DBG>(lay, a, map, s);
+  }
+  return launch_cfg_e<CG, BK, STAGES, 8, TS, A0, DBG>(lay, a, map, s);
 }
 
 template <bool TS, bool A0, bool DBG>
