@@ -65,7 +65,7 @@ typedef struct rmx_naive_stats {
   int64_t rare_groups;     /* epilogue: 32-column groups that took the exact path */
   int64_t all_groups;      /* epilogue: all 32-column groups (per warp) */
   int32_t cg;              /* CTAs per MMA tile (tcgen05 cta_group 1 or 2) */
-  int32_t _pad;
+  int32_t i8;              /* 1: exact int8 MMA on 16-bit fixed-point z (balanced groups) */
 } rmx_naive_stats;
 
 int rmx_abi_version(void);

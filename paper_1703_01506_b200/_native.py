@@ -50,7 +50,7 @@ class NaiveStats(ctypes.Structure):
         ("rare_groups", ctypes.c_int64),
         ("all_groups", ctypes.c_int64),
         ("cg", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("i8", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

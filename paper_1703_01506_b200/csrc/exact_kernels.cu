@@ -82,17 +82,48 @@ __global__ void k_prep(PrepArgs a) {
     ss = warp_sum_d(ss);
     const bool constant = (mn == mx);
     const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
-    __half* zh = a.planes + j * a.kpad;
-    for (int k = lane; k < a.kpad; k += 32) {
-      double z = 0.0;
-      if (k < a.n && !constant) z = (row[k] - mean) * inv;
-      const double q = z * z;
-      const __half h_z = __double2half(z);
-      const __half h_q = __double2half(q);
-      zh[k] = h_z;
-      zh[plane + k] = h_q;
-      zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
-      zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
+    if (a.planes8) {
+      // int8 path: zq = rint(z * scale) in [-32512, 32512], zq = 255 h + l with
+      // h, l in [-127, 127]; row j of planes8 = [h_0 .. h_kpad-1 | l_0 .. l_kpad-1]
+      double zmax = 0.0;
+      for (int k = lane; k < a.n; k += 32) zmax = fmax(zmax, fabs((row[k] - mean) * inv));
+      zmax = warp_max_d(zmax);
+      const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
+      const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
+      int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
+      double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
+      for (int k = lane; k < a.kpad; k += 32) {
+        int zq = 0;  // padded subjects and constant voxels: 0
+        if (k < a.n && !constant) {
+          const double z = (row[k] - mean) * inv;
+          zq = min(32512, max(-32512, (int)rint(z * scale)));
+          err += fabs(z - (double)zq * (double)inv_f);
+        }
+        const int h = (int)rint(zq / 255.0);
+        p8[k] = (int8_t)h;
+        p8[a.kpad + k] = (int8_t)(zq - 255 * h);
+      }
+      err = warp_sum_d(err);
+      if (lane == 0) {
+        a.inv_scale[j] = inv_f;
+        // rounded up; non-negative floats order like their bit patterns
+        atomicMax(&a.counters->emax_bits, __float_as_uint((float)(err * (1.0 + 1e-6)) + 1e-30f));
+      }
+    } else {
+      __half* zh = a.planes + j * a.kpad;
+      for (int k = lane; k < a.kpad; k += 32) {
+        double z = 0.0;
+        if (k < a.n && !constant) z = (row[k] - mean) * inv;
+        const __half h_z = __double2half(z);
+        zh[k] = h_z;
+        zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
+        if (!a.zplanes_only) {
+          const double q = z * z;
+          const __half h_q = __double2half(q);
+          zh[plane + k] = h_q;
+          zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
+        }
+      }
     }
     if (constant && lane == 0) {
       const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
@@ -186,7 +217,8 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
     if (e.y >= 0) tmax = fmaxf(tmax, __int_as_float(e.x));
   }
   for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-  const float band = kBandRel * fmaxf(fabsf(tmax), 1.0f);
+  const float band = band_abs(tmax, a.band_rel, __uint_as_float(a.counters->emax_bits),
+                              a.beta_abs, a.gamma);
   const float lo = tmax - band;
 
   double best = -DBL_MAX;
@@ -263,7 +295,10 @@ __global__ void k_transpose(const double* __restrict__ x, int64_t v, int n, doub
 }
 
 // grid (nvb, nperm): block (vb, i) evaluates perm list[i] over its voxel
-// stripe using X^T (coalesced across voxels).
+// stripe, thread per voxel.  TRANSPOSED: from X^T (coalesced across voxels,
+// for many permutations); else straight from X (v x n rows; no transpose or
+// scratch, for the few permutations of the overflow fallback).
+template <bool TRANSPOSED>
 __global__ void k_exact_rows(const double* __restrict__ xt, int64_t v, int n, int n1,
                              const int16_t* __restrict__ orders, const int32_t* perm_list,
                              int64_t perm_offset, int two_sided, double* t_out, int64_t ld,
@@ -278,7 +313,8 @@ __global__ void k_exact_rows(const double* __restrict__ xt, int64_t v, int n, in
   double best = -DBL_MAX;
   int bj = -1;
   for (int64_t j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
-    const WelchExact r = welch_exact(xt + j, v, ord, n1, n - n1);
+    const WelchExact r = TRANSPOSED ? welch_exact(xt + j, v, ord, n1, n - n1)
+                                    : welch_exact(xt + j * n, 1, ord, n1, n - n1);
     if (r.degenerate) {
       if (counters) note_degenerate(counters, p, j);
       continue;
@@ -372,12 +408,13 @@ cudaError_t launch_transpose(const double* x, int64_t v, int n, double* xt, cuda
 cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1, const int16_t* orders,
                              const int32_t* perm_list, int64_t nperm, int two_sided,
                              double* t_out, int64_t ld, double* part_val, int32_t* part_idx,
-                             int nvb, NaiveCounters* counters, cudaStream_t s) {
+                             int nvb, NaiveCounters* counters, cudaStream_t s, bool transposed) {
   if (nperm <= 0) return cudaSuccess;
+  auto kern = transposed ? k_exact_rows<true> : k_exact_rows<false>;
   for (int64_t base = 0; base < nperm; base += 65535) {
     const int64_t cnt = nperm - base < 65535 ? nperm - base : 65535;
     dim3 grid((unsigned)nvb, (unsigned)cnt);
-    k_exact_rows<<<grid, 256, n * sizeof(int16_t), s>>>(
+    kern<<<grid, 256, n * sizeof(int16_t), s>>>(
         xt, v, n, n1, orders, perm_list ? perm_list + base : nullptr, base, two_sided,
         t_out ? t_out + base * ld : nullptr, ld, part_val ? part_val + base * nvb : nullptr,
         part_idx ? part_idx + base * nvb : nullptr, counters);

@@ -15,7 +15,7 @@
 
 namespace rmx {
 
-size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad);
+size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad, bool i8);
 
 namespace {
 
@@ -104,6 +104,21 @@ bool pick_pipeline(int cg, int kpad, int* bk, int* stages) {
   return false;
 }
 
+// int8 tiles: bk = 128 K-bytes per stage (one 128B-swizzled box of
+// 256 / cg voxel rows); A = kTileM x 2 kpad bytes.  Instantiated
+// (cg, stages): (1, 4) (1, 3) (2, 7) (2, 4)
+bool pick_pipeline_i8(int cg, int kpad, int* bk, int* stages) {
+  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024 + kInvStage;
+  if (a_bytes >= kMaxSmem) return false;
+  const int fit = (int)((kMaxSmem - a_bytes) / ((size_t)(2 * kTileV / cg) * 128));
+  const int want = cg == 2 ? 7 : 4;
+  const int s = fit >= want ? want : (fit >= (cg == 2 ? 4 : 3) ? (cg == 2 ? 4 : 3) : 0);
+  if (!s) return false;
+  *bk = 128;
+  *stages = s;
+  return true;
+}
+
 }  // namespace
 
 int device_sm_count() {
@@ -115,18 +130,27 @@ int device_sm_count() {
 
 NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   NaiveLayout lay{};
-  lay.kpad = (n + 15) / 16 * 16;
-  // balanced groups: t depends on S only -> 256-voxel S-only tiles
-  lay.vt = (2 * n1 == n) ? 2 * kTileV : kTileV;
+  const bool balanced = 2 * n1 == n;
+  // balanced groups: t depends on S only -> 256-voxel S-only tiles.  Default
+  // there: exact int8 MMA on fixed-point Z; RMX_I8=0 selects fp16 hi/lo.
+  // (short K is epilogue-bound, where the fp16 tiles' cheaper epilogue wins)
+  lay.i8 = (balanced && n >= 192) ? 1 : 0;
+  if (const char* e = getenv("RMX_I8")) lay.i8 = balanced && atoi(e) != 0;
+  lay.kpad = lay.i8 ? (n + 31) / 32 * 32 : (n + 15) / 16 * 16;
+  lay.vt = balanced ? 2 * kTileV : kTileV;
   lay.n_vtiles = (int)((v + lay.vt - 1) / lay.vt);
   // CTA pairs (cta_group::2) by default; RMX_CG=1 forces single-CTA tiles
   // (pairs halve B traffic per SM and deepen the ring; short-K tiles are
   // epilogue-bound and run better as single CTAs)
   lay.cg = lay.kpad >= 192 ? 2 : 1;
   if (const char* e = getenv("RMX_CG")) lay.cg = atoi(e) == 1 ? 1 : 2;
-  if (!pick_pipeline(lay.cg, lay.kpad, &lay.bk, &lay.stages)) {
+  auto pick = [&](int cg) {
+    return lay.i8 ? pick_pipeline_i8(cg, lay.kpad, &lay.bk, &lay.stages)
+                  : pick_pipeline(cg, lay.kpad, &lay.bk, &lay.stages);
+  };
+  if (!pick(lay.cg)) {
     lay.cg = 1;
-    if (!pick_pipeline(1, lay.kpad, &lay.bk, &lay.stages)) {
+    if (!pick(1)) {
       lay.bk = 0;
       lay.stages = 0;
     }
@@ -137,7 +161,7 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
   // epilogue warps per TMEM lane quadrant: 4 for short-K single-CTA tiles
   // (latency-bound epilogue), else 2
-  lay.groups = (lay.cg == 1 && lay.kpad <= 128 && 2 * n1 == n) ? 4 : 2;
+  lay.groups = (lay.cg == 1 && lay.kpad <= 128 && balanced) ? 4 : 2;
   if (const char* g = getenv("RMX_EPI_GROUPS")) lay.groups = atoi(g) == 4 ? 4 : 2;
   // Voxel chunks per permutation tile: minimise the static round-robin
   // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
@@ -173,7 +197,10 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
 
   size_t off = 0;
   lay.off_planes = off;
-  off = align_up(off + (size_t)4 * v * lay.kpad * 2, 1024);
+  // fp16: [4][v][kpad] halves (z_hi, q_hi, z_lo, q_lo); int8: [v][2 kpad] bytes
+  off = align_up(off + (lay.i8 ? (size_t)2 * v * lay.kpad : (size_t)4 * v * lay.kpad * 2), 1024);
+  lay.off_scale = off;  // int8: per-voxel dequantisation scale, padded to whole tiles
+  off = align_up(off + (lay.i8 ? (size_t)lay.n_vtiles * lay.vt * 4 : 0), 256);
   lay.off_cand = off;
   off = align_up(off + (size_t)lay.n_mtiles * tile_perms * lay.n_chunks * lay.groups * 32, 256);
   lay.off_susp = off;
@@ -215,6 +242,8 @@ struct Ws {
   NaiveLayout lay;
   uint8_t* base;
   __half* planes() const { return reinterpret_cast<__half*>(base + lay.off_planes); }
+  uint8_t* planes8() const { return base + lay.off_planes; }
+  float* scale() const { return reinterpret_cast<float*>(base + lay.off_scale); }
   int4* cand() const { return reinterpret_cast<int4*>(base + lay.off_cand); }
   int32_t* susp() const { return reinterpret_cast<int32_t*>(base + lay.off_susp); }
   int32_t* cvox() const { return reinterpret_cast<int32_t*>(base + lay.off_cvox); }
@@ -242,15 +271,25 @@ int run_exhaustive(const double* x, int64_t v, int32_t n, int32_t n1, const int1
   double* xt = nullptr;
   double* pv = nullptr;
   int32_t* pi = nullptr;
-  const int nvb = (int)std::min<int64_t>(std::max<int64_t>(1, (v + 4095) / 4096), 64);
-  RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xt), (size_t)v * n * sizeof(double), s));
+  // voxel stripes per permutation: enough blocks to fill the GPU even when
+  // only a few permutations overflowed (one thread per voxel)
+  int64_t nvb64 = std::min<int64_t>(std::max<int64_t>(1, (v + 4095) / 4096), 64);
+  const int64_t fill = (4 * (int64_t)device_sm_count() + nperm - 1) / nperm;
+  nvb64 = std::max(nvb64, std::min(fill, (v + 255) / 256));
+  const int nvb = (int)std::min<int64_t>(nvb64, 65535);
+  // few permutations (the usual overflow case): read X rows directly; many:
+  // transpose once so the per-voxel reads coalesce
+  const bool transposed = nperm > 64;
+  if (transposed) {
+    RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xt), (size_t)v * n * sizeof(double), s));
+    RMX_CUDA(launch_transpose(x, v, n, xt, s));
+  }
   RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pv), (size_t)nperm * nvb * sizeof(double), s));
   RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pi), (size_t)nperm * nvb * sizeof(int32_t), s));
-  RMX_CUDA(launch_transpose(x, v, n, xt, s));
-  RMX_CUDA(launch_exact_rows(xt, v, n, n1, orders, perm_list, nperm, two_sided, nullptr, 0, pv, pi,
-                             nvb, counters, s));
+  RMX_CUDA(launch_exact_rows(transposed ? xt : x, v, n, n1, orders, perm_list, nperm, two_sided,
+                             nullptr, 0, pv, pi, nvb, counters, s, transposed));
   RMX_CUDA(launch_exact_reduce(pv, pi, nvb, perm_list, nperm, max_out, argmax_out, s));
-  RMX_CUDA(cudaFreeAsync(xt, s));
+  if (xt) RMX_CUDA(cudaFreeAsync(xt, s));
   RMX_CUDA(cudaFreeAsync(pv, s));
   RMX_CUDA(cudaFreeAsync(pi, s));
   return RMX_OK;
@@ -323,6 +362,13 @@ int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t
   RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
   RMX_CUDA(cudaMemsetAsync(ws.best(), 0, (size_t)L * 4, s));
   PrepArgs pa{x, v, n, n1, ws.lay.kpad, ws.planes(), ws.cvox(), ws.counters()};
+  if (ws.lay.i8) {
+    pa.planes8 = ws.planes8();
+    pa.inv_scale = ws.scale();
+    // scale padding (voxels past v) must be finite: those columns are masked
+    RMX_CUDA(cudaMemsetAsync(ws.scale(), 0, (size_t)ws.lay.n_vtiles * ws.lay.vt * 4, s));
+  }
+  pa.zplanes_only = (2 * n1 == n) ? 1 : 0;
   RMX_CUDA(launch_prep(pa, s));
   RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
   return RMX_OK;
@@ -354,7 +400,7 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   a.n = n;
   a.n1 = n1;
   a.kpad = ws.lay.kpad;
-  a.nk16 = ws.lay.kpad / 16;
+  a.nk16 = ws.lay.kpad / 16;  // MMA K-steps (int8: 2 kpad / 32)
   a.n_vtiles = ws.lay.n_vtiles;
   a.n_mtiles = ws.lay.n_mtiles;
   a.n_chunks = ws.lay.n_chunks;
@@ -365,6 +411,9 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   a.beta = (float)beta;
   a.gamma = (float)gamma;
   a.dthr = (float)(1e-4 * bmax);
+  a.band_rel = kBandRel;
+  a.beta_abs = (float)std::fabs(beta);
+  a.inv_scale = ws.lay.i8 ? ws.scale() : nullptr;
   a.cand = ws.cand();
   a.susp = ws.susp();
   a.best_t = ws.best();
@@ -377,6 +426,7 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
     stats->stages = ws.lay.stages;
     stats->bk = ws.lay.bk;
     stats->cg = ws.lay.cg;
+    stats->i8 = ws.lay.i8;
   }
   return RMX_OK;
 }
@@ -414,6 +464,13 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
   ra.n1 = n1;
   ra.slots = ws.lay.n_chunks * ws.lay.groups;
   ra.two_sided = two_sided;
+  {
+    const double dn = n, d1 = n1, d2 = n - n1;
+    const double c = (d1 * d2 / dn) * (d1 * d2 / dn);
+    ra.band_rel = kBandRel;
+    ra.beta_abs = (float)(c * (1.0 / (d1 * d1 * (d1 - 1.0)) + 1.0 / (d2 * d2 * (d2 - 1.0))));
+    ra.gamma = (float)(c * (dn - 1.0) / (d2 * (d2 - 1.0)));
+  }
   ra.cand = ws.cand();
   ra.susp = ws.susp();
   ra.cinfo = ws.cinfo();
@@ -453,6 +510,7 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
     stats->stages = ws.lay.stages;
     stats->bk = ws.lay.bk;
     stats->cg = ws.lay.cg;
+    stats->i8 = ws.lay.i8;
   }
   return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);
 }

@@ -10,11 +10,37 @@ namespace rmx {
 constexpr int kTileM = 128;  // permutations per tile = TMEM lanes = MMA M
 constexpr int kTileV = 128;  // voxels per tile; MMA N = 2 * kTileV (S | Q)
 constexpr int kSuspectCap = 1 << 16;
+constexpr int kInvStage = 4096;  // int8 K1: epilogue staging of per-voxel scales (bytes)
 // Relative half-width of the candidate band: every voxel whose tensor-core
 // statistic lies within kBandRel * max(|t*|, 1) of the permutation's best is
 // re-evaluated in fp64.  The measured |t~ - t| / max(|t|,1) is ~1e-6
 // (tests/test_gpu_parity.py::test_tensor_core_error_bound), 100x below this.
 constexpr float kBandRel = 1e-4f;
+
+// Candidate band for a permutation whose best tensor-core statistic is t
+// (two-sided: |t|).  fp16 path: kBandRel * max(|t|, 1).  int8 path (balanced
+// groups, alpha = 0): the quantised Z perturbs every group sum S by at most
+// e = max_j sum_i |z_ij - zq_ij / scale_j| (K0 measures it), and t = f(S) =
+// S / sqrt(gamma - |beta| S^2) is increasing in S, so a voxel's true statistic
+// lies in [f(S~ - e), f(S~ + e)].  The true maximum T >= lower(t~max) and the
+// voxel attaining it has t~ >= lower(T) >= lower(lower(t~max)): the band
+// t~max - lower(lower(t~max)) (+ the fp32 term) is rigorous.  A band that
+// reaches a non-positive pooled variance is infinite (-> exhaustive path).
+__device__ __forceinline__ double band_lower(double t, double e, double beta_abs, double gamma) {
+  const double d = gamma / (1.0 + beta_abs * t * t);
+  const double S = t * sqrt(d) - e;
+  const double d2 = gamma - beta_abs * S * S;
+  if (d2 <= 0.0) return -HUGE_VAL;
+  return S / sqrt(d2);
+}
+__device__ __forceinline__ float band_abs(float t, float rel, float e, float beta_abs,
+                                          float gamma) {
+  const float base = rel * fmaxf(fabsf(t), 1.0f);
+  if (!(e > 0.0f)) return base;
+  const double lo = band_lower(band_lower(t, e, beta_abs, gamma), e, beta_abs, gamma);
+  if (lo == -HUGE_VAL) return HUGE_VALF;
+  return base + (float)((double)t - lo) * 1.001f;
+}
 
 struct ConstInfo {    // voxels constant over all subjects (reference quirks kept)
   double best_t;      // max over such voxels of their exact statistic
@@ -31,7 +57,8 @@ struct NaiveCounters {
   unsigned int overflow_count;
   unsigned int band_candidates;
   unsigned int cvox_count;
-  unsigned int pad[2];
+  unsigned int emax_bits;  // int8 path: max_j sum_i |z - dequantised z| (float bits)
+  unsigned int pad;
   unsigned long long rare_groups;  // epilogue diagnostics (lane max per warp)
   unsigned long long all_groups;
 };
@@ -41,8 +68,9 @@ struct NaiveLayout {
   int kpad;           // n rounded up to 16 (MMA K granularity)
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk, groups, grid, bk, stages;
   int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
+  int i8;             // exact int8 MMA on 16-bit fixed-point Z (balanced groups)
   int vt;             // voxels per tile: 256 (S-only, n1 == n2) or 128 (S | Q)
-  size_t off_planes, off_cand, off_susp, off_cvox, off_overflow, off_best, off_const,
+  size_t off_planes, off_scale, off_cand, off_susp, off_cvox, off_overflow, off_best, off_const,
       off_counters;
   size_t total;
 };
@@ -56,6 +84,11 @@ struct PrepArgs {
   __half* planes;  // [4][v][kpad]: z_hi, q_hi, z_lo, q_lo (q = z^2)
   int32_t* cvox;   // constant voxels with a non-zero exact statistic
   NaiveCounters* counters;
+  // int8 path (balanced groups): z quantised per voxel, zq = 255 h + l,
+  // planes8[v][2 kpad] = [h | l] (s8); S = inv[j] * sum_{group 1} zq
+  uint8_t* planes8;
+  float* inv_scale;
+  int zplanes_only;  // balanced fp16 path: the Z^2 planes are not needed
 };
 
 struct TfillArgs {
@@ -65,6 +98,9 @@ struct TfillArgs {
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
   int stride_full, stride_last;  // tile visiting strides (coprime with the chunk length)
   float alpha, beta, gamma, dthr;
+  float band_rel;          // fp32 part of the refinement band (threshold seeding)
+  float beta_abs;          // |beta| (int8 band, see band_abs)
+  const float* inv_scale;  // int8 path: per-voxel 1/scale
   int4* cand;  // [L][n_chunks * groups][2]: top-4 (t~, voxel) pairs
   int32_t* susp;
   uint32_t* best_t;  // [L] running best t~ per permutation (order-encoded, 0 = none)
@@ -77,6 +113,7 @@ struct RefineArgs {
   const int16_t* orders;
   int64_t L, v;
   int n, n1, slots, two_sided;
+  float band_rel, beta_abs, gamma;  // band_abs parameters; e from counters->emax_bits
   const int4* cand;
   const int32_t* susp;
   const ConstInfo* cinfo;
@@ -98,7 +135,7 @@ cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1,
                              const int16_t* orders, const int32_t* perm_list, int64_t nperm,
                              int two_sided, double* t_out, int64_t ld, double* part_val,
                              int32_t* part_idx, int nvb, NaiveCounters* counters,
-                             cudaStream_t s);
+                             cudaStream_t s, bool transposed = true);
 cudaError_t launch_exact_reduce(const double* part_val, const int32_t* part_idx, int nvb,
                                 const int32_t* perm_list, int64_t nperm, double* max_out,
                                 int32_t* argmax_out, cudaStream_t s);

@@ -94,6 +94,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
+// Arrive on a (possibly remote) CTA's barrier with the default .release.cta
+// semantics: enough to order tcgen05 work fenced with
+// tcgen05.fence::before_thread_sync (TMEM drained -> MMA may overwrite) and
+// far cheaper than a cluster-scope release (no MEMBAR.ALL.GPU).
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -104,6 +113,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
       "r"(phase)
       : "memory");
 }
+
+// 16-byte global -> shared copy (LDGSTS), completion via cp_async_wait_all.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Generic-proxy smem writes -> visible to the async proxy (tensor core reads).
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -160,6 +177,26 @@ __device__ __forceinline__ void mma_f16_ss_2sm(uint32_t d_tmem, uint64_t a_desc,
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A . B, kind::i8 (u8 x u8 -> exact int32 accumulators)
+__device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Commit the leader's tcgen05 ops to the same-offset mbarrier in every CTA of
 // `cta_mask` (pair: 0b11).
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t cta_mask) {
@@ -213,6 +250,12 @@ __host__ __device__ constexpr uint64_t smem_desc(uint32_t addr, uint32_t lbo, ui
 
 // Instruction descriptor, kind::f16: fp16 A/B (format 0), fp32 D (format 1),
 // both K-major, N>>3 at [17,23), M>>4 at [24,29).
+// kind::i8: u8 A (a_format [7,10) = 0), s8 B (b_format [10,13) = 1), s32 D
+// (format 2), both K-major
+__host__ __device__ constexpr uint32_t idesc_u8s8_s32(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 __host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }

@@ -111,7 +111,10 @@ struct EpiConst {
 template <bool ALPHA0>
 __device__ __forceinline__ uint32_t group_hits(const uint32_t (&s)[32], const uint32_t (&q)[32],
                                                const EpiConst& ec, float k3) {
-  const uint64_t nk3 = pack2(__float_as_uint(-k3), __float_as_uint(-k3));
+  // k3 < 0 (signed, fewer than 4 non-negative keys yet): test against 0, so
+  // every column hits (superset) and a negative d~ can never hide a suspect
+  const float k3h = fmaxf(k3, 0.0f);
+  const uint64_t nk3 = pack2(__float_as_uint(-k3h), __float_as_uint(-k3h));
   uint32_t neg = 0;
 #pragma unroll
   for (int c = 30; c >= 0; c -= 2) {
@@ -131,16 +134,55 @@ __device__ __forceinline__ uint32_t group_hits(const uint32_t (&s)[32], const ui
   return ~neg;
 }
 
+// S-only tiles (alpha = 0): d = beta S^2 + gamma with beta < 0, so
+//     m > 0  <=>  S^2 > K,   K = k3' gamma / (1 - k3' beta),  k3' = max(k3, 0)
+// (denominator >= 1).  The common path is one packed FMA per column pair
+// (S^2 - K) and a 3-input AND of the sign bits: "could any column hit".  A
+// degenerate or negative-d~ column has S^2 >= gamma / |beta| > K: always hits.
+__device__ __forceinline__ float sonly_thr(float k3, const EpiConst& ec) {
+  const float k = fmaxf(k3, 0.0f);
+  return k * ec.gamma / fmaf(-k, ec.beta, 1.0f);
+}
+__device__ __forceinline__ bool sonly_any(const uint32_t (&s)[32], float K) {
+  const uint64_t nk = pack2(__float_as_uint(-K), __float_as_uint(-K));
+  uint32_t all = 0xffffffffu;
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    const uint64_t S2 = pack2(s[c], s[c + 1]);
+    const uint64_t m = fma2(S2, S2, nk);
+    all &= (uint32_t)m & (uint32_t)(m >> 32);
+  }
+  return (int)all >= 0;  // some sign bit clear
+}
+__device__ __forceinline__ uint32_t sonly_mask(const uint32_t (&s)[32], float K) {
+  const uint64_t nk = pack2(__float_as_uint(-K), __float_as_uint(-K));
+  uint32_t neg = 0;
+#pragma unroll
+  for (int c = 30; c >= 0; c -= 2) {
+    const uint64_t S2 = pack2(s[c], s[c + 1]);
+    const uint64_t m = fma2(S2, S2, nk);
+    neg = __funnelshift_l((uint32_t)(m >> 32), neg, 1);
+    neg = __funnelshift_l((uint32_t)m, neg, 1);
+  }
+  return ~neg;
+}
+
 // Rare path: the warp walks the union of its lanes' hit columns (uniform
 // loop); each column is re-read from TMEM (dynamic column = address, so no
 // register-array indexing) and every lane that flagged it re-tests exactly:
 // suspect listing for near-zero variance, else top-4 insertion.  (Batching
 // all union loads behind one wait measured slower: the typical union is 1-3
 // columns and the unrolled batch costs registers.)
-template <bool TWO_SIDED, bool SONLY>
+// I8 tiles: exact integer accumulator S_q -> fp32 S with the voxel's
+// dequantisation scale.
+__device__ __forceinline__ uint32_t i8_to_s(uint32_t sq, float inv) {
+  return __float_as_uint((float)(int)sq * inv);
+}
+
+template <bool TWO_SIDED, bool SONLY, bool I8>
 __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int jbase,
                                            const EpiConst& ec, Top4& top, int64_t p, bool prow,
-                                           const TfillArgs& a) {
+                                           const TfillArgs& a, const float* ginv) {
   uint32_t uni = __reduce_or_sync(0xffffffffu, hits);
   while (uni) {
     const int c = __ffs(uni) - 1;
@@ -152,6 +194,7 @@ __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int 
                    : "=r"(qb)
                    : "r"(taddr_s + kTileV + c));
     tmem_ld_wait();
+    if (I8) sb = i8_to_s(sb, ginv[c]);
     if ((hits >> c) & 1u) {
       float u, d;
       stat_ud<TWO_SIDED>(sb, qb, ec.alpha, ec.beta, ec.gamma, u, d);
@@ -194,6 +237,12 @@ __device__ __forceinline__ int chunk_tile(const TfillArgs& a, int t0, int t1, in
   return t0 + (int)(((int64_t)i * stride) % T);
 }
 
+// Voxel-tile range [t0, t1) of a chunk.
+__device__ __forceinline__ void chunk_range(const TfillArgs& a, int chunk, int& t0, int& t1) {
+  t0 = chunk * a.tiles_per_chunk;
+  t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+}
+
 __device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
 
 // Order-preserving float <-> uint32 map for atomicMax; 0 = "no value yet".
@@ -211,12 +260,15 @@ __device__ __forceinline__ float ord_dec(uint32_t e) {
 // seed - 2 band(seed) can matter: starting the top-4 there is exact and
 // keeps the epilogue's rare path rare.
 template <bool TWO_SIDED>
-__device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, bool prow) {
+__device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, bool prow,
+                                          const TfillArgs& a, float emax) {
   if (!prow) return -FLT_MAX;
   const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(best_t + p);
   if (e == 0u) return -FLT_MAX;
   const float t = ord_dec(e);
-  const float lo = t - 2.0f * kBandRel * fmaxf(fabsf(t), 1.0f);
+  const float band = band_abs(t, a.band_rel, emax, a.beta_abs, a.gamma);
+  if (!(band < 1e30f)) return -FLT_MAX;
+  const float lo = t - 2.0f * band;
   if (TWO_SIDED) return lo > 0.0f ? lo * lo : 0.0f;
   return lo * fabsf(lo);
 }
@@ -231,26 +283,41 @@ __device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, boo
 // ALPHA0 (n1 == n2): the pooled variance no longer depends on Q, so the tile
 // holds S only for 256 voxels (N = 256 columns of Z): half the MMA work per
 // T entry of the general (S | Q) tile.
-template <int CG, int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG>
+//
+// I8 (balanced groups): exact integer MMA (kind::i8, u8 A x s8 B -> s32).  Z
+// is quantised per voxel to zq = rint(z * scale) in [-32512, 32512] and split
+// zq = 255 h + l with h, l in [-127, 127] (s8).  B rows hold [h | l] along K
+// (K = 2 kpad), A rows [255 G | G] (u8), so one accumulator receives
+// S_q = sum_{group 1} zq exactly and S = inv[j] * S_q: the same S-only tile
+// (256 voxels) as fp16, at twice the MMA rate and half the operand bytes.
+// The refinement band covers the quantisation rigorously (band_abs).
+template <int CG, int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG,
+          bool I8>
 __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
+  static_assert(!I8 || ALPHA0, "int8 tiles are S-only (balanced groups)");
   constexpr bool SONLY = ALPHA0;
   constexpr int TV = SONLY ? 2 * kTileV : kTileV;  // voxels per tile
-  constexpr int HALF_BYTES = (kTileN / CG) * BK * 2;  // this CTA's hi (or lo) box
-  constexpr int STAGE_BYTES = 2 * HALF_BYTES;
-  constexpr int KSTEPS = BK / 16;
-  constexpr uint32_t B_LAYOUT = (BK == 64) ? 2u : 4u;  // 128B : 64B swizzle
-  constexpr uint32_t B_SBO = (BK == 64) ? 1024u : 512u;
+  constexpr int ELT = I8 ? 1 : 2;                   // operand bytes per element
+  constexpr int HALF_BYTES = (kTileN / CG) * BK * ELT;  // this CTA's hi (or lo) box
+  constexpr int STAGE_BYTES = I8 ? HALF_BYTES : 2 * HALF_BYTES;
+  constexpr int KSTEP = I8 ? 32 : 16;  // K per MMA instruction
+  constexpr int KSTEPS = BK / KSTEP;
+  constexpr int ROW_BYTES = BK * ELT;
+  constexpr uint32_t B_LAYOUT = (ROW_BYTES == 128) ? 2u : 4u;  // 128B : 64B swizzle
+  constexpr uint32_t B_SBO = (ROW_BYTES == 128) ? 1024u : 512u;
   constexpr int GROUPS = EPI_WARPS / 4;  // epilogue warps sharing a TMEM lane quadrant
   constexpr int COLGROUPS = TV / 32 / GROUPS;
-  constexpr uint32_t IDESC = idesc_f16_f32(kTileM * CG, kTileN);
+  constexpr uint32_t IDESC =
+      I8 ? idesc_u8s8_s32(kTileM * CG, kTileN) : idesc_f16_f32(kTileM * CG, kTileN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_mem = smem;
   uint8_t* a_mem = smem + STAGES * STAGE_BYTES;
-  const int a_bytes = kTileM * a.kpad * 2;
+  const int kext = I8 ? 2 * a.kpad : a.kpad;  // K extent (elements) of A rows / B rows
+  const int a_bytes = kTileM * kext * ELT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(a_mem + a_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
@@ -258,6 +325,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
   uint64_t* tempty = tfull + kNumAcc;
   uint64_t* afull = tempty + kNumAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
+  // int8: per-epilogue-warp staging of its columns' dequantisation scales
+  float* inv_smem = reinterpret_cast<float*>(a_mem + a_bytes + 256);
 
   const int warp = (int)warp_id();
   const int lane = threadIdx.x & 31;
@@ -297,14 +366,24 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       uint32_t phase = 0;
       for (int u = unit0; u < n_units; u += unit_step) {
         const int chunk = u / a.n_mtiles;
-        const int t0 = chunk * a.tiles_per_chunk;
-        const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+        int t0, t1;
+        chunk_range(a, chunk, t0, t1);
         for (int i = 0; i < t1 - t0; ++i) {
           const int t = chunk_tile(a, t0, t1, i);
-          for (int kb = 0; kb < a.kpad; kb += BK) {
+          for (int kb = 0; kb < kext; kb += BK) {
             uint8_t* dst = stage_mem + stage * STAGE_BYTES;
-            if (CG == 2) {
-              mbar_wait_cluster(&empty[stage], phase ^ 1);
+            if (I8) {  // one box per stage: this CTA's voxels x 128 K-bytes of [h | l]
+              if (CG == 2) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                tma_load_3d_2sm(dst, &pmap, &full[stage], kb, t * TV + (int)rank * kTileV, 0);
+              } else {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_expect_tx(&full[stage], STAGE_BYTES);
+                tma_load_3d(dst, &pmap, &full[stage], kb, t * TV, 0);
+              }
+            } else if (CG == 2) {
+              mbar_wait(&empty[stage], phase ^ 1);
               if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
               if (SONLY) {  // this CTA's 128 of the tile's 256 voxels, Z planes only
                 const int v0 = t * TV + (int)rank * kTileV;
@@ -334,37 +413,39 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     // ------------------------------------------------------------ MMA issuer
     if (leader) {
       const uint32_t a_base = smem_u32(a_mem);
-      const uint32_t a_sbo = (uint32_t)a.kpad * 16u;
+      const uint32_t a_sbo = (uint32_t)kext * 8u * ELT;
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0, a_phase = 0;
       int acc = 0;
       for (int u = unit0; u < n_units; u += unit_step) {
         const int chunk = u / a.n_mtiles;
-        const int t0 = chunk * a.tiles_per_chunk;
-        const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+        int t0, t1;
+        chunk_range(a, chunk, t0, t1);
         if (CG == 2) mbar_wait_cluster(afull, a_phase);
         else mbar_wait(afull, a_phase);
         a_phase ^= 1;
         tc_fence_after();
         for (int t = t0; t < t1; ++t) {
-          if (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
-          else mbar_wait(&tempty[acc], acc_phase ^ 1);
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem + (uint32_t)(acc * kTileN);
-          for (int kb = 0; kb < a.kpad; kb += BK) {
+          for (int kb = 0; kb < kext; kb += BK) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             if (elect_one()) {
               const uint32_t sb = smem_u32(stage_mem + stage * STAGE_BYTES);
 #pragma unroll
               for (int s = 0; s < KSTEPS; ++s) {
-                const int ks = kb / 16 + s;
+                const int ks = kb / KSTEP + s;
                 if (ks < a.nk16) {
                   const uint64_t adesc = smem_desc(a_base + (uint32_t)ks * 256u, 128u, a_sbo, 0u);
                   const uint64_t bh = smem_desc(sb + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
                   const uint64_t bl = smem_desc(sb + (uint32_t)HALF_BYTES + (uint32_t)s * 32u, 16u,
                                                 B_SBO, B_LAYOUT);
-                  if (CG == 2) {
+                  if (I8) {
+                    if (CG == 2) mma_i8_ss_2sm(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
+                    else mma_i8_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
+                  } else if (CG == 2) {
                     mma_f16_ss_2sm(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
                     mma_f16_ss_2sm(d_tmem, adesc, bl, IDESC, 1u);
                   } else {
@@ -375,10 +456,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
               }
               if (CG == 2) {
                 mma_commit_2sm(&empty[stage], 0x3);                       // both smem slots free
-                if (kb + BK >= a.kpad) mma_commit_2sm(&tfull[acc], 0x3);  // both accumulators
+                if (kb + BK >= kext) mma_commit_2sm(&tfull[acc], 0x3);  // both accumulators
               } else {
                 mma_commit(&empty[stage]);
-                if (kb + BK >= a.kpad) mma_commit(&tfull[acc]);
+                if (kb + BK >= kext) mma_commit(&tfull[acc]);
               }
             }
             __syncwarp();
@@ -405,6 +486,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     ec.beta = a.beta;
     ec.gamma = a.gamma;
     ec.dthr = a.dthr;
+    // int8: quantisation error bound (K0); a truly degenerate voxel
+    // (|S| = sqrt(gamma/|beta|)) then has d~ <= 2 |beta| sqrt(gamma/|beta|) e
+    const float emax = I8 ? __uint_as_float(a.counters->emax_bits) : 0.0f;
+    if (I8) ec.dthr = fmaxf(a.dthr, 2.5f * a.beta_abs * sqrtf(a.gamma / a.beta_abs) * emax);
     ec.alpha2 = pack2(__float_as_uint(a.alpha), __float_as_uint(a.alpha));
     ec.beta2 = pack2(__float_as_uint(a.beta), __float_as_uint(a.beta));
     ec.gamma2 = pack2(__float_as_uint(a.gamma), __float_as_uint(a.gamma));
@@ -414,21 +499,30 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     for (int u = unit0; u < n_units; u += unit_step) {
       const int mtile = u % a.n_mtiles;
       const int chunk = u / a.n_mtiles;
-      const int t0 = chunk * a.tiles_per_chunk;
-      const int t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+      int t0, t1;
+      chunk_range(a, chunk, t0, t1);
       const int64_t p = ((int64_t)mtile * CG + rank) * kTileM + row;
       const bool prow = p < a.L;
       if (grp == 0) {
         // A row `row`: G[p, k] = 1 for k in orders[p, :n1] (canonical K-major
         // no-swizzle layout: 8x8 core matrices, LBO = 128 B, SBO = kpad*16 B)
-        uint8_t* rbase = a_mem + (row >> 3) * (a.kpad * 16) + (row & 7) * 16;
-        for (int kc = 0; kc < a.kpad / 8; ++kc)
+        // (core matrix = 8 rows x 16 bytes: 8 fp16 or 16 u8 K-elements)
+        // (int8: K runs over [h | l], A row = [255 G | G])
+        constexpr int EPC = 16 / ELT;  // K elements per core-matrix row
+        uint8_t* rbase = a_mem + (row >> 3) * (kext * 8 * ELT) + (row & 7) * 16;
+        for (int kc = 0; kc < kext / EPC; ++kc)
           *reinterpret_cast<uint4*>(rbase + kc * 128) = make_uint4(0, 0, 0, 0);
         if (prow) {
           const int16_t* ord = a.orders + p * a.n;
           for (int i = 0; i < a.n1; ++i) {
             const int k = ord[i];
-            *reinterpret_cast<uint16_t*>(rbase + (k >> 3) * 128 + (k & 7) * 2) = 0x3C00u;  // 1.0
+            if (I8) {
+              rbase[(k / EPC) * 128 + (k % EPC)] = 255u;
+              const int k2 = a.kpad + k;
+              rbase[(k2 / EPC) * 128 + (k2 % EPC)] = 1u;
+            } else {
+              *reinterpret_cast<uint16_t*>(rbase + (k / EPC) * 128 + (k % EPC) * 2) = 0x3C00u;
+            }
           }
         }
         fence_proxy_async_smem();
@@ -436,20 +530,34 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         else mbar_arrive(afull);
       }
       Top4 top;
-      top.reset(seed_key<TWO_SIDED>(a.best_t, p, prow));
+      top.reset(seed_key<TWO_SIDED>(a.best_t, p, prow, a, emax));
+      float kthr = sonly_thr(top.k3, ec);  // S-only hit threshold on S^2
       unsigned rare_groups = 0;
+      float* winv = inv_smem + ew * (COLGROUPS * 32);  // this warp's columns
       for (int i = 0; i < t1 - t0; ++i) {
         const int t = chunk_tile(a, t0, t1, i);
-        if (CG == 2) mbar_wait_cluster(&tfull[acc], acc_phase);
-        else mbar_wait(&tfull[acc], acc_phase);
+        if (I8) {  // stage the tile's scales for our columns; lands during the MMA wait
+          __syncwarp();
+          if (lane < COLGROUPS * 8)
+            cp_async16(winv + 4 * lane, a.inv_scale + (int64_t)t * TV + grp * COLGROUPS * 32 + 4 * lane);
+          cp_async_commit();
+        }
+        // (commit-multicast arrivals; CTA-scope acquire: no L1 invalidation)
+        mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const int64_t vleft = a.v - (int64_t)t * TV;
         const int valid = vleft < TV ? (int)vleft : TV;
+        if (I8) {
+          cp_async_wait_all();
+          __syncwarp();
+        }
 #pragma unroll 1
         for (int g = 0; g < COLGROUPS; ++g) {
           const int gc = (grp * COLGROUPS + g) * 32;
           const uint32_t taddr =
               tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * kTileN + gc);
+          const int jbase = t * TV + gc;
+          const float* ginv = winv + g * 32;
           uint32_t sv[32], qv[32];
           tmem_ld32(taddr, sv);
           if (SONLY) {
@@ -459,21 +567,47 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
             tmem_ld32(taddr + kTileV, qv);
           }
           tmem_ld_wait();
-          const int jbase = t * TV + gc;
           const int gvalid = valid - gc;
+          if (I8) {  // S_q -> S = S_q * inv (packed; scales: broadcast shared loads)
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 iv = reinterpret_cast<const float4*>(ginv)[c4];
+              const uint64_t s01 = mul2(pack2(__float_as_uint((float)(int)sv[4 * c4 + 0]),
+                                              __float_as_uint((float)(int)sv[4 * c4 + 1])),
+                                        pack2(__float_as_uint(iv.x), __float_as_uint(iv.y)));
+              const uint64_t s23 = mul2(pack2(__float_as_uint((float)(int)sv[4 * c4 + 2]),
+                                              __float_as_uint((float)(int)sv[4 * c4 + 3])),
+                                        pack2(__float_as_uint(iv.z), __float_as_uint(iv.w)));
+              sv[4 * c4 + 0] = (uint32_t)s01;
+              sv[4 * c4 + 1] = (uint32_t)(s01 >> 32);
+              sv[4 * c4 + 2] = (uint32_t)s23;
+              sv[4 * c4 + 3] = (uint32_t)(s23 >> 32);
+            }
+          }
           if (DEBUG) group_debug<TWO_SIDED>(sv, qv, jbase, gvalid, ec, p, prow, a);
           if (gvalid <= 0) continue;
-          uint32_t hits = group_hits<ALPHA0>(sv, qv, ec, top.k3);
-          if (gvalid < 32) hits &= (1u << gvalid) - 1u;
-          if (__any_sync(0xffffffffu, hits != 0u)) {
-            ++rare_groups;
-            group_rare<TWO_SIDED, SONLY>(hits, taddr, jbase, ec, top, p, prow, a);
+          if constexpr (SONLY) {
+            if (!__any_sync(0xffffffffu, sonly_any(sv, kthr))) continue;
+            uint32_t hits = sonly_mask(sv, kthr);
+            if (gvalid < 32) hits &= (1u << gvalid) - 1u;
+            if (__any_sync(0xffffffffu, hits != 0u)) {
+              ++rare_groups;
+              group_rare<TWO_SIDED, SONLY, I8>(hits, taddr, jbase, ec, top, p, prow, a, ginv);
+              kthr = sonly_thr(top.k3, ec);
+            }
+          } else {
+            uint32_t hits = group_hits<ALPHA0>(sv, qv, ec, top.k3);
+            if (gvalid < 32) hits &= (1u << gvalid) - 1u;
+            if (__any_sync(0xffffffffu, hits != 0u)) {
+              ++rare_groups;
+              group_rare<TWO_SIDED, SONLY, I8>(hits, taddr, jbase, ec, top, p, prow, a, ginv);
+            }
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // accumulator drained
-          if (CG == 2) mbar_arrive_cluster(&tempty[acc], 0);
+          if (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
           else mbar_arrive(&tempty[acc]);
         }
         if (++acc == kNumAcc) {
@@ -520,18 +654,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-size_t smem_bytes_for(int cg, int bk, int stages, int kpad) {
-  const size_t stage = (size_t)2 * (kTileN / cg) * bk * 2;
-  size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024;
+size_t smem_bytes_for(int cg, int bk, int stages, int kpad, bool i8) {
+  // fp16: hi + lo boxes of bk halves; i8: one box of bk bytes of [h | l].
+  // The A tile is kTileM x kpad halves or kTileM x 2 kpad bytes: same size.
+  const size_t stage = i8 ? (size_t)(kTileN / cg) * bk : (size_t)2 * (kTileN / cg) * bk * 2;
+  size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024 + (i8 ? kInvStage : 0);
   // one CTA per SM: TMEM (512 columns) is allocated whole by each CTA
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
 
-template <int CG, int BK, int STAGES, int EPI, bool TS, bool A0, bool DBG>
+template <int CG, int BK, int STAGES, int EPI, bool TS, bool A0, bool DBG, bool I8 = false>
 cudaError_t launch_cfg_e(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                          cudaStream_t s) {
-  auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG>;
-  const size_t smem = smem_bytes_for(CG, BK, STAGES, lay.kpad);
+  auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG, I8>;
+  const size_t smem = smem_bytes_for(CG, BK, STAGES, lay.kpad, I8);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -576,9 +712,30 @@ cudaError_t dispatch(const NaiveLayout& lay, const TfillArgs& a, const CUtensorM
   return launch_cfg<1, 32, 3, TS, A0, DBG>(lay, a, map, s);
 }
 
+// integer tiles (balanced groups only): bk = 128 bytes (128B swizzle)
+template <int CG, int STAGES, bool TS, bool DBG>
+cudaError_t launch_i8(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                      cudaStream_t s) {
+  if constexpr (CG == 1 && !DBG) {
+    if (lay.groups == 4) return launch_cfg_e<CG, 128, STAGES, 16, TS, true, DBG, true>(lay, a, map, s);
+  }
+  return launch_cfg_e<CG, 128, STAGES, 8, TS, true, DBG, true>(lay, a, map, s);
+}
+template <bool TS, bool DBG>
+cudaError_t dispatch_i8(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                        cudaStream_t s) {
+  if (lay.cg == 2) {
+    if (lay.stages >= 7) return launch_i8<2, 7, TS, DBG>(lay, a, map, s);
+    return launch_i8<2, 4, TS, DBG>(lay, a, map, s);
+  }
+  if (lay.stages >= 4) return launch_i8<1, 4, TS, DBG>(lay, a, map, s);
+  return launch_i8<1, 3, TS, DBG>(lay, a, map, s);
+}
+
 template <bool TS>
 cudaError_t dispatch_a(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                        cudaStream_t s) {
+  if (lay.i8) return a.dbg_t ? dispatch_i8<TS, true>(lay, a, map, s) : dispatch_i8<TS, false>(lay, a, map, s);
   const bool a0 = a.alpha == 0.0f;
   if (a.dbg_t) return a0 ? dispatch<TS, true, true>(lay, a, map, s)
                          : dispatch<TS, false, true>(lay, a, map, s);
@@ -602,9 +759,28 @@ bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad
   return r == CUDA_SUCCESS;
 }
 
+bool make_planes8_map(CUtensorMap* map, const uint8_t* planes, int64_t v, int kpad, int cg) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  // rows [h | l] of 2 kpad bytes per voxel; box = 128 K-bytes x 256 / cg voxels
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * kpad), (cuuint64_t)v, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)(2 * kpad), (cuuint64_t)v * 2 * kpad};
+  cuuint32_t box[3] = {128u, (cuuint32_t)(2 * kTileV / cg), 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(planes), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s) {
   CUtensorMap map;
+  if (lay.i8) {
+    if (!make_planes8_map(&map, reinterpret_cast<const uint8_t*>(planes), a.v, lay.kpad, lay.cg))
+      return cudaErrorInvalidValue;
+    return two_sided ? dispatch_a<true>(lay, a, map, s) : dispatch_a<false>(lay, a, map, s);
+  }
   // box rows per TMA: S-only tiles load 256 (cg 1) or 128 (cg 2) voxels of one
   // plane; (S | Q) tiles load 128 voxels of 2 (cg 1) or 1 (cg 2) planes
   const bool sonly = a.alpha == 0.0f;
@@ -615,8 +791,8 @@ cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __
   return two_sided ? dispatch_a<true>(lay, a, map, s) : dispatch_a<false>(lay, a, map, s);
 }
 
-size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad) {
-  return smem_bytes_for(cg, bk, stages, kpad);
+size_t tfill_smem_bytes(int cg, int bk, int stages, int kpad, bool i8) {
+  return smem_bytes_for(cg, bk, stages, kpad, i8);
 }
 
 }  // namespace rmx

@@ -32,8 +32,18 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["i8", "f16"])
+def k1_mode(request, monkeypatch):
+    """Balanced designs run the int8 tensor-core path by default; RMX_I8=0
+    selects the fp16 hi/lo path.  Both must give bit-identical maxima."""
+    monkeypatch.setenv("RMX_I8", "1" if request.param == "i8" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("v,n1,n2,L,two_sided,seed", CASES)
-def test_maxima_bit_exact_vs_oracle(oracle_mod, v, n1, n2, L, two_sided, seed):
+def test_maxima_bit_exact_vs_oracle(oracle_mod, k1_mode, v, n1, n2, L, two_sided, seed):
+    if k1_mode == "f16" and n1 != n2:
+        pytest.skip("unbalanced designs have one path")
     x = _data(v, n1, n2, seed)
     plan = rmx.PermutationPlan(seed + 100, L, n1 + n2)
     res = rmx.run_naive_ex(x, plan, two_sided=two_sided)
@@ -43,8 +53,10 @@ def test_maxima_bit_exact_vs_oracle(oracle_mod, v, n1, n2, L, two_sided, seed):
     assert np.array_equal(res.argmax, am)
 
 
-def test_tensor_core_error_bound(oracle_mod):
-    """|t~ - t| of the fused tcgen05 epilogue, before fp64 refinement."""
+def test_tensor_core_error_bound(oracle_mod, k1_mode):
+    """|t~ - t| of the fused tcgen05 epilogue, before fp64 refinement.  fp16
+    hi/lo: < 1e-5 relative; int8 on 16-bit fixed-point z: bounded by the
+    quantisation (the refinement band is derived from the measured bound)."""
     import torch
 
     from paper_1703_01506_b200.naive_engine import NaiveJob, cuda_device, upload
@@ -61,7 +73,8 @@ def test_tensor_core_error_bound(oracle_mod):
                                            materialize=True)
         err = np.abs(t_dbg - T.T) / np.maximum(np.abs(T.T), 1.0)
         assert np.isfinite(t_dbg).all()
-        assert err.max() < 1e-5, (v, n1, n2, err.max())
+        bound = 1e-3 if (k1_mode == "i8" and n1 == n2) else 1e-5
+        assert err.max() < bound, (v, n1, n2, err.max())
         torch.cuda.synchronize()
 
 
@@ -137,3 +150,23 @@ def test_c1_full_config_bit_exact(oracle_mod):
                                          cfg.two_sided, threads=8)
     assert np.array_equal(res.maxima, mx)
     assert np.array_equal(res.argmax, am)
+
+
+def test_i8_near_ties_and_outliers_bit_exact(oracle_mod, k1_mode):
+    """Coarse quantisation (one huge subject per voxel) and clusters of
+    near-identical voxels: many candidates inside the band, overflow to the
+    exhaustive path; maxima must stay bit-identical."""
+    g = np.random.default_rng(77)
+    base = g.standard_normal((64, 60))
+    vals = np.repeat(base, 40, axis=0) + g.standard_normal((64 * 40, 60)) * 1e-7
+    vals[::7, 5] += 40.0  # outliers: large zmax -> coarse fixed point
+    x = rmx.DataMatrix(vals, 30, 30)
+    # 300 permutations: exhaustive fallback through X^T; 40: straight from X
+    for plan, two_sided in ((rmx.PermutationPlan(5, 300, 60), False),
+                            (rmx.PermutationPlan(6, 40, 60), True)):
+        res = rmx.run_naive_ex(x, plan, two_sided=two_sided)
+        mx, am, _ = oracle_mod.naive_maxnull(x.values, 30, plan_orders(plan).astype(np.int64),
+                                             two_sided, threads=8)
+        assert res.stats["overflow_perms"] > 0
+        assert np.array_equal(res.maxima, mx)
+        assert np.array_equal(res.argmax, am)
