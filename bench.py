@@ -269,25 +269,40 @@ def main():
 
     # ---------------- roofline of the dominant kernel (K1, tcgen05) ----------
     pk, pk_kind = peaks()
+    stats0 = sh.job.stats.as_dict() if sh.job else {}
+    i8 = bool(stats0.get("i8", 0))
     local_L = hi - lo
-    algo_flops = 4.0 * n * v * local_L  # n MACs for S1 + n for Q1 per T entry
+    algo_flops = 4.0 * n * v * local_L  # SURVEY 8d: n MACs for S1 + n for Q1 per T entry
     achieved = algo_flops / (tfill_avg / 1e3) / 1e12
-    peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")))
+    bf16_burst = float(pk.get("bf16_tflops", 0.0) or pk.get("bf16_tflops_sustained"))
+    bf16_sust = float(pk.get("bf16_tflops_sustained", bf16_burst))
     balanced = 2 * cfg.n1 == n
-    # executed tensor work per T entry: fp16 hi+lo split of Z (and Z^2 when
-    # the groups are unbalanced); balanced designs need S only (Q cancels)
-    exec_flops = (4.0 if balanced else 8.0) * n * v * local_L
+    if i8:
+        # u8 x s8 -> s32 MMA over K = 2 kpad (z = 255 h + l digit planes), S only;
+        # B200 dense int8 = 2x dense bf16 (4.5 vs 2.25 P nominal); MEASURED_PEAKS
+        # has no int8 entry, so the peak is 2x its measured bf16 figure
+        kpad = -(-n // 32) * 32
+        exec_flops = 2.0 * (2 * kpad) * v * local_L
+        peak, peak_sust = 2.0 * bf16_burst, 2.0 * bf16_sust
+        peak_kind = f"{pk_kind} bf16 dense burst x 2 (int8 dense)"
+        note = ("n1 == n2: t depends on S = G.Z only; K1 runs it as an exact int8 GEMM "
+                "(2 digit planes: 2 kpad int8 MACs per entry = 4 kpad ops ~ the algorithmic 4n)")
+    else:
+        kpad = -(-n // 16) * 16
+        exec_flops = (4.0 if balanced else 8.0) * kpad * v * local_L
+        peak, peak_sust = bf16_burst, bf16_sust
+        peak_kind = f"{pk_kind} bf16 dense burst"
+        note = ("n1 == n2: S = G.Z only, fp16 hi+lo split: 4 kpad flop per entry"
+                if balanced else "S and Q, fp16 hi+lo split: 8 kpad flop per entry")
+    exec_rate = exec_flops / (tfill_avg / 1e3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
                 "kernel": "k_tfill_tc (K1)", "algorithmic_flops_per_launch": algo_flops,
                 "algorithmic_unit": "4n flop per T entry (SURVEY 8d: n MACs for S + n for Q)",
-                "kernel_ms": tfill_avg, "peak_kind": f"{pk_kind} bf16 dense sustained",
-                "frac_of_burst": achieved / float(pk.get("bf16_tflops", peak)),
-                "executed_tensor_tflops": exec_flops / (tfill_avg / 1e3) / 1e12,
-                "executed_frac": exec_flops / (tfill_avg / 1e3) / 1e12 / peak,
-                "note": ("n1 == n2: the pooled variance does not depend on Q, so K1 executes "
-                         "S = G.Z only (fp16 hi+lo: 4n flop per entry = the algorithmic count)"
-                         if balanced else "S and Q, fp16 hi+lo split: 8n flop per entry")}
+                "kernel_ms": tfill_avg, "peak_kind": peak_kind,
+                "frac_of_sustained": achieved / peak_sust,
+                "executed_tensor_tflops": exec_rate, "executed_frac": exec_rate / peak,
+                "tensor_path": "int8" if i8 else "fp16x2", "note": note}
 
     # ---------------- e2e through the public API from host buffers -----------
     e2e = None
@@ -345,13 +360,17 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f16x2-split tensor (fp32 acc) + f64 refine",
+            "dtype": ("u8 x s8 -> s32 tensor (fixed-point z, exact) + f64 refine" if i8
+                      else "f16x2-split tensor (fp32 acc) + f64 refine"),
             "data": "synthetic (seeded smoothed Gaussian fields, BASELINE.json design)",
             "config": dict(config_out, l2="flushed between steps" if l2_flush is not None
                            else "inputs > L2 (X 8 B x v x n + fp16 planes)"),
             "clocks": clk.summary(),
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps,
+            # per step: K0 prep, const-reduce, K1, K2 refine; the exhaustive
+            # fallback (overflow) adds exact-rows + reduce (+ transpose > 64 perms)
+            "gpu_launches": args.steps * (4 + (2 + (stats0.get("overflow_perms", 0) > 64)
+                                                if stats0.get("overflow_perms", 0) else 0)),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "phases_ms": {"prepare": sum(prep_ms) / len(prep_ms), "tfill": tfill_avg,

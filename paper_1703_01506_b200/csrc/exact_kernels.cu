@@ -52,33 +52,69 @@ __device__ __forceinline__ void note_degenerate(NaiveCounters* c, int64_t perm, 
 }
 
 // ---------------------------------------------------------------- K0
-// One warp per voxel row: fp64 mean / sd, z = (x - mean) / sd, q = z^2,
-// each split into fp16 hi + lo.  Rows constant across all subjects get z = 0
-// (tensor-core t~ = 0) and, if numpy's rounding makes their exact statistic
-// non-zero, are listed for k_const_reduce.
-__global__ void k_prep(PrepArgs a) {
+// One warp per voxel row: fp64 mean / sd, z = (x - mean) / sd, then either
+// the fp16 hi + lo planes of z (and q = z^2) or the int8 digit planes.  R > 0:
+// the row is held in registers (R values per lane, n <= 32 R), so X is read
+// once with all loads in flight; R = 0: generic re-reading loop.  Rows
+// constant across all subjects get z = 0 (tensor-core t~ = 0) and, if numpy's
+// rounding makes their exact statistic non-zero, are listed for
+// k_const_reduce.
+template <int R>
+__global__ void __launch_bounds__(256, 2) k_prep(PrepArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   const int64_t plane = a.v * (int64_t)a.kpad;
+  double err_max = 0.0;  // int8: max over this warp's voxels of the quantisation bound
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < a.v;
        j += warps) {
     const double* row = a.x + j * a.n;
-    double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
-    for (int k = lane; k < a.n; k += 32) {
-      const double xv = row[k];
-      s += xv;
-      mn = fmin(mn, xv);
-      mx = fmax(mx, xv);
+    double xr[R > 0 ? R : 1];
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = lane + 32 * r;
+        xr[r] = k < a.n ? __ldg(row + k) : 0.0;
+      }
     }
+    // f(k, x) over this lane's subjects k < n
+    auto each = [&](auto&& f) {
+      if constexpr (R > 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = lane + 32 * r;
+          if (k < a.n) f(k, xr[r]);
+        }
+      } else {
+        for (int k = lane; k < a.n; k += 32) f(k, row[k]);
+      }
+    };
+    // f(k, x) over this lane's padded columns k < kpad (x = 0 past n); kpad <= 32 R
+    auto each_pad = [&](auto&& f) {
+      if constexpr (R > 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = lane + 32 * r;
+          if (k < a.kpad) f(k, xr[r]);
+        }
+      } else {
+        for (int k = lane; k < a.kpad; k += 32) f(k, k < a.n ? row[k] : 0.0);
+      }
+    };
+    double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+    each([&](int, double x) {
+      s += x;
+      mn = fmin(mn, x);
+      mx = fmax(mx, x);
+    });
     s = warp_sum_d(s);
     mn = warp_min_d(mn);
     mx = warp_max_d(mx);
     const double mean = s / a.n;
     double ss = 0.0;
-    for (int k = lane; k < a.n; k += 32) {
-      const double d = row[k] - mean;
+    each([&](int, double x) {
+      const double d = x - mean;
       ss += d * d;
-    }
+    });
     ss = warp_sum_d(ss);
     const bool constant = (mn == mx);
     const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
@@ -86,34 +122,30 @@ __global__ void k_prep(PrepArgs a) {
       // int8 path: zq = rint(z * scale) in [-32512, 32512], zq = 255 h + l with
       // h, l in [-127, 127]; row j of planes8 = [h_0 .. h_kpad-1 | l_0 .. l_kpad-1]
       double zmax = 0.0;
-      for (int k = lane; k < a.n; k += 32) zmax = fmax(zmax, fabs((row[k] - mean) * inv));
+      each([&](int, double x) { zmax = fmax(zmax, fabs((x - mean) * inv)); });
       zmax = warp_max_d(zmax);
       const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
       const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
       int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
       double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
-      for (int k = lane; k < a.kpad; k += 32) {
+      each_pad([&](int k, double x) {
         int zq = 0;  // padded subjects and constant voxels: 0
         if (k < a.n && !constant) {
-          const double z = (row[k] - mean) * inv;
+          const double z = (x - mean) * inv;
           zq = min(32512, max(-32512, (int)rint(z * scale)));
           err += fabs(z - (double)zq * (double)inv_f);
         }
-        const int h = (int)rint(zq / 255.0);
+        const int h = zq >= 0 ? (zq + 127) / 255 : -((127 - zq) / 255);  // round(zq / 255)
         p8[k] = (int8_t)h;
         p8[a.kpad + k] = (int8_t)(zq - 255 * h);
-      }
+      });
       err = warp_sum_d(err);
-      if (lane == 0) {
-        a.inv_scale[j] = inv_f;
-        // rounded up; non-negative floats order like their bit patterns
-        atomicMax(&a.counters->emax_bits, __float_as_uint((float)(err * (1.0 + 1e-6)) + 1e-30f));
-      }
+      err_max = fmax(err_max, err);
+      if (lane == 0) a.inv_scale[j] = inv_f;
     } else {
       __half* zh = a.planes + j * a.kpad;
-      for (int k = lane; k < a.kpad; k += 32) {
-        double z = 0.0;
-        if (k < a.n && !constant) z = (row[k] - mean) * inv;
+      each_pad([&](int k, double x) {
+        const double z = (k < a.n && !constant) ? (x - mean) * inv : 0.0;
         const __half h_z = __double2half(z);
         zh[k] = h_z;
         zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
@@ -123,7 +155,7 @@ __global__ void k_prep(PrepArgs a) {
           zh[plane + k] = h_q;
           zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
         }
-      }
+      });
     }
     if (constant && lane == 0) {
       const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
@@ -133,6 +165,9 @@ __global__ void k_prep(PrepArgs a) {
       }
     }
   }
+  if (a.planes8 && lane == 0 && err_max > 0.0)
+    // rounded up; non-negative floats order like their bit patterns
+    atomicMax(&a.counters->emax_bits, __float_as_uint((float)(err_max * (1.0 + 1e-6)) + 1e-30f));
 }
 
 __global__ void k_const_reduce(const double* x, int n, int n1, const int32_t* cvox,
@@ -199,13 +234,23 @@ __global__ void k_const_reduce(const double* x, int n, int n1, const int32_t* cv
 // 4th-best is inside the band might hide a fifth in-band voxel: the
 // permutation is then queued for the exhaustive exact path.
 constexpr int kRefineWarps = 8;
+constexpr int kStageMaxN = 2048;  // rows up to this many subjects are staged in smem
 
+// Evaluating one candidate: the warp copies the voxel's row into its smem
+// buffer (coalesced), then evaluates the reference arithmetic with the
+// numpy-pairwise chains spread over its lanes (welch_exact_warp: same bits);
+// the owning lane keeps the result.
+template <bool STAGE>
 __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
-  extern __shared__ int16_t ord_s[];
+  extern __shared__ __align__(16) unsigned char refine_smem[];
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  NpWarpScratch* sc = reinterpret_cast<NpWarpScratch*>(refine_smem) + w;
+  unsigned char* rest = refine_smem + kRefineWarps * sizeof(NpWarpScratch);
+  double* rowbuf = reinterpret_cast<double*>(rest) + (size_t)w * (STAGE ? a.n : 0);
+  int16_t* ord = reinterpret_cast<int16_t*>(rest + (STAGE ? (size_t)kRefineWarps * a.n * 8 : 0)) +
+                 (size_t)w * a.n;
   const int64_t p = (int64_t)blockIdx.x * kRefineWarps + w;
   if (p >= a.L) return;
-  int16_t* ord = ord_s + w * a.n;
   for (int i = lane; i < a.n; i += 32) ord[i] = a.orders[p * a.n + i];
   __syncwarp();
   const int n2 = a.n - a.n1;
@@ -225,35 +270,63 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
   int bj = -1;
   bool overflow = false;
   unsigned nref = 0;
-  auto consider = [&](int j) {
-    const WelchExact r = welch_exact(a.x + (int64_t)j * a.n, 1, ord, a.n1, n2);
-    ++nref;
-    if (r.degenerate) {
-      note_degenerate(a.counters, p, j);
-      return;
+  // warp-collective: evaluate voxel j for the lane `owner`
+  auto eval = [&](int j, int owner) {
+    const double* row = a.x + (int64_t)j * a.n;
+    if (STAGE) {
+      __syncwarp();
+      for (int i = lane; i < a.n; i += 32) rowbuf[i] = row[i];
+      __syncwarp();
+      row = rowbuf;
     }
-    const double key = a.two_sided ? fabs(r.t) : r.t;
-    if (key > best || (key == best && (bj < 0 || j < bj))) {
-      best = key;
-      bj = j;
+    const WelchExact r = welch_exact_warp(row, 1, ord, a.n1, n2, sc);
+    if (lane == owner) {
+      ++nref;
+      if (r.degenerate) {
+        note_degenerate(a.counters, p, j);
+      } else {
+        const double key = a.two_sided ? fabs(r.t) : r.t;
+        if (key > best || (key == best && (bj < 0 || j < bj))) {
+          best = key;
+          bj = j;
+        }
+      }
+    }
+  };
+  auto eval_all = [&](int j) {  // each lane's j (< 0: none), one at a time
+    unsigned m = __ballot_sync(0xffffffffu, j >= 0);
+    while (m) {
+      const int owner = __ffs(m) - 1;
+      m &= m - 1;
+      eval(__shfl_sync(0xffffffffu, j, owner), owner);
     }
   };
   if (tmax > -FLT_MAX) {
-    for (int c = lane; c < a.slots; c += 32) {
-      const int4 e0 = cp[2 * c], e1 = cp[2 * c + 1];
-      if (e0.y >= 0 && __int_as_float(e0.x) >= lo) consider(e0.y);
-      if (e0.w >= 0 && __int_as_float(e0.z) >= lo) consider(e0.w);
-      if (e1.y >= 0 && __int_as_float(e1.x) >= lo) consider(e1.y);
-      if (e1.w >= 0 && __int_as_float(e1.z) >= lo) {
-        consider(e1.w);
-        overflow = true;  // a 5th in-band voxel of this chunk could be hiding
+    for (int c0 = 0; c0 < a.slots; c0 += 32) {
+      const int c = c0 + lane;
+      int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
+      if (c < a.slots) {
+        const int4 e0 = cp[2 * c], e1 = cp[2 * c + 1];
+        if (e0.y >= 0 && __int_as_float(e0.x) >= lo) j0 = e0.y;
+        if (e0.w >= 0 && __int_as_float(e0.z) >= lo) j1 = e0.w;
+        if (e1.y >= 0 && __int_as_float(e1.x) >= lo) j2 = e1.y;
+        if (e1.w >= 0 && __int_as_float(e1.z) >= lo) {
+          j3 = e1.w;
+          overflow = true;  // a 5th in-band voxel of this chunk could be hiding
+        }
       }
+      eval_all(j0);
+      eval_all(j1);
+      eval_all(j2);
+      eval_all(j3);
     }
   }
   const unsigned scount = a.counters->susp_count;
   if (scount > 0 && scount <= (unsigned)kSuspectCap) {
-    for (unsigned i = lane; i < scount; i += 32)
-      if (a.susp[2 * i] == (int)p) consider(a.susp[2 * i + 1]);
+    for (unsigned i0 = 0; i0 < scount; i0 += 32) {
+      const unsigned i = i0 + lane;
+      eval_all((i < scount && a.susp[2 * i] == (int)p) ? a.susp[2 * i + 1] : -1);
+    }
   }
   warp_argmax(best, bj);
   const unsigned any_over = __ballot_sync(0xffffffffu, overflow);
@@ -273,6 +346,58 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
     if (any_over || bj < 0) {
       unsigned slot = atomicAdd(&a.counters->overflow_count, 1u);
       a.overflow[slot] = (int32_t)p;
+    }
+  }
+}
+
+// Exhaustive exact statistic for a few permutations straight from X: one
+// warp per voxel stages the row in smem, the warp evaluates it (welch_exact_warp).
+// grid (nvb, nperm); per-block (max, argmax) partials as k_exact_rows.
+__global__ void __launch_bounds__(32 * kRefineWarps)
+    k_exact_rows_staged(const double* __restrict__ x, int64_t v, int n, int n1,
+                        const int16_t* __restrict__ orders, const int32_t* perm_list,
+                        int64_t perm_offset, int two_sided, double* part_val, int32_t* part_idx,
+                        NaiveCounters* counters) {
+  extern __shared__ __align__(16) unsigned char ex_smem[];
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  NpWarpScratch* sc = reinterpret_cast<NpWarpScratch*>(ex_smem) + w;
+  unsigned char* rest = ex_smem + kRefineWarps * sizeof(NpWarpScratch);
+  double* rowbuf = reinterpret_cast<double*>(rest) + (size_t)w * n;
+  int16_t* ord = reinterpret_cast<int16_t*>(rest + (size_t)kRefineWarps * n * 8);
+  const int64_t i = blockIdx.y;
+  const int64_t p = perm_list ? perm_list[i] : perm_offset + i;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) ord[k] = orders[p * n + k];
+  __syncthreads();
+  const int64_t per = (v + gridDim.x - 1) / gridDim.x;
+  const int64_t jlo = blockIdx.x * per, jhi = min(v, jlo + per);
+  double best = -DBL_MAX;
+  int bj = -1;
+  for (int64_t j = jlo + w; j < jhi; j += kRefineWarps) {
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) rowbuf[k] = x[j * n + k];
+    __syncwarp();
+    const WelchExact r = welch_exact_warp(rowbuf, 1, ord, n1, n - n1, sc);
+    if (lane == 0) {
+      if (r.degenerate) {
+        if (counters) note_degenerate(counters, p, j);
+      } else {
+        const double key = two_sided ? fabs(r.t) : r.t;
+        if (key > best || (key == best && (bj < 0 || j < bj))) best = key, bj = (int)j;
+      }
+    }
+  }
+  __shared__ double sv[32];
+  __shared__ int sj[32];
+  warp_argmax(best, bj);
+  if (lane == 0) sv[w] = best, sj[w] = bj;
+  __syncthreads();
+  if (w == 0) {
+    best = lane < kRefineWarps ? sv[lane] : -DBL_MAX;
+    bj = lane < kRefineWarps ? sj[lane] : -1;
+    warp_argmax(best, bj);
+    if (lane == 0) {
+      part_val[i * gridDim.x + blockIdx.x] = best;
+      part_idx[i * gridDim.x + blockIdx.x] = bj;
     }
   }
 }
@@ -382,7 +507,11 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t s) {
   const int wpb = 8;
   int64_t blocks = (a.v + wpb - 1) / wpb;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  k_prep<<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
+  // rows up to 32 R subjects are read once into registers
+  if (a.n <= 128) k_prep<4><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
+  else if (a.n <= 256) k_prep<8><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
+  else if (a.n <= 512) k_prep<16><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
+  else k_prep<0><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -394,8 +523,24 @@ cudaError_t launch_const_reduce(const double* x, int64_t, int n, int n1, const i
 
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.L + kRefineWarps - 1) / kRefineWarps;
-  const size_t smem = (size_t)kRefineWarps * a.n * sizeof(int16_t);
-  k_refine<<<(unsigned)blocks, 32 * kRefineWarps, smem, s>>>(a);
+  const size_t scratch = kRefineWarps * sizeof(NpWarpScratch);
+  if (a.n <= kStageMaxN) {
+    const size_t smem = scratch + (size_t)kRefineWarps * a.n * (sizeof(int16_t) + sizeof(double));
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_refine<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_refine<true><<<(unsigned)blocks, 32 * kRefineWarps, smem, s>>>(a);
+  } else {
+    const size_t smem = scratch + (size_t)kRefineWarps * a.n * sizeof(int16_t);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_refine<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_refine<false><<<(unsigned)blocks, 32 * kRefineWarps, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -410,6 +555,23 @@ cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1, const 
                              double* t_out, int64_t ld, double* part_val, int32_t* part_idx,
                              int nvb, NaiveCounters* counters, cudaStream_t s, bool transposed) {
   if (nperm <= 0) return cudaSuccess;
+  if (!transposed && n <= kStageMaxN && part_val && !t_out) {
+    const size_t smem = kRefineWarps * sizeof(NpWarpScratch) + (size_t)kRefineWarps * n * sizeof(double) +
+                        (size_t)n * sizeof(int16_t);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_exact_rows_staged,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    for (int64_t base = 0; base < nperm; base += 65535) {
+      const int64_t cnt = nperm - base < 65535 ? nperm - base : 65535;
+      dim3 grid((unsigned)nvb, (unsigned)cnt);
+      k_exact_rows_staged<<<grid, 32 * kRefineWarps, smem, s>>>(
+          xt, v, n, n1, orders, perm_list ? perm_list + base : nullptr, base, two_sided,
+          part_val + base * nvb, part_idx + base * nvb, counters);
+    }
+    return cudaGetLastError();
+  }
   auto kern = transposed ? k_exact_rows<true> : k_exact_rows<false>;
   for (int64_t base = 0; base < nperm; base += 65535) {
     const int64_t cnt = nperm - base < 65535 ? nperm - base : 65535;

@@ -150,4 +150,131 @@ __device__ __forceinline__ WelchExact welch_exact_const(double c, int n1, int n2
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-parallel evaluation with the same bits.  numpy's pairwise sum is a
+// fixed tree: leaves of <= 128 terms (split at n/2 - (n/2)%8), each leaf
+// eight interleaved sequential chains combined ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) plus a sequential tail.  Every chain and every tree node
+// is kept -- only the chains run on different lanes (8 lanes per leaf, 4
+// leaves per round), so the result is bit-identical to np_pw_sum.
+struct NpWarpScratch {  // per warp, in shared memory
+  static constexpr int kMaxLeaves = 64;
+  // every leaf of a split holds >= 57 terms, so groups of <= 57 * 64 terms fit
+  static constexpr int kMaxTerms = 3584;
+  int2 leaf[kMaxLeaves];                 // (lo, n) in tree order
+  double val[kMaxLeaves];
+};
+
+template <int D>
+struct NpLeaves {
+  __device__ __noinline__ static void list(int lo, int n, int& cnt, int2* out) {
+    if (n <= 128) {
+      out[cnt++] = make_int2(lo, n);
+      return;
+    }
+    int h = n / 2;
+    h -= h % 8;
+    NpLeaves<D - 1>::list(lo, h, cnt, out);
+    NpLeaves<D - 1>::list(lo + h, n - h, cnt, out);
+  }
+  __device__ __noinline__ static double combine(int n, int& idx, const double* val) {
+    if (n <= 128) return val[idx++];
+    int h = n / 2;
+    h -= h % 8;
+    const double left = NpLeaves<D - 1>::combine(h, idx, val);
+    const double right = NpLeaves<D - 1>::combine(n - h, idx, val);
+    return __dadd_rn(left, right);
+  }
+};
+template <>
+struct NpLeaves<0> {
+  __device__ __forceinline__ static void list(int lo, int n, int& cnt, int2* out) {
+    out[cnt++] = make_int2(lo, n);
+  }
+  __device__ __forceinline__ static double combine(int, int& idx, const double* val) {
+    return val[idx++];
+  }
+};
+
+// Sum of g(0..n) in numpy's order, computed by the whole warp (all 32 lanes
+// must call; every lane returns the sum).  n <= NpWarpScratch::kMaxTerms.
+template <class G>
+__device__ __forceinline__ double np_pw_sum_warp(const G& g, int n, NpWarpScratch* sc) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & 7;
+  int nleaves = 0;
+  if (lane == 0) NpLeaves<8>::list(0, n, nleaves, sc->leaf);
+  nleaves = __shfl_sync(0xffffffffu, nleaves, 0);
+  __syncwarp();
+  for (int base = 0; base < nleaves; base += 4) {
+    const int l = base + (lane >> 3);
+    const bool act = l < nleaves;
+    const int2 lf = act ? sc->leaf[l] : make_int2(0, 0);
+    const int lo = lf.x, m = lf.y;
+    double r = 0.0;
+    if (act && m >= 8) {
+      r = g(lo + sub);
+      const int stop = m - (m % 8);
+      for (int i = 8; i < stop; i += 8) r = __dadd_rn(r, g(lo + i + sub));
+    }
+    // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) within each 8-lane group
+    double t = __shfl_down_sync(0xffffffffu, r, 1);
+    r = __dadd_rn(r, t);  // even lanes: r_k + r_k+1
+    t = __shfl_down_sync(0xffffffffu, r, 2);
+    r = __dadd_rn(r, t);  // lanes % 4 == 0: (r0+r1)+(r2+r3)
+    t = __shfl_down_sync(0xffffffffu, r, 4);
+    r = __dadd_rn(r, t);  // lane % 8 == 0: the eight-chain sum
+    if (act && sub == 0) {
+      double res;
+      int i;
+      if (m < 8) {
+        res = 0.0;
+        i = 0;
+      } else {
+        res = r;
+        i = m - (m % 8);
+      }
+      for (; i < m; ++i) res = __dadd_rn(res, g(lo + i));
+      sc->val[l] = res;
+    }
+  }
+  __syncwarp();
+  int idx = 0;
+  const double total = NpLeaves<8>::combine(n, idx, sc->val);
+  __syncwarp();
+  return total;
+}
+
+// welch_exact with the warp: identical bits, every lane gets the result.
+// Larger groups fall back to lane 0 and a broadcast.
+__device__ __forceinline__ WelchExact welch_exact_warp(const double* row, int64_t stride,
+                                                       const int16_t* ord, int n1, int n2,
+                                                       NpWarpScratch* sc) {
+  if (n1 > NpWarpScratch::kMaxTerms || n2 > NpWarpScratch::kMaxTerms) {
+    WelchExact r{};
+    if ((threadIdx.x & 31) == 0) r = welch_exact(row, stride, ord, n1, n2);
+    r.t = __shfl_sync(0xffffffffu, r.t, 0);
+    r.num = __shfl_sync(0xffffffffu, r.num, 0);
+    r.degenerate = __shfl_sync(0xffffffffu, (int)r.degenerate, 0) != 0;
+    return r;
+  }
+  GroupVals a{row, ord, stride}, b{row, ord + n1, stride};
+  const double m1 = __ddiv_rn(np_pw_sum_warp(a, n1, sc), (double)n1);
+  const double m2 = __ddiv_rn(np_pw_sum_warp(b, n2, sc), (double)n2);
+  GroupSqDev da{row, ord, stride, m1}, db{row, ord + n1, stride, m2};
+  const double v1 = __ddiv_rn(np_pw_sum_warp(da, n1, sc), (double)(n1 - 1));
+  const double v2 = __ddiv_rn(np_pw_sum_warp(db, n2, sc), (double)(n2 - 1));
+  const double var_term = __dadd_rn(__ddiv_rn(v1, (double)n1), __ddiv_rn(v2, (double)n2));
+  WelchExact r;
+  r.num = __dsub_rn(m1, m2);
+  if (var_term == 0.0) {
+    r.t = 0.0;
+    r.degenerate = (r.num != 0.0);
+  } else {
+    r.t = __ddiv_rn(r.num, __dsqrt_rn(var_term));
+    r.degenerate = false;
+  }
+  return r;
+}
+
 }  // namespace rmx

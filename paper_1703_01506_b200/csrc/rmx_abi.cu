@@ -158,11 +158,14 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   const int tile_perms = kTileM * lay.cg;
   lay.n_mtiles = (int)((L + tile_perms - 1) / tile_perms);
   const int n_clusters = std::max(1, sm_count / lay.cg);
-  // epilogue-bound when the K loop is short: 8 epilogue warps (2 per quadrant)
-  // epilogue warps per TMEM lane quadrant: 4 for short-K single-CTA tiles
-  // (latency-bound epilogue), else 2
-  lay.groups = (lay.cg == 1 && lay.kpad <= 128 && balanced) ? 4 : 2;
-  if (const char* g = getenv("RMX_EPI_GROUPS")) lay.groups = atoi(g) == 4 ? 4 : 2;
+  // Epilogue warps per TMEM lane quadrant: 4 (16 warps) where the epilogue
+  // must keep up with a fast MMA -- short-K single-CTA S-only tiles and int8
+  // tiles (twice the MMA rate) -- else 2.  16-warp variants are instantiated
+  // for S-only tiles with cg = 1 or int8 only.
+  const bool can16 = balanced && (lay.cg == 1 || lay.i8);
+  lay.groups = (can16 && (lay.kpad <= 128 || lay.i8)) ? 4 : 2;
+  if (const char* g = getenv("RMX_EPI_GROUPS"))
+    if (can16) lay.groups = atoi(g) == 4 ? 4 : 2;
   // Voxel chunks per permutation tile: minimise the static round-robin
   // makespan over `sm_count` persistent CTAs (unit = one tile of 128 perms x
   // one chunk of voxel tiles; A-tile rebuild counted as ~1/4 tile).
@@ -274,7 +277,7 @@ int run_exhaustive(const double* x, int64_t v, int32_t n, int32_t n1, const int1
   // voxel stripes per permutation: enough blocks to fill the GPU even when
   // only a few permutations overflowed (one thread per voxel)
   int64_t nvb64 = std::min<int64_t>(std::max<int64_t>(1, (v + 4095) / 4096), 64);
-  const int64_t fill = (4 * (int64_t)device_sm_count() + nperm - 1) / nperm;
+  const int64_t fill = (16 * (int64_t)device_sm_count() + nperm - 1) / nperm;
   nvb64 = std::max(nvb64, std::min(fill, (v + 255) / 256));
   const int nvb = (int)std::min<int64_t>(nvb64, 65535);
   // few permutations (the usual overflow case): read X rows directly; many:

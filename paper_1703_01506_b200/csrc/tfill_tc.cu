@@ -716,7 +716,7 @@ cudaError_t dispatch(const NaiveLayout& lay, const TfillArgs& a, const CUtensorM
 template <int CG, int STAGES, bool TS, bool DBG>
 cudaError_t launch_i8(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                       cudaStream_t s) {
-  if constexpr (CG == 1 && !DBG) {
+  if constexpr (!DBG) {
     if (lay.groups == 4) return launch_cfg_e<CG, 128, STAGES, 16, TS, true, DBG, true>(lay, a, map, s);
   }
   return launch_cfg_e<CG, 128, STAGES, 8, TS, true, DBG, true>(lay, a, map, s);
