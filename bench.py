@@ -295,8 +295,22 @@ def main():
         note = ("n1 == n2: S = G.Z only, fp16 hi+lo split: 4 kpad flop per entry"
                 if balanced else "S and Q, fp16 hi+lo split: 8 kpad flop per entry")
     exec_rate = exec_flops / (tfill_avg / 1e3) / 1e12
+    # dram bytes of the same launch from the committed ncu capture (same
+    # config, same tensor path); None when there is no capture for it
+    traffic, traffic_src = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                         f"r01_k1_traffic_{cfg.name}.json")
+    if world == 1 and os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath)).get("int8" if i8 else "fp16x2")
+            if tj:
+                traffic = float(tj["dram_bytes_read"] + tj["dram_bytes_write"])
+                traffic_src = os.path.relpath(tpath, os.path.dirname(os.path.abspath(__file__)))
+        except Exception:
+            traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
+                "traffic_source": traffic_src,
                 "kernel": "k_tfill_tc (K1)", "algorithmic_flops_per_launch": algo_flops,
                 "algorithmic_unit": "4n flop per T entry (SURVEY 8d: n MACs for S + n for Q)",
                 "kernel_ms": tfill_avg, "peak_kind": peak_kind,

@@ -120,6 +120,21 @@ int rmx_naive_tfill_debug(int64_t v, int32_t n, int32_t n1, const int16_t *order
                           int64_t L, int32_t two_sided, float *t_dbg, void *workspace,
                           size_t workspace_bytes, void *stream, rmx_status *st);
 
+/* NaivePT from HOST buffers (the reference-facing call: DataMatrix.values
+ * and the plan's label matrix live in host memory): copies X (v x n fp64) and
+ * the labels into the caller's device buffers, overlapping the X upload with
+ * K0/K1 chunk by chunk, runs the engine and copies max/argmax back into
+ * max_host/argmax_host.  Synchronous.  Results and errors as
+ * rmx_naive_maxnull.  Host buffers should be page-locked (cudaHostRegister)
+ * for the overlap; pageable buffers work but serialise the copies.
+ * Replaces reference naive.py:60-109 run_naive end to end. */
+int rmx_naive_maxnull_host(const double *x_host, int64_t v, int32_t n, int32_t n1,
+                           const int16_t *orders_host, int64_t L, int32_t two_sided,
+                           double *max_host, int32_t *argmax_host, double *x_dev,
+                           int16_t *orders_dev, double *max_dev, int32_t *argmax_dev,
+                           void *workspace, size_t workspace_bytes, void *stream,
+                           rmx_status *st, rmx_naive_stats *stats);
+
 /* ---------------------------------------------------------------- exact fp64
  * Bit-exact statistic matrix (reference _welch_rows arithmetic):
  *   t_out[p * ld + j] = t(perm p, voxel j), p < L, j < v  (perm-major; the

@@ -63,6 +63,7 @@ EXPORTS = (
     "rmx_device_check",
     "rmx_naive_workspace_bytes",
     "rmx_naive_maxnull",
+    "rmx_naive_maxnull_host",
     "rmx_naive_prepare",
     "rmx_naive_tfill",
     "rmx_naive_finish",
@@ -101,6 +102,8 @@ _SIGS = {
     "rmx_naive_workspace_bytes": ([_i64, _i32, _i64], _sz),
     "rmx_naive_maxnull": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
                           ctypes.c_int),
+    "rmx_naive_maxnull_host": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
+                                _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
     "rmx_naive_prepare": ([_vp, _i64, _i32, _i32, _i64, _vp, _sz, _vp, _SP], ctypes.c_int),
     "rmx_naive_tfill": ([_i64, _i32, _i32, _vp, _i64, _i32, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
     "rmx_naive_finish": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],

@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(256, 2) k_prep(PrepArgs a) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   const int64_t plane = a.v * (int64_t)a.kpad;
   double err_max = 0.0;  // int8: max over this warp's voxels of the quantisation bound
-  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < a.v;
-       j += warps) {
+  const int64_t jend = a.v_end > 0 ? a.v_end : a.v;
+  for (int64_t j = a.v_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+       j < jend; j += warps) {
     const double* row = a.x + j * a.n;
     double xr[R > 0 ? R : 1];
     if constexpr (R > 0) {
@@ -505,7 +506,9 @@ __global__ void k_pairs(const double* x, int64_t v, int n, int n1, const int16_t
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t s) {
   const int wpb = 8;
-  int64_t blocks = (a.v + wpb - 1) / wpb;
+  const int64_t rows = (a.v_end > 0 ? a.v_end : a.v) - a.v_begin;
+  if (rows <= 0) return cudaSuccess;
+  int64_t blocks = (rows + wpb - 1) / wpb;
   if (blocks > 148 * 64) blocks = 148 * 64;
   // rows up to 32 R subjects are read once into registers
   if (a.n <= 128) k_prep<4><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);

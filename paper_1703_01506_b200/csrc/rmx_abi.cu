@@ -354,32 +354,39 @@ size_t rmx_naive_workspace_bytes(int64_t v, int32_t n, int64_t L) {
   return std::max(naive_layout(v, n, n / 2, L, sm).total, naive_layout(v, n, 2, L, sm).total);
 }
 
-int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t L,
-                      void* workspace, size_t workspace_bytes, void* stream, rmx_status* st) {
-  clear_status(st);
-  if (int rc = check_dims(v, n, n1, L, st)) return rc;
-  Ws ws;
-  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+
+// K0 pieces: counters reset, rows [v0, v1), constant-voxel reduction
+int prep_init(const Ws& ws, int64_t L, cudaStream_t s, rmx_status* st) {
   RMX_CUDA(cudaMemsetAsync(ws.counters(), 0, sizeof(NaiveCounters), s));
   RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
   RMX_CUDA(cudaMemsetAsync(ws.best(), 0, (size_t)L * 4, s));
+  // int8 scale padding (voxels past v) must be finite: those columns are masked
+  if (ws.lay.i8)
+    RMX_CUDA(cudaMemsetAsync(ws.scale(), 0, (size_t)ws.lay.n_vtiles * ws.lay.vt * 4, s));
+  return RMX_OK;
+}
+
+int prep_rows(const double* x, int64_t v, int32_t n, int32_t n1, const Ws& ws, int64_t v0,
+              int64_t v1, cudaStream_t s, rmx_status* st) {
   PrepArgs pa{x, v, n, n1, ws.lay.kpad, ws.planes(), ws.cvox(), ws.counters()};
   if (ws.lay.i8) {
     pa.planes8 = ws.planes8();
     pa.inv_scale = ws.scale();
-    // scale padding (voxels past v) must be finite: those columns are masked
-    RMX_CUDA(cudaMemsetAsync(ws.scale(), 0, (size_t)ws.lay.n_vtiles * ws.lay.vt * 4, s));
   }
   pa.zplanes_only = (2 * n1 == n) ? 1 : 0;
+  pa.v_begin = v0;
+  pa.v_end = v1;
   RMX_CUDA(launch_prep(pa, s));
-  RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
   return RMX_OK;
 }
 
-static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
-                      int32_t two_sided, float* dbg, void* workspace, size_t workspace_bytes,
-                      void* stream, rmx_status* st, rmx_naive_stats* stats) {
+int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
+               int32_t two_sided, float* dbg, void* workspace, size_t workspace_bytes,
+               void* stream, rmx_status* st, rmx_naive_stats* stats, int chunk_begin = 0,
+               int chunk_end = -1) {
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
   Ws ws;
@@ -410,6 +417,8 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
   a.tiles_per_chunk = ws.lay.tiles_per_chunk;
   a.stride_full = golden_stride(ws.lay.tiles_per_chunk);
   a.stride_last = golden_stride(ws.lay.n_vtiles - (ws.lay.n_chunks - 1) * ws.lay.tiles_per_chunk);
+  a.chunk_begin = chunk_begin;
+  a.chunk_end = chunk_end < 0 ? ws.lay.n_chunks : chunk_end;
   a.alpha = (float)alpha;
   a.beta = (float)beta;
   a.gamma = (float)gamma;
@@ -431,6 +440,23 @@ static int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, i
     stats->cg = ws.lay.cg;
     stats->i8 = ws.lay.i8;
   }
+  return RMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t L,
+                      void* workspace, size_t workspace_bytes, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  Ws ws;
+  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int rc = prep_init(ws, L, s, st)) return rc;
+  if (int rc = prep_rows(x, v, n, n1, ws, 0, v, s, st)) return rc;
+  RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
   return RMX_OK;
 }
 
@@ -547,6 +573,109 @@ int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const i
     return rc;
   return rmx_naive_finish(x, v, n, n1, orders, L, two_sided, max_out, argmax_out, workspace,
                           workspace_bytes, stream, st, stats);
+}
+
+// Host buffers in, host results out, with the 8 B/entry upload of X overlapped
+// with the engine: X is copied chunk by chunk (K1's voxel chunks) on a copy
+// stream; K0 standardises each chunk as it lands and K1 runs that chunk's
+// units on alternating streams (so one launch's tail overlaps the next's
+// head).  The int8 quantisation bound is a running max over the chunks K0
+// has finished, which is all K1 needs for chunk c.
+int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n1,
+                           const int16_t* orders_host, int64_t L, int32_t two_sided,
+                           double* max_host, int32_t* argmax_host, double* x_dev,
+                           int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
+                           void* workspace, size_t workspace_bytes, void* stream,
+                           rmx_status* st, rmx_naive_stats* stats) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  if (!x_host || !orders_host || !max_host || !argmax_host || !x_dev || !orders_dev || !max_dev ||
+      !argmax_dev)
+    return set_status(st, RMX_E_USAGE, "null buffer");
+  Ws ws;
+  if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t xbytes = (size_t)v * n * sizeof(double);
+  const size_t obytes = (size_t)L * n * sizeof(int16_t);
+  auto finish_host = [&]() -> int {
+    RMX_CUDA(cudaMemcpyAsync(max_host, max_dev, (size_t)L * 8, cudaMemcpyDeviceToHost, s));
+    RMX_CUDA(cudaMemcpyAsync(argmax_host, argmax_dev, (size_t)L * 4, cudaMemcpyDeviceToHost, s));
+    RMX_CUDA(cudaStreamSynchronize(s));
+    return RMX_OK;
+  };
+  if (ws.lay.stages == 0) {  // exhaustive exact path: nothing to overlap
+    RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
+    RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
+    if (int rc = rmx_naive_maxnull(x_dev, v, n, n1, orders_dev, L, two_sided, max_dev, argmax_dev,
+                                   workspace, workspace_bytes, stream, st, stats))
+      return rc;
+    return finish_host();
+  }
+  struct Streams {
+    cudaStream_t cp = nullptr, pp = nullptr, k[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev;
+    ~Streams() {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+      for (cudaStream_t x : {cp, pp, k[0], k[1]})
+        if (x) cudaStreamDestroy(x);
+    }
+    cudaError_t event(cudaEvent_t* e) {
+      cudaError_t r = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+      if (r == cudaSuccess) ev.push_back(*e);
+      return r;
+    }
+  } S;
+  for (cudaStream_t* x : {&S.cp, &S.pp, &S.k[0], &S.k[1]})
+    RMX_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  const int nc = ws.lay.n_chunks;
+  cudaEvent_t e0, e_ord, e_pdone, e_k[2];
+  RMX_CUDA(S.event(&e0));
+  RMX_CUDA(S.event(&e_ord));
+  RMX_CUDA(S.event(&e_pdone));
+  RMX_CUDA(S.event(&e_k[0]));
+  RMX_CUDA(S.event(&e_k[1]));
+  std::vector<cudaEvent_t> e_rows(nc), e_prep(nc);
+  for (int c = 0; c < nc; ++c) {
+    RMX_CUDA(S.event(&e_rows[c]));
+    RMX_CUDA(S.event(&e_prep[c]));
+  }
+  // everything starts after the caller's prior work on `stream`
+  RMX_CUDA(cudaEventRecord(e0, s));
+  for (cudaStream_t x : {S.cp, S.pp, S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e0, 0));
+  // copies: labels first (K1 needs them), then X chunk by chunk
+  RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, S.cp));
+  RMX_CUDA(cudaEventRecord(e_ord, S.cp));
+  for (int c = 0; c < nc; ++c) {
+    int64_t v0, v1;
+    chunk_voxels(ws.lay, v, c, &v0, &v1);
+    if (v1 > v0)
+      RMX_CUDA(cudaMemcpyAsync(x_dev + v0 * n, x_host + v0 * n, (size_t)(v1 - v0) * n * 8,
+                               cudaMemcpyHostToDevice, S.cp));
+    RMX_CUDA(cudaEventRecord(e_rows[c], S.cp));
+  }
+  if (int rc = prep_init(ws, L, S.pp, st)) return rc;
+  for (cudaStream_t x : {S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e_ord, 0));
+  for (int c = 0; c < nc; ++c) {
+    int64_t v0, v1;
+    chunk_voxels(ws.lay, v, c, &v0, &v1);
+    RMX_CUDA(cudaStreamWaitEvent(S.pp, e_rows[c], 0));
+    if (int rc = prep_rows(x_dev, v, n, n1, ws, v0, v1, S.pp, st)) return rc;
+    RMX_CUDA(cudaEventRecord(e_prep[c], S.pp));
+    cudaStream_t ks = S.k[c & 1];
+    RMX_CUDA(cudaStreamWaitEvent(ks, e_prep[c], 0));
+    if (int rc = tfill_impl(v, n, n1, orders_dev, L, two_sided, nullptr, workspace,
+                            workspace_bytes, ks, st, stats, c, c + 1))
+      return rc;
+  }
+  RMX_CUDA(launch_const_reduce(x_dev, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), S.pp));
+  RMX_CUDA(cudaEventRecord(e_pdone, S.pp));
+  RMX_CUDA(cudaEventRecord(e_k[0], S.k[0]));
+  RMX_CUDA(cudaEventRecord(e_k[1], S.k[1]));
+  for (cudaEvent_t e : {e_pdone, e_k[0], e_k[1]}) RMX_CUDA(cudaStreamWaitEvent(s, e, 0));
+  if (int rc = rmx_naive_finish(x_dev, v, n, n1, orders_dev, L, two_sided, max_dev, argmax_dev,
+                                workspace, workspace_bytes, stream, st, stats))
+    return rc;
+  return finish_host();
 }
 
 int rmx_tstat_exact(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,

@@ -89,6 +89,7 @@ struct PrepArgs {
   uint8_t* planes8;
   float* inv_scale;
   int zplanes_only;  // balanced fp16 path: the Z^2 planes are not needed
+  int64_t v_begin, v_end;  // voxel rows [v_begin, v_end) (v_end = 0: all)
 };
 
 struct TfillArgs {
@@ -97,6 +98,7 @@ struct TfillArgs {
   int n, n1, kpad, nk16;
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
   int stride_full, stride_last;  // tile visiting strides (coprime with the chunk length)
+  int chunk_begin, chunk_end;    // voxel chunks [begin, end) of this launch
   float alpha, beta, gamma, dthr;
   float band_rel;          // fp32 part of the refinement band (threshold seeding)
   float beta_abs;          // |beta| (int8 band, see band_abs)
@@ -146,6 +148,8 @@ cudaError_t launch_pairs(const double* x, int64_t v, int n, int n1, const int16_
 // tfill_tc.cu
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s);
+// voxel range [v0, v1) covered by K1 chunk c
+void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t* v1);
 
 int device_sm_count();
 

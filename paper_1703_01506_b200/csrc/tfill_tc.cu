@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <mutex>
 
@@ -356,8 +357,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int n_units = a.n_mtiles * a.n_chunks;
-  const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
+  // units (m-tile, chunk) of chunks [chunk_begin, chunk_end), chunk-major
+  const int n_units = a.n_mtiles * a.chunk_end;
+  const int unit0 = a.n_mtiles * a.chunk_begin + blockIdx.x / CG, unit_step = gridDim.x / CG;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -671,7 +673,11 @@ cudaError_t launch_cfg_e(const NaiveLayout& lay, const TfillArgs& a, const CUten
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)lay.grid);
+  // persistent grid, at most one CTA (pair) per unit of this launch's chunks
+  const int64_t units = (int64_t)lay.n_mtiles * (a.chunk_end - a.chunk_begin);
+  const int grid = (int)std::min<int64_t>(lay.grid, (int64_t)CG * units);
+  if (grid <= 0) return cudaSuccess;
+  cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(64 + 32 * EPI);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -757,6 +763,13 @@ bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad
                    bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t* v1) {
+  const int64_t t0 = (int64_t)c * lay.tiles_per_chunk;
+  const int64_t t1 = std::min<int64_t>(t0 + lay.tiles_per_chunk, lay.n_vtiles);
+  *v0 = std::min<int64_t>(t0 * lay.vt, v);
+  *v1 = std::min<int64_t>(t1 * lay.vt, v);
 }
 
 bool make_planes8_map(CUtensorMap* map, const uint8_t* planes, int64_t v, int kpad, int cg) {

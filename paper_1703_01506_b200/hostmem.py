@@ -40,21 +40,74 @@ def _as_tensor(arr: np.ndarray):
         return torch.from_numpy(arr)
 
 
+def _owner(arr: np.ndarray) -> np.ndarray:
+    """The ndarray that owns `arr`'s memory (views -- e.g. the label cache's
+    row slices -- share one registration with their owner)."""
+    root = arr
+    while isinstance(root.base, np.ndarray):
+        root = root.base
+    lo, hi = root.ctypes.data, root.ctypes.data + root.nbytes
+    if root.flags["C_CONTIGUOUS"] and lo <= arr.ctypes.data and arr.ctypes.data + arr.nbytes <= hi:
+        return root
+    return arr
+
+
+def _register(arr: np.ndarray) -> bool:
+    """Page-lock a (large, C-contiguous) array's memory in place, once per
+    owning array (unregistered when the owner is garbage-collected)."""
+    import torch
+
+    owner = _owner(arr)
+    ptr = owner.ctypes.data
+    with _LOCK:
+        if ptr in _REGISTERED and _REGISTERED[ptr][0]() is owner:
+            return True
+    rc = torch.cuda.cudart().cudaHostRegister(ptr, owner.nbytes, 0)
+    if int(rc) != 0:
+        return False
+    with _LOCK:
+        _REGISTERED[ptr] = (weakref.ref(owner, lambda _r, p=ptr: _unregister(p)),)
+    return True
+
+
+def pinned(arr: np.ndarray) -> np.ndarray:
+    """A C-contiguous, page-locked view (large arrays, registered in place) or
+    copy (small arrays) of `arr`, for asynchronous host->device copies.  When
+    registration is refused the contiguous pageable array is returned (copies
+    then serialise but stay correct)."""
+    arr = np.ascontiguousarray(arr)
+    if arr.nbytes >= _MIN_REGISTER_BYTES:
+        _register(arr)
+        return arr
+    out = pinned_empty(arr.shape, arr.dtype)
+    out[...] = arr
+    return out
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A page-locked host array (torch's pinned allocator)."""
+    import torch
+
+    t = torch.empty(tuple(int(s) for s in shape), dtype=_torch_dtype(np.dtype(dtype)),
+                    pin_memory=True)
+    return t.numpy()
+
+
+def _torch_dtype(dt: np.dtype):
+    import torch
+
+    return {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+            np.dtype(np.int16): torch.int16, np.dtype(np.int32): torch.int32,
+            np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8}[dt]
+
+
 def to_device(arr: np.ndarray, device, stream=None):
     """Copy a C-contiguous numpy array to `device` (async on `stream`)."""
     import torch
 
     arr = np.ascontiguousarray(arr)
     if arr.nbytes >= _MIN_REGISTER_BYTES:
-        ptr = arr.ctypes.data
-        with _LOCK:
-            known = ptr in _REGISTERED and _REGISTERED[ptr][0]() is arr
-        if not known:
-            rc = torch.cuda.cudart().cudaHostRegister(ptr, arr.nbytes, 0)
-            if int(rc) == 0:
-                with _LOCK:
-                    _REGISTERED[ptr] = (weakref.ref(arr, lambda _r, p=ptr: _unregister(p)),)
-                known = True
+        _register(arr)
         host = _as_tensor(arr)
     else:
         host = _as_tensor(arr).pin_memory()

@@ -3,13 +3,16 @@
 Reference: naive.py:60-109 ``run_naive(x, plan, materialize, two_sided,
 threads, mem_cap_bytes) -> (MaxNull, StatMatrix | None, counters)``.
 
-Device pipeline (one stream, librmx.so):
-  K0 prepare  fp64 standardisation + fp16 hi/lo split planes of Z and Z^2
-  K1 tfill    tcgen05 contraction G.[Z|Z^2] + fused t / top-2 epilogue
+Device pipeline (librmx.so):
+  K0 prepare  fp64 standardisation + int8 digit planes (balanced, n >= 192)
+              or fp16 hi/lo split planes of Z (and Z^2)
+  K1 tfill    tcgen05 contraction G.[Z|Z^2] + fused t / top-4 epilogue
   K2 finish   fp64 refinement of the band candidates -> maxima bit-identical
               to the reference (numpy arithmetic restated, np_exact.cuh)
 ``materialize=True`` additionally fills the dense statistic matrix with the
 exact fp64 kernel (bit-identical to the reference's ``store[:, i] = col``).
+From host arrays (``run_naive``), one ``rmx_naive_maxnull_host`` call uploads
+X chunk by chunk and overlaps the copy with K0/K1.
 
 Threads: the reference parallelises over permutation blocks on a thread pool
 and guarantees thread-count-independent results (naive.py:86-101).  Here the
@@ -198,14 +201,38 @@ def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
     resolve_threads(threads)
     device = cuda_device()
     orders = plan_orders(plan)
-    xd, od = upload(x.values, orders, device)
-    job = NaiveJob(xd, x.n1, od, two_sided)
-    mx, am = job.run()
+    mx, am, job = _run_from_host(x.values, x.n1, orders, two_sided, device)
     T = None
     if materialize:
-        T = tstat_exact_device(xd, x.n1, od).t().contiguous().cpu().numpy()
-    return NaiveResult(mx.cpu().numpy(), am.cpu().numpy().astype(np.int64),
-                       job.stats.as_dict(), T)
+        T = tstat_exact_device(job.x, x.n1, job.orders).t().contiguous().cpu().numpy()
+    return NaiveResult(mx, am.astype(np.int64), job.stats.as_dict(), T)
+
+
+def _run_from_host(values: np.ndarray, n1: int, orders: np.ndarray, two_sided: bool, device):
+    """One rmx_naive_maxnull_host call: host X and labels in (page-locked in
+    place), the X upload overlapped with the engine chunk by chunk, host
+    max/argmax out.  Returns (max, argmax, job) -- the job keeps the device
+    copies for follow-up work (materialisation)."""
+    import torch
+
+    from .hostmem import pinned, pinned_empty
+
+    xh = pinned(np.asarray(values, dtype=np.float64))
+    oh = pinned(np.asarray(orders, dtype=np.int16))
+    v, n = xh.shape
+    L = oh.shape[0]
+    xd = torch.empty((v, n), dtype=torch.float64, device=device)
+    od = torch.empty((L, n), dtype=torch.int16, device=device)
+    job = NaiveJob(xd, n1, od, two_sided)
+    mx = pinned_empty((L,), np.float64)
+    am = pinned_empty((L,), np.int32)
+    rc = job.lib.rmx_naive_maxnull_host(
+        xh.ctypes.data, v, n, int(n1), oh.ctypes.data, L, job.two_sided, mx.ctypes.data,
+        am.ctypes.data, nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
+        nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
+        ctypes.byref(job.stats))
+    nat.raise_for(rc, job._st)
+    return mx.copy(), am.copy(), job
 
 
 def run_naive(x, plan, materialize: bool = False, two_sided: bool = False,
