@@ -2,6 +2,7 @@
 // native GROUSE training loop (reference lrmc.py:208-268).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -120,9 +121,51 @@ int rmx_complete_max(const float* u32, int64_t v, int32_t r, const float* w32, i
                      rmx_status* st) {
   rclear(st);
   if (v < 1 || r < 1 || B < 1) return rset(st, RMX_E_USAGE, "bad completion dimensions");
-  RCUDA(launch_complete_max(u32, v, r, w32, B, perm_base, sigma, mu, seed, two_sided, znoise,
-                            base, max_out, static_cast<cudaStream_t>(stream)));
-  return RMX_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Philox recovery (sigma > 0, the hot call): W U^T on the tensor cores
+  // (fp16 W, split fp16 U: |error| <= ~2^-12 sum |w_i u_i|, far below the
+  // sigma-scale noise); sigma = 0 (deterministic parity), znoise / base
+  // (training's shift estimators) keep the fp32 CUDA-core kernel.
+  NaiveLayout lay{};
+  const bool tc = !znoise && !base && sigma > 0.0 && !getenv("RMX_COMPLETE_FP32") &&
+                  (lay = complete_layout(v, r, B, device_sm_count())).stages > 0;
+  if (!tc) {
+    RCUDA(launch_complete_max(u32, v, r, w32, B, perm_base, sigma, mu, seed, two_sided, znoise,
+                              base, max_out, s));
+    return RMX_OK;
+  }
+  DevBuf<__half> planes, wA;
+  DevBuf<float> desc;
+  DevBuf<uint32_t> enc;
+  RCUDA(planes.alloc((size_t)2 * v * lay.kpad, s));
+  RCUDA(wA.alloc((size_t)B * lay.kpad, s));
+  RCUDA(desc.alloc((size_t)B, s));
+  RCUDA(enc.alloc((size_t)B, s));
+  RCUDA(cudaMemsetAsync(enc.p, 0, (size_t)B * 4, s));
+  RCUDA(launch_u_planes(u32, v, r, lay.kpad, planes.p, s));
+  RCUDA(launch_w_rows(w32, B, r, lay.kpad, wA.p, desc.p, s));
+  TfillArgs a{};
+  a.L = B;
+  a.v = v;
+  a.kpad = lay.kpad;
+  a.nk16 = lay.kpad / 16;
+  a.n_vtiles = lay.n_vtiles;
+  a.n_mtiles = lay.n_mtiles;
+  a.n_chunks = lay.n_chunks;
+  a.tiles_per_chunk = lay.tiles_per_chunk;
+  a.stride_full = golden_stride_public(lay.tiles_per_chunk);
+  a.stride_last = golden_stride_public(lay.n_vtiles - (lay.n_chunks - 1) * lay.tiles_per_chunk);
+  a.chunk_begin = 0;
+  a.chunk_end = lay.n_chunks;
+  a.wA = wA.p;
+  a.wdescale = desc.p;
+  a.maxenc = enc.p;
+  a.sigma = (float)sigma;
+  a.seed = seed;
+  a.perm_base = perm_base;
+  RCUDA(launch_complete_tc(lay, a, planes.p, two_sided, s));
+  RCUDA(launch_max_finalize(enc.p, B, mu, max_out, s));
+  return RMX_OK;  // scratch freed stream-ordered (cudaFreeAsync)
 }
 
 int rmx_to_f32(const double* a, int64_t n, float* out, void* stream, rmx_status* st) {
@@ -208,8 +251,9 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   if (k < r) return rset(st, RMX_E_USAGE, "%d observed rows per update cannot identify rank %d", k, r);
   if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  DevBuf<double> G, w, vals, resid, pred, d, sums, wn;  // sums: 0 |r|^2 1 |pred|^2 2 |t|^2 4.. chol
-  DevBuf<int32_t> flag, idxbuf;
+  // sums: 0 |r|^2 1 |pred|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
+  DevBuf<double> G, w, vals, resid, pred, d, sums, wn, ug;
+  DevBuf<int32_t> flag, idxbuf, pidx;
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
@@ -220,9 +264,24 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(sums.alloc(8, s));
   RCUDA(flag.alloc(1, s));
   RCUDA(idxbuf.alloc(k, s));
+  RCUDA(pidx.alloc(k, s));
+  RCUDA(ug.alloc((size_t)k * r, s));
   RCUDA(cudaMemsetAsync(d.p, 0, v * sizeof(double), s));
+  RCUDA(cudaMemsetAsync(pred.p, 0, v * sizeof(double), s));
+  RCUDA(cudaMemsetAsync(wn.p, 0, r * sizeof(double), s));  // finite: 0 * wn in k_pred_apply
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
+  const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
+  // the deferred rank-1 update U += (pend_a pred + d) wn^T (d nonzero on pidx)
+  bool pending = false;
+  double pend_a = 0.0;
+  auto flush = [&]() -> int {
+    if (!pending) return RMX_OK;
+    RCUDA(launch_grouse_update(u, v, r, pred.p, wn.p, pend_a, d.p, s));
+    RCUDA(launch_unscatter(pidx.p, k, d.p, s));
+    pending = false;
+    return RMX_OK;
+  };
   int64_t tcount = 0;
   int passes = 0, converged = 0;
   for (int p = 0; p < max_passes; ++p) {
@@ -235,15 +294,29 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       int32_t hflag = 0;
       int attempt = 0;
       for (;;) {
+        // U_Omega with the pending update, then the Gram of [U_Omega | t_Omega]
+        RCUDA(launch_gather_pending(u, r, idx, k, pending ? 1 : 0, pend_a, pred.p, d.p, wn.p,
+                                    ug.p, s));
         RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
-        RCUDA(launch_gram(u, r, r, idx, k, vals.p, G.p, 1, s));
-        RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
-        RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
-        RCUDA(launch_resid(u, r, idx, k, vals.p, w.p, resid.p, sums.p, s));
-        RCUDA(launch_pred(u, v, r, w.p, pred.p, sums.p, s));
-        RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
-        RCUDA(cudaMemcpyAsync(&hflag, flag.p, sizeof(hflag), cudaMemcpyDeviceToHost, s));
-        RCUDA(cudaStreamSynchronize(s));
+        RCUDA(launch_gram(ug.p, r, r, nullptr, k, vals.p, G.p, 1, s));
+        // cluster CG first (the restricted Gram of a random row sample is
+        // well conditioned); Cholesky on the same G when CG does not converge
+        bool chol = !use_cg;
+        for (;;) {
+          RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+          if (chol) RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
+          else RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13, s));
+          RCUDA(launch_resid(ug.p, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
+          // p = U' w with U' = U + pending (applied in the same pass); skipped
+          // (update stays pending) when the solve flagged the attempt
+          RCUDA(launch_pred_apply(u, v, r, w.p, pred.p, sums.p, pending ? pend_a : 0.0, d.p, wn.p,
+                                  flag.p, s));
+          RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+          RCUDA(cudaMemcpyAsync(&hflag, flag.p, sizeof(hflag), cudaMemcpyDeviceToHost, s));
+          RCUDA(cudaStreamSynchronize(s));
+          if (chol || !hflag) break;
+          chol = true;
+        }
         if (!hflag) break;
         // ill-conditioned restriction: redraw from the same stream (lrmc.py:240-250)
         if (++attempt >= 5 || !cb)
@@ -255,6 +328,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                               cudaMemcpyHostToDevice, s));
         idx = idxbuf.p;
       }
+      if (pending) {  // applied by k_pred_apply
+        RCUDA(launch_unscatter(pidx.p, k, d.p, s));
+        pending = false;
+      }
       const double resid_norm = std::sqrt(std::max(hs[0], 0.0));
       const double pred_norm = std::sqrt(std::max(hs[1], 0.0));
       const double t_norm = std::sqrt(std::max(hs[2], 0.0));
@@ -264,12 +341,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       if (do_update && resid_norm <= 1e-14 * std::max(1.0, pred_norm)) do_update = false;
       if (do_update) {
         const double theta = step * std::atan(resid_norm / pred_norm);
-        const double a = (std::cos(theta) - 1.0) / pred_norm;
+        pend_a = (std::cos(theta) - 1.0) / pred_norm;
         const double bcoef = std::sin(theta) / resid_norm;
         RCUDA(launch_scatter(idx, k, resid.p, bcoef, d.p, s));
         RCUDA(launch_scale_copy(w.p, r, 1.0 / w_norm, wn.p, s));  // w / |w|
-        RCUDA(launch_grouse_update(u, v, r, pred.p, wn.p, a, d.p, s));
-        RCUDA(launch_unscatter(idx, k, d.p, s));
+        RCUDA(cudaMemcpyAsync(pidx.p, idx, k * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        pending = true;
       }
       ++tcount;
       rel_sum += t_norm > 0 ? resid_norm / t_norm : 0.0;
@@ -277,6 +354,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
         RCUDA(cudaMemcpyAsync(final_omegas + (int64_t)i * k, idx, k * sizeof(int32_t),
                               cudaMemcpyDeviceToDevice, s));
       if (tcount % 64 == 0) {
+        if (int rc = flush()) return rc;
         double drift = 0.0;
         if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
       }
@@ -289,6 +367,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       break;
     }
   }
+  if (int rc = flush()) return rc;
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
   if (passes_out) *passes_out = passes;

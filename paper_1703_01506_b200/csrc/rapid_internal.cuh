@@ -1,5 +1,6 @@
 // rapid_internal.cuh -- launchers of rapid_kernels.cu (RapidPT on the GPU).
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -15,6 +16,17 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 // (t.t - rhs.w, w.w, min L_ii, max L_ii); flag_b = 1 on a non-positive pivot
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s);
+// K4 on tcgen05: operand preparation and the max decode
+cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
+                            cudaStream_t s);
+cudaError_t launch_w_rows(const float* W, int64_t B, int r, int kpad, __half* wA, float* descale,
+                          cudaStream_t s);
+cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, double* out,
+                                cudaStream_t s);
+// one well-conditioned system (GROUSE) by cluster CG; flag = not converged
+bool cg_solve_supported(int r);
+cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
+                            double tol, cudaStream_t s);
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
                                 int64_t perm_base, double sigma, double mu, uint64_t seed,
                                 int two_sided, const float* znoise, const double* base,
@@ -23,6 +35,12 @@ cudaError_t launch_resid(const double* U, int r, const int32_t* idx, int k, cons
                          const double* w, double* resid, double* sums, cudaStream_t s);
 cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, double* pred,
                         double* sums, cudaStream_t s);
+cudaError_t launch_gather_pending(const double* U, int r, const int32_t* idx, int k, int pending,
+                                  double a, const double* pred, const double* d, const double* wn,
+                                  double* out, cudaStream_t s);
+cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, double* pred,
+                              double* sums, double a, const double* d, const double* wn,
+                              const int32_t* flag, cudaStream_t s);
 cudaError_t launch_grouse_update(double* U, int64_t v, int r, const double* pred,
                                  const double* wn, double a, const double* dscatter,
                                  cudaStream_t s);

@@ -1,9 +1,7 @@
-// rapid_kernels.cu -- RapidPT on the GPU (reference rapid.py / lrmc.py).
-// Compiled with -fmad=false: the Omega-row statistics reproduce the
-// reference's numpy bits (np_exact.cuh); the least-squares algebra is fp64.
+// rapid_kernels.cu -- RapidPT on the GPU (reference rapid.py / lrmc.py):
+// the least-squares algebra (fp64, FMA contraction allowed) and the
+// completion.  The bit-exact Omega-row statistics live in rapid_stats.cu.
 //
-//   k_rapid_stats   K2: t_Omega[p, i] = statistic of row omega_p[i] under
-//                   perm p (rapid.py:156-170, batched _welch_rows)
 //   k_gram          K3a: G_b = [U_Omega | t]^T [U_Omega | t] for a batch of
 //                   gathered row sets (lrmc.py:136-137: gram and rhs at once)
 //   k_chol_solve    K3b: blocked Cholesky of G_b[:r,:r], w = G^-1 rhs, and a
@@ -12,33 +10,19 @@
 //   k_complete_max  K4: max_j (W U^T)[p, j] + sigma z(p, j)  (+ mu), fused
 //                   with a counter-based Philox normal (rapid.py:198-205)
 //   GROUSE helpers  k_resid, k_pred, k_grouse_update (lrmc.py:160-193)
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
 
-#include "np_exact.cuh"
+#include "philox.cuh"
 #include "rapid_internal.cuh"
+#include "sm100.cuh"
 
 namespace rmx {
 namespace {
-
-// ------------------------------------------------------------------ K2
-// grid (ceil(k / 256), L): one block per permutation chunk of Omega.
-__global__ void k_rapid_stats(const double* __restrict__ x, int n, int n1,
-                              const int16_t* __restrict__ orders, const int32_t* __restrict__ omegas,
-                              int k, double* __restrict__ t_out, unsigned long long* deg_key) {
-  extern __shared__ int16_t ord[];
-  const int64_t p = blockIdx.y;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ord[i] = orders[p * n + i];
-  __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= k) return;
-  const int64_t row = omegas[p * k + i];
-  const WelchExact r = welch_exact(x + row * n, 1, ord, n1, n - n1);
-  t_out[p * k + i] = r.t;
-  if (r.degenerate) atomicMin(deg_key, ((unsigned long long)p << 32) | (unsigned long long)i);
-}
 
 // ------------------------------------------------------------------ K3a
 // A_b = [U[idx_b[0..k)] | vals_b]  (k x (r+1)), G_b = A_b^T A_b, full
@@ -118,114 +102,208 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int6
 
 // ------------------------------------------------------------------ K3b
 // One CTA per system.  Right-looking blocked Cholesky on G[:r, :r] in place
-// (global memory, L2-resident), panel width 32 kept in smem; then a one-warp
-// forward/back substitution for w.  flag[b] = 1 when a pivot is not
+// (global memory, L2-resident), panel width 32 (the last panel padded with
+// the identity).  Per panel: one warp factors the diagonal block with the
+// block held in registers (lane = row, columns broadcast by shuffles); the
+// panel below is solved one row per thread with the row in registers and
+// L_D broadcast from smem; the trailing lower triangle is updated with 4x4
+// register tiles from the smem panel (row stride 33: conflict-free).  The
+// substitutions for w run per 32-block on one warp (shuffles), the
+// off-diagonal updates on all threads.  flag[b] = 1 when a pivot is not
 // positive relative to the largest diagonal (rank-deficient restriction).
 constexpr int kPW = 32;
+constexpr int kPS = kPW + 1;  // padded smem row stride (doubles)
 
-__global__ void __launch_bounds__(256) k_chol_solve(double* __restrict__ G, int r,
-                                                    double* __restrict__ w_out,
-                                                    int32_t* __restrict__ flag,
-                                                    double* __restrict__ resid2) {
+// Factor the 32x32 SPD block D (smem, lower part used; rows/cols >= w are
+// the identity) in place into L_D; rinv[c] = 1 / L_cc.  One warp.
+__device__ __forceinline__ void chol_block32(double* D, double* rinv, double tiny, int* bad) {
+  const int lane = threadIdx.x & 31;
+  double a[kPW];
+#pragma unroll
+  for (int l = 0; l < kPW; ++l) a[l] = D[lane * kPS + l];
+#pragma unroll
+  for (int c = 0; c < kPW; ++c) {
+    double piv = __shfl_sync(0xffffffffu, a[c], c);
+    if (!(piv > tiny)) {
+      if (lane == 0) *bad = 1;
+      piv = fmax(fabs(piv), 1e-300);
+    }
+    const double d = sqrt(piv);
+    const double inv = 1.0 / d;
+    if (lane == c) a[c] = d;
+    if (lane > c) a[c] *= inv;
+    if (lane == 0) rinv[c] = inv;
+#pragma unroll
+    for (int l = c + 1; l < kPW; ++l) {
+      const double llc = __shfl_sync(0xffffffffu, a[c], l);
+      if (lane >= l) a[l] = fma(-a[c], llc, a[l]);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < kPW; ++l) D[lane * kPS + l] = (l <= lane) ? a[l] : 0.0;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r,
+                                                   double* __restrict__ w_out,
+                                                   int32_t* __restrict__ flag,
+                                                   double* __restrict__ resid2) {
   extern __shared__ double sm[];
-  double* D = sm;                       // kPW x kPW diagonal block
-  double* P = sm + kPW * kPW;           // (r) x kPW panel
+  double* D = sm;                     // kPW x kPS: block / L_D (lower)
+  double* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
+  double* P = rinv + kPW;             // r x kPS panel
+  double* y = P + (size_t)r * kPS;    // r: right-hand side / solution
   __shared__ int bad;
   __shared__ double dmax;
   const int64_t b = blockIdx.x;
   const int ld = r + 1;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
   double* Gb = G + b * (int64_t)ld * ld;
-  if (threadIdx.x < 32) {
+  if (wid == 0) {
     double m = 0.0;
-    for (int i = threadIdx.x; i < r; i += 32) m = fmax(m, Gb[(int64_t)i * ld + i]);
+    for (int i = lane; i < r; i += 32) m = fmax(m, Gb[(int64_t)i * ld + i]);
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       bad = 0;
       dmax = m;
     }
   }
   __syncthreads();
   const double tiny = 1e-24 * dmax;
+  auto load_block = [&](int jb, int w) {  // D = G[jb.., jb..] (lower), identity padding
+    for (int e = tid; e < kPW * kPW; e += NT) {
+      const int i = e / kPW, j = e % kPW;
+      double val = (i == j) ? 1.0 : 0.0;
+      if (i < w && j < w && j <= i) val = Gb[(int64_t)(jb + i) * ld + jb + j];
+      D[i * kPS + j] = val;
+    }
+  };
   for (int jb = 0; jb < r; jb += kPW) {
     const int w = min(kPW, r - jb);
-    for (int e = threadIdx.x; e < w * w; e += blockDim.x)
-      D[(e / w) * kPW + e % w] = Gb[(int64_t)(jb + e / w) * ld + jb + e % w];
+    load_block(jb, w);
     __syncthreads();
-    if (threadIdx.x < 32) {  // factor the diagonal block (one warp)
-      const int lane = threadIdx.x;
-      for (int c = 0; c < w; ++c) {
-        double piv = D[c * kPW + c];
-        if (!(piv > tiny)) {
-          if (lane == 0) bad = 1;
-          piv = fmax(fabs(piv), 1e-300);
-        }
-        const double d = sqrt(piv);
-        __syncwarp();
-        if (lane == c) D[c * kPW + c] = d;
-        if (lane > c && lane < w) D[lane * kPW + c] /= d;
-        __syncwarp();
-        if (lane > c && lane < w)
-          for (int l = c + 1; l <= lane; ++l) D[lane * kPW + l] -= D[lane * kPW + c] * D[l * kPW + c];
-        __syncwarp();
-      }
-    }
+    if (wid == 0) chol_block32(D, rinv, tiny, &bad);
     __syncthreads();
-    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    for (int e = tid; e < w * w; e += NT) {
       const int i = e / w, j = e % w;
-      if (j <= i) Gb[(int64_t)(jb + i) * ld + jb + j] = D[i * kPW + j];
+      if (j <= i) Gb[(int64_t)(jb + i) * ld + jb + j] = D[i * kPS + j];
     }
-    // panel below: P = G[jb+w:, jb:jb+w] L_D^{-T}, one row per thread
+    // panel below: P_i L_D^T = G[i, jb:jb+w], one row per thread (registers)
     const int rows = r - jb - w;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      const int64_t gi = (int64_t)(jb + w + i) * ld + jb;
-      for (int c = 0; c < w; ++c) {
-        double s = Gb[gi + c];
-        for (int l = 0; l < c; ++l) s -= P[i * kPW + l] * D[c * kPW + l];
-        P[i * kPW + c] = s / D[c * kPW + c];
+    for (int i = tid; i < rows; i += NT) {
+      double* gi = Gb + (int64_t)(jb + w + i) * ld + jb;
+      double pr[kPW];
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) pr[c] = c < w ? gi[c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) {
+        double sacc = pr[c];
+#pragma unroll
+        for (int l = 0; l < c; ++l) sacc = fma(-pr[l], D[c * kPS + l], sacc);
+        pr[c] = sacc * rinv[c];
       }
-      for (int c = 0; c < w; ++c) Gb[gi + c] = P[i * kPW + c];
-      for (int c = w; c < kPW; ++c) P[i * kPW + c] = 0.0;  // last (narrow) panel
+      double* prow = P + (size_t)i * kPS;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) {
+        prow[c] = pr[c];
+        if (c < w) gi[c] = pr[c];
+      }
     }
     __syncthreads();
-    // trailing update: G[i, j] -= P_i . P_j for jb+w <= j <= i < r
-    // (warp per row i, lanes over j <= i)
-    {
-      const int wid = threadIdx.x / 32, lane = threadIdx.x & 31, nw = blockDim.x / 32;
-      for (int ii = wid; ii < rows; ii += nw) {
-        double pi[kPW];
+    // trailing update G[i, j] -= P_i . P_j over jb+w <= j <= i < r, 4x4 tiles
+    const int nb = (rows + 3) / 4;
+    const int ntile = nb * (nb + 1) / 2;
+    for (int t = tid; t < ntile; t += NT) {
+      int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);  // t -> (bi, bj), bj <= bi
+      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+      while (bi * (bi + 1) / 2 > t) --bi;
+      const int bj = t - bi * (bi + 1) / 2;
+      double acc[4][4] = {};
+      const double* pi = P + (size_t)(4 * bi) * kPS;
+      const double* pj = P + (size_t)(4 * bj) * kPS;
+#pragma unroll 4
+      for (int c = 0; c < kPW; ++c) {
+        double a[4], bb[4];
 #pragma unroll
-        for (int c = 0; c < kPW; ++c) pi[c] = c < w ? P[ii * kPW + c] : 0.0;
-        double* grow = Gb + (int64_t)(jb + w + ii) * ld + jb + w;
-        for (int jj = lane; jj <= ii; jj += 32) {
-          double acc = 0.0;
+        for (int q = 0; q < 4; ++q) {
+          a[q] = (4 * bi + q < rows) ? pi[q * kPS + c] : 0.0;
+          bb[q] = (4 * bj + q < rows) ? pj[q * kPS + c] : 0.0;
+        }
 #pragma unroll
-          for (int c = 0; c < kPW; ++c) acc += pi[c] * P[jj * kPW + c];
-          grow[jj] -= acc;
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], bb[u], acc[q][u]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = 4 * bi + q;
+        if (i >= rows) continue;
+        double* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * bj + u;
+          if (j <= i) grow[j] -= acc[q][u];
         }
       }
     }
     __syncthreads();
   }
-  // solve L L^T w = rhs (rhs = G[r, 0:r], the A^T t row), one warp
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double* y = P;  // reuse smem: r doubles
-    for (int i = lane; i < r; i += 32) y[i] = Gb[(int64_t)r * ld + i];
-    __syncwarp();
-    for (int j = 0; j < r; ++j) {
-      const double yj = y[j] / Gb[(int64_t)j * ld + j];
-      __syncwarp();
-      if (lane == 0) y[j] = yj;
-      for (int i = j + 1 + lane; i < r; i += 32) y[i] -= Gb[(int64_t)i * ld + j] * yj;
-      __syncwarp();
+  // solve L L^T w = rhs (rhs = G[r, 0:r], the A^T t row), blocked
+  for (int i = tid; i < r; i += NT) y[i] = Gb[(int64_t)r * ld + i];
+  __syncthreads();
+  for (int jb = 0; jb < r; jb += kPW) {  // forward: L y = rhs
+    const int w = min(kPW, r - jb);
+    load_block(jb, w);
+    __syncthreads();
+    if (wid == 0) {  // lane c holds y[jb + c]; row `lane` of L_D in registers
+      double lr[kPW];
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) lr[c] = D[lane * kPS + c];
+      double yb = lane < w ? y[jb + lane] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) {
+        if (lane == c) yb /= lr[c];
+        const double yc = __shfl_sync(0xffffffffu, yb, c);
+        if (lane > c) yb = fma(-lr[c], yc, yb);
+      }
+      if (lane < w) y[jb + lane] = yb;
     }
-    for (int j = r - 1; j >= 0; --j) {
-      const double wj = y[j] / Gb[(int64_t)j * ld + j];
-      __syncwarp();
-      if (lane == 0) y[j] = wj;
-      for (int i = lane; i < j; i += 32) y[i] -= Gb[(int64_t)j * ld + i] * wj;
-      __syncwarp();
+    __syncthreads();
+    for (int i = jb + w + tid; i < r; i += NT) {
+      const double* li = Gb + (int64_t)i * ld + jb;
+      double sacc = 0.0;
+      for (int c = 0; c < w; ++c) sacc = fma(li[c], y[jb + c], sacc);
+      y[i] -= sacc;
     }
+    __syncthreads();
+  }
+  for (int jb = ((r - 1) / kPW) * kPW; jb >= 0; jb -= kPW) {  // backward: L^T w = y
+    const int w = min(kPW, r - jb);
+    load_block(jb, w);
+    __syncthreads();
+    if (wid == 0) {  // lane c holds y[jb + c]; column `lane` of L_D in registers
+      double lc[kPW];
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) lc[c] = D[c * kPS + lane];
+      double yb = lane < w ? y[jb + lane] : 0.0;
+#pragma unroll
+      for (int c = kPW - 1; c >= 0; --c) {
+        if (lane == c) yb /= lc[c];
+        const double wc = __shfl_sync(0xffffffffu, yb, c);
+        if (lane < c) yb = fma(-lc[c], wc, yb);
+      }
+      if (lane < w) y[jb + lane] = yb;
+    }
+    __syncthreads();
+    for (int i = tid; i < jb; i += NT) {  // coalesced: row jb+c, columns i
+      double sacc = 0.0;
+      for (int c = 0; c < w; ++c) sacc = fma(Gb[(int64_t)(jb + c) * ld + i], y[jb + c], sacc);
+      y[i] -= sacc;
+    }
+    __syncthreads();
+  }
+  if (tid < 32) {
     if (w_out)
       for (int i = lane; i < r; i += 32) w_out[b * r + i] = y[i];
     if (resid2) {
@@ -257,39 +335,204 @@ __global__ void __launch_bounds__(256) k_chol_solve(double* __restrict__ G, int 
   }
 }
 
-// ------------------------------------------------------------------ Philox
-__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int i = 0; i < 10; ++i) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
-    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-    c[0] = n0;
-    c[1] = lo1;
-    c[2] = n2;
-    c[3] = lo0;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
+// ------------------------------------------------------------------ K3b (GROUSE)
+// One GROUSE solve (B = 1) on a cluster of kCgCtas CTAs: G[:r, :r] is
+// split by rows across the CTAs' shared memory (the whole Gram lives on
+// chip, 160 KB per CTA at r = 400) and solved by Jacobi-preconditioned
+// conjugate gradients.  The U_Omega Gram of a random row sample is well
+// conditioned (kappa ~ (1 + sqrt(r/k))^2 / (1 - sqrt(r/k))^2 ~ 8 at config
+// 5), so CG reaches the 1e-13 relative residual in ~50 iterations; each
+// iteration is a local 50 x 400 mat-vec plus three cluster barriers
+// (dot-product all-reduces and the direction exchange through DSMEM).
+// flag = 1 when it has not converged after r iterations: the caller then
+// runs the Cholesky kernel on the same (unmodified) G, whose pivots decide
+// the ill-conditioning exactly as before.
+constexpr int kCgCtas = 8;
+constexpr int kCgThreads = 256;
+
+__device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_ptr)), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
+
+// Sum of (a, b) over the cluster, identical bits on every CTA (fixed order).
+// slots: this CTA's [kCgCtas][2] landing area for one all-reduce.
+__device__ __forceinline__ void cg_allreduce2(double a, double b, double* slots, double* wsum,
+                                              double& A, double& B) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) {
+    wsum[2 * wid] = a;
+    wsum[2 * wid + 1] = b;
+  }
+  __syncthreads();
+  const uint32_t me = cluster_ctarank();
+  if (threadIdx.x < kCgCtas) {
+    double ta = 0.0, tb = 0.0;
+    for (int w = 0; w < kCgThreads / 32; ++w) {
+      ta += wsum[2 * w];
+      tb += wsum[2 * w + 1];
+    }
+    st_cluster_f64(slots + 2 * me, threadIdx.x, ta);
+    st_cluster_f64(slots + 2 * me + 1, threadIdx.x, tb);
+  }
+  cluster_sync();
+  A = 0.0;
+  B = 0.0;
+  for (int q = 0; q < kCgCtas; ++q) {
+    A += slots[2 * q];
+    B += slots[2 * q + 1];
   }
 }
 
-// Four N(0,1) draws for (perm, voxels 4q..4q+3), keyed by the run seed:
-// counter = (q, perm_lo, perm_hi, RESIDUAL domain), Box-Muller in fp32.
-__device__ __forceinline__ void normals4(uint64_t seed, int64_t perm, int64_t q, float z[4]) {
-  uint32_t c[4] = {(uint32_t)q, (uint32_t)perm, (uint32_t)((uint64_t)perm >> 32), 4u};
-  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
-  const float u0 = ((float)c[0] + 0.5f) * 2.3283064365386963e-10f;
-  const float u1 = ((float)c[1] + 0.5f) * 2.3283064365386963e-10f;
-  const float u2 = ((float)c[2] + 0.5f) * 2.3283064365386963e-10f;
-  const float u3 = ((float)c[3] + 0.5f) * 2.3283064365386963e-10f;
-  const float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
-  float s0, c0, s1, c1;
-  sincospif(2.0f * u1, &s0, &c0);
-  sincospif(2.0f * u3, &s1, &c1);
-  z[0] = r0 * c0;
-  z[1] = r0 * s0;
-  z[2] = r1 * c1;
-  z[3] = r1 * s1;
+__global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
+                                                         double* __restrict__ w_out,
+                                                         int32_t* __restrict__ flag,
+                                                         double* __restrict__ resid2, double tol) {
+  extern __shared__ double cs[];
+  const int R = (r + kCgCtas - 1) / kCgCtas;  // rows per CTA
+  const uint32_t me = cluster_ctarank();
+  const int r0 = (int)me * R, nr = max(0, min(R, r - r0));
+  double* Gs = cs;                       // nr x r
+  double* pfull = Gs + (size_t)R * r;    // r
+  double* vec = pfull + r;               // 5 x R: x, res, z, p, q (local rows)
+  double* x = vec, *res = vec + R, *z = vec + 2 * R, *p = vec + 3 * R, *q = vec + 4 * R;
+  double* dinv = vec + 5 * R;            // R
+  double* slots = dinv + R;              // 3 all-reduce landing areas x [kCgCtas][2]
+  double* wsum = slots + 6 * kCgCtas;    // 2 x warps
+  const int ld = r + 1;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < nr * r; e += kCgThreads) {
+    const int i = e / r, j = e % r;
+    Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
+  }
+  double pb = 0.0, pz = 0.0;
+  for (int i = tid; i < nr; i += kCgThreads) {
+    const double bi = G[(int64_t)r * ld + r0 + i];
+    const double di = G[(int64_t)(r0 + i) * ld + r0 + i];
+    dinv[i] = di > 0.0 ? 1.0 / di : 1.0;
+    x[i] = 0.0;
+    res[i] = bi;
+    z[i] = bi * dinv[i];
+    p[i] = z[i];
+    pb += bi * bi;
+    pz += bi * z[i];
+  }
+  double bb, rz;
+  cg_allreduce2(pb, pz, slots, wsum, bb, rz);
+  const double stop = tol * tol * bb;
+  int converged = bb == 0.0;
+  int it = 0;
+  for (; it < r && !converged; ++it) {
+    // share this CTA's direction rows with every CTA
+    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
+      const int i = e % nr, dst = e / nr;
+      st_cluster_f64(pfull + r0 + i, dst, p[i]);
+    }
+    cluster_sync();
+    // q = G_rows p, one warp per row
+    for (int i = wid; i < nr; i += kCgThreads / 32) {
+      const double* gi = Gs + (size_t)i * r;
+      double acc = 0.0;
+      for (int j = lane; j < r; j += 32) acc = fma(gi[j], pfull[j], acc);
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) q[i] = acc;
+    }
+    __syncthreads();
+    double pq = 0.0;
+    for (int i = tid; i < nr; i += kCgThreads) pq += p[i] * q[i];
+    double PQ, dummy;
+    cg_allreduce2(pq, 0.0, slots + 2 * kCgCtas, wsum, PQ, dummy);
+    const double alpha = PQ != 0.0 ? rz / PQ : 0.0;
+    double prz = 0.0, prr = 0.0;
+    for (int i = tid; i < nr; i += kCgThreads) {
+      x[i] = fma(alpha, p[i], x[i]);
+      res[i] = fma(-alpha, q[i], res[i]);
+      z[i] = res[i] * dinv[i];
+      prz += res[i] * z[i];
+      prr += res[i] * res[i];
+    }
+    double RZ, RR;
+    cg_allreduce2(prz, prr, slots + 4 * kCgCtas, wsum, RZ, RR);
+    if (RR <= stop) {
+      converged = 1;
+      break;
+    }
+    const double beta = rz != 0.0 ? RZ / rz : 0.0;
+    rz = RZ;
+    for (int i = tid; i < nr; i += kCgThreads) p[i] = fma(beta, p[i], z[i]);
+    __syncthreads();
+  }
+  // outputs: w, (t.t - rhs.w, |w|^2, 1, 1), flag
+  double pw = 0.0, pbw = 0.0;
+  for (int i = tid; i < nr; i += kCgThreads) {
+    if (w_out) w_out[r0 + i] = x[i];
+    pw += x[i] * x[i];
+    pbw += G[(int64_t)r * ld + r0 + i] * x[i];
+  }
+  double WW, BW;
+  cg_allreduce2(pw, pbw, slots, wsum, WW, BW);  // slot 0 is free again here
+  if (me == 0 && tid == 0) {
+    if (resid2) {
+      resid2[0] = G[(int64_t)r * ld + r] - BW;
+      resid2[1] = WW;
+      resid2[2] = 1.0;
+      resid2[3] = 1.0;
+    }
+    if (flag) flag[0] = converged ? 0 : 1;
+  }
+  cluster_sync();  // no CTA exits while others may still write into its smem
+}
+
+// ------------------------------------------------------------------ K4 (tcgen05 operands)
+// U (v x r fp32) -> planes [2][v][kpad] fp16: hi = fp16(U 2^14), lo =
+// fp16(U 2^14 - hi) (|U| <= 1 for an orthonormal basis, so 2^14 keeps both
+// halves in fp16's normal range).  W (B x r fp32) -> [B][kpad] fp16 scaled by
+// 2^e_p (max |W_p| in [2^14, 2^15)), descale[p] = 2^(-e_p - 14).
+constexpr float kUScale = 16384.0f;
+
+__global__ void k_u_planes(const float* __restrict__ U, int64_t v, int r, int kpad,
+                           __half* __restrict__ planes) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= v * kpad) return;
+  const int64_t j = e / kpad;
+  const int c = (int)(e % kpad);
+  const float x = c < r ? U[j * r + c] * kUScale : 0.0f;
+  const __half h = __float2half_rn(x);
+  planes[e] = h;
+  planes[v * kpad + e] = __float2half_rn(x - __half2float(h));
+}
+
+__global__ void k_w_rows(const float* __restrict__ W, int64_t B, int r, int kpad,
+                         __half* __restrict__ wA, float* __restrict__ descale) {
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (p >= B) return;
+  float m = 0.0f;
+  for (int c = lane; c < r; c += 32) m = fmaxf(m, fabsf(W[p * r + c]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0f) {
+    frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
+    e = 15 - e;     // m 2^(15 - e) in [2^14, 2^15)
+  }
+  const float sc = ldexpf(1.0f, e);
+  for (int c = lane; c < kpad; c += 32)
+    wA[p * kpad + c] = __float2half_rn(c < r ? W[p * r + c] * sc : 0.0f);
+  if (lane == 0) descale[p] = ldexpf(1.0f, -e) / kUScale;
+}
+
+__global__ void k_max_finalize(const uint32_t* __restrict__ enc, int64_t B, double mu,
+                               double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= B) return;
+  const uint32_t e = enc[p];
+  const float f = __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
+  out[p] = (double)f + mu;
 }
 
 // ------------------------------------------------------------------ K4
@@ -383,7 +626,7 @@ __global__ void k_resid(const double* __restrict__ U, int r, const int32_t* __re
                         double* __restrict__ resid, double* __restrict__ sums) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (warp >= k) return;
-  const double* u = U + (int64_t)idx[warp] * r;
+  const double* u = U + (int64_t)(idx ? idx[warp] : warp) * r;
   double s = 0.0;
   for (int c = lane; c < r; c += 32) s += u[c] * w[c];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -406,6 +649,60 @@ __global__ void k_pred(const double* __restrict__ U, int64_t v, int r, const dou
     const double* u = U + row * r;
     double s = 0.0;
     for (int c = lane; c < r; c += 32) s += u[c] * w[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      pred[row] = s;
+      local += s * s;
+    }
+  }
+  if (lane == 0) part[wib] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += part[i];
+    atomicAdd(&sums[1], t);
+  }
+}
+
+// GROUSE with one deferred rank-1 update.  The update of step t,
+// U += (a p_t + d_t) wn_t^T (p_t = U w_t, d_t the scattered residual), is
+// not applied when it is decided: the next step gathers its Omega rows with
+// the pending term added (k_gather_pending), and its prediction pass applies
+// the pending update row by row while computing p_{t+1} = U' w_{t+1}
+// (k_pred_apply) -- one read and one write of U per update instead of a
+// read (prediction) plus a read-modify-write (update).  Both skip when
+// *flag is set (ill-conditioned attempt: the update stays pending).
+__global__ void k_gather_pending(const double* __restrict__ U, int r,
+                                 const int32_t* __restrict__ idx, int k, int pending, double a,
+                                 const double* __restrict__ pred, const double* __restrict__ d,
+                                 const double* __restrict__ wn, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * r) return;
+  const int i = (int)(e / r), c = (int)(e % r);
+  const int64_t row = idx[i];
+  double u = U[row * r + c];
+  if (pending) u = fma(fma(a, pred[row], d[row]), wn[c], u);
+  out[e] = u;
+}
+
+__global__ void k_pred_apply(double* __restrict__ U, int64_t v, int r, const double* __restrict__ w,
+                             double* __restrict__ pred, double* __restrict__ sums, double a,
+                             const double* __restrict__ d, const double* __restrict__ wn,
+                             const int32_t* __restrict__ flag) {
+  if (*flag) return;
+  __shared__ double part[32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
+  double local = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + wib; row < v;
+       row += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    double* u = U + row * r;
+    const double coef = fma(a, pred[row], d[row]);
+    double s = 0.0;
+    for (int c = lane; c < r; c += 32) {
+      const double un = fma(coef, wn[c], u[c]);
+      u[c] = un;
+      s = fma(un, w[c], s);
+    }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
       pred[row] = s;
@@ -581,19 +878,6 @@ __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restr
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_rapid_stats(const double* x, int n, int n1, const int16_t* orders,
-                               const int32_t* omegas, int64_t L, int k, double* t_out,
-                               unsigned long long* deg_key, cudaStream_t s) {
-  for (int64_t base = 0; base < L; base += 65535) {
-    const int64_t cnt = L - base < 65535 ? L - base : 65535;
-    dim3 grid((unsigned)((k + 255) / 256), (unsigned)cnt);
-    k_rapid_stats<<<grid, 256, n * sizeof(int16_t), s>>>(x, n, n1, orders + base * n,
-                                                          omegas + base * k, k, t_out + base * k,
-                                                          deg_key);
-  }
-  return cudaGetLastError();
-}
-
 cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
                         const double* vals, double* G, int64_t B, cudaStream_t s) {
   const int nt = (r + 1 + kGT - 1) / kGT;
@@ -622,12 +906,68 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s) {
-  const size_t smem = (size_t)(kPW * kPW + (size_t)(r + kPW) * kPW) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
+  // few systems (GROUSE: one per update): a 512-thread CTA hides more of the
+  // L2 latency of the trailing updates; batches: 256 threads, several CTAs / SM
+  if (B < 148) {
+    cudaError_t e = cudaFuncSetAttribute(k_chol_solve<512>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_chol_solve<512><<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, resid2);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(k_chol_solve<256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_chol_solve<256><<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, resid2);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
+                            cudaStream_t s) {
+  const int64_t n = v * kpad;
+  k_u_planes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, v, r, kpad, planes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w_rows(const float* W, int64_t B, int r, int kpad, __half* wA, float* descale,
+                          cudaStream_t s) {
+  k_w_rows<<<(unsigned)((B + 7) / 8), 256, 0, s>>>(W, B, r, kpad, wA, descale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, double* out,
+                                cudaStream_t s) {
+  k_max_finalize<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(enc, B, mu, out);
+  return cudaGetLastError();
+}
+
+size_t cg_smem_bytes(int r) {
+  const int R = (r + kCgCtas - 1) / kCgCtas;
+  return ((size_t)R * r + r + 6 * (size_t)R + 6 * kCgCtas + 2 * (kCgThreads / 32)) * sizeof(double);
+}
+
+bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
+
+cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
+                            double tol, cudaStream_t s) {
+  const size_t smem = cg_smem_bytes(r);
+  cudaError_t e = cudaFuncSetAttribute(k_cg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  k_chol_solve<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, resid2);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kCgCtas);
+  cfg.blockDim = dim3(kCgThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCgCtas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_cg_solve, G, r, w_out, flag, resid2, tol);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
@@ -651,6 +991,24 @@ cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, doub
   int64_t blocks = (v + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_pred<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_pending(const double* U, int r, const int32_t* idx, int k, int pending,
+                                  double a, const double* pred, const double* d, const double* wn,
+                                  double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)k * r;
+  k_gather_pending<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, r, idx, k, pending, a, pred,
+                                                                   d, wn, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, double* pred,
+                              double* sums, double a, const double* d, const double* wn,
+                              const int32_t* flag, cudaStream_t s) {
+  int64_t blocks = (v + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_pred_apply<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, a, d, wn, flag);
   return cudaGetLastError();
 }
 

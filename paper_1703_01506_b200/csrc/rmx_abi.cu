@@ -222,6 +222,35 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   return lay;
 }
 
+// RapidPT completion tiles (K4 on tcgen05): fp16 S-only pipeline over
+// B permutation rows x v voxels with K = r.  Returns stages = 0 when r does
+// not fit the resident A tile.
+NaiveLayout complete_layout(int64_t v, int r, int64_t B, int sm_count) {
+  NaiveLayout lay{};
+  lay.kpad = (r + 15) / 16 * 16;
+  lay.vt = 2 * kTileV;
+  lay.n_vtiles = (int)((v + lay.vt - 1) / lay.vt);
+  lay.cg = lay.kpad >= 192 ? 2 : 1;
+  if (!pick_pipeline(lay.cg, lay.kpad, &lay.bk, &lay.stages)) {
+    lay.cg = 1;
+    if (!pick_pipeline(1, lay.kpad, &lay.bk, &lay.stages)) {
+      lay.stages = 0;
+      return lay;
+    }
+  }
+  lay.groups = 4;
+  const int tile_perms = kTileM * lay.cg;
+  lay.n_mtiles = (int)((B + tile_perms - 1) / tile_perms);
+  const int n_clusters = std::max(1, sm_count / lay.cg);
+  // chunks: enough units for the persistent grid to balance (>= 6 per cluster)
+  int c = 1;
+  while (c < lay.n_vtiles && (int64_t)lay.n_mtiles * c < 6LL * n_clusters) c *= 2;
+  lay.tiles_per_chunk = (lay.n_vtiles + c - 1) / c;
+  lay.n_chunks = (lay.n_vtiles + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
+  lay.grid = lay.cg * (int)std::min<int64_t>(n_clusters, (int64_t)lay.n_mtiles * lay.n_chunks);
+  return lay;
+}
+
 namespace {
 
 int gcd_i(int x, int y) {
@@ -574,6 +603,14 @@ int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const i
   return rmx_naive_finish(x, v, n, n1, orders, L, two_sided, max_out, argmax_out, workspace,
                           workspace_bytes, stream, st, stats);
 }
+
+}  // extern "C"
+
+namespace rmx {
+int golden_stride_public(int T) { return golden_stride(T); }
+}  // namespace rmx
+
+extern "C" {
 
 // Host buffers in, host results out, with the 8 B/entry upload of X overlapped
 // with the engine: X is copied chunk by chunk (K1's voxel chunks) on a copy

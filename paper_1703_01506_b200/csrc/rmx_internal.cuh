@@ -76,6 +76,8 @@ struct NaiveLayout {
 };
 
 NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count);
+NaiveLayout complete_layout(int64_t v, int r, int64_t B, int sm_count);
+int golden_stride_public(int T);
 
 struct PrepArgs {
   const double* x;
@@ -108,6 +110,13 @@ struct TfillArgs {
   uint32_t* best_t;  // [L] running best t~ per permutation (order-encoded, 0 = none)
   NaiveCounters* counters;
   float* dbg_t;  // [L][v] when debugging
+  // RapidPT completion (MODE 1): A = W rows, max of W U^T + sigma z
+  const __half* wA;        // [L][kpad] fp16, row p scaled by 1 / wdescale[p]
+  const float* wdescale;   // [L]: power-of-2 descale (incl. the U planes' scale)
+  uint32_t* maxenc;        // [L] order-encoded running max
+  float sigma;
+  uint64_t seed;
+  int64_t perm_base;
 };
 
 struct RefineArgs {
@@ -148,6 +157,8 @@ cudaError_t launch_pairs(const double* x, int64_t v, int n, int n1, const int16_
 // tfill_tc.cu
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s);
+cudaError_t launch_complete_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
+                               int two_sided, cudaStream_t s);
 // voxel range [v0, v1) covered by K1 chunk c
 void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t* v1);
 

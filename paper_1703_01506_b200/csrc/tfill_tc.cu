@@ -29,6 +29,7 @@
 #include <cfloat>
 #include <mutex>
 
+#include "philox.cuh"
 #include "rmx_internal.cuh"
 #include "sm100.cuh"
 
@@ -292,11 +293,18 @@ __device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, boo
 // S_q = sum_{group 1} zq exactly and S = inv[j] * S_q: the same S-only tile
 // (256 voxels) as fp16, at twice the MMA rate and half the operand bytes.
 // The refinement band covers the quantisation rigorously (band_abs).
+//
+// MODE 1 (RapidPT completion, K4): the same fp16 hi/lo S-only pipeline with
+// A = the coefficient rows W (fp16, power-of-2 row scales) and B = the basis
+// planes [U_hi | U_lo]; the epilogue adds sigma z (Philox, philox.cuh) to the
+// completed column and keeps each permutation's running max.
 template <int CG, int BK, int STAGES, int EPI_WARPS, bool TWO_SIDED, bool ALPHA0, bool DEBUG,
-          bool I8>
+          bool I8, int MODE>
 __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     k_tfill_tc(const __grid_constant__ CUtensorMap pmap, const TfillArgs a) {
   static_assert(!I8 || ALPHA0, "int8 tiles are S-only (balanced groups)");
+  static_assert(MODE == 0 || (ALPHA0 && !I8 && !DEBUG), "completion tiles are fp16 S-only");
+  constexpr int LO_PLANE = MODE == 1 ? 1 : 2;  // plane index of the lo half
   constexpr bool SONLY = ALPHA0;
   constexpr int TV = SONLY ? 2 * kTileV : kTileV;  // voxels per tile
   constexpr int ELT = I8 ? 1 : 2;                   // operand bytes per element
@@ -389,8 +397,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
               if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
               if (SONLY) {  // this CTA's 128 of the tile's 256 voxels, Z planes only
                 const int v0 = t * TV + (int)rank * kTileV;
-                tma_load_3d_2sm(dst, &pmap, &full[stage], kb, v0, 0);               // z_hi
-                tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, v0, 2);  // z_lo
+                tma_load_3d_2sm(dst, &pmap, &full[stage], kb, v0, 0);  // z_hi
+                tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, v0, LO_PLANE);  // z_lo
               } else {
                 tma_load_3d_2sm(dst, &pmap, &full[stage], kb, t * TV, (int)rank);  // z_hi | q_hi
                 tma_load_3d_2sm(dst + HALF_BYTES, &pmap, &full[stage], kb, t * TV,
@@ -399,8 +407,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
             } else {
               mbar_wait(&empty[stage], phase ^ 1);
               mbar_expect_tx(&full[stage], STAGE_BYTES);
-              tma_load_3d(dst, &pmap, &full[stage], kb, t * TV, 0);               // z_hi(, q_hi)
-              tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * TV, 2);  // z_lo(, q_lo)
+              tma_load_3d(dst, &pmap, &full[stage], kb, t * TV, 0);  // z_hi(, q_hi)
+              tma_load_3d(dst + HALF_BYTES, &pmap, &full[stage], kb, t * TV, LO_PLANE);  // z_lo
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -514,7 +522,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         uint8_t* rbase = a_mem + (row >> 3) * (kext * 8 * ELT) + (row & 7) * 16;
         for (int kc = 0; kc < kext / EPC; ++kc)
           *reinterpret_cast<uint4*>(rbase + kc * 128) = make_uint4(0, 0, 0, 0);
-        if (prow) {
+        if (MODE == 1) {  // A row = W[p] (fp16, kpad halves = kpad / 8 core-matrix rows)
+          if (prow) {
+            const uint4* src = reinterpret_cast<const uint4*>(a.wA + p * (int64_t)a.kpad);
+            for (int kc = 0; kc < a.kpad / 8; ++kc) *reinterpret_cast<uint4*>(rbase + kc * 128) = src[kc];
+          }
+        } else if (prow) {
           const int16_t* ord = a.orders + p * a.n;
           for (int i = 0; i < a.n1; ++i) {
             const int k = ord[i];
@@ -532,7 +545,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         else mbar_arrive(afull);
       }
       Top4 top;
-      top.reset(seed_key<TWO_SIDED>(a.best_t, p, prow, a, emax));
+      top.reset(MODE == 1 ? -FLT_MAX : seed_key<TWO_SIDED>(a.best_t, p, prow, a, emax));
+      float cmax = -FLT_MAX;  // MODE 1: running max of this row over the unit
+      const float wsc = (MODE == 1 && prow) ? a.wdescale[p] : 0.0f;
       float kthr = sonly_thr(top.k3, ec);  // S-only hit threshold on S^2
       unsigned rare_groups = 0;
       float* winv = inv_smem + ew * (COLGROUPS * 32);  // this warp's columns
@@ -570,6 +585,23 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           }
           tmem_ld_wait();
           const int gvalid = valid - gc;
+          if constexpr (MODE == 1) {
+            if (gvalid > 0 && prow) {
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                float z[4];
+                normals4(a.seed, a.perm_base + p, (jbase >> 2) + q4, z);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int c = 4 * q4 + e;
+                  float val = fmaf(a.sigma, z[e], __uint_as_float(sv[c]) * wsc);
+                  if (TWO_SIDED) val = fabsf(val);
+                  if (c < gvalid) cmax = fmaxf(cmax, val);
+                }
+              }
+            }
+            continue;
+          }
           if (I8) {  // S_q -> S = S_q * inv (packed; scales: broadcast shared loads)
 #pragma unroll
             for (int c4 = 0; c4 < 8; ++c4) {
@@ -616,6 +648,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           acc = 0;
           acc_phase ^= 1;
         }
+      }
+      if constexpr (MODE == 1) {
+        if (prow) atomicMax(a.maxenc + p, ord_enc(cmax));
+        continue;
       }
       if (lane == 0) {  // diagnostics: warp-groups that took the rare path / all
         atomicAdd(&a.counters->rare_groups, (unsigned long long)rare_groups);
@@ -665,10 +701,11 @@ size_t smem_bytes_for(int cg, int bk, int stages, int kpad, bool i8) {
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
 
-template <int CG, int BK, int STAGES, int EPI, bool TS, bool A0, bool DBG, bool I8 = false>
+template <int CG, int BK, int STAGES, int EPI, bool TS, bool A0, bool DBG, bool I8 = false,
+          int MODE = 0>
 cudaError_t launch_cfg_e(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
                          cudaStream_t s) {
-  auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG, I8>;
+  auto kern = k_tfill_tc<CG, BK, STAGES, EPI, TS, A0, DBG, I8, MODE>;
   const size_t smem = smem_bytes_for(CG, BK, STAGES, lay.kpad, I8);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -772,6 +809,23 @@ void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t
   *v1 = std::min<int64_t>(t1 * lay.vt, v);
 }
 
+// completion tiles: fp16 S-only configurations, 16 epilogue warps
+template <bool TS>
+cudaError_t dispatch_complete(const NaiveLayout& lay, const TfillArgs& a, const CUtensorMap& map,
+                              cudaStream_t s) {
+  if (lay.cg == 2) {
+    if (lay.bk == 64) {
+      if (lay.stages >= 6) return launch_cfg_e<2, 64, 6, 16, TS, true, false, false, 1>(lay, a, map, s);
+      return launch_cfg_e<2, 64, 4, 16, TS, true, false, false, 1>(lay, a, map, s);
+    }
+    if (lay.stages >= 7) return launch_cfg_e<2, 32, 7, 16, TS, true, false, false, 1>(lay, a, map, s);
+    return launch_cfg_e<2, 32, 4, 16, TS, true, false, false, 1>(lay, a, map, s);
+  }
+  if (lay.bk == 64) return launch_cfg_e<1, 64, 3, 16, TS, true, false, false, 1>(lay, a, map, s);
+  if (lay.stages >= 4) return launch_cfg_e<1, 32, 4, 16, TS, true, false, false, 1>(lay, a, map, s);
+  return launch_cfg_e<1, 32, 3, 16, TS, true, false, false, 1>(lay, a, map, s);
+}
+
 bool make_planes8_map(CUtensorMap* map, const uint8_t* planes, int64_t v, int kpad, int cg) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -784,6 +838,24 @@ bool make_planes8_map(CUtensorMap* map, const uint8_t* planes, int64_t v, int kp
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+cudaError_t launch_complete_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
+                               int two_sided, cudaStream_t s) {
+  // planes [2][v][kpad]: U_hi, U_lo; boxes of 256 / cg voxels of one plane
+  auto enc = get_encode();
+  if (!enc) return cudaErrorInvalidValue;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)lay.kpad, (cuuint64_t)a.v, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)lay.kpad * 2, (cuuint64_t)a.v * lay.kpad * 2};
+  cuuint32_t box[3] = {(cuuint32_t)lay.bk, (cuuint32_t)(2 * kTileV / lay.cg), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(planes), dims, strides, box,
+          estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          lay.bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return two_sided ? dispatch_complete<true>(lay, a, map, s) : dispatch_complete<false>(lay, a, map, s);
 }
 
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,

@@ -134,3 +134,27 @@ def test_trained_model_close_to_reference():
     assert s.min() > 0.999
     assert model.residual_std == pytest.approx(float(d["r1_sigma"]), rel=1e-3)
     assert counters["statistic_evaluations"] == int(d["r1_counters"][0])
+
+
+@pytest.mark.parametrize("v,r,B,two_sided", [(5000, 200, 300, False), (3001, 64, 130, True),
+                                             (20000, 400, 520, False)])
+def test_tensor_core_completion_matches_fp32(monkeypatch, v, r, B, two_sided):
+    """K4 on tcgen05 (sigma > 0): fp16 W x split-fp16 U^T accumulated in fp32,
+    against the fp32 CUDA-core kernel on the same Philox normals.  Bound:
+    |delta max_p| <= 2^-10 max_j sum_i |w_pi u_ji| (W's fp16 rounding)."""
+    import torch
+
+    from paper_1703_01506_b200 import rapid_engine as re
+
+    rng = np.random.default_rng(v + r)
+    q, _ = np.linalg.qr(rng.standard_normal((v, r)))
+    w = rng.standard_normal((B, r)) * np.sqrt(v / r) * rng.uniform(0.1, 3.0, (B, 1))
+    dev = torch.device("cuda", 0)
+    u32 = torch.from_numpy(q.astype(np.float32)).to(dev)
+    w32 = torch.from_numpy(w.astype(np.float32)).to(dev)
+    tc = re._complete_max(u32, w32, 17, 0.7, 0.25, 1703, two_sided).cpu().numpy()
+    monkeypatch.setenv("RMX_COMPLETE_FP32", "1")
+    ref = re._complete_max(u32, w32, 17, 0.7, 0.25, 1703, two_sided).cpu().numpy()
+    bound = 2.0 ** -10 * (np.abs(w) @ np.abs(q).T).max(axis=1) + 1e-5
+    assert np.all(np.isfinite(tc))
+    assert np.all(np.abs(tc - ref) <= bound), np.max(np.abs(tc - ref) / bound)
