@@ -26,25 +26,30 @@ namespace {
 
 // ------------------------------------------------------------------ K3a
 // A_b = [U[idx_b[0..k)] | vals_b]  (k x (r+1)), G_b = A_b^T A_b, full
-// (r+1)^2 row-major.  64x64 output tiles over the lower triangle, 4x4
-// micro-tiles per thread, rows streamed through smem 32 at a time.
+// (r+1)^2 row-major.  64x64 output tiles over the lower triangle, 64
+// threads with 8x8 register tiles (4 FMAs per shared load).  The system's
+// row ids are staged in smem once; gathered rows stream through a 3-stage
+// cp.async ring of 16-row chunks, so the loads of chunk c+2 are in flight
+// while chunk c is multiplied.  Optional split over the rows (K) with atomics.
 constexpr int kGT = 64;
-constexpr int kGK = 32;
+constexpr int kGK = 16;
+constexpr int kGS = 3;  // ring stages
+constexpr int kGThreads = 64;
 
-__device__ __forceinline__ double a_elem(const double* U, int64_t ldu, int r, const int32_t* idx,
-                                         const double* vals, int64_t b, int k, int row, int col) {
-  if (row >= k || col > r) return 0.0;
-  const int64_t g = idx ? (int64_t)idx[b * k + row] : (int64_t)row;
-  if (col == r) return vals ? vals[b * k + row] : 0.0;
-  return U[g * ldu + col];
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int64_t ldu, int r,
-                                              const int32_t* __restrict__ idx, int k,
-                                              const double* __restrict__ vals, double* __restrict__ G,
-                                              int rows_per_split) {
-  __shared__ double As[kGK][kGT + 1];
-  __shared__ double Bs[kGK][kGT + 1];
+__global__ void __launch_bounds__(kGThreads) k_gram(const double* __restrict__ U, int64_t ldu,
+                                                    int r, const int32_t* __restrict__ idx, int k,
+                                                    const double* __restrict__ vals,
+                                                    double* __restrict__ G, int rows_per_split) {
+  extern __shared__ __align__(16) double gsm[];
+  double (*As)[kGK][kGT] = reinterpret_cast<double (*)[kGK][kGT]>(gsm);
+  double (*Bs)[kGK][kGT] = reinterpret_cast<double (*)[kGK][kGT]>(gsm + kGS * kGK * kGT);
+  int32_t* rid = reinterpret_cast<int32_t*>(gsm + 2 * kGS * kGK * kGT);
   const int64_t b = blockIdx.y;
   // lower-triangle tile index -> (ti, tj), tj <= ti
   int ti = 0, rem = blockIdx.x;
@@ -53,48 +58,90 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ U, int6
     ++ti;
   }
   const int tj = rem;
+  const bool diag = ti == tj;
   const int i0 = ti * kGT, j0 = tj * kGT;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4] = {};
+  const int tid = threadIdx.x;
+  const int tx = tid & 7, ty = tid >> 3;
   const int kbeg = blockIdx.z * rows_per_split;
   const int kend = min(k, kbeg + rows_per_split);
-  for (int k0 = kbeg; k0 < kend; k0 += kGK) {
-    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
-      const int rr = e / kGT, cc = e % kGT;
-      const bool in = k0 + rr < kend;
-      As[rr][cc] = in ? a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, i0 + cc) : 0.0;
-      Bs[rr][cc] = in ? a_elem(U, ldu, r, idx, vals, b, k, k0 + rr, j0 + cc) : 0.0;
-    }
-    __syncthreads();
+  const int nrows = max(0, kend - kbeg);
+  for (int i = tid; i < nrows; i += kGThreads) rid[i] = idx ? idx[b * k + kbeg + i] : kbeg + i;
+  __syncthreads();
+  const double* vb = vals ? vals + b * k : nullptr;
+  // chunk c -> ring slot c % kGS; thread fills column tid of 16 rows (A, B)
+  auto issue = [&](int c) {
+    const int slot = c % kGS;
+    const int ca = i0 + tid, cb = j0 + tid;
 #pragma unroll 4
-    for (int kk = 0; kk < kGK; ++kk) {
-      double av[4], bv[4];
+    for (int rr = 0; rr < kGK; ++rr) {
+      const int row = c * kGK + rr;  // relative to kbeg
+      double* da = &As[slot][rr][tid];
+      double* db = &Bs[slot][rr][tid];
+      if (row < nrows) {
+        const double* urow = U + (int64_t)rid[row] * ldu;
+        if (ca < r) cp_async8(da, urow + ca);
+        else *da = (ca == r && vb) ? vb[kbeg + row] : 0.0;
+        if (!diag) {
+          if (cb < r) cp_async8(db, urow + cb);
+          else *db = (cb == r && vb) ? vb[kbeg + row] : 0.0;
+        }
+      } else {
+        *da = 0.0;
+        if (!diag) *db = 0.0;
+      }
+    }
+  };
+  double acc[8][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        av[q] = As[kk][ty * 4 + q];
-        bv[q] = Bs[kk][tx * 4 + q];
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[q][u] = 0.0;
+  const int nchunks = (nrows + kGK - 1) / kGK;
+  for (int c = 0; c < kGS - 1; ++c) {
+    if (c < nchunks) issue(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGS - 2) : "memory");
+    __syncthreads();  // chunk c landed for every thread; slot (c-1) % kGS is free
+    if (c + kGS - 1 < nchunks) issue(c + kGS - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const int slot = c % kGS;
+    const double (*Ap)[kGT] = As[slot];
+    const double (*Bp)[kGT] = diag ? As[slot] : Bs[slot];
+#pragma unroll 2
+    for (int kk = 0; kk < kGK; ++kk) {
+      double a[8], bb[8];
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const double2 av = *reinterpret_cast<const double2*>(&Ap[kk][ty * 8 + q]);
+        const double2 bv = *reinterpret_cast<const double2*>(&Bp[kk][tx * 8 + q]);
+        a[q] = av.x;
+        a[q + 1] = av.y;
+        bb[q] = bv.x;
+        bb[q + 1] = bv.y;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 8; ++q)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) acc[q][s] += av[q] * bv[s];
+        for (int u = 0; u < 8; ++u) acc[q][u] = fma(a[q], bb[u], acc[q][u]);
     }
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   const int ld = r + 1;
   double* Gb = G + b * (int64_t)ld * ld;
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 8; ++q)
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int i = i0 + ty * 4 + q, j = j0 + tx * 4 + s;
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + ty * 8 + q, j = j0 + tx * 8 + u;
       if (i < ld && j < ld && j <= i) {
         if (gridDim.z == 1) {
-          Gb[(int64_t)i * ld + j] = acc[q][s];
-          if (i != j) Gb[(int64_t)j * ld + i] = acc[q][s];
+          Gb[(int64_t)i * ld + j] = acc[q][u];
+          if (i != j) Gb[(int64_t)j * ld + i] = acc[q][u];
         } else {  // split-K partial sums (G zeroed by the launcher)
-          atomicAdd(&Gb[(int64_t)i * ld + j], acc[q][s]);
-          if (i != j) atomicAdd(&Gb[(int64_t)j * ld + i], acc[q][s]);
+          atomicAdd(&Gb[(int64_t)i * ld + j], acc[q][u]);
+          if (i != j) atomicAdd(&Gb[(int64_t)j * ld + i], acc[q][u]);
         }
       }
     }
@@ -548,14 +595,20 @@ __global__ void __launch_bounds__(256) k_complete_max(
     const float* __restrict__ U, int64_t v, int r, int rpad, const float* __restrict__ W,
     int64_t B, int64_t perm_base, float sigma, double mu, uint64_t seed, int two_sided,
     const float* __restrict__ znoise, const double* __restrict__ base,
-    double* __restrict__ max_out) {
+    double* __restrict__ max_out, uint32_t* __restrict__ max_enc) {
+  // grid.y splits the voxels; with gridDim.y > 1 the per-block maxima meet
+  // in max_enc (order-encoded atomicMax, decoded by k_max_finalize)
   __shared__ float Ws[kCR][kCP];
   __shared__ float Us[kCR][kCV + 4];
   __shared__ float red[16][kCP];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t p0 = (int64_t)blockIdx.x * kCP;
   float best[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-  for (int64_t j0 = 0; j0 < v; j0 += kCV) {
+  const int64_t vtiles = (v + kCV - 1) / kCV;
+  const int64_t tper = (vtiles + gridDim.y - 1) / gridDim.y;
+  const int64_t jbeg = (int64_t)blockIdx.y * tper * kCV;
+  const int64_t jend = min(v, jbeg + tper * kCV);
+  for (int64_t j0 = jbeg; j0 < jend; j0 += kCV) {
     float acc[4][8] = {};
     for (int r0 = 0; r0 < rpad; r0 += kCR) {
       for (int e = threadIdx.x; e < kCR * kCP; e += 256) {
@@ -615,7 +668,14 @@ __global__ void __launch_bounds__(256) k_complete_max(
     float m = -FLT_MAX;
     for (int t = 0; t < 16; ++t) m = fmaxf(m, red[t][threadIdx.x]);
     const int64_t p = p0 + threadIdx.x;
-    if (p < B) max_out[p] = (double)m + mu;
+    if (p < B) {
+      if (max_enc) {
+        const uint32_t bits = __float_as_uint(m);
+        atomicMax(max_enc + p, (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u));
+      } else {
+        max_out[p] = (double)m + mu;
+      }
+    }
   }
 }
 
@@ -885,8 +945,8 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
   // split the row (K) dimension when the batch alone cannot fill the GPU
   int splits = 1;
   const int64_t blocks = (int64_t)ntiles * B;
-  if (blocks < 2 * 148) {
-    splits = (int)std::min<int64_t>((2 * 148 + blocks - 1) / blocks, std::max(1, k / 64));
+  if (blocks < 6 * 148) {  // 64-thread CTAs: several per SM
+    splits = (int)std::min<int64_t>((6 * 148 + blocks - 1) / blocks, std::max(1, k / 64));
     splits = std::max(1, std::min(splits, 4096));
   }
   const int rps = ((k + splits - 1) / splits + kGK - 1) / kGK * kGK;
@@ -895,9 +955,15 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
     cudaError_t e = cudaMemsetAsync(G, 0, (size_t)B * (r + 1) * (r + 1) * sizeof(double), s);
     if (e != cudaSuccess) return e;
   }
+  const size_t smem = (size_t)2 * kGS * kGK * kGT * sizeof(double) + (size_t)rps * sizeof(int32_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   for (int64_t base = 0; base < B; base += 65535) {
     const int64_t cnt = B - base < 65535 ? B - base : 65535;
-    k_gram<<<dim3(ntiles, (unsigned)cnt, (unsigned)splits), 256, 0, s>>>(
+    k_gram<<<dim3(ntiles, (unsigned)cnt, (unsigned)splits), kGThreads, smem, s>>>(
         U, ldu, r, idx ? idx + base * k : nullptr, k, vals ? vals + base * k : nullptr,
         G + base * (int64_t)(r + 1) * (r + 1), rps);
   }
@@ -975,8 +1041,25 @@ cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W
                                 int two_sided, const float* znoise, const double* base,
                                 double* max_out, cudaStream_t s) {
   const int rpad = (r + kCR - 1) / kCR * kCR;
-  k_complete_max<<<(unsigned)((B + kCP - 1) / kCP), 256, 0, s>>>(
-      U, v, r, rpad, W, B, perm_base, (float)sigma, mu, seed, two_sided, znoise, base, max_out);
+  const int64_t bx = (B + kCP - 1) / kCP;
+  const int64_t vtiles = (v + kCV - 1) / kCV;
+  // few permutation blocks (training's shift estimators: B = ell): split the
+  // voxels too so that every SM works
+  const int vs = (int)std::min<int64_t>(vtiles, std::max<int64_t>(1, (4 * 148 + bx - 1) / bx));
+  uint32_t* enc = nullptr;
+  if (vs > 1) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&enc), (size_t)B * 4, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(enc, 0, (size_t)B * 4, s);
+    if (e != cudaSuccess) return e;
+  }
+  k_complete_max<<<dim3((unsigned)bx, (unsigned)vs), 256, 0, s>>>(
+      U, v, r, rpad, W, B, perm_base, (float)sigma, mu, seed, two_sided, znoise, base, max_out,
+      enc);
+  if (enc) {
+    k_max_finalize<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(enc, B, mu, max_out);
+    cudaFreeAsync(enc, s);
+  }
   return cudaGetLastError();
 }
 
