@@ -170,3 +170,39 @@ def test_i8_near_ties_and_outliers_bit_exact(oracle_mod, k1_mode):
         assert res.stats["overflow_perms"] > 0
         assert np.array_equal(res.maxima, mx)
         assert np.array_equal(res.argmax, am)
+
+
+def test_subjects_beyond_the_tensor_tile_use_the_exact_path(oracle_mod):
+    """n > ~640: the A tile no longer fits next to the TMA ring; the engine
+    runs the exhaustive fp64 path (still on the GPU) with the same bits."""
+    x = _data(300, 350, 350, 31)
+    plan = rmx.PermutationPlan(41, 24, 700)
+    res = rmx.run_naive_ex(x, plan, two_sided=True)
+    mx, am, _ = oracle_mod.naive_maxnull(x.values, 350, plan_orders(plan).astype(np.int64), True,
+                                         threads=8)
+    assert res.stats["overflow_perms"] == 24
+    assert np.array_equal(res.maxima, mx)
+    assert np.array_equal(res.argmax, am)
+
+
+def test_thread_count_has_no_effect():
+    """Reference contract (tests/test_naive.py:78-83): results are identical
+    for any thread count; here the parallelism is the GPU's."""
+    x = _data(2000, 12, 12, 5)
+    plan = rmx.PermutationPlan(8, 300, 24)
+    a, _, _ = rmx.run_naive(x, plan, threads=1)
+    b, _, _ = rmx.run_naive(x, plan, threads=7)
+    assert np.array_equal(a.maxima, b.maxima)
+
+
+def test_int8_pairs_many_tiles_and_chunks_bit_exact(oracle_mod):
+    """int8 CTA-pair tiles over several permutation tiles and voxel chunks,
+    uploaded and processed chunk by chunk from host memory."""
+    x = _data(20000, 128, 128, 9)
+    plan = rmx.PermutationPlan(12, 700, 256)
+    res = rmx.run_naive_ex(x, plan, two_sided=True)
+    assert res.stats["i8"] == 1 and res.stats["cg"] == 2 and res.stats["chunks"] > 1
+    mx, am, _ = oracle_mod.naive_maxnull(x.values, 128, plan_orders(plan).astype(np.int64), True,
+                                         threads=16)
+    assert np.array_equal(res.maxima, mx)
+    assert np.array_equal(res.argmax, am)
