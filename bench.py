@@ -12,10 +12,10 @@ ranks (weak in the sense of a fixed total L split N ways -> "strong").
 value: whole-job T-entries/s with inputs resident in HBM (CUDA events on the
        engine's stream, max over ranks).
 e2e:   the same metric through the public API (run_naive_ex / the sharded
-       entry) from host numpy buffers: H2D of X and the label matrix, compute,
-       D2H of maxima + argmax inside the timed region.  Label *generation*
-       (numpy SFC64 shuffles) is host input preparation, done once
-       and reported separately as label_gen_s.
+       entry) from host numpy buffers: H2D of X, the plan's labels generated on
+       the GPU (bit-identical to numpy's SFC64 shuffles, rng_kernels.cu),
+       compute, D2H of maxima + argmax, all inside the timed region.
+       label_gen_s reports the device label generation alone.
 --impl reference: the reference algorithm's CPU implementation (the bit-exact
        C port in oracle/, all host threads) on a bounded permutation sample of
        the same workload; rank 0 only.
@@ -201,18 +201,23 @@ def main():
 
     from paper_1703_01506_b200 import DataMatrix, PermutationPlan
     from paper_1703_01506_b200.datagen import make_data_torch
-    from paper_1703_01506_b200.labels import generate_orders
+    from paper_1703_01506_b200.labels import device_orders, generate_orders
     from paper_1703_01506_b200.shard import ShardedNaive, shard_bounds
 
     plan = PermutationPlan(cfg.plan_seed, L, n)
     lo, hi, per = shard_bounds(L, rank, world)
+    # the shard's label rows on the GPU (bit-identical to numpy's streams);
+    # timed once here for the report, and again inside every e2e step
+    device_orders(cfg.plan_seed, lo, min(hi, lo + 1024), n, device)  # warm the kernel
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    orders_host = generate_orders(cfg.plan_seed, lo, hi, n)
+    device_orders(cfg.plan_seed, lo, hi, n, device)
+    torch.cuda.synchronize()
     label_gen_s = time.perf_counter() - t0
 
     x_dev = make_data_torch(cfg, device)
     torch.cuda.synchronize()
-    sh = ShardedNaive(x_dev, cfg.n1, plan, cfg.two_sided, orders_host=orders_host)
+    sh = ShardedNaive(x_dev, cfg.n1, plan, cfg.two_sided)
     stream = torch.cuda.current_stream(device)
 
     l2_flush = None
@@ -321,12 +326,9 @@ def main():
     # ---------------- e2e through the public API from host buffers -----------
     e2e = None
     if not args.no_e2e:
-        from paper_1703_01506_b200.labels import _CACHE
         from paper_1703_01506_b200.naive_engine import run_naive_ex
 
         x_host = DataMatrix(x_dev.cpu().numpy(), cfg.n1, cfg.n2)
-        if world == 1:
-            _CACHE[(plan.master_seed, plan.count, plan.subjects)] = orders_host
         times = []
         for k in range(args.warmup + args.steps):
             barrier()
@@ -338,8 +340,8 @@ def main():
                 from paper_1703_01506_b200.hostmem import to_device
 
                 xd = to_device(x_host.values, device)
-                # ShardedNaive uploads this rank's label rows (H2D inside the region)
-                sh2 = ShardedNaive(xd, cfg.n1, plan, cfg.two_sided, orders_host=orders_host)
+                # ShardedNaive generates this rank's label rows on the GPU
+                sh2 = ShardedNaive(xd, cfg.n1, plan, cfg.two_sided)
                 m, a = sh2.step()
                 m.cpu(), a.cpu()
             torch.cuda.synchronize()
@@ -350,7 +352,8 @@ def main():
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": L * v / float(t[0]), "unit": UNIT,
-               "h2d_bytes_per_step": int(x_host.values.nbytes + orders_host.nbytes),
+               "h2d_bytes_per_step": int(x_host.values.nbytes),
+               "labels": "generated on the GPU inside the timed region (rmx_plan_orders)",
                "d2h_bytes_per_step": int(L * 12), "s_per_step": float(t[0]),
                "api": "paper_1703_01506_b200.run_naive_ex (N=1) / ShardedNaive (N>1)"}
 
@@ -360,6 +363,7 @@ def main():
         try:
             x_host_np = x_dev.cpu().numpy()
             threads = os.cpu_count() or 1
+            orders_host = generate_orders(cfg.plan_seed, 0, min(L, max(threads * 64, 256)), n)
             rate, text, thr, dt = cpu_sample(cfg, x_host_np, orders_host, args.cpu_seconds, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
                    "sample": text + f" in {dt:.1f}s; bit-exact C port of the reference "

@@ -127,6 +127,8 @@ int rmx_naive_tfill_debug(int64_t v, int32_t n, int32_t n1, const int16_t *order
  * max_host/argmax_host.  Synchronous.  Results and errors as
  * rmx_naive_maxnull.  Host buffers should be page-locked (cudaHostRegister)
  * for the overlap; pageable buffers work but serialise the copies.
+ * orders_host may be NULL when orders_dev already holds the labels (e.g.
+ * from rmx_plan_orders on the same stream). 
  * Replaces reference naive.py:60-109 run_naive end to end. */
 int rmx_naive_maxnull_host(const double *x_host, int64_t v, int32_t n, int32_t n1,
                            const int16_t *orders_host, int64_t L, int32_t two_sided,
@@ -134,6 +136,18 @@ int rmx_naive_maxnull_host(const double *x_host, int64_t v, int32_t n, int32_t n
                            int16_t *orders_dev, double *max_dev, int32_t *argmax_dev,
                            void *workspace, size_t workspace_bytes, void *stream,
                            rmx_status *st, rmx_naive_stats *stats);
+
+/* The reference's random streams on the device, bit-identical to numpy:
+ * row t of out (count x n, int16) = PermutationPlan(seed, ., n).shuffle(lo + t)
+ * (model.py:100-105: stream(seed, SHUFFLE, i).permutation(n), identity at 0). */
+int rmx_plan_orders(uint64_t seed, int64_t lo, int64_t count, int32_t n, int16_t *out,
+                    void *stream, rmx_status *st);
+/* row t of out (count x k, int32) = sort(stream(seed, domain, lo + t[, extra])
+ * .choice(v, k, replace=False)) (rapid.py:158-160, lrmc.py:237-241; extra < 0:
+ * no third key).  RMX_E_USAGE when numpy would take its tail-shuffle branch
+ * (v > 10000 and k > v / 50): the caller draws those on the host. */
+int rmx_omega_draws(uint64_t seed, int32_t domain, int64_t lo, int64_t count, int64_t extra,
+                    int64_t v, int32_t k, int32_t *out, void *stream, rmx_status *st);
 
 /* ---------------------------------------------------------------- exact fp64
  * Bit-exact statistic matrix (reference _welch_rows arithmetic):

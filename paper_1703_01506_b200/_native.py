@@ -64,6 +64,8 @@ EXPORTS = (
     "rmx_naive_workspace_bytes",
     "rmx_naive_maxnull",
     "rmx_naive_maxnull_host",
+    "rmx_plan_orders",
+    "rmx_omega_draws",
     "rmx_naive_prepare",
     "rmx_naive_tfill",
     "rmx_naive_finish",
@@ -104,6 +106,9 @@ _SIGS = {
                           ctypes.c_int),
     "rmx_naive_maxnull_host": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_plan_orders": ([ctypes.c_uint64, _i64, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
+    "rmx_omega_draws": ([ctypes.c_uint64, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _SP],
+                        ctypes.c_int),
     "rmx_naive_prepare": ([_vp, _i64, _i32, _i32, _i64, _vp, _sz, _vp, _SP], ctypes.c_int),
     "rmx_naive_tfill": ([_i64, _i32, _i32, _vp, _i64, _i32, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
     "rmx_naive_finish": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],

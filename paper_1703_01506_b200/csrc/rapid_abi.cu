@@ -254,6 +254,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // sums: 0 |r|^2 1 |pred|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
   DevBuf<double> G, w, vals, resid, pred, d, sums, wn, ug;
   DevBuf<int32_t> flag, idxbuf, pidx;
+  DevBuf<GrouseState> gst;
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
@@ -266,110 +267,101 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(idxbuf.alloc(k, s));
   RCUDA(pidx.alloc(k, s));
   RCUDA(ug.alloc((size_t)k * r, s));
+  RCUDA(gst.alloc(1, s));
   RCUDA(cudaMemsetAsync(d.p, 0, v * sizeof(double), s));
   RCUDA(cudaMemsetAsync(pred.p, 0, v * sizeof(double), s));
-  RCUDA(cudaMemsetAsync(wn.p, 0, r * sizeof(double), s));  // finite: 0 * wn in k_pred_apply
+  RCUDA(cudaMemsetAsync(wn.p, 0, r * sizeof(double), s));  // finite: 0 * wn in k_pred_apply_st
+  RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(GrouseState), s));
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
   const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
-  // the deferred rank-1 update U += (pend_a pred + d) wn^T (d nonzero on pidx)
-  bool pending = false;
-  double pend_a = 0.0;
-  auto flush = [&]() -> int {
-    if (!pending) return RMX_OK;
-    RCUDA(launch_grouse_update(u, v, r, pred.p, wn.p, pend_a, d.p, s));
-    RCUDA(launch_unscatter(pidx.p, k, d.p, s));
-    pending = false;
+  // One update, entirely on the device (lrmc.py:160-193): U_Omega with the
+  // deferred update, Gram, solve (cluster CG; Cholesky on the same G when CG
+  // does not converge), residual, p = U' w applying the deferred update, and
+  // k_grouse_post's decisions.  No host round trip: the host syncs only at
+  // the re-orthonormalisation cadence and at pass ends.
+  auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
+    const double step = 1.0 / (1.0 + (double)tglob / tau);
+    const double* trow = t + (int64_t)i * v;
+    RCUDA(launch_gather_pending_st(u, r, idx, k, gst.p, pred.p, d.p, wn.p, ug.p, s));
+    RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
+    RCUDA(launch_gram(ug.p, r, r, nullptr, k, vals.p, G.p, 1, s));
+    RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+    if (use_cg) {
+      RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13, s));
+      RCUDA(launch_chol_if_flag(G.p, r, w.p, flag.p, sums.p + 4, s));
+    } else {
+      RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
+    }
+    RCUDA(launch_resid(ug.p, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
+    RCUDA(launch_pred_apply_st(u, v, r, w.p, pred.p, sums.p, gst.p, d.p, wn.p, flag.p, s));
+    RCUDA(launch_grouse_post(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r, d.p,
+                             pidx.p, wn.p, final_omegas ? final_omegas + (int64_t)i * k : nullptr,
+                             s));
+    (void)p;
     return RMX_OK;
   };
-  int64_t tcount = 0;
+  auto read_state = [&](GrouseState* h) -> int {
+    RCUDA(cudaMemcpyAsync(h, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaStreamSynchronize(s));
+    return RMX_OK;
+  };
   int passes = 0, converged = 0;
-  for (int p = 0; p < max_passes; ++p) {
-    double rel_sum = 0.0;
-    for (int i = 0; i < ell; ++i) {
-      const double step = 1.0 / (1.0 + (double)tcount / tau);
-      const double* trow = t + (int64_t)i * v;
-      const int32_t* idx = omegas0 + ((int64_t)p * ell + i) * k;
-      double hs[8];
-      int32_t hflag = 0;
-      int attempt = 0;
-      for (;;) {
-        // U_Omega with the pending update, then the Gram of [U_Omega | t_Omega]
-        RCUDA(launch_gather_pending(u, r, idx, k, pending ? 1 : 0, pend_a, pred.p, d.p, wn.p,
-                                    ug.p, s));
-        RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
-        RCUDA(launch_gram(ug.p, r, r, nullptr, k, vals.p, G.p, 1, s));
-        // cluster CG first (the restricted Gram of a random row sample is
-        // well conditioned); Cholesky on the same G when CG does not converge
-        bool chol = !use_cg;
-        for (;;) {
-          RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
-          if (chol) RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
-          else RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13, s));
-          RCUDA(launch_resid(ug.p, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
-          // p = U' w with U' = U + pending (applied in the same pass); skipped
-          // (update stays pending) when the solve flagged the attempt
-          RCUDA(launch_pred_apply(u, v, r, w.p, pred.p, sums.p, pending ? pend_a : 0.0, d.p, wn.p,
-                                  flag.p, s));
-          RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
-          RCUDA(cudaMemcpyAsync(&hflag, flag.p, sizeof(hflag), cudaMemcpyDeviceToHost, s));
-          RCUDA(cudaStreamSynchronize(s));
-          if (chol || !hflag) break;
-          chol = true;
-        }
-        if (!hflag) break;
-        // ill-conditioned restriction: redraw from the same stream (lrmc.py:240-250)
-        if (++attempt >= 5 || !cb)
-          return rset(st, RMX_E_ILLCOND,
-                      "training column %d pass %d: restricted basis stayed ill-conditioned", i, p);
-        if (cb(user, i, p, attempt, host_idx.data()) != 0)
+  const int64_t total = (int64_t)max_passes * ell;
+  int64_t tglob = 0;
+  while (tglob < total) {
+    const int p = (int)(tglob / ell), i = (int)(tglob % ell);
+    if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob)) return rc;
+    ++tglob;
+    const bool reortho = tglob % 64 == 0, pass_end = tglob % ell == 0;
+    if (!reortho && !pass_end) continue;
+    GrouseState hs;
+    if (int rc = read_state(&hs)) return rc;
+    if (hs.halted) {
+      // ill-conditioned restriction at update h: redraw its Omega from the same
+      // stream (lrmc.py:240-250); updates after h were no-ops and are replayed
+      const int64_t h = hs.halt_step;
+      const int hp = (int)(h / ell), hi = (int)(h % ell);
+      bool ok = false;
+      for (int attempt = 1; attempt < 5 && cb; ++attempt) {
+        if (cb(user, hi, hp, attempt, host_idx.data()) != 0)
           return rset(st, RMX_E_USAGE, "omega callback failed");
         RCUDA(cudaMemcpyAsync(idxbuf.p, host_idx.data(), k * sizeof(int32_t),
                               cudaMemcpyHostToDevice, s));
-        idx = idxbuf.p;
+        RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(int), s));  // clear `halted`
+        if (int rc = enqueue(hp, hi, idxbuf.p, h)) return rc;
+        if (int rc = read_state(&hs)) return rc;
+        if (!hs.halted) {
+          ok = true;
+          break;
+        }
       }
-      if (pending) {  // applied by k_pred_apply
-        RCUDA(launch_unscatter(pidx.p, k, d.p, s));
-        pending = false;
-      }
-      const double resid_norm = std::sqrt(std::max(hs[0], 0.0));
-      const double pred_norm = std::sqrt(std::max(hs[1], 0.0));
-      const double t_norm = std::sqrt(std::max(hs[2], 0.0));
-      const double w_norm = std::sqrt(std::max(hs[5], 0.0));
-      bool do_update = !(step == 0.0 || resid_norm == 0.0);
-      if (do_update && (pred_norm == 0.0 || w_norm == 0.0)) do_update = false;
-      if (do_update && resid_norm <= 1e-14 * std::max(1.0, pred_norm)) do_update = false;
-      if (do_update) {
-        const double theta = step * std::atan(resid_norm / pred_norm);
-        pend_a = (std::cos(theta) - 1.0) / pred_norm;
-        const double bcoef = std::sin(theta) / resid_norm;
-        RCUDA(launch_scatter(idx, k, resid.p, bcoef, d.p, s));
-        RCUDA(launch_scale_copy(w.p, r, 1.0 / w_norm, wn.p, s));  // w / |w|
-        RCUDA(cudaMemcpyAsync(pidx.p, idx, k * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-        pending = true;
-      }
-      ++tcount;
-      rel_sum += t_norm > 0 ? resid_norm / t_norm : 0.0;
-      if (final_omegas)  // ends up holding the last executed pass (train_basis final_omegas)
-        RCUDA(cudaMemcpyAsync(final_omegas + (int64_t)i * k, idx, k * sizeof(int32_t),
-                              cudaMemcpyDeviceToDevice, s));
-      if (tcount % 64 == 0) {
-        if (int rc = flush()) return rc;
-        double drift = 0.0;
-        if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
-      }
+      if (!ok)
+        return rset(st, RMX_E_ILLCOND,
+                    "training column %d pass %d: restricted basis stayed ill-conditioned", hi, hp);
+      tglob = h + 1;  // replay the skipped updates
+      continue;
     }
-    const double rel = rel_sum / ell;
-    if (pass_resid) pass_resid[p] = rel;
-    passes = p + 1;
-    if (rel < tol) {
-      converged = 1;
-      break;
+    if (reortho) {  // lrmc.py:258-259: every 64 updates
+      RCUDA(launch_grouse_flush(u, v, r, pred.p, wn.p, gst.p, d.p, pidx.p, k, s));
+      double drift = 0.0;
+      if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+    }
+    if (pass_end) {
+      const double rel = hs.rel_sum / ell;
+      if (pass_resid) pass_resid[p] = rel;
+      passes = p + 1;
+      RCUDA(cudaMemsetAsync(&gst.p->rel_sum, 0, sizeof(double), s));
+      if (rel < tol) {
+        converged = 1;
+        break;
+      }
     }
   }
-  if (int rc = flush()) return rc;
+  RCUDA(launch_grouse_flush(u, v, r, pred.p, wn.p, gst.p, d.p, pidx.p, k, s));
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+  const int64_t tcount = (int64_t)passes * ell;
   if (passes_out) *passes_out = passes;
   if (converged_out) *converged_out = converged;
   if (updates_out) *updates_out = tcount;

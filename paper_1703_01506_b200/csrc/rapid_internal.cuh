@@ -16,6 +16,31 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 // (t.t - rhs.w, w.w, min L_ii, max L_ii); flag_b = 1 on a non-positive pivot
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s);
+// GROUSE step state kept on the device, so the update loop runs without a
+// host round trip per update (decisions by k_grouse_post).
+struct GrouseState {
+  int halted;      // a solve flagged ill-conditioning: later step kernels no-op
+  int halt_step;   // global update index that halted
+  int pending;     // a deferred rank-1 update (pend_a, d on pidx, wn) is pending
+  int pad;
+  double pend_a;
+  double rel_sum;  // sum over the pass of |r| / |t_Omega|
+};
+cudaError_t launch_gather_pending_st(const double* U, int r, const int32_t* idx, int k,
+                                     const GrouseState* st, const double* pred, const double* d,
+                                     const double* wn, double* out, cudaStream_t s);
+cudaError_t launch_pred_apply_st(double* U, int64_t v, int r, const double* w, double* pred,
+                                 double* sums, const GrouseState* st, const double* d,
+                                 const double* wn, const int32_t* flag, cudaStream_t s);
+cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
+                                cudaStream_t s);
+cudaError_t launch_grouse_post(GrouseState* st, const double* sums, const int32_t* flag,
+                               double step, int64_t step_index, const int32_t* idx, int k,
+                               const double* resid, const double* w, int r, double* d,
+                               int32_t* pidx, double* wn, int32_t* final_slot, cudaStream_t s);
+cudaError_t launch_grouse_flush(double* U, int64_t v, int r, const double* pred, const double* wn,
+                                GrouseState* st, double* d, const int32_t* pidx, int k,
+                                cudaStream_t s);
 // K4 on tcgen05: operand preparation and the max decode
 cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
                             cudaStream_t s);

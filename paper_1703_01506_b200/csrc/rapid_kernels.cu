@@ -193,8 +193,12 @@ __device__ __forceinline__ void chol_block32(double* D, double* rinv, double tin
 template <int NT>
 __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
-                                                   int32_t* __restrict__ flag,
-                                                   double* __restrict__ resid2) {
+                                                   int32_t* flag, double* __restrict__ resid2,
+                                                   const int32_t* gate = nullptr) {
+  // gate: run only when *gate != 0 (Cholesky fallback after a cluster-CG
+  // solve that did not converge, decided on the device)
+  if (gate && *gate == 0) return;
+  __syncthreads();  // every thread has read the gate before it is overwritten
   extern __shared__ double sm[];
   double* D = sm;                     // kPW x kPS: block / L_D (lower)
   double* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
@@ -778,6 +782,139 @@ __global__ void k_pred_apply(double* __restrict__ U, int64_t v, int r, const dou
   }
 }
 
+// ---- device-resident GROUSE step (no host round trip per update)
+__global__ void k_gather_pending_st(const double* __restrict__ U, int r,
+                                    const int32_t* __restrict__ idx, int k,
+                                    const GrouseState* __restrict__ st,
+                                    const double* __restrict__ pred, const double* __restrict__ d,
+                                    const double* __restrict__ wn, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * r) return;
+  const int i = (int)(e / r), c = (int)(e % r);
+  const int64_t row = idx[i];
+  double u = U[row * r + c];
+  if (st->pending) u = fma(fma(st->pend_a, pred[row], d[row]), wn[c], u);
+  out[e] = u;
+}
+
+__global__ void k_pred_apply_st(double* __restrict__ U, int64_t v, int r,
+                                const double* __restrict__ w, double* __restrict__ pred,
+                                double* __restrict__ sums, const GrouseState* __restrict__ st,
+                                const double* __restrict__ d, const double* __restrict__ wn,
+                                const int32_t* __restrict__ flag) {
+  if (st->halted || *flag) return;
+  const double a = st->pending ? st->pend_a : 0.0;  // not pending: d = 0, so coef = 0
+  __shared__ double part[32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
+  double local = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + wib; row < v;
+       row += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    double* u = U + row * r;
+    const double coef = fma(a, pred[row], d[row]);
+    double sacc = 0.0;
+    for (int c = lane; c < r; c += 32) {
+      const double un = fma(coef, wn[c], u[c]);
+      u[c] = un;
+      sacc = fma(un, w[c], sacc);
+    }
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) {
+      pred[row] = sacc;
+      local += sacc * sacc;
+    }
+  }
+  if (lane == 0) part[wib] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += part[i];
+    atomicAdd(&sums[1], t);
+  }
+}
+
+// The host's per-update decisions of lrmc.py:160-193, on the device: norms,
+// step angle, the deferred update's coefficients; unscatter the applied
+// update, scatter the new one.  A flagged solve halts the loop (the host
+// resamples at its next sync point).
+__global__ void __launch_bounds__(1024) k_grouse_post(
+    GrouseState* __restrict__ st, const double* __restrict__ sums, const int32_t* __restrict__ flag,
+    double step, int64_t step_index, const int32_t* __restrict__ idx, int k,
+    const double* __restrict__ resid, const double* __restrict__ w, int r, double* __restrict__ d,
+    int32_t* __restrict__ pidx, double* __restrict__ wn, int32_t* __restrict__ final_slot) {
+  __shared__ int skip, old_pending, do_update;
+  __shared__ double sb, sinvw, sa;
+  if (threadIdx.x == 0) {
+    skip = 0;
+    if (st->halted) {
+      skip = 1;
+    } else if (*flag) {
+      st->halted = 1;
+      st->halt_step = (int)step_index;
+      skip = 1;
+    } else {
+      const double resid_norm = sqrt(fmax(sums[0], 0.0));
+      const double pred_norm = sqrt(fmax(sums[1], 0.0));
+      const double t_norm = sqrt(fmax(sums[2], 0.0));
+      const double w_norm = sqrt(fmax(sums[5], 0.0));
+      int upd = !(step == 0.0 || resid_norm == 0.0);
+      if (upd && (pred_norm == 0.0 || w_norm == 0.0)) upd = 0;
+      if (upd && resid_norm <= 1e-14 * fmax(1.0, pred_norm)) upd = 0;
+      double a = 0.0, bcoef = 0.0;
+      if (upd) {
+        const double theta = step * atan(resid_norm / pred_norm);
+        a = (cos(theta) - 1.0) / pred_norm;
+        bcoef = sin(theta) / resid_norm;
+      }
+      old_pending = st->pending;
+      do_update = upd;
+      sa = a;
+      sb = bcoef;
+      sinvw = upd ? 1.0 / w_norm : 0.0;
+      st->rel_sum += t_norm > 0.0 ? resid_norm / t_norm : 0.0;
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  if (old_pending)  // applied by k_pred_apply_st in this step
+    for (int i = threadIdx.x; i < k; i += blockDim.x) d[pidx[i]] = 0.0;
+  __syncthreads();
+  if (do_update) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      d[idx[i]] = sb * resid[i];
+      pidx[i] = idx[i];
+    }
+    for (int c = threadIdx.x; c < r; c += blockDim.x) wn[c] = w[c] * sinvw;
+  }
+  if (final_slot)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) final_slot[i] = idx[i];
+  if (threadIdx.x == 0) {
+    st->pending = do_update;
+    st->pend_a = sa;
+  }
+}
+
+// apply a pending update to all of U (before a re-orthonormalisation)
+__global__ void k_grouse_flush_update(double* __restrict__ U, int64_t v, int r,
+                                      const double* __restrict__ pred,
+                                      const double* __restrict__ wn,
+                                      const GrouseState* __restrict__ st,
+                                      const double* __restrict__ d) {
+  if (!st->pending) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= v * r) return;
+  const int64_t row = e / r;
+  const int c = (int)(e % r);
+  U[e] = fma(fma(st->pend_a, pred[row], d[row]), wn[c], U[e]);
+}
+
+__global__ void k_grouse_flush_done(GrouseState* __restrict__ st, double* __restrict__ d,
+                                    const int32_t* __restrict__ pidx, int k) {
+  if (!st->pending) return;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) d[pidx[i]] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) st->pending = 0;
+}
+
 // U += dir (w/|w|)^T, dir = a * pred + b * scatter(resid over idx)
 __global__ void k_grouse_update(double* __restrict__ U, int64_t v, int r,
                                 const double* __restrict__ pred, const double* __restrict__ wn,
@@ -1092,6 +1229,52 @@ cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, doub
   int64_t blocks = (v + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_pred_apply<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, a, d, wn, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_pending_st(const double* U, int r, const int32_t* idx, int k,
+                                     const GrouseState* st, const double* pred, const double* d,
+                                     const double* wn, double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)k * r;
+  k_gather_pending_st<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, r, idx, k, st, pred, d,
+                                                                      wn, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pred_apply_st(double* U, int64_t v, int r, const double* w, double* pred,
+                                 double* sums, const GrouseState* st, const double* d,
+                                 const double* wn, const int32_t* flag, cudaStream_t s) {
+  int64_t blocks = (v + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_pred_apply_st<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, st, d, wn, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
+                                cudaStream_t s) {
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_chol_solve<512>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_chol_solve<512><<<1, 512, smem, s>>>(G, r, w_out, flag, resid2, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouse_post(GrouseState* st, const double* sums, const int32_t* flag,
+                               double step, int64_t step_index, const int32_t* idx, int k,
+                               const double* resid, const double* w, int r, double* d,
+                               int32_t* pidx, double* wn, int32_t* final_slot, cudaStream_t s) {
+  k_grouse_post<<<1, 1024, 0, s>>>(st, sums, flag, step, step_index, idx, k, resid, w, r, d, pidx,
+                                   wn, final_slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouse_flush(double* U, int64_t v, int r, const double* pred, const double* wn,
+                                GrouseState* st, double* d, const int32_t* pidx, int k,
+                                cudaStream_t s) {
+  const int64_t total = v * r;
+  k_grouse_flush_update<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, v, r, pred, wn, st, d);
+  k_grouse_flush_done<<<1, 1024, 0, s>>>(st, d, pidx, k);
   return cudaGetLastError();
 }
 

@@ -626,8 +626,7 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                            rmx_status* st, rmx_naive_stats* stats) {
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
-  if (!x_host || !orders_host || !max_host || !argmax_host || !x_dev || !orders_dev || !max_dev ||
-      !argmax_dev)
+  if (!x_host || !max_host || !argmax_host || !x_dev || !orders_dev || !max_dev || !argmax_dev)
     return set_status(st, RMX_E_USAGE, "null buffer");
   Ws ws;
   if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
@@ -642,7 +641,8 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
   };
   if (ws.lay.stages == 0) {  // exhaustive exact path: nothing to overlap
     RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
-    RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
+    if (orders_host)
+      RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
     if (int rc = rmx_naive_maxnull(x_dev, v, n, n1, orders_dev, L, two_sided, max_dev, argmax_dev,
                                    workspace, workspace_bytes, stream, st, stats))
       return rc;
@@ -680,7 +680,10 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
   RMX_CUDA(cudaEventRecord(e0, s));
   for (cudaStream_t x : {S.cp, S.pp, S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e0, 0));
   // copies: labels first (K1 needs them), then X chunk by chunk
-  RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, S.cp));
+  // (orders_host == NULL: the caller generated the labels on the device,
+  // stream-ordered before this call)
+  if (orders_host)
+    RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, S.cp));
   RMX_CUDA(cudaEventRecord(e_ord, S.cp));
   for (int c = 0; c < nc; ++c) {
     int64_t v0, v1;
@@ -713,6 +716,32 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                                 workspace, workspace_bytes, stream, st, stats))
     return rc;
   return finish_host();
+}
+
+int rmx_plan_orders(uint64_t seed, int64_t lo, int64_t count, int32_t n, int16_t* out,
+                    void* stream, rmx_status* st) {
+  clear_status(st);
+  if (n < 1 || n > 32767 || lo < 0 || count < 0 || lo + count > 0xFFFFFFFFLL || !out)
+    return set_status(st, RMX_E_USAGE, "plan rows [%lld, %lld) of n=%d not representable",
+                      (long long)lo, (long long)(lo + count), n);
+  RMX_CUDA(launch_plan_orders(seed, lo, count, n, out, static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
+}
+
+int rmx_omega_draws(uint64_t seed, int32_t domain, int64_t lo, int64_t count, int64_t extra,
+                    int64_t v, int32_t k, int32_t* out, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (k < 1 || v < k || v > 0xFFFFFFFFLL || lo < 0 || lo + count > 0xFFFFFFFFLL || extra > 0xFFFFFFFFLL ||
+      domain < 0 || !out)
+    return set_status(st, RMX_E_USAGE, "observation draws out of range (v=%lld, k=%d)",
+                      (long long)v, k);
+  if (v > 10000 && k > v / 50)  // numpy's tail-shuffle branch: not on the device
+    return set_status(st, RMX_E_USAGE, "k=%d of v=%lld takes numpy's tail-shuffle branch", k,
+                      (long long)v);
+  RMX_CUDA(launch_omega_draws(seed, (uint32_t)domain, lo, count, extra >= 0 ? 1 : 0,
+                              (uint32_t)(extra >= 0 ? extra : 0), (uint32_t)v, k, out,
+                              static_cast<cudaStream_t>(stream)));
+  return RMX_OK;
 }
 
 int rmx_tstat_exact(const double* x, int64_t v, int32_t n, int32_t n1, const int16_t* orders,

@@ -164,4 +164,11 @@ void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t
 
 int device_sm_count();
 
+// rng_kernels.cu: the reference's streams on the device
+cudaError_t launch_plan_orders(uint64_t seed, int64_t lo, int64_t count, int n, int16_t* out,
+                               cudaStream_t s);
+cudaError_t launch_omega_draws(uint64_t seed, uint32_t domain, int64_t lo, int64_t count,
+                               int has_extra, uint32_t extra, uint32_t v, int k, int32_t* out,
+                               cudaStream_t s);
+
 }  // namespace rmx

@@ -6,9 +6,11 @@ order matters for the bit-exact refinement, which sums in that order, as the
 reference's fancy-indexed blocks do; reference model.py:65-69).
 
 Generating a shuffle costs ~26-30 us of host time per permutation (numpy
-SeedSequence + SFC64), i.e. ~3 s for L = 1e5 on one core, so the
-matrix is generated once per plan with a process pool and cached in host
-memory.  bench.py reports this cost separately from the device clock.
+SeedSequence + SFC64), i.e. ~3 s for L = 1e5 on one core.  The
+engine therefore generates the rows on the GPU (``device_orders``: the same
+streams restated bit for bit in rng_kernels.cu, ~ms for 1e5 rows); the host
+path (``plan_orders``: forked workers, cached) serves the CPU-side users
+(the oracle, materialised-T bookkeeping, the reference arm).
 """
 
 from __future__ import annotations
@@ -61,6 +63,29 @@ def plan_orders(plan, lo: int = 0, hi: int | None = None) -> np.ndarray:
             _, old = _CACHE.popitem(last=False)
             _CACHE_BYTES -= old.nbytes
     return full[lo:hi]
+
+
+def device_orders(seed: int, lo: int, hi: int, n: int, device, stream=None):
+    """Rows [lo, hi) of the plan's order matrix generated on the GPU
+    (rmx_plan_orders: numpy's SeedSequence -> SFC64 -> permutation restated
+    bit for bit), as an (hi - lo, n) int16 CUDA tensor."""
+    import ctypes
+
+    import torch
+
+    from . import _native as nat
+
+    if n > 32767:
+        raise UsageError(f"subject count {n} exceeds the int16 label format")
+    out = torch.empty((max(hi - lo, 0), n), dtype=torch.int16, device=device)
+    if hi > lo:
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        st = nat.Status()
+        rc = nat.load().rmx_plan_orders(ctypes.c_uint64(int(seed) & ((1 << 64) - 1)), int(lo),
+                                        int(hi - lo), int(n), nat.ptr(out), nat.stream_handle(s),
+                                        ctypes.byref(st))
+        nat.raise_for(rc, st)
+    return out
 
 
 def clear_cache() -> None:

@@ -32,7 +32,6 @@ import numpy as np
 from . import _native as nat
 from .domain import MaxNull, StatMatrix, as_data_matrix, as_plan
 from .exceptions import EngineUnavailableError, UsageError
-from .labels import plan_orders
 
 DEFAULT_MEM_CAP_BYTES = 2 << 30
 
@@ -200,34 +199,34 @@ def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
             )
     resolve_threads(threads)
     device = cuda_device()
-    orders = plan_orders(plan)
-    mx, am, job = _run_from_host(x.values, x.n1, orders, two_sided, device)
+    mx, am, job = _run_from_host(x.values, x.n1, plan, two_sided, device)
     T = None
     if materialize:
         T = tstat_exact_device(job.x, x.n1, job.orders).t().contiguous().cpu().numpy()
     return NaiveResult(mx, am.astype(np.int64), job.stats.as_dict(), T)
 
 
-def _run_from_host(values: np.ndarray, n1: int, orders: np.ndarray, two_sided: bool, device):
-    """One rmx_naive_maxnull_host call: host X and labels in (page-locked in
-    place), the X upload overlapped with the engine chunk by chunk, host
-    max/argmax out.  Returns (max, argmax, job) -- the job keeps the device
-    copies for follow-up work (materialisation)."""
+def _run_from_host(values: np.ndarray, n1: int, plan, two_sided: bool, device):
+    """One rmx_naive_maxnull_host call: host X in (page-locked in place), the
+    plan's labels generated on the device (rmx_plan_orders, bit-identical to
+    numpy's streams), the X upload overlapped with the engine chunk by chunk,
+    host max/argmax out.  Returns (max, argmax, job) -- the job keeps the
+    device copies for follow-up work (materialisation)."""
     import torch
 
     from .hostmem import pinned, pinned_empty
+    from .labels import device_orders
 
     xh = pinned(np.asarray(values, dtype=np.float64))
-    oh = pinned(np.asarray(orders, dtype=np.int16))
     v, n = xh.shape
-    L = oh.shape[0]
+    L = int(plan.count)
     xd = torch.empty((v, n), dtype=torch.float64, device=device)
-    od = torch.empty((L, n), dtype=torch.int16, device=device)
+    od = device_orders(plan.master_seed, 0, L, n, device)
     job = NaiveJob(xd, n1, od, two_sided)
     mx = pinned_empty((L,), np.float64)
     am = pinned_empty((L,), np.int32)
     rc = job.lib.rmx_naive_maxnull_host(
-        xh.ctypes.data, v, n, int(n1), oh.ctypes.data, L, job.two_sided, mx.ctypes.data,
+        xh.ctypes.data, v, n, int(n1), None, L, job.two_sided, mx.ctypes.data,
         am.ctypes.data, nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
         nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
         ctypes.byref(job.stats))

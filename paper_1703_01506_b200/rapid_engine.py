@@ -56,7 +56,7 @@ from .exceptions import (
     NumericalError,
     UsageError,
 )
-from .labels import plan_orders
+from .labels import device_orders, plan_orders
 from .naive_engine import cuda_device, resolve_threads, tstat_exact_device
 from .rng import BASIS_INIT, RECOVER_OMEGA, SHIFT_GAP, TRAIN_OMEGA, omega_draw, stream
 
@@ -77,6 +77,25 @@ def draw_omegas(seed: int, domain: int, lo: int, hi: int, v: int, k: int,
         return omega_draw(stream(seed, *path), v, k)
 
     return fill_rows((k,), np.int32, row, hi - lo, workers)
+
+
+def device_omegas(seed: int, domain: int, lo: int, hi: int, v: int, k: int, dev,
+                  extra: Optional[int] = None):
+    """draw_omegas on the GPU (rmx_omega_draws: numpy's Generator.choice
+    restated bit for bit), as an (hi - lo, k) int32 CUDA tensor; numpy's
+    tail-shuffle branch (v > 10000 and k > v / 50) is drawn on the host."""
+    torch = _torch()
+    out = torch.empty((max(hi - lo, 0), k), dtype=torch.int32, device=dev)
+    if hi <= lo:
+        return out
+    if v > 10000 and k > v // 50:
+        return _to_dev(draw_omegas(seed, domain, lo, hi, v, k, extra=extra), dev)
+    st = nat.Status()
+    rc = nat.load().rmx_omega_draws(ctypes.c_uint64(int(seed) & ((1 << 64) - 1)), int(domain),
+                                    int(lo), int(hi - lo), -1 if extra is None else int(extra),
+                                    int(v), int(k), nat.ptr(out), _stream(dev), ctypes.byref(st))
+    nat.raise_for(rc, st)
+    return out
 
 
 def draw_normals(seed: int, domain: int, lo: int, hi: int, v: int) -> np.ndarray:
@@ -242,10 +261,9 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
     dev = t_dev.device
     u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, rank)), dev)
     _orthonormalize(u, force=True)
-    om = np.empty((max_passes, ell, k), dtype=np.int32)
-    for p in range(max_passes):
-        om[p] = draw_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, extra=p)
-    om_dev = _to_dev(om, dev)
+    om_dev = torch.empty((max_passes, ell, k), dtype=torch.int32, device=dev)
+    for p in range(max_passes):  # stream(seed, TRAIN_OMEGA, i, p), drawn on the GPU
+        om_dev[p] = device_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, dev, extra=p)
     final = torch.empty((ell, k), dtype=torch.int32, device=dev)
     pass_resid = (ctypes.c_double * max_passes)()
     passes, conv, updates = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int64(0)
@@ -298,7 +316,7 @@ def _train_device(x, cfg):
     plan = cfg.plan_for(x)
     dev = cuda_device()
     xd = _to_dev(x.values, dev)
-    od = _to_dev(plan_orders(plan, 0, ell), dev)
+    od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
     u, final, passes, conv, _, _ = _train_basis_device(t_dev, v, ell, k, rank, cfg.seed,
                                                        cfg.max_passes, cfg.tolerance)
@@ -381,17 +399,16 @@ def recover(x, model: SubspaceModel, plan, cfg):
     maxima = np.empty(L, dtype=np.float64)
     maxima[:ell] = model.training_maxima
     nrec = L - ell
-    orders = plan_orders(plan, ell, L)
-    omegas = draw_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k)
     xd = _to_dev(x.values, dev)
-    od = _to_dev(orders, dev)
-    omd = _to_dev(omegas, dev)
+    od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
+    omd = device_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k, dev)
     t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
     st = nat.Status()
     rc = nat.load().rmx_rapid_stats(nat.ptr(xd), v, x.subjects, n1, nat.ptr(od), nat.ptr(omd),
                                     nrec, k, nat.ptr(t), _stream(dev), ctypes.byref(st))
     if rc == nat.RMX_E_DEGENERATE:
-        _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel), omegas, orders)
+        _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel),
+                                omd.cpu().numpy(), od.cpu().numpy())
     nat.raise_for(rc, st)
     W, flags, norms = _lsq(u, r, omd, k, t, nrec)
     evals = nrec * k

@@ -64,27 +64,30 @@ def gather_maxima(local_max, local_arg, L: int, per: int, group=None):
 class ShardedNaive:
     """NaivePT over this rank's permutation shard with device-resident inputs.
 
-    x_dev: (v, n) float64 replica on this rank's GPU; orders for the shard
-    are generated host-side from the plan (labels.py) and uploaded once.
+    x_dev: (v, n) float64 replica on this rank's GPU; the shard's label rows
+    are generated on the GPU from the plan (labels.device_orders), or
+    uploaded from ``orders_host`` when given.
     """
 
     def __init__(self, x_dev, n1: int, plan, two_sided: bool, group=None,
                  orders_host: Optional[np.ndarray] = None):
         import torch
 
-        from .labels import plan_orders
+        from .labels import device_orders
         from .naive_engine import NaiveJob
 
         self.group = group
         self.rank, self.world = dist_info(group)
         self.L = int(plan.count)
         self.lo, self.hi, self.per = shard_bounds(self.L, self.rank, self.world)
-        if orders_host is None:
-            orders_host = plan_orders(plan, self.lo, self.hi)
         self.orders_host = orders_host
         self.job = None
         if self.hi > self.lo:
-            od = torch.from_numpy(np.ascontiguousarray(orders_host)).to(x_dev.device)
+            if orders_host is None:
+                od = device_orders(plan.master_seed, self.lo, self.hi, int(x_dev.shape[1]),
+                                   x_dev.device)
+            else:
+                od = torch.from_numpy(np.ascontiguousarray(orders_host)).to(x_dev.device)
             self.job = NaiveJob(x_dev, n1, od, two_sided)
         self.device = x_dev.device
 
@@ -120,12 +123,9 @@ def run_naive_distributed(x, plan, two_sided: bool = False, group=None):
     if plan.subjects != x.subjects:
         raise UsageError("plan and data matrix disagree on subject count")
     dev = cuda_device()
-    rank, world = dist_info(group)
-    lo, hi, _ = shard_bounds(plan.count, rank, world)
-    from .labels import plan_orders
+    from .hostmem import to_device
 
-    orders = plan_orders(plan, lo, hi)
-    xd, _ = upload(x.values, orders[:0], dev)
-    sh = ShardedNaive(xd, x.n1, plan, two_sided, group, orders_host=orders)
+    xd = to_device(np.ascontiguousarray(x.values, dtype=np.float64), dev)
+    sh = ShardedNaive(xd, x.n1, plan, two_sided, group)
     m, a = sh.step()
     return MaxNull(m.cpu().numpy()), a.cpu().numpy().astype(np.int64)
