@@ -255,6 +255,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   DevBuf<double> G, w, vals, resid, pred, d, sums, wn, ug;
   DevBuf<int32_t> flag, idxbuf, pidx;
   DevBuf<GrouseState> gst;
+  DevBuf<double> H, hg, hdrift;  // tracked U^T U, its update vector, drift
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
@@ -268,6 +269,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(pidx.alloc(k, s));
   RCUDA(ug.alloc((size_t)k * r, s));
   RCUDA(gst.alloc(1, s));
+  RCUDA(H.alloc((size_t)r * r, s));
+  RCUDA(hg.alloc((size_t)r + 1, s));
+  RCUDA(hdrift.alloc(1, s));
+  RCUDA(launch_h_identity(H.p, r, s));  // the caller hands in an orthonormalised U
   RCUDA(cudaMemsetAsync(d.p, 0, v * sizeof(double), s));
   RCUDA(cudaMemsetAsync(pred.p, 0, v * sizeof(double), s));
   RCUDA(cudaMemsetAsync(wn.p, 0, r * sizeof(double), s));  // finite: 0 * wn in k_pred_apply_st
@@ -298,11 +303,15 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(launch_grouse_post(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r, d.p,
                              pidx.p, wn.p, final_omegas ? final_omegas + (int64_t)i * k : nullptr,
                              s));
+    RCUDA(launch_h_update(H.p, r, gst.p, w.p, wn.p, ug.p, k, vals.p, resid.p, sums.p, hg.p, s));
     (void)p;
     return RMX_OK;
   };
+  double hdrift_host = 0.0;
   auto read_state = [&](GrouseState* h) -> int {
+    RCUDA(launch_h_drift(H.p, r, hdrift.p, s));
     RCUDA(cudaMemcpyAsync(h, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaMemcpyAsync(&hdrift_host, hdrift.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
     return RMX_OK;
   };
@@ -342,10 +351,13 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       tglob = h + 1;  // replay the skipped updates
       continue;
     }
-    if (reortho) {  // lrmc.py:258-259: every 64 updates
+    if (reortho && hdrift_host > 1e-8) {  // lrmc.py:258-259: every 64 updates
+      // ||U^T U - I||_max from the tracked H (which includes the pending
+      // update): re-orthonormalise with the pending update applied
       RCUDA(launch_grouse_flush(u, v, r, pred.p, wn.p, gst.p, d.p, pidx.p, k, s));
       double drift = 0.0;
-      if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+      if (int rc = rmx_orthonormalize(u, v, r, 1, &drift, stream, st)) return rc;
+      RCUDA(launch_h_identity(H.p, r, s));
     }
     if (pass_end) {
       const double rel = hs.rel_sum / ell;

@@ -25,7 +25,16 @@ struct GrouseState {
   int pad;
   double pend_a;
   double rel_sum;  // sum over the pass of |r| / |t_Omega|
+  double pend_b;   // beta of the pending update (d = beta r on Omega)
+  double aa;       // |a|^2 of the pending update a = pend_a p + d
 };
+// H = U^T U tracked through the rank-1 updates (the every-64-updates drift
+// check of lrmc.py:258-259 without a 168 GFLOP Gram)
+cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* w,
+                            const double* wn, const double* ug, int k, const double* vals,
+                            const double* resid, const double* sums, double* g, cudaStream_t s);
+cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
+cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
 cudaError_t launch_gather_pending_st(const double* U, int r, const int32_t* idx, int k,
                                      const GrouseState* st, const double* pred, const double* d,
                                      const double* wn, double* out, cudaStream_t s);

@@ -65,8 +65,10 @@ __global__ void __launch_bounds__(kGThreads) k_gram(const double* __restrict__ U
   const int kbeg = blockIdx.z * rows_per_split;
   const int kend = min(k, kbeg + rows_per_split);
   const int nrows = max(0, kend - kbeg);
-  for (int i = tid; i < nrows; i += kGThreads) rid[i] = idx ? idx[b * k + kbeg + i] : kbeg + i;
-  __syncthreads();
+  if (idx) {  // gathered rows: stage the ids (dense: the row number itself)
+    for (int i = tid; i < nrows; i += kGThreads) rid[i] = idx[b * k + kbeg + i];
+    __syncthreads();
+  }
   const double* vb = vals ? vals + b * k : nullptr;
   // chunk c -> ring slot c % kGS; thread fills column tid of 16 rows (A, B)
   auto issue = [&](int c) {
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(kGThreads) k_gram(const double* __restrict__ U
       double* da = &As[slot][rr][tid];
       double* db = &Bs[slot][rr][tid];
       if (row < nrows) {
-        const double* urow = U + (int64_t)rid[row] * ldu;
+        const double* urow = U + (int64_t)(idx ? rid[row] : kbeg + row) * ldu;
         if (ca < r) cp_async8(da, urow + ca);
         else *da = (ca == r && vb) ? vb[kbeg + row] : 0.0;
         if (!diag) {
@@ -890,7 +892,73 @@ __global__ void __launch_bounds__(1024) k_grouse_post(
   if (threadIdx.x == 0) {
     st->pending = do_update;
     st->pend_a = sa;
+    st->pend_b = sb;
   }
+}
+
+// H tracking: after k_grouse_post decided update t (a = pend_a p + d, b =
+// w/|w|, U the matrix before the update, ug = U[Omega] gathered rows):
+//   g = U^T a = pend_a H w + pend_b ug^T resid,
+//   |a|^2 = pend_a^2 |p|^2 + 2 pend_a pend_b (ug w).resid + pend_b^2 |resid|^2,
+//   H += b g^T + g b^T + |a|^2 b b^T.
+// k_h_g: warp per column c of g (and the scalar |a|^2 in block 0).
+__global__ void k_h_g(const double* __restrict__ H, int r, const GrouseState* __restrict__ st,
+                      const double* __restrict__ w, const double* __restrict__ ug, int k,
+                      const double* __restrict__ vals, const double* __restrict__ resid,
+                      const double* __restrict__ sums, double* __restrict__ g,
+                      double* __restrict__ aa_out) {
+  if (st->halted || !st->pending) return;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const double a = st->pend_a, bb = st->pend_b;
+  if (c < r) {
+    double hw = 0.0, ur = 0.0;
+    for (int j = lane; j < r; j += 32) hw = fma(H[(int64_t)c * r + j], w[j], hw);
+    for (int i = lane; i < k; i += 32) ur = fma(ug[(int64_t)i * r + c], resid[i], ur);
+    for (int o = 16; o > 0; o >>= 1) {
+      hw += __shfl_xor_sync(0xffffffffu, hw, o);
+      ur += __shfl_xor_sync(0xffffffffu, ur, o);
+    }
+    if (lane == 0) g[c] = a * hw + bb * ur;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // |a|^2 (ug w = vals - resid)
+    double pr = 0.0;
+    for (int i = lane; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
+    for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    if (lane == 0) *aa_out = a * a * sums[1] + 2.0 * a * bb * pr + bb * bb * sums[0];
+  }
+}
+
+__global__ void k_h_rank2(double* __restrict__ H, int r, const GrouseState* __restrict__ st,
+                          const double* __restrict__ b, const double* __restrict__ g,
+                          const double* __restrict__ aa) {
+  if (st->halted || !st->pending) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)r * r) return;
+  const int i = (int)(e / r), j = (int)(e % r);
+  H[e] += b[i] * g[j] + g[i] * b[j] + *aa * b[i] * b[j];
+}
+
+__global__ void k_h_drift(const double* __restrict__ H, int r, double* __restrict__ out) {
+  __shared__ double part[32];
+  double m = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)r * r; e += blockDim.x) {
+    const int i = (int)(e / r), j = (int)(e % r);
+    m = fmax(m, fabs(H[e] - (i == j ? 1.0 : 0.0)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t = fmax(t, part[w]);
+    *out = t;
+  }
+}
+
+__global__ void k_h_identity(double* __restrict__ H, int r) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (int64_t)r * r) H[e] = (e / r == e % r) ? 1.0 : 0.0;
 }
 
 // apply a pending update to all of U (before a re-orthonormalisation)
@@ -1092,7 +1160,8 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
     cudaError_t e = cudaMemsetAsync(G, 0, (size_t)B * (r + 1) * (r + 1) * sizeof(double), s);
     if (e != cudaSuccess) return e;
   }
-  const size_t smem = (size_t)2 * kGS * kGK * kGT * sizeof(double) + (size_t)rps * sizeof(int32_t);
+  const size_t smem =
+      (size_t)2 * kGS * kGK * kGT * sizeof(double) + (idx ? (size_t)rps * sizeof(int32_t) : 0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -1229,6 +1298,26 @@ cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, doub
   int64_t blocks = (v + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_pred_apply<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, a, d, wn, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* w,
+                            const double* wn, const double* ug, int k, const double* vals,
+                            const double* resid, const double* sums, double* g, cudaStream_t s) {
+  k_h_g<<<(unsigned)((r + 7) / 8), 256, 0, s>>>(H, r, st, w, ug, k, vals, resid, sums, g, g + r);
+  const int64_t n = (int64_t)r * r;
+  k_h_rank2<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, r, st, wn, g, g + r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s) {
+  k_h_drift<<<1, 1024, 0, s>>>(H, r, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
+  const int64_t n = (int64_t)r * r;
+  k_h_identity<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, r);
   return cudaGetLastError();
 }
 
