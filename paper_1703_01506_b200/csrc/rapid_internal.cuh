@@ -69,18 +69,6 @@ cudaError_t launch_resid(const double* U, int r, const int32_t* idx, int k, cons
                          const double* w, double* resid, double* sums, cudaStream_t s);
 cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, double* pred,
                         double* sums, cudaStream_t s);
-cudaError_t launch_gather_pending(const double* U, int r, const int32_t* idx, int k, int pending,
-                                  double a, const double* pred, const double* d, const double* wn,
-                                  double* out, cudaStream_t s);
-cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, double* pred,
-                              double* sums, double a, const double* d, const double* wn,
-                              const int32_t* flag, cudaStream_t s);
-cudaError_t launch_grouse_update(double* U, int64_t v, int r, const double* pred,
-                                 const double* wn, double a, const double* dscatter,
-                                 cudaStream_t s);
-cudaError_t launch_scatter(const int32_t* idx, int k, const double* resid, double bcoef,
-                           double* d, cudaStream_t s);
-cudaError_t launch_unscatter(const int32_t* idx, int k, double* d, cudaStream_t s);
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s);
 cudaError_t launch_gather_vals(const double* t, const int32_t* idx, int k, double* vals,
                                cudaStream_t s);
@@ -94,6 +82,4 @@ cudaError_t launch_to_f32(const double* a, int64_t n, float* out, cudaStream_t s
 cudaError_t launch_gather_rows(const double* t, int64_t ldt, const int32_t* idx, int k, int64_t B,
                                double* out, cudaStream_t s);
 cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s);
-cudaError_t launch_scale_copy(const double* a, int n, double sc, double* out, cudaStream_t s);
-
 }  // namespace rmx

@@ -7,9 +7,12 @@
 //   k_chol_solve    K3b: blocked Cholesky of G_b[:r,:r], w = G^-1 rhs, and a
 //                   singularity flag (lrmc.py:138-148; see DESIGN.md for the
 //                   condition-number deviation)
-//   k_complete_max  K4: max_j (W U^T)[p, j] + sigma z(p, j)  (+ mu), fused
-//                   with a counter-based Philox normal (rapid.py:198-205)
-//   GROUSE helpers  k_resid, k_pred, k_grouse_update (lrmc.py:160-193)
+//   k_cg_solve      K3b for one GROUSE system: cluster CG, Gram in DSMEM
+//   k_complete_max  K4 on CUDA cores: max_j (W U^T)[p, j] + sigma z(p, j)
+//                   (+ mu) (rapid.py:198-205; the tcgen05 version is
+//                   k_tfill_tc<..., MODE 1> in tfill_tc.cu)
+//   GROUSE step     k_gather_pending_st, k_resid, k_pred_apply_st,
+//                   k_grouse_post, k_h_g / k_h_rank2 (lrmc.py:160-193)
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -730,61 +733,14 @@ __global__ void k_pred(const double* __restrict__ U, int64_t v, int r, const dou
   }
 }
 
-// GROUSE with one deferred rank-1 update.  The update of step t,
-// U += (a p_t + d_t) wn_t^T (p_t = U w_t, d_t the scattered residual), is
-// not applied when it is decided: the next step gathers its Omega rows with
-// the pending term added (k_gather_pending), and its prediction pass applies
-// the pending update row by row while computing p_{t+1} = U' w_{t+1}
-// (k_pred_apply) -- one read and one write of U per update instead of a
-// read (prediction) plus a read-modify-write (update).  Both skip when
-// *flag is set (ill-conditioned attempt: the update stays pending).
-__global__ void k_gather_pending(const double* __restrict__ U, int r,
-                                 const int32_t* __restrict__ idx, int k, int pending, double a,
-                                 const double* __restrict__ pred, const double* __restrict__ d,
-                                 const double* __restrict__ wn, double* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)k * r) return;
-  const int i = (int)(e / r), c = (int)(e % r);
-  const int64_t row = idx[i];
-  double u = U[row * r + c];
-  if (pending) u = fma(fma(a, pred[row], d[row]), wn[c], u);
-  out[e] = u;
-}
-
-__global__ void k_pred_apply(double* __restrict__ U, int64_t v, int r, const double* __restrict__ w,
-                             double* __restrict__ pred, double* __restrict__ sums, double a,
-                             const double* __restrict__ d, const double* __restrict__ wn,
-                             const int32_t* __restrict__ flag) {
-  if (*flag) return;
-  __shared__ double part[32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
-  double local = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + wib; row < v;
-       row += (int64_t)gridDim.x * (blockDim.x / 32)) {
-    double* u = U + row * r;
-    const double coef = fma(a, pred[row], d[row]);
-    double s = 0.0;
-    for (int c = lane; c < r; c += 32) {
-      const double un = fma(coef, wn[c], u[c]);
-      u[c] = un;
-      s = fma(un, w[c], s);
-    }
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      pred[row] = s;
-      local += s * s;
-    }
-  }
-  if (lane == 0) part[wib] = local;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += part[i];
-    atomicAdd(&sums[1], t);
-  }
-}
-
 // ---- device-resident GROUSE step (no host round trip per update)
+// The rank-1 update of step t, U += (a p_t + d_t) wn_t^T (p_t = U w_t, d_t
+// the scattered residual), is deferred: the next step gathers its Omega rows
+// with the pending term added (k_gather_pending_st) and its prediction pass
+// applies the update row by row while forming p_{t+1} = U' w_{t+1}
+// (k_pred_apply_st) -- one read and one write of U per update instead of a
+// read (prediction) plus a read-modify-write (update).  A flagged solve
+// halts the loop: the update stays pending until the host has resampled.
 __global__ void k_gather_pending_st(const double* __restrict__ U, int r,
                                     const int32_t* __restrict__ idx, int k,
                                     const GrouseState* __restrict__ st,
@@ -983,28 +939,6 @@ __global__ void k_grouse_flush_done(GrouseState* __restrict__ st, double* __rest
   if (threadIdx.x == 0) st->pending = 0;
 }
 
-// U += dir (w/|w|)^T, dir = a * pred + b * scatter(resid over idx)
-__global__ void k_grouse_update(double* __restrict__ U, int64_t v, int r,
-                                const double* __restrict__ pred, const double* __restrict__ wn,
-                                double a, const double* __restrict__ dscatter) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= v * r) return;
-  const int64_t row = e / r;
-  const int c = (int)(e % r);
-  U[e] += (a * pred[row] + dscatter[row]) * wn[c];
-}
-
-__global__ void k_scatter(const int32_t* __restrict__ idx, int k, const double* __restrict__ resid,
-                          double bcoef, double* __restrict__ d) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) d[idx[i]] = bcoef * resid[i];
-}
-
-__global__ void k_unscatter(const int32_t* __restrict__ idx, int k, double* __restrict__ d) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) d[idx[i]] = 0.0;
-}
-
 // X <- X L^{-T} for the lower Cholesky factor L stored in G (ld = r + 1):
 // row i solves y L^T = x, i.e. L y^T = x^T (forward substitution).  One
 // warp per row, lanes split the dot products.
@@ -1128,11 +1062,6 @@ __global__ void k_mean_var(const double* __restrict__ a, int64_t n, double* out)
     out[0] = m;
     out[1] = n > 1 ? t / (double)(n - 1) : 0.0;
   }
-}
-
-__global__ void k_scale_copy(const double* __restrict__ a, int n, double sc, double* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = a[i] * sc;
 }
 
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ out) {
@@ -1283,24 +1212,6 @@ cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, doub
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_pending(const double* U, int r, const int32_t* idx, int k, int pending,
-                                  double a, const double* pred, const double* d, const double* wn,
-                                  double* out, cudaStream_t s) {
-  const int64_t total = (int64_t)k * r;
-  k_gather_pending<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, r, idx, k, pending, a, pred,
-                                                                   d, wn, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pred_apply(double* U, int64_t v, int r, const double* w, double* pred,
-                              double* sums, double a, const double* d, const double* wn,
-                              const int32_t* flag, cudaStream_t s) {
-  int64_t blocks = (v + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_pred_apply<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, a, d, wn, flag);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* w,
                             const double* wn, const double* ug, int k, const double* vals,
                             const double* resid, const double* sums, double* g, cudaStream_t s) {
@@ -1367,25 +1278,6 @@ cudaError_t launch_grouse_flush(double* U, int64_t v, int r, const double* pred,
   return cudaGetLastError();
 }
 
-cudaError_t launch_grouse_update(double* U, int64_t v, int r, const double* pred,
-                                 const double* wn, double a, const double* dscatter,
-                                 cudaStream_t s) {
-  const int64_t total = v * r;
-  k_grouse_update<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, v, r, pred, wn, a, dscatter);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scatter(const int32_t* idx, int k, const double* resid, double bcoef,
-                           double* d, cudaStream_t s) {
-  k_scatter<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(idx, k, resid, bcoef, d);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_unscatter(const int32_t* idx, int k, double* d, cudaStream_t s) {
-  k_unscatter<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(idx, k, d);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s) {
   const int wpb = 4;
   k_trsm_lt<<<(unsigned)((v + wpb - 1) / wpb), 32 * wpb, (size_t)wpb * r * sizeof(double), s>>>(
@@ -1429,11 +1321,6 @@ cudaError_t launch_gather_rows(const double* t, int64_t ldt, const int32_t* idx,
 
 cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s) {
   k_mean_var<<<1, 1024, 0, s>>>(a, n, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scale_copy(const double* a, int n, double sc, double* out, cudaStream_t s) {
-  k_scale_copy<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n, sc, out);
   return cudaGetLastError();
 }
 
