@@ -64,7 +64,7 @@ int check_dims(int64_t v, int32_t n, int32_t n1, int64_t L, rmx_status* st) {
 // does not fit next to a minimal ring (n > ~640).  Instantiated configs
 // (tfill_tc.cu): cg=1 (64,3) (32,4) (32,3); cg=2 (64,6) (64,4) (32,7) (32,4).
 bool pick_pipeline(int cg, int kpad, int* bk, int* stages) {
-  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024;
+  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024 + kTileM * 8;  // + row bests
   if (a_bytes >= kMaxSmem) return false;
   const size_t avail = kMaxSmem - a_bytes;
   auto fit = [&](int b) { return (int)(avail / ((size_t)2 * (2 * kTileV / cg) * b * 2)); };
@@ -108,7 +108,7 @@ bool pick_pipeline(int cg, int kpad, int* bk, int* stages) {
 // 256 / cg voxel rows); A = kTileM x 2 kpad bytes.  Instantiated
 // (cg, stages): (1, 4) (1, 3) (2, 7) (2, 4)
 bool pick_pipeline_i8(int cg, int kpad, int* bk, int* stages) {
-  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024 + kInvStage;
+  const size_t a_bytes = (size_t)kTileM * kpad * 2 + 256 + 1024 + kInvStage + kTileM * 8;
   if (a_bytes >= kMaxSmem) return false;
   const int fit = (int)((kMaxSmem - a_bytes) / ((size_t)(2 * kTileV / cg) * 128));
   const int want = cg == 2 ? 7 : 4;

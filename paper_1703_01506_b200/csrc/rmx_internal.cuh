@@ -33,6 +33,24 @@ __device__ __forceinline__ double band_lower(double t, double e, double beta_abs
   if (d2 <= 0.0) return -HUGE_VAL;
   return S / sqrt(d2);
 }
+// fp32 version for K1's running floors (t - 2 band): its rounding error is
+// far inside the factor 2 of the floor, and a vanishing pooled variance
+// gives an infinite band (no floor), so it is only ever conservative.
+__device__ __forceinline__ float band_lower_f(float t, float e, float beta_abs, float gamma) {
+  const float d = gamma / fmaf(beta_abs * t, t, 1.0f);
+  const float S = t * sqrtf(d) - e;
+  const float d2 = fmaf(-beta_abs * S, S, gamma);
+  if (!(d2 > 1e-6f * gamma)) return -HUGE_VALF;
+  return S * rsqrtf(d2);
+}
+__device__ __forceinline__ float band_abs_fast(float t, float rel, float e, float beta_abs,
+                                               float gamma) {
+  const float base = rel * fmaxf(fabsf(t), 1.0f);
+  if (!(e > 0.0f)) return base;
+  const float lo = band_lower_f(band_lower_f(t, e, beta_abs, gamma), e, beta_abs, gamma);
+  if (lo == -HUGE_VALF) return HUGE_VALF;
+  return base + (t - lo) * 1.01f;
+}
 __device__ __forceinline__ float band_abs(float t, float rel, float e, float beta_abs,
                                           float gamma) {
   const float base = rel * fmaxf(fabsf(t), 1.0f);

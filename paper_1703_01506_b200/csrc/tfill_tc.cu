@@ -184,7 +184,8 @@ __device__ __forceinline__ uint32_t i8_to_s(uint32_t sq, float inv) {
 template <bool TWO_SIDED, bool SONLY, bool I8>
 __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int jbase,
                                            const EpiConst& ec, Top4& top, int64_t p, bool prow,
-                                           const TfillArgs& a, const float* ginv) {
+                                           const TfillArgs& a, const float* ginv,
+                                           float kfloor = -FLT_MAX) {
   uint32_t uni = __reduce_or_sync(0xffffffffu, hits);
   while (uni) {
     const int c = __ffs(uni) - 1;
@@ -210,7 +211,7 @@ __device__ __forceinline__ void group_rare(uint32_t hits, uint32_t taddr_s, int 
             a.susp[2 * slot + 1] = j;
           }
         }
-      } else if (u > top.k3 * d) {
+      } else if (u > fmaxf(top.k3, kfloor) * d) {
         top.insert(u / d, j);
       }
     }
@@ -269,6 +270,18 @@ __device__ __forceinline__ float seed_key(const uint32_t* best_t, int64_t p, boo
   if (e == 0u) return -FLT_MAX;
   const float t = ord_dec(e);
   const float band = band_abs(t, a.band_rel, emax, a.beta_abs, a.gamma);
+  if (!(band < 1e30f)) return -FLT_MAX;
+  const float lo = t - 2.0f * band;
+  if (TWO_SIDED) return lo > 0.0f ? lo * lo : 0.0f;
+  return lo * fabsf(lo);
+}
+
+// The same floor for a running best t (shared across the CTA's epilogue
+// groups within a unit, see the epilogue): nothing below t - 2 band(t) can
+// become a refinement candidate.
+template <bool TWO_SIDED>
+__device__ __forceinline__ float floor_key(float t, const TfillArgs& a, float emax) {
+  const float band = band_abs_fast(t, a.band_rel, emax, a.beta_abs, a.gamma);
   if (!(band < 1e30f)) return -FLT_MAX;
   const float lo = t - 2.0f * band;
   if (TWO_SIDED) return lo > 0.0f ? lo * lo : 0.0f;
@@ -336,6 +349,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
   // int8: per-epilogue-warp staging of its columns' dequantisation scales
   float* inv_smem = reinterpret_cast<float*>(a_mem + a_bytes + 256);
+  // per-row running best t~ of the unit, shared by the epilogue groups:
+  // (unit index << 32) | order-encoded t~ (a new unit supersedes old tags)
+  unsigned long long* rowbest =
+      reinterpret_cast<unsigned long long*>(a_mem + a_bytes + 256 + (I8 ? kInvStage : 0));
 
   const int warp = (int)warp_id();
   const int lane = threadIdx.x & 31;
@@ -359,6 +376,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     if (CG == 2) tmem_alloc_2sm(tmem_slot, 512);
     else tmem_alloc(tmem_slot, 512);
   }
+  for (int i = threadIdx.x; i < kTileM; i += blockDim.x) rowbest[i] = 0ull;
   tc_fence_before();
   if (CG == 2) cluster_sync();
   else __syncthreads();
@@ -549,6 +567,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       float cmax = -FLT_MAX;  // MODE 1: running max of this row over the unit
       const float wsc = (MODE == 1 && prow) ? a.wdescale[p] : 0.0f;
       float kthr = sonly_thr(top.k3, ec);  // S-only hit threshold on S^2
+      uint32_t seen_enc = 0u;              // the row's running best (all groups)
+      float kfloor = -FLT_MAX;             // and the key floor it implies
       unsigned rare_groups = 0;
       float* winv = inv_smem + ew * (COLGROUPS * 32);  // this warp's columns
       for (int i = 0; i < t1 - t0; ++i) {
@@ -567,6 +587,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         if (I8) {
           cp_async_wait_all();
           __syncwarp();
+        }
+        if constexpr (SONLY && MODE == 0) {  // pick up the other groups' best for this row
+          const unsigned long long rb = rowbest[row];
+          const uint32_t enc = (uint32_t)rb;
+          if ((uint32_t)(rb >> 32) == (uint32_t)u && enc > seen_enc) {
+            seen_enc = enc;
+            kfloor = floor_key<TWO_SIDED>(ord_dec(enc), a, emax);
+            kthr = sonly_thr(fmaxf(top.k3, kfloor), ec);
+          }
         }
 #pragma unroll 1
         for (int g = 0; g < COLGROUPS; ++g) {
@@ -626,8 +655,17 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
             if (gvalid < 32) hits &= (1u << gvalid) - 1u;
             if (__any_sync(0xffffffffu, hits != 0u)) {
               ++rare_groups;
-              group_rare<TWO_SIDED, SONLY, I8>(hits, taddr, jbase, ec, top, p, prow, a, ginv);
-              kthr = sonly_thr(top.k3, ec);
+              group_rare<TWO_SIDED, SONLY, I8>(hits, taddr, jbase, ec, top, p, prow, a, ginv,
+                                               kfloor);
+              if (prow && top.j0 >= 0) {  // publish a new row best to the other groups
+                const uint32_t enc = ord_enc(key_to_t(top.k0));
+                if (enc > seen_enc) {
+                  seen_enc = enc;
+                  kfloor = floor_key<TWO_SIDED>(key_to_t(top.k0), a, emax);
+                  atomicMax(&rowbest[row], ((unsigned long long)u << 32) | enc);
+                }
+              }
+              kthr = sonly_thr(fmaxf(top.k3, kfloor), ec);
             }
           } else {
             uint32_t hits = group_hits<ALPHA0>(sv, qv, ec, top.k3);
@@ -696,7 +734,8 @@ size_t smem_bytes_for(int cg, int bk, int stages, int kpad, bool i8) {
   // fp16: hi + lo boxes of bk halves; i8: one box of bk bytes of [h | l].
   // The A tile is kTileM x kpad halves or kTileM x 2 kpad bytes: same size.
   const size_t stage = i8 ? (size_t)(kTileN / cg) * bk : (size_t)2 * (kTileN / cg) * bk * 2;
-  size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024 + (i8 ? kInvStage : 0);
+  size_t bytes = stages * stage + (size_t)kTileM * kpad * 2 + 256 + 1024 + (i8 ? kInvStage : 0) +
+                 kTileM * sizeof(unsigned long long);
   // one CTA per SM: TMEM (512 columns) is allocated whole by each CTA
   return bytes < 120 * 1024 ? 120 * 1024 : bytes;
 }
