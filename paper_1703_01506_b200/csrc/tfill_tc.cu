@@ -440,8 +440,14 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (leader) {
-      const uint32_t a_base = smem_u32(a_mem);
+      // Descriptors are built once; per MMA only the 14-bit start-address
+      // field moves (A: +256 B per K step, B: +32 B per K step within a
+      // stage), so the single issuing thread spends ~3 uniform instructions
+      // per MMA -- at the int8 rate (128 cycles per M256 N256 K32 MMA) the
+      // descriptor arithmetic otherwise throttles the tensor pipe.
       const uint32_t a_sbo = (uint32_t)kext * 8u * ELT;
+      const uint64_t adesc0 = smem_desc(smem_u32(a_mem), 128u, a_sbo, 0u);
+      const uint64_t bdesc0 = smem_desc(smem_u32(stage_mem), 16u, B_SBO, B_LAYOUT);
       int stage = 0;
       uint32_t phase = 0, acc_phase = 0, a_phase = 0;
       int acc = 0;
@@ -461,25 +467,29 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             if (elect_one()) {
-              const uint32_t sb = smem_u32(stage_mem + stage * STAGE_BYTES);
+              const int ks0 = kb / KSTEP;
+              const int nmma = min(KSTEPS, a.nk16 - ks0);  // last stage may be partial
+              const uint64_t bst = bdesc0 + (uint64_t)((stage * STAGE_BYTES) >> 4);
+              uint64_t adesc = adesc0 + (uint64_t)(ks0 * 16);  // 256 B per K step
 #pragma unroll
               for (int s = 0; s < KSTEPS; ++s) {
-                const int ks = kb / KSTEP + s;
-                if (ks < a.nk16) {
-                  const uint64_t adesc = smem_desc(a_base + (uint32_t)ks * 256u, 128u, a_sbo, 0u);
-                  const uint64_t bh = smem_desc(sb + (uint32_t)s * 32u, 16u, B_SBO, B_LAYOUT);
-                  const uint64_t bl = smem_desc(sb + (uint32_t)HALF_BYTES + (uint32_t)s * 32u, 16u,
-                                                B_SBO, B_LAYOUT);
+                if (s < nmma) {
+                  const uint32_t accum = (ks0 + s) > 0 ? 1u : 0u;
+                  const uint64_t bh = bst + (uint64_t)(s * 2);  // 32 B per K step
                   if (I8) {
-                    if (CG == 2) mma_i8_ss_2sm(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
-                    else mma_i8_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
-                  } else if (CG == 2) {
-                    mma_f16_ss_2sm(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
-                    mma_f16_ss_2sm(d_tmem, adesc, bl, IDESC, 1u);
+                    if (CG == 2) mma_i8_ss_2sm(d_tmem, adesc, bh, IDESC, accum);
+                    else mma_i8_ss(d_tmem, adesc, bh, IDESC, accum);
                   } else {
-                    mma_f16_ss(d_tmem, adesc, bh, IDESC, ks > 0 ? 1u : 0u);
-                    mma_f16_ss(d_tmem, adesc, bl, IDESC, 1u);
+                    const uint64_t bl = bh + (uint64_t)(HALF_BYTES >> 4);
+                    if (CG == 2) {
+                      mma_f16_ss_2sm(d_tmem, adesc, bh, IDESC, accum);
+                      mma_f16_ss_2sm(d_tmem, adesc, bl, IDESC, 1u);
+                    } else {
+                      mma_f16_ss(d_tmem, adesc, bh, IDESC, accum);
+                      mma_f16_ss(d_tmem, adesc, bl, IDESC, 1u);
+                    }
                   }
+                  adesc += 16u;
                 }
               }
               if (CG == 2) {
