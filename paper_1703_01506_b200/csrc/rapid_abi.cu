@@ -251,44 +251,58 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   if (k < r) return rset(st, RMX_E_USAGE, "%d observed rows per update cannot identify rank %d", k, r);
   if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // sums: 0 |r|^2 1 |pred|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
-  DevBuf<double> G, w, vals, resid, pred, d, sums, wn, ug;
-  DevBuf<int32_t> flag, idxbuf, pidx;
+  // sums: 0 |r|^2 1 |p|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
+  DevBuf<double> G, w, vals, resid, sums, wn, ug, ub2, M, cmat, dval, H, hg, hdrift, hw, mw, dots;
+  DevBuf<int32_t> flag, idxbuf, didx;
   DevBuf<GrouseState> gst;
-  DevBuf<double> H, hg, hdrift;  // tracked U^T U, its update vector, drift
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
   RCUDA(vals.alloc(k, s));
   RCUDA(resid.alloc(k, s));
-  RCUDA(pred.alloc(v, s));
-  RCUDA(d.alloc(v, s));
   RCUDA(sums.alloc(8, s));
   RCUDA(flag.alloc(1, s));
   RCUDA(idxbuf.alloc(k, s));
-  RCUDA(pidx.alloc(k, s));
   RCUDA(ug.alloc((size_t)k * r, s));
-  RCUDA(gst.alloc(1, s));
+  RCUDA(ub2.alloc((size_t)v * r, s));
+  RCUDA(M.alloc((size_t)r * r, s));
+  RCUDA(cmat.alloc((size_t)kDeferCap * r, s));
+  RCUDA(dval.alloc((size_t)kDeferCap * k, s));
+  RCUDA(didx.alloc((size_t)kDeferCap * k, s));
   RCUDA(H.alloc((size_t)r * r, s));
   RCUDA(hg.alloc((size_t)r + 1, s));
   RCUDA(hdrift.alloc(1, s));
-  RCUDA(launch_h_identity(H.p, r, s));  // the caller hands in an orthonormalised U
-  RCUDA(cudaMemsetAsync(d.p, 0, v * sizeof(double), s));
-  RCUDA(cudaMemsetAsync(pred.p, 0, v * sizeof(double), s));
-  RCUDA(cudaMemsetAsync(wn.p, 0, r * sizeof(double), s));  // finite: 0 * wn in k_pred_apply_st
+  RCUDA(hw.alloc(r, s));
+  RCUDA(mw.alloc(r, s));
+  RCUDA(dots.alloc(kDeferCap, s));
+  RCUDA(gst.alloc(1, s));
   RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(GrouseState), s));
+  RCUDA(launch_flush_reset(M.p, r, gst.p, s));  // M = I, no terms
+  RCUDA(launch_h_identity(H.p, r, s));          // the caller hands in an orthonormalised U
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
   const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
-  // One update, entirely on the device (lrmc.py:160-193): U_Omega with the
-  // deferred update, Gram, solve (cluster CG; Cholesky on the same G when CG
-  // does not converge), residual, p = U' w applying the deferred update, and
-  // k_grouse_post's decisions.  No host round trip: the host syncs only at
-  // the re-orthonormalisation cadence and at pass ends.
+  // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE);
+  // ubase alternates between the caller's u and ub2 at every flush
+  double* ubase = u;
+  double* uother = ub2.p;
+  auto flush = [&]() -> int {
+    RCUDA(launch_gemm_rm(ubase, r, nullptr, v, r, M.p, uother, s));
+    RCUDA(launch_sparse_terms(uother, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
+    std::swap(ubase, uother);
+    RCUDA(launch_flush_reset(M.p, r, gst.p, s));
+    return RMX_OK;
+  };
+  // One update, entirely on the device (lrmc.py:160-193): the Omega rows of
+  // U (ubase[Omega] M + the sparse terms), Gram, solve (cluster CG; Cholesky
+  // on the same G when CG does not converge), residual, |p|^2 from H, and
+  // k_grouse_post_m's decisions; the update itself only touches M, the
+  // terms and H.  No host round trip: the host syncs every 64 updates.
   auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
     const double* trow = t + (int64_t)i * v;
-    RCUDA(launch_gather_pending_st(u, r, idx, k, gst.p, pred.p, d.p, wn.p, ug.p, s));
+    RCUDA(launch_gemm_rm(ubase, r, idx, k, r, M.p, ug.p, s));
+    RCUDA(launch_sparse_terms(ug.p, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
     RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
     RCUDA(launch_gram(ug.p, r, r, nullptr, k, vals.p, G.p, 1, s));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
@@ -299,11 +313,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
     }
     RCUDA(launch_resid(ug.p, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
-    RCUDA(launch_pred_apply_st(u, v, r, w.p, pred.p, sums.p, gst.p, d.p, wn.p, flag.p, s));
-    RCUDA(launch_grouse_post(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r, d.p,
-                             pidx.p, wn.p, final_omegas ? final_omegas + (int64_t)i * k : nullptr,
-                             s));
-    RCUDA(launch_h_update(H.p, r, gst.p, w.p, wn.p, ug.p, k, vals.p, resid.p, sums.p, hg.p, s));
+    RCUDA(launch_defer_vec(H.p, M.p, cmat.p, w.p, r, gst.p, hw.p, mw.p, dots.p, s));
+    RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
+                               didx.p, dval.p, cmat.p, wn.p,
+                               final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));
+    RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, k, vals.p, resid.p, sums.p, hg.p, s));
+    RCUDA(launch_defer_apply(M.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r, s));
     (void)p;
     return RMX_OK;
   };
@@ -322,7 +337,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const int p = (int)(tglob / ell), i = (int)(tglob % ell);
     if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob)) return rc;
     ++tglob;
-    const bool reortho = tglob % 64 == 0, pass_end = tglob % ell == 0;
+    const bool reortho = tglob % kDeferCap == 0, pass_end = tglob % ell == 0;
     if (!reortho && !pass_end) continue;
     GrouseState hs;
     if (int rc = read_state(&hs)) return rc;
@@ -351,13 +366,13 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       tglob = h + 1;  // replay the skipped updates
       continue;
     }
-    if (reortho && hdrift_host > 1e-8) {  // lrmc.py:258-259: every 64 updates
-      // ||U^T U - I||_max from the tracked H (which includes the pending
-      // update): re-orthonormalise with the pending update applied
-      RCUDA(launch_grouse_flush(u, v, r, pred.p, wn.p, gst.p, d.p, pidx.p, k, s));
-      double drift = 0.0;
-      if (int rc = rmx_orthonormalize(u, v, r, 1, &drift, stream, st)) return rc;
-      RCUDA(launch_h_identity(H.p, r, s));
+    if (reortho) {  // at most kDeferCap deferred terms: rewrite U
+      if (int rc = flush()) return rc;
+      if (hdrift_host > 1e-8) {  // lrmc.py:258-259 every 64 updates, from the tracked H
+        double drift = 0.0;
+        if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
+        RCUDA(launch_h_identity(H.p, r, s));
+      }
     }
     if (pass_end) {
       const double rel = hs.rel_sum / ell;
@@ -370,9 +385,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       }
     }
   }
-  RCUDA(launch_grouse_flush(u, v, r, pred.p, wn.p, gst.p, d.p, pidx.p, k, s));
+  if (int rc = flush()) return rc;
   double drift = 0.0;
-  if (int rc = rmx_orthonormalize(u, v, r, 0, &drift, stream, st)) return rc;
+  if (int rc = rmx_orthonormalize(ubase, v, r, 0, &drift, stream, st)) return rc;
+  if (ubase != u)
+    RCUDA(cudaMemcpyAsync(u, ubase, (size_t)v * r * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const int64_t tcount = (int64_t)passes * ell;
   if (passes_out) *passes_out = passes;
   if (converged_out) *converged_out = converged;

@@ -26,11 +26,32 @@ struct GrouseState {
   double pend_a;
   double rel_sum;  // sum over the pass of |r| / |t_Omega|
   double pend_b;   // beta of the pending update (d = beta r on Omega)
-  double aa;       // |a|^2 of the pending update a = pend_a p + d
+  double aa;       // |p|^2 = w^T H w of the pending update
+  int nterms;      // deferred sparse terms since the last flush (M-deferred GROUSE)
+  int pad2;
 };
+// M-deferred GROUSE: U = U_base M + sum_s d_s c_s^T (d_s sparse on Omega_s)
+constexpr int kDeferCap = 64;  // terms between flushes (the host flushes every 64 updates)
+cudaError_t launch_gemm_rm(const double* A, int64_t lda, const int32_t* idx, int64_t rows, int r,
+                           const double* B, double* C, cudaStream_t s);
+cudaError_t launch_sparse_terms(double* out, int r, const int32_t* rows_sorted, int k,
+                                const int32_t* d_idx, const double* d_val, const double* cmat,
+                                const GrouseState* st, int dense, cudaStream_t s);
+cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
+                             const double* w, int r, const GrouseState* st, double* hw, double* mw,
+                             double* dots, cudaStream_t s);
+cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int32_t* flag,
+                                 double step, int64_t step_index, const int32_t* idx, int k,
+                                 const double* resid, const double* w, int r, int32_t* d_idx,
+                                 double* d_val, double* cmat, double* wn, int32_t* final_slot,
+                                 const double* hw, cudaStream_t s);
+cudaError_t launch_defer_apply(double* M, double* cmat, double* H, const double* hg,
+                               GrouseState* st, const double* mw, const double* dots,
+                               const double* wn, int r, cudaStream_t s);
+cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s);
 // H = U^T U tracked through the rank-1 updates (the every-64-updates drift
 // check of lrmc.py:258-259 without a 168 GFLOP Gram)
-cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* w,
+cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
                             const double* wn, const double* ug, int k, const double* vals,
                             const double* resid, const double* sums, double* g, cudaStream_t s);
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);

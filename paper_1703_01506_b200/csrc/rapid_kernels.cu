@@ -857,42 +857,33 @@ __global__ void __launch_bounds__(1024) k_grouse_post(
 //   g = U^T a = pend_a H w + pend_b ug^T resid,
 //   |a|^2 = pend_a^2 |p|^2 + 2 pend_a pend_b (ug w).resid + pend_b^2 |resid|^2,
 //   H += b g^T + g b^T + |a|^2 b b^T.
-// k_h_g: warp per column c of g (and the scalar |a|^2 in block 0).
-__global__ void k_h_g(const double* __restrict__ H, int r, const GrouseState* __restrict__ st,
-                      const double* __restrict__ w, const double* __restrict__ ug, int k,
-                      const double* __restrict__ vals, const double* __restrict__ resid,
-                      const double* __restrict__ sums, double* __restrict__ g,
-                      double* __restrict__ aa_out) {
+// k_h_g: g = pend_a hw + pend_b ug^T resid (block of 32 columns x 8 row
+// lanes: coalesced over the gathered rows) and |a|^2 in block 0.
+__global__ void k_h_g(const double* __restrict__ hw, int r, const GrouseState* __restrict__ st,
+                      const double* __restrict__ ug, int k, const double* __restrict__ vals,
+                      const double* __restrict__ resid, const double* __restrict__ sums,
+                      double* __restrict__ g, double* __restrict__ aa_out) {
   if (st->halted || !st->pending) return;
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  __shared__ double part[8][33];
   const double a = st->pend_a, bb = st->pend_b;
-  if (c < r) {
-    double hw = 0.0, ur = 0.0;
-    for (int j = lane; j < r; j += 32) hw = fma(H[(int64_t)c * r + j], w[j], hw);
-    for (int i = lane; i < k; i += 32) ur = fma(ug[(int64_t)i * r + c], resid[i], ur);
-    for (int o = 16; o > 0; o >>= 1) {
-      hw += __shfl_xor_sync(0xffffffffu, hw, o);
-      ur += __shfl_xor_sync(0xffffffffu, ur, o);
-    }
-    if (lane == 0) g[c] = a * hw + bb * ur;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  double ur = 0.0;
+  if (c < r)
+    for (int i = ty; i < k; i += 8) ur = fma(ug[(int64_t)i * r + c], resid[i], ur);
+  part[ty][tx] = ur;
+  __syncthreads();
+  if (ty == 0 && c < r) {
+    double t = 0.0;
+    for (int q = 0; q < 8; ++q) t += part[q][tx];
+    g[c] = a * hw[c] + bb * t;
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {  // |a|^2 (ug w = vals - resid)
+  if (blockIdx.x == 0 && ty == 1) {  // |a|^2 (ug w = vals - resid; |p|^2 in st->aa)
     double pr = 0.0;
-    for (int i = lane; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
+    for (int i = tx; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
     for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
-    if (lane == 0) *aa_out = a * a * sums[1] + 2.0 * a * bb * pr + bb * bb * sums[0];
+    if (tx == 0) *aa_out = a * a * st->aa + 2.0 * a * bb * pr + bb * bb * sums[0];
   }
-}
-
-__global__ void k_h_rank2(double* __restrict__ H, int r, const GrouseState* __restrict__ st,
-                          const double* __restrict__ b, const double* __restrict__ g,
-                          const double* __restrict__ aa) {
-  if (st->halted || !st->pending) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)r * r) return;
-  const int i = (int)(e / r), j = (int)(e % r);
-  H[e] += b[i] * g[j] + g[i] * b[j] + *aa * b[i] * b[j];
 }
 
 __global__ void k_h_drift(const double* __restrict__ H, int r, double* __restrict__ out) {
@@ -915,6 +906,248 @@ __global__ void k_h_drift(const double* __restrict__ H, int r, double* __restric
 __global__ void k_h_identity(double* __restrict__ H, int r) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < (int64_t)r * r) H[e] = (e / r == e % r) ? 1.0 : 0.0;
+}
+
+// ---- M-deferred GROUSE (no pass over U per update)
+// U_t = U_base M_t + sum_s d_s c_s^T: the rotation part of every update
+// folds into the r x r matrix M (M <- M (I + a w b^T)), the residual part
+// stays a sparse term (d_s = beta_s r_s on Omega_s, c_s its r-vector, itself
+// rotated by later updates), and |p| = |U w| comes from the tracked
+// H = U^T U.  U_base is rewritten once per 64 updates (k_gemm_rm + the
+// sparse terms), instead of a read + write of U every update.
+
+// C[i][c] = sum_j A[row_i][j] B[j][c]  (row_i = idx ? idx[i] : i), r x r B,
+// 64x64 output tiles, 256 threads with 4x4 register tiles, K chunks of 16
+constexpr int kMT = 64, kMK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm_rm(const double* __restrict__ A, int64_t lda,
+                                                 const int32_t* __restrict__ idx, int64_t rows,
+                                                 int r, const double* __restrict__ B,
+                                                 double* __restrict__ C) {
+  __shared__ __align__(16) double As[kMK][kMT + 2];
+  __shared__ __align__(16) double Bs[kMK][kMT];
+  const int64_t i0 = (int64_t)blockIdx.x * kMT;
+  const int c0 = blockIdx.y * kMT;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // cols tx*4, rows ty*4
+  double acc[4][4] = {};
+  for (int j0 = 0; j0 < r; j0 += kMK) {
+    for (int e = tid; e < kMT * kMK; e += 256) {  // A chunk, transposed into As[j][i]
+      const int ii = e / kMK, jj = e % kMK;
+      const int64_t i = i0 + ii;
+      double val = 0.0;
+      if (i < rows && j0 + jj < r) val = A[(idx ? (int64_t)idx[i] : i) * lda + j0 + jj];
+      As[jj][ii] = val;
+    }
+    for (int e = tid; e < kMK * kMT; e += 256) {
+      const int jj = e / kMT, cc = e % kMT;
+      Bs[jj][cc] = (j0 + jj < r && c0 + cc < r) ? B[(int64_t)(j0 + jj) * r + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < kMK; ++jj) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = As[jj][ty * 4 + q];
+        b[q] = Bs[jj][tx * 4 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], b[u], acc[q][u]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t i = i0 + ty * 4 + q;
+    if (i >= rows) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + tx * 4 + u;
+      if (c < r) C[i * r + c] = acc[q][u];
+    }
+  }
+}
+
+// out += sum_s d_s c_s^T restricted to out's rows.  dense: out has v rows
+// (the flush, row index = voxel); else out row i holds voxel rows_sorted[i]
+// (the gathered Omega rows) and each term's voxels are located there by
+// binary search.  Block per term, thread per entry of Omega_s.
+__global__ void k_sparse_terms(double* __restrict__ out, int r,
+                               const int32_t* __restrict__ rows_sorted, int k,
+                               const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
+                               const double* __restrict__ cmat, const GrouseState* __restrict__ st,
+                               int dense) {
+  const int sterm = blockIdx.x;
+  if (st->halted || sterm >= st->nterms) return;
+  const int32_t* di = d_idx + (int64_t)sterm * k;
+  const double* dv = d_val + (int64_t)sterm * k;
+  const double* cs = cmat + (int64_t)sterm * r;
+  for (int q = threadIdx.x; q < k; q += blockDim.x) {
+    const int32_t vox = di[q];
+    int64_t row = -1;
+    if (dense) {
+      row = vox;
+    } else {  // position of vox in the sorted Omega, if present
+      int lo = 0, hi = k - 1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int32_t x = rows_sorted[mid];
+        if (x == vox) {
+          row = mid;
+          break;
+        }
+        if (x < vox) lo = mid + 1;
+        else hi = mid - 1;
+      }
+    }
+    if (row < 0) continue;
+    const double dq = dv[q];
+    double* o = out + row * r;
+    for (int c = 0; c < r; ++c) atomicAdd(o + c, dq * cs[c]);
+  }
+}
+
+// Per-update matrix-vector products, one warp per output (coalesced rows):
+// hw = H w (for |p|^2 = w.hw and the H update), mw = M w (the M update) and
+// dots[s] = w . c_s for the live terms.
+__global__ void k_defer_vec(const double* __restrict__ H, const double* __restrict__ M,
+                            const double* __restrict__ cmat, const double* __restrict__ w, int r,
+                            const GrouseState* __restrict__ st, double* __restrict__ hw,
+                            double* __restrict__ mw, double* __restrict__ dots) {
+  const int task = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  const double* row;
+  double* out;
+  if (task < r) {
+    row = H + (int64_t)task * r;
+    out = hw + task;
+  } else if (task < 2 * r) {
+    row = M + (int64_t)(task - r) * r;
+    out = mw + (task - r);
+  } else if (task < 2 * r + st->nterms) {
+    row = cmat + (int64_t)(task - 2 * r) * r;
+    out = dots + (task - 2 * r);
+  } else {
+    return;
+  }
+  double acc = 0.0;
+  for (int j = lane; j < r; j += 32) acc = fma(row[j], w[j], acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) *out = acc;
+}
+
+// decisions as k_grouse_post; the update becomes deferred term nterms
+__global__ void __launch_bounds__(1024) k_grouse_post_m(
+    GrouseState* __restrict__ st, const double* __restrict__ sums, const int32_t* __restrict__ flag,
+    double step, int64_t step_index, const int32_t* __restrict__ idx, int k,
+    const double* __restrict__ resid, const double* __restrict__ w, int r,
+    int32_t* __restrict__ d_idx, double* __restrict__ d_val, double* __restrict__ cmat,
+    double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw) {
+  __shared__ int skip, do_update, slot;
+  __shared__ double sb, sinvw, sa, pnorm2;
+  __shared__ double part[32];
+  {  // |p|^2 = |U w|^2 = w^T H w
+    double acc = 0.0;
+    for (int c = threadIdx.x; c < r; c += blockDim.x) acc = fma(w[c], hw[c], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += part[i];
+      pnorm2 = t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    skip = 0;
+    if (st->halted) {
+      skip = 1;
+    } else if (*flag) {
+      st->halted = 1;
+      st->halt_step = (int)step_index;
+      skip = 1;
+    } else {
+      const double resid_norm = sqrt(fmax(sums[0], 0.0));
+      const double pred_norm = sqrt(fmax(pnorm2, 0.0));
+      const double t_norm = sqrt(fmax(sums[2], 0.0));
+      const double w_norm = sqrt(fmax(sums[5], 0.0));
+      int upd = !(step == 0.0 || resid_norm == 0.0);
+      if (upd && (pred_norm == 0.0 || w_norm == 0.0)) upd = 0;
+      if (upd && resid_norm <= 1e-14 * fmax(1.0, pred_norm)) upd = 0;
+      double a = 0.0, bcoef = 0.0;
+      if (upd) {
+        const double theta = step * atan(resid_norm / pred_norm);
+        a = (cos(theta) - 1.0) / pred_norm;
+        bcoef = sin(theta) / resid_norm;
+      }
+      do_update = upd;
+      sa = a;
+      sb = bcoef;
+      sinvw = upd ? 1.0 / w_norm : 0.0;
+      slot = st->nterms;
+      st->aa = pnorm2;  // |p|^2 for the H update
+      st->rel_sum += t_norm > 0.0 ? resid_norm / t_norm : 0.0;
+    }
+  }
+  __syncthreads();
+  if (skip) return;
+  if (do_update) {
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+      d_idx[(int64_t)slot * k + i] = idx[i];
+      d_val[(int64_t)slot * k + i] = sb * resid[i];
+    }
+    for (int c = threadIdx.x; c < r; c += blockDim.x) {
+      const double bc = w[c] * sinvw;
+      wn[c] = bc;
+      cmat[(int64_t)slot * r + c] = bc;
+    }
+  }
+  if (final_slot)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) final_slot[i] = idx[i];
+  if (threadIdx.x == 0) {
+    st->pending = do_update;
+    st->pend_a = sa;
+    st->pend_b = sb;
+  }
+}
+
+// after k_grouse_post_m (+ the H update): M <- M + a (M w) b^T and the older
+// terms c_s <- c_s + a (w . c_s) b; block row y: M row y (y < r) or term
+// y - r; then k_defer_count adds the new term
+__global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ cmat,
+                              double* __restrict__ H, const double* __restrict__ g,
+                              const GrouseState* __restrict__ st, const double* __restrict__ mw,
+                              const double* __restrict__ dots, const double* __restrict__ b,
+                              int r) {
+  if (st->halted || !st->pending) return;
+  const int y = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= r) return;
+  const double a = st->pend_a;
+  if (y < r) {
+    M[(int64_t)y * r + c] = fma(a * mw[y], b[c], M[(int64_t)y * r + c]);
+  } else if (y < 2 * r) {  // H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2)
+    const int i = y - r;
+    H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
+  } else if (y - 2 * r < st->nterms) {
+    const int sterm = y - 2 * r;
+    cmat[(int64_t)sterm * r + c] = fma(a * dots[sterm], b[c], cmat[(int64_t)sterm * r + c]);
+  }
+}
+
+__global__ void k_defer_count(GrouseState* __restrict__ st) {
+  if (st->halted || !st->pending) return;
+  st->nterms += 1;
+  st->pending = 0;
+}
+
+__global__ void k_flush_reset(double* __restrict__ M, int r, GrouseState* __restrict__ st) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (int64_t)r * r) M[e] = (e / r == e % r) ? 1.0 : 0.0;
+  if (e == 0) st->nterms = 0;
 }
 
 // apply a pending update to all of U (before a re-orthonormalisation)
@@ -1212,12 +1445,12 @@ cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, doub
   return cudaGetLastError();
 }
 
-cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* w,
+cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
                             const double* wn, const double* ug, int k, const double* vals,
                             const double* resid, const double* sums, double* g, cudaStream_t s) {
-  k_h_g<<<(unsigned)((r + 7) / 8), 256, 0, s>>>(H, r, st, w, ug, k, vals, resid, sums, g, g + r);
-  const int64_t n = (int64_t)r * r;
-  k_h_rank2<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, r, st, wn, g, g + r);
+  (void)H;
+  (void)wn;
+  k_h_g<<<(unsigned)((r + 31) / 32), 256, 0, s>>>(hw, r, st, ug, k, vals, resid, sums, g, g + r);
   return cudaGetLastError();
 }
 
@@ -1229,6 +1462,54 @@ cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s) 
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
   const int64_t n = (int64_t)r * r;
   k_h_identity<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_rm(const double* A, int64_t lda, const int32_t* idx, int64_t rows, int r,
+                           const double* B, double* C, cudaStream_t s) {
+  const int64_t bx = (rows + kMT - 1) / kMT;
+  k_gemm_rm<<<dim3((unsigned)bx, (unsigned)((r + kMT - 1) / kMT)), 256, 0, s>>>(A, lda, idx, rows,
+                                                                                   r, B, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_terms(double* out, int r, const int32_t* rows_sorted, int k,
+                                const int32_t* d_idx, const double* d_val, const double* cmat,
+                                const GrouseState* st, int dense, cudaStream_t s) {
+  k_sparse_terms<<<kDeferCap, 256, 0, s>>>(out, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
+                             const double* w, int r, const GrouseState* st, double* hw, double* mw,
+                             double* dots, cudaStream_t s) {
+  const int tasks = 2 * r + kDeferCap;
+  k_defer_vec<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(H, M, cmat, w, r, st, hw, mw, dots);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int32_t* flag,
+                                 double step, int64_t step_index, const int32_t* idx, int k,
+                                 const double* resid, const double* w, int r, int32_t* d_idx,
+                                 double* d_val, double* cmat, double* wn, int32_t* final_slot,
+                                 const double* hw, cudaStream_t s) {
+  k_grouse_post_m<<<1, 1024, 0, s>>>(st, sums, flag, step, step_index, idx, k, resid, w, r, d_idx,
+                                     d_val, cmat, wn, final_slot, hw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_defer_apply(double* M, double* cmat, double* H, const double* hg,
+                               GrouseState* st, const double* mw, const double* dots,
+                               const double* wn, int r, cudaStream_t s) {
+  k_defer_apply<<<dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)), 256, 0, s>>>(
+      M, cmat, H, hg, st, mw, dots, wn, r);
+  k_defer_count<<<1, 1, 0, s>>>(st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s) {
+  const int64_t n = (int64_t)r * r;
+  k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, r, st);
   return cudaGetLastError();
 }
 
