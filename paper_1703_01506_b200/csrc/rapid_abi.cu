@@ -8,6 +8,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "../../include/rmx.h"
 #include "rapid_internal.cuh"
 #include "rmx_internal.cuh"
@@ -40,6 +42,34 @@ void rclear(rmx_status* st) {
     if (_e != cudaSuccess)                                                           \
       return rset(st, RMX_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(_e));   \
   } while (0)
+
+#define RBLAS(call)                                                                  \
+  do {                                                                               \
+    cublasStatus_t _b = (call);                                                      \
+    if (_b != CUBLAS_STATUS_SUCCESS)                                                 \
+      return rset(st, RMX_E_CUDA, "%s failed: cuBLAS status %d", #call, (int)_b);    \
+  } while (0)
+
+// plain fp64 library GEMMs of the deferred GROUSE (row-major operands)
+struct Blas {
+  cublasHandle_t h = nullptr;
+  ~Blas() {
+    if (h) cublasDestroy(h);
+  }
+  // C (m x n, ldc) = A (m x kk, lda) B (kk x n, ldb)
+  cublasStatus_t gemm_rm(int64_t m, int n, int kk, const double* A, int64_t lda, const double* B,
+                         int64_t ldb, double* C, int64_t ldc) const {
+    const double one = 1.0, zero = 0.0;
+    return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)m, kk, &one, B, (int)ldb, A, (int)lda,
+                       &zero, C, (int)ldc);
+  }
+  // G (n x n, row- or column-major: symmetric) = A^T A, A (rows x n, lda)
+  cublasStatus_t gram(int64_t rows, int n, const double* A, int64_t lda, double* G) const {
+    const double one = 1.0, zero = 0.0;
+    return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, (int)rows, &one, A, (int)lda, A,
+                       (int)lda, &zero, G, n);
+  }
+};
 
 size_t gram_bytes(int r) { return (size_t)(r + 1) * (r + 1) * sizeof(double); }
 
@@ -252,7 +282,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // sums: 0 |r|^2 1 |p|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
-  DevBuf<double> G, w, vals, resid, sums, wn, ug, ub2, M, cmat, dval, H, hg, hdrift, hw, mw, dots;
+  DevBuf<double> G, w, vals, resid, sums, wn, ug, ubuf, ub2, M, cmat, dval, H, hg, hdrift, hw, mw,
+      dots, wprev;
   DevBuf<int32_t> flag, idxbuf, didx;
   DevBuf<GrouseState> gst;
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
@@ -263,19 +294,32 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(sums.alloc(8, s));
   RCUDA(flag.alloc(1, s));
   RCUDA(idxbuf.alloc(k, s));
-  RCUDA(ug.alloc((size_t)k * r, s));
+  const int64_t lu = r + 1;  // ug rows: [U_Omega row | t_Omega] (the Gram's operand)
+  RCUDA(ug.alloc((size_t)k * lu, s));
+  RCUDA(ubuf.alloc((size_t)k * r, s));
+  Blas blas;
+  RBLAS(cublasCreate(&blas.h));
+  RBLAS(cublasSetStream(blas.h, s));
   RCUDA(ub2.alloc((size_t)v * r, s));
   RCUDA(M.alloc((size_t)r * r, s));
   RCUDA(cmat.alloc((size_t)kDeferCap * r, s));
   RCUDA(dval.alloc((size_t)kDeferCap * k, s));
   RCUDA(didx.alloc((size_t)kDeferCap * k, s));
   RCUDA(H.alloc((size_t)r * r, s));
-  RCUDA(hg.alloc((size_t)r + 1, s));
+  RCUDA(hg.alloc((size_t)r + 1 + 16 * (size_t)r, s));  // g, |a|^2, k_h_g partials
   RCUDA(hdrift.alloc(1, s));
   RCUDA(hw.alloc(r, s));
   RCUDA(mw.alloc(r, s));
   RCUDA(dots.alloc(kDeferCap, s));
   RCUDA(gst.alloc(1, s));
+  // each column's CG solution from the previous pass warm-starts its next
+  // solve (same stopping rule |G w - b| <= 1e-13 |b|, far fewer iterations
+  // once the basis settles)
+  const bool warm = !getenv("RMX_GROUSE_COLD");
+  if (warm) {
+    RCUDA(wprev.alloc((size_t)ell * r, s));
+    RCUDA(cudaMemsetAsync(wprev.p, 0, (size_t)ell * r * sizeof(double), s));
+  }
   RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(GrouseState), s));
   RCUDA(launch_flush_reset(M.p, r, gst.p, s));  // M = I, no terms
   RCUDA(launch_h_identity(H.p, r, s));          // the caller hands in an orthonormalised U
@@ -287,8 +331,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   double* ubase = u;
   double* uother = ub2.p;
   auto flush = [&]() -> int {
-    RCUDA(launch_gemm_rm(ubase, r, nullptr, v, r, M.p, uother, s));
-    RCUDA(launch_sparse_terms(uother, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
+    RBLAS(blas.gemm_rm(v, r, r, ubase, r, M.p, r, uother, r));
+    RCUDA(launch_sparse_terms(uother, r, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
     std::swap(ubase, uother);
     RCUDA(launch_flush_reset(M.p, r, gst.p, s));
     return RMX_OK;
@@ -301,23 +345,26 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
     const double* trow = t + (int64_t)i * v;
-    RCUDA(launch_gemm_rm(ubase, r, idx, k, r, M.p, ug.p, s));
-    RCUDA(launch_sparse_terms(ug.p, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
-    RCUDA(launch_gather_vals(trow, idx, k, vals.p, s));
-    RCUDA(launch_gram(ug.p, r, r, nullptr, k, vals.p, G.p, 1, s));
+    RCUDA(launch_gather_urows(ubase, r, idx, k, ubuf.p, s));
+    RBLAS(blas.gemm_rm(k, r, r, ubuf.p, r, M.p, r, ug.p, lu));
+    RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
+    RCUDA(launch_gather_vals_aug(trow, idx, k, vals.p, ug.p + r, lu, s));
+    RBLAS(blas.gram(k, (int)lu, ug.p, lu, G.p));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
     if (use_cg) {
-      RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13, s));
+      RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,
+                            warm ? wprev.p + (int64_t)i * r : nullptr, s));
       RCUDA(launch_chol_if_flag(G.p, r, w.p, flag.p, sums.p + 4, s));
     } else {
       RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
     }
-    RCUDA(launch_resid(ug.p, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
+    RCUDA(launch_resid(ug.p, lu, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
     RCUDA(launch_defer_vec(H.p, M.p, cmat.p, w.p, r, gst.p, hw.p, mw.p, dots.p, s));
     RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
                                didx.p, dval.p, cmat.p, wn.p,
                                final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));
-    RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, k, vals.p, resid.p, sums.p, hg.p, s));
+    RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, lu, k, vals.p, resid.p, sums.p, hg.p,
+                          s));
     RCUDA(launch_defer_apply(M.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r, s));
     (void)p;
     return RMX_OK;

@@ -17,11 +17,11 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s);
 // GROUSE step state kept on the device, so the update loop runs without a
-// host round trip per update (decisions by k_grouse_post).
+// host round trip per update (decisions by k_grouse_post_m).
 struct GrouseState {
   int halted;      // a solve flagged ill-conditioning: later step kernels no-op
   int halt_step;   // global update index that halted
-  int pending;     // a deferred rank-1 update (pend_a, d on pidx, wn) is pending
+  int pending;     // this step's update (pend_a, pend_b, wn) is still to be folded into M/H
   int pad;
   double pend_a;
   double rel_sum;  // sum over the pass of |r| / |t_Omega|
@@ -32,11 +32,14 @@ struct GrouseState {
 };
 // M-deferred GROUSE: U = U_base M + sum_s d_s c_s^T (d_s sparse on Omega_s)
 constexpr int kDeferCap = 64;  // terms between flushes (the host flushes every 64 updates)
-cudaError_t launch_gemm_rm(const double* A, int64_t lda, const int32_t* idx, int64_t rows, int r,
-                           const double* B, double* C, cudaStream_t s);
-cudaError_t launch_sparse_terms(double* out, int r, const int32_t* rows_sorted, int k,
+cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
                                 const int32_t* d_idx, const double* d_val, const double* cmat,
                                 const GrouseState* st, int dense, cudaStream_t s);
+cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
+                                cudaStream_t s);
+// vals[i] = t[idx[i]] and aug[i * ldaug] = the same (the Gram's extra column)
+cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
+                                   double* aug, int64_t ldaug, cudaStream_t s);
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
                              double* dots, cudaStream_t s);
@@ -52,24 +55,12 @@ cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s
 // H = U^T U tracked through the rank-1 updates (the every-64-updates drift
 // check of lrmc.py:258-259 without a 168 GFLOP Gram)
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
-                            const double* wn, const double* ug, int k, const double* vals,
-                            const double* resid, const double* sums, double* g, cudaStream_t s);
+                            const double* wn, const double* ug, int64_t ldu, int k,
+                            const double* vals, const double* resid, const double* sums, double* g,
+                            cudaStream_t s);
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
-cudaError_t launch_gather_pending_st(const double* U, int r, const int32_t* idx, int k,
-                                     const GrouseState* st, const double* pred, const double* d,
-                                     const double* wn, double* out, cudaStream_t s);
-cudaError_t launch_pred_apply_st(double* U, int64_t v, int r, const double* w, double* pred,
-                                 double* sums, const GrouseState* st, const double* d,
-                                 const double* wn, const int32_t* flag, cudaStream_t s);
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                                cudaStream_t s);
-cudaError_t launch_grouse_post(GrouseState* st, const double* sums, const int32_t* flag,
-                               double step, int64_t step_index, const int32_t* idx, int k,
-                               const double* resid, const double* w, int r, double* d,
-                               int32_t* pidx, double* wn, int32_t* final_slot, cudaStream_t s);
-cudaError_t launch_grouse_flush(double* U, int64_t v, int r, const double* pred, const double* wn,
-                                GrouseState* st, double* d, const int32_t* pidx, int k,
                                 cudaStream_t s);
 // K4 on tcgen05: operand preparation and the max decode
 cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
@@ -78,21 +69,21 @@ cudaError_t launch_w_rows(const float* W, int64_t B, int r, int kpad, __half* wA
                           cudaStream_t s);
 cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, double* out,
                                 cudaStream_t s);
-// one well-conditioned system (GROUSE) by cluster CG; flag = not converged
+// one well-conditioned system (GROUSE) by cluster CG; flag = not converged;
+// x0 (optional, in/out): starting point, overwritten with the solution
 bool cg_solve_supported(int r);
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                            double tol, cudaStream_t s);
+                            double tol, double* x0, cudaStream_t s);
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
                                 int64_t perm_base, double sigma, double mu, uint64_t seed,
                                 int two_sided, const float* znoise, const double* base,
                                 double* max_out, cudaStream_t s);
-cudaError_t launch_resid(const double* U, int r, const int32_t* idx, int k, const double* vals,
-                         const double* w, double* resid, double* sums, cudaStream_t s);
+cudaError_t launch_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
+                         const double* vals, const double* w, double* resid, double* sums,
+                         cudaStream_t s);
 cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, double* pred,
                         double* sums, cudaStream_t s);
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s);
-cudaError_t launch_gather_vals(const double* t, const int32_t* idx, int k, double* vals,
-                               cudaStream_t s);
 cudaError_t launch_max_dev_identity(const double* G, int r, double* out, cudaStream_t s);
 cudaError_t launch_row_max(const double* A, int64_t rows, int64_t cols, int two_sided,
                            double* out, cudaStream_t s);

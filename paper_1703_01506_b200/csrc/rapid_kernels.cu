@@ -11,8 +11,10 @@
 //   k_complete_max  K4 on CUDA cores: max_j (W U^T)[p, j] + sigma z(p, j)
 //                   (+ mu) (rapid.py:198-205; the tcgen05 version is
 //                   k_tfill_tc<..., MODE 1> in tfill_tc.cu)
-//   GROUSE step     k_gather_pending_st, k_resid, k_pred_apply_st,
-//                   k_grouse_post, k_h_g / k_h_rank2 (lrmc.py:160-193)
+//   GROUSE step     M-deferred (lrmc.py:160-193): k_gather_urows + cuBLAS
+//                   DGEMM by M, k_sparse_terms, cuBLAS Gram, k_cg_solve
+//                   (warm-started), k_resid, k_defer_vec, k_grouse_post_m,
+//                   k_h_g_part/_fin, k_defer_apply; flush every 64 updates
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -448,7 +450,8 @@ __device__ __forceinline__ void cg_allreduce2(double a, double b, double* slots,
 __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
                                                          double* __restrict__ w_out,
                                                          int32_t* __restrict__ flag,
-                                                         double* __restrict__ resid2, double tol) {
+                                                         double* __restrict__ resid2, double tol,
+                                                         double* __restrict__ x0) {
   extern __shared__ double cs[];
   const int R = (r + kCgCtas - 1) / kCgCtas;  // rows per CTA
   const uint32_t me = cluster_ctarank();
@@ -466,22 +469,43 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     const int i = e / r, j = e % r;
     Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
   }
-  double pb = 0.0, pz = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
-    const double bi = G[(int64_t)r * ld + r0 + i];
     const double di = G[(int64_t)(r0 + i) * ld + r0 + i];
     dinv[i] = di > 0.0 ? 1.0 / di : 1.0;
-    x[i] = 0.0;
-    res[i] = bi;
-    z[i] = bi * dinv[i];
+    x[i] = x0 ? x0[r0 + i] : 0.0;
+    q[i] = 0.0;
+  }
+  if (x0) {  // warm start (the column's solution from the previous pass): q = G x0
+    __syncthreads();
+    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
+      const int i = e % nr, dst = e / nr;
+      st_cluster_f64(pfull + r0 + i, dst, x[i]);
+    }
+    cluster_sync();
+    for (int i = wid; i < nr; i += kCgThreads / 32) {
+      const double* gi = Gs + (size_t)i * r;
+      double acc = 0.0;
+      for (int j = lane; j < r; j += 32) acc = fma(gi[j], pfull[j], acc);
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) q[i] = acc;
+    }
+    __syncthreads();
+  }
+  double pb = 0.0, pz = 0.0, pr = 0.0;
+  for (int i = tid; i < nr; i += kCgThreads) {
+    const double bi = G[(int64_t)r * ld + r0 + i];
+    res[i] = bi - q[i];
+    z[i] = res[i] * dinv[i];
     p[i] = z[i];
     pb += bi * bi;
-    pz += bi * z[i];
+    pz += res[i] * z[i];
+    pr += res[i] * res[i];
   }
-  double bb, rz;
+  double bb, rz, rr0 = 0.0, dummy0;
   cg_allreduce2(pb, pz, slots, wsum, bb, rz);
+  if (x0) cg_allreduce2(pr, 0.0, slots + 2 * kCgCtas, wsum, rr0, dummy0);
   const double stop = tol * tol * bb;
-  int converged = bb == 0.0;
+  int converged = bb == 0.0 || (x0 && rr0 <= stop);
   int it = 0;
   for (; it < r && !converged; ++it) {
     // share this CTA's direction rows with every CTA
@@ -527,6 +551,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   double pw = 0.0, pbw = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
     if (w_out) w_out[r0 + i] = x[i];
+    if (x0) x0[r0 + i] = x[i];
     pw += x[i] * x[i];
     pbw += G[(int64_t)r * ld + r0 + i] * x[i];
   }
@@ -690,12 +715,13 @@ __global__ void __launch_bounds__(256) k_complete_max(
 
 // ------------------------------------------------------------------ GROUSE
 // resid[i] = vals[i] - U[idx[i], :] . w   (k rows, one warp per row)
-__global__ void k_resid(const double* __restrict__ U, int r, const int32_t* __restrict__ idx, int k,
+__global__ void k_resid(const double* __restrict__ U, int64_t ldu, int r,
+                        const int32_t* __restrict__ idx, int k,
                         const double* __restrict__ vals, const double* __restrict__ w,
                         double* __restrict__ resid, double* __restrict__ sums) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (warp >= k) return;
-  const double* u = U + (int64_t)(idx ? idx[warp] : warp) * r;
+  const double* u = U + (int64_t)(idx ? idx[warp] : warp) * ldu;
   double s = 0.0;
   for (int c = lane; c < r; c += 32) s += u[c] * w[c];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -733,156 +759,59 @@ __global__ void k_pred(const double* __restrict__ U, int64_t v, int r, const dou
   }
 }
 
-// ---- device-resident GROUSE step (no host round trip per update)
-// The rank-1 update of step t, U += (a p_t + d_t) wn_t^T (p_t = U w_t, d_t
-// the scattered residual), is deferred: the next step gathers its Omega rows
-// with the pending term added (k_gather_pending_st) and its prediction pass
-// applies the update row by row while forming p_{t+1} = U' w_{t+1}
-// (k_pred_apply_st) -- one read and one write of U per update instead of a
-// read (prediction) plus a read-modify-write (update).  A flagged solve
-// halts the loop: the update stays pending until the host has resampled.
-__global__ void k_gather_pending_st(const double* __restrict__ U, int r,
-                                    const int32_t* __restrict__ idx, int k,
-                                    const GrouseState* __restrict__ st,
-                                    const double* __restrict__ pred, const double* __restrict__ d,
-                                    const double* __restrict__ wn, double* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)k * r) return;
-  const int i = (int)(e / r), c = (int)(e % r);
-  const int64_t row = idx[i];
-  double u = U[row * r + c];
-  if (st->pending) u = fma(fma(st->pend_a, pred[row], d[row]), wn[c], u);
-  out[e] = u;
-}
-
-__global__ void k_pred_apply_st(double* __restrict__ U, int64_t v, int r,
-                                const double* __restrict__ w, double* __restrict__ pred,
-                                double* __restrict__ sums, const GrouseState* __restrict__ st,
-                                const double* __restrict__ d, const double* __restrict__ wn,
-                                const int32_t* __restrict__ flag) {
-  if (st->halted || *flag) return;
-  const double a = st->pending ? st->pend_a : 0.0;  // not pending: d = 0, so coef = 0
-  __shared__ double part[32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
-  double local = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + wib; row < v;
-       row += (int64_t)gridDim.x * (blockDim.x / 32)) {
-    double* u = U + row * r;
-    const double coef = fma(a, pred[row], d[row]);
-    double sacc = 0.0;
-    for (int c = lane; c < r; c += 32) {
-      const double un = fma(coef, wn[c], u[c]);
-      u[c] = un;
-      sacc = fma(un, w[c], sacc);
-    }
-    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-    if (lane == 0) {
-      pred[row] = sacc;
-      local += sacc * sacc;
-    }
-  }
-  if (lane == 0) part[wib] = local;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += part[i];
-    atomicAdd(&sums[1], t);
-  }
-}
-
-// The host's per-update decisions of lrmc.py:160-193, on the device: norms,
-// step angle, the deferred update's coefficients; unscatter the applied
-// update, scatter the new one.  A flagged solve halts the loop (the host
-// resamples at its next sync point).
-__global__ void __launch_bounds__(1024) k_grouse_post(
-    GrouseState* __restrict__ st, const double* __restrict__ sums, const int32_t* __restrict__ flag,
-    double step, int64_t step_index, const int32_t* __restrict__ idx, int k,
-    const double* __restrict__ resid, const double* __restrict__ w, int r, double* __restrict__ d,
-    int32_t* __restrict__ pidx, double* __restrict__ wn, int32_t* __restrict__ final_slot) {
-  __shared__ int skip, old_pending, do_update;
-  __shared__ double sb, sinvw, sa;
-  if (threadIdx.x == 0) {
-    skip = 0;
-    if (st->halted) {
-      skip = 1;
-    } else if (*flag) {
-      st->halted = 1;
-      st->halt_step = (int)step_index;
-      skip = 1;
-    } else {
-      const double resid_norm = sqrt(fmax(sums[0], 0.0));
-      const double pred_norm = sqrt(fmax(sums[1], 0.0));
-      const double t_norm = sqrt(fmax(sums[2], 0.0));
-      const double w_norm = sqrt(fmax(sums[5], 0.0));
-      int upd = !(step == 0.0 || resid_norm == 0.0);
-      if (upd && (pred_norm == 0.0 || w_norm == 0.0)) upd = 0;
-      if (upd && resid_norm <= 1e-14 * fmax(1.0, pred_norm)) upd = 0;
-      double a = 0.0, bcoef = 0.0;
-      if (upd) {
-        const double theta = step * atan(resid_norm / pred_norm);
-        a = (cos(theta) - 1.0) / pred_norm;
-        bcoef = sin(theta) / resid_norm;
-      }
-      old_pending = st->pending;
-      do_update = upd;
-      sa = a;
-      sb = bcoef;
-      sinvw = upd ? 1.0 / w_norm : 0.0;
-      st->rel_sum += t_norm > 0.0 ? resid_norm / t_norm : 0.0;
-    }
-  }
-  __syncthreads();
-  if (skip) return;
-  if (old_pending)  // applied by k_pred_apply_st in this step
-    for (int i = threadIdx.x; i < k; i += blockDim.x) d[pidx[i]] = 0.0;
-  __syncthreads();
-  if (do_update) {
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-      d[idx[i]] = sb * resid[i];
-      pidx[i] = idx[i];
-    }
-    for (int c = threadIdx.x; c < r; c += blockDim.x) wn[c] = w[c] * sinvw;
-  }
-  if (final_slot)
-    for (int i = threadIdx.x; i < k; i += blockDim.x) final_slot[i] = idx[i];
-  if (threadIdx.x == 0) {
-    st->pending = do_update;
-    st->pend_a = sa;
-    st->pend_b = sb;
-  }
-}
-
 // H tracking: after k_grouse_post decided update t (a = pend_a p + d, b =
 // w/|w|, U the matrix before the update, ug = U[Omega] gathered rows):
 //   g = U^T a = pend_a H w + pend_b ug^T resid,
 //   |a|^2 = pend_a^2 |p|^2 + 2 pend_a pend_b (ug w).resid + pend_b^2 |resid|^2,
 //   H += b g^T + g b^T + |a|^2 b b^T.
-// k_h_g: g = pend_a hw + pend_b ug^T resid (block of 32 columns x 8 row
-// lanes: coalesced over the gathered rows) and |a|^2 in block 0.
-__global__ void k_h_g(const double* __restrict__ hw, int r, const GrouseState* __restrict__ st,
-                      const double* __restrict__ ug, int k, const double* __restrict__ vals,
-                      const double* __restrict__ resid, const double* __restrict__ sums,
-                      double* __restrict__ g, double* __restrict__ aa_out) {
+// k_h_g_part: partial ug^T resid over row slice blockIdx.y (32 columns x 8
+// row lanes per block, coalesced over the gathered rows); k_h_g_fin: g =
+// pend_a hw + pend_b sum(partials) and |a|^2 (ug w = vals - resid; |p|^2 in
+// st->aa) in g[r].
+constexpr int kHgSplit = 16;
+
+__global__ void k_h_g_part(int r, const GrouseState* __restrict__ st,
+                           const double* __restrict__ ug, int64_t ldu, int k,
+                           const double* __restrict__ resid, double* __restrict__ gpart) {
   if (st->halted || !st->pending) return;
   __shared__ double part[8][33];
-  const double a = st->pend_a, bb = st->pend_b;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
+  const int rows = (k + kHgSplit - 1) / kHgSplit;
+  const int i0 = blockIdx.y * rows, i1 = min(k, i0 + rows);
   double ur = 0.0;
   if (c < r)
-    for (int i = ty; i < k; i += 8) ur = fma(ug[(int64_t)i * r + c], resid[i], ur);
+#pragma unroll 4
+    for (int i = i0 + ty; i < i1; i += 8) ur = fma(ug[(int64_t)i * ldu + c], resid[i], ur);
   part[ty][tx] = ur;
   __syncthreads();
   if (ty == 0 && c < r) {
     double t = 0.0;
+#pragma unroll
     for (int q = 0; q < 8; ++q) t += part[q][tx];
+    gpart[(int64_t)blockIdx.y * r + c] = t;
+  }
+}
+
+__global__ void k_h_g_fin(const double* __restrict__ hw, int r, const GrouseState* __restrict__ st,
+                          int k, const double* __restrict__ vals, const double* __restrict__ resid,
+                          const double* __restrict__ sums, const double* __restrict__ gpart,
+                          double* __restrict__ g) {
+  if (st->halted || !st->pending) return;
+  const double a = st->pend_a, bb = st->pend_b;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < r) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kHgSplit; ++q) t += gpart[(int64_t)q * r + c];
     g[c] = a * hw[c] + bb * t;
   }
-  if (blockIdx.x == 0 && ty == 1) {  // |a|^2 (ug w = vals - resid; |p|^2 in st->aa)
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     double pr = 0.0;
-    for (int i = tx; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
+    for (int i = lane; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
     for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
-    if (tx == 0) *aa_out = a * a * st->aa + 2.0 * a * bb * pr + bb * bb * sums[0];
+    if (lane == 0) g[r] = a * a * st->aa + 2.0 * a * bb * pr + bb * bb * sums[0];
   }
 }
 
@@ -913,100 +842,68 @@ __global__ void k_h_identity(double* __restrict__ H, int r) {
 // folds into the r x r matrix M (M <- M (I + a w b^T)), the residual part
 // stays a sparse term (d_s = beta_s r_s on Omega_s, c_s its r-vector, itself
 // rotated by later updates), and |p| = |U w| comes from the tracked
-// H = U^T U.  U_base is rewritten once per 64 updates (k_gemm_rm + the
-// sparse terms), instead of a read + write of U every update.
+// H = U^T U.  U_base is rewritten once per 64 updates (a cuBLAS DGEMM by M +
+// the sparse terms), instead of a read + write of U every update.
 
-// C[i][c] = sum_j A[row_i][j] B[j][c]  (row_i = idx ? idx[i] : i), r x r B,
-// 64x64 output tiles, 256 threads with 4x4 register tiles, K chunks of 16
-constexpr int kMT = 64, kMK = 16;
-
-__global__ void __launch_bounds__(256) k_gemm_rm(const double* __restrict__ A, int64_t lda,
-                                                 const int32_t* __restrict__ idx, int64_t rows,
-                                                 int r, const double* __restrict__ B,
-                                                 double* __restrict__ C) {
-  __shared__ __align__(16) double As[kMK][kMT + 2];
-  __shared__ __align__(16) double Bs[kMK][kMT];
-  const int64_t i0 = (int64_t)blockIdx.x * kMT;
-  const int c0 = blockIdx.y * kMT;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // cols tx*4, rows ty*4
-  double acc[4][4] = {};
-  for (int j0 = 0; j0 < r; j0 += kMK) {
-    for (int e = tid; e < kMT * kMK; e += 256) {  // A chunk, transposed into As[j][i]
-      const int ii = e / kMK, jj = e % kMK;
-      const int64_t i = i0 + ii;
-      double val = 0.0;
-      if (i < rows && j0 + jj < r) val = A[(idx ? (int64_t)idx[i] : i) * lda + j0 + jj];
-      As[jj][ii] = val;
-    }
-    for (int e = tid; e < kMK * kMT; e += 256) {
-      const int jj = e / kMT, cc = e % kMT;
-      Bs[jj][cc] = (j0 + jj < r && c0 + cc < r) ? B[(int64_t)(j0 + jj) * r + c0 + cc] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int jj = 0; jj < kMK; ++jj) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = As[jj][ty * 4 + q];
-        b[q] = Bs[jj][tx * 4 + q];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], b[u], acc[q][u]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t i = i0 + ty * 4 + q;
-    if (i >= rows) continue;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + tx * 4 + u;
-      if (c < r) C[i * r + c] = acc[q][u];
-    }
-  }
-}
-
-// out += sum_s d_s c_s^T restricted to out's rows.  dense: out has v rows
-// (the flush, row index = voxel); else out row i holds voxel rows_sorted[i]
-// (the gathered Omega rows) and each term's voxels are located there by
-// binary search.  Block per term, thread per entry of Omega_s.
-__global__ void k_sparse_terms(double* __restrict__ out, int r,
+__global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
                                const int32_t* __restrict__ rows_sorted, int k,
                                const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
                                const double* __restrict__ cmat, const GrouseState* __restrict__ st,
                                int dense) {
+  __shared__ int64_t hit_row[256];
+  __shared__ double hit_val[256];
+  __shared__ int nhit;
   const int sterm = blockIdx.x;
   if (st->halted || sterm >= st->nterms) return;
   const int32_t* di = d_idx + (int64_t)sterm * k;
   const double* dv = d_val + (int64_t)sterm * k;
   const double* cs = cmat + (int64_t)sterm * r;
-  for (int q = threadIdx.x; q < k; q += blockDim.x) {
-    const int32_t vox = di[q];
-    int64_t row = -1;
-    if (dense) {
-      row = vox;
-    } else {  // position of vox in the sorted Omega, if present
-      int lo = 0, hi = k - 1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const int32_t x = rows_sorted[mid];
-        if (x == vox) {
-          row = mid;
-          break;
+  for (int base = 0; base < k; base += 256) {
+    if (threadIdx.x == 0) nhit = 0;
+    __syncthreads();
+    const int q = base + threadIdx.x;
+    if (q < k) {
+      const int32_t vox = di[q];
+      int64_t row = -1;
+      if (dense) {
+        row = vox;
+      } else {  // position of vox in the sorted Omega, if present
+        int lo = 0, hi = k - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int32_t x = rows_sorted[mid];
+          if (x == vox) {
+            row = mid;
+            break;
+          }
+          if (x < vox) lo = mid + 1;
+          else hi = mid - 1;
         }
-        if (x < vox) lo = mid + 1;
-        else hi = mid - 1;
+      }
+      if (row >= 0) {
+        const int slot = atomicAdd(&nhit, 1);
+        hit_row[slot] = row;
+        hit_val[slot] = dv[q];
       }
     }
-    if (row < 0) continue;
-    const double dq = dv[q];
-    double* o = out + row * r;
-    for (int c = 0; c < r; ++c) atomicAdd(o + c, dq * cs[c]);
+    __syncthreads();
+    const int n = nhit;
+    for (int h = 0; h < n; ++h) {  // the block adds d_q c_s^T to the hit rows
+      double* o = out + hit_row[h] * ldo;
+      const double dq = hit_val[h];
+      for (int c = threadIdx.x; c < r; c += blockDim.x) atomicAdd(o + c, dq * cs[c]);
+    }
+    __syncthreads();
   }
+}
+
+// gathered rows of U (k x r, row-major) for the cuBLAS product with M
+__global__ void k_gather_urows(const double* __restrict__ U, int r, const int32_t* __restrict__ idx,
+                               int k, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * r) return;
+  const int i = (int)(e / r), c = (int)(e - (int64_t)i * r);
+  out[e] = U[(int64_t)idx[i] * r + c];
 }
 
 // Per-update matrix-vector products, one warp per output (coalesced rows):
@@ -1150,28 +1047,6 @@ __global__ void k_flush_reset(double* __restrict__ M, int r, GrouseState* __rest
   if (e == 0) st->nterms = 0;
 }
 
-// apply a pending update to all of U (before a re-orthonormalisation)
-__global__ void k_grouse_flush_update(double* __restrict__ U, int64_t v, int r,
-                                      const double* __restrict__ pred,
-                                      const double* __restrict__ wn,
-                                      const GrouseState* __restrict__ st,
-                                      const double* __restrict__ d) {
-  if (!st->pending) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= v * r) return;
-  const int64_t row = e / r;
-  const int c = (int)(e % r);
-  U[e] = fma(fma(st->pend_a, pred[row], d[row]), wn[c], U[e]);
-}
-
-__global__ void k_grouse_flush_done(GrouseState* __restrict__ st, double* __restrict__ d,
-                                    const int32_t* __restrict__ pidx, int k) {
-  if (!st->pending) return;
-  for (int i = threadIdx.x; i < k; i += blockDim.x) d[pidx[i]] = 0.0;
-  __syncthreads();
-  if (threadIdx.x == 0) st->pending = 0;
-}
-
 // X <- X L^{-T} for the lower Cholesky factor L stored in G (ld = r + 1):
 // row i solves y L^T = x, i.e. L y^T = x^T (forward substitution).  One
 // warp per row, lanes split the dot products.
@@ -1195,9 +1070,12 @@ __global__ void k_trsm_lt(double* __restrict__ X, int64_t v, int r, const double
 }
 
 __global__ void k_gather_vals(const double* __restrict__ t, const int32_t* __restrict__ idx, int k,
-                              double* __restrict__ vals) {
+                              double* __restrict__ vals, double* __restrict__ aug, int64_t ldaug) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) vals[i] = t[idx[i]];
+  if (i >= k) return;
+  const double x = t[idx[i]];
+  vals[i] = x;
+  if (aug) aug[(int64_t)i * ldaug] = x;
 }
 
 // out = max |G[i][j] - delta_ij| over the leading r x r block (ld = r + 1)
@@ -1384,7 +1262,7 @@ size_t cg_smem_bytes(int r) {
 bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
 
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                            double tol, cudaStream_t s) {
+                            double tol, double* x0, cudaStream_t s) {
   const size_t smem = cg_smem_bytes(r);
   cudaError_t e = cudaFuncSetAttribute(k_cg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -1401,7 +1279,7 @@ cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_cg_solve, G, r, w_out, flag, resid2, tol);
+  return cudaLaunchKernelEx(&cfg, k_cg_solve, G, r, w_out, flag, resid2, tol, x0);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
@@ -1431,9 +1309,11 @@ cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W
   return cudaGetLastError();
 }
 
-cudaError_t launch_resid(const double* U, int r, const int32_t* idx, int k, const double* vals,
-                         const double* w, double* resid, double* sums, cudaStream_t s) {
-  k_resid<<<(unsigned)((k * 32 + 255) / 256), 256, 0, s>>>(U, r, idx, k, vals, w, resid, sums);
+cudaError_t launch_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
+                         const double* vals, const double* w, double* resid, double* sums,
+                         cudaStream_t s) {
+  k_resid<<<(unsigned)((k * 32 + 255) / 256), 256, 0, s>>>(U, ldu, r, idx, k, vals, w, resid,
+                                                          sums);
   return cudaGetLastError();
 }
 
@@ -1446,11 +1326,14 @@ cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, doub
 }
 
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
-                            const double* wn, const double* ug, int k, const double* vals,
+                            const double* wn, const double* ug, int64_t ldu, int k,
+                            const double* vals,
                             const double* resid, const double* sums, double* g, cudaStream_t s) {
   (void)H;
   (void)wn;
-  k_h_g<<<(unsigned)((r + 31) / 32), 256, 0, s>>>(hw, r, st, ug, k, vals, resid, sums, g, g + r);
+  double* gpart = g + r + 1;  // kHgSplit x r scratch after g[0..r]
+  k_h_g_part<<<dim3((unsigned)((r + 31) / 32), kHgSplit), 256, 0, s>>>(r, st, ug, ldu, k, resid, gpart);
+  k_h_g_fin<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(hw, r, st, k, vals, resid, sums, gpart, g);
   return cudaGetLastError();
 }
 
@@ -1465,18 +1348,24 @@ cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm_rm(const double* A, int64_t lda, const int32_t* idx, int64_t rows, int r,
-                           const double* B, double* C, cudaStream_t s) {
-  const int64_t bx = (rows + kMT - 1) / kMT;
-  k_gemm_rm<<<dim3((unsigned)bx, (unsigned)((r + kMT - 1) / kMT)), 256, 0, s>>>(A, lda, idx, rows,
-                                                                                   r, B, C);
+cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
+                                const int32_t* d_idx, const double* d_val, const double* cmat,
+                                const GrouseState* st, int dense, cudaStream_t s) {
+  k_sparse_terms<<<kDeferCap, 256, 0, s>>>(out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st,
+                                           dense);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sparse_terms(double* out, int r, const int32_t* rows_sorted, int k,
-                                const int32_t* d_idx, const double* d_val, const double* cmat,
-                                const GrouseState* st, int dense, cudaStream_t s) {
-  k_sparse_terms<<<kDeferCap, 256, 0, s>>>(out, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
+cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
+                                cudaStream_t s) {
+  const int64_t n = (int64_t)k * r;
+  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
+                                   double* aug, int64_t ldaug, cudaStream_t s) {
+  k_gather_vals<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(t, idx, k, vals, aug, ldaug);
   return cudaGetLastError();
 }
 
@@ -1513,24 +1402,6 @@ cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_pending_st(const double* U, int r, const int32_t* idx, int k,
-                                     const GrouseState* st, const double* pred, const double* d,
-                                     const double* wn, double* out, cudaStream_t s) {
-  const int64_t total = (int64_t)k * r;
-  k_gather_pending_st<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, r, idx, k, st, pred, d,
-                                                                      wn, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pred_apply_st(double* U, int64_t v, int r, const double* w, double* pred,
-                                 double* sums, const GrouseState* st, const double* d,
-                                 const double* wn, const int32_t* flag, cudaStream_t s) {
-  int64_t blocks = (v + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_pred_apply_st<<<(unsigned)blocks, 256, 0, s>>>(U, v, r, w, pred, sums, st, d, wn, flag);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
                                 cudaStream_t s) {
   const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
@@ -1541,34 +1412,10 @@ cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_grouse_post(GrouseState* st, const double* sums, const int32_t* flag,
-                               double step, int64_t step_index, const int32_t* idx, int k,
-                               const double* resid, const double* w, int r, double* d,
-                               int32_t* pidx, double* wn, int32_t* final_slot, cudaStream_t s) {
-  k_grouse_post<<<1, 1024, 0, s>>>(st, sums, flag, step, step_index, idx, k, resid, w, r, d, pidx,
-                                   wn, final_slot);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_grouse_flush(double* U, int64_t v, int r, const double* pred, const double* wn,
-                                GrouseState* st, double* d, const int32_t* pidx, int k,
-                                cudaStream_t s) {
-  const int64_t total = v * r;
-  k_grouse_flush_update<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(U, v, r, pred, wn, st, d);
-  k_grouse_flush_done<<<1, 1024, 0, s>>>(st, d, pidx, k);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s) {
   const int wpb = 4;
   k_trsm_lt<<<(unsigned)((v + wpb - 1) / wpb), 32 * wpb, (size_t)wpb * r * sizeof(double), s>>>(
       X, v, r, L);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_vals(const double* t, const int32_t* idx, int k, double* vals,
-                               cudaStream_t s) {
-  k_gather_vals<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(t, idx, k, vals);
   return cudaGetLastError();
 }
 
