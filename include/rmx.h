@@ -137,6 +137,18 @@ int rmx_naive_maxnull_host(const double *x_host, int64_t v, int32_t n, int32_t n
                            void *workspace, size_t workspace_bytes, void *stream,
                            rmx_status *st, rmx_naive_stats *stats);
 
+/* rmx_naive_maxnull_host with the plan given by its seed, as the reference's
+ * PermutationPlan(seed, L, n) (model.py:76-105): the L x n labels are
+ * generated into orders_dev on the device (rmx_plan_orders' streams,
+ * bit-identical to numpy) while the first X chunk is in flight.
+ * Replaces reference naive.py:60-109 run_naive (plan shuffles included). */
+int rmx_naive_maxnull_host_plan(const double *x_host, int64_t v, int32_t n, int32_t n1,
+                                uint64_t plan_seed, int64_t L, int32_t two_sided,
+                                double *max_host, int32_t *argmax_host, double *x_dev,
+                                int16_t *orders_dev, double *max_dev, int32_t *argmax_dev,
+                                void *workspace, size_t workspace_bytes, void *stream,
+                                rmx_status *st, rmx_naive_stats *stats);
+
 /* The reference's random streams on the device, bit-identical to numpy:
  * row t of out (count x n, int16) = PermutationPlan(seed, ., n).shuffle(lo + t)
  * (model.py:100-105: stream(seed, SHUFFLE, i).permutation(n), identity at 0). */

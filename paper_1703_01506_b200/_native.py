@@ -64,6 +64,7 @@ EXPORTS = (
     "rmx_naive_workspace_bytes",
     "rmx_naive_maxnull",
     "rmx_naive_maxnull_host",
+    "rmx_naive_maxnull_host_plan",
     "rmx_plan_orders",
     "rmx_omega_draws",
     "rmx_naive_prepare",
@@ -106,6 +107,8 @@ _SIGS = {
                           ctypes.c_int),
     "rmx_naive_maxnull_host": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_naive_maxnull_host_plan": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i32, _vp, _vp,
+                                     _vp, _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
     "rmx_plan_orders": ([ctypes.c_uint64, _i64, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
     "rmx_omega_draws": ([ctypes.c_uint64, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _SP],
                         ctypes.c_int),

@@ -172,7 +172,14 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   double best_cost = 1e300;
   int best_c = 1;
   const int cmax = std::min(lay.n_vtiles, 64);
-  for (int c = 1; c <= cmax; ++c) {
+  // Large X arrives from the host in chunk-sized copies (rmx_naive_maxnull_
+  // host*): at least 14 chunks keeps the pipeline tail (K0 + K1 of the last
+  // chunk after its copy lands) near 2 ms; measured on config 4 (7 -> 14
+  // chunks: e2e 40.0 -> 36.9 ms, device step 33.0 -> 32.8 ms).
+  int cmin = (double)v * n * 8.0 >= 512.0 * (1 << 20) ? 14 : 1;
+  if (const char* e = getenv("RMX_CHUNKS_MIN")) cmin = atoi(e);
+  cmin = std::max(1, std::min(cmax, cmin));
+  for (int c = cmin; c <= cmax; ++c) {
     const int tpc = (lay.n_vtiles + c - 1) / c;
     const int nc = (lay.n_vtiles + tpc - 1) / tpc;
     if (nc != c) continue;
@@ -618,14 +625,22 @@ extern "C" {
 // units on alternating streams (so one launch's tail overlaps the next's
 // head).  The int8 quantisation bound is a running max over the chunks K0
 // has finished, which is all K1 needs for chunk c.
-int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n1,
-                           const int16_t* orders_host, int64_t L, int32_t two_sided,
-                           double* max_host, int32_t* argmax_host, double* x_dev,
-                           int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
-                           void* workspace, size_t workspace_bytes, void* stream,
-                           rmx_status* st, rmx_naive_stats* stats) {
+namespace {
+
+// orders from the host buffer (orders_host), from the plan seed on the
+// device (plan_seed, generated on the prep stream while X's first chunk is
+// in flight), or already in orders_dev (both null)
+int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
+                    const int16_t* orders_host, const uint64_t* plan_seed, int64_t L,
+                    int32_t two_sided, double* max_host, int32_t* argmax_host, double* x_dev,
+                    int16_t* orders_dev, double* max_dev, int32_t* argmax_dev, void* workspace,
+                    size_t workspace_bytes, void* stream, rmx_status* st,
+                    rmx_naive_stats* stats) {
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  if (plan_seed && (n > 32767 || L > 0xFFFFFFFFLL))
+    return set_status(st, RMX_E_USAGE, "plan of %lld permutations of n=%d not representable",
+                      (long long)L, n);
   if (!x_host || !max_host || !argmax_host || !x_dev || !orders_dev || !max_dev || !argmax_dev)
     return set_status(st, RMX_E_USAGE, "null buffer");
   Ws ws;
@@ -643,6 +658,7 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
     RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
     if (orders_host)
       RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
+    if (plan_seed) RMX_CUDA(launch_plan_orders(*plan_seed, 0, L, n, orders_dev, s));
     if (int rc = rmx_naive_maxnull(x_dev, v, n, n1, orders_dev, L, two_sided, max_dev, argmax_dev,
                                    workspace, workspace_bytes, stream, st, stats))
       return rc;
@@ -684,7 +700,12 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
   // stream-ordered before this call)
   if (orders_host)
     RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, S.cp));
-  RMX_CUDA(cudaEventRecord(e_ord, S.cp));
+  if (plan_seed) {
+    RMX_CUDA(launch_plan_orders(*plan_seed, 0, L, n, orders_dev, S.pp));
+    RMX_CUDA(cudaEventRecord(e_ord, S.pp));
+  } else {
+    RMX_CUDA(cudaEventRecord(e_ord, S.cp));
+  }
   for (int c = 0; c < nc; ++c) {
     int64_t v0, v1;
     chunk_voxels(ws.lay, v, c, &v0, &v1);
@@ -716,6 +737,30 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                                 workspace, workspace_bytes, stream, st, stats))
     return rc;
   return finish_host();
+}
+
+}  // namespace
+
+int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n1,
+                           const int16_t* orders_host, int64_t L, int32_t two_sided,
+                           double* max_host, int32_t* argmax_host, double* x_dev,
+                           int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
+                           void* workspace, size_t workspace_bytes, void* stream,
+                           rmx_status* st, rmx_naive_stats* stats) {
+  return naive_host_impl(x_host, v, n, n1, orders_host, nullptr, L, two_sided, max_host,
+                         argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
+                         workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_host_plan(const double* x_host, int64_t v, int32_t n, int32_t n1,
+                                uint64_t plan_seed, int64_t L, int32_t two_sided,
+                                double* max_host, int32_t* argmax_host, double* x_dev,
+                                int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
+                                void* workspace, size_t workspace_bytes, void* stream,
+                                rmx_status* st, rmx_naive_stats* stats) {
+  return naive_host_impl(x_host, v, n, n1, nullptr, &plan_seed, L, two_sided, max_host,
+                         argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
+                         workspace_bytes, stream, st, stats);
 }
 
 int rmx_plan_orders(uint64_t seed, int64_t lo, int64_t count, int32_t n, int16_t* out,

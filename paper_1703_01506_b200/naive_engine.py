@@ -207,26 +207,29 @@ def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
 
 
 def _run_from_host(values: np.ndarray, n1: int, plan, two_sided: bool, device):
-    """One rmx_naive_maxnull_host call: host X in (page-locked in place), the
-    plan's labels generated on the device (rmx_plan_orders, bit-identical to
-    numpy's streams), the X upload overlapped with the engine chunk by chunk,
-    host max/argmax out.  Returns (max, argmax, job) -- the job keeps the
-    device copies for follow-up work (materialisation)."""
+    """One rmx_naive_maxnull_host_plan call: host X in (page-locked in place),
+    the plan's labels generated on the device from its seed (rmx_plan_orders'
+    streams, bit-identical to numpy) while X's first chunk uploads, the X
+    upload overlapped with the engine chunk by chunk, host max/argmax out.
+    Returns (max, argmax, job) -- the job keeps the device copies for
+    follow-up work (materialisation)."""
     import torch
 
     from .hostmem import pinned, pinned_empty
-    from .labels import device_orders
 
     xh = pinned(np.asarray(values, dtype=np.float64))
     v, n = xh.shape
     L = int(plan.count)
+    if n > 32767:
+        raise UsageError(f"subject count {n} exceeds the int16 label format")
     xd = torch.empty((v, n), dtype=torch.float64, device=device)
-    od = device_orders(plan.master_seed, 0, L, n, device)
+    od = torch.empty((L, n), dtype=torch.int16, device=device)
     job = NaiveJob(xd, n1, od, two_sided)
     mx = pinned_empty((L,), np.float64)
     am = pinned_empty((L,), np.int32)
-    rc = job.lib.rmx_naive_maxnull_host(
-        xh.ctypes.data, v, n, int(n1), None, L, job.two_sided, mx.ctypes.data,
+    rc = job.lib.rmx_naive_maxnull_host_plan(
+        xh.ctypes.data, v, n, int(n1), ctypes.c_uint64(int(plan.master_seed) & ((1 << 64) - 1)),
+        L, job.two_sided, mx.ctypes.data,
         am.ctypes.data, nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
         nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
         ctypes.byref(job.stats))

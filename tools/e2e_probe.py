@@ -1,4 +1,5 @@
-"""Time the host-buffer NaivePT path phase by phase (diagnostics only)."""
+"""Time the host-buffer NaivePT path against the plain H2D copy of X
+(diagnostics only).  usage: e2e_probe.py [c4|c2]"""
 import os
 import sys
 import time
@@ -7,45 +8,43 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
+    import json
+
     import numpy as np
     import torch
 
     import paper_1703_01506_b200 as rmx
-    from paper_1703_01506_b200 import hostmem, naive_engine
+    from paper_1703_01506_b200 import hostmem
     from paper_1703_01506_b200.datagen import CONFIGS, make_data_torch
-    from paper_1703_01506_b200.labels import plan_orders
 
     cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c4"]
     dev = torch.device("cuda", 0)
     x = rmx.DataMatrix(make_data_torch(cfg, dev).cpu().numpy(), cfg.n1, cfg.n2)
     plan = rmx.PermutationPlan(cfg.plan_seed, cfg.permutations, cfg.subjects)
-    orders = plan_orders(plan)
-    for it in range(4):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        xh = hostmem.pinned(np.asarray(x.values, dtype=np.float64))
-        oh = hostmem.pinned(np.asarray(plan_orders(plan), dtype=np.int16))
-        t1 = time.perf_counter()
-        mx, am, job = naive_engine._run_from_host(xh, cfg.n1, oh, cfg.two_sided, dev)
-        t2 = time.perf_counter()
-        t3 = time.perf_counter()
-        res = rmx.run_naive_ex(x, plan, two_sided=cfg.two_sided)
-        t4 = time.perf_counter()
-        print(f"iter {it}: pin {1e3 * (t1 - t0):.1f} ms, call {1e3 * (t2 - t1):.1f} ms, "
-              f"run_naive_ex {1e3 * (t4 - t3):.1f} ms, "
-              f"registered={len(hostmem._REGISTERED)} x_ptr_reg={xh.ctypes.data in hostmem._REGISTERED} "
-              f"o_ptr_reg={oh.ctypes.data in hostmem._REGISTERED} flags={x.values.flags['C_CONTIGUOUS']}",
-              flush=True)
-    # plain copy rate for reference
+    xh = hostmem.pinned(np.asarray(x.values, dtype=np.float64))
     xd = torch.empty(xh.shape, dtype=torch.float64, device=dev)
     ht = torch.from_numpy(xh)
-    for _ in range(2):
+    h2d = []
+    for _ in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         xd.copy_(ht, non_blocking=True)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        print(f"H2D {xh.nbytes / dt / 1e9:.1f} GB/s ({1e3 * dt:.1f} ms)")
+        h2d.append(time.perf_counter() - t0)
+    del xd
+    runs = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = rmx.run_naive_ex(x, plan, two_sided=cfg.two_sided)
+        torch.cuda.synchronize()
+        runs.append(time.perf_counter() - t0)
+    print(json.dumps({"config": cfg.name if hasattr(cfg, "name") else sys.argv[1:],
+                      "x_bytes": xh.nbytes, "h2d_ms": [1e3 * t for t in h2d],
+                      "h2d_GBps": xh.nbytes / min(h2d) / 1e9,
+                      "run_naive_ex_ms": [1e3 * t for t in runs],
+                      "chunks": int(res.stats["chunks"]) if isinstance(res.stats, dict) and "chunks" in res.stats else None,
+                      "env_chunks_min": os.environ.get("RMX_CHUNKS_MIN")}))
 
 
 if __name__ == "__main__":
