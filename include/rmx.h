@@ -149,6 +149,26 @@ int rmx_naive_maxnull_host_plan(const double *x_host, int64_t v, int32_t n, int3
                                 void *workspace, size_t workspace_bytes, void *stream,
                                 rmx_status *st, rmx_naive_stats *stats);
 
+/* rmx_naive_maxnull_host / _host_plan with X given as float32 on the host
+ * (v x n row-major; the BASELINE.json configs' data type): half the upload
+ * bytes.  Each chunk lands in x32_dev (v x n fp32 device buffer, 16-byte
+ * aligned) and is upcast into x_dev (v x n fp64) before K0 sees it, so the
+ * results are those of rmx_naive_maxnull_host on the float64 upcast -- the
+ * matrix the reference's DataMatrix holds (model.py:21-24, np.float64).
+ * Replaces reference naive.py:60-109 run_naive end to end. */
+int rmx_naive_maxnull_host_f32(const float *x_host, int64_t v, int32_t n, int32_t n1,
+                               const int16_t *orders_host, int64_t L, int32_t two_sided,
+                               double *max_host, int32_t *argmax_host, float *x32_dev,
+                               double *x_dev, int16_t *orders_dev, double *max_dev,
+                               int32_t *argmax_dev, void *workspace, size_t workspace_bytes,
+                               void *stream, rmx_status *st, rmx_naive_stats *stats);
+int rmx_naive_maxnull_host_plan_f32(const float *x_host, int64_t v, int32_t n, int32_t n1,
+                                    uint64_t plan_seed, int64_t L, int32_t two_sided,
+                                    double *max_host, int32_t *argmax_host, float *x32_dev,
+                                    double *x_dev, int16_t *orders_dev, double *max_dev,
+                                    int32_t *argmax_dev, void *workspace, size_t workspace_bytes,
+                                    void *stream, rmx_status *st, rmx_naive_stats *stats);
+
 /* The reference's random streams on the device, bit-identical to numpy:
  * row t of out (count x n, int16) = PermutationPlan(seed, ., n).shuffle(lo + t)
  * (model.py:100-105: stream(seed, SHUFFLE, i).permutation(n), identity at 0). */
@@ -207,6 +227,22 @@ int rmx_lsq_solve(const double *u, int64_t ldu, int32_t r, const int32_t *idx, i
                   const double *vals, int64_t B, double *w_out, int32_t *flag_out,
                   double *norms_out, void *workspace, size_t workspace_bytes, void *stream,
                   rmx_status *st);
+
+/* rmx_lsq_solve with the Gram on the tensor cores (v = rows of U): G~ =
+ * [U_Omega | vals]^T [U_Omega | vals] from fp16 hi/lo planes (tcgen05,
+ * fp32-accurate), Cholesky of G~ in fp64, then two steps of iterative
+ * refinement with the fp64 residual U_Omega^T (vals - U_Omega w): the result
+ * is the fp64 normal-equations solution (relative difference ~1e-12 at the
+ * well-conditioned restrictions of random Omega).  Systems whose factor is
+ * singular (flag_out, as rmx_lsq_solve) or whose refinement has not settled
+ * are re-solved with the fp64 Gram.  stats (optional, 2 ints): [tensor path
+ * used, systems re-solved in fp64].  Falls back to rmx_lsq_solve for shapes
+ * the tensor path does not take (r + 1 > 512) or when RMX_GRAM_FP64 is set.
+ * Replaces reference lrmc.py:127-149 solve_block (batched). */
+int rmx_lsq_solve_tc(const double *u, int64_t ldu, int64_t v, int32_t r, const int32_t *idx,
+                     int32_t k, const double *vals, int64_t B, double *w_out, int32_t *flag_out,
+                     void *workspace, size_t workspace_bytes, int32_t *stats, void *stream,
+                     rmx_status *st);
 
 /* Completion + residual + max (rapid.py:198-205): for each of B columns,
  *   max_out[b] = max_j op(W[b] . U[j] + sigma * z(perm_base + b, j)) + mu,

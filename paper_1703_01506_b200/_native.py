@@ -65,6 +65,8 @@ EXPORTS = (
     "rmx_naive_maxnull",
     "rmx_naive_maxnull_host",
     "rmx_naive_maxnull_host_plan",
+    "rmx_naive_maxnull_host_f32",
+    "rmx_naive_maxnull_host_plan_f32",
     "rmx_plan_orders",
     "rmx_omega_draws",
     "rmx_naive_prepare",
@@ -76,6 +78,7 @@ EXPORTS = (
     "rmx_rapid_stats",
     "rmx_lsq_workspace_bytes",
     "rmx_lsq_solve",
+    "rmx_lsq_solve_tc",
     "rmx_complete_max",
     "rmx_to_f32",
     "rmx_row_max",
@@ -109,6 +112,11 @@ _SIGS = {
                                 _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
     "rmx_naive_maxnull_host_plan": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i32, _vp, _vp,
                                      _vp, _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_naive_maxnull_host_f32": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_naive_maxnull_host_plan_f32": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i32, _vp,
+                                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
+                                        ctypes.c_int),
     "rmx_plan_orders": ([ctypes.c_uint64, _i64, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
     "rmx_omega_draws": ([ctypes.c_uint64, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _SP],
                         ctypes.c_int),
@@ -123,6 +131,8 @@ _SIGS = {
                         ctypes.c_int),
     "rmx_rapid_stats": ([_vp, _i64, _i32, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
     "rmx_lsq_workspace_bytes": ([_i32, _i64], _sz),
+    "rmx_lsq_solve_tc": ([_vp, _i64, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp,
+                          _SP], ctypes.c_int),
     "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],
                       ctypes.c_int),
     "rmx_complete_max": ([_vp, _i64, _i32, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double,

@@ -9,11 +9,13 @@
 //   k_exact_rows    exhaustive exact statistic (materialised T / fallback)
 //   k_exact_reduce  per-permutation max/argmax of k_exact_rows' partials
 //   k_pairs         exact statistic at explicit (perm, voxel) pairs
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
 #include "np_exact.cuh"
 #include "rmx_internal.cuh"
+#include "sm100.cuh"
 
 namespace rmx {
 
@@ -59,12 +61,116 @@ __device__ __forceinline__ void note_degenerate(NaiveCounters* c, int64_t perm, 
 // constant across all subjects get z = 0 (tensor-core t~ = 0) and, if numpy's
 // rounding makes their exact statistic non-zero, are listed for
 // k_const_reduce.
+// One voxel row j held by one warp: R > 0: xr[r] = x[j, lane + 32 r] (0 past
+// n); R = 0: re-read from `row`.  err_max: running int8 quantisation bound.
+template <int R>
+__device__ __forceinline__ void prep_row(const PrepArgs& a, int64_t j, int lane,
+                                         const double (&xr)[R > 0 ? R : 1], const double* row,
+                                         double& err_max) {
+  const int64_t plane = a.v * (int64_t)a.kpad;
+  // f(k, x) over this lane's subjects k < n
+  auto each = [&](auto&& f) {
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = lane + 32 * r;
+        if (k < a.n) f(k, xr[r]);
+      }
+    } else {
+      for (int k = lane; k < a.n; k += 32) f(k, row[k]);
+    }
+  };
+  // f(k, x) over this lane's padded columns k < kpad (x = 0 past n); kpad <= 32 R
+  auto each_pad = [&](auto&& f) {
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k = lane + 32 * r;
+        if (k < a.kpad) f(k, xr[r]);
+      }
+    } else {
+      for (int k = lane; k < a.kpad; k += 32) f(k, k < a.n ? row[k] : 0.0);
+    }
+  };
+  double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+  each([&](int, double x) {
+    s += x;
+    mn = fmin(mn, x);
+    mx = fmax(mx, x);
+  });
+  s = warp_sum_d(s);
+  mn = warp_min_d(mn);
+  mx = warp_max_d(mx);
+  const double mean = s / a.n;
+  double ss = 0.0;
+  each([&](int, double x) {
+    const double d = x - mean;
+    ss += d * d;
+  });
+  ss = warp_sum_d(ss);
+  const bool constant = (mn == mx);
+  const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
+  if (a.planes8) {
+    // int8 path: zq = rint(z * scale) in [-32512, 32512], zq = 255 h + l with
+    // h, l in [-127, 127]; row j of planes8 = [h_0 .. h_kpad-1 | l_0 .. l_kpad-1]
+    double zmax = 0.0;
+    each([&](int, double x) { zmax = fmax(zmax, fabs((x - mean) * inv)); });
+    zmax = warp_max_d(zmax);
+    const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
+    const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
+    int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
+    double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
+    each_pad([&](int k, double x) {
+      int zq = 0;  // padded subjects and constant voxels: 0
+      if (k < a.n && !constant) {
+        const double z = (x - mean) * inv;
+        zq = min(32512, max(-32512, (int)rint(z * scale)));
+        err += fabs(z - (double)zq * (double)inv_f);
+      }
+      const int h = zq >= 0 ? (zq + 127) / 255 : -((127 - zq) / 255);  // round(zq / 255)
+      p8[k] = (int8_t)h;
+      p8[a.kpad + k] = (int8_t)(zq - 255 * h);
+    });
+    err = warp_sum_d(err);
+    err_max = fmax(err_max, err);
+    if (lane == 0) a.inv_scale[j] = inv_f;
+  } else {
+    __half* zh = a.planes + j * a.kpad;
+    each_pad([&](int k, double x) {
+      const double z = (k < a.n && !constant) ? (x - mean) * inv : 0.0;
+      const __half h_z = __double2half(z);
+      zh[k] = h_z;
+      zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
+      if (!a.zplanes_only) {
+        const double q = z * z;
+        const __half h_q = __double2half(q);
+        zh[plane + k] = h_q;
+        zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
+      }
+    });
+  }
+  if (constant && lane == 0) {
+    const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
+    if (w.t != 0.0 || w.degenerate) {
+      unsigned slot = atomicAdd(&a.counters->cvox_count, 1u);
+      a.cvox[slot] = (int32_t)j;
+    }
+  }
+}
+
+__device__ __forceinline__ void prep_publish_err(const PrepArgs& a, int lane, double err_max) {
+  if (a.planes8 && lane == 0 && err_max > 0.0)
+    // rounded up; non-negative floats order like their bit patterns
+    atomicMax(&a.counters->emax_bits, __float_as_uint((float)(err_max * (1.0 + 1e-6)) + 1e-30f));
+}
+
+// K0, generic: one warp per voxel row, the row read straight from global
+// memory into registers (R > 0, n <= 32 R) or re-read (R = 0).
 template <int R>
 __global__ void __launch_bounds__(256, 2) k_prep(PrepArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  const int64_t plane = a.v * (int64_t)a.kpad;
-  double err_max = 0.0;  // int8: max over this warp's voxels of the quantisation bound
+  double err_max = 0.0;
   const int64_t jend = a.v_end > 0 ? a.v_end : a.v;
   for (int64_t j = a.v_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
        j < jend; j += warps) {
@@ -77,98 +183,172 @@ __global__ void __launch_bounds__(256, 2) k_prep(PrepArgs a) {
         xr[r] = k < a.n ? __ldg(row + k) : 0.0;
       }
     }
-    // f(k, x) over this lane's subjects k < n
-    auto each = [&](auto&& f) {
-      if constexpr (R > 0) {
+    prep_row<R>(a, j, lane, xr, row, err_max);
+  }
+  prep_publish_err(a, lane, err_max);
+}
+
+// K0, streamed (even n): X rows are contiguous, so each CTA pulls tiles of
+// kPrepRows consecutive rows (kPrepRows * n * 8 bytes) with 1-D bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a kPrepStages ring; warp w
+// standardises row w of the tile from shared memory.  The loads of the next
+// kPrepStages - 1 tiles are in flight while a tile is processed, independent
+// of the register budget that limits the generic kernel to one row per warp.
+constexpr int kPrepRows = 8;  // = warps per CTA
+constexpr int kPrepStages = 4;
+
+// One voxel row from shared memory, lane-contiguous mapping: lane owns the
+// subjects k = 4 lane + 128 g + e (g < G, e < 4), so the int8 digits (and
+// fp16 halves) of four consecutive subjects leave as one packed store.  Same
+// arithmetic as prep_row (explicit fma where an unfused product was not
+// needed); the quantisation bound is measured on the values actually stored.
+template <int G>
+__device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane,
+                                          const double* srow, double& err_max) {
+  double d[G][4];
+  double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int k = lane + 32 * r;
-          if (k < a.n) f(k, xr[r]);
-        }
-      } else {
-        for (int k = lane; k < a.n; k += 32) f(k, row[k]);
-      }
-    };
-    // f(k, x) over this lane's padded columns k < kpad (x = 0 past n); kpad <= 32 R
-    auto each_pad = [&](auto&& f) {
-      if constexpr (R > 0) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int k = lane + 32 * r;
-          if (k < a.kpad) f(k, xr[r]);
-        }
-      } else {
-        for (int k = lane; k < a.kpad; k += 32) f(k, k < a.n ? row[k] : 0.0);
-      }
-    };
-    double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
-    each([&](int, double x) {
-      s += x;
-      mn = fmin(mn, x);
-      mx = fmax(mx, x);
-    });
-    s = warp_sum_d(s);
-    mn = warp_min_d(mn);
-    mx = warp_max_d(mx);
-    const double mean = s / a.n;
-    double ss = 0.0;
-    each([&](int, double x) {
-      const double d = x - mean;
-      ss += d * d;
-    });
-    ss = warp_sum_d(ss);
-    const bool constant = (mn == mx);
-    const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
-    if (a.planes8) {
-      // int8 path: zq = rint(z * scale) in [-32512, 32512], zq = 255 h + l with
-      // h, l in [-127, 127]; row j of planes8 = [h_0 .. h_kpad-1 | l_0 .. l_kpad-1]
-      double zmax = 0.0;
-      each([&](int, double x) { zmax = fmax(zmax, fabs((x - mean) * inv)); });
-      zmax = warp_max_d(zmax);
-      const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
-      const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
-      int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
-      double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
-      each_pad([&](int k, double x) {
-        int zq = 0;  // padded subjects and constant voxels: 0
-        if (k < a.n && !constant) {
-          const double z = (x - mean) * inv;
-          zq = min(32512, max(-32512, (int)rint(z * scale)));
-          err += fabs(z - (double)zq * (double)inv_f);
-        }
-        const int h = zq >= 0 ? (zq + 127) / 255 : -((127 - zq) / 255);  // round(zq / 255)
-        p8[k] = (int8_t)h;
-        p8[a.kpad + k] = (int8_t)(zq - 255 * h);
-      });
-      err = warp_sum_d(err);
-      err_max = fmax(err_max, err);
-      if (lane == 0) a.inv_scale[j] = inv_f;
+  for (int g = 0; g < G; ++g) {
+    const int k0 = 4 * lane + 128 * g;
+    if (k0 < a.n) {  // n even and k0 % 4 == 0: pairs are whole
+      const double2 p0 = *reinterpret_cast<const double2*>(srow + k0);
+      const double2 p1 = k0 + 2 < a.n ? *reinterpret_cast<const double2*>(srow + k0 + 2)
+                                      : make_double2(0.0, 0.0);
+      d[g][0] = p0.x;
+      d[g][1] = p0.y;
+      d[g][2] = p1.x;
+      d[g][3] = p1.y;
     } else {
-      __half* zh = a.planes + j * a.kpad;
-      each_pad([&](int k, double x) {
-        const double z = (k < a.n && !constant) ? (x - mean) * inv : 0.0;
-        const __half h_z = __double2half(z);
-        zh[k] = h_z;
-        zh[2 * plane + k] = __double2half(z - (double)__half2float(h_z));
-        if (!a.zplanes_only) {
-          const double q = z * z;
-          const __half h_q = __double2half(q);
-          zh[plane + k] = h_q;
-          zh[3 * plane + k] = __double2half(q - (double)__half2float(h_q));
-        }
-      });
+#pragma unroll
+      for (int e = 0; e < 4; ++e) d[g][e] = 0.0;
     }
-    if (constant && lane == 0) {
-      const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
-      if (w.t != 0.0 || w.degenerate) {
-        unsigned slot = atomicAdd(&a.counters->cvox_count, 1u);
-        a.cvox[slot] = (int32_t)j;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (k0 + e < a.n) {
+        s += d[g][e];
+        mn = fmin(mn, d[g][e]);
+        mx = fmax(mx, d[g][e]);
       }
     }
   }
-  if (a.planes8 && lane == 0 && err_max > 0.0)
-    // rounded up; non-negative floats order like their bit patterns
-    atomicMax(&a.counters->emax_bits, __float_as_uint((float)(err_max * (1.0 + 1e-6)) + 1e-30f));
+  s = warp_sum_d(s);
+  mn = warp_min_d(mn);
+  mx = warp_max_d(mx);
+  const double mean = s / a.n;
+  const bool constant = (mn == mx);
+  double ss = 0.0;
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool in = 4 * lane + 128 * g + e < a.n;
+      d[g][e] = (in && !constant) ? d[g][e] - mean : 0.0;  // centred; 0 past n
+      ss = fma(d[g][e], d[g][e], ss);
+    }
+  ss = warp_sum_d(ss);
+  const double inv = constant ? 0.0 : 1.0 / sqrt(ss / (a.n - 1));
+  if (a.planes8) {
+    double dmax = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dmax = fmax(dmax, fabs(d[g][e]));
+    const double zmax = warp_max_d(dmax) * inv;
+    const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
+    const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
+    const double c = inv * scale, inv_d = (double)inv_f;
+    int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
+    double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int k0 = 4 * lane + 128 * g;
+      if (k0 >= a.kpad) continue;  // kpad % 16 == 0: groups are whole
+      uint32_t hw = 0u, lw = 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int zq = min(32512, max(-32512, __double2int_rn(d[g][e] * c)));
+        err += fabs(fma(-(double)zq, inv_d, d[g][e] * inv));
+        const int h = __float2int_rn((float)zq * (1.0f / 255.0f));  // |zq/255 - h| <= 0.498
+        hw |= (uint32_t)(uint8_t)(int8_t)h << (8 * e);
+        lw |= (uint32_t)(uint8_t)(int8_t)(zq - 255 * h) << (8 * e);
+      }
+      *reinterpret_cast<uint32_t*>(p8 + k0) = hw;
+      *reinterpret_cast<uint32_t*>(p8 + a.kpad + k0) = lw;
+    }
+    err = warp_sum_d(err);
+    err_max = fmax(err_max, err);
+    if (lane == 0) a.inv_scale[j] = inv_f;
+  } else {
+    const int64_t plane = a.v * (int64_t)a.kpad;
+    __half* zh = a.planes + j * a.kpad;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int k0 = 4 * lane + 128 * g;
+      if (k0 >= a.kpad) continue;
+      __half hz[4], lz[4], hq[4], lq[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double z = d[g][e] * inv;
+        hz[e] = __double2half(z);
+        lz[e] = __double2half(z - (double)__half2float(hz[e]));
+        const double q = z * z;
+        hq[e] = __double2half(q);
+        lq[e] = __double2half(q - (double)__half2float(hq[e]));
+      }
+      *reinterpret_cast<uint2*>(zh + k0) = *reinterpret_cast<const uint2*>(hz);
+      *reinterpret_cast<uint2*>(zh + 2 * plane + k0) = *reinterpret_cast<const uint2*>(lz);
+      if (!a.zplanes_only) {
+        *reinterpret_cast<uint2*>(zh + plane + k0) = *reinterpret_cast<const uint2*>(hq);
+        *reinterpret_cast<uint2*>(zh + 3 * plane + k0) = *reinterpret_cast<const uint2*>(lq);
+      }
+    }
+  }
+  if (constant && lane == 0) {
+    const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
+    if (w.t != 0.0 || w.degenerate) {
+      unsigned slot = atomicAdd(&a.counters->cvox_count, 1u);
+      a.cvox[slot] = (int32_t)j;
+    }
+  }
+}
+
+template <int R>  // R = 4-subject groups per lane (kpad <= 128 R)
+__global__ void __launch_bounds__(32 * kPrepRows, 2) k_prep_bulk(PrepArgs a) {
+  extern __shared__ __align__(128) uint8_t psm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(psm);
+  double* tiles = reinterpret_cast<double*>(psm + 128);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t jend = a.v_end > 0 ? a.v_end : a.v;
+  const int64_t ntiles = (jend - a.v_begin + kPrepRows - 1) / kPrepRows;
+  const int64_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t tile_elems = (int64_t)kPrepRows * a.n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPrepStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t i) {  // thread 0: tile blockIdx.x + i * gridDim.x -> stage i % S
+    const int64_t r0 = a.v_begin + (blockIdx.x + i * gridDim.x) * kPrepRows;
+    const int64_t nr = min((int64_t)kPrepRows, jend - r0);
+    const uint32_t bytes = (uint32_t)(nr * a.n * 8);
+    uint64_t* bar = &full[i % kPrepStages];
+    mbar_expect_tx(bar, bytes);
+    bulk_load(tiles + (i % kPrepStages) * tile_elems, a.x + r0 * a.n, bytes, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < kPrepStages && i < mine; ++i) issue(i);
+  double err_max = 0.0;
+  for (int64_t i = 0; i < mine; ++i) {
+    mbar_wait(&full[i % kPrepStages], (uint32_t)((i / kPrepStages) & 1));
+    const int64_t j = a.v_begin + (blockIdx.x + i * gridDim.x) * kPrepRows + warp;
+    if (j < jend) {
+      const double* srow = tiles + (i % kPrepStages) * tile_elems + (int64_t)warp * a.n;
+      prep_row4<R>(a, j, lane, srow, err_max);
+    }
+    __syncthreads();  // every warp is done with stage i % S
+    if (threadIdx.x == 0 && i + kPrepStages < mine) issue(i + kPrepStages);
+  }
+  prep_publish_err(a, lane, err_max);
 }
 
 __global__ void k_const_reduce(const double* x, int n, int n1, const int32_t* cvox,
@@ -510,6 +690,23 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   int64_t blocks = (rows + wpb - 1) / wpb;
   if (blocks > 148 * 64) blocks = 148 * 64;
+  // even n (16-byte aligned rows for the bulk copies), n <= 512: streamed
+  if (a.n % 2 == 0 && a.kpad <= 512 && a.kpad % 16 == 0 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
+    const size_t smem = 128 + (size_t)kPrepStages * kPrepRows * a.n * sizeof(double);
+    const int64_t tiles = (rows + kPrepRows - 1) / kPrepRows;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, 2 * 148);
+    auto go = [&](auto kern) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, 32 * kPrepRows, smem, s>>>(a);
+      return cudaGetLastError();
+    };
+    if (a.kpad <= 128) return go(k_prep_bulk<1>);
+    if (a.kpad <= 256) return go(k_prep_bulk<2>);
+    if (a.kpad <= 384) return go(k_prep_bulk<3>);
+    return go(k_prep_bulk<4>);
+  }
   // rows up to 32 R subjects are read once into registers
   if (a.n <= 128) k_prep<4><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);
   else if (a.n <= 256) k_prep<8><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a);

@@ -145,6 +145,70 @@ int rmx_lsq_solve(const double* u, int64_t ldu, int32_t r, const int32_t* idx, i
   return RMX_OK;
 }
 
+int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_t* idx,
+                     int32_t k, const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                     void* workspace, size_t workspace_bytes, int32_t* stats, void* stream,
+                     rmx_status* st) {
+  rclear(st);
+  if (r < 1 || k < r || B < 1 || !vals || !w_out || !idx || v < 1)
+    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!gram_tc_supported(r, k) || getenv("RMX_GRAM_FP64")) {
+    if (stats) stats[0] = stats[1] = 0;
+    return rmx_lsq_solve(u, ldu, r, idx, k, vals, B, w_out, flag_out, nullptr, workspace,
+                         workspace_bytes, stream, st);
+  }
+  const size_t per = gram_bytes(r);
+  int64_t chunk = (int64_t)((workspace_bytes > 256 ? workspace_bytes - 256 : 0) /
+                            (per + 4 * sizeof(double)));
+  if (chunk < 1) return rset(st, RMX_E_USAGE, "lsq workspace too small");
+  chunk = std::min<int64_t>(chunk, B);
+  double* G = static_cast<double*>(workspace);
+  double* nrm = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + chunk * per);
+  DevBuf<__half> planes;
+  DevBuf<double> g;
+  DevBuf<int32_t> flags, nconv;
+  RCUDA(planes.alloc((size_t)2 * v * gram_tc_kpg(r), s));
+  RCUDA(g.alloc((size_t)chunk * r, s));
+  RCUDA(flags.alloc((size_t)B, s));
+  RCUDA(nconv.alloc((size_t)B, s));
+  RCUDA(launch_gram_planes(u, ldu, v, r, planes.p, s));
+  const int sms = device_sm_count();
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t cnt = std::min(chunk, B - b0);
+    const int32_t* ib = idx + b0 * k;
+    const double* vb = vals + b0 * k;
+    double* wb = w_out + b0 * r;
+    RCUDA(launch_gram_tc(planes.p, v, r, ib, k, vb, G, cnt, sms, s));
+    RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
+    // two refinement steps with the fp64 residual (contraction ~ cond * 1e-6 each)
+    for (int it = 0; it < 2; ++it) {
+      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
+      RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
+    }
+  }
+  // systems whose factor was singular or whose refinement has not settled:
+  // the fp64 Gram + Cholesky, one by one (rare: ill-conditioned restrictions)
+  std::vector<int32_t> hf((size_t)B), hn((size_t)B);
+  RCUDA(cudaMemcpyAsync(hf.data(), flags.p, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaMemcpyAsync(hn.data(), nconv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaStreamSynchronize(s));
+  int32_t redo = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    if (hf[b] == 0 && hn[b] == 0) continue;
+    ++redo;
+    RCUDA(launch_gram(u, ldu, r, idx + b * k, k, vals + b * k, G, 1, s));
+    RCUDA(launch_chol_solve(G, r, 1, w_out + b * r, flags.p + b, nrm, s));
+  }
+  if (flag_out) RCUDA(cudaMemcpyAsync(flag_out, flags.p, (size_t)B * 4, cudaMemcpyDeviceToDevice, s));
+  if (stats) {
+    stats[0] = 1;
+    stats[1] = redo;
+  }
+  RCUDA(cudaStreamSynchronize(s));
+  return RMX_OK;
+}
+
 int rmx_complete_max(const float* u32, int64_t v, int32_t r, const float* w32, int64_t B,
                      int64_t perm_base, double sigma, double mu, uint64_t seed, int32_t two_sided,
                      const float* znoise, const double* base, double* max_out, void* stream,

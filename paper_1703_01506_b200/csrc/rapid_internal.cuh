@@ -16,6 +16,24 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 // (t.t - rhs.w, w.w, min L_ii, max L_ii); flag_b = 1 on a non-positive pivot
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s);
+// refinement solve with the factor k_chol_solve left in G: w_b += (L L^T)^-1 rhs_b;
+// nconv_b = 1 when the correction exceeds 1e-7 |w_b|
+cudaError_t launch_chol_resolve(double* G, int r, int64_t B, const double* rhs, double* w_inout,
+                                int32_t* nconv, cudaStream_t s);
+// Tensor-core Gram (gram_tc.cu): G_b ~ [U[idx_b] | vals_b]^T [U[idx_b] | vals_b]
+// (lower triangle, (r+1)^2 each) from fp16 hi/lo planes of U (gram_planes),
+// fp32-accurate; refined to fp64 accuracy by lsq_resid + launch_chol_resolve
+bool gram_tc_supported(int r, int k);
+int gram_tc_kpg(int r);  // plane row pitch (halves)
+cudaError_t launch_gram_planes(const double* U, int64_t ldu, int64_t v, int r, __half* planes,
+                               cudaStream_t s);
+cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t* idx, int k,
+                           const double* vals, double* G, int64_t B, int sm_count,
+                           cudaStream_t s);
+// g_b = U_Omega^T (t - U_Omega w_b) in fp64 (one gather of the rows)
+cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
+                             const double* vals, const double* W, int64_t B, double* g,
+                             cudaStream_t s);
 // GROUSE step state kept on the device, so the update loop runs without a
 // host round trip per update (decisions by k_grouse_post_m).
 struct GrouseState {

@@ -201,9 +201,12 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
                                                    int32_t* flag, double* __restrict__ resid2,
-                                                   const int32_t* gate = nullptr) {
+                                                   const int32_t* gate = nullptr,
+                                                   const double* __restrict__ rhs_ext = nullptr) {
   // gate: run only when *gate != 0 (Cholesky fallback after a cluster-CG
   // solve that did not converge, decided on the device)
+  // rhs_ext (refinement): G already holds the factor L; solve L L^T d =
+  // rhs_ext[b], w_out[b] += d, flag[b] = 1 when |d| > 1e-7 |w| (not converged)
   if (gate && *gate == 0) return;
   __syncthreads();  // every thread has read the gate before it is overwritten
   extern __shared__ double sm[];
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   double* Gb = G + b * (int64_t)ld * ld;
-  if (wid == 0) {
+  if (wid == 0 && !rhs_ext) {
     double m = 0.0;
     for (int i = lane; i < r; i += 32) m = fmax(m, Gb[(int64_t)i * ld + i]);
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r
       D[i * kPS + j] = val;
     }
   };
-  for (int jb = 0; jb < r; jb += kPW) {
+  for (int jb = 0; jb < (rhs_ext ? 0 : r); jb += kPW) {
     const int w = min(kPW, r - jb);
     load_block(jb, w);
     __syncthreads();
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r
     __syncthreads();
   }
   // solve L L^T w = rhs (rhs = G[r, 0:r], the A^T t row), blocked
-  for (int i = tid; i < r; i += NT) y[i] = Gb[(int64_t)r * ld + i];
+  for (int i = tid; i < r; i += NT) y[i] = rhs_ext ? rhs_ext[b * r + i] : Gb[(int64_t)r * ld + i];
   __syncthreads();
   for (int jb = 0; jb < r; jb += kPW) {  // forward: L y = rhs
     const int w = min(kPW, r - jb);
@@ -360,6 +363,23 @@ __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r
       y[i] -= sacc;
     }
     __syncthreads();
+  }
+  if (rhs_ext) {
+    if (tid < 32) {
+      double dd = 0.0, ww = 0.0;
+      for (int i = lane; i < r; i += 32) {
+        const double wn = w_out[b * r + i] + y[i];
+        w_out[b * r + i] = wn;
+        dd += y[i] * y[i];
+        ww += wn * wn;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        dd += __shfl_xor_sync(0xffffffffu, dd, o);
+        ww += __shfl_xor_sync(0xffffffffu, ww, o);
+      }
+      if (lane == 0 && flag) flag[b] = (dd > 1e-14 * ww) ? 1 : 0;
+    }
+    return;
   }
   if (tid < 32) {
     if (w_out)
@@ -1232,6 +1252,16 @@ cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_
     if (e != cudaSuccess) return e;
     k_chol_solve<256><<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, resid2);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_resolve(double* G, int r, int64_t B, const double* rhs, double* w_inout,
+                                int32_t* nconv, cudaStream_t s) {
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_chol_solve<256>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_chol_solve<256><<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs);
   return cudaGetLastError();
 }
 

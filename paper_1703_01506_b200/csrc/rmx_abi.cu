@@ -615,6 +615,34 @@ int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const i
 
 namespace rmx {
 int golden_stride_public(int T) { return golden_stride(T); }
+
+// fp32 host X (x_host32, staged through x32_dev): each chunk is upcast into
+// x_dev on the prep stream before K0 sees it.  Exact: every float32 is a
+// float64, so the engine computes on the same values as from a float64 host
+// matrix holding the upcast (reference model.py:21-24 makes that upcast).
+__global__ void k_upcast(const float* __restrict__ a, int64_t count, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // float4 / double2 path when both sides are 16-byte aligned (chunk offsets
+  // v0 * n need not be)
+  const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t c4 = vec ? count >> 2 : 0;
+  for (int64_t j = i; j < c4; j += stride) {
+    float4 f = reinterpret_cast<const float4*>(a)[j];
+    double2* o = reinterpret_cast<double2*>(out) + 2 * j;
+    o[0] = make_double2(f.x, f.y);
+    o[1] = make_double2(f.z, f.w);
+  }
+  for (int64_t j = 4 * c4 + i; j < count; j += stride) out[j] = a[j];
+}
+
+cudaError_t launch_upcast(const float* a, int64_t count, double* out, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((count / 4 + 255) / 256 + 1, 4 * 148);
+  k_upcast<<<blocks, 256, 0, s>>>(a, count, out);
+  return cudaGetLastError();
+}
+
 }  // namespace rmx
 
 extern "C" {
@@ -629,8 +657,10 @@ namespace {
 
 // orders from the host buffer (orders_host), from the plan seed on the
 // device (plan_seed, generated on the prep stream while X's first chunk is
-// in flight), or already in orders_dev (both null)
-int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
+// in flight), or already in orders_dev (both null).  X from x_host (fp64) or
+// x_host32 (fp32, staged in x32_dev).
+int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
+                    int64_t v, int32_t n, int32_t n1,
                     const int16_t* orders_host, const uint64_t* plan_seed, int64_t L,
                     int32_t two_sided, double* max_host, int32_t* argmax_host, double* x_dev,
                     int16_t* orders_dev, double* max_dev, int32_t* argmax_dev, void* workspace,
@@ -641,8 +671,11 @@ int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
   if (plan_seed && (n > 32767 || L > 0xFFFFFFFFLL))
     return set_status(st, RMX_E_USAGE, "plan of %lld permutations of n=%d not representable",
                       (long long)L, n);
-  if (!x_host || !max_host || !argmax_host || !x_dev || !orders_dev || !max_dev || !argmax_dev)
+  if ((!x_host && !(x_host32 && x32_dev)) || !max_host || !argmax_host || !x_dev ||
+      !orders_dev || !max_dev || !argmax_dev)
     return set_status(st, RMX_E_USAGE, "null buffer");
+  if ((reinterpret_cast<uintptr_t>(x_host32) | reinterpret_cast<uintptr_t>(x32_dev)) & 15)
+    return set_status(st, RMX_E_USAGE, "fp32 X buffers must be 16-byte aligned");
   Ws ws;
   if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -655,7 +688,12 @@ int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
     return RMX_OK;
   };
   if (ws.lay.stages == 0) {  // exhaustive exact path: nothing to overlap
-    RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
+    if (x_host) {
+      RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
+    } else {
+      RMX_CUDA(cudaMemcpyAsync(x32_dev, x_host32, xbytes / 2, cudaMemcpyHostToDevice, s));
+      RMX_CUDA(rmx::launch_upcast(x32_dev, v * n, x_dev, s));
+    }
     if (orders_host)
       RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
     if (plan_seed) RMX_CUDA(launch_plan_orders(*plan_seed, 0, L, n, orders_dev, s));
@@ -709,8 +747,11 @@ int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
   for (int c = 0; c < nc; ++c) {
     int64_t v0, v1;
     chunk_voxels(ws.lay, v, c, &v0, &v1);
-    if (v1 > v0)
+    if (v1 > v0 && x_host)
       RMX_CUDA(cudaMemcpyAsync(x_dev + v0 * n, x_host + v0 * n, (size_t)(v1 - v0) * n * 8,
+                               cudaMemcpyHostToDevice, S.cp));
+    else if (v1 > v0)
+      RMX_CUDA(cudaMemcpyAsync(x32_dev + v0 * n, x_host32 + v0 * n, (size_t)(v1 - v0) * n * 4,
                                cudaMemcpyHostToDevice, S.cp));
     RMX_CUDA(cudaEventRecord(e_rows[c], S.cp));
   }
@@ -720,6 +761,7 @@ int naive_host_impl(const double* x_host, int64_t v, int32_t n, int32_t n1,
     int64_t v0, v1;
     chunk_voxels(ws.lay, v, c, &v0, &v1);
     RMX_CUDA(cudaStreamWaitEvent(S.pp, e_rows[c], 0));
+    if (!x_host) RMX_CUDA(rmx::launch_upcast(x32_dev + v0 * n, (v1 - v0) * n, x_dev + v0 * n, S.pp));
     if (int rc = prep_rows(x_dev, v, n, n1, ws, v0, v1, S.pp, st)) return rc;
     RMX_CUDA(cudaEventRecord(e_prep[c], S.pp));
     cudaStream_t ks = S.k[c & 1];
@@ -747,7 +789,7 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                            int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                            void* workspace, size_t workspace_bytes, void* stream,
                            rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, v, n, n1, orders_host, nullptr, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, orders_host, nullptr, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -758,8 +800,32 @@ int rmx_naive_maxnull_host_plan(const double* x_host, int64_t v, int32_t n, int3
                                 int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                                 void* workspace, size_t workspace_bytes, void* stream,
                                 rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, v, n, n1, nullptr, &plan_seed, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
+                         workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_host_f32(const float* x_host, int64_t v, int32_t n, int32_t n1,
+                               const int16_t* orders_host, int64_t L, int32_t two_sided,
+                               double* max_host, int32_t* argmax_host, float* x32_dev,
+                               double* x_dev, int16_t* orders_dev, double* max_dev,
+                               int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
+                               void* stream, rmx_status* st, rmx_naive_stats* stats) {
+  if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
+  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, orders_host, nullptr, L, two_sided,
+                         max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
+                         workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_host_plan_f32(const float* x_host, int64_t v, int32_t n, int32_t n1,
+                                    uint64_t plan_seed, int64_t L, int32_t two_sided,
+                                    double* max_host, int32_t* argmax_host, float* x32_dev,
+                                    double* x_dev, int16_t* orders_dev, double* max_dev,
+                                    int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
+                                    void* stream, rmx_status* st, rmx_naive_stats* stats) {
+  if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
+  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, L, two_sided,
+                         max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
 

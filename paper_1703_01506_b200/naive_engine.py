@@ -180,6 +180,19 @@ def upload(x_values: np.ndarray, orders: np.ndarray, device):
     return xd, od
 
 
+def data_to_device(x, device):
+    """(v, n) float64 device copy of a DataMatrix, uploaded from its float32
+    source when it keeps one (half the bytes; the upcast is exact)."""
+    import torch
+
+    from .hostmem import to_device
+
+    x = as_data_matrix(x)
+    if x.float32_values is not None:
+        return to_device(x.float32_values, device).to(dtype=torch.float64)
+    return to_device(x.values, device)
+
+
 def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
                  threads: Optional[int] = None,
                  mem_cap_bytes: int = DEFAULT_MEM_CAP_BYTES) -> NaiveResult:
@@ -199,15 +212,16 @@ def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
             )
     resolve_threads(threads)
     device = cuda_device()
-    mx, am, job = _run_from_host(x.values, x.n1, plan, two_sided, device)
+    mx, am, job = _run_from_host(x, plan, two_sided, device)
     T = None
     if materialize:
         T = tstat_exact_device(job.x, x.n1, job.orders).t().contiguous().cpu().numpy()
     return NaiveResult(mx, am.astype(np.int64), job.stats.as_dict(), T)
 
 
-def _run_from_host(values: np.ndarray, n1: int, plan, two_sided: bool, device):
-    """One rmx_naive_maxnull_host_plan call: host X in (page-locked in place),
+def _run_from_host(x, plan, two_sided: bool, device):
+    """One rmx_naive_maxnull_host_plan(_f32) call: host X in (page-locked in
+    place; the float32 source when the DataMatrix keeps one),
     the plan's labels generated on the device from its seed (rmx_plan_orders'
     streams, bit-identical to numpy) while X's first chunk uploads, the X
     upload overlapped with the engine chunk by chunk, host max/argmax out.
@@ -217,7 +231,9 @@ def _run_from_host(values: np.ndarray, n1: int, plan, two_sided: bool, device):
 
     from .hostmem import pinned, pinned_empty
 
-    xh = pinned(np.asarray(values, dtype=np.float64))
+    n1 = x.n1
+    f32 = x.float32_values
+    xh = pinned(f32 if f32 is not None else x.values)
     v, n = xh.shape
     L = int(plan.count)
     if n > 32767:
@@ -227,12 +243,19 @@ def _run_from_host(values: np.ndarray, n1: int, plan, two_sided: bool, device):
     job = NaiveJob(xd, n1, od, two_sided)
     mx = pinned_empty((L,), np.float64)
     am = pinned_empty((L,), np.int32)
-    rc = job.lib.rmx_naive_maxnull_host_plan(
-        xh.ctypes.data, v, n, int(n1), ctypes.c_uint64(int(plan.master_seed) & ((1 << 64) - 1)),
-        L, job.two_sided, mx.ctypes.data,
-        am.ctypes.data, nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
-        nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
-        ctypes.byref(job.stats))
+    seed = ctypes.c_uint64(int(plan.master_seed) & ((1 << 64) - 1))
+    tail = (L, job.two_sided, mx.ctypes.data, am.ctypes.data)
+    bufs = (nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
+            nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
+            ctypes.byref(job.stats))
+    if f32 is not None:
+        x32 = torch.empty((v, n), dtype=torch.float32, device=device)
+        rc = job.lib.rmx_naive_maxnull_host_plan_f32(xh.ctypes.data, v, n, int(n1), seed, *tail,
+                                                     nat.ptr(x32), *bufs)
+        del x32  # the call is synchronous
+    else:
+        rc = job.lib.rmx_naive_maxnull_host_plan(xh.ctypes.data, v, n, int(n1), seed, *tail,
+                                                 *bufs)
     nat.raise_for(rc, job._st)
     return mx.copy(), am.copy(), job
 

@@ -149,6 +149,24 @@ def _lsq(u_dev, r: int, idx_dev, k: int, vals_dev, B: int):
     return W, flags, norms
 
 
+def _lsq_tc(u_dev, r: int, idx_dev, k: int, vals_dev, B: int):
+    """Batched solve_block with the tensor-core Gram + fp64 refinement
+    (rmx_lsq_solve_tc) -> (W (B x r), flags (B), stats [tc used, fp64 redos])."""
+    torch = _torch()
+    dev = u_dev.device
+    W = torch.empty((B, r), dtype=torch.float64, device=dev)
+    flags = torch.empty(B, dtype=torch.int32, device=dev)
+    per = (r + 1) * (r + 1) * 8 + 32
+    batch = max(1, min(B, _LSQ_BATCH_BYTES // per))
+    ws_bytes = int(nat.load().rmx_lsq_workspace_bytes(r, batch))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    stats = (ctypes.c_int32 * 2)()
+    nat.call("rmx_lsq_solve_tc", nat.ptr(u_dev), r, int(u_dev.shape[0]), r, nat.ptr(idx_dev), k,
+             nat.ptr(vals_dev), B, nat.ptr(W), nat.ptr(flags), nat.ptr(ws), ws_bytes, stats,
+             _stream(dev))
+    return W, flags, (int(stats[0]), int(stats[1]))
+
+
 def _orthonormalize(u_dev, force: bool) -> float:
     drift = ctypes.c_double(0.0)
     v, r = u_dev.shape
@@ -410,7 +428,7 @@ def recover(x, model: SubspaceModel, plan, cfg):
         _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel),
                                 omd.cpu().numpy(), od.cpu().numpy())
     nat.raise_for(rc, st)
-    W, flags, norms = _lsq(u, r, omd, k, t, nrec)
+    W, flags, _ = _lsq_tc(u, r, omd, k, t, nrec)
     evals = nrec * k
     bad = np.flatnonzero(flags.cpu().numpy() != 0)
     for j in bad:  # rapid.py:173-196: redraw from the same stream, up to 5 times

@@ -116,16 +116,14 @@ def run_naive_distributed(x, plan, two_sided: bool = False, group=None):
     the full (MaxNull, argmax) on every rank.  Single-process when
     torch.distributed is not initialised."""
     from .domain import MaxNull, as_data_matrix, as_plan
-    from .naive_engine import cuda_device, upload
+    from .naive_engine import cuda_device, data_to_device
 
     x = as_data_matrix(x)
     plan = as_plan(plan)
     if plan.subjects != x.subjects:
         raise UsageError("plan and data matrix disagree on subject count")
     dev = cuda_device()
-    from .hostmem import to_device
-
-    xd = to_device(np.ascontiguousarray(x.values, dtype=np.float64), dev)
+    xd = data_to_device(x, dev)
     sh = ShardedNaive(xd, x.n1, plan, two_sided, group)
     m, a = sh.step()
     return MaxNull(m.cpu().numpy()), a.cpu().numpy().astype(np.int64)

@@ -206,3 +206,25 @@ def test_int8_pairs_many_tiles_and_chunks_bit_exact(oracle_mod):
                                          threads=16)
     assert np.array_equal(res.maxima, mx)
     assert np.array_equal(res.argmax, am)
+
+
+@pytest.mark.parametrize("v,n1,n2,L,seed", [(4099, 200, 200, 300, 21), (3001, 10, 11, 257, 22),
+                                            (1, 3, 3, 30, 23)])
+def test_float32_host_upload_bit_exact(oracle_mod, v, n1, n2, L, seed):
+    """A DataMatrix built from float32 data uploads the float32 source
+    (rmx_naive_maxnull_host_plan_f32; odd n makes the chunk offsets
+    misaligned for the vector upcast); results equal the float64 upload's and
+    the oracle's bit for bit."""
+    g = np.random.default_rng(seed)
+    f32 = g.standard_normal((v, n1 + n2)).astype(np.float32)
+    x32 = rmx.DataMatrix(f32, n1, n2)
+    assert x32.float32_values is not None
+    x64 = rmx.DataMatrix(f32.astype(np.float64), n1, n2)
+    assert x64.float32_values is None
+    plan = rmx.PermutationPlan(seed + 100, L, n1 + n2)
+    r32 = rmx.run_naive_ex(x32, plan)
+    r64 = rmx.run_naive_ex(x64, plan)
+    mx, am, _ = oracle_mod.naive_maxnull(x64.values, n1, plan_orders(plan).astype(np.int64),
+                                         False, threads=8)
+    assert np.array_equal(r32.maxima, r64.maxima) and np.array_equal(r32.maxima, mx)
+    assert np.array_equal(r32.argmax, r64.argmax) and np.array_equal(r32.argmax, am)

@@ -158,3 +158,38 @@ def test_tensor_core_completion_matches_fp32(monkeypatch, v, r, B, two_sided):
     bound = 2.0 ** -10 * (np.abs(w) @ np.abs(q).T).max(axis=1) + 1e-5
     assert np.all(np.isfinite(tc))
     assert np.all(np.abs(tc - ref) <= bound), np.max(np.abs(tc - ref) / bound)
+
+
+@pytest.mark.parametrize("v,r,k,B", [(6000, 100, 700, 300), (20000, 400, 1836, 160),
+                                     (3000, 31, 200, 50), (9000, 130, 520, 200)])
+def test_tensor_core_gram_lsq_matches_fp64(v, r, k, B):
+    """rmx_lsq_solve_tc (tcgen05 Gram of fp16 hi/lo planes + two fp64
+    refinement steps) against the fp64 Gram + Cholesky path, on orthonormal
+    bases and random observation sets: 1e-10 relative, with no system falling
+    back to fp64 (so the tensor-core Gram itself is accurate); a rank-deficient
+    restriction is flagged exactly as in the fp64 path."""
+    import torch
+
+    from paper_1703_01506_b200 import rapid_engine as re
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(v + r)
+    u = np.linalg.qr(rng.standard_normal((v, r)))[0]
+    idx = np.stack([np.sort(rng.choice(v, k, replace=False)) for _ in range(B)]).astype(np.int32)
+    vals = rng.standard_normal((B, k)) * 3.0 + (u[idx] @ rng.standard_normal(r)) * 40.0
+    # one restriction made rank-deficient: a basis column vanishes on its rows
+    u[idx[B // 2], r // 3] = 0.0
+    ud = torch.from_numpy(u).to(dev)
+    idd = torch.from_numpy(idx).to(dev)
+    vd = torch.from_numpy(vals).to(dev)
+    W, F, stats = re._lsq_tc(ud, r, idd, k, vd, B)
+    W0, F0, _ = re._lsq(ud, r, idd, k, vd, B)
+    torch.cuda.synchronize()
+    W, W0 = W.cpu().numpy(), W0.cpu().numpy()
+    F, F0 = F.cpu().numpy(), F0.cpu().numpy()
+    assert stats[0] == 1
+    assert np.array_equal(F, F0) and F[B // 2] == 1
+    ok = F0 == 0
+    err = np.abs(W[ok] - W0[ok]).max() / np.abs(W0[ok]).max()
+    assert err < 1e-10, err
+    assert stats[1] == 1, stats  # only the rank-deficient system was re-solved in fp64

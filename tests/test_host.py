@@ -67,6 +67,19 @@ def test_data_matrix_validation_messages():
         rmx.DataMatrix(bad, 2, 2)
     x = rmx.DataMatrix(np.arange(12.0).reshape(3, 4), 2, 2)
     assert not x.values.flags.writeable
+    assert x.float32_values is None
+
+
+def test_data_matrix_keeps_float32_source():
+    """float32 input: values is the exact float64 upcast; the float32 copy is
+    private (caller mutation does not leak) and read-only."""
+    src = np.random.default_rng(0).standard_normal((5, 4)).astype(np.float32)
+    x = rmx.DataMatrix(src, 2, 2)
+    assert x.values.dtype == np.float64 and x.float32_values.dtype == np.float32
+    assert np.array_equal(x.float32_values.astype(np.float64), x.values)
+    src[0, 0] = 99.0
+    assert x.float32_values[0, 0] != 99.0 and x.values[0, 0] != 99.0
+    assert not x.float32_values.flags.writeable
 
 
 def test_runconfig_resolve_defaults_and_errors():
