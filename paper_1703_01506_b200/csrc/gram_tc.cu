@@ -19,14 +19,16 @@
 //
 // Work split.  G is symmetric, so only the upper block triangle is formed:
 // 128-row strips m = 0.. of A^T (rows = basis columns 128 m ..), each times
-// the columns [128 m, rp) (rp = r + 1 rounded up to 32).  Strips are packed
+// the columns [128 m, rp).  t sits at Gram index rt = round_up(r, 8), so the
+// 16-byte piece that carries it holds no U column and is built in registers
+// (rp = rt + 1 rounded up to 32; the epilogue maps rt back to index r).  Strips are packed
 // into jobs whose TMEM columns sum(rp - 128 m) fit the 512-column
 // accumulator; one CTA runs one (system, job) unit at a time (persistent
 // grid).  Roles: warp 0 allocates TMEM and issues the MMAs (one thread),
 // warps 4-7 drain the accumulator (TMEM lane quadrants 0-3) into G (fp64,
 // written transposed so that each warp store is one coalesced row segment of
 // G's lower triangle), warps 8-11 gather rows with cp.async into a
-// kGStages-deep ring.
+// kGStages-deep ring (the unit's row ids and t halves staged in smem first).
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -40,9 +42,9 @@
 namespace rmx {
 namespace {
 
-constexpr int kGBK = 32;        // gathered rows per ring stage
-constexpr int kGStages = 4;     // ring depth
-constexpr int kGLag = 2;        // stages a producer keeps in flight before publishing
+constexpr int kGBK = 16;        // gathered rows per ring stage (one MMA K step)
+constexpr int kGStages = 7;     // ring depth
+constexpr int kGLag = 5;        // stages a producer keeps in flight before publishing
 constexpr int kGProd = 128;     // producer threads (warps 8-11)
 constexpr int kGThreadsTc = 384;
 constexpr int kGMaxJobs = 4;
@@ -51,7 +53,8 @@ constexpr float kGUScale = 16384.0f;  // U planes hold U 2^14 (|U| <= 1)
 struct GramTcArgs {
   const __half* planes;  // [2][v][kpg]: hi, lo of U 2^14; columns >= r are 0
   int64_t v;
-  int r, kpg, rp;         // rp = round_up(r + 1, 32) <= kpg
+  int r, kpg, rp;         // rp = round_up(rt + 1, 32) = kpg
+  int rt;                 // Gram index of t: round_up(r, 8) (its 8-column piece holds no U)
   const int32_t* idx;     // [B][k]
   int k;
   const double* vals;     // [B][k]
@@ -60,11 +63,17 @@ struct GramTcArgs {
   int njobs;
   int job_s0[kGMaxJobs], job_s1[kGMaxJobs];
   int stage_mn;           // columns per stage plane (>= every job's extent)
+  uint32_t stage_off;     // byte offset of the per-unit staging (row ids, t halves)
 };
 
-__device__ __forceinline__ void cp_async16_cg(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_cg_u32(uint32_t smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
 
 // power-of-2 scale bringing max |t| into [2^14, 2^15)
@@ -102,6 +111,8 @@ __global__ void __launch_bounds__(kGThreadsTc, 1) k_gram_tc(const __grid_constan
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   double* red = reinterpret_cast<double*>(tmem_slot + 4);  // 2 x 4 doubles
+  int32_t* sidx = reinterpret_cast<int32_t*>(sm + a.stage_off);  // unit's row ids [k]
+  __half2* st2 = reinterpret_cast<__half2*>(sidx + ((a.k + 3) & ~3));  // (t hi, t lo) [k]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t SBO = kGBK * 16u, LBO = 128u;
 
@@ -176,48 +187,56 @@ __global__ void __launch_bounds__(kGThreadsTc, 1) k_gram_tc(const __grid_constan
     }
   } else if (warp >= 8) {
     // ---------------------------------------------------------- producers
-    const int ptid = threadIdx.x - 256;
+    // per unit: the row ids and the scaled t halves are staged in shared
+    // memory once, so a piece costs one smem read + two cp.async (no
+    // dependent global load per piece); warp pw gathers rows pw, pw + 4, ..
+    // of each stage, lanes over the row's 16-byte pieces (coalesced)
+    const int ptid = threadIdx.x - 256, pw = ptid >> 5;
     int64_t g = 0;
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int64_t b = u / a.njobs;
       const int job = (int)(u % a.njobs);
       const int col0 = 128 * a.job_s0[job];
       const int ppr = (a.rp - col0) / 8;  // 16-byte pieces per gathered row
+      const int tq = (a.rt - col0) / 8;   // the piece holding t (no U columns)
       const int32_t* ib = a.idx + b * a.k;
       const double* tb = a.vals + b * a.k;
+      // every producer is done issuing the previous unit (staging reusable)
+      asm volatile("bar.sync 1, %0;" ::"n"(kGProd) : "memory");
       const double tsc = t_scale(block_absmax_t(tb, a.k, ptid, kGProd, red, 1));
-      const int tpiece = (a.r - col0) / 8;  // piece holding column r (t)
-      const int tpos = (a.r - col0) % 8;
+      for (int i = ptid; i < a.k; i += kGProd) {
+        sidx[i] = ib[i];
+        const double x = tb[i] * tsc;
+        const __half th = __double2half(x);
+        st2[i] = __halves2half2(th, __double2half(x - (double)__half2float(th)));
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kGProd) : "memory");
       for (int c = 0; c < nst; ++c, ++g) {
         const int st = (int)(g % kGStages);
         mbar_wait(&empty[st], (uint32_t)(((g / kGStages) & 1) ^ 1));
-        uint8_t* hi = stages + st * stage_bytes;
-        uint8_t* lo = hi + plane_bytes;
+        const uint32_t hi = smem_u32(stages + st * stage_bytes), lo = hi + plane_bytes;
         const int kk0 = c * kGBK;
-        for (int e = ptid; e < kGBK * ppr; e += kGProd) {
-          const int kr = e / ppr, q = e - kr * ppr;
-          const uint32_t off = (uint32_t)q * SBO + (uint32_t)(kr >> 3) * LBO + (kr & 7) * 16u;
+        for (int kr = pw; kr < kGBK; kr += kGProd / 32) {
           const int kk = kk0 + kr;
+          const uint32_t roff = (uint32_t)(kr >> 3) * LBO + (kr & 7) * 16u;
           if (kk < a.k) {
-            const int64_t row = ib[kk];
-            const __half* ph = a.planes + row * a.kpg + col0 + 8 * q;
-            if (q == tpiece) {  // U columns (zeros past r) + t at column r
-              uint4 vh = *reinterpret_cast<const uint4*>(ph);
-              uint4 vl = *reinterpret_cast<const uint4*>(ph + a.v * a.kpg);
-              const double x = tb[kk] * tsc;
-              const __half th = __double2half(x);
-              const __half tl = __double2half(x - (double)__half2float(th));
-              reinterpret_cast<__half*>(&vh)[tpos] = th;
-              reinterpret_cast<__half*>(&vl)[tpos] = tl;
-              *reinterpret_cast<uint4*>(hi + off) = vh;
-              *reinterpret_cast<uint4*>(lo + off) = vl;
-            } else {
-              cp_async16_cg(hi + off, ph);
-              cp_async16_cg(lo + off, ph + a.v * a.kpg);
+            const __half* ph = a.planes + (int64_t)sidx[kk] * a.kpg + col0;
+            for (int q = lane; q < ppr; q += 32) {
+              const uint32_t off = (uint32_t)q * SBO + roff;
+              if (q == tq) {  // [t, 0, .., 0]
+                const __half2 t2 = st2[kk];
+                st_shared_v4(hi + off, make_uint4(__half_as_ushort(__low2half(t2)), 0, 0, 0));
+                st_shared_v4(lo + off, make_uint4(__half_as_ushort(__high2half(t2)), 0, 0, 0));
+              } else {
+                cp_async16_cg_u32(hi + off, ph + 8 * q);
+                cp_async16_cg_u32(lo + off, ph + a.v * a.kpg + 8 * q);
+              }
             }
           } else {  // rows past k: zero
-            *reinterpret_cast<uint4*>(hi + off) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(lo + off) = make_uint4(0, 0, 0, 0);
+            for (int q = lane; q < ppr; q += 32) {
+              st_shared_v4(hi + (uint32_t)q * SBO + roff, make_uint4(0, 0, 0, 0));
+              st_shared_v4(lo + (uint32_t)q * SBO + roff, make_uint4(0, 0, 0, 0));
+            }
           }
         }
         cp_async_commit();
@@ -248,16 +267,20 @@ __global__ void __launch_bounds__(kGThreadsTc, 1) k_gram_tc(const __grid_constan
       tc_fence_after();
       uint32_t tcol = 0;
       for (int m = s0; m < s1; ++m) {
-        const int i = 128 * m + 32 * quad + lane;  // this thread's row of G~ (a basis column)
+        // this thread's row of G~: a basis column (< r) or t (rt -> index r)
+        const int gi = 128 * m + 32 * quad + lane;
+        const bool irow = gi < a.r || gi == a.rt;
+        const int i = gi == a.rt ? a.r : gi;
         for (int j0 = 128 * m; j0 < a.rp; j0 += 32) {
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(32 * quad) << 16) + tcol + (uint32_t)(j0 - 128 * m), v);
           tmem_ld_wait();
-          if (i <= a.r) {
+          if (irow) {
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
-              const int j = j0 + jj;
-              if (j >= i && j <= a.r) {
+              const int gj = j0 + jj;
+              if (gj >= gi && (gj < a.r || gj == a.rt)) {
+                const int j = gj == a.rt ? a.r : gj;
                 const double sc = (j == a.r) ? (i == a.r ? dtt : dut) : duu;
                 Gb[(int64_t)j * ld + i] = (double)__uint_as_float(v[jj]) * sc;
               }
@@ -349,7 +372,8 @@ __global__ void __launch_bounds__(32 * kRWarps) k_lsq_resid(const double* __rest
 
 }  // namespace
 
-int gram_tc_kpg(int r) { return (r + 1 + 31) / 32 * 32; }
+static int gram_tc_rt(int r) { return (r + 7) / 8 * 8; }
+int gram_tc_kpg(int r) { return (gram_tc_rt(r) + 1 + 31) / 32 * 32; }
 
 // strips of 128 basis columns, packed into jobs of <= 512 TMEM columns
 static int gram_tc_jobs(int rp, int* s0, int* s1) {
@@ -372,7 +396,7 @@ static int gram_tc_jobs(int rp, int* s0, int* s1) {
 }
 
 bool gram_tc_supported(int r, int k) {
-  if (r < 16 || k < 16 || r + 1 > 512) return false;
+  if (r < 16 || k < 16 || gram_tc_kpg(r) > 512) return false;
   int s0[8], s1[8];
   return gram_tc_jobs(gram_tc_kpg(r), s0, s1) <= kGMaxJobs;
 }
@@ -409,7 +433,9 @@ cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t
     mn = std::max(mn, std::max(a.rp - 128 * s0[j], 128 * (s1[j] - s0[j])));
   }
   a.stage_mn = mn;
-  const size_t smem = 1024 + (size_t)kGStages * 2 * kGBK * mn * 2 + 256;
+  a.rt = gram_tc_rt(r);
+  a.stage_off = (uint32_t)((size_t)kGStages * 2 * kGBK * mn * 2 + 256);
+  const size_t smem = 1024 + a.stage_off + (size_t)((k + 3) & ~3) * 4 + (size_t)k * 4;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

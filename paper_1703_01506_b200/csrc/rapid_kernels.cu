@@ -197,6 +197,9 @@ __device__ __forceinline__ void chol_block32(double* D, double* rinv, double tin
   for (int l = 0; l < kPW; ++l) D[lane * kPS + l] = (l <= lane) ? a[l] : 0.0;
 }
 
+// rows of the panel below the first diagonal block (the largest panel)
+__host__ __device__ constexpr int chol_panel_rows(int r) { return r > kPW ? r - kPW : 1; }
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r
   extern __shared__ double sm[];
   double* D = sm;                     // kPW x kPS: block / L_D (lower)
   double* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
-  double* P = rinv + kPW;             // r x kPS panel
-  double* y = P + (size_t)r * kPS;    // r: right-hand side / solution
+  double* P = rinv + kPW;             // chol_panel_rows(r) x kPS panel (factor only)
+  double* y = rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS;  // r: rhs / solution
   __shared__ int bad;
   __shared__ double dmax;
   const int64_t b = blockIdx.x;
@@ -1238,7 +1241,9 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
 
 cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_t* flag,
                               double* resid2, cudaStream_t s) {
-  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
+  // panel sized to the largest one (r - 32 rows): 109 KB at r = 400, two CTAs per SM
+  const size_t smem =
+      ((size_t)kPW * kPS + kPW + (size_t)chol_panel_rows(r) * kPS + (size_t)r) * sizeof(double);
   // few systems (GROUSE: one per update): a 512-thread CTA hides more of the
   // L2 latency of the trailing updates; batches: 256 threads, several CTAs / SM
   if (B < 148) {
@@ -1257,7 +1262,7 @@ cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_
 
 cudaError_t launch_chol_resolve(double* G, int r, int64_t B, const double* rhs, double* w_inout,
                                 int32_t* nconv, cudaStream_t s) {
-  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(double);  // no panel
   cudaError_t e = cudaFuncSetAttribute(k_chol_solve<256>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
