@@ -245,6 +245,108 @@ __device__ __forceinline__ double np_pw_sum_warp(const G& g, int n, NpWarpScratc
   return total;
 }
 
+// Leaf plan of a group size (numpy's pairwise tree depends on n only), built
+// once per block and shared by every row the block evaluates.
+struct NpLeafPlan {
+  int n, nleaves;
+  int2 leaf[NpWarpScratch::kMaxLeaves];
+};
+__device__ __forceinline__ void np_leaf_plan(int n, NpLeafPlan* p) {  // one thread
+  int cnt = 0;
+  NpLeaves<8>::list(0, n, cnt, p->leaf);
+  p->n = n;
+  p->nleaves = cnt;
+}
+
+// Both groups of one row in one warp pass: the leaves of group 1 then of
+// group 2 are spread over the 4 eight-lane slots of each round, each slot
+// running one leaf's eight chains exactly as np_pw_sum_warp does, so the two
+// sums carry np_pw_sum's bits.  f(i, grp) = the i-th term of group grp (0/1).
+// val: per-warp scratch of P1.nleaves + P2.nleaves doubles.
+template <class F>
+__device__ __forceinline__ void np_pw_sum2_warp(const F& f, const NpLeafPlan& P1,
+                                                const NpLeafPlan& P2, double* val, double& s1,
+                                                double& s2) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & 7;
+  const int total = P1.nleaves + P2.nleaves;
+  for (int base = 0; base < total; base += 4) {
+    const int l = base + (lane >> 3);
+    const bool act = l < total;
+    const int grp = (l < P1.nleaves) ? 0 : 1;
+    const int2 lf = !act ? make_int2(0, 0) : (grp == 0 ? P1.leaf[l] : P2.leaf[l - P1.nleaves]);
+    const int lo = lf.x, m = lf.y;
+    double r = 0.0;
+    if (act && m >= 8) {
+      r = f(lo + sub, grp);
+      const int stop = m - (m % 8);
+      for (int i = 8; i < stop; i += 8) r = __dadd_rn(r, f(lo + i + sub, grp));
+    }
+    double t = __shfl_down_sync(0xffffffffu, r, 1);
+    r = __dadd_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 2);
+    r = __dadd_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 4);
+    r = __dadd_rn(r, t);
+    if (act && sub == 0) {
+      double res;
+      int i;
+      if (m < 8) {
+        res = 0.0;
+        i = 0;
+      } else {
+        res = r;
+        i = m - (m % 8);
+      }
+      for (; i < m; ++i) res = __dadd_rn(res, f(lo + i, grp));
+      val[l] = res;
+    }
+  }
+  __syncwarp();
+  double a = 0.0, b = 0.0;
+  if (lane == 0) {
+    int idx = 0;
+    a = NpLeaves<8>::combine(P1.n, idx, val);
+    idx = 0;
+    b = NpLeaves<8>::combine(P2.n, idx, val + P1.nleaves);
+  }
+  s1 = __shfl_sync(0xffffffffu, a, 0);
+  s2 = __shfl_sync(0xffffffffu, b, 0);
+  __syncwarp();
+}
+
+// welch_exact of a row staged in shared memory (stride 1), both groups per
+// pass with precomputed leaf plans: the bits of welch_exact.
+__device__ __forceinline__ WelchExact welch_exact_warp2(const double* row, const int16_t* ord,
+                                                        const NpLeafPlan& P1,
+                                                        const NpLeafPlan& P2, double* val) {
+  const int n1 = P1.n, n2 = P2.n;
+  double s1, s2;
+  np_pw_sum2_warp([&](int i, int grp) { return row[ord[i + grp * n1]]; }, P1, P2, val, s1, s2);
+  const double m1 = __ddiv_rn(s1, (double)n1);
+  const double m2 = __ddiv_rn(s2, (double)n2);
+  double q1, q2;
+  np_pw_sum2_warp(
+      [&](int i, int grp) {
+        const double d = __dsub_rn(row[ord[i + grp * n1]], grp ? m2 : m1);
+        return __dmul_rn(d, d);
+      },
+      P1, P2, val, q1, q2);
+  const double v1 = __ddiv_rn(q1, (double)(n1 - 1));
+  const double v2 = __ddiv_rn(q2, (double)(n2 - 1));
+  const double var_term = __dadd_rn(__ddiv_rn(v1, (double)n1), __ddiv_rn(v2, (double)n2));
+  WelchExact r;
+  r.num = __dsub_rn(m1, m2);
+  if (var_term == 0.0) {
+    r.t = 0.0;
+    r.degenerate = (r.num != 0.0);
+  } else {
+    r.t = __ddiv_rn(r.num, __dsqrt_rn(var_term));
+    r.degenerate = false;
+  }
+  return r;
+}
+
 // welch_exact with the warp: identical bits, every lane gets the result.
 // Larger groups fall back to lane 0 and a broadcast.
 __device__ __forceinline__ WelchExact welch_exact_warp(const double* row, int64_t stride,
