@@ -245,10 +245,7 @@ int rmx_complete_max(const float* u32, int64_t v, int32_t r, const float* w32, i
   a.nk16 = lay.kpad / 16;
   a.n_vtiles = lay.n_vtiles;
   a.n_mtiles = lay.n_mtiles;
-  a.n_chunks = lay.n_chunks;
-  a.tiles_per_chunk = lay.tiles_per_chunk;
-  a.stride_full = golden_stride_public(lay.tiles_per_chunk);
-  a.stride_last = golden_stride_public(lay.n_vtiles - (lay.n_chunks - 1) * lay.tiles_per_chunk);
+  fill_chunks(lay, &a);
   a.chunk_begin = 0;
   a.chunk_end = lay.n_chunks;
   a.wA = wA.p;

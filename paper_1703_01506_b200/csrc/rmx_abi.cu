@@ -136,7 +136,9 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
   // (short K is epilogue-bound, where the fp16 tiles' cheaper epilogue wins)
   lay.i8 = (balanced && n >= 192) ? 1 : 0;
   if (const char* e = getenv("RMX_I8")) lay.i8 = balanced && atoi(e) != 0;
-  lay.kpad = lay.i8 ? (n + 31) / 32 * 32 : (n + 15) / 16 * 16;
+  // int8: the digit planes [h | l] share one K extent 2 kpad, a multiple of
+  // the 32-byte MMA K step whenever kpad is a multiple of 16
+  lay.kpad = (n + 15) / 16 * 16;
   lay.vt = balanced ? 2 * kTileV : kTileV;
   lay.n_vtiles = (int)((v + lay.vt - 1) / lay.vt);
   // CTA pairs (cta_group::2) by default; RMX_CG=1 forces single-CTA tiles
@@ -201,8 +203,20 @@ NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
       best_c = c;
     }
   }
-  lay.tiles_per_chunk = (lay.n_vtiles + best_c - 1) / best_c;
-  lay.n_chunks = (lay.n_vtiles + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
+  // leading short chunks (8 then 32 tiles): the cold top-4 storm of a unit's
+  // first tiles is confined to 8 tiles, and the following chunks start from
+  // the permutation's best over 2,048 and then 10,240 voxels (RMX_RAMP=0: off)
+  lay.n_ramp = 0;
+  lay.ramp_start[0] = 0;
+  const char* re = getenv("RMX_RAMP");
+  if (lay.n_vtiles >= 512 && best_c >= 4 && !(re && atoi(re) == 0)) {
+    lay.n_ramp = 2;
+    lay.ramp_start[1] = 8;
+    lay.ramp_start[2] = 40;
+  }
+  const int bulk = lay.n_vtiles - lay.ramp_start[lay.n_ramp];
+  lay.tiles_per_chunk = (bulk + best_c - 1) / best_c;
+  lay.n_chunks = lay.n_ramp + (bulk + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
   lay.grid = lay.cg * (int)std::min<int64_t>(n_clusters, (int64_t)lay.n_mtiles * lay.n_chunks);
 
   size_t off = 0;
@@ -252,6 +266,8 @@ NaiveLayout complete_layout(int64_t v, int r, int64_t B, int sm_count) {
   // chunks: enough units for the persistent grid to balance (>= 6 per cluster)
   int c = 1;
   while (c < lay.n_vtiles && (int64_t)lay.n_mtiles * c < 6LL * n_clusters) c *= 2;
+  lay.n_ramp = 0;
+  lay.ramp_start[0] = 0;
   lay.tiles_per_chunk = (lay.n_vtiles + c - 1) / c;
   lay.n_chunks = (lay.n_vtiles + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
   lay.grid = lay.cg * (int)std::min<int64_t>(n_clusters, (int64_t)lay.n_mtiles * lay.n_chunks);
@@ -449,10 +465,7 @@ int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t 
   a.nk16 = ws.lay.kpad / 16;  // MMA K-steps (int8: 2 kpad / 32)
   a.n_vtiles = ws.lay.n_vtiles;
   a.n_mtiles = ws.lay.n_mtiles;
-  a.n_chunks = ws.lay.n_chunks;
-  a.tiles_per_chunk = ws.lay.tiles_per_chunk;
-  a.stride_full = golden_stride(ws.lay.tiles_per_chunk);
-  a.stride_last = golden_stride(ws.lay.n_vtiles - (ws.lay.n_chunks - 1) * ws.lay.tiles_per_chunk);
+  fill_chunks(ws.lay, &a);
   a.chunk_begin = chunk_begin;
   a.chunk_end = chunk_end < 0 ? ws.lay.n_chunks : chunk_end;
   a.alpha = (float)alpha;

@@ -81,10 +81,28 @@ struct NaiveCounters {
   unsigned long long all_groups;
 };
 
+// Voxel chunks of a permutation tile: n_ramp short leading chunks (tiles
+// [ramp_start[c], ramp_start[c+1])) -- a cold unit's top-4 threshold climbs
+// from nothing, so the first chunks are kept short and every later unit
+// starts from the permutation's best over a growing prefix -- then uniform
+// chunks of tpc tiles.
+constexpr int kMaxRamp = 3;
+__host__ __device__ inline void chunk_tiles(int n_ramp, const int* ramp_start, int tpc,
+                                            int n_vtiles, int chunk, int* t0, int* t1) {
+  if (chunk < n_ramp) {
+    *t0 = ramp_start[chunk];
+    *t1 = ramp_start[chunk + 1];
+  } else {
+    *t0 = ramp_start[n_ramp] + (chunk - n_ramp) * tpc;
+    *t1 = *t0 + tpc < n_vtiles ? *t0 + tpc : n_vtiles;
+  }
+}
+
 // Workspace carve-up for one naive call.
 struct NaiveLayout {
   int kpad;           // n rounded up to 16 (MMA K granularity)
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk, groups, grid, bk, stages;
+  int n_ramp, ramp_start[kMaxRamp + 1];  // leading short chunks (chunk_tiles)
   int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
   int i8;             // exact int8 MMA on 16-bit fixed-point Z (balanced groups)
   int vt;             // voxels per tile: 256 (S-only, n1 == n2) or 128 (S | Q)
@@ -96,6 +114,8 @@ struct NaiveLayout {
 NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count);
 NaiveLayout complete_layout(int64_t v, int r, int64_t B, int sm_count);
 int golden_stride_public(int T);
+// chunk / stride fields of TfillArgs from a layout
+void fill_chunks(const NaiveLayout& lay, struct TfillArgs* a);
 
 struct PrepArgs {
   const double* x;
@@ -118,6 +138,7 @@ struct TfillArgs {
   int n, n1, kpad, nk16;
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
   int stride_full, stride_last;  // tile visiting strides (coprime with the chunk length)
+  int n_ramp, ramp_start[kMaxRamp + 1], ramp_stride[kMaxRamp];  // leading short chunks
   int chunk_begin, chunk_end;    // voxel chunks [begin, end) of this launch
   float alpha, beta, gamma, dthr;
   float band_rel;          // fp32 part of the refinement band (threshold seeding)

@@ -101,6 +101,7 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
 struct EpiConst {
   uint64_t alpha2, beta2, gamma2;  // packed (x, x)
   float alpha, beta, gamma, dthr;
+  float sdeg;  // S-only signed tiles: |S| beyond which d~ may fall below dthr (suspects)
 };
 
 // Common path over 32 columns (voxels jbase..jbase+31) of one accumulator
@@ -145,6 +146,20 @@ __device__ __forceinline__ float sonly_thr(float k3, const EpiConst& ec) {
   const float k = fmaxf(k3, 0.0f);
   return k * ec.gamma / fmaf(-k, ec.beta, 1.0f);
 }
+// Signed (one-sided) S-only tiles, hit mask (only for groups whose S^2 test
+// fired): a column can matter only if S > sqrt(K) (t above the row's
+// threshold) or S < -sdeg (near-zero d~: a suspected degenerate voxel,
+// listed whatever its sign).  The S^2 test alone would also send every
+// strongly negative t of the row through the rare path (half of the rare
+// groups at config 4).
+// K == 0 (the row's top-4 not yet full of non-negative keys): every column.
+__device__ __forceinline__ float sonly_signed_thr(float K, const EpiConst& ec) {
+  return K > 0.0f ? fminf(sqrtf(K) * (1.0f - 1e-6f), ec.sdeg) : -FLT_MAX;
+}
+
+// Common path: S^2 > K, one packed FMA per column pair (for signed tiles a
+// superset that also admits strongly negative t; sonly_mask then sorts them
+// out before the rare path).
 __device__ __forceinline__ bool sonly_any(const uint32_t (&s)[32], float K) {
   const uint64_t nk = pack2(__float_as_uint(-K), __float_as_uint(-K));
   uint32_t all = 0xffffffffu;
@@ -156,15 +171,32 @@ __device__ __forceinline__ bool sonly_any(const uint32_t (&s)[32], float K) {
   }
   return (int)all >= 0;  // some sign bit clear
 }
-__device__ __forceinline__ uint32_t sonly_mask(const uint32_t (&s)[32], float K) {
-  const uint64_t nk = pack2(__float_as_uint(-K), __float_as_uint(-K));
+template <bool TWO_SIDED>
+__device__ __forceinline__ uint32_t sonly_mask(const uint32_t (&s)[32], float K,
+                                               const EpiConst& ec) {
   uint32_t neg = 0;
+  if constexpr (TWO_SIDED) {
+    const uint64_t nk = pack2(__float_as_uint(-K), __float_as_uint(-K));
 #pragma unroll
-  for (int c = 30; c >= 0; c -= 2) {
-    const uint64_t S2 = pack2(s[c], s[c + 1]);
-    const uint64_t m = fma2(S2, S2, nk);
-    neg = __funnelshift_l((uint32_t)(m >> 32), neg, 1);
-    neg = __funnelshift_l((uint32_t)m, neg, 1);
+    for (int c = 30; c >= 0; c -= 2) {
+      const uint64_t S2 = pack2(s[c], s[c + 1]);
+      const uint64_t m = fma2(S2, S2, nk);
+      neg = __funnelshift_l((uint32_t)(m >> 32), neg, 1);
+      neg = __funnelshift_l((uint32_t)m, neg, 1);
+    }
+  } else {
+    const float thr = sonly_signed_thr(K, ec);
+    const uint64_t one = pack2(__float_as_uint(1.0f), __float_as_uint(1.0f));
+    const uint64_t mone = pack2(__float_as_uint(-1.0f), __float_as_uint(-1.0f));
+    const uint64_t nt = pack2(__float_as_uint(-thr), __float_as_uint(-thr));
+    const uint64_t nd = pack2(__float_as_uint(-ec.sdeg), __float_as_uint(-ec.sdeg));
+#pragma unroll
+    for (int c = 30; c >= 0; c -= 2) {
+      const uint64_t S2 = pack2(s[c], s[c + 1]);
+      const uint64_t m = fma2(S2, one, nt) & fma2(S2, mone, nd);
+      neg = __funnelshift_l((uint32_t)(m >> 32), neg, 1);
+      neg = __funnelshift_l((uint32_t)m, neg, 1);
+    }
   }
   return ~neg;
 }
@@ -234,16 +266,16 @@ __device__ __forceinline__ void group_debug(const uint32_t (&s)[32], const uint3
 // i-th tile of a unit's chunk in a low-discrepancy (golden-ratio stride)
 // order: every permutation's top-4 threshold is close to final after the
 // first few percent of the sweep, which keeps the epilogue's rare path rare.
-__device__ __forceinline__ int chunk_tile(const TfillArgs& a, int t0, int t1, int i) {
+__device__ __forceinline__ int chunk_tile(const TfillArgs& a, int chunk, int t0, int t1, int i) {
   const int T = t1 - t0;
-  const int stride = (T == a.tiles_per_chunk) ? a.stride_full : a.stride_last;
+  const int stride = chunk < a.n_ramp ? a.ramp_stride[chunk]
+                                      : ((T == a.tiles_per_chunk) ? a.stride_full : a.stride_last);
   return t0 + (int)(((int64_t)i * stride) % T);
 }
 
 // Voxel-tile range [t0, t1) of a chunk.
 __device__ __forceinline__ void chunk_range(const TfillArgs& a, int chunk, int& t0, int& t1) {
-  t0 = chunk * a.tiles_per_chunk;
-  t1 = min(t0 + a.tiles_per_chunk, a.n_vtiles);
+  chunk_tiles(a.n_ramp, a.ramp_start, a.tiles_per_chunk, a.n_vtiles, chunk, &t0, &t1);
 }
 
 __device__ __forceinline__ float key_to_t(float key) { return copysignf(sqrtf(fabsf(key)), key); }
@@ -397,7 +429,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
         int t0, t1;
         chunk_range(a, chunk, t0, t1);
         for (int i = 0; i < t1 - t0; ++i) {
-          const int t = chunk_tile(a, t0, t1, i);
+          const int t = chunk_tile(a, chunk, t0, t1, i);
           for (int kb = 0; kb < kext; kb += BK) {
             uint8_t* dst = stage_mem + stage * STAGE_BYTES;
             if (I8) {  // one box per stage: this CTA's voxels x 128 K-bytes of [h | l]
@@ -531,6 +563,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     ec.alpha2 = pack2(__float_as_uint(a.alpha), __float_as_uint(a.alpha));
     ec.beta2 = pack2(__float_as_uint(a.beta), __float_as_uint(a.beta));
     ec.gamma2 = pack2(__float_as_uint(a.gamma), __float_as_uint(a.gamma));
+    // d~ = beta S^2 + gamma < dthr  <=>  S^2 > (gamma - dthr) / |beta| (alpha = 0);
+    // 1e-4 relative margin for the fp32 rounding of d~
+    ec.sdeg = (a.gamma > ec.dthr && a.beta_abs > 0.0f)
+                  ? sqrtf((a.gamma - ec.dthr) / a.beta_abs) * (1.0f - 1e-4f)
+                  : 0.0f;
     const int slots = a.n_chunks * GROUPS;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -582,7 +619,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       unsigned rare_groups = 0;
       float* winv = inv_smem + ew * (COLGROUPS * 32);  // this warp's columns
       for (int i = 0; i < t1 - t0; ++i) {
-        const int t = chunk_tile(a, t0, t1, i);
+        const int t = chunk_tile(a, chunk, t0, t1, i);
         if (I8) {  // stage the tile's scales for our columns; lands during the MMA wait
           __syncwarp();
           if (lane < COLGROUPS * 8)
@@ -661,7 +698,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
           if (gvalid <= 0) continue;
           if constexpr (SONLY) {
             if (!__any_sync(0xffffffffu, sonly_any(sv, kthr))) continue;
-            uint32_t hits = sonly_mask(sv, kthr);
+            uint32_t hits = sonly_mask<TWO_SIDED>(sv, kthr, ec);
             if (gvalid < 32) hits &= (1u << gvalid) - 1u;
             if (__any_sync(0xffffffffu, hits != 0u)) {
               ++rare_groups;
@@ -852,10 +889,22 @@ bool make_planes_map(CUtensorMap* map, const __half* planes, int64_t v, int kpad
 }
 
 void chunk_voxels(const NaiveLayout& lay, int64_t v, int c, int64_t* v0, int64_t* v1) {
-  const int64_t t0 = (int64_t)c * lay.tiles_per_chunk;
-  const int64_t t1 = std::min<int64_t>(t0 + lay.tiles_per_chunk, lay.n_vtiles);
-  *v0 = std::min<int64_t>(t0 * lay.vt, v);
-  *v1 = std::min<int64_t>(t1 * lay.vt, v);
+  int t0, t1;
+  chunk_tiles(lay.n_ramp, lay.ramp_start, lay.tiles_per_chunk, lay.n_vtiles, c, &t0, &t1);
+  *v0 = std::min<int64_t>((int64_t)t0 * lay.vt, v);
+  *v1 = std::min<int64_t>((int64_t)t1 * lay.vt, v);
+}
+
+void fill_chunks(const NaiveLayout& lay, TfillArgs* a) {
+  a->n_chunks = lay.n_chunks;
+  a->tiles_per_chunk = lay.tiles_per_chunk;
+  a->n_ramp = lay.n_ramp;
+  for (int i = 0; i <= lay.n_ramp; ++i) a->ramp_start[i] = lay.ramp_start[i];
+  for (int i = 0; i < lay.n_ramp; ++i)
+    a->ramp_stride[i] = golden_stride_public(lay.ramp_start[i + 1] - lay.ramp_start[i]);
+  const int bulk = lay.n_vtiles - lay.ramp_start[lay.n_ramp];
+  a->stride_full = golden_stride_public(lay.tiles_per_chunk);
+  a->stride_last = golden_stride_public(bulk - (lay.n_chunks - lay.n_ramp - 1) * lay.tiles_per_chunk);
 }
 
 // completion tiles: fp16 S-only configurations, 16 epilogue warps
