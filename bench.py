@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rapid", action="store_true",
+                    help="skip the RapidPT config-5 max-null timing (N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work for the cpu_baseline sample")
     return ap.parse_args()
@@ -75,7 +77,34 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self) -> bool:
+        """Poll NVML every 10 ms (the timed region of a step is ~35 ms)."""
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return False
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = get_reasons(h)
+                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.rows.append([str(self.idx), str(sm), str(mx), f"{pw:.1f}", hex(rs)] +
+                                 ["Active" if rs & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+        return True
+
     def _run(self):
+        if self._run_nvml():
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -111,6 +140,45 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(self.rows)}
+
+
+def rapid_block(device):
+    """RapidPT max-null wall time at BASELINE.json config 5 (n = 400 (120/280),
+    v = 524,288, L = 1e5, eta = 0.35 %, r = l = n, 50 GROUSE passes) through the
+    public run_rapid API, inputs already on the host as numpy (float32-valued X):
+    training (exact training columns, GROUSE, sigma / mu) + recovery (device
+    Omega draws and statistics, tensor-core LS + fp64 refinement, tcgen05
+    completion with Philox residuals).  A small warm-up run first loads the
+    kernels.  One timed run (~17 s)."""
+    import torch
+
+    import paper_1703_01506_b200 as rmx
+    from paper_1703_01506_b200.datagen import CONFIGS, make_data_torch, scaled
+
+    def one(cfg0, L, passes):
+        x = rmx.DataMatrix(make_data_torch(cfg0, device).to(torch.float32).cpu().numpy(),
+                           cfg0.n1, cfg0.n2)
+        rc = rmx.RunConfig(permutations=L, seed=cfg0.plan_seed, engine="rapid",
+                           training_columns=cfg0.training_columns, rank=cfg0.rank,
+                           sample_rate=cfg0.sample_rate, max_passes=passes)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        null, model, counters = rmx.run_rapid(x, rc)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, null, model, counters, x
+
+    cfg5 = CONFIGS["c5"]
+    one(scaled(cfg5, (64, 64, 32), 2048), 2048, 1)  # warm-up: kernels, cuBLAS handles
+    dt, null, model, counters, x = one(cfg5, cfg5.permutations, 50)
+    L, v = cfg5.permutations, x.voxels
+    return {"config": "c5: RapidPT n=400 (120/280) v=524288 L=100000 eta=0.35% r=400 "
+                      "l=400, 50 GROUSE passes",
+            "max_null_s": dt, "train_s": counters["train_seconds"],
+            "recover_s": counters["recover_seconds"],
+            "value": L * v / dt, "unit": "T-entries/s (L x v / max-null wall time)",
+            "statistic_evaluations": counters["statistic_evaluations"],
+            "sigma": model.residual_std, "mu": model.max_shift,
+            "api": "paper_1703_01506_b200.run_rapid (host numpy in, MaxNull out)"}
 
 
 def cpu_sample(cfg, x_host, orders_host, seconds: float, threads: int):
@@ -376,6 +444,14 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"failed: {exc}"}
 
+    # ---------------- RapidPT, config 5 (N=1; training is not sharded) -------
+    rapid = None
+    if rank == 0 and world == 1 and not args.no_rapid:
+        try:
+            rapid = rapid_block(device)
+        except Exception as exc:
+            rapid = {"failed": str(exc)[:200]}
+
     if rank == 0:
         stats = sh.job.stats.as_dict() if sh.job else {}
         line = {
@@ -399,6 +475,7 @@ def main():
                           "finish+gather": sum(fin_ms) / len(fin_ms)},
             "engine": stats,
             "label_gen_s": label_gen_s,
+            "rapid": rapid,
         }
         print(json.dumps(line))
     if world > 1:

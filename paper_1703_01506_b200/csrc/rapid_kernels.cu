@@ -437,37 +437,82 @@ __device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank,
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
 
-// Sum of (a, b) over the cluster, identical bits on every CTA (fixed order).
-// slots: this CTA's [kCgCtas][2] landing area for one all-reduce.
-__device__ __forceinline__ void cg_allreduce2(double a, double b, double* slots, double* wsum,
-                                              double& A, double& B) {
+
+// Pipelined preconditioned CG (Ghysels & Vanroose, p-PCG): besides x, r,
+// u = M r and w = A u, the recurrences carry m = M w, n = A m, z, q, s, p, so
+// an iteration needs ONE matrix-vector product (n = A m) and ONE global
+// reduction (r.u, w.u, r.r), and both exchanges -- m's rows for the product
+// and the three partial dot products -- are posted to every CTA of the
+// cluster before a single cluster barrier (DSMEM, double-buffered by
+// iteration parity: a CTA can be at most one barrier ahead of another).  The
+// classic PCG needed three barriers per iteration.  The stopping test uses
+// the recurrence residual; the result is then checked against the true
+// residual b - A x, and flag = 1 (Cholesky fallback) when that check or the
+// iteration cap fails.
+__device__ __forceinline__ void cg_block_reduce3(double a, double b, double c, double* wsum,
+                                                 double& A, double& B, double& C) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
     b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
   }
   if (lane == 0) {
-    wsum[2 * wid] = a;
-    wsum[2 * wid + 1] = b;
+    wsum[3 * wid] = a;
+    wsum[3 * wid + 1] = b;
+    wsum[3 * wid + 2] = c;
   }
   __syncthreads();
+  A = B = C = 0.0;
+  for (int w = 0; w < kCgThreads / 32; ++w) {
+    A += wsum[3 * w];
+    B += wsum[3 * w + 1];
+    C += wsum[3 * w + 2];
+  }
+}
+
+// Post this CTA's rows of `v` (nr values) into every CTA's `full` and this
+// CTA's totals (a, b, c) into every CTA's slot row `me`, then one cluster
+// barrier; returns the cluster sums (same order, same bits on every CTA).
+__device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, double* full,
+                                            double a, double b, double c, double* slots,
+                                            double* wsum, double& A, double& B, double& C) {
   const uint32_t me = cluster_ctarank();
-  if (threadIdx.x < kCgCtas) {
-    double ta = 0.0, tb = 0.0;
-    for (int w = 0; w < kCgThreads / 32; ++w) {
-      ta += wsum[2 * w];
-      tb += wsum[2 * w + 1];
+  double ta, tb, tc;
+  cg_block_reduce3(a, b, c, wsum, ta, tb, tc);
+  const int tid = threadIdx.x;
+  if (v)
+    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
+      const int i = e % nr, dst = e / nr;
+      st_cluster_f64(full + r0 + i, dst, v[i]);
     }
-    st_cluster_f64(slots + 2 * me, threadIdx.x, ta);
-    st_cluster_f64(slots + 2 * me + 1, threadIdx.x, tb);
+  if (tid < kCgCtas) {
+    st_cluster_f64(slots + 3 * me, tid, ta);
+    st_cluster_f64(slots + 3 * me + 1, tid, tb);
+    st_cluster_f64(slots + 3 * me + 2, tid, tc);
   }
   cluster_sync();
-  A = 0.0;
-  B = 0.0;
+  A = B = C = 0.0;
   for (int q = 0; q < kCgCtas; ++q) {
-    A += slots[2 * q];
-    B += slots[2 * q + 1];
+    A += slots[3 * q];
+    B += slots[3 * q + 1];
+    C += slots[3 * q + 2];
   }
+  __syncthreads();  // wsum reusable
+}
+
+// out[i] = G_rows[i] . full (one warp per row)
+__device__ __forceinline__ void cg_matvec(const double* Gs, int nr, int r, const double* full,
+                                          double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = wid; i < nr; i += kCgThreads / 32) {
+    const double* gi = Gs + (size_t)i * r;
+    double acc = 0.0;
+    for (int j = lane; j < r; j += 32) acc = fma(gi[j], full[j], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[i] = acc;
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
@@ -480,106 +525,111 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   const uint32_t me = cluster_ctarank();
   const int r0 = (int)me * R, nr = max(0, min(R, r - r0));
   double* Gs = cs;                       // nr x r
-  double* pfull = Gs + (size_t)R * r;    // r
-  double* vec = pfull + r;               // 5 x R: x, res, z, p, q (local rows)
-  double* x = vec, *res = vec + R, *z = vec + 2 * R, *p = vec + 3 * R, *q = vec + 4 * R;
-  double* dinv = vec + 5 * R;            // R
-  double* slots = dinv + R;              // 3 all-reduce landing areas x [kCgCtas][2]
-  double* wsum = slots + 6 * kCgCtas;    // 2 x warps
+  double* full = Gs + (size_t)R * r;     // 2 x r: exchanged vector, by parity
+  double* vec = full + 2 * (size_t)r;    // 11 x R local rows
+  double *x = vec, *rv = vec + R, *u = vec + 2 * R, *w = vec + 3 * R, *m = vec + 4 * R,
+         *nv = vec + 5 * R, *z = vec + 6 * R, *q = vec + 7 * R, *sv = vec + 8 * R,
+         *p = vec + 9 * R, *dinv = vec + 10 * R;
+  double* slots = vec + 11 * R;          // 2 x kCgCtas x 3 partials, by parity
+  double* wsum = slots + 6 * kCgCtas;    // 3 x warps
   const int ld = r + 1;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   for (int e = tid; e < nr * r; e += kCgThreads) {
     const int i = e / r, j = e % r;
     Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
   }
+  double pb = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
     const double di = G[(int64_t)(r0 + i) * ld + r0 + i];
     dinv[i] = di > 0.0 ? 1.0 / di : 1.0;
     x[i] = x0 ? x0[r0 + i] : 0.0;
-    q[i] = 0.0;
-  }
-  if (x0) {  // warm start (the column's solution from the previous pass): q = G x0
-    __syncthreads();
-    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
-      const int i = e % nr, dst = e / nr;
-      st_cluster_f64(pfull + r0 + i, dst, x[i]);
-    }
-    cluster_sync();
-    for (int i = wid; i < nr; i += kCgThreads / 32) {
-      const double* gi = Gs + (size_t)i * r;
-      double acc = 0.0;
-      for (int j = lane; j < r; j += 32) acc = fma(gi[j], pfull[j], acc);
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) q[i] = acc;
-    }
-    __syncthreads();
-  }
-  double pb = 0.0, pz = 0.0, pr = 0.0;
-  for (int i = tid; i < nr; i += kCgThreads) {
     const double bi = G[(int64_t)r * ld + r0 + i];
-    res[i] = bi - q[i];
-    z[i] = res[i] * dinv[i];
-    p[i] = z[i];
+    rv[i] = bi;
     pb += bi * bi;
-    pz += res[i] * z[i];
-    pr += res[i] * res[i];
+    z[i] = q[i] = sv[i] = p[i] = 0.0;
   }
-  double bb, rz, rr0 = 0.0, dummy0;
-  cg_allreduce2(pb, pz, slots, wsum, bb, rz);
-  if (x0) cg_allreduce2(pr, 0.0, slots + 2 * kCgCtas, wsum, rr0, dummy0);
-  const double stop = tol * tol * bb;
-  int converged = bb == 0.0 || (x0 && rr0 <= stop);
+  __syncthreads();
+  int par = 0;
+  double BB, d0, d1;
+  if (x0) {  // r = b - A x0
+    cg_exchange(x, nr, r0, full + par * r, pb, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum, BB,
+                d0, d1);
+    cg_matvec(Gs, nr, r, full + par * r, nv);
+    for (int i = tid; i < nr; i += kCgThreads) rv[i] -= nv[i];
+    par ^= 1;
+    __syncthreads();
+  }
+  for (int i = tid; i < nr; i += kCgThreads) u[i] = rv[i] * dinv[i];
+  __syncthreads();
+  // w = A u (and |b|^2 when not yet reduced)
+  cg_exchange(u, nr, r0, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum,
+              d0, d1, d1);
+  if (!x0) BB = d0;
+  cg_matvec(Gs, nr, r, full + par * r, w);
+  par ^= 1;
+  const double stop = tol * tol * BB;
+  int converged = BB == 0.0;
+  double gamma_prev = 1.0, alpha_prev = 1.0;
   int it = 0;
   for (; it < r && !converged; ++it) {
-    // share this CTA's direction rows with every CTA
-    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
-      const int i = e % nr, dst = e / nr;
-      st_cluster_f64(pfull + r0 + i, dst, p[i]);
-    }
-    cluster_sync();
-    // q = G_rows p, one warp per row
-    for (int i = wid; i < nr; i += kCgThreads / 32) {
-      const double* gi = Gs + (size_t)i * r;
-      double acc = 0.0;
-      for (int j = lane; j < r; j += 32) acc = fma(gi[j], pfull[j], acc);
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) q[i] = acc;
-    }
-    __syncthreads();
-    double pq = 0.0;
-    for (int i = tid; i < nr; i += kCgThreads) pq += p[i] * q[i];
-    double PQ, dummy;
-    cg_allreduce2(pq, 0.0, slots + 2 * kCgCtas, wsum, PQ, dummy);
-    const double alpha = PQ != 0.0 ? rz / PQ : 0.0;
-    double prz = 0.0, prr = 0.0;
+    double pg = 0.0, pd = 0.0, pr = 0.0;
     for (int i = tid; i < nr; i += kCgThreads) {
-      x[i] = fma(alpha, p[i], x[i]);
-      res[i] = fma(-alpha, q[i], res[i]);
-      z[i] = res[i] * dinv[i];
-      prz += res[i] * z[i];
-      prr += res[i] * res[i];
+      pg += rv[i] * u[i];
+      pd += w[i] * u[i];
+      pr += rv[i] * rv[i];
+      m[i] = w[i] * dinv[i];
     }
-    double RZ, RR;
-    cg_allreduce2(prz, prr, slots + 4 * kCgCtas, wsum, RZ, RR);
+    double GAM, DEL, RR;
+    cg_exchange(m, nr, r0, full + par * r, pg, pd, pr, slots + par * 3 * kCgCtas, wsum, GAM, DEL,
+                RR);
+    const int used = par;
+    par ^= 1;  // every exchange flips the buffers (also on the way out)
     if (RR <= stop) {
       converged = 1;
       break;
     }
-    const double beta = rz != 0.0 ? RZ / rz : 0.0;
-    rz = RZ;
-    for (int i = tid; i < nr; i += kCgThreads) p[i] = fma(beta, p[i], z[i]);
+    cg_matvec(Gs, nr, r, full + used * r, nv);  // n = A m
+    double alpha, beta;
+    if (it == 0) {
+      beta = 0.0;
+      alpha = DEL != 0.0 ? GAM / DEL : 0.0;
+    } else {
+      beta = GAM / gamma_prev;
+      const double den = DEL - beta * GAM / alpha_prev;
+      alpha = den != 0.0 ? GAM / den : 0.0;
+    }
+    if (!(alpha == alpha) || alpha == 0.0) break;  // breakdown: not converged
+    gamma_prev = GAM;
+    alpha_prev = alpha;
+    for (int i = tid; i < nr; i += kCgThreads) {
+      z[i] = fma(beta, z[i], nv[i]);
+      q[i] = fma(beta, q[i], m[i]);
+      sv[i] = fma(beta, sv[i], w[i]);
+      p[i] = fma(beta, p[i], u[i]);
+      x[i] = fma(alpha, p[i], x[i]);
+      rv[i] = fma(-alpha, sv[i], rv[i]);
+      u[i] = fma(-alpha, q[i], u[i]);
+      w[i] = fma(-alpha, z[i], w[i]);
+    }
     __syncthreads();
   }
-  // outputs: w, (t.t - rhs.w, |w|^2, 1, 1), flag
-  double pw = 0.0, pbw = 0.0;
+  // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
+  cg_exchange(x, nr, r0, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum, d0, d1,
+              d1);
+  cg_matvec(Gs, nr, r, full + par * r, nv);
+  par ^= 1;
+  double ptr = 0.0, pw = 0.0, pbw = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
+    const double bi = G[(int64_t)r * ld + r0 + i];
+    const double ti = bi - nv[i];
+    ptr += ti * ti;
+    pw += x[i] * x[i];
+    pbw += bi * x[i];
     if (w_out) w_out[r0 + i] = x[i];
     if (x0) x0[r0 + i] = x[i];
-    pw += x[i] * x[i];
-    pbw += G[(int64_t)r * ld + r0 + i] * x[i];
   }
-  double WW, BW;
-  cg_allreduce2(pw, pbw, slots, wsum, WW, BW);  // slot 0 is free again here
+  double TR, WW, BW;
+  cg_exchange(nullptr, 0, r0, nullptr, ptr, pw, pbw, slots + par * 3 * kCgCtas, wsum, TR, WW, BW);
   if (me == 0 && tid == 0) {
     if (resid2) {
       resid2[0] = G[(int64_t)r * ld + r] - BW;
@@ -587,7 +637,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       resid2[2] = 1.0;
       resid2[3] = 1.0;
     }
-    if (flag) flag[0] = converged ? 0 : 1;
+    if (flag) flag[0] = (converged && (BB == 0.0 || TR <= 16.0 * stop)) ? 0 : 1;
   }
   cluster_sync();  // no CTA exits while others may still write into its smem
 }
@@ -1291,7 +1341,8 @@ cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, doubl
 
 size_t cg_smem_bytes(int r) {
   const int R = (r + kCgCtas - 1) / kCgCtas;
-  return ((size_t)R * r + r + 6 * (size_t)R + 6 * kCgCtas + 2 * (kCgThreads / 32)) * sizeof(double);
+  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * kCgCtas + 3 * (kCgThreads / 32)) *
+         sizeof(double);
 }
 
 bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }

@@ -1,10 +1,13 @@
 """Parallel host-side draws from the reference's RNG streams.
 
-numpy's Generator holds the GIL while it fills arrays, so threads do not
-scale; a process pool scales but pickling hundreds of MB back costs more
-than the draws.  Here forked workers write their rows straight into an
-anonymous shared mapping created before the fork.  Each row comes from its
-own ``stream(seed, *path)``, so the result is identical to a serial loop.
+Each row comes from its own ``stream(seed, *path)``, so any parallel order
+gives the result of a serial loop.  Long rows (e.g. v normals per row) go to
+a thread pool: numpy releases the GIL while it fills an array, and threads
+need no fork -- forking a process that holds page-locked (cudaHostRegister)
+buffers makes the kernel copy those pages eagerly into every child.  Short
+rows (a permutation of n subjects: the per-row cost is Python-level stream
+construction under the GIL) go to forked workers writing into an anonymous
+shared mapping created before the fork.
 """
 
 from __future__ import annotations
@@ -15,6 +18,7 @@ import os
 import numpy as np
 
 _MIN_PARALLEL_ROWS = 64
+_THREAD_ROW_ELEMS = 1 << 16
 
 
 def fill_rows(shape, dtype, row_fn, nrows: int, workers: int | None = None) -> np.ndarray:
@@ -23,6 +27,18 @@ def fill_rows(shape, dtype, row_fn, nrows: int, workers: int | None = None) -> n
     out_shape = (nrows,) + tuple(shape)
     nbytes = int(np.prod(out_shape)) * np.dtype(dtype).itemsize
     workers = workers or min(os.cpu_count() or 1, 32)
+    row_elems = int(np.prod(shape)) if len(shape) else 1
+    if workers > 1 and nrows > 1 and row_elems >= _THREAD_ROW_ELEMS:
+        from concurrent.futures import ThreadPoolExecutor
+
+        out = np.empty(out_shape, dtype=dtype)
+
+        def one(i):
+            out[i] = row_fn(i)
+
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(one, range(nrows)))
+        return out
     if workers <= 1 or nrows < _MIN_PARALLEL_ROWS or not hasattr(os, "fork") or nbytes == 0:
         out = np.empty(out_shape, dtype=dtype)
         for i in range(nrows):

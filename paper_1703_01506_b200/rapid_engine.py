@@ -57,7 +57,7 @@ from .exceptions import (
     UsageError,
 )
 from .labels import device_orders, plan_orders
-from .naive_engine import cuda_device, resolve_threads, tstat_exact_device
+from .naive_engine import cuda_device, data_to_device, resolve_threads, tstat_exact_device
 from .rng import BASIS_INIT, RECOVER_OMEGA, SHIFT_GAP, TRAIN_OMEGA, omega_draw, stream
 
 COND_LIMIT = 1e12
@@ -272,12 +272,43 @@ class TrainingResult:
         self.converged = converged
 
 
+def _basis_init_async(seed: int, v: int, rank: int):
+    """Start drawing init_basis's normals (lrmc.py:85-93: ONE sequential
+    stream(seed, BASIS_INIT) of v x rank doubles, ~2-3 s of host time at
+    config 5) on a background thread -- numpy releases the GIL while it fills
+    the array -- so that the X upload, the training columns and the Omega
+    draws run on the GPU meanwhile.  Returns a callable that joins."""
+    import threading
+
+    box = {}
+
+    def work():
+        try:
+            box["a"] = stream(seed, BASIS_INIT).standard_normal((v, rank))
+        except BaseException as exc:  # re-raised by the joiner
+            box["e"] = exc
+
+    th = threading.Thread(target=work, name="rmx-basis-init", daemon=True)
+    th.start()
+
+    def join():
+        th.join()
+        if "e" in box:
+            raise box["e"]
+        return box.pop("a")
+
+    return join
+
+
 def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
-                        max_passes: int, tolerance: float):
-    """GROUSE on device.  t_dev: (ell, v) fp64 training statistics."""
+                        max_passes: int, tolerance: float, init=None):
+    """GROUSE on device.  t_dev: (ell, v) fp64 training statistics; init: a
+    joiner from _basis_init_async (else the normals are drawn here)."""
     torch = _torch()
     dev = t_dev.device
-    u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, rank)), dev)
+    normals = init() if init is not None else stream(seed, BASIS_INIT).standard_normal((v, rank))
+    u = _to_dev(normals, dev)
+    del normals
     _orthonormalize(u, force=True)
     om_dev = torch.empty((max_passes, ell, k), dtype=torch.int32, device=dev)
     for p in range(max_passes):  # stream(seed, TRAIN_OMEGA, i, p), drawn on the GPU
@@ -333,11 +364,12 @@ def _train_device(x, cfg):
     k = observed_rows(cfg.sample_rate, v)
     plan = cfg.plan_for(x)
     dev = cuda_device()
-    xd = _to_dev(x.values, dev)
+    init = _basis_init_async(cfg.seed, v, rank)         # host, overlapped with the GPU work below
+    xd = data_to_device(x, dev)
     od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
     u, final, passes, conv, _, _ = _train_basis_device(t_dev, v, ell, k, rank, cfg.seed,
-                                                       cfg.max_passes, cfg.tolerance)
+                                                       cfg.max_passes, cfg.tolerance, init)
     # fits of the frozen basis on the final pass's observed rows (rapid.py:90-97)
     vals = torch.empty((ell, k), dtype=torch.float64, device=dev)
     nat.call("rmx_gather_rows", nat.ptr(t_dev), v, nat.ptr(final), k, ell, nat.ptr(vals),
@@ -417,7 +449,7 @@ def recover(x, model: SubspaceModel, plan, cfg):
     maxima = np.empty(L, dtype=np.float64)
     maxima[:ell] = model.training_maxima
     nrec = L - ell
-    xd = _to_dev(x.values, dev)
+    xd = data_to_device(x, dev)
     od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
     omd = device_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k, dev)
     t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
