@@ -23,7 +23,8 @@
  *        RMX_OK 0, RMX_E_USAGE 1 -> UsageError,
  *        RMX_E_DEGENERATE 2 -> DegenerateVoxelError(voxel, value = mean_diff),
  *        RMX_E_ILLCOND 3 -> IllConditionedBasisError(value = cond),
- *        RMX_E_CUDA 4 / RMX_E_NUMERIC 5 -> NumericalError.
+ *        RMX_E_CUDA 4 / RMX_E_NUMERIC 5 -> NumericalError,
+ *        RMX_E_FORMAT 6 -> DataFormatError, RMX_E_IO 7 -> OSError.
  */
 #ifndef RMX_H_
 #define RMX_H_
@@ -41,6 +42,8 @@ extern "C" {
 #define RMX_E_ILLCOND 3
 #define RMX_E_CUDA 4
 #define RMX_E_NUMERIC 5
+#define RMX_E_FORMAT 6 /* -> DataFormatError (a malformed .mat0 payload) */
+#define RMX_E_IO 7     /* -> OSError (open / read / write failed) */
 
 #define RMX_ABI_VERSION 1
 
@@ -168,6 +171,31 @@ int rmx_naive_maxnull_host_plan_f32(const float *x_host, int64_t v, int32_t n, i
                                     double *x_dev, int16_t *orders_dev, double *max_dev,
                                     int32_t *argmax_dev, void *workspace, size_t workspace_bytes,
                                     void *stream, rmx_status *st, rmx_naive_stats *stats);
+
+/* ---------------------------------------------------------------- .mat0 I/O
+ * The reference's binary matrix format (matio.py:23-91): 44-byte header
+ * "<8sIQQQQ" = magic "RMXMAT0\0", u32 version (1), u64 rows, cols, n1, n2;
+ * then rows x cols little-endian float64, row-major.  Host-side only. */
+typedef struct rmx_mat0_info {
+  char magic[8];
+  uint32_t version;
+  uint32_t _pad;
+  int64_t rows, cols, n1, n2;
+  int64_t header_bytes; /* bytes of header present (< 44: truncated) */
+  int64_t file_bytes;
+} rmx_mat0_info;
+/* Raw header fields and file size (validation and the reference's messages
+ * are the caller's: matio.py).  Replaces reference matio.py:40-57. */
+int rmx_mat0_header(const char *path, rmx_mat0_info *info, rmx_status *st);
+/* rows x cols payload -> out (any host buffer, e.g. page-locked), read by
+ * `threads` parallel positional reads, scanned for non-finite values in the
+ * same pass: RMX_E_FORMAT with *bad_index = first non-finite element (flat
+ * index).  Replaces reference matio.py:58-72. */
+int rmx_mat0_read(const char *path, int64_t rows, int64_t cols, double *out, int32_t threads,
+                  int64_t *bad_index, rmx_status *st);
+/* Header + payload.  Replaces reference matio.py:30-37 write_array. */
+int rmx_mat0_write(const char *path, const double *a, int64_t rows, int64_t cols, int64_t n1,
+                   int64_t n2, rmx_status *st);
 
 /* The reference's random streams on the device, bit-identical to numpy:
  * row t of out (count x n, int16) = PermutationPlan(seed, ., n).shuffle(lo + t)

@@ -29,6 +29,15 @@ from .exceptions import (  # noqa: F401
     NumericalError,
     UsageError,
 )
+from .matfiles import (  # noqa: F401
+    load_matrix,
+    read_array,
+    read_matrix,
+    read_matrix_csv,
+    write_array,
+    write_matrix,
+    write_matrix_csv,
+)
 from .naive_engine import NaiveJob, NaiveResult, run_naive, run_naive_ex  # noqa: F401
 from .rapid_engine import (  # noqa: F401
     complete_column,
@@ -58,4 +67,6 @@ __all__ = [
     "run_naive", "run_naive_ex", "column_max", "pvalue", "reject_set", "stat_map",
     "threshold_at", "tstat_full", "tstat_subset", "complete_column", "fit_coefficients",
     "init_basis", "recover", "run_rapid", "solve_block", "train", "train_basis",
+    "load_matrix", "read_array", "read_matrix", "read_matrix_csv", "write_array", "write_matrix",
+    "write_matrix_csv",
 ]

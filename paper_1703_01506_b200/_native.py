@@ -13,6 +13,7 @@ import os
 import subprocess
 
 from .exceptions import (
+    DataFormatError,
     DegenerateVoxelError,
     EngineUnavailableError,
     IllConditionedBasisError,
@@ -24,7 +25,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "librmx.so")
 CSRC = os.path.join(_PKG, "csrc")
 
-RMX_OK, RMX_E_USAGE, RMX_E_DEGENERATE, RMX_E_ILLCOND, RMX_E_CUDA, RMX_E_NUMERIC = range(6)
+(RMX_OK, RMX_E_USAGE, RMX_E_DEGENERATE, RMX_E_ILLCOND, RMX_E_CUDA, RMX_E_NUMERIC, RMX_E_FORMAT,
+ RMX_E_IO) = range(8)
 
 
 class Status(ctypes.Structure):
@@ -55,6 +57,13 @@ class NaiveStats(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class Mat0Info(ctypes.Structure):
+    _fields_ = [("magic", ctypes.c_uint8 * 8), ("version", ctypes.c_uint32),
+                ("_pad", ctypes.c_uint32), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
+                ("header_bytes", ctypes.c_int64), ("file_bytes", ctypes.c_int64)]
 
 
 # Every symbol include/rmx.h declares (tests check the library exports them).
@@ -88,6 +97,9 @@ EXPORTS = (
     "rmx_mean_var",
     "rmx_orthonormalize",
     "rmx_grouse_train",
+    "rmx_mat0_header",
+    "rmx_mat0_read",
+    "rmx_mat0_write",
 )
 
 
@@ -131,6 +143,10 @@ _SIGS = {
                         ctypes.c_int),
     "rmx_rapid_stats": ([_vp, _i64, _i32, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
     "rmx_lsq_workspace_bytes": ([_i32, _i64], _sz),
+    "rmx_mat0_header": ([ctypes.c_char_p, ctypes.POINTER(Mat0Info), _SP], ctypes.c_int),
+    "rmx_mat0_read": ([ctypes.c_char_p, _i64, _i64, _vp, _i32, ctypes.POINTER(_i64), _SP],
+                      ctypes.c_int),
+    "rmx_mat0_write": ([ctypes.c_char_p, _vp, _i64, _i64, _i64, _i64, _SP], ctypes.c_int),
     "rmx_lsq_solve_tc": ([_vp, _i64, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp,
                           _SP], ctypes.c_int),
     "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],
@@ -190,6 +206,10 @@ def raise_for(rc: int, st: Status) -> None:
         raise DegenerateVoxelError(int(st.voxel), float(st.value))
     if rc == RMX_E_ILLCOND:
         raise IllConditionedBasisError(float(st.value))
+    if rc == RMX_E_FORMAT:
+        raise DataFormatError(msg)
+    if rc == RMX_E_IO:
+        raise OSError(msg)
     raise NumericalError(f"librmx error {rc}: {msg}")
 
 

@@ -206,7 +206,80 @@ def rapid():
     np.savez_compressed(os.path.join(HERE, "rapid_cases.npz"), **out)
 
 
+def matio():
+    """Files written by the reference's matio and the reference's error
+    messages for malformed files (path replaced by <PATH>)."""
+    import struct
+    import tempfile
+
+    from rapidmaxnull import matio as M
+
+    g = np.random.default_rng(7)
+    vals = g.standard_normal((7, 5))
+    vals[0, 0], vals[1, 1], vals[2, 2] = -0.0, 1e-300, 1.2345678901234567e300
+    x = R.DataMatrix(vals, 2, 3)
+    out = {"values": vals, "n1": 2, "n2": 3}
+    with tempfile.TemporaryDirectory() as d:
+        pb, pc = os.path.join(d, "x.mat0"), os.path.join(d, "x.csv")
+        M.write_matrix(x, pb)
+        M.write_matrix_csv(x, pc)
+        out["mat0_bytes"] = np.frombuffer(open(pb, "rb").read(), dtype=np.uint8)
+        out["csv_bytes"] = np.frombuffer(open(pc, "rb").read(), dtype=np.uint8)
+        good = open(pb, "rb").read()
+        hdr = struct.Struct("<8sIQQQQ")
+        nan = bytearray(good)
+        nan[44 + (3 * 5 + 4) * 8:44 + (3 * 5 + 5) * 8] = struct.pack("<d", float("nan"))
+        cases = {
+            "truncated_header": good[:20],
+            "bad_magic": b"RMXMAT1\x00" + good[8:],
+            "bad_version": good[:8] + struct.pack("<I", 2) + good[12:],
+            "empty_dims": hdr.pack(b"RMXMAT0\x00", 1, 0, 5, 2, 3),
+            "short_payload": good[:-8],
+            "long_payload": good + b"\x00" * 8,
+            "non_finite": bytes(nan),
+            "bare": hdr.pack(b"RMXMAT0\x00", 1, 7, 5, 0, 0) + good[44:],
+            "bad_split": hdr.pack(b"RMXMAT0\x00", 1, 7, 5, 1, 4) + good[44:],
+        }
+        names, msgs = [], []
+        for name, data in cases.items():
+            fp = os.path.join(d, name + ".mat0")
+            open(fp, "wb").write(data)
+            try:
+                M.read_matrix(fp)
+                msg = "OK"
+            except Exception as e:  # DataFormatError
+                msg = type(e).__name__ + ": " + str(e).replace(fp, "<PATH>")
+            names.append(name)
+            msgs.append(msg)
+            out["case_" + name] = np.frombuffer(data, dtype=np.uint8)
+        csv_cases = {
+            "csv_header": "1,2,3\n",
+            "csv_nonint": "a,b,c,d\n",
+            "csv_short": "3,2,1,1\n1,2\n3,4\n",
+            "csv_cells": "2,2,1,1\n1,2\n3\n",
+            "csv_cell": "2,2,1,1\n1,x\n3,4\n",
+            "csv_inf": "2,2,1,1\n1,inf\n3,4\n",
+            "csv_trailing": "1,4,2,2\n1,2,3,4\n5\n",
+            "csv_zero": "0,2,1,1\n",
+        }
+        for name, text in csv_cases.items():
+            fp = os.path.join(d, name + ".csv")
+            open(fp, "w").write(text)
+            try:
+                M.read_matrix_csv(fp)
+                msg = "OK"
+            except Exception as e:
+                msg = type(e).__name__ + ": " + str(e).replace(fp, "<PATH>")
+            names.append(name)
+            msgs.append(msg)
+            out["case_" + name] = np.frombuffer(text.encode(), dtype=np.uint8)
+    out["case_names"] = np.array(names)
+    out["case_msgs"] = np.array(msgs)
+    np.savez_compressed(os.path.join(HERE, "matio.npz"), **out)
+
+
 if __name__ == "__main__":
+    matio()
     shuffles()
     naive()
     c1()
