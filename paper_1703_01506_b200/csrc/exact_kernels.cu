@@ -199,43 +199,47 @@ constexpr int kPrepStages = 4;
 
 // One voxel row from shared memory, lane-contiguous mapping: lane owns the
 // subjects k = 4 lane + 128 g + e (g < G, e < 4), so the int8 digits (and
-// fp16 halves) of four consecutive subjects leave as one packed store.  Same
-// arithmetic as prep_row (explicit fma where an unfused product was not
-// needed); the quantisation bound is measured on the values actually stored.
+// fp16 halves) of four consecutive subjects leave as one packed store.
+// Constancy is tested against subject 0's value (one compare per element,
+// one vote).  int8 quantisation bound, with tq = z / inv (inv = zmax / 32512
+// the exact step, inv_f = fp32(inv) the step the epilogue uses) and
+// zq = rint(tq):
+//   |z - zq inv_f| <= |tq - zq| inv + |zq| |inv - inv_f|
+// so e_j = inv sum_i |tq_i - zq_i| + n 32512 |inv - inv_f| (each with a
+// 2^-40 relative margin for the fp64 roundings of z and tq) bounds
+// |S~ - S| for every grouping; the first sum is accumulated from the
+// rounding residuals tq - rint(tq) (two fp64 ops per element).
 template <int G>
 __device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane,
                                           const double* srow, double& err_max) {
   double d[G][4];
-  double s = 0.0, mn = DBL_MAX, mx = -DBL_MAX;
+  double s = 0.0;
+  const double x0 = srow[0];
+  bool varies = false;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int k0 = 4 * lane + 128 * g;
     if (k0 < a.n) {  // n even and k0 % 4 == 0: pairs are whole
       const double2 p0 = *reinterpret_cast<const double2*>(srow + k0);
       const double2 p1 = k0 + 2 < a.n ? *reinterpret_cast<const double2*>(srow + k0 + 2)
-                                      : make_double2(0.0, 0.0);
+                                      : make_double2(x0, x0);
       d[g][0] = p0.x;
       d[g][1] = p0.y;
       d[g][2] = p1.x;
       d[g][3] = p1.y;
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) d[g][e] = 0.0;
+      for (int e = 0; e < 4; ++e) d[g][e] = x0;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      if (k0 + e < a.n) {
-        s += d[g][e];
-        mn = fmin(mn, d[g][e]);
-        mx = fmax(mx, d[g][e]);
-      }
+      varies |= d[g][e] != x0;
+      if (k0 + e < a.n) s += d[g][e];
     }
   }
   s = warp_sum_d(s);
-  mn = warp_min_d(mn);
-  mx = warp_max_d(mx);
+  const bool constant = !__any_sync(0xffffffffu, varies);
   const double mean = s / a.n;
-  const bool constant = (mn == mx);
   double ss = 0.0;
 #pragma unroll
   for (int g = 0; g < G; ++g)
@@ -256,9 +260,9 @@ __device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane
     const double zmax = warp_max_d(dmax) * inv;
     const double scale = zmax > 0.0 ? 32512.0 / zmax : 0.0;
     const float inv_f = zmax > 0.0 ? (float)(zmax / 32512.0) : 0.0f;
-    const double c = inv * scale, inv_d = (double)inv_f;
+    const double c = inv * scale;  // zq = rint(d c); |d c| <= 32512 (+ rounding < 0.5)
     int8_t* p8 = reinterpret_cast<int8_t*>(a.planes8) + j * (int64_t)(2 * a.kpad);
-    double err = 0.0;  // sum_i |z_i - dequantised z_i|: bounds |S~ - S| for any grouping
+    double fr = 0.0;  // sum of |tq - rint(tq)|
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int k0 = 4 * lane + 128 * g;
@@ -266,8 +270,10 @@ __device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane
       uint32_t hw = 0u, lw = 0u;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int zq = min(32512, max(-32512, __double2int_rn(d[g][e] * c)));
-        err += fabs(fma(-(double)zq, inv_d, d[g][e] * inv));
+        const double tq = d[g][e] * c;
+        const double rq = rint(tq);
+        fr += fabs(tq - rq);
+        const int zq = (int)rq;
         const int h = __float2int_rn((float)zq * (1.0f / 255.0f));  // |zq/255 - h| <= 0.498
         hw |= (uint32_t)(uint8_t)(int8_t)h << (8 * e);
         lw |= (uint32_t)(uint8_t)(int8_t)(zq - 255 * h) << (8 * e);
@@ -275,8 +281,13 @@ __device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane
       *reinterpret_cast<uint32_t*>(p8 + k0) = hw;
       *reinterpret_cast<uint32_t*>(p8 + a.kpad + k0) = lw;
     }
-    err = warp_sum_d(err);
-    err_max = fmax(err_max, err);
+    fr = warp_sum_d(fr);
+    if (!constant) {
+      const double step = zmax / 32512.0;
+      const double e = (step * fr + (double)a.n * 32512.0 * fabs(step - (double)inv_f)) *
+                       (1.0 + 0x1p-40);
+      err_max = fmax(err_max, e);
+    }
     if (lane == 0) a.inv_scale[j] = inv_f;
   } else {
     const int64_t plane = a.v * (int64_t)a.kpad;
@@ -304,7 +315,7 @@ __device__ __forceinline__ void prep_row4(const PrepArgs& a, int64_t j, int lane
     }
   }
   if (constant && lane == 0) {
-    const WelchExact w = welch_exact_const(mn, a.n1, a.n - a.n1);
+    const WelchExact w = welch_exact_const(x0, a.n1, a.n - a.n1);
     if (w.t != 0.0 || w.degenerate) {
       unsigned slot = atomicAdd(&a.counters->cvox_count, 1u);
       a.cvox[slot] = (int32_t)j;

@@ -201,7 +201,7 @@ __device__ __forceinline__ void chol_block32(double* D, double* rinv, double tin
 __host__ __device__ constexpr int chol_panel_rows(int r) { return r > kPW ? r - kPW : 1; }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_chol_solve(double* __restrict__ G, int r,
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
                                                    int32_t* flag, double* __restrict__ resid2,
                                                    const int32_t* gate = nullptr,
