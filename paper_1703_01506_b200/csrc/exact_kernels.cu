@@ -441,11 +441,23 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
   double* rowbuf = reinterpret_cast<double*>(rest) + (size_t)w * (STAGE ? a.n : 0);
   int16_t* ord = reinterpret_cast<int16_t*>(rest + (STAGE ? (size_t)kRefineWarps * a.n * 8 : 0)) +
                  (size_t)w * a.n;
+  // leaf plans of the two group sizes, once per block (welch_exact_warp2)
+  unsigned char* tail = rest + (STAGE ? (size_t)kRefineWarps * a.n * 8 : 0) +
+                        (size_t)kRefineWarps * a.n * sizeof(int16_t);
+  NpLeafPlan* plans = reinterpret_cast<NpLeafPlan*>(
+      (reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  double* pvals = reinterpret_cast<double*>(plans + 2) + (size_t)w * 2 * NpWarpScratch::kMaxLeaves;
+  const int n2 = a.n - a.n1;
+  const bool two_pass = a.n1 <= NpWarpScratch::kMaxTerms && n2 <= NpWarpScratch::kMaxTerms;
+  if (two_pass) {
+    if (threadIdx.x == 0) np_leaf_plan(a.n1, &plans[0]);
+    if (threadIdx.x == 32 % blockDim.x) np_leaf_plan(n2, &plans[1]);
+  }
+  __syncthreads();
   const int64_t p = (int64_t)blockIdx.x * kRefineWarps + w;
   if (p >= a.L) return;
   for (int i = lane; i < a.n; i += 32) ord[i] = a.orders[p * a.n + i];
   __syncwarp();
-  const int n2 = a.n - a.n1;
   const int4* cp = a.cand + 2 * p * a.slots;
 
   float tmax = -FLT_MAX;
@@ -471,7 +483,8 @@ __global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
       __syncwarp();
       row = rowbuf;
     }
-    const WelchExact r = welch_exact_warp(row, 1, ord, a.n1, n2, sc);
+    const WelchExact r = two_pass ? welch_exact_warp2(row, ord, plans[0], plans[1], pvals)
+                                  : welch_exact_warp(row, 1, ord, a.n1, n2, sc);
     if (lane == owner) {
       ++nref;
       if (r.degenerate) {
@@ -734,7 +747,9 @@ cudaError_t launch_const_reduce(const double* x, int64_t, int n, int n1, const i
 
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t s) {
   const int64_t blocks = (a.L + kRefineWarps - 1) / kRefineWarps;
-  const size_t scratch = kRefineWarps * sizeof(NpWarpScratch);
+  // per-warp scratch + leaf plans (2) and per-warp leaf sums (welch_exact_warp2)
+  const size_t scratch = kRefineWarps * sizeof(NpWarpScratch) + 16 + 2 * sizeof(NpLeafPlan) +
+                         (size_t)kRefineWarps * 2 * NpWarpScratch::kMaxLeaves * sizeof(double);
   if (a.n <= kStageMaxN) {
     const size_t smem = scratch + (size_t)kRefineWarps * a.n * (sizeof(int16_t) + sizeof(double));
     if (smem > 48 * 1024) {
