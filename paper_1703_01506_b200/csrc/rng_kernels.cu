@@ -156,6 +156,45 @@ __global__ void k_plan_orders(uint64_t seed, int64_t lo, int64_t count, int n, i
   }
 }
 
+// The same with the rows shuffled in shared memory (the swaps of a
+// Fisher-Yates pass are dependent, random accesses: in global memory they
+// thrash L1 and serialise on L2 latency), then written out coalesced: the
+// block's kPlanRows rows are contiguous in `out`.
+constexpr int kPlanRows = 64;
+__global__ void __launch_bounds__(kPlanRows) k_plan_orders_smem(uint64_t seed, int64_t lo,
+                                                                int64_t count, int n,
+                                                                int16_t* out) {
+  extern __shared__ __align__(16) int16_t prow[];
+  const int64_t t0 = (int64_t)blockIdx.x * kPlanRows;
+  const int rows = (int)(count - t0 < kPlanRows ? count - t0 : kPlanRows);
+  int16_t* row = prow + (size_t)threadIdx.x * n;
+  if ((int)threadIdx.x < rows) {
+    for (int i = 0; i < n; ++i) row[i] = (int16_t)i;
+    const int64_t index = lo + t0 + threadIdx.x;
+    if (index != 0) {
+      const uint32_t key[2] = {1u /* SHUFFLE */, (uint32_t)index};
+      Sfc64 g;
+      sfc64_seed(g, seed, key, 2);
+      for (int i = n - 1; i > 0; --i) {
+        const int j = (int)random_interval32(g, (uint32_t)i);
+        const int16_t tmp = row[i];
+        row[i] = row[j];
+        row[j] = tmp;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t elems = (int64_t)rows * n;
+  int16_t* dst = out + t0 * n;
+  if (((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)(elems * 2)) & 15) == 0) {
+    const uint4* src4 = reinterpret_cast<const uint4*>(prow);
+    uint4* dst4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t e = threadIdx.x; e < elems / 8; e += kPlanRows) dst4[e] = src4[e];
+  } else {
+    for (int64_t e = threadIdx.x; e < elems; e += kPlanRows) dst[e] = prow[e];
+  }
+}
+
 // one warp per observation set: lane 0 runs Floyd's sampling with numpy's
 // open-addressing set (smem), then the warp bitonic-sorts the k values
 constexpr int kOmegaWarps = 4;
@@ -221,6 +260,17 @@ __global__ void __launch_bounds__(32 * kOmegaWarps)
 cudaError_t launch_plan_orders(uint64_t seed, int64_t lo, int64_t count, int n, int16_t* out,
                                cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
+  const size_t smem = (size_t)kPlanRows * n * sizeof(int16_t);
+  if (smem <= 160 * 1024) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_plan_orders_smem,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_plan_orders_smem<<<(unsigned)((count + kPlanRows - 1) / kPlanRows), kPlanRows, smem, s>>>(
+        seed, lo, count, n, out);
+    return cudaGetLastError();
+  }
   k_plan_orders<<<(unsigned)((count + 127) / 128), 128, 0, s>>>(seed, lo, count, n, out);
   return cudaGetLastError();
 }
