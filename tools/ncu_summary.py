@@ -18,15 +18,20 @@ def run(args):
     return subprocess.run(["ncu", "-i"] + args, capture_output=True, text=True).stdout
 
 
-def main(rep, top=25):
+def main(rep, top=25, kernel=None):
     rows = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    pick = [r for r in rows[2:] if kernel is None or kernel in r[ki]]
+    vals = pick[0]
     print(f"# {rep}")
     print(f"kernel: {vals[hdr.index('Kernel Name')][:120]}")
     for k in KEYS:
         for i, h in enumerate(hdr):
             if h.endswith(k):
                 print(f"{k} = {vals[i]} {units[i]}")
+    if kernel is not None:
+        return  # per-kernel source pages of multi-kernel reports: capture separately
     src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv"]))))
     h = src[1]
     isrc, iall, iex = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), \
@@ -40,4 +45,5 @@ def main(rep, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25,
+         sys.argv[3] if len(sys.argv) > 3 else None)
