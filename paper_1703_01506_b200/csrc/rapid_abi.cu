@@ -58,10 +58,10 @@ struct Blas {
   }
   // C (m x n, ldc) = A (m x kk, lda) B (kk x n, ldb)
   cublasStatus_t gemm_rm(int64_t m, int n, int kk, const double* A, int64_t lda, const double* B,
-                         int64_t ldb, double* C, int64_t ldc) const {
-    const double one = 1.0, zero = 0.0;
+                         int64_t ldb, double* C, int64_t ldc, double beta = 0.0) const {
+    const double one = 1.0;
     return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)m, kk, &one, B, (int)ldb, A, (int)lda,
-                       &zero, C, (int)ldc);
+                       &beta, C, (int)ldc);
   }
   // G (n x n, row- or column-major: symmetric) = A^T A, A (rows x n, lda)
   cublasStatus_t gram(int64_t rows, int n, const double* A, int64_t lda, double* G) const {
@@ -343,8 +343,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // sums: 0 |r|^2 1 |p|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
-  DevBuf<double> G, w, vals, resid, sums, wn, ug, ubuf, ub2, M, cmat, dval, H, hg, hdrift, hw, mw,
-      dots, wprev;
+  DevBuf<double> G, w, vals, resid, sums, wn, ug, ub2, M, cmat, dval, H, hg, hdrift, hw, mw,
+      dots, wprev, Xf, Yf, tk;
   DevBuf<int32_t> flag, idxbuf, didx;
   DevBuf<GrouseState> gst;
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
@@ -357,12 +357,14 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(idxbuf.alloc(k, s));
   const int64_t lu = r + 1;  // ug rows: [U_Omega row | t_Omega] (the Gram's operand)
   RCUDA(ug.alloc((size_t)k * lu, s));
-  RCUDA(ubuf.alloc((size_t)k * r, s));
   Blas blas;
   RBLAS(cublasCreate(&blas.h));
   RBLAS(cublasSetStream(blas.h, s));
-  RCUDA(ub2.alloc((size_t)v * r, s));
+  RCUDA(ub2.alloc((size_t)v * kDeferCap, s));  // T = U_base X (flush)
   RCUDA(M.alloc((size_t)r * r, s));
+  RCUDA(Xf.alloc((size_t)r * kDeferCap, s));
+  RCUDA(Yf.alloc((size_t)kDeferCap * r, s));
+  RCUDA(tk.alloc((size_t)k * kDeferCap, s));
   RCUDA(cmat.alloc((size_t)kDeferCap * r, s));
   RCUDA(dval.alloc((size_t)kDeferCap * k, s));
   RCUDA(didx.alloc((size_t)kDeferCap * k, s));
@@ -382,20 +384,23 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(cudaMemsetAsync(wprev.p, 0, (size_t)ell * r * sizeof(double), s));
   }
   RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(GrouseState), s));
-  RCUDA(launch_flush_reset(M.p, r, gst.p, s));  // M = I, no terms
+  RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));  // M = I, X = Y = 0, no terms
   RCUDA(launch_h_identity(H.p, r, s));          // the caller hands in an orthonormalised U
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
   const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
-  // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE);
-  // ubase alternates between the caller's u and ub2 at every flush
+  // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE),
+  // M = I + X Y^T with one column of X / row of Y^T per deferred update
+  // (k_defer_apply): the flush U <- U M + terms is U += (U X) Y^T in place
+  // (4 v r nt flops instead of 2 v r^2), the per-update gather likewise.
   double* ubase = u;
-  double* uother = ub2.p;
-  auto flush = [&]() -> int {
-    RBLAS(blas.gemm_rm(v, r, r, ubase, r, M.p, r, uother, r));
-    RCUDA(launch_sparse_terms(uother, r, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
-    std::swap(ubase, uother);
-    RCUDA(launch_flush_reset(M.p, r, gst.p, s));
+  auto flush = [&](int nt) -> int {
+    if (nt > 0) {
+      RBLAS(blas.gemm_rm(v, nt, r, ubase, r, Xf.p, kDeferCap, ub2.p, kDeferCap));
+      RBLAS(blas.gemm_rm(v, r, nt, ub2.p, kDeferCap, Yf.p, r, ubase, r, 1.0));
+    }
+    RCUDA(launch_sparse_terms(ubase, r, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
+    RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));
     return RMX_OK;
   };
   // One update, entirely on the device (lrmc.py:160-193): the Omega rows of
@@ -406,8 +411,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
     const double* trow = t + (int64_t)i * v;
-    RCUDA(launch_gather_urows(ubase, r, idx, k, ubuf.p, s));
-    RBLAS(blas.gemm_rm(k, r, r, ubuf.p, r, M.p, r, ug.p, lu));
+    // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
+    RCUDA(launch_gather_urows_ld(ubase, r, idx, k, ug.p, lu, s));
+    RBLAS(blas.gemm_rm(k, kDeferCap, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap));
+    RBLAS(blas.gemm_rm(k, r, kDeferCap, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1.0));
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
     RCUDA(launch_gather_vals_aug(trow, idx, k, vals.p, ug.p + r, lu, s));
     RBLAS(blas.gram(k, (int)lu, ug.p, lu, G.p));
@@ -426,7 +433,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                                final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));
     RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, lu, k, vals.p, resid.p, sums.p, hg.p,
                           s));
-    RCUDA(launch_defer_apply(M.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r, s));
+    RCUDA(launch_defer_apply(M.p, Xf.p, Yf.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r,
+                             s));
     (void)p;
     return RMX_OK;
   };
@@ -475,7 +483,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       continue;
     }
     if (reortho) {  // at most kDeferCap deferred terms: rewrite U
-      if (int rc = flush()) return rc;
+      if (int rc = flush(hs.nterms)) return rc;
       if (hdrift_host > 1e-8) {  // lrmc.py:258-259 every 64 updates, from the tracked H
         double drift = 0.0;
         if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
@@ -493,11 +501,14 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       }
     }
   }
-  if (int rc = flush()) return rc;
+  {
+    GrouseState hs;
+    RCUDA(cudaMemcpyAsync(&hs, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaStreamSynchronize(s));
+    if (int rc = flush(hs.nterms)) return rc;
+  }
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(ubase, v, r, 0, &drift, stream, st)) return rc;
-  if (ubase != u)
-    RCUDA(cudaMemcpyAsync(u, ubase, (size_t)v * r * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const int64_t tcount = (int64_t)passes * ell;
   if (passes_out) *passes_out = passes;
   if (converged_out) *converged_out = converged;

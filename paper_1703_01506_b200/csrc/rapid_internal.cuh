@@ -55,6 +55,8 @@ cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* 
                                 const GrouseState* st, int dense, cudaStream_t s);
 cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
                                 cudaStream_t s);
+cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, int k, double* out,
+                                   int64_t ldo, cudaStream_t s);
 // vals[i] = t[idx[i]] and aug[i * ldaug] = the same (the Gram's extra column)
 cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
                                    double* aug, int64_t ldaug, cudaStream_t s);
@@ -66,10 +68,13 @@ cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int3
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
                                  const double* hw, cudaStream_t s);
-cudaError_t launch_defer_apply(double* M, double* cmat, double* H, const double* hg,
-                               GrouseState* st, const double* mw, const double* dots,
-                               const double* wn, int r, cudaStream_t s);
-cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s);
+// M += a (M w) b^T, and the same term as factors M = I + X Yt (X: r x
+// kDeferCap, Yt: kDeferCap x r, column / row nterms)
+cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
+                               const double* hg, GrouseState* st, const double* mw,
+                               const double* dots, const double* wn, int r, cudaStream_t s);
+cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
+                               cudaStream_t s);
 // H = U^T U tracked through the rank-1 updates (the every-64-updates drift
 // check of lrmc.py:258-259 without a 168 GFLOP Gram)
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,

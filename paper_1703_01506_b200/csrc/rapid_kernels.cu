@@ -972,11 +972,11 @@ __global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
 
 // gathered rows of U (k x r, row-major) for the cuBLAS product with M
 __global__ void k_gather_urows(const double* __restrict__ U, int r, const int32_t* __restrict__ idx,
-                               int k, double* __restrict__ out) {
+                               int k, double* __restrict__ out, int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)k * r) return;
   const int i = (int)(e / r), c = (int)(e - (int64_t)i * r);
-  out[e] = U[(int64_t)idx[i] * r + c];
+  out[(int64_t)i * ldo + c] = U[(int64_t)idx[i] * r + c];
 }
 
 // Per-update matrix-vector products, one warp per output (coalesced rows):
@@ -1087,7 +1087,8 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
 // after k_grouse_post_m (+ the H update): M <- M + a (M w) b^T and the older
 // terms c_s <- c_s + a (w . c_s) b; block row y: M row y (y < r) or term
 // y - r; then k_defer_count adds the new term
-__global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ cmat,
+__global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
+                              double* __restrict__ Yt, double* __restrict__ cmat,
                               double* __restrict__ H, const double* __restrict__ g,
                               const GrouseState* __restrict__ st, const double* __restrict__ mw,
                               const double* __restrict__ dots, const double* __restrict__ b,
@@ -1099,6 +1100,10 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ cmat,
   const double a = st->pend_a;
   if (y < r) {
     M[(int64_t)y * r + c] = fma(a * mw[y], b[c], M[(int64_t)y * r + c]);
+    // the same rank-1 term as factors: M = I + X Yt (column / row nterms)
+    const int nt = st->nterms;
+    if (c == 0) X[(int64_t)y * kDeferCap + nt] = a * mw[y];
+    if (y == 0) Yt[(int64_t)nt * r + c] = b[c];
   } else if (y < 2 * r) {  // H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2)
     const int i = y - r;
     H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
@@ -1114,9 +1119,14 @@ __global__ void k_defer_count(GrouseState* __restrict__ st) {
   st->pending = 0;
 }
 
-__global__ void k_flush_reset(double* __restrict__ M, int r, GrouseState* __restrict__ st) {
+__global__ void k_flush_reset(double* __restrict__ M, double* __restrict__ X,
+                              double* __restrict__ Yt, int r, GrouseState* __restrict__ st) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < (int64_t)r * r) M[e] = (e / r == e % r) ? 1.0 : 0.0;
+  if (e < (int64_t)r * kDeferCap) {
+    X[e] = 0.0;
+    Yt[e] = 0.0;
+  }
   if (e == 0) st->nterms = 0;
 }
 
@@ -1449,7 +1459,14 @@ cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* 
 cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
                                 cudaStream_t s) {
   const int64_t n = (int64_t)k * r;
-  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out);
+  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, int k, double* out,
+                                   int64_t ldo, cudaStream_t s) {
+  const int64_t n = (int64_t)k * r;
+  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, ldo);
   return cudaGetLastError();
 }
 
@@ -1477,18 +1494,19 @@ cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int3
   return cudaGetLastError();
 }
 
-cudaError_t launch_defer_apply(double* M, double* cmat, double* H, const double* hg,
-                               GrouseState* st, const double* mw, const double* dots,
-                               const double* wn, int r, cudaStream_t s) {
+cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
+                               const double* hg, GrouseState* st, const double* mw,
+                               const double* dots, const double* wn, int r, cudaStream_t s) {
   k_defer_apply<<<dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)), 256, 0, s>>>(
-      M, cmat, H, hg, st, mw, dots, wn, r);
+      M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
   k_defer_count<<<1, 1, 0, s>>>(st);
   return cudaGetLastError();
 }
 
-cudaError_t launch_flush_reset(double* M, int r, GrouseState* st, cudaStream_t s) {
-  const int64_t n = (int64_t)r * r;
-  k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, r, st);
+cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
+                               cudaStream_t s) {
+  const int64_t n = (int64_t)r * std::max(r, kDeferCap);
+  k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, X, Yt, r, st);
   return cudaGetLastError();
 }
 
