@@ -481,23 +481,37 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, dou
   double ta, tb, tc;
   cg_block_reduce3(a, b, c, wsum, ta, tb, tc);
   const int tid = threadIdx.x;
-  if (v)
-    for (int e = tid; e < nr * kCgCtas; e += kCgThreads) {
-      const int i = e % nr, dst = e / nr;
-      st_cluster_f64(full + r0 + i, dst, v[i]);
-    }
+  if (v && tid < 8 * 32) {  // thread (dst = tid / 16 ... ): rows i = lane16, lane16 + 16, ..
+    const int dst = tid >> 4, sub = tid & 15;  // 16 threads per destination CTA pair
+    for (int d = dst; d < kCgCtas; d += 16)
+      for (int i = sub; i < nr; i += 16) st_cluster_f64(full + r0 + i, d, v[i]);
+  }
   if (tid < kCgCtas) {
     st_cluster_f64(slots + 3 * me, tid, ta);
     st_cluster_f64(slots + 3 * me + 1, tid, tb);
     st_cluster_f64(slots + 3 * me + 2, tid, tc);
   }
   cluster_sync();
-  A = B = C = 0.0;
-  for (int q = 0; q < kCgCtas; ++q) {
-    A += slots[3 * q];
-    B += slots[3 * q + 1];
-    C += slots[3 * q + 2];
+  // every warp sums the kCgCtas partials with the same shuffle tree: the
+  // same bits on every CTA (they all take the same convergence decision)
+  static_assert(kCgCtas <= 32 && (kCgCtas & (kCgCtas - 1)) == 0, "power-of-2 cluster");
+  const int lane = tid & 31;
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  if (lane < kCgCtas) {
+    sa = slots[3 * lane];
+    sb = slots[3 * lane + 1];
+    sc = slots[3 * lane + 2];
   }
+#pragma unroll
+  for (int o = kCgCtas / 2; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  }
+  // lanes >= kCgCtas summed zeros: every thread takes lane 0's totals
+  A = __shfl_sync(0xffffffffu, sa, 0);
+  B = __shfl_sync(0xffffffffu, sb, 0);
+  C = __shfl_sync(0xffffffffu, sc, 0);
   __syncthreads();  // wsum reusable
 }
 
