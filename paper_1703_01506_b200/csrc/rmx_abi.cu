@@ -6,6 +6,8 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <string>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -128,7 +130,33 @@ int device_sm_count() {
   return sms;
 }
 
+static NaiveLayout naive_layout_compute(int64_t v, int n, int n1, int64_t L, int sm_count);
+
+// The layout (with its chunk-count makespan search, ~0.1 ms of host time at
+// config 4) is needed by every phase call; the last few are memoised, keyed
+// by the arguments and the tuning environment variables.
 NaiveLayout naive_layout(int64_t v, int n, int n1, int64_t L, int sm_count) {
+  std::string key = std::to_string(v) + "," + std::to_string(n) + "," + std::to_string(n1) + "," +
+                    std::to_string(L) + "," + std::to_string(sm_count);
+  for (const char* name : {"RMX_I8", "RMX_CG", "RMX_CHUNKS_MIN", "RMX_RAMP", "RMX_EPI_GROUPS"}) {
+    const char* e = getenv(name);
+    key += e ? std::string("|") + e : std::string("|-");
+  }
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, NaiveLayout>> cache;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& kv : cache)
+      if (kv.first == key) return kv.second;
+  }
+  const NaiveLayout lay = naive_layout_compute(v, n, n1, L, sm_count);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() >= 8) cache.erase(cache.begin());
+  cache.emplace_back(key, lay);
+  return lay;
+}
+
+static NaiveLayout naive_layout_compute(int64_t v, int n, int n1, int64_t L, int sm_count) {
   NaiveLayout lay{};
   const bool balanced = 2 * n1 == n;
   // balanced groups: t depends on S only -> 256-voxel S-only tiles.  Default

@@ -228,3 +228,34 @@ def test_float32_host_upload_bit_exact(oracle_mod, v, n1, n2, L, seed):
                                          False, threads=8)
     assert np.array_equal(r32.maxima, r64.maxima) and np.array_equal(r32.maxima, mx)
     assert np.array_equal(r32.argmax, r64.argmax) and np.array_equal(r32.argmax, am)
+
+
+@pytest.mark.parametrize("n1,n2", [(100, 100), (30, 50)])
+def test_permutation_shards_bit_identical_to_single_gpu(n1, n2):
+    """What each rank of an N-GPU run computes (shard.py: contiguous
+    permutation ranges, labels generated on the device from the global
+    index) reassembles to the single-GPU result bit for bit, for any N."""
+    import torch
+
+    from paper_1703_01506_b200.labels import device_orders
+    from paper_1703_01506_b200.naive_engine import NaiveJob
+    from paper_1703_01506_b200.shard import shard_bounds
+
+    dev = torch.device("cuda", 0)
+    x = _data(5000, n1, n2, 31)
+    L = 1000
+    plan = rmx.PermutationPlan(77, L, n1 + n2)
+    full = rmx.run_naive_ex(x, plan)
+    xd = torch.from_numpy(np.ascontiguousarray(x.values)).to(dev)
+    for world in (2, 3, 8):
+        mx, am = [], []
+        for rank in range(world):
+            lo, hi, _ = shard_bounds(L, rank, world)
+            if hi <= lo:
+                continue
+            job = NaiveJob(xd, n1, device_orders(77, lo, hi, n1 + n2, dev), False)
+            m, a = job.run()
+            mx.append(m.cpu().numpy())
+            am.append(a.cpu().numpy())
+        assert np.array_equal(np.concatenate(mx), full.maxima), world
+        assert np.array_equal(np.concatenate(am).astype(np.int64), full.argmax), world
