@@ -58,7 +58,8 @@ struct GramTcArgs {
   const int32_t* idx;     // [B][k]
   int k;
   const double* vals;     // [B][k]
-  double* G;              // [B][(r+1)^2], lower triangle written
+  void* G;                // [B][(r+1)^2], lower triangle written (fp64 or fp32)
+  int g_f32;
   int64_t B;
   int njobs;
   int job_s0[kGMaxJobs], job_s1[kGMaxJobs];
@@ -262,7 +263,8 @@ __global__ void __launch_bounds__(kGThreadsTc, 1) k_gram_tc(const __grid_constan
       const double tsc = t_scale(block_absmax_t(a.vals + b * a.k, a.k, etid, 128, red + 4, 2));
       const double duu = 1.0 / ((double)kGUScale * kGUScale);
       const double dut = 1.0 / ((double)kGUScale * tsc), dtt = 1.0 / (tsc * tsc);
-      double* Gb = a.G + b * (int64_t)ld * ld;
+      double* Gb = static_cast<double*>(a.G) + b * (int64_t)ld * ld;
+      float* Gf = static_cast<float*>(a.G) + b * (int64_t)ld * ld;
       mbar_wait(tfull, acc_phase);
       tc_fence_after();
       uint32_t tcol = 0;
@@ -282,7 +284,9 @@ __global__ void __launch_bounds__(kGThreadsTc, 1) k_gram_tc(const __grid_constan
               if (gj >= gi && (gj < a.r || gj == a.rt)) {
                 const int j = gj == a.rt ? a.r : gj;
                 const double sc = (j == a.r) ? (i == a.r ? dtt : dut) : duu;
-                Gb[(int64_t)j * ld + i] = (double)__uint_as_float(v[jj]) * sc;
+                const double gv = (double)__uint_as_float(v[jj]) * sc;
+                if (a.g_f32) Gf[(int64_t)j * ld + i] = (float)gv;
+                else Gb[(int64_t)j * ld + i] = gv;
               }
             }
           }
@@ -410,7 +414,7 @@ cudaError_t launch_gram_planes(const double* U, int64_t ldu, int64_t v, int r, _
 }
 
 cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t* idx, int k,
-                           const double* vals, double* G, int64_t B, int sm_count,
+                           const double* vals, void* G, int g_f32, int64_t B, int sm_count,
                            cudaStream_t s) {
   GramTcArgs a{};
   a.planes = planes;
@@ -422,6 +426,7 @@ cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t
   a.k = k;
   a.vals = vals;
   a.G = G;
+  a.g_f32 = g_f32;
   a.B = B;
   int s0[8], s1[8];
   a.njobs = gram_tc_jobs(a.rp, s0, s1);

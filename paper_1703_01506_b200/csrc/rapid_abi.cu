@@ -158,11 +158,15 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
     return rmx_lsq_solve(u, ldu, r, idx, k, vals, B, w_out, flag_out, nullptr, workspace,
                          workspace_bytes, stream, st);
   }
-  const size_t per = gram_bytes(r);
+  // G~ in fp32 (its precision is the tensor cores' anyway): half the bytes,
+  // a twice-as-fast factor; RMX_GRAM_CHOL64=1 keeps the factor in fp64
+  const bool f32 = !getenv("RMX_GRAM_CHOL64");
+  const size_t per = f32 ? gram_bytes(r) / 2 : gram_bytes(r);
   int64_t chunk = (int64_t)((workspace_bytes > 256 ? workspace_bytes - 256 : 0) /
                             (per + 4 * sizeof(double)));
   if (chunk < 1) return rset(st, RMX_E_USAGE, "lsq workspace too small");
   chunk = std::min<int64_t>(chunk, B);
+  void* Graw = workspace;
   double* G = static_cast<double*>(workspace);
   double* nrm = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + chunk * per);
   DevBuf<__half> planes;
@@ -179,12 +183,16 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
     const int32_t* ib = idx + b0 * k;
     const double* vb = vals + b0 * k;
     double* wb = w_out + b0 * r;
-    RCUDA(launch_gram_tc(planes.p, v, r, ib, k, vb, G, cnt, sms, s));
-    RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
-    // two refinement steps with the fp64 residual (contraction ~ cond * 1e-6 each)
+    RCUDA(launch_gram_tc(planes.p, v, r, ib, k, vb, Graw, f32 ? 1 : 0, cnt, sms, s));
+    if (f32) RCUDA(launch_chol_solve_f32(static_cast<float*>(Graw), r, cnt, wb, flags.p + b0, s));
+    else RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
+    // two refinement steps with the fp64 residual (contraction ~ cond * 1e-5 each)
     for (int it = 0; it < 2; ++it) {
       RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
-      RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
+      if (f32)
+        RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0,
+                                      s));
+      else RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
     }
   }
   // systems whose factor was singular or whose refinement has not settled:

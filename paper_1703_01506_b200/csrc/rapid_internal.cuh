@@ -20,6 +20,12 @@ cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_
 // nconv_b = 1 when the correction exceeds 1e-7 |w_b|
 cudaError_t launch_chol_resolve(double* G, int r, int64_t B, const double* rhs, double* w_inout,
                                 int32_t* nconv, cudaStream_t s);
+// the same on an fp32 G (the tensor-core Gram's precision; the fp64
+// refinement restores the solution's accuracy)
+cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int32_t* flag,
+                                  cudaStream_t s);
+cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,
+                                    double* w_inout, int32_t* nconv, cudaStream_t s);
 // Tensor-core Gram (gram_tc.cu): G_b ~ [U[idx_b] | vals_b]^T [U[idx_b] | vals_b]
 // (lower triangle, (r+1)^2 each) from fp16 hi/lo planes of U (gram_planes),
 // fp32-accurate; refined to fp64 accuracy by lsq_resid + launch_chol_resolve
@@ -27,8 +33,9 @@ bool gram_tc_supported(int r, int k);
 int gram_tc_kpg(int r);  // plane row pitch (halves)
 cudaError_t launch_gram_planes(const double* U, int64_t ldu, int64_t v, int r, __half* planes,
                                cudaStream_t s);
+// G: fp64 (g_f32 = 0) or fp32 (g_f32 = 1) (r+1)^2 per system
 cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t* idx, int k,
-                           const double* vals, double* G, int64_t B, int sm_count,
+                           const double* vals, void* G, int g_f32, int64_t B, int sm_count,
                            cudaStream_t s);
 // g_b = U_Omega^T (t - U_Omega w_b) in fp64 (one gather of the rows)
 cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,

@@ -170,26 +170,27 @@ constexpr int kPS = kPW + 1;  // padded smem row stride (doubles)
 
 // Factor the 32x32 SPD block D (smem, lower part used; rows/cols >= w are
 // the identity) in place into L_D; rinv[c] = 1 / L_cc.  One warp.
-__device__ __forceinline__ void chol_block32(double* D, double* rinv, double tiny, int* bad) {
+template <typename T>
+__device__ __forceinline__ void chol_block32(T* D, T* rinv, T tiny, int* bad) {
   const int lane = threadIdx.x & 31;
-  double a[kPW];
+  T a[kPW];
 #pragma unroll
   for (int l = 0; l < kPW; ++l) a[l] = D[lane * kPS + l];
 #pragma unroll
   for (int c = 0; c < kPW; ++c) {
-    double piv = __shfl_sync(0xffffffffu, a[c], c);
+    T piv = __shfl_sync(0xffffffffu, a[c], c);
     if (!(piv > tiny)) {
       if (lane == 0) *bad = 1;
       piv = fmax(fabs(piv), 1e-300);
     }
-    const double d = sqrt(piv);
-    const double inv = 1.0 / d;
+    const T d = sqrt(piv);
+    const T inv = 1.0 / d;
     if (lane == c) a[c] = d;
     if (lane > c) a[c] *= inv;
     if (lane == 0) rinv[c] = inv;
 #pragma unroll
     for (int l = c + 1; l < kPW; ++l) {
-      const double llc = __shfl_sync(0xffffffffu, a[c], l);
+      const T llc = __shfl_sync(0xffffffffu, a[c], l);
       if (lane >= l) a[l] = fma(-a[c], llc, a[l]);
     }
   }
@@ -200,8 +201,8 @@ __device__ __forceinline__ void chol_block32(double* D, double* rinv, double tin
 // rows of the panel below the first diagonal block (the largest panel)
 __host__ __device__ constexpr int chol_panel_rows(int r) { return r > kPW ? r - kPW : 1; }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __restrict__ G, int r,
+template <int NT, typename T = double>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(T* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
                                                    int32_t* flag, double* __restrict__ resid2,
                                                    const int32_t* gate = nullptr,
@@ -212,20 +213,21 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
   // rhs_ext[b], w_out[b] += d, flag[b] = 1 when |d| > 1e-7 |w| (not converged)
   if (gate && *gate == 0) return;
   __syncthreads();  // every thread has read the gate before it is overwritten
-  extern __shared__ double sm[];
-  double* D = sm;                     // kPW x kPS: block / L_D (lower)
-  double* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
-  double* P = rinv + kPW;             // chol_panel_rows(r) x kPS panel (factor only)
-  double* y = rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS;  // r: rhs / solution
+  extern __shared__ __align__(16) unsigned char chol_smem[];
+  T* sm = reinterpret_cast<T*>(chol_smem);
+  T* D = sm;                     // kPW x kPS: block / L_D (lower)
+  T* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
+  T* P = rinv + kPW;             // chol_panel_rows(r) x kPS panel (factor only)
+  T* y = rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS;  // r: rhs / solution
   __shared__ int bad;
-  __shared__ double dmax;
+  __shared__ T dmax;
   const int64_t b = blockIdx.x;
   const int ld = r + 1;
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
-  double* Gb = G + b * (int64_t)ld * ld;
+  T* Gb = G + b * (int64_t)ld * ld;
   if (wid == 0 && !rhs_ext) {
-    double m = 0.0;
+    T m = 0.0;
     for (int i = lane; i < r; i += 32) m = fmax(m, Gb[(int64_t)i * ld + i]);
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) {
@@ -234,11 +236,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
     }
   }
   __syncthreads();
-  const double tiny = 1e-24 * dmax;
+  const T tiny = 1e-24 * dmax;
   auto load_block = [&](int jb, int w) {  // D = G[jb.., jb..] (lower), identity padding
     for (int e = tid; e < kPW * kPW; e += NT) {
       const int i = e / kPW, j = e % kPW;
-      double val = (i == j) ? 1.0 : 0.0;
+      T val = (i == j) ? 1.0 : 0.0;
       if (i < w && j < w && j <= i) val = Gb[(int64_t)(jb + i) * ld + jb + j];
       D[i * kPS + j] = val;
     }
@@ -256,18 +258,18 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
     // panel below: P_i L_D^T = G[i, jb:jb+w], one row per thread (registers)
     const int rows = r - jb - w;
     for (int i = tid; i < rows; i += NT) {
-      double* gi = Gb + (int64_t)(jb + w + i) * ld + jb;
-      double pr[kPW];
+      T* gi = Gb + (int64_t)(jb + w + i) * ld + jb;
+      T pr[kPW];
 #pragma unroll
       for (int c = 0; c < kPW; ++c) pr[c] = c < w ? gi[c] : 0.0;
 #pragma unroll
       for (int c = 0; c < kPW; ++c) {
-        double sacc = pr[c];
+        T sacc = pr[c];
 #pragma unroll
         for (int l = 0; l < c; ++l) sacc = fma(-pr[l], D[c * kPS + l], sacc);
         pr[c] = sacc * rinv[c];
       }
-      double* prow = P + (size_t)i * kPS;
+      T* prow = P + (size_t)i * kPS;
 #pragma unroll
       for (int c = 0; c < kPW; ++c) {
         prow[c] = pr[c];
@@ -283,12 +285,12 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
       while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
       while (bi * (bi + 1) / 2 > t) --bi;
       const int bj = t - bi * (bi + 1) / 2;
-      double acc[4][4] = {};
-      const double* pi = P + (size_t)(4 * bi) * kPS;
-      const double* pj = P + (size_t)(4 * bj) * kPS;
+      T acc[4][4] = {};
+      const T* pi = P + (size_t)(4 * bi) * kPS;
+      const T* pj = P + (size_t)(4 * bj) * kPS;
 #pragma unroll 4
       for (int c = 0; c < kPW; ++c) {
-        double a[4], bb[4];
+        T a[4], bb[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           a[q] = (4 * bi + q < rows) ? pi[q * kPS + c] : 0.0;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
       for (int q = 0; q < 4; ++q) {
         const int i = 4 * bi + q;
         if (i >= rows) continue;
-        double* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
+        T* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = 4 * bj + u;
@@ -321,22 +323,22 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
     load_block(jb, w);
     __syncthreads();
     if (wid == 0) {  // lane c holds y[jb + c]; row `lane` of L_D in registers
-      double lr[kPW];
+      T lr[kPW];
 #pragma unroll
       for (int c = 0; c < kPW; ++c) lr[c] = D[lane * kPS + c];
-      double yb = lane < w ? y[jb + lane] : 0.0;
+      T yb = lane < w ? y[jb + lane] : 0.0;
 #pragma unroll
       for (int c = 0; c < kPW; ++c) {
         if (lane == c) yb /= lr[c];
-        const double yc = __shfl_sync(0xffffffffu, yb, c);
+        const T yc = __shfl_sync(0xffffffffu, yb, c);
         if (lane > c) yb = fma(-lr[c], yc, yb);
       }
       if (lane < w) y[jb + lane] = yb;
     }
     __syncthreads();
     for (int i = jb + w + tid; i < r; i += NT) {
-      const double* li = Gb + (int64_t)i * ld + jb;
-      double sacc = 0.0;
+      const T* li = Gb + (int64_t)i * ld + jb;
+      T sacc = 0.0;
       for (int c = 0; c < w; ++c) sacc = fma(li[c], y[jb + c], sacc);
       y[i] -= sacc;
     }
@@ -347,21 +349,21 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
     load_block(jb, w);
     __syncthreads();
     if (wid == 0) {  // lane c holds y[jb + c]; column `lane` of L_D in registers
-      double lc[kPW];
+      T lc[kPW];
 #pragma unroll
       for (int c = 0; c < kPW; ++c) lc[c] = D[c * kPS + lane];
-      double yb = lane < w ? y[jb + lane] : 0.0;
+      T yb = lane < w ? y[jb + lane] : 0.0;
 #pragma unroll
       for (int c = kPW - 1; c >= 0; --c) {
         if (lane == c) yb /= lc[c];
-        const double wc = __shfl_sync(0xffffffffu, yb, c);
+        const T wc = __shfl_sync(0xffffffffu, yb, c);
         if (lane < c) yb = fma(-lc[c], wc, yb);
       }
       if (lane < w) y[jb + lane] = yb;
     }
     __syncthreads();
     for (int i = tid; i < jb; i += NT) {  // coalesced: row jb+c, columns i
-      double sacc = 0.0;
+      T sacc = 0.0;
       for (int c = 0; c < w; ++c) sacc = fma(Gb[(int64_t)(jb + c) * ld + i], y[jb + c], sacc);
       y[i] -= sacc;
     }
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
     if (tid < 32) {
       double dd = 0.0, ww = 0.0;
       for (int i = lane; i < r; i += 32) {
-        const double wn = w_out[b * r + i] + y[i];
+        const double wn = w_out[b * r + i] + (double)y[i];
         w_out[b * r + i] = wn;
         dd += y[i] * y[i];
         ww += wn * wn;
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(double* __
       for (int i = lane; i < r; i += 32) {
         rw += Gb[(int64_t)r * ld + i] * y[i];
         ww += y[i] * y[i];
-        const double dd = Gb[(int64_t)i * ld + i];
+        const T dd = Gb[(int64_t)i * ld + i];
         dmn = fmin(dmn, dd);
         dmx = fmax(dmx, dd);
       }
@@ -1331,6 +1333,27 @@ cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_
     if (e != cudaSuccess) return e;
     k_chol_solve<256><<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, resid2);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int32_t* flag,
+                                  cudaStream_t s) {
+  const size_t smem =
+      ((size_t)kPW * kPS + kPW + (size_t)chol_panel_rows(r) * kPS + (size_t)r) * sizeof(float);
+  auto kern = k_chol_solve<256, float>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,
+                                    double* w_inout, int32_t* nconv, cudaStream_t s) {
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(float);
+  auto kern = k_chol_solve<256, float>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs);
   return cudaGetLastError();
 }
 
