@@ -354,7 +354,7 @@ def main():
         # u8 x s8 -> s32 MMA over K = 2 kpad (z = 255 h + l digit planes), S only;
         # B200 dense int8 = 2x dense bf16 (4.5 vs 2.25 P nominal); MEASURED_PEAKS
         # has no int8 entry, so the peak is 2x its measured bf16 figure
-        kpad = -(-n // 32) * 32
+        kpad = -(-n // 16) * 16  # the [h | l] planes share one K extent 2 kpad (32-byte MMA K step)
         exec_flops = 2.0 * (2 * kpad) * v * local_L
         peak, peak_sust = 2.0 * bf16_burst, 2.0 * bf16_sust
         peak_kind = f"{pk_kind} bf16 dense burst x 2 (int8 dense)"

@@ -44,6 +44,7 @@ from .domain import (
     Basis,
     MaxNull,
     ObservedColumn,
+    PendingBasis,
     SubspaceModel,
     as_data_matrix,
     as_plan,
@@ -272,44 +273,83 @@ class TrainingResult:
         self.converged = converged
 
 
-def _basis_init_async(seed: int, v: int, rank: int):
-    """Start drawing init_basis's normals (lrmc.py:85-93: ONE sequential
-    stream(seed, BASIS_INIT) of v x rank doubles, ~2-3 s of host time at
-    config 5) on a background thread -- numpy releases the GIL while it fills
-    the array -- so that the X upload, the training columns and the Omega
-    draws run on the GPU meanwhile.  Returns a callable that joins."""
-    import threading
+def _basis_init_async(seed: int, v: int, rank: int, dev):
+    """Draw init_basis's normals (lrmc.py:85-93: ONE sequential
+    stream(seed, BASIS_INIT) of v x rank doubles, ~1.9 s of host time at
+    config 5) on a background thread -- numpy releases the GIL for the whole
+    fill -- while the X upload, the training columns, the Omega draws and
+    the recovery statistics run on the GPU.  (Drawing in blocks and uploading
+    each behind the next was slower: every block re-acquires the GIL from a
+    main thread that is busy issuing that GPU work.)  Returns a joiner giving
+    the (v, rank) fp64 device tensor."""
+    join = _host_async(lambda: stream(seed, BASIS_INIT).standard_normal((v, rank)))
 
-    box = {}
+    def joined():
+        return _to_dev(join(), dev)
+
+    return joined
+
+
+def _host_array_async(shape):
+    """A float64 host array with every page already touched, prepared on a
+    host thread while the GPU runs GROUSE (the host is otherwise idle)."""
 
     def work():
-        try:
-            box["a"] = stream(seed, BASIS_INIT).standard_normal((v, rank))
-        except BaseException as exc:  # re-raised by the joiner
-            box["e"] = exc
+        a = np.empty(shape, dtype=np.float64)
+        a.fill(0.0)
+        return a
 
-    th = threading.Thread(target=work, name="rmx-basis-init", daemon=True)
-    th.start()
+    return _host_async(work)
 
-    def join():
-        th.join()
-        if "e" in box:
-            raise box["e"]
-        return box.pop("a")
 
-    return join
+def _d2h_async(t, dest):
+    """Copy the device tensor `t` into the host array dest() on a side stream
+    from a host thread, overlapping later GPU work: 32 MB row blocks through
+    two page-locked buffers, block c + 1 in flight while block c is copied
+    out on the host.  Returns the joiner."""
+    torch = _torch()
+    side = torch.cuda.Stream(t.device)
+    side.wait_stream(torch.cuda.current_stream(t.device))
+
+    def work():
+        h = dest()
+        v, width = t.shape
+        rows = max(1, min(v, (32 << 20) // (8 * width)))
+        bufs = [torch.empty((rows, width), dtype=t.dtype, pin_memory=True) for _ in range(2)]
+        evs = [torch.cuda.Event(), torch.cuda.Event()]
+        blocks = [(lo, min(v, lo + rows)) for lo in range(0, v, rows)]
+
+        def issue(c):
+            lo, hi = blocks[c]
+            bufs[c & 1][: hi - lo].copy_(t[lo:hi], non_blocking=True)
+            evs[c & 1].record(side)
+
+        with torch.cuda.stream(side):
+            issue(0)
+            for c, (lo, hi) in enumerate(blocks):
+                evs[c & 1].synchronize()
+                if c + 1 < len(blocks):
+                    issue(c + 1)
+                h[lo:hi] = bufs[c & 1].numpy()[: hi - lo]
+        return h
+
+    return _host_async(work)
 
 
 def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
-                        max_passes: int, tolerance: float, init=None):
+                        max_passes: int, tolerance: float, init=None, host_basis: bool = False):
     """GROUSE on device.  t_dev: (ell, v) fp64 training statistics; init: a
     joiner from _basis_init_async (else the normals are drawn here)."""
     torch = _torch()
     dev = t_dev.device
-    normals = init() if init is not None else stream(seed, BASIS_INIT).standard_normal((v, rank))
-    u = _to_dev(normals, dev)
-    del normals
+    if init is not None:
+        u = init()
+    else:
+        u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, rank)), dev)
+    host_u = _host_array_async((v, rank)) if host_basis else None
+    _mark("basis_normals_ready")
     _orthonormalize(u, force=True)
+    _mark("basis_upload+qr")
     om_dev = torch.empty((max_passes, ell, k), dtype=torch.int32, device=dev)
     for p in range(max_passes):  # stream(seed, TRAIN_OMEGA, i, p), drawn on the GPU
         om_dev[p] = device_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, dev, extra=p)
@@ -325,12 +365,14 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
         except Exception:
             return 1
 
+    _mark("train_omegas")
     cbf = nat.OMEGA_CB(cb)
     nat.call("rmx_grouse_train", nat.ptr(t_dev), v, ell, rank, k, nat.ptr(om_dev), max_passes,
              float(tolerance), nat.ptr(u), cbf, None, pass_resid, ctypes.byref(passes),
              ctypes.byref(conv), ctypes.byref(updates), nat.ptr(final), _stream(dev))
+    _mark("grouse")
     res = [pass_resid[i] for i in range(passes.value)]
-    return u, final, int(passes.value), bool(conv.value), int(updates.value), res
+    return u, final, int(passes.value), bool(conv.value), int(updates.value), res, host_u
 
 
 def train_basis(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int = 50,
@@ -344,7 +386,7 @@ def train_basis(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int 
         raise UsageError(f"observed rows {k} exceed voxel count {v}")
     dev = cuda_device()
     t_dev = _to_dev(np.ascontiguousarray(t_ex.T), dev)
-    u, final, passes, conv, updates, res = _train_basis_device(t_dev, v, ell, k, rank, seed,
+    u, final, passes, conv, updates, res, _ = _train_basis_device(t_dev, v, ell, k, rank, seed,
                                                                max_passes, tolerance)
     fo = final.cpu().numpy()
     return TrainingResult(Basis(u.cpu().numpy(), copy=False), passes, updates, res,
@@ -352,9 +394,67 @@ def train_basis(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int 
 
 
 # ---------------------------------------------------------------- train / recover
-def _train_device(x, cfg):
+_PHASE_LOG = None  # tools/rapid_phases.py sets a list: (tag, seconds) marks, device-synchronised
+
+
+def _mark(tag: str) -> None:
+    if _PHASE_LOG is not None:
+        _torch().cuda.synchronize()
+        _PHASE_LOG.append((tag, time.perf_counter()))
+
+
+def _host_async(fn):
+    """Run fn() on a background host thread; returns a joiner that re-raises."""
+    import threading
+
+    box = {}
+
+    def work():
+        try:
+            box["a"] = fn()
+        except BaseException as exc:  # re-raised by the joiner
+            box["e"] = exc
+
+    th = threading.Thread(target=work, name="rmx-host-draw", daemon=True)
+    th.start()
+
+    def join():
+        th.join()
+        if "e" in box:
+            raise box["e"]
+        return box.pop("a")
+
+    return join
+
+
+class _RecoverInputs:
+    """Recovery inputs that do not depend on the trained basis (rapid.py:
+    158-168: the shuffles, the Omega draws and the exact statistics at the
+    Omega rows), computed by run_rapid while the host draws init_basis's
+    normals.  A degenerate-voxel report is kept and raised when recovery
+    starts, i.e. in the reference's order (after training)."""
+
+    def __init__(self, x, xd, plan, seed: int, ell: int, k: int, dev):
+        torch = _torch()
+        L, v = plan.count, x.voxels
+        self.key = (int(seed), ell, k, L, plan.master_seed)
+        self.xd = xd
+        self.od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
+        self.omd = device_omegas(seed, RECOVER_OMEGA, ell, L, v, k, dev)
+        self.t = torch.empty((L - ell, k), dtype=torch.float64, device=dev)
+        self.st = nat.Status()
+        self.rc = nat.load().rmx_rapid_stats(nat.ptr(xd), v, x.subjects, x.n1, nat.ptr(self.od),
+                                             nat.ptr(self.omd), L - ell, k, nat.ptr(self.t),
+                                             _stream(dev), ctypes.byref(self.st))
+
+
+def _train_device(x, cfg, prefetch_recovery: bool = False):
     """Shared by train() and run_rapid(): returns (model, training maxima,
-    t_dev (ell x v, device), u_dev, u32_dev)."""
+    t_dev (ell x v, device), recovery inputs or None).  The GPU work that
+    does not need the basis (X upload, training columns, Omega draws and --
+    for run_rapid -- the recovery statistics) runs while a host thread draws
+    init_basis's sequential normals (the max-gap normals on other host
+    threads); the basis's host array is prepared during GROUSE."""
     torch = _torch()
     cfg = cfg.resolve(x)
     if cfg.engine != "rapid":
@@ -364,12 +464,21 @@ def _train_device(x, cfg):
     k = observed_rows(cfg.sample_rate, v)
     plan = cfg.plan_for(x)
     dev = cuda_device()
-    init = _basis_init_async(cfg.seed, v, rank)         # host, overlapped with the GPU work below
+    init = _basis_init_async(cfg.seed, v, rank, dev)    # host, overlapped with the GPU work below
+    gap = None
+    if cfg.shift_override is None and cfg.shift_estimator != "residual-sup":
+        gap = _host_async(lambda: draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v))
     xd = data_to_device(x, dev)
     od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
-    u, final, passes, conv, _, _ = _train_basis_device(t_dev, v, ell, k, rank, cfg.seed,
-                                                       cfg.max_passes, cfg.tolerance, init)
+    _mark("x_upload+training_columns")
+    pre = None
+    if prefetch_recovery and ell < plan.count:
+        pre = _RecoverInputs(x, xd, plan, cfg.seed, ell, k, dev)
+        _mark("recovery_prefetch")
+    u, final, passes, conv, _, _, host_u = _train_basis_device(
+        t_dev, v, ell, k, rank, cfg.seed, cfg.max_passes, cfg.tolerance, init,
+        host_basis=prefetch_recovery)
     # fits of the frozen basis on the final pass's observed rows (rapid.py:90-97)
     vals = torch.empty((ell, k), dtype=torch.float64, device=dev)
     nat.call("rmx_gather_rows", nat.ptr(t_dev), v, nat.ptr(final), k, ell, nat.ptr(vals),
@@ -377,6 +486,7 @@ def _train_device(x, cfg):
     W, flags, norms = _lsq(u, rank, final, k, vals, ell)
     if int(flags.max().item()) != 0:
         raise IllConditionedBasisError(math.inf)
+    _mark("final_fits")
     if cfg.sigma_override is not None:
         sigma = float(cfg.sigma_override)
         if sigma < 0:
@@ -392,6 +502,7 @@ def _train_device(x, cfg):
     nat.call("rmx_row_max", nat.ptr(t_dev), ell, v, int(cfg.two_sided), nat.ptr(tmax),
              _stream(dev))
     training_maxima = tmax.cpu().numpy()
+    _mark("sigma+training_maxima")
     u32 = u.to(torch.float32)
     w32 = W.to(torch.float32)
     if cfg.shift_override is not None:
@@ -400,22 +511,28 @@ def _train_device(x, cfg):
         m = _complete_max(u32, w32, 0, 0.0, 0.0, cfg.seed, cfg.two_sided, base=t_dev)
         mu = float(m.max().item())
     else:  # max-gap: gaps to synthetic columns with the reference's SHIFT_GAP normals
-        z = _to_dev(draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v), dev)
+        z = _to_dev(gap(), dev)
         synth = _complete_max(u32, w32, 0, sigma, 0.0, cfg.seed, cfg.two_sided, znoise=z)
         mu = float(np.mean(training_maxima - synth.cpu().numpy()))
+    _mark("shift")
+    if prefetch_recovery:  # run_rapid: the host copy overlaps recovery (joined before it returns)
+        basis = PendingBasis(_d2h_async(u, host_u), tuple(u.shape))
+    else:
+        basis = Basis(u.cpu().numpy(), copy=False)
     model = SubspaceModel(
-        basis=Basis(u.cpu().numpy(), copy=False), residual_std=sigma, max_shift=mu,
+        basis=basis, residual_std=sigma, max_shift=mu,
         training_columns=ell, sample_rate=cfg.sample_rate, training_maxima=training_maxima,
         two_sided=cfg.two_sided, seed=cfg.seed, passes=passes, converged=conv)
     object.__setattr__(model, "_rmx_dev", (dev, u, u32))
-    return model, training_maxima, t_dev
+    _mark("model_basis_d2h")
+    return model, training_maxima, t_dev, pre
 
 
 def train(x, cfg):
     """Training phase (reference rapid.py:72-135) -> (model, training maxima,
     training columns t_ex (v x ell))."""
     x = as_data_matrix(x)
-    model, training_maxima, t_dev = _train_device(x, cfg)
+    model, training_maxima, t_dev, _ = _train_device(x, cfg)
     return model, training_maxima, t_dev.t().contiguous().cpu().numpy()
 
 
@@ -431,8 +548,9 @@ def _degenerate_in_recovery(x, plan, ell, L, k, t_perm_idx, omega_idx, omegas, o
     raise DegenerateVoxelError(int(voxel), float(m))
 
 
-def recover(x, model: SubspaceModel, plan, cfg):
-    """Recovery phase (reference rapid.py:209-250) -> (MaxNull, counters)."""
+def recover(x, model: SubspaceModel, plan, cfg, _pre: Optional[_RecoverInputs] = None):
+    """Recovery phase (reference rapid.py:209-250) -> (MaxNull, counters).
+    `_pre`: run_rapid's basis-independent inputs computed during training."""
     torch = _torch()
     x = as_data_matrix(x)
     plan = as_plan(plan)
@@ -449,13 +567,16 @@ def recover(x, model: SubspaceModel, plan, cfg):
     maxima = np.empty(L, dtype=np.float64)
     maxima[:ell] = model.training_maxima
     nrec = L - ell
-    xd = data_to_device(x, dev)
-    od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
-    omd = device_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k, dev)
-    t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
-    st = nat.Status()
-    rc = nat.load().rmx_rapid_stats(nat.ptr(xd), v, x.subjects, n1, nat.ptr(od), nat.ptr(omd),
-                                    nrec, k, nat.ptr(t), _stream(dev), ctypes.byref(st))
+    if _pre is not None and _pre.key == (int(model.seed), ell, k, L, plan.master_seed):
+        xd, od, omd, t, st, rc = _pre.xd, _pre.od, _pre.omd, _pre.t, _pre.st, _pre.rc
+    else:
+        xd = data_to_device(x, dev)
+        od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
+        omd = device_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k, dev)
+        t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
+        st = nat.Status()
+        rc = nat.load().rmx_rapid_stats(nat.ptr(xd), v, x.subjects, n1, nat.ptr(od), nat.ptr(omd),
+                                        nrec, k, nat.ptr(t), _stream(dev), ctypes.byref(st))
     if rc == nat.RMX_E_DEGENERATE:
         _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel),
                                 omd.cpu().numpy(), od.cpu().numpy())
@@ -500,9 +621,10 @@ def run_rapid(x, cfg):
     cfg = cfg.resolve(x)
     plan = cfg.plan_for(x)
     t0 = time.perf_counter()
-    model, _, _ = _train_device(x, cfg)
+    model, _, _, pre = _train_device(x, cfg, prefetch_recovery=True)
     t1 = time.perf_counter()
-    null, rec = recover(x, model, plan, cfg)
+    null, rec = recover(x, model, plan, cfg, _pre=pre)
+    model.basis.matrix  # the basis's host copy, overlapped with recovery
     t2 = time.perf_counter()
     v = x.voxels
     counters = {

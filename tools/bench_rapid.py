@@ -38,10 +38,11 @@ def main():
     t_inputs = time.perf_counter() - t0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    model, _, _ = re._train_device(x, cfg)
+    model, _, _, pre = re._train_device(x, cfg, prefetch_recovery=True)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    null, counters = rmx.recover(x, model, plan, cfg)
+    null, counters = re.recover(x, model, plan, cfg, _pre=pre)
+    model.basis.matrix  # host copy of the basis (overlapped with recovery)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     print(json.dumps({"config": args.config, "L": L, "v": x.voxels, "passes": model.passes,

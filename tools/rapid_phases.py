@@ -36,22 +36,37 @@ def main():
             return r
         setattr(mod, name, g)
 
-    for nm in ("draw_normals", "_train_basis_device", "_to_dev", "tstat_exact_device", "_lsq",
-               "_lsq_tc", "_complete_max", "device_orders", "device_omegas"):
+    for nm in ("_lsq_tc", "_complete_max"):
         if hasattr(re, nm):
             wrap(re, nm)
+    orig_init = re._basis_init_async
+
+    def timed_init(seed, v, rank, dev):
+        t0 = time.perf_counter()
+        j = orig_init(seed, v, rank, dev)
+
+        def join():
+            t1 = time.perf_counter()
+            a = j()
+            acc["basis_init_wait"] = time.perf_counter() - t1
+            acc["basis_init_ready_after"] = time.perf_counter() - t0
+            return a
+        return join
+    re._basis_init_async = timed_init
     cfg0 = CONFIGS[args.config]
     dev = torch.device("cuda", 0)
     x = rmx.DataMatrix(make_data_torch(cfg0, dev).to(torch.float32).cpu().numpy(), cfg0.n1, cfg0.n2)
     rc = rmx.RunConfig(permutations=cfg0.permutations, seed=cfg0.plan_seed, engine="rapid",
                        training_columns=cfg0.training_columns, rank=cfg0.rank,
                        sample_rate=cfg0.sample_rate, max_passes=50)
+    re._PHASE_LOG = []
     t0 = time.perf_counter()
     null, model, counters = rmx.run_rapid(x, rc)
     torch.cuda.synchronize()
     print(json.dumps({"total_s": time.perf_counter() - t0, "train_s": counters["train_seconds"],
                       "recover_s": counters["recover_seconds"],
-                      "phases_s": {k: round(v, 3) for k, v in acc.items()}}))
+                      "phases_s": {k: round(v, 3) for k, v in acc.items()},
+                      "train_marks_s": [(tag, round(t - t0, 3)) for tag, t in re._PHASE_LOG]}))
 
 
 if __name__ == "__main__":
