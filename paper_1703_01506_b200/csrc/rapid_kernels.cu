@@ -808,17 +808,32 @@ __global__ void k_resid(const double* __restrict__ U, int64_t ldu, int r,
                         const int32_t* __restrict__ idx, int k,
                         const double* __restrict__ vals, const double* __restrict__ w,
                         double* __restrict__ resid, double* __restrict__ sums) {
+  __shared__ double part[2][8];  // blockDim.x == 256
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
-  if (warp >= k) return;
-  const double* u = U + (int64_t)(idx ? idx[warp] : warp) * ldu;
-  double s = 0.0;
-  for (int c = lane; c < r; c += 32) s += u[c] * w[c];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
+  double ee = 0.0, tt = 0.0;
+  if (warp < k) {
+    const double* u = U + (int64_t)(idx ? idx[warp] : warp) * ldu;
+    double s = 0.0;
+    for (int c = lane; c < r; c += 32) s += u[c] * w[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const double e = vals[warp] - s;
-    resid[warp] = e;
-    atomicAdd(&sums[0], e * e);                    // |resid|^2
-    atomicAdd(&sums[2], vals[warp] * vals[warp]);  // |t_Omega|^2
+    if (lane == 0) resid[warp] = e;
+    ee = e * e;
+    tt = vals[warp] * vals[warp];
+  }
+  if (lane == 0) {
+    part[0][threadIdx.x >> 5] = ee;
+    part[1][threadIdx.x >> 5] = tt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one pair of atomics per block, not per row
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      a += part[0][q];
+      b += part[1][q];
+    }
+    atomicAdd(&sums[0], a);  // |resid|^2
+    atomicAdd(&sums[2], b);  // |t_Omega|^2
   }
 }
 
@@ -895,12 +910,19 @@ __global__ void k_h_g_fin(const double* __restrict__ hw, int r, const GrouseStat
     for (int q = 0; q < kHgSplit; ++q) t += gpart[(int64_t)q * r + c];
     g[c] = a * hw[c] + bb * t;
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    const int lane = threadIdx.x;
+  if (blockIdx.x == 0) {  // (ug w).resid over the k rows: the whole block (k / 256 loads each)
+    __shared__ double part[32];
+    const int lane = threadIdx.x & 31;
     double pr = 0.0;
-    for (int i = lane; i < k; i += 32) pr = fma(vals[i] - resid[i], resid[i], pr);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) pr = fma(vals[i] - resid[i], resid[i], pr);
     for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
-    if (lane == 0) g[r] = a * a * st->aa + 2.0 * a * bb * pr + bb * bb * sums[0];
+    if (lane == 0) part[threadIdx.x >> 5] = pr;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += part[q];
+      g[r] = a * a * st->aa + 2.0 * a * bb * t + bb * bb * sums[0];
+    }
   }
 }
 
@@ -934,6 +956,9 @@ __global__ void k_h_identity(double* __restrict__ H, int r) {
 // H = U^T U.  U_base is rewritten once per 64 updates (a cuBLAS DGEMM by M +
 // the sparse terms), instead of a read + write of U every update.
 
+// grid (kDeferCap terms) x (k / 256 pieces of the term's index list): one
+// binary search per thread, so the latency is one search, not k / 256 of
+// them in sequence (expected hits per term: k^2 / v, ~6 at config 5)
 __global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
                                const int32_t* __restrict__ rows_sorted, int k,
                                const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
@@ -947,42 +972,39 @@ __global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
   const int32_t* di = d_idx + (int64_t)sterm * k;
   const double* dv = d_val + (int64_t)sterm * k;
   const double* cs = cmat + (int64_t)sterm * r;
-  for (int base = 0; base < k; base += 256) {
-    if (threadIdx.x == 0) nhit = 0;
-    __syncthreads();
-    const int q = base + threadIdx.x;
-    if (q < k) {
-      const int32_t vox = di[q];
-      int64_t row = -1;
-      if (dense) {
-        row = vox;
-      } else {  // position of vox in the sorted Omega, if present
-        int lo = 0, hi = k - 1;
-        while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
-          const int32_t x = rows_sorted[mid];
-          if (x == vox) {
-            row = mid;
-            break;
-          }
-          if (x < vox) lo = mid + 1;
-          else hi = mid - 1;
+  if (threadIdx.x == 0) nhit = 0;
+  __syncthreads();
+  const int q = blockIdx.y * 256 + threadIdx.x;
+  if (q < k) {
+    const int32_t vox = di[q];
+    int64_t row = -1;
+    if (dense) {
+      row = vox;
+    } else {  // position of vox in the sorted Omega, if present
+      int lo = 0, hi = k - 1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int32_t x = __ldg(rows_sorted + mid);
+        if (x == vox) {
+          row = mid;
+          break;
         }
-      }
-      if (row >= 0) {
-        const int slot = atomicAdd(&nhit, 1);
-        hit_row[slot] = row;
-        hit_val[slot] = dv[q];
+        if (x < vox) lo = mid + 1;
+        else hi = mid - 1;
       }
     }
-    __syncthreads();
-    const int n = nhit;
-    for (int h = 0; h < n; ++h) {  // the block adds d_q c_s^T to the hit rows
-      double* o = out + hit_row[h] * ldo;
-      const double dq = hit_val[h];
-      for (int c = threadIdx.x; c < r; c += blockDim.x) atomicAdd(o + c, dq * cs[c]);
+    if (row >= 0) {
+      const int slot = atomicAdd(&nhit, 1);
+      hit_row[slot] = row;
+      hit_val[slot] = dv[q];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  const int n = nhit;
+  for (int h = 0; h < n; ++h) {  // the block adds d_q c_s^T to the hit rows
+    double* o = out + hit_row[h] * ldo;
+    const double dq = hit_val[h];
+    for (int c = threadIdx.x; c < r; c += blockDim.x) atomicAdd(o + c, dq * cs[c]);
   }
 }
 
@@ -1488,8 +1510,8 @@ cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
 cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
                                 const int32_t* d_idx, const double* d_val, const double* cmat,
                                 const GrouseState* st, int dense, cudaStream_t s) {
-  k_sparse_terms<<<kDeferCap, 256, 0, s>>>(out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st,
-                                           dense);
+  k_sparse_terms<<<dim3(kDeferCap, (unsigned)((k + 255) / 256)), 256, 0, s>>>(
+      out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
   return cudaGetLastError();
 }
 

@@ -290,6 +290,30 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
     return joined
 
 
+def _to_dev_async(draw, dev):
+    """draw() on a host thread, then its upload on a side stream from the
+    same thread (the GPU meanwhile runs GROUSE); the joiner orders the
+    current stream after the copy."""
+    torch = _torch()
+    side = torch.cuda.Stream(dev)
+
+    def work():
+        a = draw()
+        with torch.cuda.stream(side):
+            return _to_dev(a, dev)
+
+    join = _host_async(work)
+
+    def joined():
+        t = join()
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_stream(side)
+        t.record_stream(cur)  # allocated on the side stream, consumed on this one
+        return t
+
+    return joined
+
+
 def _host_array_async(shape):
     """A float64 host array with every page already touched, prepared on a
     host thread while the GPU runs GROUSE (the host is otherwise idle)."""
@@ -467,7 +491,7 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
     init = _basis_init_async(cfg.seed, v, rank, dev)    # host, overlapped with the GPU work below
     gap = None
     if cfg.shift_override is None and cfg.shift_estimator != "residual-sup":
-        gap = _host_async(lambda: draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v))
+        gap = _to_dev_async(lambda: draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v), dev)
     xd = data_to_device(x, dev)
     od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
@@ -511,7 +535,7 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
         m = _complete_max(u32, w32, 0, 0.0, 0.0, cfg.seed, cfg.two_sided, base=t_dev)
         mu = float(m.max().item())
     else:  # max-gap: gaps to synthetic columns with the reference's SHIFT_GAP normals
-        z = _to_dev(gap(), dev)
+        z = gap()
         synth = _complete_max(u32, w32, 0, sigma, 0.0, cfg.seed, cfg.two_sided, znoise=z)
         mu = float(np.mean(training_maxima - synth.cpu().numpy()))
     _mark("shift")
