@@ -515,6 +515,13 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(cudaStreamSynchronize(s));
     if (int rc = flush(hs.nterms)) return rc;
   }
+  if (getenv("RMX_CG_STATS")) {
+    unsigned long long cs[2] = {0, 0};
+    cudaStreamSynchronize(s);
+    cg_stats(cs);
+    fprintf(stderr, "rmx cg: %llu solves, %llu iterations (%.1f per solve)\n", cs[0], cs[1],
+            cs[0] ? (double)cs[1] / (double)cs[0] : 0.0);
+  }
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(ubase, v, r, 0, &drift, stream, st)) return rc;
   const int64_t tcount = (int64_t)passes * ell;

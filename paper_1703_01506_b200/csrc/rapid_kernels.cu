@@ -476,6 +476,7 @@ __device__ __forceinline__ void cg_block_reduce3(double a, double b, double c, d
 // Post this CTA's rows of `v` (nr values) into every CTA's `full` and this
 // CTA's totals (a, b, c) into every CTA's slot row `me`, then one cluster
 // barrier; returns the cluster sums (same order, same bits on every CTA).
+template <int NC>
 __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, double* full,
                                             double a, double b, double c, double* slots,
                                             double* wsum, double& A, double& B, double& C) {
@@ -485,32 +486,32 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, dou
   const int tid = threadIdx.x;
   if (v && tid < 8 * 32) {  // thread (dst = tid / 16 ... ): rows i = lane16, lane16 + 16, ..
     const int dst = tid >> 4, sub = tid & 15;  // 16 threads per destination CTA pair
-    for (int d = dst; d < kCgCtas; d += 16)
+    for (int d = dst; d < NC; d += 16)
       for (int i = sub; i < nr; i += 16) st_cluster_f64(full + r0 + i, d, v[i]);
   }
-  if (tid < kCgCtas) {
+  if (tid < NC) {
     st_cluster_f64(slots + 3 * me, tid, ta);
     st_cluster_f64(slots + 3 * me + 1, tid, tb);
     st_cluster_f64(slots + 3 * me + 2, tid, tc);
   }
   cluster_sync();
-  // every warp sums the kCgCtas partials with the same shuffle tree: the
+  // every warp sums the NC partials with the same shuffle tree: the
   // same bits on every CTA (they all take the same convergence decision)
-  static_assert(kCgCtas <= 32 && (kCgCtas & (kCgCtas - 1)) == 0, "power-of-2 cluster");
+  static_assert(NC <= 32 && (NC & (NC - 1)) == 0, "power-of-2 cluster");
   const int lane = tid & 31;
   double sa = 0.0, sb = 0.0, sc = 0.0;
-  if (lane < kCgCtas) {
+  if (lane < NC) {
     sa = slots[3 * lane];
     sb = slots[3 * lane + 1];
     sc = slots[3 * lane + 2];
   }
 #pragma unroll
-  for (int o = kCgCtas / 2; o > 0; o >>= 1) {
+  for (int o = NC / 2; o > 0; o >>= 1) {
     sa += __shfl_xor_sync(0xffffffffu, sa, o);
     sb += __shfl_xor_sync(0xffffffffu, sb, o);
     sc += __shfl_xor_sync(0xffffffffu, sc, o);
   }
-  // lanes >= kCgCtas summed zeros: every thread takes lane 0's totals
+  // lanes >= NC summed zeros: every thread takes lane 0's totals
   A = __shfl_sync(0xffffffffu, sa, 0);
   B = __shfl_sync(0xffffffffu, sb, 0);
   C = __shfl_sync(0xffffffffu, sc, 0);
@@ -531,13 +532,16 @@ __device__ __forceinline__ void cg_matvec(const double* Gs, int nr, int r, const
   __syncthreads();
 }
 
+__device__ unsigned long long g_cg_iters[2];  // (solves, iterations): RMX_CG_STATS diagnostics
+
+template <int NC>
 __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
                                                          double* __restrict__ w_out,
                                                          int32_t* __restrict__ flag,
                                                          double* __restrict__ resid2, double tol,
                                                          double* __restrict__ x0) {
   extern __shared__ double cs[];
-  const int R = (r + kCgCtas - 1) / kCgCtas;  // rows per CTA
+  const int R = (r + NC - 1) / NC;  // rows per CTA
   const uint32_t me = cluster_ctarank();
   const int r0 = (int)me * R, nr = max(0, min(R, r - r0));
   double* Gs = cs;                       // nr x r
@@ -546,8 +550,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   double *x = vec, *rv = vec + R, *u = vec + 2 * R, *w = vec + 3 * R, *m = vec + 4 * R,
          *nv = vec + 5 * R, *z = vec + 6 * R, *q = vec + 7 * R, *sv = vec + 8 * R,
          *p = vec + 9 * R, *dinv = vec + 10 * R;
-  double* slots = vec + 11 * R;          // 2 x kCgCtas x 3 partials, by parity
-  double* wsum = slots + 6 * kCgCtas;    // 3 x warps
+  double* slots = vec + 11 * R;          // 2 x NC x 3 partials, by parity
+  double* wsum = slots + 6 * NC;    // 3 x warps
   const int ld = r + 1;
   const int tid = threadIdx.x;
   for (int e = tid; e < nr * r; e += kCgThreads) {
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   int par = 0;
   double BB, d0, d1;
   if (x0) {  // r = b - A x0
-    cg_exchange(x, nr, r0, full + par * r, pb, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum, BB,
+    cg_exchange<NC>(x, nr, r0, full + par * r, pb, 0.0, 0.0, slots + par * 3 * NC, wsum, BB,
                 d0, d1);
     cg_matvec(Gs, nr, r, full + par * r, nv);
     for (int i = tid; i < nr; i += kCgThreads) rv[i] -= nv[i];
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   for (int i = tid; i < nr; i += kCgThreads) u[i] = rv[i] * dinv[i];
   __syncthreads();
   // w = A u (and |b|^2 when not yet reduced)
-  cg_exchange(u, nr, r0, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum,
+  cg_exchange<NC>(u, nr, r0, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * NC, wsum,
               d0, d1, d1);
   if (!x0) BB = d0;
   cg_matvec(Gs, nr, r, full + par * r, w);
@@ -596,7 +600,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       m[i] = w[i] * dinv[i];
     }
     double GAM, DEL, RR;
-    cg_exchange(m, nr, r0, full + par * r, pg, pd, pr, slots + par * 3 * kCgCtas, wsum, GAM, DEL,
+    cg_exchange<NC>(m, nr, r0, full + par * r, pg, pd, pr, slots + par * 3 * NC, wsum, GAM, DEL,
                 RR);
     const int used = par;
     par ^= 1;  // every exchange flips the buffers (also on the way out)
@@ -627,10 +631,11 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       u[i] = fma(-alpha, q[i], u[i]);
       w[i] = fma(-alpha, z[i], w[i]);
     }
-    __syncthreads();
+    // no barrier: the next iteration's partial sums read only this thread's
+    // rows, and cg_exchange's block reduction syncs before the rows are posted
   }
   // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
-  cg_exchange(x, nr, r0, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * kCgCtas, wsum, d0, d1,
+  cg_exchange<NC>(x, nr, r0, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * NC, wsum, d0, d1,
               d1);
   cg_matvec(Gs, nr, r, full + par * r, nv);
   par ^= 1;
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     if (x0) x0[r0 + i] = x[i];
   }
   double TR, WW, BW;
-  cg_exchange(nullptr, 0, r0, nullptr, ptr, pw, pbw, slots + par * 3 * kCgCtas, wsum, TR, WW, BW);
+  cg_exchange<NC>(nullptr, 0, r0, nullptr, ptr, pw, pbw, slots + par * 3 * NC, wsum, TR, WW, BW);
   if (me == 0 && tid == 0) {
     if (resid2) {
       resid2[0] = G[(int64_t)r * ld + r] - BW;
@@ -654,6 +659,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       resid2[3] = 1.0;
     }
     if (flag) flag[0] = (converged && (BB == 0.0 || TR <= 16.0 * stop)) ? 0 : 1;
+    atomicAdd(&g_cg_iters[0], 1ull);
+    atomicAdd(&g_cg_iters[1], (unsigned long long)it);
   }
   cluster_sync();  // no CTA exits while others may still write into its smem
 }
@@ -1408,37 +1415,54 @@ cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, doubl
   return cudaGetLastError();
 }
 
-size_t cg_smem_bytes(int r) {
-  const int R = (r + kCgCtas - 1) / kCgCtas;
-  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * kCgCtas + 3 * (kCgThreads / 32)) *
+int cg_ctas() {  // cluster size of the GROUSE solve: 16 (default) or 8 (RMX_CG_CTAS=8)
+  static const int c = [] {
+    const char* e = getenv("RMX_CG_CTAS");
+    return (e && atoi(e) == 8) ? 8 : kCgCtas;
+  }();
+  return c;
+}
+
+size_t cg_smem_bytes_c(int r, int C) {
+  const int R = (r + C - 1) / C;
+  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * C + 3 * (kCgThreads / 32)) *
          sizeof(double);
 }
 
+size_t cg_smem_bytes(int r) { return cg_smem_bytes_c(r, cg_ctas()); }
+
 bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
 
-cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                            double tol, double* x0, cudaStream_t s) {
-  const size_t smem = cg_smem_bytes(r);
-  cudaError_t e = cudaFuncSetAttribute(k_cg_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int C>
+cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* flag,
+                              double* resid2, double tol, double* x0, cudaStream_t s) {
+  const size_t smem = cg_smem_bytes_c(r, C);
+  cudaError_t e = cudaFuncSetAttribute(k_cg_solve<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  if (kCgCtas > 8) {
-    e = cudaFuncSetAttribute(k_cg_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k_cg_solve<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(kCgCtas);
+  cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(kCgThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCgCtas;
+  attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_cg_solve, G, r, w_out, flag, resid2, tol, x0);
+  return cudaLaunchKernelEx(&cfg, k_cg_solve<C>, G, r, w_out, flag, resid2, tol, x0);
+}
+
+cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
+                            double tol, double* x0, cudaStream_t s) {
+  return cg_ctas() == 8 ? launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s)
+                        : launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
@@ -1567,6 +1591,10 @@ cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseSt
   const int64_t n = (int64_t)r * std::max(r, kDeferCap);
   k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, X, Yt, r, st);
   return cudaGetLastError();
+}
+
+void cg_stats(unsigned long long out[2]) {
+  cudaMemcpyFromSymbol(out, g_cg_iters, sizeof(unsigned long long) * 2);
 }
 
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
