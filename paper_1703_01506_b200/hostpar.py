@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import mmap
 import os
+import threading
 
 import numpy as np
 
@@ -39,7 +40,10 @@ def fill_rows(shape, dtype, row_fn, nrows: int, workers: int | None = None) -> n
         with ThreadPoolExecutor(max_workers=workers) as ex:
             list(ex.map(one, range(nrows)))
         return out
-    if workers <= 1 or nrows < _MIN_PARALLEL_ROWS or not hasattr(os, "fork") or nbytes == 0:
+    # no fork while other threads run (run_rapid's host draws): a child
+    # could inherit a lock one of them holds
+    if (workers <= 1 or nrows < _MIN_PARALLEL_ROWS or not hasattr(os, "fork") or nbytes == 0
+            or threading.active_count() > 1):
         out = np.empty(out_shape, dtype=dtype)
         for i in range(nrows):
             out[i] = row_fn(i)

@@ -206,6 +206,30 @@ def rapid():
     np.savez_compressed(os.path.join(HERE, "rapid_cases.npz"), **out)
 
 
+def rapid_degenerate():
+    """A voxel whose within-group variances vanish under a recovery
+    permutation (values {1, 1, 2 | 1, 2, 2}, split 1/2 by some shuffle) but
+    not under the training ones: the reference raises DegenerateVoxelError
+    from recover() (rapid.py:166 -> teststat.py:42-49) with the flat index
+    into the span's (count x k) block."""
+    g = np.random.default_rng(5)
+    x = f32(g.standard_normal((10, 6)))
+    x[3] = [1, 1, 2, 1, 2, 2]
+    seed = 1
+    cfg = R.RunConfig(permutations=40, seed=seed, engine="rapid", training_columns=3, rank=2,
+                      sample_rate=1.0, max_passes=3)
+    dm = R.DataMatrix(x, 3, 3)
+    model, _, _ = R.train(dm, cfg)
+    try:
+        R.recover(dm, model, cfg.plan_for(dm), cfg)
+        raise SystemExit("expected a degenerate voxel in recovery")
+    except R.DegenerateVoxelError as e:
+        voxel, mean_diff, msg = e.voxel, e.mean_diff, str(e)
+    np.savez_compressed(os.path.join(HERE, "rapid_degenerate.npz"), x=x.astype(np.float32),
+                        meta=np.array([40, seed, 3, 2, 3], dtype=np.int64), voxel=np.array(voxel),
+                        mean_diff=np.array(mean_diff), msg=np.array(msg))
+
+
 def matio():
     """Files written by the reference's matio and the reference's error
     messages for malformed files (path replaced by <PATH>)."""
@@ -285,6 +309,7 @@ if __name__ == "__main__":
     c1()
     teststat()
     rapid()
+    rapid_degenerate()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

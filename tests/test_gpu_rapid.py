@@ -193,3 +193,47 @@ def test_tensor_core_gram_lsq_matches_fp64(v, r, k, B):
     err = np.abs(W[ok] - W0[ok]).max() / np.abs(W0[ok]).max()
     assert err < 1e-10, err
     assert stats[1] == 1, stats  # only the rank-deficient system was re-solved in fp64
+
+
+def test_run_rapid_prefetched_recovery_and_pending_basis():
+    """run_rapid computes recovery's basis-independent inputs during training
+    and copies the basis to the host behind recovery (rapid_engine.py
+    _RecoverInputs / PendingBasis): the maxima equal a plain recover() with
+    the same model, and the host basis equals the device basis bit for bit
+    (v x r x 8 = 38 MB: two 32 MB copy blocks)."""
+    from paper_1703_01506_b200.domain import PendingBasis
+
+    x = _data(16000, 150, 150, seed=21)
+    cfg = rmx.RunConfig(permutations=400, seed=77, engine="rapid", training_columns=300, rank=300,
+                        sample_rate=0.02, max_passes=2)
+    null, model, counters = rmx.run_rapid(x, cfg)
+    assert isinstance(model.basis, PendingBasis)
+    u_dev = model._rmx_dev[1].cpu().numpy()
+    assert model.basis.matrix.shape == (16000, 300)
+    assert np.array_equal(model.basis.matrix, u_dev)
+    assert model.basis.orthonormality_error() < 1e-10
+    again, rec = rmx.recover(x, model, cfg.plan_for(x), cfg)
+    assert np.array_equal(null.maxima, again.maxima)
+    assert rec["subsampled_statistic_evaluations"] == counters["subsampled_statistic_evaluations"]
+
+
+@pytest.mark.parametrize("entry", ["recover", "run_rapid"])
+def test_degenerate_voxel_in_recovery_matches_reference(entry):
+    """A voxel degenerate under a recovery permutation only: recover() and
+    run_rapid() (whose recovery statistics are computed during training)
+    raise the reference's DegenerateVoxelError -- same flat block index,
+    mean difference and message (tests/golden/rapid_degenerate.npz)."""
+    d = np.load(os.path.join(GOLD, "rapid_degenerate.npz"))
+    L, seed, ell, rank, passes = (int(a) for a in d["meta"])
+    x = rmx.DataMatrix(d["x"].astype(np.float64), 3, 3)
+    cfg = rmx.RunConfig(permutations=L, seed=seed, engine="rapid", training_columns=ell,
+                        rank=rank, sample_rate=1.0, max_passes=passes)
+    with pytest.raises(rmx.DegenerateVoxelError) as err:
+        if entry == "recover":
+            model, _, _ = rmx.train(x, cfg)
+            rmx.recover(x, model, cfg.plan_for(x), cfg)
+        else:
+            rmx.run_rapid(x, cfg)
+    assert err.value.voxel == int(d["voxel"])
+    assert err.value.mean_diff == float(d["mean_diff"])
+    assert str(err.value) == str(d["msg"])
