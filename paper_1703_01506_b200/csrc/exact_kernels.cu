@@ -433,7 +433,7 @@ constexpr int kStageMaxN = 2048;  // rows up to this many subjects are staged in
 // numpy-pairwise chains spread over its lanes (welch_exact_warp: same bits);
 // the owning lane keeps the result.
 template <bool STAGE>
-__global__ void __launch_bounds__(32 * kRefineWarps) k_refine(RefineArgs a) {
+__global__ void __launch_bounds__(32 * kRefineWarps, 4) k_refine(RefineArgs a) {
   extern __shared__ __align__(16) unsigned char refine_smem[];
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
   NpWarpScratch* sc = reinterpret_cast<NpWarpScratch*>(refine_smem) + w;
