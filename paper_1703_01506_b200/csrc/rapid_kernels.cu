@@ -518,16 +518,29 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, dou
   __syncthreads();  // wsum reusable
 }
 
-// out[i] = G_rows[i] . full (one warp per row)
+// out[i] = G_rows[i] . full: warp wid owns rows wid + q W (W warps), four
+// rows at a time as independent fma chains (the per-row order -- lane
+// strided, then the butterfly -- is unchanged, so are the bits)
 __device__ __forceinline__ void cg_matvec(const double* Gs, int nr, int r, const double* full,
                                           double* out) {
+  constexpr int W = kCgThreads / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = wid; i < nr; i += kCgThreads / 32) {
-    const double* gi = Gs + (size_t)i * r;
-    double acc = 0.0;
-    for (int j = lane; j < r; j += 32) acc = fma(gi[j], full[j], acc);
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[i] = acc;
+  for (int i0 = wid; i0 < nr; i0 += 4 * W) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = lane; j < r; j += 32) {
+      const double f = full[j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + q * W < nr) acc[q] = fma(Gs[(size_t)(i0 + q * W) * r + j], f, acc[q]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + q * W < nr) out[i0 + q * W] = acc[q];
   }
   __syncthreads();
 }
