@@ -433,6 +433,18 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(T* __restr
 constexpr int kCgCtas = 16;  // non-portable cluster size (GPCs hold >= 16 SMs)
 constexpr int kCgThreads = 256;
 
+// remote store that signals the destination CTA's mbarrier (complete_tx of
+// 8 bytes): the receiver waits on its own barrier, no cluster-wide barrier
+__device__ __forceinline__ void st_async_f64(double* local_ptr, uint32_t rank, double v,
+                                             uint64_t* local_bar) {
+  uint32_t raddr, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local_ptr)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+               ::"r"(raddr), "d"(v), "r"(rbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank, double v) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_ptr)), "r"(rank));
@@ -477,24 +489,33 @@ __device__ __forceinline__ void cg_block_reduce3(double a, double b, double c, d
 // CTA's totals (a, b, c) into every CTA's slot row `me`, then one cluster
 // barrier; returns the cluster sums (same order, same bits on every CTA).
 template <int NC>
-__device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, double* full,
+__device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, int rtot, double* full,
                                             double a, double b, double c, double* slots,
-                                            double* wsum, double& A, double& B, double& C) {
+                                            double* wsum, uint64_t* bars, int par, uint32_t& xph,
+                                            double& A, double& B, double& C) {
   const uint32_t me = cluster_ctarank();
   double ta, tb, tc;
   cg_block_reduce3(a, b, c, wsum, ta, tb, tc);
   const int tid = threadIdx.x;
+  uint64_t* bar = bars + par;
+  // this CTA receives every CTA's rows (rtot values when v is posted) and
+  // NC x 3 partials; the arrival may follow the data (tx-count goes negative)
+  if (tid == 0) mbar_expect_tx(bar, (uint32_t)(((v ? rtot : 0) + 3 * NC) * sizeof(double)));
   if (v && tid < 8 * 32) {  // thread (dst = tid / 16 ... ): rows i = lane16, lane16 + 16, ..
-    const int dst = tid >> 4, sub = tid & 15;  // 16 threads per destination CTA pair
+    const int dst = tid >> 4, sub = tid & 15;  // 16 threads per destination CTA
     for (int d = dst; d < NC; d += 16)
-      for (int i = sub; i < nr; i += 16) st_cluster_f64(full + r0 + i, d, v[i]);
+      for (int i = sub; i < nr; i += 16) st_async_f64(full + r0 + i, d, v[i], bar);
   }
   if (tid < NC) {
-    st_cluster_f64(slots + 3 * me, tid, ta);
-    st_cluster_f64(slots + 3 * me + 1, tid, tb);
-    st_cluster_f64(slots + 3 * me + 2, tid, tc);
+    st_async_f64(slots + 3 * me, tid, ta, bar);
+    st_async_f64(slots + 3 * me + 1, tid, tb, bar);
+    st_async_f64(slots + 3 * me + 2, tid, tc, bar);
   }
-  cluster_sync();
+  // a sender can be at most one exchange ahead of this CTA: it needs this
+  // CTA's next post before its own next-but-one wait, so the two parity
+  // buffers/barriers never see data of two exchanges at once
+  mbar_wait(bar, (xph >> par) & 1u);
+  xph ^= 1u << par;
   // every warp sums the NC partials with the same shuffle tree: the
   // same bits on every CTA (they all take the same convergence decision)
   static_assert(NC <= 32 && (NC & (NC - 1)) == 0, "power-of-2 cluster");
@@ -565,8 +586,15 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
          *p = vec + 9 * R, *dinv = vec + 10 * R;
   double* slots = vec + 11 * R;          // 2 x NC x 3 partials, by parity
   double* wsum = slots + 6 * NC;    // 3 x warps
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(wsum + 3 * (kCgThreads / 32));  // 2, by parity
+  uint32_t xph = 0;                      // phase bit of each exchange barrier
   const int ld = r + 1;
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_mbar_init();
+  }
   for (int e = tid; e < nr * r; e += kCgThreads) {
     const int i = e / r, j = e % r;
     Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
@@ -581,12 +609,12 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     pb += bi * bi;
     z[i] = q[i] = sv[i] = p[i] = 0.0;
   }
-  __syncthreads();
+  cluster_sync();  // every CTA's exchange barriers are initialised before any st.async
   int par = 0;
   double BB, d0, d1;
   if (x0) {  // r = b - A x0
-    cg_exchange<NC>(x, nr, r0, full + par * r, pb, 0.0, 0.0, slots + par * 3 * NC, wsum, BB,
-                d0, d1);
+    cg_exchange<NC>(x, nr, r0, r, full + par * r, pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
+                    par, xph, BB, d0, d1);
     cg_matvec(Gs, nr, r, full + par * r, nv);
     for (int i = tid; i < nr; i += kCgThreads) rv[i] -= nv[i];
     par ^= 1;
@@ -595,8 +623,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   for (int i = tid; i < nr; i += kCgThreads) u[i] = rv[i] * dinv[i];
   __syncthreads();
   // w = A u (and |b|^2 when not yet reduced)
-  cg_exchange<NC>(u, nr, r0, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * NC, wsum,
-              d0, d1, d1);
+  cg_exchange<NC>(u, nr, r0, r, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
+                    par, xph, d0, d1, d1);
   if (!x0) BB = d0;
   cg_matvec(Gs, nr, r, full + par * r, w);
   par ^= 1;
@@ -613,8 +641,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       m[i] = w[i] * dinv[i];
     }
     double GAM, DEL, RR;
-    cg_exchange<NC>(m, nr, r0, full + par * r, pg, pd, pr, slots + par * 3 * NC, wsum, GAM, DEL,
-                RR);
+    cg_exchange<NC>(m, nr, r0, r, full + par * r, pg, pd, pr, slots + par * 3 * NC, wsum, xbar,
+                    par, xph, GAM, DEL, RR);
     const int used = par;
     par ^= 1;  // every exchange flips the buffers (also on the way out)
     if (RR <= stop) {
@@ -648,8 +676,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     // rows, and cg_exchange's block reduction syncs before the rows are posted
   }
   // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
-  cg_exchange<NC>(x, nr, r0, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * NC, wsum, d0, d1,
-              d1);
+  cg_exchange<NC>(x, nr, r0, r, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
+                    par, xph, d0, d1, d1);
   cg_matvec(Gs, nr, r, full + par * r, nv);
   par ^= 1;
   double ptr = 0.0, pw = 0.0, pbw = 0.0;
@@ -663,7 +691,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     if (x0) x0[r0 + i] = x[i];
   }
   double TR, WW, BW;
-  cg_exchange<NC>(nullptr, 0, r0, nullptr, ptr, pw, pbw, slots + par * 3 * NC, wsum, TR, WW, BW);
+  cg_exchange<NC>(nullptr, 0, r0, r, nullptr, ptr, pw, pbw, slots + par * 3 * NC, wsum, xbar,
+                    par, xph, TR, WW, BW);
   if (me == 0 && tid == 0) {
     if (resid2) {
       resid2[0] = G[(int64_t)r * ld + r] - BW;
@@ -1438,8 +1467,8 @@ int cg_ctas() {  // cluster size of the GROUSE solve: 16 (default) or 8 (RMX_CG_
 
 size_t cg_smem_bytes_c(int r, int C) {
   const int R = (r + C - 1) / C;
-  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * C + 3 * (kCgThreads / 32)) *
-         sizeof(double);
+  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * C + 3 * (kCgThreads / 32) + 2) *
+         sizeof(double);  // + the two exchange mbarriers
 }
 
 size_t cg_smem_bytes(int r) { return cg_smem_bytes_c(r, cg_ctas()); }
