@@ -264,7 +264,9 @@ def main():
 
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
-    if world > 1:
+    # RMX_BENCH_FORCE_DIST=1 (tests): the multi-rank plumbing at world size 1
+    dist_on = world > 1 or os.environ.get("RMX_BENCH_FORCE_DIST") == "1"
+    if dist_on:
         dist.init_process_group("nccl", device_id=device)
 
     from paper_1703_01506_b200 import DataMatrix, PermutationPlan
@@ -293,7 +295,7 @@ def main():
         l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=device)
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -335,7 +337,7 @@ def main():
     fin_ms = [e2.elapsed_time(e3) for (_, _, e2, e3) in ev]
     tot = torch.tensor([sum(step_ms) / len(step_ms), sum(tfill_ms) / len(tfill_ms)],
                        dtype=torch.float64, device=device)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_per_step, tfill_avg = float(tot[0]), float(tot[1])
     value = L * v / (ms_per_step / 1e3)
@@ -404,7 +406,7 @@ def main():
         for k in range(args.warmup + args.steps):
             barrier()
             t0 = time.perf_counter()
-            if world == 1:
+            if not dist_on:
                 res = run_naive_ex(x_host, plan, two_sided=cfg.two_sided)
                 _ = res.maxima
             else:
@@ -420,7 +422,7 @@ def main():
             if k >= args.warmup:
                 times.append(dt)
         t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=device)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": L * v / float(t[0]), "unit": UNIT,
                "h2d_bytes_per_step": h2d_bytes,
@@ -478,7 +480,7 @@ def main():
             "rapid": rapid,
         }
         print(json.dumps(line))
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 
