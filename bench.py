@@ -410,13 +410,12 @@ def main():
                 res = run_naive_ex(x_host, plan, two_sided=cfg.two_sided)
                 _ = res.maxima
             else:
-                from paper_1703_01506_b200.naive_engine import data_to_device
+                # each rank: its permutation shard from the host X (upload
+                # overlapped with K0/K1, labels generated on its GPU), then
+                # the all-gather of (max, argmax)
+                from paper_1703_01506_b200.shard import run_naive_distributed
 
-                xd = data_to_device(x_host, device)
-                # ShardedNaive generates this rank's label rows on the GPU
-                sh2 = ShardedNaive(xd, cfg.n1, plan, cfg.two_sided)
-                m, a = sh2.step()
-                m.cpu(), a.cpu()
+                run_naive_distributed(x_host, plan, two_sided=cfg.two_sided)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if k >= args.warmup:
@@ -429,7 +428,7 @@ def main():
                "x_host": "float32 v x n, page-locked (upcast to float64 on the device, exact)",
                "labels": "generated on the GPU inside the timed region (rmx_plan_orders)",
                "d2h_bytes_per_step": int(L * 12), "s_per_step": float(t[0]),
-               "api": "paper_1703_01506_b200.run_naive_ex (N=1) / ShardedNaive (N>1)"}
+               "api": "paper_1703_01506_b200.run_naive_ex (N=1) / run_naive_distributed (N>1)"}
 
     # ---------------- CPU baseline (rank 0, N=1) ------------------------------
     cpu = None

@@ -172,6 +172,30 @@ int rmx_naive_maxnull_host_plan_f32(const float *x_host, int64_t v, int32_t n, i
                                     int32_t *argmax_dev, void *workspace, size_t workspace_bytes,
                                     void *stream, rmx_status *st, rmx_naive_stats *stats);
 
+/* _host_plan(_f32) over the permutation range [perm_base, perm_base + L) of
+ * the plan: one rank's shard of a multi-GPU run, the labels of
+ * the global indices generated on the device, X uploaded and overlapped as
+ * above; max_host/argmax_host get the L local entries.  The statistic of a
+ * permutation depends only on its labels, so every shard reproduces its
+ * slice of the single-GPU result bit for bit.  Replaces the per-range body
+ * of reference naive.py:49-57 (_max_block over [lo, hi)) for a process
+ * that owns that range. */
+int rmx_naive_maxnull_host_plan_range(const double *x_host, int64_t v, int32_t n, int32_t n1,
+                                      uint64_t plan_seed, int64_t perm_base, int64_t L,
+                                      int32_t two_sided, double *max_host, int32_t *argmax_host,
+                                      double *x_dev, int16_t *orders_dev, double *max_dev,
+                                      int32_t *argmax_dev, void *workspace,
+                                      size_t workspace_bytes, void *stream, rmx_status *st,
+                                      rmx_naive_stats *stats);
+int rmx_naive_maxnull_host_plan_range_f32(const float *x_host, int64_t v, int32_t n, int32_t n1,
+                                          uint64_t plan_seed, int64_t perm_base, int64_t L,
+                                          int32_t two_sided, double *max_host,
+                                          int32_t *argmax_host, float *x32_dev, double *x_dev,
+                                          int16_t *orders_dev, double *max_dev,
+                                          int32_t *argmax_dev, void *workspace,
+                                          size_t workspace_bytes, void *stream, rmx_status *st,
+                                          rmx_naive_stats *stats);
+
 /* ---------------------------------------------------------------- .mat0 I/O
  * The reference's binary matrix format (matio.py:23-91): 44-byte header
  * "<8sIQQQQ" = magic "RMXMAT0\0", u32 version (1), u64 rows, cols, n1, n2;

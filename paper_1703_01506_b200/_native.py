@@ -76,6 +76,8 @@ EXPORTS = (
     "rmx_naive_maxnull_host_plan",
     "rmx_naive_maxnull_host_f32",
     "rmx_naive_maxnull_host_plan_f32",
+    "rmx_naive_maxnull_host_plan_range",
+    "rmx_naive_maxnull_host_plan_range_f32",
     "rmx_plan_orders",
     "rmx_omega_draws",
     "rmx_naive_prepare",
@@ -129,6 +131,12 @@ _SIGS = {
     "rmx_naive_maxnull_host_plan_f32": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i32, _vp,
                                          _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
                                         ctypes.c_int),
+    "rmx_naive_maxnull_host_plan_range": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i64, _i32,
+                                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
+                                          ctypes.c_int),
+    "rmx_naive_maxnull_host_plan_range_f32": ([_vp, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i64,
+                                               _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                               _vp, _SP, _NP], ctypes.c_int),
     "rmx_plan_orders": ([ctypes.c_uint64, _i64, _i64, _i32, _vp, _vp, _SP], ctypes.c_int),
     "rmx_omega_draws": ([ctypes.c_uint64, _i32, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _SP],
                         ctypes.c_int),

@@ -702,14 +702,14 @@ namespace {
 // x_host32 (fp32, staged in x32_dev).
 int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
                     int64_t v, int32_t n, int32_t n1,
-                    const int16_t* orders_host, const uint64_t* plan_seed, int64_t L,
-                    int32_t two_sided, double* max_host, int32_t* argmax_host, double* x_dev,
+                    const int16_t* orders_host, const uint64_t* plan_seed, int64_t perm_base,
+                    int64_t L, int32_t two_sided, double* max_host, int32_t* argmax_host, double* x_dev,
                     int16_t* orders_dev, double* max_dev, int32_t* argmax_dev, void* workspace,
                     size_t workspace_bytes, void* stream, rmx_status* st,
                     rmx_naive_stats* stats) {
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
-  if (plan_seed && (n > 32767 || L > 0xFFFFFFFFLL))
+  if (plan_seed && (n > 32767 || perm_base < 0 || perm_base + L > 0xFFFFFFFFLL))
     return set_status(st, RMX_E_USAGE, "plan of %lld permutations of n=%d not representable",
                       (long long)L, n);
   if ((!x_host && !(x_host32 && x32_dev)) || !max_host || !argmax_host || !x_dev ||
@@ -737,7 +737,7 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
     }
     if (orders_host)
       RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, s));
-    if (plan_seed) RMX_CUDA(launch_plan_orders(*plan_seed, 0, L, n, orders_dev, s));
+    if (plan_seed) RMX_CUDA(launch_plan_orders(*plan_seed, perm_base, L, n, orders_dev, s));
     if (int rc = rmx_naive_maxnull(x_dev, v, n, n1, orders_dev, L, two_sided, max_dev, argmax_dev,
                                    workspace, workspace_bytes, stream, st, stats))
       return rc;
@@ -780,7 +780,7 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
   if (orders_host)
     RMX_CUDA(cudaMemcpyAsync(orders_dev, orders_host, obytes, cudaMemcpyHostToDevice, S.cp));
   if (plan_seed) {
-    RMX_CUDA(launch_plan_orders(*plan_seed, 0, L, n, orders_dev, S.pp));
+    RMX_CUDA(launch_plan_orders(*plan_seed, perm_base, L, n, orders_dev, S.pp));
     RMX_CUDA(cudaEventRecord(e_ord, S.pp));
   } else {
     RMX_CUDA(cudaEventRecord(e_ord, S.cp));
@@ -830,7 +830,7 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                            int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                            void* workspace, size_t workspace_bytes, void* stream,
                            rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, orders_host, nullptr, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, orders_host, nullptr, 0, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -841,7 +841,7 @@ int rmx_naive_maxnull_host_plan(const double* x_host, int64_t v, int32_t n, int3
                                 int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                                 void* workspace, size_t workspace_bytes, void* stream,
                                 rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, 0, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -853,7 +853,7 @@ int rmx_naive_maxnull_host_f32(const float* x_host, int64_t v, int32_t n, int32_
                                int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
                                void* stream, rmx_status* st, rmx_naive_stats* stats) {
   if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
-  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, orders_host, nullptr, L, two_sided,
+  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, orders_host, nullptr, 0, L, two_sided,
                          max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -865,9 +865,35 @@ int rmx_naive_maxnull_host_plan_f32(const float* x_host, int64_t v, int32_t n, i
                                     int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
                                     void* stream, rmx_status* st, rmx_naive_stats* stats) {
   if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
-  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, L, two_sided,
+  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, 0, L, two_sided,
                          max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_host_plan_range(const double* x_host, int64_t v, int32_t n, int32_t n1,
+                                      uint64_t plan_seed, int64_t perm_base, int64_t L,
+                                      int32_t two_sided, double* max_host, int32_t* argmax_host,
+                                      double* x_dev, int16_t* orders_dev, double* max_dev,
+                                      int32_t* argmax_dev, void* workspace,
+                                      size_t workspace_bytes, void* stream, rmx_status* st,
+                                      rmx_naive_stats* stats) {
+  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, perm_base, L,
+                         two_sided, max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev,
+                         workspace, workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_host_plan_range_f32(const float* x_host, int64_t v, int32_t n, int32_t n1,
+                                          uint64_t plan_seed, int64_t perm_base, int64_t L,
+                                          int32_t two_sided, double* max_host,
+                                          int32_t* argmax_host, float* x32_dev, double* x_dev,
+                                          int16_t* orders_dev, double* max_dev,
+                                          int32_t* argmax_dev, void* workspace,
+                                          size_t workspace_bytes, void* stream, rmx_status* st,
+                                          rmx_naive_stats* stats) {
+  if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
+  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, perm_base, L,
+                         two_sided, max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev,
+                         workspace, workspace_bytes, stream, st, stats);
 }
 
 int rmx_plan_orders(uint64_t seed, int64_t lo, int64_t count, int32_t n, int16_t* out,

@@ -219,14 +219,15 @@ def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,
     return NaiveResult(mx, am.astype(np.int64), job.stats.as_dict(), T)
 
 
-def _run_from_host(x, plan, two_sided: bool, device):
+def _run_from_host(x, plan, two_sided: bool, device, lo: int = 0, hi: Optional[int] = None):
     """One rmx_naive_maxnull_host_plan(_f32) call: host X in (page-locked in
     place; the float32 source when the DataMatrix keeps one),
     the plan's labels generated on the device from its seed (rmx_plan_orders'
     streams, bit-identical to numpy) while X's first chunk uploads, the X
     upload overlapped with the engine chunk by chunk, host max/argmax out.
     Returns (max, argmax, job) -- the job keeps the device copies for
-    follow-up work (materialisation)."""
+    follow-up work (materialisation).  [lo, hi): a permutation range of the
+    plan (one rank's shard, rmx_naive_maxnull_host_plan_range*)."""
     import torch
 
     from .hostmem import pinned, pinned_empty
@@ -235,7 +236,9 @@ def _run_from_host(x, plan, two_sided: bool, device):
     f32 = x.float32_values
     xh = pinned(f32 if f32 is not None else x.values)
     v, n = xh.shape
-    L = int(plan.count)
+    hi = int(plan.count) if hi is None else int(hi)
+    L = hi - int(lo)
+    ranged = lo != 0 or hi != int(plan.count)
     if n > 32767:
         raise UsageError(f"subject count {n} exceeds the int16 label format")
     xd = torch.empty((v, n), dtype=torch.float64, device=device)
@@ -248,14 +251,17 @@ def _run_from_host(x, plan, two_sided: bool, device):
     bufs = (nat.ptr(xd), nat.ptr(od), nat.ptr(job.max_out), nat.ptr(job.argmax_out),
             nat.ptr(job.workspace), job.ws_bytes, job._s(), ctypes.byref(job._st),
             ctypes.byref(job.stats))
+    head = (xh.ctypes.data, v, n, int(n1), seed) + ((int(lo),) if ranged else ())
     if f32 is not None:
         x32 = torch.empty((v, n), dtype=torch.float32, device=device)
-        rc = job.lib.rmx_naive_maxnull_host_plan_f32(xh.ctypes.data, v, n, int(n1), seed, *tail,
-                                                     nat.ptr(x32), *bufs)
+        fn = (job.lib.rmx_naive_maxnull_host_plan_range_f32 if ranged
+              else job.lib.rmx_naive_maxnull_host_plan_f32)
+        rc = fn(*head, *tail, nat.ptr(x32), *bufs)
         del x32  # the call is synchronous
     else:
-        rc = job.lib.rmx_naive_maxnull_host_plan(xh.ctypes.data, v, n, int(n1), seed, *tail,
-                                                 *bufs)
+        fn = (job.lib.rmx_naive_maxnull_host_plan_range if ranged
+              else job.lib.rmx_naive_maxnull_host_plan)
+        rc = fn(*head, *tail, *bufs)
     nat.raise_for(rc, job._st)
     return mx.copy(), am.copy(), job
 

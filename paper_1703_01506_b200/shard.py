@@ -112,18 +112,30 @@ class ShardedNaive:
 
 
 def run_naive_distributed(x, plan, two_sided: bool = False, group=None):
-    """Public multi-GPU entry: every rank passes the same (x, plan); returns
-    the full (MaxNull, argmax) on every rank.  Single-process when
+    """Public multi-GPU entry: every rank passes the same host (x, plan) and
+    gets the full (MaxNull, argmax).  Each rank runs its permutation shard
+    through the host-input engine (rmx_naive_maxnull_host_plan_range*: X
+    uploaded chunk by chunk under K0/K1, the shard's labels generated on its
+    GPU), then one all-gather of (max, argmax).  Single-process when
     torch.distributed is not initialised."""
+    import torch
+
     from .domain import MaxNull, as_data_matrix, as_plan
-    from .naive_engine import cuda_device, data_to_device
+    from .naive_engine import _run_from_host, cuda_device
 
     x = as_data_matrix(x)
     plan = as_plan(plan)
     if plan.subjects != x.subjects:
         raise UsageError("plan and data matrix disagree on subject count")
     dev = cuda_device()
-    xd = data_to_device(x, dev)
-    sh = ShardedNaive(xd, x.n1, plan, two_sided, group)
-    m, a = sh.step()
+    rank, world = dist_info(group)
+    L = int(plan.count)
+    lo, hi, per = shard_bounds(L, rank, world)
+    if hi > lo:
+        _, _, job = _run_from_host(x, plan, two_sided, dev, lo, hi)
+        lm, la = job.max_out, job.argmax_out
+    else:
+        lm = torch.empty(0, dtype=torch.float64, device=dev)
+        la = torch.empty(0, dtype=torch.int32, device=dev)
+    m, a = gather_maxima(lm, la, L, per, group)
     return MaxNull(m.cpu().numpy()), a.cpu().numpy().astype(np.int64)

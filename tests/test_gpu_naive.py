@@ -259,3 +259,38 @@ def test_permutation_shards_bit_identical_to_single_gpu(n1, n2):
             am.append(a.cpu().numpy())
         assert np.array_equal(np.concatenate(mx), full.maxima), world
         assert np.array_equal(np.concatenate(am).astype(np.int64), full.argmax), world
+
+
+@pytest.mark.parametrize("f32", [False, True])
+def test_host_range_shards_bit_identical_to_single_gpu(f32):
+    """rmx_naive_maxnull_host_plan_range(_f32), the host-input path each rank
+    of run_naive_distributed runs: every permutation range reproduces its
+    slice of the single-GPU result bit for bit (labels of the global indices
+    generated on the device, X uploaded chunk by chunk), and the public
+    multi-GPU entry at world size 1 equals run_naive_ex."""
+    import torch
+
+    from paper_1703_01506_b200.naive_engine import _run_from_host
+    from paper_1703_01506_b200.shard import run_naive_distributed, shard_bounds
+
+    dev = torch.device("cuda", 0)
+    vals = np.random.default_rng(41).standard_normal((6000, 24)).astype(np.float32)
+    x = rmx.DataMatrix(vals if f32 else vals.astype(np.float64), 12, 12)
+    assert (x.float32_values is not None) == f32
+    L = 900
+    plan = rmx.PermutationPlan(1234, L, 24)
+    full = rmx.run_naive_ex(x, plan)
+    for world in (2, 3, 8):
+        mx, am = [], []
+        for rank in range(world):
+            lo, hi, _ = shard_bounds(L, rank, world)
+            if hi <= lo:
+                continue
+            m, a, _ = _run_from_host(x, plan, False, dev, lo, hi)
+            mx.append(m)
+            am.append(a)
+        assert np.array_equal(np.concatenate(mx), full.maxima), world
+        assert np.array_equal(np.concatenate(am).astype(np.int64), full.argmax), world
+    null, arg = run_naive_distributed(x, plan)
+    assert np.array_equal(null.maxima, full.maxima)
+    assert np.array_equal(arg, full.argmax)
