@@ -202,7 +202,7 @@ __device__ __forceinline__ void chol_block32(T* D, T* rinv, T tiny, int* bad) {
 __host__ __device__ constexpr int chol_panel_rows(int r) { return r > kPW ? r - kPW : 1; }
 
 template <int NT, typename T = double>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_chol_solve(T* __restrict__ G, int r,
+__global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) k_chol_solve(T* __restrict__ G, int r,
                                                    double* __restrict__ w_out,
                                                    int32_t* flag, double* __restrict__ resid2,
                                                    const int32_t* gate = nullptr,
