@@ -420,11 +420,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const double step = 1.0 / (1.0 + (double)tglob / tau);
     const double* trow = t + (int64_t)i * v;
     // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
-    RCUDA(launch_gather_urows_ld(ubase, r, idx, k, ug.p, lu, s));
+    RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, s));
     RBLAS(blas.gemm_rm(k, kDeferCap, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap));
     RBLAS(blas.gemm_rm(k, r, kDeferCap, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1.0));
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
-    RCUDA(launch_gather_vals_aug(trow, idx, k, vals.p, ug.p + r, lu, s));
     RBLAS(blas.gram(k, (int)lu, ug.p, lu, G.p));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
     if (use_cg) {
@@ -434,8 +433,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     } else {
       RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
     }
-    RCUDA(launch_resid(ug.p, lu, r, nullptr, k, vals.p, w.p, resid.p, sums.p, s));
-    RCUDA(launch_defer_vec(H.p, M.p, cmat.p, w.p, r, gst.p, hw.p, mw.p, dots.p, s));
+    RCUDA(launch_resid_defer_vec(ug.p, lu, r, k, vals.p, w.p, resid.p, sums.p, H.p, M.p, cmat.p,
+                                 gst.p, hw.p, mw.p, dots.p, s));
     RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
                                didx.p, dval.p, cmat.p, wn.p,
                                final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));

@@ -67,6 +67,12 @@ cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, i
 // vals[i] = t[idx[i]] and aug[i * ldaug] = the same (the Gram's extra column)
 cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
                                    double* aug, int64_t ldaug, cudaStream_t s);
+cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
+                                   const double* w, double* resid, double* sums, const double* H,
+                                   const double* M, const double* cmat, const GrouseState* st,
+                                   double* hw, double* mw, double* dots, cudaStream_t s);
+cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
+                                     int64_t ldo, const double* t, double* vals, cudaStream_t s);
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
                              double* dots, cudaStream_t s);

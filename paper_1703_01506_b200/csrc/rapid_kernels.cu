@@ -853,12 +853,13 @@ __global__ void __launch_bounds__(256) k_complete_max(
 
 // ------------------------------------------------------------------ GROUSE
 // resid[i] = vals[i] - U[idx[i], :] . w   (k rows, one warp per row)
-__global__ void k_resid(const double* __restrict__ U, int64_t ldu, int r,
-                        const int32_t* __restrict__ idx, int k,
-                        const double* __restrict__ vals, const double* __restrict__ w,
-                        double* __restrict__ resid, double* __restrict__ sums) {
+__device__ __forceinline__ void resid_block(int bid, const double* __restrict__ U, int64_t ldu,
+                                            int r, const int32_t* __restrict__ idx, int k,
+                                            const double* __restrict__ vals,
+                                            const double* __restrict__ w,
+                                            double* __restrict__ resid, double* __restrict__ sums) {
   __shared__ double part[2][8];  // blockDim.x == 256
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
+  const int warp = (bid * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   double ee = 0.0, tt = 0.0;
   if (warp < k) {
     const double* u = U + (int64_t)(idx ? idx[warp] : warp) * ldu;
@@ -884,6 +885,13 @@ __global__ void k_resid(const double* __restrict__ U, int64_t ldu, int r,
     atomicAdd(&sums[0], a);  // |resid|^2
     atomicAdd(&sums[2], b);  // |t_Omega|^2
   }
+}
+
+__global__ void k_resid(const double* __restrict__ U, int64_t ldu, int r,
+                        const int32_t* __restrict__ idx, int k,
+                        const double* __restrict__ vals, const double* __restrict__ w,
+                        double* __restrict__ resid, double* __restrict__ sums) {
+  resid_block(blockIdx.x, U, ldu, r, idx, k, vals, w, resid, sums);
 }
 
 // pred = U w (v rows, one warp per row), sums[1] += |pred|^2
@@ -1069,11 +1077,14 @@ __global__ void k_gather_urows(const double* __restrict__ U, int r, const int32_
 // Per-update matrix-vector products, one warp per output (coalesced rows):
 // hw = H w (for |p|^2 = w.hw and the H update), mw = M w (the M update) and
 // dots[s] = w . c_s for the live terms.
-__global__ void k_defer_vec(const double* __restrict__ H, const double* __restrict__ M,
-                            const double* __restrict__ cmat, const double* __restrict__ w, int r,
-                            const GrouseState* __restrict__ st, double* __restrict__ hw,
-                            double* __restrict__ mw, double* __restrict__ dots) {
-  const int task = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+__device__ __forceinline__ void defer_vec_block(int bid, const double* __restrict__ H,
+                                                const double* __restrict__ M,
+                                                const double* __restrict__ cmat,
+                                                const double* __restrict__ w, int r,
+                                                const GrouseState* __restrict__ st,
+                                                double* __restrict__ hw, double* __restrict__ mw,
+                                                double* __restrict__ dots) {
+  const int task = bid * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const double* row;
   double* out;
@@ -1093,6 +1104,46 @@ __global__ void k_defer_vec(const double* __restrict__ H, const double* __restri
   for (int j = lane; j < r; j += 32) acc = fma(row[j], w[j], acc);
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) *out = acc;
+}
+
+__global__ void k_defer_vec(const double* __restrict__ H, const double* __restrict__ M,
+                            const double* __restrict__ cmat, const double* __restrict__ w, int r,
+                            const GrouseState* __restrict__ st, double* __restrict__ hw,
+                            double* __restrict__ mw, double* __restrict__ dots) {
+  defer_vec_block(blockIdx.x, H, M, cmat, w, r, st, hw, mw, dots);
+}
+
+// one launch for the two independent consumers of the solve: the residual
+// on Omega (blocks [0, nres)) and H w, M w, C w (the rest)
+__global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int r, int k,
+                                  const double* __restrict__ vals, const double* __restrict__ w,
+                                  double* __restrict__ resid, double* __restrict__ sums,
+                                  const double* __restrict__ H, const double* __restrict__ M,
+                                  const double* __restrict__ cmat,
+                                  const GrouseState* __restrict__ st, double* __restrict__ hw,
+                                  double* __restrict__ mw, double* __restrict__ dots, int nres) {
+  if ((int)blockIdx.x < nres)
+    resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums);
+  else
+    defer_vec_block(blockIdx.x - nres, H, M, cmat, w, r, st, hw, mw, dots);
+}
+
+// gathered rows of U (k x r at ld ldo) and, from the threads of column 0,
+// the statistic column t[Omega] into vals and into column r of the rows
+__global__ void k_gather_urows_vals(const double* __restrict__ U, int r,
+                                    const int32_t* __restrict__ idx, int k, double* __restrict__ out,
+                                    int64_t ldo, const double* __restrict__ t,
+                                    double* __restrict__ vals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * r) return;
+  const int i = (int)(e / r), c = (int)(e - (int64_t)i * r);
+  const int64_t row = idx[i];
+  out[(int64_t)i * ldo + c] = U[row * r + c];
+  if (c == 0) {
+    const double x = t[row];
+    vals[i] = x;
+    out[(int64_t)i * ldo + r] = x;
+  }
 }
 
 // decisions as k_grouse_post; the update becomes deferred term nterms
@@ -1598,6 +1649,24 @@ cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, i
 cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
                                    double* aug, int64_t ldaug, cudaStream_t s) {
   k_gather_vals<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(t, idx, k, vals, aug, ldaug);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
+                                   const double* w, double* resid, double* sums, const double* H,
+                                   const double* M, const double* cmat, const GrouseState* st,
+                                   double* hw, double* mw, double* dots, cudaStream_t s) {
+  const int nres = (k * 32 + 255) / 256;
+  const int ndv = (2 * r + kDeferCap + 7) / 8;
+  k_resid_defer_vec<<<(unsigned)(nres + ndv), 256, 0, s>>>(U, ldu, r, k, vals, w, resid, sums, H,
+                                                           M, cmat, st, hw, mw, dots, nres);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
+                                     int64_t ldo, const double* t, double* vals, cudaStream_t s) {
+  const int64_t n = (int64_t)k * r;
+  k_gather_urows_vals<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, ldo, t, vals);
   return cudaGetLastError();
 }
 
