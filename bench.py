@@ -167,9 +167,16 @@ def rapid_block(device):
         torch.cuda.synchronize()
         return time.perf_counter() - t0, null, model, counters, x
 
+    from paper_1703_01506_b200 import rapid_engine as re
+
     cfg5 = CONFIGS["c5"]
     one(scaled(cfg5, (64, 64, 32), 2048), 2048, 1)  # warm-up: kernels, cuBLAS handles
-    dt, null, model, counters, x = one(cfg5, cfg5.permutations, 50)
+    marks = [] if os.environ.get("RMX_BENCH_RAPID_MARKS") else None
+    re._PHASE_LOG = marks  # device-synchronised phase marks (diagnostics only)
+    try:
+        dt, null, model, counters, x = one(cfg5, cfg5.permutations, 50)
+    finally:
+        re._PHASE_LOG = None
     L, v = cfg5.permutations, x.voxels
     return {"config": "c5: RapidPT n=400 (120/280) v=524288 L=100000 eta=0.35% r=400 "
                       "l=400, 50 GROUSE passes",
@@ -178,7 +185,8 @@ def rapid_block(device):
             "value": L * v / dt, "unit": "T-entries/s (L x v / max-null wall time)",
             "statistic_evaluations": counters["statistic_evaluations"],
             "sigma": model.residual_std, "mu": model.max_shift,
-            "api": "paper_1703_01506_b200.run_rapid (host numpy in, MaxNull out)"}
+            "api": "paper_1703_01506_b200.run_rapid (host numpy in, MaxNull out)",
+            **({"marks": [(tag, t - marks[0][1]) for tag, t in marks]} if marks else {})}
 
 
 def cpu_sample(cfg, x_host, orders_host, seconds: float, threads: int):

@@ -605,7 +605,9 @@ def recover(x, model: SubspaceModel, plan, cfg, _pre: Optional[_RecoverInputs] =
         _degenerate_in_recovery(x, plan, ell, L, k, int(st.perm), int(st.voxel),
                                 omd.cpu().numpy(), od.cpu().numpy())
     nat.raise_for(rc, st)
+    _mark("recover_inputs")
     W, flags, _ = _lsq_tc(u, r, omd, k, t, nrec)
+    _mark("recover_lsq")
     evals = nrec * k
     bad = np.flatnonzero(flags.cpu().numpy() != 0)
     for j in bad:  # rapid.py:173-196: redraw from the same stream, up to 5 times
@@ -648,7 +650,9 @@ def run_rapid(x, cfg):
     model, _, _, pre = _train_device(x, cfg, prefetch_recovery=True)
     t1 = time.perf_counter()
     null, rec = recover(x, model, plan, cfg, _pre=pre)
+    _mark("recover")
     model.basis.matrix  # the basis's host copy, overlapped with recovery
+    _mark("basis_host_copy_join")
     t2 = time.perf_counter()
     v = x.voxels
     counters = {
