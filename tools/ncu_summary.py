@@ -36,7 +36,15 @@ def main(rep, top=25, kernel=None):
     h = src[1]
     isrc, iall, iex = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), \
         h.index("Instructions Executed")
-    data = src[2:]
+    # multi-kernel reports: the source page repeats a title + header per
+    # kernel; keep the first kernel's rows
+    data = []
+    for r in src[2:]:
+        if len(r) <= iall or not r[iall].strip().isdigit():
+            if data:
+                break
+            continue
+        data.append(r)
     tot = sum(int(r[iall] or 0) for r in data)
     print(f"stall samples total: {tot}")
     for k, r in sorted(enumerate(data), key=lambda kr: -int(kr[1][iall] or 0))[:top]:
