@@ -280,6 +280,27 @@ int rmx_lsq_solve(const double *u, int64_t ldu, int32_t r, const int32_t *idx, i
                   double *norms_out, void *workspace, size_t workspace_bytes, void *stream,
                   rmx_status *st);
 
+/* Reference-semantics batched least squares (replaces lrmc.py:127-149
+ * solve_block and the condition test of lrmc.py:96-104 _gram_fit /
+ * lrmc.py:107-124 fit_coefficients): G = [U[idx_b] | vals_b]^T [..] in fp64;
+ * cond_b = sqrt(lambda_max / lambda_min) of G's r x r block (Householder
+ * tridiagonalisation + bisection on the device; inf when lambda_min <= 0);
+ * flag_b = cond_b > 1e12 (COND_LIMIT, lrmc.py:22).  Accepted systems: w by
+ * Cholesky, or by pivoted LU when the Cholesky meets a non-positive pivot;
+ * rejected: w = U_Omega^T vals (the reference's solve against the identity).
+ * u, idx, vals, w_out: device; flag_out, cond_out: HOST arrays (nullable). */
+int rmx_lsq_solve_exact(const double *u, int64_t ldu, int32_t r, const int32_t *idx, int32_t k,
+                        const double *vals, int64_t B, double *w_out, int32_t *flag_out,
+                        double *cond_out, void *stream, rmx_status *st);
+
+/* One GROUSE update in place (replaces lrmc.py:160-193 track_update): u
+ * (v x r, device, row-major), idx (sorted, device), vals (device).  Returns
+ * RMX_E_ILLCOND (st->value = cond) when the restricted basis is rejected;
+ * *resid_norm (host) = |vals - U_Omega w| before the update. */
+int rmx_track_update(double *u, int64_t v, int32_t r, const int32_t *idx, int32_t k,
+                     const double *vals, double step, double *resid_norm, void *stream,
+                     rmx_status *st);
+
 /* rmx_lsq_solve with the Gram on the tensor cores (v = rows of U): G~ =
  * [U_Omega | vals]^T [U_Omega | vals] from fp16 hi/lo planes (tcgen05,
  * fp32-accurate), Cholesky of G~ in fp64, then two steps of iterative

@@ -176,3 +176,91 @@ def recover_noise_free(x: np.ndarray, n1: int, u: np.ndarray, orders: np.ndarray
     cols = w @ u.T
     vals = np.abs(cols).max(axis=1) if two_sided else cols.max(axis=1)
     return vals + mu, w, stats
+
+
+# --------------------------------------------------------------------------
+# GROUSE training (numpy restatement; reference lrmc.py:85-104,160-193,208-268)
+# --------------------------------------------------------------------------
+
+def _stream(seed: int, *path: int) -> np.random.Generator:
+    """streams.py:31-38: SeedSequence(seed mod 2^64, spawn_key=path) -> SFC64."""
+    key = np.random.SeedSequence(entropy=int(seed) & ((1 << 64) - 1),
+                                 spawn_key=tuple(int(p) for p in path))
+    return np.random.Generator(np.random.SFC64(key))
+
+
+def init_basis(v: int, r: int, seed: int) -> np.ndarray:
+    """lrmc.py:85-93: Q of the QR of a BASIS_INIT (domain 5) Gaussian draw."""
+    return np.ascontiguousarray(np.linalg.qr(_stream(seed, 5).standard_normal((v, r)))[0])
+
+
+def grouse(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int = 50,
+           tolerance: float = 1e-3, force_halt=(), basis0=None):
+    """train_basis (lrmc.py:208-268) with track_update (lrmc.py:160-193) and
+    _gram_fit (lrmc.py:96-104) restated in numpy fp64.
+
+    force_halt: global update indices whose FIRST observation draw is treated
+    as ill-conditioned (the reference then redraws from the same generator,
+    lrmc.py:240-250) -- the test hook matching RMX_GROUSE_TEST_HALT.
+    Returns (U, passes, pass_residuals, final_omegas, converged)."""
+    v, ell = t_ex.shape
+    u = init_basis(v, rank, seed) if basis0 is None else np.array(basis0, dtype=np.float64)
+    tau = ell * max_passes / 2.0
+    t = 0
+    res = []
+    omegas = []
+    passes, converged = 0, False
+    for p in range(max_passes):
+        rel_sum = 0.0
+        omegas = []
+        for i in range(ell):
+            g = _stream(seed, 2, i, p)
+            step = 1.0 / (1.0 + t / tau)
+            for attempt in range(5):
+                idx = np.sort(g.choice(v, size=k, replace=False))
+                if attempt == 0 and t in force_halt:
+                    continue
+                vals = t_ex[idx, i]
+                uo = u[idx]
+                gram = uo.T @ uo
+                lam = np.linalg.eigvalsh(gram)
+                cond = np.inf if lam[0] <= 0.0 else float(np.sqrt(lam[-1] / lam[0]))
+                if cond > 1e12:
+                    continue
+                w = np.linalg.solve(gram, uo.T @ vals)
+                break
+            else:
+                raise ArithmeticError("restricted basis stayed ill-conditioned")
+            resid = vals - uo @ w
+            rn = float(np.linalg.norm(resid))
+            if step != 0.0 and rn != 0.0:
+                pred = u @ w
+                pn = float(np.linalg.norm(pred))
+                wn = float(np.linalg.norm(w))
+                if pn != 0.0 and wn != 0.0 and rn > 1e-14 * max(1.0, pn):
+                    theta = step * np.arctan(rn / pn)
+                    d = (np.cos(theta) - 1.0) / pn * pred
+                    d[idx] += np.sin(theta) / rn * resid
+                    u += np.outer(d, w / wn)
+            t += 1
+            nb = float(np.linalg.norm(vals))
+            rel_sum += rn / nb if nb > 0 else 0.0
+            omegas.append(idx)
+            if t % 64 == 0 and np.abs(u.T @ u - np.eye(rank)).max() > 1e-8:
+                u = np.ascontiguousarray(np.linalg.qr(u)[0])
+        rel = rel_sum / ell
+        res.append(rel)
+        passes = p + 1
+        if rel < tolerance:
+            converged = True
+            break
+    if np.abs(u.T @ u - np.eye(rank)).max() > 1e-8:
+        u = np.ascontiguousarray(np.linalg.qr(u)[0])
+    return u, passes, res, omegas, converged
+
+
+def principal_cosines(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Cosines of the principal angles between span(a) and span(b) (columns)."""
+    qa = np.linalg.qr(a)[0]
+    qb = np.linalg.qr(b)[0]
+    return np.clip(np.linalg.svd(qa.T @ qb, compute_uv=False), 0.0, 1.0)

@@ -46,10 +46,21 @@ from .rapid_engine import (  # noqa: F401
     recover,
     run_rapid,
     solve_block,
+    track_update,
     train,
     train_basis,
 )
+from .metrics import (  # noqa: F401
+    HistogramPair,
+    RiskResult,
+    ThresholdRow,
+    build_histogram_pair,
+    kl_divergence,
+    resampling_risk,
+    threshold_table,
+)
 from .stats import (  # noqa: F401
+    StatColumn,
     column_max,
     pvalue,
     reject_set,
@@ -67,6 +78,8 @@ __all__ = [
     "run_naive", "run_naive_ex", "column_max", "pvalue", "reject_set", "stat_map",
     "threshold_at", "tstat_full", "tstat_subset", "complete_column", "fit_coefficients",
     "init_basis", "recover", "run_rapid", "solve_block", "train", "train_basis",
+    "track_update", "StatColumn", "HistogramPair", "RiskResult", "ThresholdRow",
+    "build_histogram_pair", "kl_divergence", "resampling_risk", "threshold_table",
     "load_matrix", "read_array", "read_matrix", "read_matrix_csv", "write_array", "write_matrix",
     "write_matrix_csv",
 ]

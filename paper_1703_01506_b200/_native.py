@@ -90,6 +90,8 @@ EXPORTS = (
     "rmx_lsq_workspace_bytes",
     "rmx_lsq_solve",
     "rmx_lsq_solve_tc",
+    "rmx_lsq_solve_exact",
+    "rmx_track_update",
     "rmx_complete_max",
     "rmx_to_f32",
     "rmx_row_max",
@@ -159,6 +161,10 @@ _SIGS = {
                           _SP], ctypes.c_int),
     "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],
                       ctypes.c_int),
+    "rmx_lsq_solve_exact": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _SP],
+                            ctypes.c_int),
+    "rmx_track_update": ([_vp, _i64, _i32, _vp, _i32, _vp, ctypes.c_double,
+                          ctypes.POINTER(ctypes.c_double), _vp, _SP], ctypes.c_int),
     "rmx_complete_max": ([_vp, _i64, _i32, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double,
                           ctypes.c_uint64, _i32, _vp, _vp, _vp, _vp, _SP], ctypes.c_int),
     "rmx_to_f32": ([_vp, _i64, _vp, _vp, _SP], ctypes.c_int),

@@ -71,6 +71,8 @@ struct Blas {
   }
 };
 
+constexpr double kCondLimit = 1e12;  // lrmc.py:22 COND_LIMIT
+
 size_t gram_bytes(int r) { return (size_t)(r + 1) * (r + 1) * sizeof(double); }
 
 template <class T>
@@ -145,6 +147,121 @@ int rmx_lsq_solve(const double* u, int64_t ldu, int32_t r, const int32_t* idx, i
   return RMX_OK;
 }
 
+// Reference-semantics batched LS (lrmc.py:127-149 solve_block, and the
+// cond > COND_LIMIT test of _gram_fit / fit_coefficients): the fp64 Gram of
+// [U_Omega | vals]; cond = sqrt(lambda_max / lambda_min) of its r x r block
+// from k_sym_extreme_eigs (inf when lambda_min <= 0); accepted systems are
+// solved by Cholesky, or by pivoted LU (np.linalg.solve's algorithm) when
+// the Cholesky meets a non-positive pivot; rejected systems (cond > 1e12)
+// get w = U_Omega^T vals, the reference's solve against the identity.
+int rmx_lsq_solve_exact(const double* u, int64_t ldu, int32_t r, const int32_t* idx, int32_t k,
+                        const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                        double* cond_out, void* stream, rmx_status* st) {
+  rclear(st);
+  if (r < 1 || k < r || B < 1 || !vals || !w_out)
+    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t ld = r + 1;
+  const size_t per = gram_bytes(r) + sym_extreme_eigs_work(r, 1) + 8 * sizeof(double);
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, ((int64_t)1 << 30) / (int64_t)per));
+  DevBuf<double> G, work, lam, nrm, cond;
+  DevBuf<int32_t> cflag, sel;
+  RCUDA(G.alloc((size_t)chunk * ld * ld, s));
+  RCUDA(work.alloc(std::max(sym_extreme_eigs_work(r, chunk), lu_solve_work(r, 1)) / 8 + 1, s));
+  RCUDA(lam.alloc((size_t)2 * chunk, s));
+  RCUDA(nrm.alloc((size_t)4 * chunk, s));
+  RCUDA(cond.alloc((size_t)B, s));
+  RCUDA(cflag.alloc((size_t)chunk, s));
+  RCUDA(sel.alloc(1, s));
+  std::vector<double> hl((size_t)2 * chunk), hc((size_t)B);
+  std::vector<int32_t> hf((size_t)chunk), hflag((size_t)B);
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t cnt = std::min(chunk, B - b0);
+    const int32_t* ib = idx ? idx + b0 * k : nullptr;
+    RCUDA(launch_gram(u, ldu, r, ib, k, vals + b0 * k, G.p, cnt, s));
+    RCUDA(launch_sym_extreme_eigs(G.p, ld * ld, (int)ld, r, nullptr, cnt, work.p, lam.p, s));
+    RCUDA(launch_chol_solve(G.p, r, cnt, w_out + b0 * r, cflag.p, nrm.p, s));
+    RCUDA(cudaMemcpyAsync(hl.data(), lam.p, (size_t)2 * cnt * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaMemcpyAsync(hf.data(), cflag.p, (size_t)cnt * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaStreamSynchronize(s));
+    for (int64_t j = 0; j < cnt; ++j) {
+      const double lo = hl[2 * j], hi = hl[2 * j + 1];
+      const double c = lo > 0.0 ? std::sqrt(hi / lo) : INFINITY;
+      const int64_t b = b0 + j;
+      hc[b] = c;
+      const bool bad = !(c <= kCondLimit);
+      hflag[b] = bad ? 1 : 0;
+      if (!bad && hf[j] == 0) continue;
+      // rare: re-form this system's Gram, then LU (accepted) or w = rhs (rejected)
+      RCUDA(launch_gram(u, ldu, r, idx ? idx + b * k : nullptr, k, vals + b * k, G.p, 1, s));
+      if (bad) {
+        RCUDA(cudaMemcpyAsync(w_out + b * r, G.p + (int64_t)r * ld, (size_t)r * sizeof(double),
+                              cudaMemcpyDeviceToDevice, s));
+      } else {
+        const int32_t zero = 0;
+        RCUDA(cudaMemcpyAsync(sel.p, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        RCUDA(launch_lu_solve(G.p, ld * ld, (int)ld, r, sel.p, 1, work.p, w_out + b * r, nullptr,
+                              s));
+      }
+      RCUDA(cudaStreamSynchronize(s));
+    }
+  }
+  if (cond_out) std::memcpy(cond_out, hc.data(), (size_t)B * sizeof(double));
+  if (flag_out) std::memcpy(flag_out, hflag.data(), (size_t)B * sizeof(int32_t));
+  return RMX_OK;
+}
+
+// One GROUSE update (lrmc.py:160-193 track_update) on a device basis U (v x
+// r, row-major, updated in place); idx (sorted) / vals: the observed column
+// on the device.  *resid_norm = |vals - U_Omega w| before the update.
+int rmx_track_update(double* u, int64_t v, int32_t r, const int32_t* idx, int32_t k,
+                     const double* vals, double step, double* resid_norm, void* stream,
+                     rmx_status* st) {
+  rclear(st);
+  if (k < r)
+    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevBuf<double> w, resid, pred, sums;
+  RCUDA(w.alloc((size_t)r, s));
+  RCUDA(resid.alloc((size_t)k, s));
+  RCUDA(pred.alloc((size_t)v, s));
+  RCUDA(sums.alloc(8, s));
+  int32_t bad = 0;
+  double cond = 0.0;
+  if (int rc = rmx_lsq_solve_exact(u, r, r, idx, k, vals, 1, w.p, &bad, &cond, stream, st))
+    return rc;
+  if (bad) {
+    st->value = cond;
+    return rset(st, RMX_E_ILLCOND, "restricted basis condition number %.3e exceeds 1e12", cond);
+  }
+  RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+  RCUDA(launch_resid(u, r, r, idx, k, vals, w.p, resid.p, sums.p, s));
+  double hs[8];
+  RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaStreamSynchronize(s));
+  const double rn = std::sqrt(std::max(hs[0], 0.0));
+  if (resid_norm) *resid_norm = rn;
+  if (step == 0.0 || rn == 0.0) return RMX_OK;
+  RCUDA(launch_pred(u, v, r, w.p, pred.p, sums.p, s));
+  std::vector<double> hw((size_t)r);
+  RCUDA(cudaMemcpyAsync(hw.data(), w.p, (size_t)r * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaMemcpyAsync(hs, sums.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  RCUDA(cudaStreamSynchronize(s));
+  const double pn = std::sqrt(std::max(hs[1], 0.0));
+  double ww = 0.0;
+  for (int c = 0; c < r; ++c) ww += hw[c] * hw[c];
+  const double wn = std::sqrt(ww);
+  if (pn == 0.0 || wn == 0.0) return RMX_OK;
+  if (rn <= 1e-14 * std::max(1.0, pn)) return RMX_OK;
+  const double theta = step * std::atan(rn / pn);
+  const double a = (std::cos(theta) - 1.0) / pn, b = std::sin(theta) / rn;
+  RCUDA(launch_track_apply(u, v, r, pred.p, a, idx, k, resid.p, b, w.p, 1.0 / wn, s));
+  RCUDA(cudaStreamSynchronize(s));
+  return RMX_OK;
+}
+
 int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_t* idx,
                      int32_t k, const double* vals, int64_t B, double* w_out, int32_t* flag_out,
                      void* workspace, size_t workspace_bytes, int32_t* stats, void* stream,
@@ -195,19 +312,27 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
       else RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
     }
   }
-  // systems whose factor was singular or whose refinement has not settled:
-  // the fp64 Gram + Cholesky, one by one (rare: ill-conditioned restrictions)
+  // systems whose fp32 factor was singular or whose refinement has not
+  // settled (rare: cond(U_Omega) >~ 1e3): the reference's decision on the
+  // fp64 Gram -- exact cond vs 1e12, Cholesky or pivoted LU, w = rhs when
+  // rejected (rmx_lsq_solve_exact), one by one
   std::vector<int32_t> hf((size_t)B), hn((size_t)B);
   RCUDA(cudaMemcpyAsync(hf.data(), flags.p, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
   RCUDA(cudaMemcpyAsync(hn.data(), nconv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
   RCUDA(cudaStreamSynchronize(s));
+  (void)G;
+  (void)nrm;
   int32_t redo = 0;
   for (int64_t b = 0; b < B; ++b) {
     if (hf[b] == 0 && hn[b] == 0) continue;
     ++redo;
-    RCUDA(launch_gram(u, ldu, r, idx + b * k, k, vals + b * k, G, 1, s));
-    RCUDA(launch_chol_solve(G, r, 1, w_out + b * r, flags.p + b, nrm, s));
+    int32_t bad = 0;
+    if (int rc = rmx_lsq_solve_exact(u, ldu, r, idx + b * k, k, vals + b * k, 1, w_out + b * r,
+                                     &bad, nullptr, stream, st))
+      return rc;
+    hf[b] = bad;
   }
+  if (redo) RCUDA(cudaMemcpyAsync(flags.p, hf.data(), (size_t)B * 4, cudaMemcpyHostToDevice, s));
   if (flag_out) RCUDA(cudaMemcpyAsync(flag_out, flags.p, (size_t)B * 4, cudaMemcpyDeviceToDevice, s));
   if (stats) {
     stats[0] = 1;
@@ -456,57 +581,90 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   int passes = 0, converged = 0;
   const int64_t total = (int64_t)max_passes * ell;
   int64_t tglob = 0;
+  // a checkpoint follows update tglob - 1 when tglob is a flush point (every
+  // kDeferCap updates) or a pass end; the host reads the device state there
+  auto is_checkpoint = [&](int64_t tg) { return tg % kDeferCap == 0 || tg % ell == 0; };
+  const bool force_halt = getenv("RMX_GROUSE_TEST_HALT") != nullptr;  // tests: halt at these steps
+  std::vector<int64_t> halt_at;
+  if (force_halt) {
+    for (const char* c = getenv("RMX_GROUSE_TEST_HALT"); *c;) {
+      char* e = nullptr;
+      const long long hv = strtoll(c, &e, 10);
+      if (e == c) break;
+      halt_at.push_back(hv);
+      c = (*e == ',') ? e + 1 : e;
+    }
+  }
+  std::vector<char> halt_used(halt_at.size(), 0);
   while (tglob < total) {
     const int p = (int)(tglob / ell), i = (int)(tglob % ell);
+    for (size_t q = 0; q < halt_at.size(); ++q)
+      if (halt_at[q] == tglob && !halt_used[q]) {  // test hook: as if this solve flagged
+        halt_used[q] = 1;
+        RCUDA(launch_force_halt(gst.p, tglob, s));
+      }
     if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob)) return rc;
     ++tglob;
-    const bool reortho = tglob % kDeferCap == 0, pass_end = tglob % ell == 0;
-    if (!reortho && !pass_end) continue;
-    GrouseState hs;
-    if (int rc = read_state(&hs)) return rc;
-    if (hs.halted) {
-      // ill-conditioned restriction at update h: redraw its Omega from the same
-      // stream (lrmc.py:240-250); updates after h were no-ops and are replayed
-      const int64_t h = hs.halt_step;
-      const int hp = (int)(h / ell), hi = (int)(h % ell);
-      bool ok = false;
-      for (int attempt = 1; attempt < 5 && cb; ++attempt) {
-        if (cb(user, hi, hp, attempt, host_idx.data()) != 0)
-          return rset(st, RMX_E_USAGE, "omega callback failed");
-        RCUDA(cudaMemcpyAsync(idxbuf.p, host_idx.data(), k * sizeof(int32_t),
-                              cudaMemcpyHostToDevice, s));
-        RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(int), s));  // clear `halted`
-        if (int rc = enqueue(hp, hi, idxbuf.p, h)) return rc;
-        if (int rc = read_state(&hs)) return rc;
-        if (!hs.halted) {
-          ok = true;
-          break;
+    bool stop = false;
+    // Process the checkpoint at tglob.  After a halt is resolved by a redraw,
+    // the updates after the halted one are replayed from h + 1 -- and when h
+    // + 1 is itself a checkpoint, it is processed here before any further
+    // update is enqueued (so at most kDeferCap terms are ever pending, and no
+    // pass end is skipped).
+    while (is_checkpoint(tglob)) {
+      GrouseState hs;
+      if (int rc = read_state(&hs)) return rc;
+      if (hs.overflow)
+        return rset(st, RMX_E_CUDA, "GROUSE: more than %d deferred updates between flushes",
+                    kDeferCap);
+      if (hs.halted) {
+        // ill-conditioned restriction at update h: redraw its Omega from the same
+        // stream (lrmc.py:240-250); updates after h were no-ops and are replayed
+        const int64_t h = hs.halt_step;
+        const int hp = (int)(h / ell), hi = (int)(h % ell);
+        bool ok = false;
+        for (int attempt = 1; attempt < 5 && cb; ++attempt) {
+          if (cb(user, hi, hp, attempt, host_idx.data()) != 0)
+            return rset(st, RMX_E_USAGE, "omega callback failed");
+          RCUDA(cudaMemcpyAsync(idxbuf.p, host_idx.data(), k * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+          RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(int), s));  // clear `halted`
+          if (int rc = enqueue(hp, hi, idxbuf.p, h)) return rc;
+          if (int rc = read_state(&hs)) return rc;
+          if (!hs.halted) {
+            ok = true;
+            break;
+          }
+        }
+        if (!ok)
+          return rset(st, RMX_E_ILLCOND,
+                      "training column %d pass %d: restricted basis stayed ill-conditioned", hi,
+                      hp);
+        tglob = h + 1;  // replay the skipped updates (checkpoint at h + 1 first, if any)
+        continue;
+      }
+      const int pc = (int)((tglob - 1) / ell);  // pass of the update before the checkpoint
+      if (tglob % kDeferCap == 0) {  // at most kDeferCap deferred terms: rewrite U
+        if (int rc = flush(hs.nterms)) return rc;
+        if (hdrift_host > 1e-8) {  // lrmc.py:258-259 every 64 updates, from the tracked H
+          double drift = 0.0;
+          if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
+          RCUDA(launch_h_identity(H.p, r, s));
         }
       }
-      if (!ok)
-        return rset(st, RMX_E_ILLCOND,
-                    "training column %d pass %d: restricted basis stayed ill-conditioned", hi, hp);
-      tglob = h + 1;  // replay the skipped updates
-      continue;
-    }
-    if (reortho) {  // at most kDeferCap deferred terms: rewrite U
-      if (int rc = flush(hs.nterms)) return rc;
-      if (hdrift_host > 1e-8) {  // lrmc.py:258-259 every 64 updates, from the tracked H
-        double drift = 0.0;
-        if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
-        RCUDA(launch_h_identity(H.p, r, s));
+      if (tglob % ell == 0) {
+        const double rel = hs.rel_sum / ell;
+        if (pass_resid) pass_resid[pc] = rel;
+        passes = pc + 1;
+        RCUDA(cudaMemsetAsync(&gst.p->rel_sum, 0, sizeof(double), s));
+        if (rel < tol) {
+          converged = 1;
+          stop = true;
+        }
       }
+      break;
     }
-    if (pass_end) {
-      const double rel = hs.rel_sum / ell;
-      if (pass_resid) pass_resid[p] = rel;
-      passes = p + 1;
-      RCUDA(cudaMemsetAsync(&gst.p->rel_sum, 0, sizeof(double), s));
-      if (rel < tol) {
-        converged = 1;
-        break;
-      }
-    }
+    if (stop) break;
   }
   {
     GrouseState hs;

@@ -47,7 +47,7 @@ struct GrouseState {
   int halted;      // a solve flagged ill-conditioning: later step kernels no-op
   int halt_step;   // global update index that halted
   int pending;     // this step's update (pend_a, pend_b, wn) is still to be folded into M/H
-  int pad;
+  int overflow;    // a term would have exceeded kDeferCap (host bug guard): halted, error
   double pend_a;
   double rel_sum;  // sum over the pass of |r| / |t_Omega|
   double pend_b;   // beta of the pending update (d = beta r on Omega)
@@ -86,6 +86,8 @@ cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int3
 cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
                                const double* hg, GrouseState* st, const double* mw,
                                const double* dots, const double* wn, int r, cudaStream_t s);
+// test hook: mark update `step` as halted (ill-conditioned) before it runs
+cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s);
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
                                cudaStream_t s);
 // H = U^T U tracked through the rank-1 updates (the every-64-updates drift
@@ -130,5 +132,21 @@ cudaError_t launch_resid_batch(const double* U, int r, const int32_t* idx, int k
 cudaError_t launch_to_f32(const double* a, int64_t n, float* out, cudaStream_t s);
 cudaError_t launch_gather_rows(const double* t, int64_t ldt, const int32_t* idx, int k, int64_t B,
                                double* out, cudaStream_t s);
+// dense_small.cu: exact condition numbers (Householder tridiagonalisation +
+// Sturm bisection) and a pivoted LU fallback solve, one CTA per system.
+// G: systems at stride gstride, leading dimension ldg; sel: system ids
+// (nullable for sym_extreme_eigs = 0..count-1); lam: (min, max) per entry
+cudaError_t launch_sym_extreme_eigs(const double* G, int64_t gstride, int ldg, int r,
+                                    const int32_t* sel, int64_t count, double* work, double* lam,
+                                    cudaStream_t s);
+size_t sym_extreme_eigs_work(int r, int64_t count);
+cudaError_t launch_lu_solve(const double* G, int64_t gstride, int ldg, int r, const int32_t* sel,
+                            int64_t count, double* work, double* w, int32_t* singular,
+                            cudaStream_t s);
+size_t lu_solve_work(int r, int64_t count);
+// track_update's rotation: d = a pred, d[idx] += b resid, U += d (w winv)^T
+cudaError_t launch_track_apply(double* U, int64_t v, int r, double* pred, double a,
+                               const int32_t* idx, int k, const double* resid, double b,
+                               const double* w, double winv, cudaStream_t s);
 cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s);
 }  // namespace rmx

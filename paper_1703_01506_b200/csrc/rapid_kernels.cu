@@ -1173,6 +1173,11 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
     skip = 0;
     if (st->halted) {
       skip = 1;
+    } else if (st->nterms >= kDeferCap) {  // never with a correct host loop
+      st->halted = 1;
+      st->overflow = 1;
+      st->halt_step = (int)step_index;
+      skip = 1;
     } else if (*flag) {
       st->halted = 1;
       st->halt_step = (int)step_index;
@@ -1255,6 +1260,12 @@ __global__ void k_defer_count(GrouseState* __restrict__ st) {
   if (st->halted || !st->pending) return;
   st->nterms += 1;
   st->pending = 0;
+}
+
+__global__ void k_force_halt(GrouseState* __restrict__ st, int64_t step) {
+  if (st->halted) return;
+  st->halted = 1;
+  st->halt_step = (int)step;
 }
 
 __global__ void k_flush_reset(double* __restrict__ M, double* __restrict__ X,
@@ -1701,6 +1712,11 @@ cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseSt
                                cudaStream_t s) {
   const int64_t n = (int64_t)r * std::max(r, kDeferCap);
   k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, X, Yt, r, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s) {
+  k_force_halt<<<1, 1, 0, s>>>(st, step);
   return cudaGetLastError();
 }
 

@@ -101,18 +101,43 @@ def _torch_dtype(dt: np.dtype):
             np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8}[dt]
 
 
+# (host array, CUDA event) of asynchronous copies out of memory registered in
+# place: torch does not track the lifetime of memory it did not allocate, so
+# the source (and its registration) is kept alive here until the copy has
+# completed -- otherwise a temporary passed by a caller could be freed, and
+# unregistered, while the DMA still reads it.
+_INFLIGHT: list = []
+
+
+def _prune_inflight() -> None:
+    with _LOCK:
+        _INFLIGHT[:] = [(a, ev) for a, ev in _INFLIGHT if not ev.query()]
+
+
 def to_device(arr: np.ndarray, device, stream=None):
     """Copy a C-contiguous numpy array to `device` (async on `stream`)."""
     import torch
 
+    _prune_inflight()
     arr = np.ascontiguousarray(arr)
-    if arr.nbytes >= _MIN_REGISTER_BYTES:
-        _register(arr)
-        host = _as_tensor(arr)
-    else:
-        host = _as_tensor(arr).pin_memory()
+    registered = arr.nbytes >= _MIN_REGISTER_BYTES and _register(arr)
+    host = _as_tensor(arr) if registered else _as_tensor(arr).pin_memory()
     out = torch.empty(arr.shape, dtype=host.dtype, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
     with torch.cuda.stream(s):
         out.copy_(host, non_blocking=True)
+        if registered:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            with _LOCK:
+                _INFLIGHT.append((arr, ev))
     return out
+
+
+def wait_inflight() -> None:
+    """Block until every in-place-registered source copy has completed."""
+    with _LOCK:
+        pending = list(_INFLIGHT)
+    for _, ev in pending:
+        ev.synchronize()
+    _prune_inflight()

@@ -216,12 +216,26 @@ def init_basis(v: int, r: int, seed: int) -> Basis:
     return Basis(u.cpu().numpy(), copy=False)
 
 
+def _lsq_exact(u_dev, r: int, idx_dev, k: int, vals_dev, B: int):
+    """rmx_lsq_solve_exact: reference-semantics fits -> (W (B x r) on the
+    device, flags (B,) host, conds (B,) host)."""
+    torch = _torch()
+    dev = u_dev.device
+    W = torch.empty((B, r), dtype=torch.float64, device=dev)
+    flags = np.zeros(B, dtype=np.int32)
+    conds = np.zeros(B, dtype=np.float64)
+    nat.call("rmx_lsq_solve_exact", nat.ptr(u_dev), r, r, nat.ptr(idx_dev), k, nat.ptr(vals_dev),
+             B, nat.ptr(W), flags.ctypes.data, conds.ctypes.data, _stream(dev))
+    return W, flags, conds
+
+
 def solve_block(u_stack: np.ndarray, values: np.ndarray):
     """Batched LS fits (reference lrmc.py:127-149) -> (w (B, r), conds (B,)).
 
-    conds: inf for a rank-deficient restriction (non-positive Cholesky pivot),
-    else max(L_ii) / min(L_ii) of the Gram's Cholesky factor -- a lower bound
-    of the reference's sqrt(lambda_max / lambda_min)."""
+    conds = sqrt(lambda_max / lambda_min) of each normal matrix (inf when
+    lambda_min <= 0), from the device's Householder tridiagonalisation +
+    bisection; systems with cond > 1e12 get w = U_Omega^T values (the
+    reference's solve against the identity)."""
     u_stack = np.ascontiguousarray(u_stack, dtype=np.float64)
     values = np.ascontiguousarray(values, dtype=np.float64)
     B, k, r = u_stack.shape
@@ -229,11 +243,7 @@ def solve_block(u_stack: np.ndarray, values: np.ndarray):
     torch = _torch()
     U = _to_dev(u_stack.reshape(B * k, r), dev)
     idx = torch.arange(B * k, dtype=torch.int32, device=dev).reshape(B, k)
-    W, flags, norms = _lsq(U, r, idx, k, _to_dev(values, dev), B)
-    n = norms.cpu().numpy()
-    f = flags.cpu().numpy()
-    with np.errstate(divide="ignore", invalid="ignore"):
-        conds = np.where(f != 0, np.inf, n[:, 3] / n[:, 2])
+    W, _, conds = _lsq_exact(U, r, idx, k, _to_dev(values, dev), B)
     return W.cpu().numpy(), conds
 
 
@@ -247,6 +257,25 @@ def fit_coefficients(b: Basis, col: ObservedColumn) -> np.ndarray:
     if not np.isfinite(conds[0]) or conds[0] > COND_LIMIT:
         raise IllConditionedBasisError(float(conds[0]))
     return w[0]
+
+
+def track_update(b: Basis, col: ObservedColumn, step: float):
+    """One GROUSE update (reference lrmc.py:160-193) on the device: mutates and
+    returns `b`, plus the pre-update fit residual norm on the observed rows.
+    Raises IllConditionedBasisError(cond) like the reference's _gram_fit."""
+    if col.size < b.rank:
+        raise UsageError(f"{col.size} observed rows cannot determine {b.rank} coefficients")
+    if col.indices[-1] >= b.voxels:
+        raise UsageError("observed row index outside the basis")
+    dev = cuda_device()
+    u = _to_dev(b.matrix, dev)
+    idx = _to_dev(np.asarray(col.indices, dtype=np.int32), dev)
+    vals = _to_dev(np.asarray(col.values, dtype=np.float64), dev)
+    rn = ctypes.c_double(0.0)
+    nat.call("rmx_track_update", nat.ptr(u), b.voxels, b.rank, nat.ptr(idx), col.size,
+             nat.ptr(vals), float(step), ctypes.byref(rn), _stream(dev))
+    b.matrix[...] = u.cpu().numpy()
+    return b, float(rn.value)
 
 
 def complete_column(b: Basis, w: np.ndarray) -> np.ndarray:
@@ -613,6 +642,7 @@ def recover(x, model: SubspaceModel, plan, cfg, _pre: Optional[_RecoverInputs] =
     for j in bad:  # rapid.py:173-196: redraw from the same stream, up to 5 times
         i = ell + int(j)
         ok = False
+        last_cond = float("inf")
         for attempt in range(1, _RESAMPLE_ATTEMPTS + 1):
             idx = _resample(model.seed, (RECOVER_OMEGA, i), attempt, v, k)
             idx_d = _to_dev(idx[None], dev)
@@ -620,14 +650,16 @@ def recover(x, model: SubspaceModel, plan, cfg, _pre: Optional[_RecoverInputs] =
             nat.call("rmx_rapid_stats", nat.ptr(xd), v, x.subjects, n1, nat.ptr(od[j:j + 1]),
                      nat.ptr(idx_d), 1, k, nat.ptr(tj), _stream(dev))
             evals += k
-            wj, fj, _ = _lsq(u, r, idx_d, k, tj, 1)
-            if int(fj.item()) == 0:
+            wj, fj, cj = _lsq_exact(u, r, idx_d, k, tj, 1)
+            last_cond = float(cj[0])
+            if int(fj[0]) == 0:
                 W[j] = wj[0]
                 ok = True
                 break
         if not ok:
             raise NumericalError(
-                f"permutation {i}: restricted basis stayed ill-conditioned after "
+                f"permutation {i}: restricted basis stayed ill-conditioned "
+                f"(last condition number {last_cond:.3e}) after "
                 f"{_RESAMPLE_ATTEMPTS} observation resamples")
     m = _complete_max(u32, W.to(torch.float32), ell, model.residual_std, model.max_shift,
                       model.seed, model.two_sided)

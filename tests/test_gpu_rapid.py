@@ -30,11 +30,71 @@ def test_solve_block_matches_reference():
     d = g()
     w, conds = rmx.solve_block(d["sb_u"], d["sb_vals"])
     assert np.allclose(w, d["sb_w"], rtol=0, atol=1e-10)
-    assert np.all(conds < 100)
+    # the reference's exact condition numbers sqrt(lambda_max / lambda_min)
+    assert np.allclose(conds, d["sb_conds"], rtol=1e-9, atol=0)
     u = np.zeros((10, 2))
     u[0, 0] = u[1, 1] = 1.0
-    _, c = rmx.solve_block(np.stack([u[[0, 1, 2]], u[[5, 6, 7]]]), np.zeros((2, 3)))
-    assert c[0] < 10 and (not np.isfinite(c[1]) or c[1] > 1e12)
+    vals = np.array([[1.0, 2.0, 3.0], [4.0, 5.0, 6.0]])
+    w, c = rmx.solve_block(np.stack([u[[0, 1, 2]], u[[5, 6, 7]]]), vals)
+    assert c[0] == 1.0 and not np.isfinite(c[1])
+    # rejected system: the reference solves against the identity (w = U^T t = 0)
+    assert np.array_equal(w[0], [1.0, 2.0]) and np.array_equal(w[1], [0.0, 0.0])
+
+
+def test_exact_condition_numbers_match_eigvalsh():
+    """cond = sqrt(lambda_max / lambda_min) over six decades, including
+    restrictions the Cholesky fast path cannot factor (cond(U_O) ~ 1e9: the
+    Gram's condition is 1e18) and rank-deficient ones (lambda_min ~ +-eps)."""
+    rg = np.random.default_rng(5)
+    B, k, r = 9, 60, 12
+    us = []
+    for i in range(B):
+        q1 = np.linalg.qr(rg.standard_normal((k, r)))[0]
+        q2 = np.linalg.qr(rg.standard_normal((r, r)))[0]
+        sv = np.logspace(0, -float(i), r)  # cond(U_O) = 10^i
+        us.append(q1 @ np.diag(sv) @ q2)
+    us = np.stack(us)
+    vals = rg.standard_normal((B, k))
+    w, conds = rmx.solve_block(us, vals)
+    gram = np.matmul(us.transpose(0, 2, 1), us)
+    lam = np.linalg.eigvalsh(gram)
+    ref = np.sqrt(np.where(lam[:, 0] > 0, lam[:, -1] / np.where(lam[:, 0] > 0, lam[:, 0], 1), np.inf))
+    # well resolved (cond <= 1e6): same value; beyond, both are eps-level noise in
+    # lambda_min, so only the decision side matters and it stays below 1e12 here
+    assert np.allclose(conds[:7], ref[:7], rtol=1e-6)
+    assert np.all(conds[7:] > 1e6)
+    ok = conds <= 1e12
+    wref = np.linalg.solve(gram[ok], np.matmul(us[ok].transpose(0, 2, 1), vals[ok][..., None]))[..., 0]
+    assert np.allclose(w[ok][:5], wref[:5], rtol=1e-8, atol=1e-8)
+
+
+def test_track_update_matches_reference_step():
+    """One update through the C ABI (rmx_track_update) vs lrmc.py:160-193
+    restated in numpy."""
+    rg = np.random.default_rng(8)
+    v, r, k = 3000, 10, 200
+    b = rmx.init_basis(v, r, seed=4)
+    u0 = b.matrix.copy()
+    idx = np.sort(rg.choice(v, k, replace=False))
+    col = rg.standard_normal(v)
+    b2, rn = rmx.track_update(b, rmx.ObservedColumn(idx, col[idx]), 0.7)
+    assert b2 is b
+    uo = u0[idx]
+    w = np.linalg.solve(uo.T @ uo, uo.T @ col[idx])
+    res = col[idx] - uo @ w
+    assert rn == pytest.approx(np.linalg.norm(res), rel=1e-12)
+    pred = u0 @ w
+    theta = 0.7 * np.arctan(np.linalg.norm(res) / np.linalg.norm(pred))
+    d = (np.cos(theta) - 1.0) / np.linalg.norm(pred) * pred
+    d[idx] += np.sin(theta) / np.linalg.norm(res) * res
+    ref = u0 + np.outer(d, w / np.linalg.norm(w))
+    assert np.allclose(b.matrix, ref, rtol=0, atol=1e-12)
+    same, rn0 = rmx.track_update(rmx.Basis(u0), rmx.ObservedColumn(idx, col[idx]), 0.0)
+    assert np.array_equal(same.matrix, u0) and rn0 == pytest.approx(rn, rel=1e-12)
+    bad = np.zeros((10, 3))
+    bad[0, 0] = bad[1, 1] = bad[2, 2] = 1.0
+    with pytest.raises(rmx.IllConditionedBasisError):
+        rmx.track_update(rmx.Basis(bad), rmx.ObservedColumn(np.array([5, 6, 7, 8]), np.ones(4)), 1.0)
 
 
 def test_fit_and_complete_column():
@@ -237,3 +297,41 @@ def test_degenerate_voxel_in_recovery_matches_reference(entry):
     assert err.value.voxel == int(d["voxel"])
     assert err.value.mean_diff == float(d["mean_diff"])
     assert str(err.value) == str(d["msg"])
+
+
+def _grouse_case(v=6000, ell=24, r=24, eta=0.05, seed=77):
+    rg = np.random.default_rng(seed)
+    # low-rank-plus-noise training columns (a t-statistic matrix's structure)
+    t_ex = rg.standard_normal((v, 6)) @ rg.standard_normal((6, ell)) + 0.3 * rg.standard_normal(
+        (v, ell))
+    return t_ex, int(np.ceil(eta * v)), r, seed
+
+
+def test_grouse_matches_oracle_numpy_restatement(oracle_mod):
+    """Device GROUSE vs the numpy restatement of lrmc.py:208-268 (pinned to
+    the reference's basis in test_oracle_golden): same Omega draws, so the
+    trajectories agree to fp64 solver precision."""
+    t_ex, k, r, seed = _grouse_case()
+    res = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=4)
+    u, passes, pres, om, conv = oracle_mod.grouse(t_ex, k, r, seed, max_passes=4)
+    assert res.passes == passes == 4
+    assert np.allclose(res.pass_residuals, pres, rtol=1e-9, atol=0)
+    assert oracle_mod.principal_cosines(res.basis.matrix, u).min() > 1 - 1e-10
+    assert all(np.array_equal(a, b) for a, b in zip(res.final_omegas, om))
+
+
+@pytest.mark.parametrize("halts", ["63", "71", "95", "63,71,95", "0,40"])
+def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, monkeypatch):
+    """An ill-conditioned restriction at update h is redrawn from the same
+    stream (lrmc.py:240-250).  h = 63 ends a 64-update flush block, h = 71 a
+    pass (ell = 24), h = 95 the whole training: the checkpoint at h + 1 must
+    still run (it was skipped, overflowing the deferred terms)."""
+    t_ex, k, r, seed = _grouse_case()
+    hs = tuple(int(h) for h in halts.split(","))
+    monkeypatch.setenv("RMX_GROUSE_TEST_HALT", halts)
+    res = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=4)
+    u, passes, pres, om, conv = oracle_mod.grouse(t_ex, k, r, seed, max_passes=4, force_halt=hs)
+    assert res.passes == passes == 4 and res.updates == 96
+    assert np.allclose(res.pass_residuals, pres, rtol=1e-9, atol=0)
+    assert oracle_mod.principal_cosines(res.basis.matrix, u).min() > 1 - 1e-10
+    assert all(np.array_equal(a, b) for a, b in zip(res.final_omegas, om))
