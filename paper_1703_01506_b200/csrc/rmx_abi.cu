@@ -439,9 +439,35 @@ size_t rmx_naive_workspace_bytes(int64_t v, int32_t n, int64_t L) {
 namespace {
 
 // K0 pieces: counters reset, rows [v0, v1), constant-voxel reduction
-int prep_init(const Ws& ws, int64_t L, cudaStream_t s, rmx_status* st) {
+// A priori bound on |S~ - S| for the fp16 hi/lo S-only tiles (balanced
+// designs on the fp16 path: configs 1-2).  S = sum_{G1} z with
+// sum_all z^2 = n - 1, so sum_{G1} |z| <= sqrt(n1 (n - 1)) =: P.
+//  * split: z = hi + lo + delta, |delta| <= 2^-22 |z| + 2^-25 (lo subnormal);
+//  * products hi * g, lo * g with g in {0, 1} are exact in fp32;
+//  * accumulation: each tcgen05.mma (K = 16) adds at most 2^-22 (|C| + sum
+//    |products|) <= 2^-22 1.001 P -- four fp32 ulps of the magnitude sum, a
+//    model that covers truncated (non-IEEE) alignment inside the tensor core
+//    (tests/test_gpu_naive.py::test_fp16_accumulation_model checks it
+//    against adversarial inputs);
+// so e = 2^-22 P + n1 2^-25 + (2 kpad / 16 + 1) 2^-22 1.001 P.  Fed to the
+// same band machinery as the int8 quantisation bound (band_abs): rigorous.
+float fp16_sonly_error_bound(int n, int n1, int kpad) {
+  const double P = std::sqrt((double)n1 * (double)(n - 1));
+  const double u = std::ldexp(1.0, -22);
+  const double nmma = 2.0 * kpad / 16.0;
+  const double e = u * P + n1 * std::ldexp(1.0, -25) + (nmma + 1.0) * u * 1.001 * P;
+  return (float)(e * 1.01);
+}
+
+int prep_init(const Ws& ws, int32_t n, int32_t n1, int64_t L, cudaStream_t s, rmx_status* st) {
   RMX_CUDA(cudaMemsetAsync(ws.counters(), 0, sizeof(NaiveCounters), s));
   RMX_CUDA(cudaMemsetAsync(&ws.counters()->deg_key, 0xff, sizeof(unsigned long long), s));
+  if (!ws.lay.i8 && 2 * n1 == n) {  // fp16 S-only: the a priori bound (K0 adds nothing)
+    static thread_local float e;  // pageable source: staged before the call returns
+    e = fp16_sonly_error_bound(n, n1, ws.lay.kpad);
+    RMX_CUDA(cudaMemcpyAsync(&ws.counters()->emax_bits, &e, sizeof(float), cudaMemcpyHostToDevice,
+                             s));
+  }
   RMX_CUDA(cudaMemsetAsync(ws.best(), 0, (size_t)L * 4, s));
   // int8 scale padding (voxels past v) must be finite: those columns are masked
   if (ws.lay.i8)
@@ -531,7 +557,7 @@ int rmx_naive_prepare(const double* x, int64_t v, int32_t n, int32_t n1, int64_t
   Ws ws;
   if (int rc = get_ws(v, n, n1, L, workspace, workspace_bytes, &ws, st)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (int rc = prep_init(ws, L, s, st)) return rc;
+  if (int rc = prep_init(ws, n, n1, L, s, st)) return rc;
   if (int rc = prep_rows(x, v, n, n1, ws, 0, v, s, st)) return rc;
   RMX_CUDA(launch_const_reduce(x, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), s));
   return RMX_OK;
@@ -796,7 +822,7 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
                                cudaMemcpyHostToDevice, S.cp));
     RMX_CUDA(cudaEventRecord(e_rows[c], S.cp));
   }
-  if (int rc = prep_init(ws, L, S.pp, st)) return rc;
+  if (int rc = prep_init(ws, n, n1, L, S.pp, st)) return rc;
   for (cudaStream_t x : {S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e_ord, 0));
   for (int c = 0; c < nc; ++c) {
     int64_t v0, v1;

@@ -558,8 +558,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
     ec.dthr = a.dthr;
     // int8: quantisation error bound (K0); a truly degenerate voxel
     // (|S| = sqrt(gamma/|beta|)) then has d~ <= 2 |beta| sqrt(gamma/|beta|) e
-    const float emax = I8 ? __uint_as_float(a.counters->emax_bits) : 0.0f;
-    if (I8) ec.dthr = fmaxf(a.dthr, 2.5f * a.beta_abs * sqrtf(a.gamma / a.beta_abs) * emax);
+    // fp16 S-only: the a priori bound on |S~ - S| (rmx_abi.cu fp16_sonly_error_bound)
+    constexpr bool EBOUND = MODE == 0 && (I8 || SONLY);
+    const float emax = EBOUND ? __uint_as_float(a.counters->emax_bits) : 0.0f;
+    if (EBOUND)
+      ec.dthr = fmaxf(a.dthr, 2.5f * a.beta_abs * sqrtf(a.gamma / a.beta_abs) * emax);
     ec.alpha2 = pack2(__float_as_uint(a.alpha), __float_as_uint(a.alpha));
     ec.beta2 = pack2(__float_as_uint(a.beta), __float_as_uint(a.beta));
     ec.gamma2 = pack2(__float_as_uint(a.gamma), __float_as_uint(a.gamma));

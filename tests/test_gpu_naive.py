@@ -294,3 +294,92 @@ def test_host_range_shards_bit_identical_to_single_gpu(f32):
     null, arg = run_naive_distributed(x, plan)
     assert np.array_equal(null.maxima, full.maxima)
     assert np.array_equal(arg, full.argmax)
+
+
+def _near_identity_orders(n, n1, L, seed):
+    """Identity, then labellings that swap 1..3 subjects across the groups:
+    the highest-kappa statistics a strong effect can produce (the group-1
+    mean offset stays almost whole, the within-group variance tiny)."""
+    g = np.random.default_rng(seed)
+    rows = [np.arange(n)]
+    while len(rows) < L:
+        o = np.arange(n)
+        k = int(g.integers(1, 4))
+        a = g.choice(n1, k, replace=False)
+        b = n1 + g.choice(n - n1, k, replace=False)
+        o[a], o[b] = b, a
+        g.shuffle(o[:n1])
+        g.shuffle(o[n1:])
+        rows.append(o)
+    return np.stack(rows).astype(np.int16)
+
+
+def _high_kappa_data(v, n1, n2, seed, effect=3.0, noise=0.02):
+    g = np.random.default_rng(seed)
+    vals = g.standard_normal((v, n1 + n2)) * noise
+    vals[: v // 2, :n1] += effect          # kappa ~ 1 + (effect / 2 / noise)^2 ~ 5600
+    vals[v // 2:, :] += g.standard_normal((v - v // 2, 1)) * 5.0  # large voxel offsets
+    return rmx.DataMatrix(vals.astype(np.float32).astype(np.float64), n1, n2)
+
+
+@pytest.mark.parametrize("n1,n2,mode", [(10, 10, "f16"), (50, 50, "f16"), (200, 200, "i8"),
+                                        (200, 200, "f16"), (30, 70, "f16"), (120, 280, "f16")])
+def test_high_kappa_stress_bit_exact(oracle_mod, monkeypatch, n1, n2, mode):
+    """the refinement band must hold where cancellation in
+    Q - S^2/n1 is worst (strong effect, tiny within-group variance, labellings
+    one to three swaps from the truth).  Maxima and argmax must still equal
+    the oracle's bit for bit."""
+    from paper_1703_01506_b200.naive_engine import NaiveJob, cuda_device, upload
+
+    monkeypatch.setenv("RMX_I8", "1" if mode == "i8" else "0")
+    v, L = 3000, 384
+    x = _high_kappa_data(v, n1, n2, seed=n1 + n2)
+    orders = _near_identity_orders(n1 + n2, n1, L, seed=7)
+    xd, od = upload(x.values, orders, cuda_device())
+    mx, am = NaiveJob(xd, n1, od, False).run()
+    ref_mx, ref_am, _ = oracle_mod.naive_maxnull(x.values, n1, orders.astype(np.int64), False,
+                                                 threads=8)
+    assert np.array_equal(mx.cpu().numpy(), ref_mx)
+    assert np.array_equal(am.cpu().numpy(), ref_am)
+
+
+@pytest.mark.parametrize("n1", [10, 50])
+def test_fp16_accumulation_model(oracle_mod, monkeypatch, n1):
+    """The fp16 S-only band is derived (rmx_abi.cu fp16_sonly_error_bound) from
+    a model of the tensor core's fp32 accumulation: at most 2^-22 (|C| + sum
+    |products|) per K = 16 MMA.  Check the implied |S~ - S| against that bound
+    on adversarial rows: one dominant subject (|z| ~ sqrt(n)), alternating
+    signs (cancellation in the accumulator), near-constant rows (subnormal
+    lo halves)."""
+    from paper_1703_01506_b200.naive_engine import NaiveJob, cuda_device, upload
+
+    monkeypatch.setenv("RMX_I8", "0")
+    n = 2 * n1
+    g = np.random.default_rng(n1)
+    v, L = 4096, 256
+    vals = g.standard_normal((v, n))
+    vals[0::4, 0] += 1e3                                   # one dominant subject
+    vals[1::4] = np.where(np.arange(n) % 2, 1.0, -1.0) * (1 + 1e-3 * g.standard_normal(n))
+    vals[2::4] = 7.0 + 1e-4 * g.standard_normal((v // 4, n))  # tiny spread around a large mean
+    x = rmx.DataMatrix(vals.astype(np.float32).astype(np.float64), n1, n1)
+    plan = rmx.PermutationPlan(99, L, n)
+    orders = plan_orders(plan)
+    xd, od = upload(x.values, orders, cuda_device())
+    t_dbg = NaiveJob(xd, n1, od, False).tfill_debug().cpu().numpy().astype(np.float64)
+    _, _, T = oracle_mod.naive_maxnull(x.values, n1, orders.astype(np.int64), False,
+                                       materialize=True)
+    T = T.T
+    d1 = float(n1)
+    c = (d1 * d1 / n) ** 2
+    beta = c * (2.0 / (d1 * d1 * (d1 - 1.0)))
+    gamma = c * (n - 1.0) / (d1 * (d1 - 1.0))
+    s_of = lambda t: t * np.sqrt(gamma / (1.0 + beta * t * t))  # inverse of t = S / sqrt(gamma - beta S^2)
+    ok = np.isfinite(t_dbg)
+    dS = np.abs(s_of(t_dbg[ok]) - s_of(T[ok]))
+    kpad = (n + 15) // 16 * 16
+    P = np.sqrt(n1 * (n - 1.0))
+    u = 2.0 ** -22
+    e = u * P + n1 * 2.0 ** -25 + (2 * kpad / 16 + 1) * u * 1.001 * P
+    slack = 2e-7 * np.abs(s_of(T[ok])) + 1e-7   # the epilogue's own fp32 evaluation of t~
+    assert (dS <= e + slack).all(), (dS.max(), e)
+    assert dS.max() < 0.25 * e  # the model is conservative by a wide margin
