@@ -189,9 +189,10 @@ def rapid_block(device):
             **({"marks": [(tag, t - marks[0][1]) for tag, t in marks]} if marks else {})}
 
 
-def cpu_sample(cfg, x_host, orders_host, seconds: float, threads: int):
+def cpu_sample(cfg, x_host, orders_host, seconds: float, threads: int, min_perms: int = 0):
     """Time the oracle (C port of the reference path) on a bounded sample of
-    permutations of the same workload; returns (entries/s, sample text, threads)."""
+    permutations of the same workload (the plan's first P, P >= min_perms);
+    returns (entries/s, sample text, threads, seconds, maxima, argmax)."""
     from oracle import oracle
 
     v = x_host.shape[0]
@@ -203,23 +204,149 @@ def cpu_sample(cfg, x_host, orders_host, seconds: float, threads: int):
     dt = time.perf_counter() - t0
     per_round = max(dt, 1e-6)
     rounds = max(1, int(seconds / per_round))
-    P = min(orders_host.shape[0], p * rounds)
+    P = min(orders_host.shape[0], max(p * rounds, min_perms))
     t0 = time.perf_counter()
-    oracle.naive_maxnull(x_host, cfg.n1, orders_host[:P].astype("int64"), cfg.two_sided,
-                         threads=threads)
+    mx, am, _ = oracle.naive_maxnull(x_host, cfg.n1, orders_host[:P].astype("int64"),
+                                     cfg.two_sided, threads=threads)
     dt = time.perf_counter() - t0
-    return P * v / dt, f"{P} permutations x {v} voxels (first {P} of the plan)", threads, dt
+    return (P * v / dt, f"{P} permutations x {v} voxels (first {P} of the plan)", threads, dt,
+            mx, am)
+
+
+def _ref_import():
+    """The unmodified reference package installed in baseline/_ref (pure
+    Python; `pip install --target baseline/_ref /root/reference/pkg`)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "rapidmaxnull")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import rapidmaxnull
+
+    return rapidmaxnull
+
+
+def reference_numpy_naive(cfg, x_vals, perms: int = 2):
+    """The reference's own numpy engine (rapidmaxnull.run_naive from
+    baseline/_ref) on the plan's first `perms` permutations of the same
+    workload.  Below 32 permutations its block rule (naive.py:93) makes one
+    block, i.e. one thread: the rate is per core."""
+    R = _ref_import()
+    if R is None:
+        return {"unavailable": "baseline/_ref not installed"}
+    x = R.DataMatrix(x_vals, cfg.n1, cfg.n2)
+    plan = R.PermutationPlan(cfg.plan_seed, perms, cfg.subjects)
+    R.run_naive(x, R.PermutationPlan(cfg.plan_seed, 1, cfg.subjects), two_sided=cfg.two_sided,
+                threads=1)  # warm-up (page-in, BLAS init)
+    t0 = time.perf_counter()
+    null, _, _ = R.run_naive(x, plan, two_sided=cfg.two_sided, threads=1)
+    dt = time.perf_counter() - t0
+    return {"value": perms * cfg.voxels / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "seconds": dt, "maxima": [float(m) for m in null.maxima],
+            "sample": f"rapidmaxnull.run_naive (the unmodified reference, baseline/_ref) on the "
+                      f"plan's first {perms} permutations x {cfg.voxels} voxels, threads=1"}
+
+
+def reference_rapid_sample(x_vals, n1: int, n2: int):
+    """The reference's RapidPT at config 5 (n=400 (120/280), v=524,288,
+    L=1e5, eta=0.35%, r=l=400, 50 passes) timed by phase on bounded samples
+    and extrapolated: one exact training column
+    (tstat_full), 5 GROUSE updates (track_update on an orthonormal basis of
+    the right shape -- the update's cost does not depend on its values), and
+    one 32-permutation recovery span (the reference's span worker).
+    Basis-init QR (one 524,288 x 400 Householder QR) is not included."""
+    R = _ref_import()
+    if R is None:
+        return {"unavailable": "baseline/_ref not installed"}
+    import numpy as np
+    from rapidmaxnull import lrmc as RL
+    from rapidmaxnull import rapid as RR
+    from rapidmaxnull import streams as RS
+
+    v, n = x_vals.shape
+    ell = r = n
+    L, passes = 100_000, 50
+    k = int(np.ceil(0.0035 * v))
+    x = R.DataMatrix(x_vals, n1, n2)
+    plan = R.PermutationPlan(1703015065, L, n)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    x1, x2 = x.group_blocks(plan.shuffle(1))
+    col = R.tstat_full(x1, x2)
+    t_col = time.perf_counter() - t0
+    # an orthonormal v x r basis without the 40 s QR: the first r DCT-II
+    # vectors (exactly orthonormal; dense, so random row restrictions stay
+    # well conditioned like a trained basis)
+    i = (np.arange(v, dtype=np.float64) + 0.5) * (np.pi / v)
+    u = np.cos(np.outer(i, np.arange(r, dtype=np.float64))) * np.sqrt(2.0 / v)
+    u[:, 0] = 1.0 / np.sqrt(v)
+    b = R.Basis(u, copy=False)
+    upd = []
+    for i in range(5):
+        idx = np.sort(RS.stream(1703015065, RS.TRAIN_OMEGA, i, 0).choice(v, size=k, replace=False))
+        t0 = time.perf_counter()
+        RL.track_update(b, R.ObservedColumn(idx, col[idx]), 0.5)
+        upd.append(time.perf_counter() - t0)
+    t_upd = statistics.median(upd)
+    model = RR.SubspaceModel(basis=b, residual_std=0.5, max_shift=0.0, training_columns=ell,
+                             sample_rate=0.0035, training_maxima=np.zeros(ell), two_sided=False,
+                             seed=1703015065, passes=passes, converged=False)
+    # recovery: the reference's span worker (rapid.py:138-206) on a 32-permutation
+    # span, one thread; the reference runs spans on `threads` workers
+    # (rapid.py:232-240) -- extrapolated with ideal scaling over them
+    span = 32
+    out = np.empty(L)
+    t0 = time.perf_counter()
+    RR._recover_block(x, model, plan, ell, ell + span, k, out, [])
+    t_perm = (time.perf_counter() - t0) / span
+    train_s = ell * t_col + ell * passes * t_upd
+    recover_s = (L - ell) * t_perm / threads
+    return {"kind": "reference", "cores": threads, "extrapolated": True,
+            "train_s": train_s, "recover_s": recover_s, "max_null_s": train_s + recover_s,
+            "value": L * v / (train_s + recover_s), "unit": "T-entries/s (L x v / max-null time)",
+            "sample": (f"rapidmaxnull (baseline/_ref) at c5 shape: 1 training column "
+                       f"{t_col:.2f}s (x{ell}), median of 5 GROUSE updates {t_upd * 1e3:.0f} ms "
+                       f"(x{ell * passes}), one {span}-permutation recovery span "
+                       f"{t_perm * 1e3:.0f} ms/perm on one thread (x{L - ell} / {threads} "
+                       f"threads, ideal scaling); basis-init QR not included")}
+
+
+def _self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (never silently one GPU)."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "impl": args.impl, "n_gpus": args.gpus,
+                          "unavailable": f"--gpus {args.gpus} but {have} GPU(s) visible"}))
+        return 2
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     import numpy as np
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus and not (
+            world == 1 and os.environ.get("RMX_BENCH_FORCE_DIST")):
+        print(json.dumps({"metric": METRIC, "impl": args.impl, "n_gpus": world,
+                          "unavailable": f"WORLD_SIZE={world} but --gpus={args.gpus}"}))
+        return 2
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world != 1:
-        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
 
     from paper_1703_01506_b200.datagen import CONFIGS
 
@@ -229,7 +356,9 @@ def main():
                               f"grid={'x'.join(map(str, cfg.grid))} L={L} "
                               f"{'two-sided max|t|' if cfg.two_sided else 'signed max t'}",
                   "n": n, "n1": cfg.n1, "voxels": v, "permutations": L,
-                  "two_sided": cfg.two_sided, "parallelism": f"perm-shard x{args.gpus}"}
+                  "two_sided": cfg.two_sided, "parallelism": f"perm-shard x{args.gpus}",
+                  "l2": ("inputs > L2 (X 8 B x v x n + planes)" if v * n * 8 > 2 * 126e6
+                         else "L2 flushed between steps (256 MB write)")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -240,28 +369,48 @@ def main():
         from paper_1703_01506_b200.labels import generate_orders
 
         threads = os.cpu_count() or 1
-        # the reference statistic does not depend on the values' distribution for
-        # timing; build the full-size matrix with the deterministic generator
+        # the same workload's data (the deterministic numpy generator; the
+        # statistic's cost does not depend on the values)
         small = scaled(cfg, cfg.grid, L)
         x_host = make_data_numpy(small)
         need = min(L, max(threads * 64, 256))
         orders = generate_orders(cfg.plan_seed, 0, need, n)
-        vals = []
-        samples = []
+        vals, samples, secs = [], [], []
         for i in range(args.warmup + args.steps):
-            rate, text, thr, dt = cpu_sample(cfg, x_host, orders, args.cpu_seconds / 3, threads)
+            rate, text, thr, dt, _, _ = cpu_sample(cfg, x_host, orders, args.cpu_seconds / 3,
+                                                   threads)
             if i >= args.warmup:
                 vals.append(rate)
                 samples.append(text)
+                secs.append(dt)
         value = statistics.median(vals)
+        # beside the port: the reference's own numpy engine, and its RapidPT
+        # at config 5 by phase (both from baseline/_ref, measured once)
+        try:
+            ref_np = reference_numpy_naive(cfg, x_host, perms=2)
+        except Exception as exc:
+            ref_np = {"unavailable": str(exc)[:200]}
+        ref_rapid = None
+        if not args.no_rapid:
+            try:
+                ref_rapid = reference_rapid_sample(x_host, 120, 280)
+            except Exception as exc:
+                ref_rapid = {"unavailable": str(exc)[:200]}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * L / value * 1e3,
+                "steps": args.steps, "warmup": args.warmup,
+                # one step = one bounded sample (its measured wall time); the
+                # full workload at this rate would take full_workload_s_extrapolated
+                "ms_per_step": statistics.median(secs) * 1e3,
+                "ms_per_step_is": "measured wall time of one bounded sample (see cpu_baseline)",
+                "full_workload_s_extrapolated": v * L / value,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded smoothed Gaussian fields)",
                 "config": config_out, "impl": "reference",
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                                  "sample": samples[-1] + "; bit-exact C port of the reference "
                                  "statistic path (oracle/rmx_oracle.c), all host threads"},
+                "reference_numpy": {k: v_ for k, v_ in ref_np.items() if k != "maxima"},
+                "rapid": ref_rapid,
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -411,6 +560,7 @@ def main():
         x_host = DataMatrix(x_dev.to(torch.float32).cpu().numpy(), cfg.n1, cfg.n2)
         h2d_bytes = int(x_host.float32_values.nbytes)
         times = []
+        first_call_s = None
         for k in range(args.warmup + args.steps):
             barrier()
             t0 = time.perf_counter()
@@ -426,6 +576,8 @@ def main():
                 run_naive_distributed(x_host, plan, two_sided=cfg.two_sided)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            if k == 0:
+                first_call_s = dt  # includes page-locking X (cudaHostRegister) once
             if k >= args.warmup:
                 times.append(dt)
         t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=device)
@@ -436,22 +588,48 @@ def main():
                "x_host": "float32 v x n, page-locked (upcast to float64 on the device, exact)",
                "labels": "generated on the GPU inside the timed region (rmx_plan_orders)",
                "d2h_bytes_per_step": int(L * 12), "s_per_step": float(t[0]),
+               "first_call_s": first_call_s,
+               "first_call_note": "first call on a fresh host array: includes page-locking it "
+                                  "in place (cudaHostRegister, amortised by later calls)",
                "api": "paper_1703_01506_b200.run_naive_ex (N=1) / run_naive_distributed (N>1)"}
 
     # ---------------- CPU baseline (rank 0, N=1) ------------------------------
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        x_host_np = x_dev.cpu().numpy()
+        threads = os.cpu_count() or 1
+        orders_host = generate_orders(cfg.plan_seed, 0, min(L, max(threads * 64, 256)), n)
         try:
-            x_host_np = x_dev.cpu().numpy()
-            threads = os.cpu_count() or 1
-            orders_host = generate_orders(cfg.plan_seed, 0, min(L, max(threads * 64, 256)), n)
-            rate, text, thr, dt = cpu_sample(cfg, x_host_np, orders_host, args.cpu_seconds, threads)
+            rate, text, thr, dt, mx, am = cpu_sample(cfg, x_host_np, orders_host,
+                                                     args.cpu_seconds, threads, min_perms=256)
             cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
                    "sample": text + f" in {dt:.1f}s; bit-exact C port of the reference "
                                     "statistic path (oracle/rmx_oracle.c)"}
         except Exception as exc:  # the baseline never blocks our number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"failed: {exc}"}
+            mx = None
+        if mx is not None:
+            # the measured run's own maxima (the last timed step, same input) vs
+            # the oracle's on the same permutations: bit for bit
+            P = int(mx.size)
+            gm = sh.job.max_out[:P].cpu().numpy()
+            ga = sh.job.argmax_out[:P].cpu().numpy().astype(np.int64)
+            parity = {"perms_checked": P, "voxels": v, "bit_exact": bool(np.array_equal(gm, mx)),
+                      "argmax_equal": bool(np.array_equal(ga, am)),
+                      "maxima_differing": int(np.sum(gm != mx)),
+                      "against": "oracle/rmx_oracle.c (pinned bit-exact to the reference) on "
+                                 "the benchmarked input's first permutations"}
+        try:  # and the unmodified reference's own numpy engine on the first two
+            rn = reference_numpy_naive(cfg, x_host_np, perms=2)
+            if "maxima" in rn:
+                rm = np.asarray(rn.pop("maxima"))
+                parity["reference_numpy_perms_checked"] = int(rm.size)
+                parity["reference_numpy_bit_exact"] = bool(
+                    np.array_equal(sh.job.max_out[:rm.size].cpu().numpy(), rm))
+            cpu["reference_numpy"] = rn
+        except Exception as exc:
+            cpu["reference_numpy"] = {"unavailable": str(exc)[:200]}
 
     # ---------------- RapidPT, config 5 (N=1; training is not sharded) -------
     rapid = None
@@ -470,8 +648,7 @@ def main():
             "dtype": ("u8 x s8 -> s32 tensor (fixed-point z, exact) + f64 refine" if i8
                       else "f16x2-split tensor (fp32 acc) + f64 refine"),
             "data": "synthetic (seeded smoothed Gaussian fields, BASELINE.json design)",
-            "config": dict(config_out, l2="flushed between steps" if l2_flush is not None
-                           else "inputs > L2 (X 8 B x v x n + fp16 planes)"),
+            "config": config_out,
             "clocks": clk.summary(),
             "e2e": e2e,
             # per step: K0 prep, const-reduce, K1, K2 refine; the exhaustive
@@ -480,6 +657,7 @@ def main():
                                                 if stats0.get("overflow_perms", 0) else 0)),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
             "phases_ms": {"prepare": sum(prep_ms) / len(prep_ms), "tfill": tfill_avg,
                           "finish+gather": sum(fin_ms) / len(fin_ms)},
             "engine": stats,
@@ -489,6 +667,10 @@ def main():
         print(json.dumps(line))
     if dist_on:
         dist.destroy_process_group()
+    if parity is not None and not (parity["bit_exact"] and parity["argmax_equal"] and
+                                   parity.get("reference_numpy_bit_exact", True)):
+        print("bench: the measured run's maxima differ from the oracle's", file=sys.stderr)
+        return 3
     return 0
 
 
