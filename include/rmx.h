@@ -301,6 +301,27 @@ int rmx_track_update(double *u, int64_t v, int32_t r, const int32_t *idx, int32_
                      const double *vals, double step, double *resid_norm, void *stream,
                      rmx_status *st);
 
+/* numpy's Generator.standard_normal over the reference's streams, bit for
+ * bit, on host cores (replaces the normal draws of lrmc.py:85-93 BASIS_INIT
+ * and rapid.py:115-121 SHIFT_GAP).  rmx_normal_tables_set installs numpy's
+ * ziggurat tables (k, w, f: 256 entries each; normals.py reads them from the
+ * installed numpy).  rmx_standard_normal: stream(seed, *path) (npath <= 3)
+ * -> out[0..count) (host).  rmx_standard_normal_rows: rows i in [lo, hi) of
+ * stream(seed, domain, i), count each, into out32 (float, as numpy's float64
+ * cast) or out64, on `threads` host threads (0 = all). */
+int rmx_normal_tables_set(const uint64_t *k, const double *w, const double *f);
+int rmx_standard_normal(uint64_t seed, const uint32_t *path, int32_t npath, int64_t count,
+                        double *out, rmx_status *st);
+int rmx_standard_normal_rows(uint64_t seed, uint32_t domain, int64_t lo, int64_t hi,
+                             int64_t count, float *out32, double *out64, int32_t threads,
+                             rmx_status *st);
+/* The same stream drawn in consecutive pieces (open / fill* / close). */
+typedef struct rmx_normal_stream rmx_normal_stream;
+int rmx_normal_stream_open(uint64_t seed, const uint32_t *path, int32_t npath,
+                           rmx_normal_stream **out, rmx_status *st);
+int rmx_normal_stream_fill(rmx_normal_stream *h, int64_t count, double *out);
+int rmx_normal_stream_close(rmx_normal_stream *h);
+
 /* rmx_lsq_solve with the Gram on the tensor cores (v = rows of U): G~ =
  * [U_Omega | vals]^T [U_Omega | vals] from fp16 hi/lo planes (tcgen05,
  * fp32-accurate), Cholesky of G~ in fp64, then two steps of iterative

@@ -92,6 +92,12 @@ EXPORTS = (
     "rmx_lsq_solve_tc",
     "rmx_lsq_solve_exact",
     "rmx_track_update",
+    "rmx_normal_tables_set",
+    "rmx_standard_normal",
+    "rmx_standard_normal_rows",
+    "rmx_normal_stream_open",
+    "rmx_normal_stream_fill",
+    "rmx_normal_stream_close",
     "rmx_complete_max",
     "rmx_to_f32",
     "rmx_row_max",
@@ -165,6 +171,14 @@ _SIGS = {
                             ctypes.c_int),
     "rmx_track_update": ([_vp, _i64, _i32, _vp, _i32, _vp, ctypes.c_double,
                           ctypes.POINTER(ctypes.c_double), _vp, _SP], ctypes.c_int),
+    "rmx_normal_tables_set": ([_vp, _vp, _vp], ctypes.c_int),
+    "rmx_standard_normal": ([ctypes.c_uint64, _vp, _i32, _i64, _vp, _SP], ctypes.c_int),
+    "rmx_standard_normal_rows": ([ctypes.c_uint64, ctypes.c_uint32, _i64, _i64, _i64, _vp, _vp,
+                                  _i32, _SP], ctypes.c_int),
+    "rmx_normal_stream_open": ([ctypes.c_uint64, _vp, _i32, ctypes.POINTER(_vp), _SP],
+                               ctypes.c_int),
+    "rmx_normal_stream_fill": ([_vp, _i64, _vp], ctypes.c_int),
+    "rmx_normal_stream_close": ([_vp], ctypes.c_int),
     "rmx_complete_max": ([_vp, _i64, _i32, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double,
                           ctypes.c_uint64, _i32, _vp, _vp, _vp, _vp, _SP], ctypes.c_int),
     "rmx_to_f32": ([_vp, _i64, _vp, _vp, _SP], ctypes.c_int),

@@ -100,9 +100,12 @@ def device_omegas(seed: int, domain: int, lo: int, hi: int, v: int, k: int, dev,
 
 
 def draw_normals(seed: int, domain: int, lo: int, hi: int, v: int) -> np.ndarray:
-    """stream(seed, domain, i).standard_normal(v) for i in [lo, hi), fp32."""
-    return fill_rows((v,), np.float32,
-                     lambda i: stream(seed, domain, lo + i).standard_normal(v), hi - lo)
+    """stream(seed, domain, i).standard_normal(v) for i in [lo, hi), fp32
+    (numpy's float64 values, cast), by the native generator on all host
+    threads (normals.py)."""
+    from .normals import standard_normal_rows
+
+    return standard_normal_rows(seed, domain, lo, hi, v, dtype=np.float32)
 
 
 def _resample(seed: int, path: tuple, attempt: int, v: int, k: int) -> np.ndarray:
@@ -211,7 +214,7 @@ def init_basis(v: int, r: int, seed: int) -> Basis:
     if r < 1:
         raise UsageError("rank must be >= 1")
     dev = cuda_device()
-    u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, r)), dev)
+    u = _basis_init_async(seed, v, r, dev)()
     _orthonormalize(u, force=True)
     return Basis(u.cpu().numpy(), copy=False)
 
@@ -303,18 +306,52 @@ class TrainingResult:
 
 
 def _basis_init_async(seed: int, v: int, rank: int, dev):
-    """Draw init_basis's normals (lrmc.py:85-93: ONE sequential
-    stream(seed, BASIS_INIT) of v x rank doubles, ~1.9 s of host time at
-    config 5) on a background thread -- numpy releases the GIL for the whole
-    fill -- while the X upload, the training columns, the Omega draws and
-    the recovery statistics run on the GPU.  (Drawing in blocks and uploading
-    each behind the next was slower: every block re-acquires the GIL from a
-    main thread that is busy issuing that GPU work.)  Returns a joiner giving
-    the (v, rank) fp64 device tensor."""
-    join = _host_async(lambda: stream(seed, BASIS_INIT).standard_normal((v, rank)))
+    """init_basis's normals (lrmc.py:85-93: ONE sequential stream(seed,
+    BASIS_INIT) of v x rank doubles, 2.1e8 at config 5) drawn by the native
+    generator (normals.py, bit-identical to numpy) on a host thread while the
+    X upload, the training columns, the Omega draws and the recovery
+    statistics run on the GPU: 8 MB blocks into two page-locked buffers,
+    each block's upload (side stream) overlapping the next block's draw.
+    Returns a joiner giving the (v, rank) fp64 device tensor."""
+    torch = _torch()
+    from .hostmem import pinned_empty
+    from .normals import NormalStream
+
+    side = torch.cuda.Stream(dev)
+    out = torch.empty((v, rank), dtype=torch.float64, device=dev)
+    flat = out.view(-1)
+    total = v * rank
+    block = 1 << 20
+    bufs = [pinned_empty((block,), np.float64) for _ in range(2)]
+    done = [None, None]
+
+    def work():
+        torch.cuda.set_device(dev)
+        gen = NormalStream(seed, (BASIS_INIT,))
+        try:
+            for i, lo in enumerate(range(0, total, block)):
+                n = min(block, total - lo)
+                b = i & 1
+                if done[b] is not None:
+                    done[b].synchronize()  # the buffer's previous upload has left it
+                gen.fill(bufs[b][:n])
+                with torch.cuda.stream(side):
+                    flat[lo:lo + n].copy_(torch.from_numpy(bufs[b][:n]), non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                done[b] = ev
+        finally:
+            gen.close()
+        return out
+
+    join = _host_async(work)
 
     def joined():
-        return _to_dev(join(), dev)
+        t = join()
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_stream(side)
+        t.record_stream(cur)
+        return t
 
     return joined
 
@@ -395,10 +432,9 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
     joiner from _basis_init_async (else the normals are drawn here)."""
     torch = _torch()
     dev = t_dev.device
-    if init is not None:
-        u = init()
-    else:
-        u = _to_dev(stream(seed, BASIS_INIT).standard_normal((v, rank)), dev)
+    if init is None:
+        init = _basis_init_async(seed, v, rank, dev)
+    u = init()
     host_u = _host_array_async((v, rank)) if host_basis else None
     _mark("basis_normals_ready")
     _orthonormalize(u, force=True)
