@@ -51,16 +51,72 @@ inline double next_double(rmx::sfc::Sfc64& g) {
   return (double)(g.next64() >> 11) * (1.0 / 9007199254740992.0);
 }
 
-inline double standard_normal(rmx::sfc::Sfc64& g) {
-  for (;;) {
-    uint64_t r = g.next64();
-    const int idx = (int)(r & 0xff);
-    r >>= 8;
-    const int sign = (int)(r & 0x1);
+// rabs < 2^52 as a double, exactly (the bits of 2^52 + rabs, minus 2^52):
+// numpy's (double)rabs without x86's slow unsigned 64-bit conversion
+inline double exact_u52(uint64_t rabs) {
+  const uint64_t b = 0x4330000000000000ULL | rabs;
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d - 4503599627370496.0;
+}
+
+// The rare paths (idx 0 tail, wedge test), given the first word's parts.
+__attribute__((noinline)) double standard_normal_slow(rmx::sfc::Sfc64& g, int idx, uint64_t rabs,
+                                                      double x);
+
+// out[0..n) = the stream's next n normals.  The generator state lives in
+// registers across the loop and is written back only around the rare path.
+void fill_normals(rmx::sfc::Sfc64& g, int64_t n, double* out) {
+  uint64_t a = g.a, b = g.b, c = g.c, w = g.w;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t r0 = a + b + w++;  // Sfc64::next64, inlined on locals
+    a = b ^ (b >> 11);
+    b = c + (c << 3);
+    c = ((c << 24) | (c >> 40)) + r0;
+    const int idx = (int)(r0 & 0xff);
+    const uint64_t r = r0 >> 8;
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-    double x = (double)rabs * g_zig.w[idx];
-    if (sign & 0x1) x = -x;
-    if (rabs < g_zig.k[idx]) return x;  // ~99.3%
+    double x = exact_u52(rabs) * g_zig.w[idx];
+    uint64_t xb;
+    std::memcpy(&xb, &x, 8);
+    xb ^= (r & 0x1) << 63;
+    std::memcpy(&x, &xb, 8);
+    if (__builtin_expect(rabs < g_zig.k[idx], 1)) {
+      out[i] = x;
+      continue;
+    }
+    g.a = a;
+    g.b = b;
+    g.c = c;
+    g.w = w;
+    out[i] = standard_normal_slow(g, idx, rabs, x);
+    a = g.a;
+    b = g.b;
+    c = g.c;
+    w = g.w;
+  }
+  g.a = a;
+  g.b = b;
+  g.c = c;
+  g.w = w;
+}
+
+inline double standard_normal(rmx::sfc::Sfc64& g) {
+  const uint64_t r0 = g.next64();
+  const int idx = (int)(r0 & 0xff);
+  const uint64_t r = r0 >> 8;
+  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+  double x = exact_u52(rabs) * g_zig.w[idx];
+  uint64_t xb;  // x = -x when the sign bit is set, without a branch (50/50)
+  std::memcpy(&xb, &x, 8);
+  xb ^= (r & 0x1) << 63;
+  std::memcpy(&x, &xb, 8);
+  if (__builtin_expect(rabs < g_zig.k[idx], 1)) return x;  // ~99.3%
+  return standard_normal_slow(g, idx, rabs, x);
+}
+
+double standard_normal_slow(rmx::sfc::Sfc64& g, int idx, uint64_t rabs, double x) {
+  for (;;) {
     if (idx == 0) {
       for (;;) {  // 1 - U avoids log(0)
         const double xx = -kZigInvR * std::log1p(-next_double(g));
@@ -73,6 +129,15 @@ inline double standard_normal(rmx::sfc::Sfc64& g) {
           std::exp(-0.5 * x * x))
         return x;
     }
+    // rejected: numpy's loop draws a fresh word
+    uint64_t r = g.next64();
+    idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    rabs = (r >> 1) & 0x000fffffffffffffULL;
+    x = exact_u52(rabs) * g_zig.w[idx];
+    if (sign & 0x1) x = -x;
+    if (rabs < g_zig.k[idx]) return x;
   }
 }
 
@@ -111,7 +176,7 @@ int rmx_standard_normal(uint64_t seed, const uint32_t* path, int32_t npath, int6
     return fail(st, RMX_E_USAGE, "bad standard_normal arguments");
   rmx::sfc::Sfc64 g;
   seed_stream(g, seed, path, npath);
-  for (int64_t i = 0; i < count; ++i) out[i] = standard_normal(g);
+  fill_normals(g, count, out);
   return RMX_OK;
 }
 
@@ -137,7 +202,7 @@ int rmx_normal_stream_open(uint64_t seed, const uint32_t* path, int32_t npath,
 
 int rmx_normal_stream_fill(rmx_normal_stream* h, int64_t count, double* out) {
   if (!h || count < 0 || (count > 0 && !out)) return RMX_E_USAGE;
-  for (int64_t i = 0; i < count; ++i) out[i] = standard_normal(h->g);
+  fill_normals(h->g, count, out);
   return RMX_OK;
 }
 
@@ -167,8 +232,7 @@ int rmx_standard_normal_rows(uint64_t seed, uint32_t domain, int64_t lo, int64_t
       rmx::sfc::Sfc64 g;
       seed_stream(g, seed, path, 2);
       if (out64) {
-        double* o = out64 + i * count;
-        for (int64_t j = 0; j < count; ++j) o[j] = standard_normal(g);
+        fill_normals(g, count, out64 + i * count);
       } else {
         float* o = out32 + i * count;
         for (int64_t j = 0; j < count; ++j) o[j] = (float)standard_normal(g);

@@ -8,8 +8,6 @@
 #include <cstring>
 #include <vector>
 
-#include <cublas_v2.h>
-
 #include "../../include/rmx.h"
 #include "rapid_internal.cuh"
 #include "rmx_internal.cuh"
@@ -42,34 +40,6 @@ void rclear(rmx_status* st) {
     if (_e != cudaSuccess)                                                           \
       return rset(st, RMX_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(_e));   \
   } while (0)
-
-#define RBLAS(call)                                                                  \
-  do {                                                                               \
-    cublasStatus_t _b = (call);                                                      \
-    if (_b != CUBLAS_STATUS_SUCCESS)                                                 \
-      return rset(st, RMX_E_CUDA, "%s failed: cuBLAS status %d", #call, (int)_b);    \
-  } while (0)
-
-// plain fp64 library GEMMs of the deferred GROUSE (row-major operands)
-struct Blas {
-  cublasHandle_t h = nullptr;
-  ~Blas() {
-    if (h) cublasDestroy(h);
-  }
-  // C (m x n, ldc) = A (m x kk, lda) B (kk x n, ldb)
-  cublasStatus_t gemm_rm(int64_t m, int n, int kk, const double* A, int64_t lda, const double* B,
-                         int64_t ldb, double* C, int64_t ldc, double beta = 0.0) const {
-    const double one = 1.0;
-    return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)m, kk, &one, B, (int)ldb, A, (int)lda,
-                       &beta, C, (int)ldc);
-  }
-  // G (n x n, row- or column-major: symmetric) = A^T A, A (rows x n, lda)
-  cublasStatus_t gram(int64_t rows, int n, const double* A, int64_t lda, double* G) const {
-    const double one = 1.0, zero = 0.0;
-    return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, (int)rows, &one, A, (int)lda, A,
-                       (int)lda, &zero, G, n);
-  }
-};
 
 constexpr double kCondLimit = 1e12;  // lrmc.py:22 COND_LIMIT
 
@@ -490,9 +460,6 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(idxbuf.alloc(k, s));
   const int64_t lu = r + 1;  // ug rows: [U_Omega row | t_Omega] (the Gram's operand)
   RCUDA(ug.alloc((size_t)k * lu, s));
-  Blas blas;
-  RBLAS(cublasCreate(&blas.h));
-  RBLAS(cublasSetStream(blas.h, s));
   RCUDA(ub2.alloc((size_t)v * kDeferCap, s));  // T = U_base X (flush)
   RCUDA(M.alloc((size_t)r * r, s));
   RCUDA(Xf.alloc((size_t)r * kDeferCap, s));
@@ -529,8 +496,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   double* ubase = u;
   auto flush = [&](int nt) -> int {
     if (nt > 0) {
-      RBLAS(blas.gemm_rm(v, nt, r, ubase, r, Xf.p, kDeferCap, ub2.p, kDeferCap));
-      RBLAS(blas.gemm_rm(v, r, nt, ub2.p, kDeferCap, Yf.p, r, ubase, r, 1.0));
+      RCUDA(launch_dgemm_rm(v, nt, r, ubase, r, Xf.p, kDeferCap, ub2.p, kDeferCap, 0, s));
+      RCUDA(launch_dgemm_rm(v, r, nt, ub2.p, kDeferCap, Yf.p, r, ubase, r, 1, s));
     }
     RCUDA(launch_sparse_terms(ubase, r, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
     RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));
@@ -546,10 +513,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const double* trow = t + (int64_t)i * v;
     // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
     RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, s));
-    RBLAS(blas.gemm_rm(k, kDeferCap, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap));
-    RBLAS(blas.gemm_rm(k, r, kDeferCap, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1.0));
+    RCUDA(launch_dgemm_rm(k, kDeferCap, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap, 0, s));
+    RCUDA(launch_dgemm_rm(k, r, kDeferCap, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
-    RBLAS(blas.gram(k, (int)lu, ug.p, lu, G.p));
+    // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
+    RCUDA(launch_gram(ug.p, lu, r, nullptr, k, vals.p, G.p, 1, s));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
     if (use_cg) {
       RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,

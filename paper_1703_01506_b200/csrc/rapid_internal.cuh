@@ -148,5 +148,9 @@ size_t lu_solve_work(int r, int64_t count);
 cudaError_t launch_track_apply(double* U, int64_t v, int r, double* pred, double a,
                                const int32_t* idx, int k, const double* resid, double b,
                                const double* w, double winv, cudaStream_t s);
+// dgemm.cu: C (m x n, ldc) = A (m x kk, lda) B (kk x n, ldb) (+ C when accum), row-major fp64
+cudaError_t launch_dgemm_rm(int64_t m, int n, int kk, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double* C, int64_t ldc, int accum,
+                            cudaStream_t s);
 cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s);
 }  // namespace rmx

@@ -34,3 +34,13 @@ def test_abi_version_and_sm100_code():
                           text=True).stdout
     # tcgen05 MMA, TMA tile loads and TMEM loads are in the binary (sm_100a)
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_no_library_gemm_linked():
+    """the GROUSE products are the engine's own kernels
+    (csrc/dgemm.cu, k_gram), not cuBLAS: nothing links or imports it."""
+    out = subprocess.run(["ldd", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in out.lower()
+    und = subprocess.run(["nm", "-D", "--undefined-only", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "cublas" not in und.lower()
