@@ -124,63 +124,105 @@ int rmx_lsq_solve(const double* u, int64_t ldu, int32_t r, const int32_t* idx, i
 // solved by Cholesky, or by pivoted LU (np.linalg.solve's algorithm) when
 // the Cholesky meets a non-positive pivot; rejected systems (cond > 1e12)
 // get w = U_Omega^T vals, the reference's solve against the identity.
-int rmx_lsq_solve_exact(const double* u, int64_t ldu, int32_t r, const int32_t* idx, int32_t k,
-                        const double* vals, int64_t B, double* w_out, int32_t* flag_out,
-                        double* cond_out, void* stream, rmx_status* st) {
-  rclear(st);
-  if (r < 1 || k < r || B < 1 || !vals || !w_out)
-    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+
+// Pivot ratio max L_ii / min L_ii of the Gram's Cholesky factor (a lower
+// bound of cond(U_Omega)) above which a system's condition number is
+// evaluated exactly (the reference's decision needs it only near 1e12; the
+// restrictions of a random row sample sit at ~2-10).
+constexpr double kBorderRatio = 1e4;
+
+// exact_all: every system's cond exactly (public solve_block semantics);
+// else only the Cholesky-flagged or borderline ones (internal fits).
+int lsq_exact_impl(const double* u, int64_t ldu, int32_t r, const int32_t* idx, int32_t k,
+                   const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                   double* cond_out, bool exact_all, cudaStream_t s, rmx_status* st) {
   const int64_t ld = r + 1;
-  const size_t per = gram_bytes(r) + sym_extreme_eigs_work(r, 1) + 8 * sizeof(double);
+  const size_t per = gram_bytes(r) + (exact_all ? sym_extreme_eigs_work(r, 1) : 0) +
+                     8 * sizeof(double);
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, ((int64_t)1 << 30) / (int64_t)per));
-  DevBuf<double> G, work, lam, nrm, cond;
+  DevBuf<double> G, work, lam, nrm;
   DevBuf<int32_t> cflag, sel;
   RCUDA(G.alloc((size_t)chunk * ld * ld, s));
-  RCUDA(work.alloc(std::max(sym_extreme_eigs_work(r, chunk), lu_solve_work(r, 1)) / 8 + 1, s));
+  const size_t wbytes = std::max(sym_extreme_eigs_work(r, exact_all ? chunk : 1),
+                                 lu_solve_work(r, 1));
+  RCUDA(work.alloc(wbytes / 8 + 1, s));
   RCUDA(lam.alloc((size_t)2 * chunk, s));
   RCUDA(nrm.alloc((size_t)4 * chunk, s));
-  RCUDA(cond.alloc((size_t)B, s));
   RCUDA(cflag.alloc((size_t)chunk, s));
   RCUDA(sel.alloc(1, s));
-  std::vector<double> hl((size_t)2 * chunk), hc((size_t)B);
-  std::vector<int32_t> hf((size_t)chunk), hflag((size_t)B);
+  const int32_t zero = 0;
+  RCUDA(cudaMemcpyAsync(sel.p, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  std::vector<double> hl((size_t)2 * chunk), hn((size_t)4 * chunk);
+  std::vector<int32_t> hf((size_t)chunk);
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t cnt = std::min(chunk, B - b0);
     const int32_t* ib = idx ? idx + b0 * k : nullptr;
     RCUDA(launch_gram(u, ldu, r, ib, k, vals + b0 * k, G.p, cnt, s));
-    RCUDA(launch_sym_extreme_eigs(G.p, ld * ld, (int)ld, r, nullptr, cnt, work.p, lam.p, s));
+    if (exact_all)
+      RCUDA(launch_sym_extreme_eigs(G.p, ld * ld, (int)ld, r, nullptr, cnt, work.p, lam.p, s));
     RCUDA(launch_chol_solve(G.p, r, cnt, w_out + b0 * r, cflag.p, nrm.p, s));
-    RCUDA(cudaMemcpyAsync(hl.data(), lam.p, (size_t)2 * cnt * sizeof(double),
+    if (exact_all)
+      RCUDA(cudaMemcpyAsync(hl.data(), lam.p, (size_t)2 * cnt * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaMemcpyAsync(hn.data(), nrm.p, (size_t)4 * cnt * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
     RCUDA(cudaMemcpyAsync(hf.data(), cflag.p, (size_t)cnt * sizeof(int32_t),
                           cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
     for (int64_t j = 0; j < cnt; ++j) {
-      const double lo = hl[2 * j], hi = hl[2 * j + 1];
-      const double c = lo > 0.0 ? std::sqrt(hi / lo) : INFINITY;
       const int64_t b = b0 + j;
-      hc[b] = c;
+      const double ratio = hn[4 * j + 2] > 0.0 ? hn[4 * j + 3] / hn[4 * j + 2] : INFINITY;
+      const bool known = exact_all;
+      const bool need = hf[j] != 0 || !(ratio <= kBorderRatio);
+      double c = ratio;  // a lower bound, exact below
+      bool reform = false;
+      if (known) {
+        const double lo = hl[2 * j], hi = hl[2 * j + 1];
+        c = lo > 0.0 ? std::sqrt(hi / lo) : INFINITY;
+      } else if (need) {  // borderline: this system's exact cond (re-form its Gram)
+        RCUDA(launch_gram(u, ldu, r, idx ? idx + b * k : nullptr, k, vals + b * k, G.p, 1, s));
+        RCUDA(launch_sym_extreme_eigs(G.p, ld * ld, (int)ld, r, sel.p, 1, work.p, lam.p, s));
+        double l2[2];
+        RCUDA(cudaMemcpyAsync(l2, lam.p, sizeof(l2), cudaMemcpyDeviceToHost, s));
+        RCUDA(cudaStreamSynchronize(s));
+        c = l2[0] > 0.0 ? std::sqrt(l2[1] / l2[0]) : INFINITY;
+        reform = true;
+      }
+      if (cond_out) cond_out[b] = c;
       const bool bad = !(c <= kCondLimit);
-      hflag[b] = bad ? 1 : 0;
+      if (flag_out) flag_out[b] = bad ? 1 : 0;
       if (!bad && hf[j] == 0) continue;
-      // rare: re-form this system's Gram, then LU (accepted) or w = rhs (rejected)
-      RCUDA(launch_gram(u, ldu, r, idx ? idx + b * k : nullptr, k, vals + b * k, G.p, 1, s));
+      // rare: LU (accepted, Cholesky failed) or w = rhs (rejected)
+      if (!reform)
+        RCUDA(launch_gram(u, ldu, r, idx ? idx + b * k : nullptr, k, vals + b * k, G.p, 1, s));
       if (bad) {
         RCUDA(cudaMemcpyAsync(w_out + b * r, G.p + (int64_t)r * ld, (size_t)r * sizeof(double),
                               cudaMemcpyDeviceToDevice, s));
       } else {
-        const int32_t zero = 0;
-        RCUDA(cudaMemcpyAsync(sel.p, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, s));
         RCUDA(launch_lu_solve(G.p, ld * ld, (int)ld, r, sel.p, 1, work.p, w_out + b * r, nullptr,
                               s));
       }
       RCUDA(cudaStreamSynchronize(s));
     }
   }
-  if (cond_out) std::memcpy(cond_out, hc.data(), (size_t)B * sizeof(double));
-  if (flag_out) std::memcpy(flag_out, hflag.data(), (size_t)B * sizeof(int32_t));
   return RMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rmx_lsq_solve_exact(const double* u, int64_t ldu, int32_t r, const int32_t* idx, int32_t k,
+                        const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                        double* cond_out, void* stream, rmx_status* st) {
+  rclear(st);
+  if (r < 1 || k < r || B < 1 || !vals || !w_out)
+    return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
+  return lsq_exact_impl(u, ldu, r, idx, k, vals, B, w_out, flag_out, cond_out, true,
+                        static_cast<cudaStream_t>(stream), st);
 }
 
 // One GROUSE update (lrmc.py:160-193 track_update) on a device basis U (v x
@@ -297,8 +339,8 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
     if (hf[b] == 0 && hn[b] == 0) continue;
     ++redo;
     int32_t bad = 0;
-    if (int rc = rmx_lsq_solve_exact(u, ldu, r, idx + b * k, k, vals + b * k, 1, w_out + b * r,
-                                     &bad, nullptr, stream, st))
+    if (int rc = lsq_exact_impl(u, ldu, r, idx + b * k, k, vals + b * k, 1, w_out + b * r, &bad,
+                                nullptr, false, s, st))
       return rc;
     hf[b] = bad;
   }

@@ -105,7 +105,10 @@ def make_data_numpy(cfg: Config, workers: Optional[int] = None) -> np.ndarray:
         import multiprocessing as mp
         from concurrent.futures import ProcessPoolExecutor
 
-        with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as pool:
+        # forkserver: the workers fork from a clean server process, never from
+        # this one (which may hold CUDA contexts and host threads: forking it
+        # can deadlock the child)
+        with ProcessPoolExecutor(workers, mp_context=mp.get_context("forkserver")) as pool:
             cols = list(pool.map(_subject_numpy, jobs, chunksize=4))
     else:
         cols = [_subject_numpy(a) for a in jobs]

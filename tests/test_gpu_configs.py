@@ -50,11 +50,13 @@ def _report(key, obj):
 
 
 def _data(name):
-    if name not in _CACHE:
-        cfg = CONFIGS[name]
-        vals = make_data_numpy(cfg)
-        _CACHE[name] = (cfg, vals)
-    return _CACHE[name]
+    # config 3 runs on config 2's data, config 5 on config 4's grid and noise
+    # but its own group split (different effect subjects): key by the data
+    cfg = CONFIGS[name]
+    key = (cfg.grid, cfg.n1, cfg.n2, cfg.seed, cfg.effect, cfg.sigma)
+    if key not in _CACHE:
+        _CACHE[key] = make_data_numpy(cfg)
+    return cfg, _CACHE[key]
 
 
 def _sha(a):
