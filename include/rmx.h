@@ -196,6 +196,35 @@ int rmx_naive_maxnull_host_plan_range_f32(const float *x_host, int64_t v, int32_
                                           size_t workspace_bytes, void *stream, rmx_status *st,
                                           rmx_naive_stats *stats);
 
+/* NaivePT straight from a .mat0 data file (the reference CLI
+ * path cli.py:70-116 = read_matrix -> run_naive -> [write_array of T]):
+ * the v x n float64 payload is streamed file -> ring_host (page-locked,
+ * ring_bytes, 2-3 slots) -> device in pieces by parallel positional reads,
+ * each chunk standardised (K0) and contracted (K1) as it lands while the
+ * host reads the next; labels of plan rows [perm_base, perm_base + L) are
+ * generated on the device.  Non-finite payload entries: RMX_E_FORMAT with
+ * *bad_index = the flat element index (the reference's read_array check).
+ * Header validation and n1/n2 are the caller's (matio.py messages).
+ * x_dev (v x n fp64) keeps the data for a follow-up rmx_tstat_dump_mat0. */
+int rmx_naive_maxnull_mat0(const char *path, int64_t v, int32_t n, int32_t n1,
+                           uint64_t plan_seed, int64_t perm_base, int64_t L, int32_t two_sided,
+                           double *max_host, int32_t *argmax_host, double *ring_host,
+                           size_t ring_bytes, int32_t threads, int64_t *bad_index, double *x_dev,
+                           int16_t *orders_dev, double *max_dev, int32_t *argmax_dev,
+                           void *workspace, size_t workspace_bytes, void *stream,
+                           rmx_status *st, rmx_naive_stats *stats);
+/* The streamed --dump-T writer (reference naive.py:79-87 materialize=True +
+ * cli.py:114-116 write_array(mat.values)): the (v, L) float64 statistic
+ * matrix T[j, i] = tstat(perm i, voxel j) -- the reference's exact bits
+ * (k_exact_rows) -- written to `path` as a bare .mat0 (n1 = n2 = 0) in voxel
+ * slabs: slab b computed, transposed and copied to one half of ring_host
+ * while the host writes slab b - 1.  Never holds T on the host; no memory
+ * cap.  A degenerate (perm, voxel) raises RMX_E_DEGENERATE and removes the
+ * file. */
+int rmx_tstat_dump_mat0(const double *x_dev, int64_t v, int32_t n, int32_t n1,
+                        const int16_t *orders_dev, int64_t L, const char *path, double *ring_host,
+                        size_t ring_bytes, int32_t threads, void *stream, rmx_status *st);
+
 /* ---------------------------------------------------------------- .mat0 I/O
  * The reference's binary matrix format (matio.py:23-91): 44-byte header
  * "<8sIQQQQ" = magic "RMXMAT0\0", u32 version (1), u64 rows, cols, n1, n2;
@@ -217,6 +246,20 @@ int rmx_mat0_header(const char *path, rmx_mat0_info *info, rmx_status *st);
  * index).  Replaces reference matio.py:58-72. */
 int rmx_mat0_read(const char *path, int64_t rows, int64_t cols, double *out, int32_t threads,
                   int64_t *bad_index, rmx_status *st);
+/* Rows [row0, row1) of a cols-wide payload -> out (same checks as
+ * rmx_mat0_read; *bad_index is a flat index of the whole file).  The piece
+ * reader of the streamed engine entry rmx_naive_maxnull_mat0.  Replaces the
+ * payload read of reference matio.py:58-72 for a row range. */
+int rmx_mat0_read_rows(const char *path, int64_t cols, int64_t row0, int64_t row1, double *out,
+                       int32_t threads, int64_t *bad_index, rmx_status *st);
+/* Create (truncate) a .mat0 file: header + a rows x cols payload to be
+ * filled by rmx_mat0_write_rows (the streamed --dump-T writer). */
+int rmx_mat0_create(const char *path, int64_t rows, int64_t cols, int64_t n1, int64_t n2,
+                    rmx_status *st);
+/* Rows [row0, row1) of the payload from a (row1 - row0) x cols host buffer,
+ * parallel positional writes. */
+int rmx_mat0_write_rows(const char *path, int64_t cols, int64_t row0, int64_t row1,
+                        const double *a, int32_t threads, rmx_status *st);
 /* Header + payload.  Replaces reference matio.py:30-37 write_array. */
 int rmx_mat0_write(const char *path, const double *a, int64_t rows, int64_t cols, int64_t n1,
                    int64_t n2, rmx_status *st);

@@ -38,7 +38,14 @@ from .matfiles import (  # noqa: F401
     write_matrix,
     write_matrix_csv,
 )
-from .naive_engine import NaiveJob, NaiveResult, run_naive, run_naive_ex  # noqa: F401
+from .naive_engine import (  # noqa: F401
+    NaiveJob,
+    NaiveResult,
+    dump_statistic_matrix,
+    run_naive,
+    run_naive_ex,
+    run_naive_mat0,
+)
 from .rapid_engine import (  # noqa: F401
     complete_column,
     fit_coefficients,
@@ -75,7 +82,7 @@ __all__ = [
     "RunConfig", "StatMatrix", "SubspaceModel", "min_sample_rate", "permute_columns", "relabel",
     "DataFormatError", "DegenerateVoxelError", "EngineUnavailableError",
     "IllConditionedBasisError", "NumericalError", "UsageError", "NaiveJob", "NaiveResult",
-    "run_naive", "run_naive_ex", "column_max", "pvalue", "reject_set", "stat_map",
+    "run_naive", "run_naive_ex", "run_naive_mat0", "dump_statistic_matrix", "column_max", "pvalue", "reject_set", "stat_map",
     "threshold_at", "tstat_full", "tstat_subset", "complete_column", "fit_coefficients",
     "init_basis", "recover", "run_rapid", "solve_block", "train", "train_basis",
     "track_update", "StatColumn", "HistogramPair", "RiskResult", "ThresholdRow",

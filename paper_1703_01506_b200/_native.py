@@ -110,6 +110,11 @@ EXPORTS = (
     "rmx_mat0_header",
     "rmx_mat0_read",
     "rmx_mat0_write",
+    "rmx_mat0_read_rows",
+    "rmx_mat0_create",
+    "rmx_mat0_write_rows",
+    "rmx_naive_maxnull_mat0",
+    "rmx_tstat_dump_mat0",
 )
 
 
@@ -163,6 +168,15 @@ _SIGS = {
     "rmx_mat0_read": ([ctypes.c_char_p, _i64, _i64, _vp, _i32, ctypes.POINTER(_i64), _SP],
                       ctypes.c_int),
     "rmx_mat0_write": ([ctypes.c_char_p, _vp, _i64, _i64, _i64, _i64, _SP], ctypes.c_int),
+    "rmx_mat0_read_rows": ([ctypes.c_char_p, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_i64),
+                            _SP], ctypes.c_int),
+    "rmx_mat0_create": ([ctypes.c_char_p, _i64, _i64, _i64, _i64, _SP], ctypes.c_int),
+    "rmx_mat0_write_rows": ([ctypes.c_char_p, _i64, _i64, _i64, _vp, _i32, _SP], ctypes.c_int),
+    "rmx_naive_maxnull_mat0": ([ctypes.c_char_p, _i64, _i32, _i32, ctypes.c_uint64, _i64, _i64,
+                                _i32, _vp, _vp, _vp, _sz, _i32, ctypes.POINTER(_i64), _vp, _vp,
+                                _vp, _vp, _vp, _sz, _vp, _SP, _NP], ctypes.c_int),
+    "rmx_tstat_dump_mat0": ([_vp, _i64, _i32, _i32, _vp, _i64, ctypes.c_char_p, _vp, _sz, _i32,
+                             _vp, _SP], ctypes.c_int),
     "rmx_lsq_solve_tc": ([_vp, _i64, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp,
                           _SP], ctypes.c_int),
     "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],

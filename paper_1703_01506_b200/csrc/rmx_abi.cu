@@ -12,6 +12,8 @@
 #include <cstring>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/rmx.h"
 #include "rmx_internal.cuh"
 
@@ -726,7 +728,49 @@ namespace {
 // device (plan_seed, generated on the prep stream while X's first chunk is
 // in flight), or already in orders_dev (both null).  X from x_host (fp64) or
 // x_host32 (fp32, staged in x32_dev).
-int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
+// X streamed from a .mat0 file (rmx_naive_maxnull_mat0): rows are read by
+// parallel positional reads into a caller-provided page-locked ring of
+// `nslots` slots and copied from there; the host reads piece p + 1 while the
+// copy engine moves piece p and the GPU standardises / contracts the
+// chunks already landed.  A slot is reused only after its copy completed.
+struct FileSrc {
+  const char* path = nullptr;
+  double* ring = nullptr;
+  int64_t slot_rows = 0;
+  int nslots = 0;
+  int threads = 0;
+  int64_t* bad_index = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<bool> used;
+  int next = 0;
+  ~FileSrc() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+  // rows [r0, r1) of the file -> x_dev (row-major, n columns) on stream cp
+  int rows_to_device(int64_t r0, int64_t r1, int32_t n, double* x_dev, cudaStream_t cp,
+                     rmx_status* st) {
+    if (ev.empty()) {
+      ev.resize(nslots);
+      used.assign(nslots, false);
+      for (auto& e : ev) RMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (int64_t a = r0; a < r1; a += slot_rows) {
+      const int64_t b = std::min(r1, a + slot_rows);
+      const int slot = next;
+      next = (next + 1) % nslots;
+      if (used[slot]) RMX_CUDA(cudaEventSynchronize(ev[slot]));
+      double* buf = ring + (size_t)slot * slot_rows * n;
+      if (int rc = rmx_mat0_read_rows(path, n, a, b, buf, threads, bad_index, st)) return rc;
+      RMX_CUDA(cudaMemcpyAsync(x_dev + a * n, buf, (size_t)(b - a) * n * 8,
+                               cudaMemcpyHostToDevice, cp));
+      RMX_CUDA(cudaEventRecord(ev[slot], cp));
+      used[slot] = true;
+    }
+    return RMX_OK;
+  }
+};
+
+int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev, FileSrc* fsrc,
                     int64_t v, int32_t n, int32_t n1,
                     const int16_t* orders_host, const uint64_t* plan_seed, int64_t perm_base,
                     int64_t L, int32_t two_sided, double* max_host, int32_t* argmax_host, double* x_dev,
@@ -738,7 +782,7 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
   if (plan_seed && (n > 32767 || perm_base < 0 || perm_base + L > 0xFFFFFFFFLL))
     return set_status(st, RMX_E_USAGE, "plan of %lld permutations of n=%d not representable",
                       (long long)L, n);
-  if ((!x_host && !(x_host32 && x32_dev)) || !max_host || !argmax_host || !x_dev ||
+  if ((!x_host && !(x_host32 && x32_dev) && !fsrc) || !max_host || !argmax_host || !x_dev ||
       !orders_dev || !max_dev || !argmax_dev)
     return set_status(st, RMX_E_USAGE, "null buffer");
   if ((reinterpret_cast<uintptr_t>(x_host32) | reinterpret_cast<uintptr_t>(x32_dev)) & 15)
@@ -755,7 +799,12 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
     return RMX_OK;
   };
   if (ws.lay.stages == 0) {  // exhaustive exact path: nothing to overlap
-    if (x_host) {
+    if (fsrc) {
+      if (int rc = fsrc->rows_to_device(0, v, n, x_dev, s, st)) {
+        cudaStreamSynchronize(s);
+        return rc;
+      }
+    } else if (x_host) {
       RMX_CUDA(cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, s));
     } else {
       RMX_CUDA(cudaMemcpyAsync(x32_dev, x_host32, xbytes / 2, cudaMemcpyHostToDevice, s));
@@ -811,24 +860,30 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
   } else {
     RMX_CUDA(cudaEventRecord(e_ord, S.cp));
   }
-  for (int c = 0; c < nc; ++c) {
-    int64_t v0, v1;
-    chunk_voxels(ws.lay, v, c, &v0, &v1);
-    if (v1 > v0 && x_host)
-      RMX_CUDA(cudaMemcpyAsync(x_dev + v0 * n, x_host + v0 * n, (size_t)(v1 - v0) * n * 8,
-                               cudaMemcpyHostToDevice, S.cp));
-    else if (v1 > v0)
-      RMX_CUDA(cudaMemcpyAsync(x32_dev + v0 * n, x_host32 + v0 * n, (size_t)(v1 - v0) * n * 4,
-                               cudaMemcpyHostToDevice, S.cp));
-    RMX_CUDA(cudaEventRecord(e_rows[c], S.cp));
-  }
   if (int rc = prep_init(ws, n, n1, L, S.pp, st)) return rc;
   for (cudaStream_t x : {S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e_ord, 0));
+  // chunk c: its rows' copy (after the host read them, for a file), then K0
+  // and K1 on them; enqueued chunk by chunk so a file's reads overlap the
+  // copies and the engine work of the chunks before
   for (int c = 0; c < nc; ++c) {
     int64_t v0, v1;
     chunk_voxels(ws.lay, v, c, &v0, &v1);
+    if (v1 > v0 && fsrc) {
+      if (int rc = fsrc->rows_to_device(v0, v1, n, x_dev, S.cp, st)) {
+        for (cudaStream_t x : {S.cp, S.pp, S.k[0], S.k[1]}) cudaStreamSynchronize(x);
+        return rc;
+      }
+    } else if (v1 > v0 && x_host) {
+      RMX_CUDA(cudaMemcpyAsync(x_dev + v0 * n, x_host + v0 * n, (size_t)(v1 - v0) * n * 8,
+                               cudaMemcpyHostToDevice, S.cp));
+    } else if (v1 > v0) {
+      RMX_CUDA(cudaMemcpyAsync(x32_dev + v0 * n, x_host32 + v0 * n, (size_t)(v1 - v0) * n * 4,
+                               cudaMemcpyHostToDevice, S.cp));
+    }
+    RMX_CUDA(cudaEventRecord(e_rows[c], S.cp));
     RMX_CUDA(cudaStreamWaitEvent(S.pp, e_rows[c], 0));
-    if (!x_host) RMX_CUDA(rmx::launch_upcast(x32_dev + v0 * n, (v1 - v0) * n, x_dev + v0 * n, S.pp));
+    if (!x_host && !fsrc)
+      RMX_CUDA(rmx::launch_upcast(x32_dev + v0 * n, (v1 - v0) * n, x_dev + v0 * n, S.pp));
     if (int rc = prep_rows(x_dev, v, n, n1, ws, v0, v1, S.pp, st)) return rc;
     RMX_CUDA(cudaEventRecord(e_prep[c], S.pp));
     cudaStream_t ks = S.k[c & 1];
@@ -856,7 +911,7 @@ int rmx_naive_maxnull_host(const double* x_host, int64_t v, int32_t n, int32_t n
                            int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                            void* workspace, size_t workspace_bytes, void* stream,
                            rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, orders_host, nullptr, 0, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, nullptr, v, n, n1, orders_host, nullptr, 0, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -867,7 +922,7 @@ int rmx_naive_maxnull_host_plan(const double* x_host, int64_t v, int32_t n, int3
                                 int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
                                 void* workspace, size_t workspace_bytes, void* stream,
                                 rmx_status* st, rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, 0, L, two_sided, max_host,
+  return naive_host_impl(x_host, nullptr, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, 0, L, two_sided, max_host,
                          argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -879,7 +934,7 @@ int rmx_naive_maxnull_host_f32(const float* x_host, int64_t v, int32_t n, int32_
                                int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
                                void* stream, rmx_status* st, rmx_naive_stats* stats) {
   if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
-  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, orders_host, nullptr, 0, L, two_sided,
+  return naive_host_impl(nullptr, x_host, x32_dev, nullptr, v, n, n1, orders_host, nullptr, 0, L, two_sided,
                          max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -891,7 +946,7 @@ int rmx_naive_maxnull_host_plan_f32(const float* x_host, int64_t v, int32_t n, i
                                     int32_t* argmax_dev, void* workspace, size_t workspace_bytes,
                                     void* stream, rmx_status* st, rmx_naive_stats* stats) {
   if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
-  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, 0, L, two_sided,
+  return naive_host_impl(nullptr, x_host, x32_dev, nullptr, v, n, n1, nullptr, &plan_seed, 0, L, two_sided,
                          max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev, workspace,
                          workspace_bytes, stream, st, stats);
 }
@@ -903,7 +958,7 @@ int rmx_naive_maxnull_host_plan_range(const double* x_host, int64_t v, int32_t n
                                       int32_t* argmax_dev, void* workspace,
                                       size_t workspace_bytes, void* stream, rmx_status* st,
                                       rmx_naive_stats* stats) {
-  return naive_host_impl(x_host, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, perm_base, L,
+  return naive_host_impl(x_host, nullptr, nullptr, nullptr, v, n, n1, nullptr, &plan_seed, perm_base, L,
                          two_sided, max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev,
                          workspace, workspace_bytes, stream, st, stats);
 }
@@ -917,9 +972,111 @@ int rmx_naive_maxnull_host_plan_range_f32(const float* x_host, int64_t v, int32_
                                           size_t workspace_bytes, void* stream, rmx_status* st,
                                           rmx_naive_stats* stats) {
   if (!x_host) return set_status(st, RMX_E_USAGE, "null buffer");
-  return naive_host_impl(nullptr, x_host, x32_dev, v, n, n1, nullptr, &plan_seed, perm_base, L,
+  return naive_host_impl(nullptr, x_host, x32_dev, nullptr, v, n, n1, nullptr, &plan_seed, perm_base, L,
                          two_sided, max_host, argmax_host, x_dev, orders_dev, max_dev, argmax_dev,
                          workspace, workspace_bytes, stream, st, stats);
+}
+
+int rmx_naive_maxnull_mat0(const char* path, int64_t v, int32_t n, int32_t n1,
+                           uint64_t plan_seed, int64_t perm_base, int64_t L, int32_t two_sided,
+                           double* max_host, int32_t* argmax_host, double* ring_host,
+                           size_t ring_bytes, int32_t threads, int64_t* bad_index, double* x_dev,
+                           int16_t* orders_dev, double* max_dev, int32_t* argmax_dev,
+                           void* workspace, size_t workspace_bytes, void* stream,
+                           rmx_status* st, rmx_naive_stats* stats) {
+  clear_status(st);
+  if (bad_index) *bad_index = -1;
+  if (!path || !ring_host) return set_status(st, RMX_E_USAGE, "null buffer");
+  FileSrc fs;
+  fs.path = path;
+  fs.ring = ring_host;
+  fs.threads = threads;
+  fs.bad_index = bad_index;
+  const int64_t row_bytes = (int64_t)n * 8;
+  fs.nslots = (int64_t)ring_bytes / row_bytes >= 3 * 1024 ? 3 : 2;
+  fs.slot_rows = std::min<int64_t>((int64_t)ring_bytes / fs.nslots / std::max<int64_t>(1, row_bytes), v);
+  if (n < 1 || fs.slot_rows < 1)
+    return set_status(st, RMX_E_USAGE, "staging ring of %zu bytes holds no %d-column row",
+                      ring_bytes, n);
+  return naive_host_impl(nullptr, nullptr, nullptr, &fs, v, n, n1, nullptr, &plan_seed, perm_base,
+                         L, two_sided, max_host, argmax_host, x_dev, orders_dev, max_dev,
+                         argmax_dev, workspace, workspace_bytes, stream, st, stats);
+}
+
+int rmx_tstat_dump_mat0(const double* x_dev, int64_t v, int32_t n, int32_t n1,
+                        const int16_t* orders_dev, int64_t L, const char* path, double* ring_host,
+                        size_t ring_bytes, int32_t threads, void* stream, rmx_status* st) {
+  clear_status(st);
+  if (int rc = check_dims(v, n, n1, L, st)) return rc;
+  if (!x_dev || !orders_dev || !path || !ring_host)
+    return set_status(st, RMX_E_USAGE, "null buffer");
+  // voxel slabs of `rows` voxels x all L permutations: one slab is a
+  // contiguous run of the (v, L) row-major payload.  Two host slots: the
+  // GPU computes + copies slab b while the host writes slab b - 1.
+  const int64_t rows = std::min<int64_t>(v, (int64_t)(ring_bytes / 2) / (L * 8));
+  if (rows < 1)
+    return set_status(st, RMX_E_USAGE,
+                      "staging ring of %zu bytes holds no two %lld-permutation voxel rows",
+                      ring_bytes, (long long)L);
+  if (int rc = rmx_mat0_create(path, v, L, 0, 0, st)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  struct Dev {
+    double *xt = nullptr, *tp = nullptr, *tv = nullptr;
+    NaiveCounters* c = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+    ~Dev() {
+      if (s) cudaStreamSynchronize(s);
+      for (void* p : {(void*)xt, (void*)tp, (void*)tv, (void*)c})
+        if (p) cudaFree(p);
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } d;
+  d.s = s;
+  RMX_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.xt), (size_t)rows * n * 8));
+  RMX_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.tp), (size_t)rows * L * 8));
+  RMX_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.tv), (size_t)rows * L * 8));
+  RMX_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.c), sizeof(NaiveCounters)));
+  for (auto& e : d.ev) RMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int64_t nslab = (v + rows - 1) / rows;
+  auto write_slab = [&](int64_t b) -> int {
+    const int64_t v0 = b * rows, v1 = std::min(v, v0 + rows);
+    RMX_CUDA(cudaEventSynchronize(d.ev[b & 1]));
+    return rmx_mat0_write_rows(path, L, v0, v1, ring_host + (size_t)(b & 1) * rows * L, threads,
+                               st);
+  };
+  for (int64_t b = 0; b < nslab; ++b) {
+    const int64_t v0 = b * rows, v1 = std::min(v, v0 + rows), nv = v1 - v0;
+    RMX_CUDA(cudaMemsetAsync(d.c, 0, sizeof(NaiveCounters), s));
+    RMX_CUDA(cudaMemsetAsync(&d.c->deg_key, 0xff, sizeof(unsigned long long), s));
+    // the slab's X^T (n x nv), its L x nv statistics (k_exact_rows: numpy's
+    // pairwise sums, the reference's bits), then (nv x L) for the file
+    RMX_CUDA(launch_transpose(x_dev + v0 * n, nv, n, d.xt, s));
+    const int nvb = (int)std::max<int64_t>(1, std::min<int64_t>((nv + 1023) / 1024, 1024));
+    RMX_CUDA(launch_exact_rows(d.xt, nv, n, n1, orders_dev, nullptr, L, 0, d.tp, nv, nullptr,
+                               nullptr, nvb, d.c, s));
+    RMX_CUDA(launch_transpose(d.tp, L, (int)nv, d.tv, s));
+    RMX_CUDA(cudaMemcpyAsync(ring_host + (size_t)(b & 1) * rows * L, d.tv, (size_t)nv * L * 8,
+                             cudaMemcpyDeviceToHost, s));
+    unsigned long long key = 0;
+    RMX_CUDA(cudaMemcpyAsync(&key, &d.c->deg_key, 8, cudaMemcpyDeviceToHost, s));
+    RMX_CUDA(cudaEventRecord(d.ev[b & 1], s));
+    if (b > 0)
+      if (int rc = write_slab(b - 1)) return rc;
+    RMX_CUDA(cudaEventSynchronize(d.ev[b & 1]));
+    if (key != ~0ull) {  // a degenerate entry: the reference raises before writing
+      const int rc = report_degenerate(x_dev + v0 * n, nv, n, n1, orders_dev, key, s, st);
+      st->voxel += v0;
+      set_status(st, rc,
+                 "voxel %lld: zero pooled variance with group mean difference %.6g "
+                 "(permutation %lld); statistic would be infinite",
+                 (long long)st->voxel, st->value, (long long)st->perm);
+      unlink(path);
+      return rc;
+    }
+  }
+  return write_slab(nslab - 1);
 }
 
 int rmx_plan_orders(uint64_t seed, int64_t lo, int64_t count, int32_t n, int16_t* out,

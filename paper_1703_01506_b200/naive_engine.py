@@ -279,3 +279,142 @@ def run_naive(x, plan, materialize: bool = False, two_sided: bool = False,
     }
     mat = StatMatrix(res.T, plan) if res.T is not None else None
     return MaxNull(res.maxima), mat, counters
+
+
+# ---------------------------------------------------------------------------
+# .mat0 file in, streamed: the reference CLI's naive run
+# (cli.py:70-116: read_matrix -> run_naive(materialize=dump_t) -> write_array)
+# without ever holding X or T on the host.
+
+_RING: dict = {}
+
+
+def _staging_ring(nbytes: int) -> np.ndarray:
+    """A cached page-locked float64 staging ring of at least `nbytes`."""
+    from .hostmem import pinned_empty
+
+    have = _RING.get("ring")
+    if have is None or have.nbytes < nbytes:
+        have = pinned_empty((-(-nbytes // 8),), np.float64)
+        _RING["ring"] = have
+    return have
+
+
+def _mat0_data_header(path):
+    """(v, n, n1, n2) of a .mat0 data file, with the reference read_matrix's
+    DataFormatError for a bare matrix or an invalid group split
+    (matio.py:83-91 + DataMatrix validation, model.py)."""
+    from .exceptions import DataFormatError
+    from .matfiles import mat0_info
+
+    v, n, n1, n2 = mat0_info(path)
+    if n1 == 0 and n2 == 0:
+        raise DataFormatError(
+            f"{path}: header carries no group split (n1=n2=0); "
+            f"this file stores a bare matrix, not subject data")
+    if min(n1, n2) < 2:
+        raise DataFormatError(
+            f"{path}: need at least two subjects per group for variance estimates, "
+            f"got n1={n1}, n2={n2}")
+    if n1 + n2 != n:
+        raise DataFormatError(
+            f"{path}: group sizes n1+n2={n1 + n2} do not match column count {n}")
+    return v, n, n1, n2
+
+
+def run_naive_mat0(path, plan, two_sided: bool = False, dump_t=None,
+                   threads: Optional[int] = None, staging_bytes: int = 192 << 20,
+                   lo: int = 0, hi: Optional[int] = None) -> NaiveResult:
+    """NaivePT over the data matrix stored in the .mat0 file `path`.
+
+    The float64 payload is streamed file -> page-locked ring -> device by
+    ``rmx_naive_maxnull_mat0`` (parallel positional reads of the next piece
+    while the copy engine moves this one and K0/K1 work on the chunks that
+    have landed), so the read overlaps the engine instead of preceding it.
+    With ``dump_t`` the (v, L) statistic matrix is then written to that path
+    as a bare .mat0 straight from the device (``rmx_tstat_dump_mat0``,
+    slab by slab), bit-identical to the reference's ``write_array(mat.values,
+    dump_t)`` and with no memory cap.  ``[lo, hi)``: a permutation range of
+    the plan (one rank's shard); ``maxima`` then holds those entries.
+    Results equal ``run_naive_ex(read_matrix(path), plan, ...)`` bit for bit.
+    """
+    import torch
+
+    from .exceptions import DataFormatError
+    from .hostmem import pinned_empty
+    from .matfiles import _bpath, nonfinite_error
+
+    plan = as_plan(plan)
+    v, n, n1, n2 = _mat0_data_header(path)
+    if plan.subjects != n:
+        raise UsageError("plan and data matrix disagree on subject count")
+    nthreads = resolve_threads(threads)
+    device = cuda_device()
+    hi = int(plan.count) if hi is None else int(hi)
+    L = hi - int(lo)
+    if not 0 <= lo < hi <= plan.count:
+        raise UsageError(f"permutation range [{lo}, {hi}) outside the plan of {plan.count}")
+    if n > 32767:
+        raise UsageError(f"subject count {n} exceeds the int16 label format")
+    xd = torch.empty((v, n), dtype=torch.float64, device=device)
+    od = torch.empty((L, n), dtype=torch.int16, device=device)
+    job = NaiveJob(xd, n1, od, two_sided)
+    mx = pinned_empty((L,), np.float64)
+    am = pinned_empty((L,), np.int32)
+    ring_bytes = max(int(staging_bytes), 3 * n * 8)
+    ring = _staging_ring(ring_bytes)
+    bad = ctypes.c_int64(-1)
+    seed = ctypes.c_uint64(int(plan.master_seed) & ((1 << 64) - 1))
+    rc = job.lib.rmx_naive_maxnull_mat0(
+        _bpath(path), v, n, n1, seed, int(lo), L, job.two_sided, mx.ctypes.data, am.ctypes.data,
+        ring.ctypes.data, ring_bytes, nthreads, ctypes.byref(bad), nat.ptr(xd), nat.ptr(od),
+        nat.ptr(job.max_out), nat.ptr(job.argmax_out), nat.ptr(job.workspace), job.ws_bytes,
+        job._s(), ctypes.byref(job._st), ctypes.byref(job.stats))
+    if rc == nat.RMX_E_FORMAT and bad.value >= 0:
+        raise nonfinite_error(path, bad.value, n)
+    if rc == nat.RMX_E_FORMAT:
+        raise DataFormatError(job._st.msg.decode(errors="replace"))
+    nat.raise_for(rc, job._st)
+    res = NaiveResult(mx.copy(), am.astype(np.int64), job.stats.as_dict(), None)
+    if dump_t is not None:
+        dump_statistic_matrix_device(job.x, n1, job.orders, dump_t, threads=nthreads,
+                                     stream=job.stream)
+    return res
+
+
+def dump_statistic_matrix_device(x, n1: int, orders, path, threads: Optional[int] = None,
+                                 staging_bytes: int = 256 << 20, stream=None) -> None:
+    """Write the (v, L) statistic matrix of device-resident X (v x n float64)
+    and labels (L x n int16) to `path` as a bare .mat0, streamed slab by slab
+    (rmx_tstat_dump_mat0)."""
+    import torch
+
+    from .matfiles import _bpath
+
+    lib = nat.load()
+    v, n = int(x.shape[0]), int(x.shape[1])
+    L = int(orders.shape[0])
+    ring_bytes = max(int(staging_bytes), 2 * L * 8)
+    ring = _staging_ring(ring_bytes)
+    stream = stream if stream is not None else torch.cuda.current_stream(x.device)
+    st = nat.Status()
+    rc = lib.rmx_tstat_dump_mat0(nat.ptr(x), v, n, int(n1), nat.ptr(orders), L, _bpath(path),
+                                 ring.ctypes.data, ring_bytes, resolve_threads(threads),
+                                 nat.stream_handle(stream), ctypes.byref(st))
+    nat.raise_for(rc, st)
+
+
+def dump_statistic_matrix(x, plan, path, threads: Optional[int] = None) -> None:
+    """The reference's ``--dump-T`` output for an in-memory DataMatrix:
+    ``write_array(run_naive(x, plan, materialize=True)[1].values, path)``,
+    streamed from the device instead of materialised on the host."""
+    from .labels import device_orders
+
+    x = as_data_matrix(x)
+    plan = as_plan(plan)
+    if plan.subjects != x.subjects:
+        raise UsageError("plan and data matrix disagree on subject count")
+    device = cuda_device()
+    xd = data_to_device(x, device)
+    od = device_orders(plan.master_seed, 0, plan.count, x.subjects, device)
+    dump_statistic_matrix_device(xd, x.n1, od, path, threads=threads)

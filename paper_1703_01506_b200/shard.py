@@ -38,13 +38,12 @@ def dist_info(group=None) -> tuple[int, int]:
     return 0, 1
 
 
-def gather_maxima(local_max, local_arg, L: int, per: int, group=None):
-    """All-gather padded per-rank (max, argmax) shards; returns the first L
-    entries in global permutation order (same tensors on every rank)."""
+def pack_maxima(local_max, local_arg, per: int):
+    """(per, 3) int32 rows [max as two int32 words | argmax]: one buffer, so
+    the exchange is one collective of 12 B per permutation.  Padding rows
+    carry NaN / -1."""
     import torch
-    import torch.distributed as dist
 
-    rank, world = dist_info(group)
     dev = local_max.device
     pm = torch.full((per,), float("nan"), dtype=torch.float64, device=dev)
     pa = torch.full((per,), -1, dtype=torch.int32, device=dev)
@@ -52,13 +51,83 @@ def gather_maxima(local_max, local_arg, L: int, per: int, group=None):
     if k:
         pm[:k] = local_max
         pa[:k] = local_arg
+    return torch.cat([pm.view(torch.int32).view(per, 2), pa.view(per, 1)], dim=1).contiguous()
+
+
+def unpack_maxima(packed):
+    """Inverse of pack_maxima over any number of rows: (max fp64, argmax int32)."""
+    import torch
+
+    m = packed[:, :2].contiguous().view(torch.float64).reshape(-1)
+    return m, packed[:, 2].contiguous()
+
+
+def gather_maxima(local_max, local_arg, L: int, per: int, group=None):
+    """All-gather padded per-rank (max, argmax) shards in ONE collective of
+    12 B per permutation (all_gather_into_tensor over NCCL; the list form on
+    backends without it, e.g. gloo); returns the first L entries in global
+    permutation order (same tensors on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist_info(group)
+    packed = pack_maxima(local_max, local_arg, per)
     if world == 1:
-        return pm[:L], pa[:L]
-    gm = [torch.empty_like(pm) for _ in range(world)]
-    ga = [torch.empty_like(pa) for _ in range(world)]
-    dist.all_gather(gm, pm, group=group)
-    dist.all_gather(ga, pa, group=group)
-    return torch.cat(gm)[:L], torch.cat(ga)[:L]
+        m, a = unpack_maxima(packed)
+        return m[:L], a[:L]
+    out = torch.empty((world * per, 3), dtype=torch.int32, device=packed.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, packed, group=group)
+    else:
+        dist.all_gather(list(out.chunk(world)), packed, group=group)
+    m, a = unpack_maxima(out)
+    return m[:L], a[:L]
+
+
+def row_bounds(v: int, rank: int, world: int) -> tuple[int, int, int]:
+    """(lo, hi, per): this rank's voxel-row slice of X for the shared upload."""
+    per = -(-v // world)
+    lo = min(v, rank * per)
+    return lo, min(v, lo + per), per
+
+
+def replicate_rows(x_host, device, group=None):
+    """Every rank gets all of X (v x n, the host array's dtype) on `device`
+    while uploading only its own 1/world slice of the rows over PCIe: each
+    rank copies rows [lo, hi) from its (page-locked) host array, then one
+    all-gather over NVLink assembles the replica.  At world 1 this is a plain
+    upload.  Bit-exact (a copy)."""
+    import torch
+    import torch.distributed as dist
+
+    from .hostmem import to_device
+
+    def upload(a):
+        a = np.ascontiguousarray(a)
+        if torch.device(device).type == "cpu":  # gloo tests
+            return torch.from_numpy(a.copy())
+        return to_device(a, device)
+
+    rank, world = dist_info(group)
+    v, n = x_host.shape
+    if world == 1:
+        return upload(x_host)
+    lo, hi, per = row_bounds(v, rank, world)
+    local = torch.zeros((per, n), dtype=_torch_dtype(x_host.dtype), device=device)
+    if hi > lo:
+        local[: hi - lo] = upload(x_host[lo:hi])
+    full = torch.empty((world * per, n), dtype=local.dtype, device=device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, local, group=group)
+    else:
+        dist.all_gather(list(full.chunk(world)), local, group=group)
+    return full[:v]
+
+
+def _torch_dtype(dt):
+    import torch
+
+    return {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[np.dtype(dt)]
 
 
 class ShardedNaive:
@@ -111,13 +180,29 @@ class ShardedNaive:
         return gather_maxima(m, a, self.L, self.per, self.group)
 
 
+def _shard_compute(x_dev, n1: int, plan, lo: int, hi: int, two_sided: bool):
+    """This rank's permutations [lo, hi) over the device replica of X: the
+    shard's labels generated on its GPU from the plan seed, then the engine
+    (K0 / K1 / K2 through rmx_naive_maxnull).  Returns device (max, argmax)."""
+    from .labels import device_orders
+    from .naive_engine import NaiveJob
+
+    od = device_orders(plan.master_seed, lo, hi, int(x_dev.shape[1]), x_dev.device)
+    job = NaiveJob(x_dev, n1, od, two_sided)
+    return job.run()
+
+
 def run_naive_distributed(x, plan, two_sided: bool = False, group=None):
     """Public multi-GPU entry: every rank passes the same host (x, plan) and
-    gets the full (MaxNull, argmax).  Each rank runs its permutation shard
-    through the host-input engine (rmx_naive_maxnull_host_plan_range*: X
-    uploaded chunk by chunk under K0/K1, the shard's labels generated on its
-    GPU), then one all-gather of (max, argmax).  Single-process when
-    torch.distributed is not initialised."""
+    gets the full (MaxNull, argmax).
+
+    world 1: the single-GPU host engine (rmx_naive_maxnull_host_plan*: X
+    uploaded chunk by chunk under K0/K1).  world N > 1: each rank uploads
+    only its 1/N row slice of X (the float32 source when the DataMatrix
+    keeps one) and one NCCL all-gather over NVLink assembles the replica
+    (replicate_rows: ~1/N of the PCIe time instead of every rank moving all
+    of X), then the rank runs its permutation shard and one all-gather of
+    12 B per permutation returns the maxima in global order."""
     import torch
 
     from .domain import MaxNull, as_data_matrix, as_plan
@@ -127,15 +212,28 @@ def run_naive_distributed(x, plan, two_sided: bool = False, group=None):
     plan = as_plan(plan)
     if plan.subjects != x.subjects:
         raise UsageError("plan and data matrix disagree on subject count")
-    dev = cuda_device()
+    dev = _device()
     rank, world = dist_info(group)
     L = int(plan.count)
     lo, hi, per = shard_bounds(L, rank, world)
-    if hi > lo:
-        _, _, job = _run_from_host(x, plan, two_sided, dev, lo, hi)
+    if world == 1:
+        _, _, job = _run_from_host(x, plan, two_sided, cuda_device(), lo, hi)
         lm, la = job.max_out, job.argmax_out
     else:
-        lm = torch.empty(0, dtype=torch.float64, device=dev)
-        la = torch.empty(0, dtype=torch.int32, device=dev)
+        src = x.float32_values if x.float32_values is not None else x.values
+        xd = replicate_rows(src, dev, group)
+        if xd.dtype != torch.float64:
+            xd = xd.to(torch.float64)  # exact upcast of the float32 source
+        if hi > lo:
+            lm, la = _shard_compute(xd, x.n1, plan, lo, hi, two_sided)
+        else:
+            lm = torch.empty(0, dtype=torch.float64, device=dev)
+            la = torch.empty(0, dtype=torch.int32, device=dev)
     m, a = gather_maxima(lm, la, L, per, group)
     return MaxNull(m.cpu().numpy()), a.cpu().numpy().astype(np.int64)
+
+
+def _device():
+    from .naive_engine import cuda_device
+
+    return cuda_device()

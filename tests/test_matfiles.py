@@ -58,3 +58,38 @@ def test_large_parallel_read_and_missing_file(tmp_path):
         mf.read_matrix(tmp_path / "b.mat0")
     with pytest.raises(FileNotFoundError):
         mf.read_array(tmp_path / "missing.mat0")
+
+
+def test_ranged_rows_read_and_write(tmp_path):
+    """rmx_mat0_read_rows / rmx_mat0_create / rmx_mat0_write_rows (the piece
+    reader of the streamed engine and the --dump-T writer): ranges of a file
+    equal slices of read_array; a file written in ragged row ranges equals
+    write_array's bytes."""
+    import ctypes
+
+    from paper_1703_01506_b200 import _native as nat
+
+    lib = nat.load()
+    a = np.random.default_rng(4).standard_normal((1031, 13))
+    p = tmp_path / "a.mat0"
+    mf.write_array(a, p, 0, 0)
+    st, bad = nat.Status(), ctypes.c_int64(-1)
+    for r0, r1 in ((0, 1031), (5, 6), (100, 977), (1000, 1031)):
+        out = np.empty((r1 - r0, 13))
+        rc = lib.rmx_mat0_read_rows(bytes(p), 13, r0, r1, out.ctypes.data, 3, ctypes.byref(bad),
+                                    ctypes.byref(st))
+        assert rc == 0 and np.array_equal(out, a[r0:r1])
+    q = tmp_path / "b.mat0"
+    assert lib.rmx_mat0_create(bytes(q), 1031, 13, 0, 0, ctypes.byref(st)) == 0
+    for r0, r1 in ((700, 1031), (0, 3), (3, 700)):
+        blk = np.ascontiguousarray(a[r0:r1])
+        assert lib.rmx_mat0_write_rows(bytes(q), 13, r0, r1, blk.ctypes.data, 4,
+                                       ctypes.byref(st)) == 0
+    assert q.read_bytes() == p.read_bytes()
+    b = a.copy()
+    b[600, 4] = np.inf
+    mf.write_array(b, p, 0, 0)
+    out = np.empty((500, 13))
+    rc = lib.rmx_mat0_read_rows(bytes(p), 13, 500, 1000, out.ctypes.data, 2, ctypes.byref(bad),
+                                ctypes.byref(st))
+    assert rc == nat.RMX_E_FORMAT and bad.value == 600 * 13 + 4
