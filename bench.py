@@ -55,6 +55,11 @@ def parse():
     return ap.parse_args()
 
 
+def progress(msg: str) -> None:
+    """Phase marks on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -456,9 +461,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    progress(f"rank {rank}: inputs ready, warm-up")
     for _ in range(args.warmup):
         sh.step()
     barrier()
+    progress("timed steps")
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -553,6 +560,7 @@ def main():
     # ---------------- e2e through the public API from host buffers -----------
     e2e = None
     if not args.no_e2e:
+        progress("e2e")
         from paper_1703_01506_b200.naive_engine import run_naive_ex
 
         # the configs' X is float32 (BASELINE.json); DataMatrix keeps that
@@ -596,6 +604,7 @@ def main():
     # ---------------- CPU baseline (rank 0, N=1) ------------------------------
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        progress("cpu baseline + parity")
         x_host_np = x_dev.cpu().numpy()
         threads = os.cpu_count() or 1
         orders_host = generate_orders(cfg.plan_seed, 0, min(L, max(threads * 64, 256)), n)
@@ -620,6 +629,7 @@ def main():
                       "maxima_differing": int(np.sum(gm != mx)),
                       "against": "oracle/rmx_oracle.c (pinned bit-exact to the reference) on "
                                  "the benchmarked input's first permutations"}
+        progress("reference numpy engine, 2 permutations")
         try:  # and the unmodified reference's own numpy engine on the first two
             rn = reference_numpy_naive(cfg, x_host_np, perms=2)
             if "maxima" in rn:
@@ -634,6 +644,7 @@ def main():
     # ---------------- RapidPT, config 5 (N=1; training is not sharded) -------
     rapid = None
     if rank == 0 and world == 1 and not args.no_rapid:
+        progress("rapid (config 5)")
         try:
             rapid = rapid_block(device)
         except Exception as exc:

@@ -555,11 +555,17 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const double* trow = t + (int64_t)i * v;
     // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
     RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, s));
-    RCUDA(launch_dgemm_rm(k, kDeferCap, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap, 0, s));
-    RCUDA(launch_dgemm_rm(k, r, kDeferCap, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
+    // pending deferred terms <= updates since the last flush (tglob % kDeferCap;
+    // a halted update adds none), and the unused columns of X / Y are zero:
+    // only the first ntc columns take part (none right after a flush)
+    const int ntc = std::min(kDeferCap, ((int)(tglob % kDeferCap) + 15) / 16 * 16);
+    if (ntc > 0) {
+      RCUDA(launch_dgemm_rm(k, ntc, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap, 0, s));
+      RCUDA(launch_dgemm_rm(k, r, ntc, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
+    }
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
-    RCUDA(launch_gram(ug.p, lu, r, nullptr, k, vals.p, G.p, 1, s));
+    RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
     if (use_cg) {
       RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,

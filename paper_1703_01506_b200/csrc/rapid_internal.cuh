@@ -152,5 +152,8 @@ cudaError_t launch_track_apply(double* U, int64_t v, int r, double* pred, double
 cudaError_t launch_dgemm_rm(int64_t m, int n, int kk, const double* A, int64_t lda,
                             const double* B, int64_t ldb, double* C, int64_t ldc, int accum,
                             cudaStream_t s);
+// G (n x n, both halves) = A^T A, A (kk x n) row-major (dgemm.cu)
+cudaError_t launch_dsyrk_rm(int kk, int n, const double* A, int64_t lda, double* C, int64_t ldc,
+                            cudaStream_t s);
 cudaError_t launch_mean_var(const double* a, int64_t n, double* out, cudaStream_t s);
 }  // namespace rmx

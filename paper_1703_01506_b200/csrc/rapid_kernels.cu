@@ -21,6 +21,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "philox.cuh"
 #include "rapid_internal.cuh"
@@ -1473,6 +1474,16 @@ cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int
                                   cudaStream_t s) {
   const size_t smem =
       ((size_t)kPW * kPS + kPW + (size_t)chol_panel_rows(r) * kPS + (size_t)r) * sizeof(float);
+  // RMX_CHOL_NT=512: one 512-thread CTA per SM (working set of the trailing
+  // updates ~148 systems -> L2-resident) instead of three 256-thread CTAs
+  const char* ntv = getenv("RMX_CHOL_NT");
+  if (ntv && atoi(ntv) == 512) {
+    auto kern = k_chol_solve<512, float>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr);
+    return cudaGetLastError();
+  }
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -17,7 +17,10 @@ import weakref
 import numpy as np
 
 _REGISTERED: dict = {}
-_LOCK = threading.Lock()
+# re-entrant: dropping the last reference to a registered array (e.g. an
+# _INFLIGHT entry pruned under the lock) runs its weakref callback, which
+# takes the lock again on the same thread
+_LOCK = threading.RLock()
 _MIN_REGISTER_BYTES = 64 << 20
 
 
@@ -110,8 +113,12 @@ _INFLIGHT: list = []
 
 
 def _prune_inflight() -> None:
+    done, keep = [], []
     with _LOCK:
-        _INFLIGHT[:] = [(a, ev) for a, ev in _INFLIGHT if not ev.query()]
+        for item in _INFLIGHT:
+            (done if item[1].query() else keep).append(item)
+        _INFLIGHT[:] = keep
+    del done  # the sources' last references (and their unregistration) go outside the lock
 
 
 def to_device(arr: np.ndarray, device, stream=None):

@@ -143,3 +143,33 @@ def test_accepts_reference_objects_duck_typed():
 
     assert as_data_matrix(RefDM()).voxels == 4
     assert as_plan(RefPlan()).count == 7
+
+
+def test_inflight_prune_releases_sources_without_self_deadlock():
+    """hostmem._prune_inflight drops the last reference to a copied source
+    array; that array's weakref callback (cudaHostUnregister bookkeeping)
+    takes hostmem's lock again.  It must not deadlock (it did with a plain
+    Lock: the C5 RapidPT test hung in data_to_device)."""
+    import threading
+    import weakref
+
+    from paper_1703_01506_b200 import hostmem
+
+    class Done:
+        def query(self):
+            return True
+
+    fired = []
+
+    def cb(_ref):
+        with hostmem._LOCK:
+            fired.append(1)
+
+    a = np.ones(8)
+    ref = weakref.ref(a, cb)
+    hostmem._INFLIGHT.append((a, Done()))
+    del a
+    th = threading.Thread(target=hostmem._prune_inflight, daemon=True)
+    th.start()
+    th.join(timeout=10)
+    assert not th.is_alive() and fired == [1] and ref() is None
