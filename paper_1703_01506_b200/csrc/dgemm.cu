@@ -8,9 +8,7 @@
 //                              G = [U_Omega | t]^T [U_Omega | t]  (SYRK)
 //
 // 64 x 64 output tile per 256-thread CTA (4 x 4 per thread), K in steps of
-// 16 through a double-buffered shared-memory stage (the next step's global
-// loads are in registers while the current one is multiplied).  The A tile
-// is stored transposed so both operands are read as 2-wide vectors.
+// 16 through a 4-stage cp.async shared-memory ring.
 //
 // The per-update products have few output tiles (SYRK: 28 lower tiles of
 // the 401 x 401 Gram; Tk: 29 tiles) but a long K, so the K range is split
@@ -28,8 +26,11 @@ namespace rmx {
 namespace {
 
 constexpr int kBM = 64, kBN = 64, kBK = 16, kT = 256;
-constexpr int kStage = 2 * 2 * kBK * (kBM + 2);  // doubles: As + Bs, double-buffered
-constexpr int kPart = kBM * (kBN + 1);          // doubles: the CTA's partial tile
+constexpr int kStages = 4;                                   // cp.async ring depth
+constexpr int kTileD = kBK * (kBM + 2);                      // doubles per operand tile
+constexpr int kStage = kStages * 2 * kTileD;                 // doubles: the A + B ring
+constexpr int kPart = kBM * (kBN + 1);                       // doubles: the CTA's partial tile
+static_assert(kPart <= kStage, "the partial tile reuses the ring");
 
 __device__ __forceinline__ double ld_cluster_f64(const double* local, uint32_t rank) {
   uint32_t ra;
@@ -39,17 +40,24 @@ __device__ __forceinline__ double ld_cluster_f64(const double* local, uint32_t r
   return v;
 }
 
+__device__ __forceinline__ void cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 // SYRK = false: C (m x n) (+)= A (m x kk) B (kk x n).
 // SYRK = true:  C (n x n, symmetric, both halves written) = A^T A with A
 //               (kk x n) row-major; blockIdx.x enumerates the lower tiles.
+// Operand tiles stream through a kStages-deep cp.async ring (8-byte copies:
+// any leading dimension), A^T tiles stored [k][m] so both operands are read
+// as 2-wide vectors.
 template <bool SYRK>
-__global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
-                                                 const double* __restrict__ A, int64_t lda,
-                                                 const double* __restrict__ B, int64_t ldb,
-                                                 double* __restrict__ C, int64_t ldc, int accum) {
+__global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
+                                                    const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ B, int64_t ldb,
+                                                    double* __restrict__ C, int64_t ldc, int accum) {
   extern __shared__ __align__(16) double dsm[];
-  double (*As)[kBK][kBM + 2] = reinterpret_cast<double (*)[kBK][kBM + 2]>(dsm);
-  double (*Bs)[kBK][kBN + 2] = reinterpret_cast<double (*)[kBK][kBN + 2]>(dsm + 2 * kBK * (kBM + 2));
+  auto As = [&](int st) { return dsm + (size_t)st * 2 * kTileD; };
+  auto Bs = [&](int st) { return dsm + (size_t)st * 2 * kTileD + kTileD; };
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   int64_t m0;
@@ -70,68 +78,64 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
   const int S = gridDim.z, z = blockIdx.z;
   const int kper = ((kk + S - 1) / S + kBK - 1) / kBK * kBK;
   const int kb = min(kk, z * kper), ke = min(kk, kb + kper);
-  // loader mapping.  GEMM A tile (kBM x kBK): thread -> row tid / 4, cols
-  // 4 (tid % 4) ..; SYRK A^T tile = rows of A: thread -> row tid / 16, cols
-  // 4 (tid % 16) .. (coalesced).  B tile (kBK x kBN): row tid / 16, cols 4 (tid % 16) ..
-  const int ar = tid >> 2, ac = (tid & 3) * 4;
-  const int br = tid >> 4, bc = (tid & 15) * 4;
-  double ra[4], rb[4];
-  auto load = [&](int k0) {
-    if (SYRK) {
-      const int krow = k0 + br;
+  const int nk = (ke - kb + kBK - 1) / kBK;
+  // stage t: K rows [kb + 16 t, +16).  Element e = tid + 256 q (q < 4) of a
+  // 16 x 64 tile.  SYRK: (row e / 64, col e % 64) of A for both operands
+  // (coalesced along rows); GEMM: A tile (row e / 16, k e % 16) -> As[k][row],
+  // B tile (k e / 64, col e % 64).
+  auto issue = [&](int t) {
+    const int st = t % kStages, k0 = kb + t * kBK;
+    double* as = As(st);
+    double* bs = Bs(st);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int ci = (int)m0 + bc + q, cj = n0 + bc + q;
-        const bool rowok = krow < ke;
-        ra[q] = (rowok && ci < n) ? A[(int64_t)krow * lda + ci] : 0.0;
-        rb[q] = (rowok && cj < n) ? A[(int64_t)krow * lda + cj] : 0.0;
-      }
-    } else {
-      const int64_t row = m0 + ar;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = k0 + ac + q;
-        ra[q] = (row < m && c < ke) ? A[row * lda + c] : 0.0;
-      }
-      const int krow = k0 + br;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = n0 + bc + q;
-        rb[q] = (krow < ke && c < n) ? B[(int64_t)krow * ldb + c] : 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + kT * q;
+      if (SYRK) {
+        const int kr = e >> 6, cc = e & 63, krow = k0 + kr;
+        const int ci = (int)m0 + cc, cj = n0 + cc;
+        double* da = as + kr * (kBM + 2) + cc;
+        double* db = bs + kr * (kBN + 2) + cc;
+        if (krow < ke && ci < n) cp8(da, A + (int64_t)krow * lda + ci); else *da = 0.0;
+        if (krow < ke && cj < n) cp8(db, A + (int64_t)krow * lda + cj); else *db = 0.0;
+      } else {
+        const int ar = e >> 4, ak = e & 15;
+        const int64_t row = m0 + ar;
+        const int c = k0 + ak;
+        double* da = as + ak * (kBM + 2) + ar;
+        if (row < m && c < ke) cp8(da, A + row * lda + c); else *da = 0.0;
+        const int br = e >> 6, bc = e & 63, krow = k0 + br, cn = n0 + bc;
+        double* db = bs + br * (kBN + 2) + bc;
+        if (krow < ke && cn < n) cp8(db, B + (int64_t)krow * ldb + cn); else *db = 0.0;
       }
     }
-  };
-  auto store = [&](int buf) {
-    if (SYRK) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) As[buf][br][bc + q] = ra[q];
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) As[buf][ac + q][ar] = ra[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) Bs[buf][br][bc + q] = rb[q];
   };
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  const int nk = (ke - kb + kBK - 1) / kBK;
-  if (nk > 0) {
-    load(kb);
-    store(0);
+#pragma unroll
+  for (int t = 0; t < kStages - 1; ++t) {
+    if (t < nk) issue(t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __syncthreads();
   for (int t = 0; t < nk; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < nk) load(kb + (t + 1) * kBK);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
+    __syncthreads();  // stage t landed for every thread; stage t - 1's slot is free
+    if (t + kStages - 1 < nk) issue(t + kStages - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* as = As(t % kStages);
+    const double* bs = Bs(t % kStages);
+    // thread (tx, ty): rows 2 ty + {0, 1, 32, 33}, columns 2 tx + {0, 1, 32,
+    // 33}: a warp's B reads are 256 contiguous bytes (2 wavefronts, no bank
+    // conflicts) and its A reads two broadcast addresses, so the fp64 FMA
+    // pipe, not shared memory, bounds the loop
 #pragma unroll
     for (int k = 0; k < kBK; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&As[buf][k][ty * 4]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&As[buf][k][ty * 4 + 2]);
-      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][k][tx * 4]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][k][tx * 4 + 2]);
+      const double2 a01 = *reinterpret_cast<const double2*>(as + k * (kBM + 2) + ty * 2);
+      const double2 a23 = *reinterpret_cast<const double2*>(as + k * (kBM + 2) + ty * 2 + 32);
+      const double2 b01 = *reinterpret_cast<const double2*>(bs + k * (kBN + 2) + tx * 2);
+      const double2 b23 = *reinterpret_cast<const double2*>(bs + k * (kBN + 2) + tx * 2 + 32);
       const double a[4] = {a01.x, a01.y, a23.x, a23.y};
       const double b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
@@ -139,9 +143,9 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
-    if (t + 1 < nk) store(buf ^ 1);
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();  // the ring is free (the partial tile reuses it)
   auto put = [&](int64_t row, int c, double val) {
     if (SYRK) {
       if (row < n && c < n && c <= row) {
@@ -153,19 +157,21 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
       *p = accum ? *p + val : val;
     }
   };
+  auto rof = [&](int i) { return ty * 2 + (i & 1) + (i >> 1) * 32; };  // tile row of acc[i]
+  auto cof = [&](int j) { return tx * 2 + (j & 1) + (j >> 1) * 32; };  // tile column of acc[.][j]
   if (S == 1) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) put(m0 + ty * 4 + i, n0 + tx * 4 + j, acc[i][j]);
+      for (int j = 0; j < 4; ++j) put(m0 + rof(i), n0 + cof(j), acc[i][j]);
     return;
   }
   // cluster split-K: partial tile -> smem, then CTA z reduces its row band
-  double* P = dsm + kStage;
+  double* P = dsm;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) P[(ty * 4 + i) * (kBN + 1) + tx * 4 + j] = acc[i][j];
+    for (int j = 0; j < 4; ++j) P[rof(i) * (kBN + 1) + cof(j)] = acc[i][j];
   cluster_sync();
   const int band = kBM / S;
   for (int e = tid; e < band * kBN; e += kT) {
@@ -178,10 +184,10 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
 }
 
 // K split for grids that cannot fill the GPU: up to 8 CTAs per tile while
-// the grid stays within ~3 CTAs per SM and every CTA keeps >= 16 K rows
+// the grid stays within ~2 waves of 2 CTAs per SM and every CTA keeps >= 32 K rows
 int pick_split(int64_t tiles, int kk) {
   int S = 1;
-  while (S < 8 && tiles * S * 2 <= 3 * 148 && kk / (2 * S) >= kBK) S *= 2;
+  while (S < 8 && tiles * S * 2 <= 4 * 148 && kk / (2 * S) >= 2 * kBK) S *= 2;
   return S;
 }
 
@@ -189,12 +195,12 @@ template <bool SYRK>
 cudaError_t launch(dim3 grid, int S, int64_t m, int n, int kk, const double* A, int64_t lda,
                    const double* B, int64_t ldb, double* C, int64_t ldc, int accum,
                    cudaStream_t s) {
-  const size_t smem = (size_t)(kStage + (S > 1 ? kPart : 0)) * sizeof(double);
+  const size_t smem = (size_t)kStage * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_dgemm_rm<SYRK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((kStage + kPart) * sizeof(double)));
+                                         (int)(kStage * sizeof(double)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }

@@ -313,8 +313,16 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
     const double* vb = vals + b0 * k;
     double* wb = w_out + b0 * r;
     RCUDA(launch_gram_tc(planes.p, v, r, ib, k, vb, Graw, f32 ? 1 : 0, cnt, sms, s));
-    if (f32) RCUDA(launch_chol_solve_f32(static_cast<float*>(Graw), r, cnt, wb, flags.p + b0, s));
-    else RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
+    if (f32 && chol_cluster_supported(r)) {
+      // factor on chip (4-CTA clusters), then the first solve as a resolve
+      // from w = 0 (its convergence flag is overwritten by the refinements)
+      RCUDA(launch_chol_cluster_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, flags.p + b0, s));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s));
+    } else if (f32) {
+      RCUDA(launch_chol_solve_f32(static_cast<float*>(Graw), r, cnt, wb, flags.p + b0, s));
+    } else {
+      RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
+    }
     // two refinement steps with the fp64 residual (contraction ~ cond * 1e-5 each)
     for (int it = 0; it < 2; ++it) {
       RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
@@ -500,7 +508,9 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(sums.alloc(8, s));
   RCUDA(flag.alloc(1, s));
   RCUDA(idxbuf.alloc(k, s));
-  const int64_t lu = r + 1;  // ug rows: [U_Omega row | t_Omega] (the Gram's operand)
+  // ug rows: [U_Omega row | t_Omega] (the Gram's operand), padded to an even
+  // length (16-byte aligned rows)
+  const int64_t lu = (r + 2) / 2 * 2;
   RCUDA(ug.alloc((size_t)k * lu, s));
   RCUDA(ub2.alloc((size_t)v * kDeferCap, s));  // T = U_base X (flush)
   RCUDA(M.alloc((size_t)r * r, s));

@@ -22,6 +22,11 @@ cudaError_t launch_chol_resolve(double* G, int r, int64_t B, const double* rhs, 
                                 int32_t* nconv, cudaStream_t s);
 // the same on an fp32 G (the tensor-core Gram's precision; the fp64
 // refinement restores the solution's accuracy)
+// K3b on chip: one system per 4-CTA cluster (r <= 416); writes L into G's
+// lower triangle, rhs_out (B x r) = G row r, w_out = 0, flag = bad pivot
+bool chol_cluster_supported(int r);
+cudaError_t launch_chol_cluster_f32(float* G, int r, int64_t B, double* rhs_out, double* w_out,
+                                    int32_t* flag, cudaStream_t s);
 cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int32_t* flag,
                                   cudaStream_t s);
 cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,

@@ -170,29 +170,62 @@ constexpr int kPW = 32;
 constexpr int kPS = kPW + 1;  // padded smem row stride (doubles)
 
 // Factor the 32x32 SPD block D (smem, lower part used; rows/cols >= w are
-// the identity) in place into L_D; rinv[c] = 1 / L_cc.  One warp.
-template <typename T>
-__device__ __forceinline__ void chol_block32(T* D, T* rinv, T tiny, int* bad) {
-  const int lane = threadIdx.x & 31;
-  T a[kPW];
-#pragma unroll
-  for (int l = 0; l < kPW; ++l) a[l] = D[lane * kPS + l];
-#pragma unroll
-  for (int c = 0; c < kPW; ++c) {
-    T piv = __shfl_sync(0xffffffffu, a[c], c);
+// the identity) in place into L_D; rinv[c] = 1 / L_cc.  One warp, lane =
+// row, the row in registers.  The column loop is unrolled by template
+// recursion (a plain 32 x 31 unrolled loop nest is left rolled by the
+// compiler, which then indexes a[] dynamically -- through local memory).
+template <typename T, int C>
+struct Chol32Step {
+  __device__ __forceinline__ static void run(T (&a)[kPW], T* rinv, T tiny, int* bad, int lane) {
+    T piv = __shfl_sync(0xffffffffu, a[C], C);
     if (!(piv > tiny)) {
       if (lane == 0) *bad = 1;
       piv = fmax(fabs(piv), 1e-300);
     }
     const T d = sqrt(piv);
     const T inv = 1.0 / d;
-    if (lane == c) a[c] = d;
-    if (lane > c) a[c] *= inv;
-    if (lane == 0) rinv[c] = inv;
+    if (lane == C) a[C] = d;
+    if (lane > C) a[C] *= inv;
+    if (lane == 0) rinv[C] = inv;
 #pragma unroll
-    for (int l = c + 1; l < kPW; ++l) {
-      const T llc = __shfl_sync(0xffffffffu, a[c], l);
-      if (lane >= l) a[l] = fma(-a[c], llc, a[l]);
+    for (int l = C + 1; l < kPW; ++l) {
+      const T llc = __shfl_sync(0xffffffffu, a[C], l);
+      if (lane >= l) a[l] = fma(-a[C], llc, a[l]);
+    }
+    Chol32Step<T, C + 1>::run(a, rinv, tiny, bad, lane);
+  }
+};
+template <typename T>
+struct Chol32Step<T, kPW> {
+  __device__ __forceinline__ static void run(T (&)[kPW], T*, T, int*, int) {}
+};
+
+template <typename T>
+__device__ __forceinline__ void chol_block32(T* D, T* rinv, T tiny, int* bad) {
+  const int lane = threadIdx.x & 31;
+  T a[kPW];
+#pragma unroll
+  for (int l = 0; l < kPW; ++l) a[l] = D[lane * kPS + l];
+  if constexpr (sizeof(T) == 4) {
+    Chol32Step<T, 0>::run(a, rinv, tiny, bad, lane);
+  } else {  // fp64: the loop form spills less under the 2-CTA register cap
+#pragma unroll
+    for (int c = 0; c < kPW; ++c) {
+      T piv = __shfl_sync(0xffffffffu, a[c], c);
+      if (!(piv > tiny)) {
+        if (lane == 0) *bad = 1;
+        piv = fmax(fabs(piv), 1e-300);
+      }
+      const T d = sqrt(piv);
+      const T inv = 1.0 / d;
+      if (lane == c) a[c] = d;
+      if (lane > c) a[c] *= inv;
+      if (lane == 0) rinv[c] = inv;
+#pragma unroll
+      for (int l = c + 1; l < kPW; ++l) {
+        const T llc = __shfl_sync(0xffffffffu, a[c], l);
+        if (lane >= l) a[l] = fma(-a[c], llc, a[l]);
+      }
     }
   }
 #pragma unroll
@@ -1491,8 +1524,369 @@ cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K3b (cluster)
+// Batched Cholesky factor of G~ (fp32, the tcgen05 Gram) with the whole
+// matrix ON CHIP: one system per cluster of kClC CTAs, its rows dealt out by
+// quads (rows 4q..4q+3 -> CTA q % kClC) and stored packed (quad q keeps
+// columns 0..4q+3) in that CTA's shared memory, the dimension padded to a
+// multiple of 32 with identity rows.  Right-looking, panel width 32:
+//   1. every CTA gathers the 32 x 32 diagonal block through DSMEM and
+//      factors it redundantly (one warp, chol_block32) -- no broadcast;
+//   2. the owners solve their panel rows P_i = G[i, panel] L_D^-T;
+//   3. cluster barrier; every CTA copies all panel rows (16-byte DSMEM loads)
+//      into a local panel buffer;
+//   4. trailing update of the CTA's own rows, 4 x 4 register tiles from the
+//      panel buffer (G[i, j] -= P_i . P_j), in place in its storage;
+//   5. cluster barrier.
+// The factor is then written to G's lower triangle (for the refinement
+// resolves), G's row r (the right-hand side A^T t) to rhs_out as fp64 and
+// w_out zeroed; flag = non-positive pivot (relative to the largest diagonal).
+// Replaces the global-memory right-looking factor, whose trailing matrix
+// (1,667 systems x 643 KB) streamed through HBM at every panel.
+constexpr int kClC = 4;       // CTAs per system
+constexpr int kClT = 256;     // threads per CTA
+constexpr int kClPS = 36;     // panel-buffer row stride (floats; 16-byte rows)
+constexpr int kClMaxN = 416;  // padded dimension supported (r <= 416)
+
+__host__ __device__ inline int cl_quad_off(int t, int c) {  // floats before own quad t
+  return 16 * (kClC * t * (t - 1) / 2 + t * (c + 1));
+}
+
+__device__ __forceinline__ uint32_t cl_map(const void* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ float cl_ld(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 cl_ld4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClT, 1)
+    k_chol_cluster(float* __restrict__ G, int r, double* __restrict__ rhs_out,
+                   double* __restrict__ w_out, int32_t* __restrict__ flag) {
+  extern __shared__ __align__(16) float clsm[];
+  const uint32_t c = cluster_ctarank();
+  const int64_t b = blockIdx.x / kClC;
+  const int N = (r + 31) / 32 * 32;
+  const int nq = N / 4;
+  const int nt = (nq - (int)c + kClC - 1) / kClC;  // own quads: q = t kClC + c
+  const int stor = cl_quad_off(nt, (int)c);
+  // red and St sit at the same offsets in every CTA of the cluster (peers
+  // address them through DSMEM); the rest is local and follows St
+  float* red = clsm;                                    // the CTA's diagonal maximum
+  float* St = clsm + 4;                                 // packed own rows
+  float* D = St + (stor + 3) / 4 * 4;                   // 32 x kPS diagonal block
+  float* rinv = D + kPW * kPS;                          // 32
+  float* Pf = rinv + 32;                                // panel rows (N x kClPS)
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  const int ld = r + 1;
+  float* Gb = G + b * (int64_t)ld * ld;
+  // local address of global row i (owned by this CTA), column 0
+  auto row_ptr = [&](float* base, int i, int owner) -> int {  // float offset in owner's St
+    const int q = i >> 2, t = q / kClC;
+    return cl_quad_off(t, owner) + (i & 3) * (4 * q + 4);
+  };
+  if (tid == 0) red[0] = 0.f;
+  __syncthreads();
+  // load own rows (lower part, identity beyond r), the local diagonal maximum
+  float dmx = 0.f;
+  for (int t = 0; t < nt; ++t) {
+    const int q = t * kClC + (int)c, len = 4 * q + 4;
+    float* base = St + cl_quad_off(t, (int)c);
+    for (int e = tid; e < 4 * len; e += kClT) {
+      const int ii = e / len, j = e - ii * len, i = 4 * q + ii;
+      float val = 0.f;
+      if (i < r && j <= i) val = Gb[(int64_t)i * ld + j];
+      else if (i >= r && j == i) val = 1.f;
+      base[ii * len + j] = val;
+      if (j == i && i < r) dmx = fmaxf(dmx, val);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) dmx = fmaxf(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+  if ((tid & 31) == 0) atomicMax(reinterpret_cast<int*>(&red[0]), __float_as_int(dmx));  // dmx >= 0
+  if (tid == 0) bad = 0;
+  // the right-hand side and the zeroed solution (CTA 0)
+  if (c == 0) {
+    for (int i = tid; i < r; i += kClT) {
+      rhs_out[b * r + i] = (double)Gb[(int64_t)r * ld + i];
+      w_out[b * r + i] = 0.0;
+    }
+  }
+  cluster_sync();
+  float gmax = 0.f;
+  for (uint32_t p = 0; p < kClC; ++p) gmax = fmaxf(gmax, cl_ld(cl_map(&red[0], p)));
+  const float tiny = 1e-24f * gmax;
+  for (int jb = 0; jb < N; jb += kPW) {
+    // 1. diagonal block from its owners
+    for (int e = tid; e < kPW * kPW; e += kClT) {
+      const int ii = e / kPW, jj = e % kPW, i = jb + ii;
+      const int owner = (i >> 2) % kClC;
+      float val = 0.f;
+      if (jj <= ii) val = cl_ld(cl_map(St + row_ptr(St, i, owner) + jb + jj, (uint32_t)owner));
+      D[ii * kPS + jj] = val;
+    }
+    __syncthreads();
+    if (tid < 32) chol_block32(D, rinv, tiny, &bad);
+    __syncthreads();
+    // 2. own panel rows (i >= jb + 32): own row k = 4 (t - tp) + ii of the
+    // quads from tp on, one per thread (the whole warp solves at once)
+    {
+      int tp = 0;
+      while (tp < nt && 4 * (tp * kClC + (int)c) < jb + kPW) ++tp;
+      for (int k = tid; k < 4 * (nt - tp); k += kClT) {
+        const int t = tp + (k >> 2), ii = k & 3;
+        const int q = t * kClC + (int)c, len = 4 * q + 4;
+        {
+          float* gi = St + cl_quad_off(t, (int)c) + ii * len + jb;
+          float pr[kPW];
+#pragma unroll
+          for (int cc = 0; cc < kPW; cc += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(gi + cc);
+            pr[cc] = v.x, pr[cc + 1] = v.y, pr[cc + 2] = v.z, pr[cc + 3] = v.w;
+          }
+#pragma unroll
+          for (int cc = 0; cc < kPW; ++cc) {
+            float sacc = pr[cc];
+#pragma unroll
+            for (int l = 0; l < cc; ++l) sacc = fmaf(-pr[l], D[cc * kPS + l], sacc);
+            pr[cc] = sacc * rinv[cc];
+          }
+#pragma unroll
+          for (int cc = 0; cc < kPW; cc += 4)
+            *reinterpret_cast<float4*>(gi + cc) = make_float4(pr[cc], pr[cc + 1], pr[cc + 2], pr[cc + 3]);
+        }
+      }
+    }
+    cluster_sync();  // every CTA has gathered the diagonal block and solved its panel rows
+    // own rows of the diagonal block <- L_D (nobody reads them again)
+    for (int t = 0; t < nt; ++t) {
+      const int q = t * kClC + (int)c;
+      if (4 * q < jb || 4 * q >= jb + kPW) continue;
+      float* base = St + cl_quad_off(t, (int)c);
+      const int len = 4 * q + 4;
+      for (int e = tid; e < 4 * kPW; e += kClT) {
+        const int ii = e / kPW, cc = e % kPW, i = 4 * q + ii;
+        if (cc <= i - jb) base[ii * len + jb + cc] = D[(i - jb) * kPS + cc];
+      }
+    }
+    // 3. all panel rows -> Pf (row i - jb - 32)
+    const int prow0 = jb + kPW, nrows = N - prow0;
+    for (int e = tid; e < nrows * (kPW / 4); e += kClT) {
+      const int pr = e / (kPW / 4), c4 = (e % (kPW / 4)) * 4, i = prow0 + pr;
+      const int owner = (i >> 2) % kClC;
+      const float4 v = cl_ld4(cl_map(St + row_ptr(St, i, owner) + jb + c4, (uint32_t)owner));
+      *reinterpret_cast<float4*>(Pf + (size_t)pr * kClPS + c4) = v;
+    }
+    __syncthreads();
+    // 4. trailing update of own rows: (own quad Q) x (column quad J), J <= Q
+    const int J0 = prow0 / 4;
+    int t0 = 0;
+    while (t0 < nt && t0 * kClC + (int)c < J0) ++t0;
+    const int nown = nt - t0, ncq = nq - J0;
+    for (int e = tid; e < nown * ncq; e += kClT) {
+      const int tt = t0 + e / ncq, J = J0 + e % ncq;
+      const int Q = tt * kClC + (int)c;
+      if (J > Q) continue;
+      const float* pi = Pf + (size_t)(4 * Q - prow0) * kClPS;
+      const float* pj = Pf + (size_t)(4 * J - prow0) * kClPS;
+      float acc[4][4] = {};
+#pragma unroll 2
+      for (int kk = 0; kk < kPW; kk += 4) {
+        float4 a[4], bq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = *reinterpret_cast<const float4*>(pi + u * kClPS + kk);
+          bq[u] = *reinterpret_cast<const float4*>(pj + u * kClPS + kk);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            acc[u][v] = fmaf(a[u].x, bq[v].x, acc[u][v]);
+            acc[u][v] = fmaf(a[u].y, bq[v].y, acc[u][v]);
+            acc[u][v] = fmaf(a[u].z, bq[v].z, acc[u][v]);
+            acc[u][v] = fmaf(a[u].w, bq[v].w, acc[u][v]);
+          }
+      }
+      float* base = St + cl_quad_off(tt, (int)c);
+      const int len = 4 * Q + 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float4* g4 = reinterpret_cast<float4*>(base + u * len + 4 * J);
+        float4 gv = *g4;
+        gv.x -= acc[u][0];
+        gv.y -= acc[u][1];
+        gv.z -= acc[u][2];
+        gv.w -= acc[u][3];
+        *g4 = gv;
+      }
+    }
+    cluster_sync();
+  }
+  // the factor back to G's lower triangle (the resolves read it there)
+  for (int t = 0; t < nt; ++t) {
+    const int q = t * kClC + (int)c, len = 4 * q + 4;
+    const float* base = St + cl_quad_off(t, (int)c);
+    for (int e = tid; e < 4 * len; e += kClT) {
+      const int ii = e / len, j = e - ii * len, i = 4 * q + ii;
+      if (i < r && j <= i) Gb[(int64_t)i * ld + j] = base[ii * len + j];
+    }
+  }
+  if (c == 0 && tid == 0 && flag) flag[b] = bad;
+}
+
+size_t chol_cluster_smem(int r) {
+  const int N = (r + 31) / 32 * 32, nq = N / 4;
+  int stor = 0;
+  for (int c = 0; c < kClC; ++c) {
+    const int nt = (nq - c + kClC - 1) / kClC;
+    stor = std::max(stor, cl_quad_off(nt, c));
+  }
+  return (4 + (size_t)(stor + 3) / 4 * 4 + kPW * kPS + 32 + (size_t)N * kClPS) * sizeof(float);
+}
+
+bool chol_cluster_supported(int r) {
+  return r >= 1 && r <= kClMaxN && chol_cluster_smem(r) <= 232448 && !getenv("RMX_CHOL_CTA");
+}
+
+cudaError_t launch_chol_cluster_f32(float* G, int r, int64_t B, double* rhs_out, double* w_out,
+                                    int32_t* flag, cudaStream_t s) {
+  const size_t smem = chol_cluster_smem(r);
+  cudaError_t e = cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_chol_cluster<<<(unsigned)(B * kClC), kClT, smem, s>>>(G, r, rhs_out, w_out, flag);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3b'
+// Refinement resolve with a factor already in G (lower triangle of the
+// row-major (r+1) x (r+1) fp32 G~): L L^T d = rhs_b, w_b += d, nconv_b = 1
+// when |d|^2 > 1e-14 |w|^2.  ONE WARP PER SYSTEM (all of a batch's systems
+// resident at once, the solves' serial chains overlapped across warps):
+//   forward, block jb: lane l owns row i = jb + l; its dot product with the
+//     solved y[0:jb] streams the row (16-byte loads, y broadcast from smem),
+//     then the 32 x 32 diagonal block is solved by shuffles with the row's
+//     32 diagonal-block entries in registers;
+//   backward, block jb (descending): lane l owns column j = jb + l; the rows
+//     below the block are read as coalesced 128-byte row segments, then the
+//     block's transpose is solved by shuffles.
+// fp32 arithmetic as the CTA version (the correction needs ~fp32 accuracy).
+constexpr int kTrsvWarps = 4;
+
+__global__ void __launch_bounds__(32 * kTrsvWarps) k_trsv_warp(const float* __restrict__ G, int r,
+                                                                int64_t B, const double* __restrict__ rhs,
+                                                                double* __restrict__ w_inout,
+                                                                int32_t* __restrict__ nconv) {
+  extern __shared__ __align__(16) float ty[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * kTrsvWarps + wid;
+  if (b >= B) return;
+  const int ld = r + 1;
+  const int rp = (r + 31) / 32 * 32;
+  float* y = ty + (size_t)wid * rp;
+  const float* Gb = G + b * (int64_t)ld * ld;
+  const double* rb = rhs + b * r;
+  for (int jb = 0; jb < r; jb += 32) {  // forward: L y = rhs
+    const int i = jb + lane;
+    const bool live = i < r;
+    const float* li = Gb + (int64_t)(live ? i : jb) * ld;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (live) {
+      // row i is not 16-byte aligned in general (ld = r + 1): scalar head
+      // up to alignment, then 16-byte loads
+      int c = 0;
+      const int head = (int)((4 - ((reinterpret_cast<uintptr_t>(li) >> 2) & 3)) & 3);
+      for (; c < head && c < jb; ++c) s0 = fmaf(li[c], y[c], s0);
+      for (; c + 4 <= jb; c += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(li + c);
+        s0 = fmaf(l4.x, y[c], s0);
+        s1 = fmaf(l4.y, y[c + 1], s1);
+        s2 = fmaf(l4.z, y[c + 2], s2);
+        s3 = fmaf(l4.w, y[c + 3], s3);
+      }
+      for (; c < jb; ++c) s0 = fmaf(li[c], y[c], s0);
+    }
+    float yb = live ? (float)rb[i] - ((s0 + s1) + (s2 + s3)) : 0.f;
+    float lr[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) lr[c] = (live && jb + c <= i) ? li[jb + c] : (c == lane ? 1.f : 0.f);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (lane == c) yb /= lr[c];
+      const float yc = __shfl_sync(0xffffffffu, yb, c);
+      if (lane > c) yb = fmaf(-lr[c], yc, yb);
+    }
+    if (live) y[i] = yb;
+    __syncwarp();
+  }
+  for (int jb = (r - 1) / 32 * 32; jb >= 0; jb -= 32) {  // backward: L^T d = y
+    const int j = jb + lane;
+    const bool live = j < r;
+    float s0 = 0.f, s1 = 0.f;
+    int i = jb + 32;
+    for (; i + 1 < r; i += 2) {
+      if (live) {
+        s0 = fmaf(Gb[(int64_t)i * ld + j], y[i], s0);
+        s1 = fmaf(Gb[(int64_t)(i + 1) * ld + j], y[i + 1], s1);
+      }
+    }
+    if (i < r && live) s0 = fmaf(Gb[(int64_t)i * ld + j], y[i], s0);
+    float db = live ? y[j] - (s0 + s1) : 0.f;
+    float lc[32];  // column j of the diagonal block: L[jb + c][j]
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      lc[c] = (live && jb + c < r && jb + c >= j) ? Gb[(int64_t)(jb + c) * ld + j] : (c == lane ? 1.f : 0.f);
+#pragma unroll
+    for (int c = 31; c >= 0; --c) {
+      if (lane == c) db /= lc[c];
+      const float dc = __shfl_sync(0xffffffffu, db, c);
+      if (lane < c) db = fmaf(-lc[c], dc, db);
+    }
+    __syncwarp();
+    if (live) y[j] = db;
+    __syncwarp();
+  }
+  double dd = 0.0, ww = 0.0;
+  for (int i = lane; i < r; i += 32) {
+    const double d = (double)y[i];
+    const double wn = w_inout[b * r + i] + d;
+    w_inout[b * r + i] = wn;
+    dd += d * d;
+    ww += wn * wn;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    ww += __shfl_xor_sync(0xffffffffu, ww, o);
+  }
+  if (lane == 0 && nconv) nconv[b] = (dd > 1e-14 * ww) ? 1 : 0;
+}
+
 cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,
                                     double* w_inout, int32_t* nconv, cudaStream_t s) {
+  if (!getenv("RMX_TRSV_CTA")) {  // one warp per system (RMX_TRSV_CTA=1: the CTA version)
+    const int rp = (r + 31) / 32 * 32;
+    const size_t smem = (size_t)kTrsvWarps * rp * sizeof(float);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_trsv_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_trsv_warp<<<(unsigned)((B + kTrsvWarps - 1) / kTrsvWarps), 32 * kTrsvWarps, smem, s>>>(
+        G, r, B, rhs, w_inout, nconv);
+    return cudaGetLastError();
+  }
   const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(float);
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

