@@ -1,14 +1,18 @@
 // dgemm.cu -- the fp64 products of the M-deferred GROUSE (reference
-// lrmc.py:160-193 / 208-268, restructured in rapid_abi.cu): register-tiled
-// CUDA-core DGEMM / SYRK, row-major.  B200 runs fp64 FMA on the CUDA cores
-// at the same rate as fp64 DMMA, so this is the plain dense kernel:
+// lrmc.py:160-193 / 208-268, restructured in rapid_abi.cu), row-major, on the
+// fp64 tensor cores (DMMA, mma.sync.m8n8k4.f64):
 //
 //   flush (every 64 updates):  T = U X (v x r . r x nt), U += T Y^T
 //   per update:                Tk = U_Omega X, U_Omega += Tk Y^T
 //                              G = [U_Omega | t]^T [U_Omega | t]  (SYRK)
 //
-// 64 x 64 output tile per 256-thread CTA (4 x 4 per thread), K in steps of
-// 16 through a 4-stage cp.async shared-memory ring.
+// 64 x 64 output tile per 128-thread CTA, each warp a 32 x 32 quadrant as
+// 4 x 4 DMMA tiles (32 fp64 accumulators per thread).  K in steps of 16
+// through a 4-stage cp.async shared-memory ring; both operands are stored
+// k-major ([k][m], [k][n]) so a DMMA fragment (lane l: row / column l / 4,
+// k = l % 4) is one 8-byte shared load.  A DMMA does 256 multiply-adds per
+// warp instruction -- the CUDA-core DFMA version of this kernel was bound
+// by shared-memory traffic and issue (mio_throttle), not by the fp64 pipe.
 //
 // The per-update products have few output tiles (SYRK: 28 lower tiles of
 // the 401 x 401 Gram; Tk: 29 tiles) but a long K, so the K range is split
@@ -25,9 +29,10 @@
 namespace rmx {
 namespace {
 
-constexpr int kBM = 64, kBN = 64, kBK = 16, kT = 256;
+constexpr int kBM = 64, kBN = 64, kBK = 16, kT = 128;
+constexpr int kLd = 72;                                      // smem row stride (doubles)
 constexpr int kStages = 4;                                   // cp.async ring depth
-constexpr int kTileD = kBK * (kBM + 2);                      // doubles per operand tile
+constexpr int kTileD = kBK * kLd;                            // doubles per operand tile
 constexpr int kStage = kStages * 2 * kTileD;                 // doubles: the A + B ring
 constexpr int kPart = kBM * (kBN + 1);                       // doubles: the CTA's partial tile
 static_assert(kPart <= kStage, "the partial tile reuses the ring");
@@ -36,30 +41,37 @@ __device__ __forceinline__ double ld_cluster_f64(const double* local, uint32_t r
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
   double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  // no memory clobber: ordering comes from the cluster barriers, so the S
+  // loads of one output element are all in flight before the first add
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
   return v;
 }
 
 __device__ __forceinline__ void cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
 // SYRK = false: C (m x n) (+)= A (m x kk) B (kk x n).
 // SYRK = true:  C (n x n, symmetric, both halves written) = A^T A with A
 //               (kk x n) row-major; blockIdx.x enumerates the lower tiles.
-// Operand tiles stream through a kStages-deep cp.async ring (8-byte copies:
-// any leading dimension), A^T tiles stored [k][m] so both operands are read
-// as 2-wide vectors.
 template <bool SYRK>
-__global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
-                                                    const double* __restrict__ A, int64_t lda,
-                                                    const double* __restrict__ B, int64_t ldb,
-                                                    double* __restrict__ C, int64_t ldc, int accum) {
+__global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
+                                                 const double* __restrict__ A, int64_t lda,
+                                                 const double* __restrict__ B, int64_t ldb,
+                                                 double* __restrict__ C, int64_t ldc, int accum) {
   extern __shared__ __align__(16) double dsm[];
   auto As = [&](int st) { return dsm + (size_t)st * 2 * kTileD; };
   auto Bs = [&](int st) { return dsm + (size_t)st * 2 * kTileD + kTileD; };
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t m0;
   int n0;
   if (SYRK) {  // lower-triangle tile index -> (ti, tj), tj <= ti
@@ -79,41 +91,80 @@ __global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
   const int kper = ((kk + S - 1) / S + kBK - 1) / kBK * kBK;
   const int kb = min(kk, z * kper), ke = min(kk, kb + kper);
   const int nk = (ke - kb + kBK - 1) / kBK;
-  // stage t: K rows [kb + 16 t, +16).  Element e = tid + 256 q (q < 4) of a
-  // 16 x 64 tile.  SYRK: (row e / 64, col e % 64) of A for both operands
-  // (coalesced along rows); GEMM: A tile (row e / 16, k e % 16) -> As[k][row],
-  // B tile (k e / 64, col e % 64).
+  // 16-byte copies when the rows (and so every even column) are 16-byte aligned
+  const bool a16 = SYRK && ((lda & 1) == 0) && lda >= n + (n & 1) &&
+                   ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool b16 = !SYRK && ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+  // stage t: K rows [kb + 16 t, +16)
   auto issue = [&](int t) {
     const int st = t % kStages, k0 = kb + t * kBK;
     double* as = As(st);
     double* bs = Bs(st);
+    if (SYRK) {  // both operands are rows of A: [k][m0 + c] and [k][n0 + c]
+      if (a16) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + kT * q;
-      if (SYRK) {
-        const int kr = e >> 6, cc = e & 63, krow = k0 + kr;
-        const int ci = (int)m0 + cc, cj = n0 + cc;
-        double* da = as + kr * (kBM + 2) + cc;
-        double* db = bs + kr * (kBN + 2) + cc;
-        if (krow < ke && ci < n) cp8(da, A + (int64_t)krow * lda + ci); else *da = 0.0;
-        if (krow < ke && cj < n) cp8(db, A + (int64_t)krow * lda + cj); else *db = 0.0;
+        for (int q = 0; q < 4; ++q) {  // 16 x 32 pairs per operand
+          const int e = tid + kT * q, kr = e >> 5, cc = (e & 31) * 2, krow = k0 + kr;
+          const int ci = (int)m0 + cc, cj = n0 + cc;
+          double* da = as + kr * kLd + cc;
+          double* db = bs + kr * kLd + cc;
+          // a pair starting at n - 1 reads the (allocated, even-length row)
+          // padding column: only output entries of columns >= n see it, and
+          // they are never written
+          if (krow < ke && ci < n) cp16(da, A + (int64_t)krow * lda + ci); else da[0] = da[1] = 0.0;
+          if (krow < ke && cj < n) cp16(db, A + (int64_t)krow * lda + cj); else db[0] = db[1] = 0.0;
+        }
       } else {
-        const int ar = e >> 4, ak = e & 15;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = tid + kT * q, kr = e >> 6, cc = e & 63, krow = k0 + kr;
+          const int ci = (int)m0 + cc, cj = n0 + cc;
+          double* da = as + kr * kLd + cc;
+          double* db = bs + kr * kLd + cc;
+          if (krow < ke && ci < n) cp8(da, A + (int64_t)krow * lda + ci); else *da = 0.0;
+          if (krow < ke && cj < n) cp8(db, A + (int64_t)krow * lda + cj); else *db = 0.0;
+        }
+      }
+    } else {
+      // A tile (64 rows x 16 k) -> [k][row]: 8-byte scatter
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = tid + kT * q, ar = e >> 4, ak = e & 15;
         const int64_t row = m0 + ar;
         const int c = k0 + ak;
-        double* da = as + ak * (kBM + 2) + ar;
+        double* da = as + ak * kLd + ar;
         if (row < m && c < ke) cp8(da, A + row * lda + c); else *da = 0.0;
-        const int br = e >> 6, bc = e & 63, krow = k0 + br, cn = n0 + bc;
-        double* db = bs + br * (kBN + 2) + bc;
-        if (krow < ke && cn < n) cp8(db, B + (int64_t)krow * ldb + cn); else *db = 0.0;
+      }
+      if (b16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = tid + kT * q, br = e >> 5, bc = (e & 31) * 2, krow = k0 + br, cn = n0 + bc;
+          double* db = bs + br * kLd + bc;
+          if (krow < ke && cn + 1 < n) {
+            cp16(db, B + (int64_t)krow * ldb + cn);
+          } else {
+            db[0] = (krow < ke && cn < n) ? B[(int64_t)krow * ldb + cn] : 0.0;
+            db[1] = 0.0;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = tid + kT * q, br = e >> 6, bc = e & 63, krow = k0 + br, cn = n0 + bc;
+          double* db = bs + br * kLd + bc;
+          if (krow < ke && cn < n) cp8(db, B + (int64_t)krow * ldb + cn); else *db = 0.0;
+        }
       }
     }
   };
-  double acc[4][4];
+  // warp quadrant (32 x 32) and this lane's fragment coordinates
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
   for (int t = 0; t < kStages - 1; ++t) {
     if (t < nk) issue(t);
@@ -126,22 +177,17 @@ __global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* as = As(t % kStages);
     const double* bs = Bs(t % kStages);
-    // thread (tx, ty): rows 2 ty + {0, 1, 32, 33}, columns 2 tx + {0, 1, 32,
-    // 33}: a warp's B reads are 256 contiguous bytes (2 wavefronts, no bank
-    // conflicts) and its A reads two broadcast addresses, so the fp64 FMA
-    // pipe, not shared memory, bounds the loop
 #pragma unroll
-    for (int k = 0; k < kBK; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(as + k * (kBM + 2) + ty * 2);
-      const double2 a23 = *reinterpret_cast<const double2*>(as + k * (kBM + 2) + ty * 2 + 32);
-      const double2 b01 = *reinterpret_cast<const double2*>(bs + k * (kBN + 2) + tx * 2);
-      const double2 b23 = *reinterpret_cast<const double2*>(bs + k * (kBN + 2) + tx * 2 + 32);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+    for (int k4 = 0; k4 < kBK; k4 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[(k4 + fk) * kLd + wr + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[(k4 + fk) * kLd + wc + 8 * j + fr];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -157,13 +203,16 @@ __global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
       *p = accum ? *p + val : val;
     }
   };
-  auto rof = [&](int i) { return ty * 2 + (i & 1) + (i >> 1) * 32; };  // tile row of acc[i]
-  auto cof = [&](int j) { return tx * 2 + (j & 1) + (j >> 1) * 32; };  // tile column of acc[.][j]
+  // accumulator (i, j, h): tile row wr + 8 i + lane / 4, column wc + 8 j + 2 (lane % 4) + h
+  const int cr = lane >> 2, cc2 = (lane & 3) * 2;
   if (S == 1) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) put(m0 + rof(i), n0 + cof(j), acc[i][j]);
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          put(m0 + wr + 8 * i + cr, n0 + wc + 8 * j + cc2 + h, acc[i][j][h]);
     return;
   }
   // cluster split-K: partial tile -> smem, then CTA z reduces its row band
@@ -171,20 +220,29 @@ __global__ void __launch_bounds__(kT, 2) k_dgemm_rm(int64_t m, int n, int kk,
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) P[rof(i) * (kBN + 1) + cof(j)] = acc[i][j];
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        P[(wr + 8 * i + cr) * (kBN + 1) + wc + 8 * j + cc2 + h] = acc[i][j][h];
   cluster_sync();
   const int band = kBM / S;
   for (int e = tid; e < band * kBN; e += kT) {
     const int i = z * band + e / kBN, j = e % kBN;
+    double part[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      part[s] = s < S ? ld_cluster_f64(P + i * (kBN + 1) + j, (uint32_t)s) : 0.0;
     double sum = 0.0;
-    for (int s = 0; s < S; ++s) sum += ld_cluster_f64(P + i * (kBN + 1) + j, (uint32_t)s);
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < S) sum += part[s];  // fixed order: deterministic
     put(m0 + i, n0 + j, sum);
   }
   cluster_sync();  // no CTA leaves while a peer still reads its partial
 }
 
 // K split for grids that cannot fill the GPU: up to 8 CTAs per tile while
-// the grid stays within ~2 waves of 2 CTAs per SM and every CTA keeps >= 32 K rows
+// the grid stays within ~4 CTAs per SM and every CTA keeps >= 32 K rows
 int pick_split(int64_t tiles, int kk) {
   int S = 1;
   while (S < 8 && tiles * S * 2 <= 4 * 148 && kk / (2 * S) >= 2 * kBK) S *= 2;
@@ -199,8 +257,7 @@ cudaError_t launch(dim3 grid, int S, int64_t m, int n, int kk, const double* A, 
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_dgemm_rm<SYRK>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kStage * sizeof(double)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }

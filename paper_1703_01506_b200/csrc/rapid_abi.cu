@@ -527,6 +527,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(mw.alloc(r, s));
   RCUDA(dots.alloc(kDeferCap, s));
   RCUDA(gst.alloc(1, s));
+  DevBuf<double> pscr;  // the gated Cholesky fallback's panel
+  RCUDA(pscr.alloc(chol_panel_scratch_doubles(r), s));
   // each column's CG solution from the previous pass warm-starts its next
   // solve (same stopping rule |G w - b| <= 1e-13 |b|, far fewer iterations
   // once the basis settles)
@@ -541,6 +543,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
   const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
+  // tests: every CG solve is treated as not converged (the Cholesky fallback runs)
+  const bool force_fallback = getenv("RMX_GROUSE_FORCE_FALLBACK") != nullptr;
   // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE),
   // M = I + X Y^T with one column of X / row of Y^T per deferred update
   // (k_defer_apply): the flush U <- U M + terms is U += (U X) Y^T in place
@@ -560,11 +564,37 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // on the same G when CG does not converge), residual, |p|^2 from H, and
   // k_grouse_post_m's decisions; the update itself only touches M, the
   // terms and H.  No host round trip: the host syncs every 64 updates.
+  // RMX_GROUSE_PROFILE=1 (diagnostics): CUDA events between the phases of
+  // updates [128, 192) -> per-phase in-stream time (kernel + any idle gap
+  // before it) printed to stderr at the end
+  struct PhaseProf {
+    enum { kPh = 9, kLo = 128, kN = 64 };
+    bool on = getenv("RMX_GROUSE_PROFILE") != nullptr;
+    std::vector<cudaEvent_t> ev;
+    int64_t cur = -1;
+    int slot = 0;
+    void mark(cudaStream_t st) {
+      if (cur < 0) return;
+      cudaEventRecord(ev[(size_t)(cur - kLo) * kPh + slot++], st);
+    }
+    ~PhaseProf() {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+  } prof;
+  if (prof.on) {
+    prof.ev.resize((size_t)PhaseProf::kPh * PhaseProf::kN);
+    for (auto& e : prof.ev) RCUDA(cudaEventCreate(&e));
+  }
   auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
+    prof.cur = (prof.on && tglob >= PhaseProf::kLo && tglob < PhaseProf::kLo + PhaseProf::kN)
+                   ? tglob : -1;
+    prof.slot = 0;
+    prof.mark(s);
     const double* trow = t + (int64_t)i * v;
     // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
     RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, s));
+    prof.mark(s);
     // pending deferred terms <= updates since the last flush (tglob % kDeferCap;
     // a halted update adds none), and the unused columns of X / Y are zero:
     // only the first ntc columns take part (none right after a flush)
@@ -573,19 +603,27 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       RCUDA(launch_dgemm_rm(k, ntc, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap, 0, s));
       RCUDA(launch_dgemm_rm(k, r, ntc, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
     }
+    prof.mark(s);
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
+    prof.mark(s);
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
     RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));
     RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+    prof.mark(s);
     if (use_cg) {
       RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,
                             warm ? wprev.p + (int64_t)i * r : nullptr, s));
-      RCUDA(launch_chol_if_flag(G.p, r, w.p, flag.p, sums.p + 4, s));
+      prof.mark(s);
+      if (force_fallback) RCUDA(cudaMemsetAsync(flag.p, 0x01, 1, s));  // tests: flag = 1
+      RCUDA(launch_chol_if_flag(G.p, r, w.p, flag.p, sums.p + 4, pscr.p, s));
     } else {
       RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
+      prof.mark(s);
     }
+    prof.mark(s);
     RCUDA(launch_resid_defer_vec(ug.p, lu, r, k, vals.p, w.p, resid.p, sums.p, H.p, M.p, cmat.p,
                                  gst.p, hw.p, mw.p, dots.p, s));
+    prof.mark(s);
     RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
                                didx.p, dval.p, cmat.p, wn.p,
                                final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));
@@ -593,6 +631,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                           s));
     RCUDA(launch_defer_apply(M.p, Xf.p, Yf.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r,
                              s));
+    prof.mark(s);
     (void)p;
     return RMX_OK;
   };
@@ -691,6 +730,24 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       break;
     }
     if (stop) break;
+  }
+  if (prof.on && tglob >= PhaseProf::kLo + PhaseProf::kN) {
+    RCUDA(cudaStreamSynchronize(s));
+    static const char* names[PhaseProf::kPh - 1] = {"gather", "deferred_dgemms", "sparse_terms",
+                                                     "syrk+memset", "cg", "chol_gate",
+                                                     "resid", "post+h_update+defer"};
+    double tot[PhaseProf::kPh - 1] = {};
+    for (int u = 0; u < PhaseProf::kN; ++u)
+      for (int q = 0; q + 1 < PhaseProf::kPh; ++q) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, prof.ev[(size_t)u * PhaseProf::kPh + q],
+                             prof.ev[(size_t)u * PhaseProf::kPh + q + 1]);
+        tot[q] += ms;
+      }
+    fprintf(stderr, "{\"grouse_phase_us_per_update\": {");
+    for (int q = 0; q + 1 < PhaseProf::kPh; ++q)
+      fprintf(stderr, "%s\"%s\": %.2f", q ? ", " : "", names[q], 1e3 * tot[q] / PhaseProf::kN);
+    fprintf(stderr, "}}\n");
   }
   {
     GrouseState hs;

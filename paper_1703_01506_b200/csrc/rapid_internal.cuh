@@ -104,8 +104,11 @@ cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const doubl
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
 void cg_stats(unsigned long long out[2]);  // k_cg_solve (solves, iterations) so far
+// the gated Cholesky fallback after a non-converged cluster CG; pscratch:
+// chol_panel_scratch_doubles(r) doubles of global scratch for the panel
+size_t chol_panel_scratch_doubles(int r);
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                                cudaStream_t s);
+                                double* pscratch, cudaStream_t s);
 // K4 on tcgen05: operand preparation and the max decode
 cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
                             cudaStream_t s);

@@ -183,7 +183,7 @@ struct Chol32Step {
       piv = fmax(fabs(piv), 1e-300);
     }
     const T d = sqrt(piv);
-    const T inv = 1.0 / d;
+    const T inv = T(1) / d;  // fp32: a float division (the serial chain's longest step)
     if (lane == C) a[C] = d;
     if (lane > C) a[C] *= inv;
     if (lane == 0) rinv[C] = inv;
@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
                                                    double* __restrict__ w_out,
                                                    int32_t* flag, double* __restrict__ resid2,
                                                    const int32_t* gate = nullptr,
-                                                   const double* __restrict__ rhs_ext = nullptr) {
+                                                   const double* __restrict__ rhs_ext = nullptr,
+                                                   T* __restrict__ pscratch = nullptr) {
+  // pscratch (the gated GROUSE fallback): the panel in global memory, so the
+  // launch needs only a few KB of shared memory (its common case is to exit
+  // at the gate; a 100+ KB request would reconfigure the SMs every update)
   // gate: run only when *gate != 0 (Cholesky fallback after a cluster-CG
   // solve that did not converge, decided on the device)
   // rhs_ext (refinement): G already holds the factor L; solve L L^T d =
@@ -251,8 +255,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
   T* sm = reinterpret_cast<T*>(chol_smem);
   T* D = sm;                     // kPW x kPS: block / L_D (lower)
   T* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
-  T* P = rinv + kPW;             // chol_panel_rows(r) x kPS panel (factor only)
-  T* y = rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS;  // r: rhs / solution
+  T* after = rinv + kPW;
+  T* P = pscratch ? pscratch : after;  // chol_panel_rows(r) x kPS panel (factor only)
+  T* y = pscratch ? after : (rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS);  // r: rhs / solution
   __shared__ int bad;
   __shared__ T dmax;
   const int64_t b = blockIdx.x;
@@ -1514,13 +1519,13 @@ cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int
     auto kern = k_chol_solve<512, float>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr);
+    kern<<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr);
     return cudaGetLastError();
   }
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr);
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -1557,17 +1562,19 @@ __device__ __forceinline__ uint32_t cl_map(const void* local, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
   return ra;
 }
+// DSMEM loads without a memory clobber (ordering comes from the cluster
+// barriers), so a thread's independent remote loads are all in flight
+// before the first result is used
 __device__ __forceinline__ float cl_ld(uint32_t addr) {
   float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float4 cl_ld4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
+               : "r"(addr));
   return v;
 }
 
@@ -1628,13 +1635,21 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClT, 1)
   for (uint32_t p = 0; p < kClC; ++p) gmax = fmaxf(gmax, cl_ld(cl_map(&red[0], p)));
   const float tiny = 1e-24f * gmax;
   for (int jb = 0; jb < N; jb += kPW) {
-    // 1. diagonal block from its owners
-    for (int e = tid; e < kPW * kPW; e += kClT) {
-      const int ii = e / kPW, jj = e % kPW, i = jb + ii;
-      const int owner = (i >> 2) % kClC;
-      float val = 0.f;
-      if (jj <= ii) val = cl_ld(cl_map(St + row_ptr(St, i, owner) + jb + jj, (uint32_t)owner));
-      D[ii * kPS + jj] = val;
+    // 1. diagonal block from its owners (all of a thread's loads issued first)
+    {
+      float val[kPW * kPW / kClT];
+#pragma unroll
+      for (int u = 0; u < kPW * kPW / kClT; ++u) {
+        const int e = tid + u * kClT, ii = e / kPW, jj = e % kPW, i = jb + ii;
+        const int owner = (i >> 2) % kClC;
+        val[u] = 0.f;
+        if (jj <= ii) val[u] = cl_ld(cl_map(St + row_ptr(St, i, owner) + jb + jj, (uint32_t)owner));
+      }
+#pragma unroll
+      for (int u = 0; u < kPW * kPW / kClT; ++u) {
+        const int e = tid + u * kClT;
+        D[(e / kPW) * kPS + e % kPW] = val[u];
+      }
     }
     __syncthreads();
     if (tid < 32) chol_block32(D, rinv, tiny, &bad);
@@ -1682,11 +1697,23 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClT, 1)
     }
     // 3. all panel rows -> Pf (row i - jb - 32)
     const int prow0 = jb + kPW, nrows = N - prow0;
-    for (int e = tid; e < nrows * (kPW / 4); e += kClT) {
-      const int pr = e / (kPW / 4), c4 = (e % (kPW / 4)) * 4, i = prow0 + pr;
-      const int owner = (i >> 2) % kClC;
-      const float4 v = cl_ld4(cl_map(St + row_ptr(St, i, owner) + jb + c4, (uint32_t)owner));
-      *reinterpret_cast<float4*>(Pf + (size_t)pr * kClPS + c4) = v;
+    for (int e0 = 0; e0 < nrows * (kPW / 4); e0 += 4 * kClT) {  // 4 loads in flight per thread
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + tid + u * kClT;
+        if (e < nrows * (kPW / 4)) {
+          const int pr = e / (kPW / 4), c4 = (e % (kPW / 4)) * 4, i = prow0 + pr;
+          const int owner = (i >> 2) % kClC;
+          v[u] = cl_ld4(cl_map(St + row_ptr(St, i, owner) + jb + c4, (uint32_t)owner));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + tid + u * kClT;
+        if (e < nrows * (kPW / 4))
+          *reinterpret_cast<float4*>(Pf + (size_t)(e / (kPW / 4)) * kClPS + (e % (kPW / 4)) * 4) = v[u];
+      }
     }
     __syncthreads();
     // 4. trailing update of own rows: (own quad Q) x (column quad J), J <= Q
@@ -1757,7 +1784,8 @@ size_t chol_cluster_smem(int r) {
 }
 
 bool chol_cluster_supported(int r) {
-  return r >= 1 && r <= kClMaxN && chol_cluster_smem(r) <= 232448 && !getenv("RMX_CHOL_CTA");
+  const char* e = getenv("RMX_CHOL_CLUSTER");
+  return e && atoi(e) == 1 && r >= 1 && r <= kClMaxN && chol_cluster_smem(r) <= 232448;
 }
 
 cudaError_t launch_chol_cluster_f32(float* G, int r, int64_t B, double* rhs_out, double* w_out,
@@ -1891,7 +1919,7 @@ cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rh
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs);
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs, nullptr);
   return cudaGetLastError();
 }
 
@@ -2129,13 +2157,12 @@ void cg_stats(unsigned long long out[2]) {
   cudaMemcpyFromSymbol(out, g_cg_iters, sizeof(unsigned long long) * 2);
 }
 
+size_t chol_panel_scratch_doubles(int r) { return (size_t)chol_panel_rows(r) * kPS; }
+
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                                cudaStream_t s) {
-  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r * kPS + (size_t)r) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_chol_solve<512>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_chol_solve<512><<<1, 512, smem, s>>>(G, r, w_out, flag, resid2, flag);
+                                double* pscratch, cudaStream_t s) {
+  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(double);
+  k_chol_solve<512><<<1, 512, smem, s>>>(G, r, w_out, flag, resid2, flag, nullptr, pscratch);
   return cudaGetLastError();
 }
 

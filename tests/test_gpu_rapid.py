@@ -222,9 +222,10 @@ def test_tensor_core_completion_matches_fp32(monkeypatch, v, r, B, two_sided):
     assert np.all(np.abs(tc - ref) <= bound), np.max(np.abs(tc - ref) / bound)
 
 
+@pytest.mark.parametrize("chol", ["cta", "cluster"])
 @pytest.mark.parametrize("v,r,k,B", [(6000, 100, 700, 300), (20000, 400, 1836, 160),
                                      (3000, 31, 200, 50), (9000, 130, 520, 200)])
-def test_tensor_core_gram_lsq_matches_fp64(v, r, k, B):
+def test_tensor_core_gram_lsq_matches_fp64(monkeypatch, chol, v, r, k, B):
     """rmx_lsq_solve_tc (tcgen05 Gram of fp16 hi/lo planes + two fp64
     refinement steps) against the fp64 Gram + Cholesky path, on orthonormal
     bases and random observation sets: 1e-10 relative, with no system falling
@@ -234,6 +235,10 @@ def test_tensor_core_gram_lsq_matches_fp64(v, r, k, B):
 
     from paper_1703_01506_b200 import rapid_engine as re
 
+    # the batched fp32 factor: one CTA per system (default) or the on-chip
+    # 4-CTA-cluster variant (RMX_CHOL_CLUSTER=1); refinement resolves: one
+    # warp per system
+    monkeypatch.setenv("RMX_CHOL_CLUSTER", "1" if chol == "cluster" else "0")
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(v + r)
     u = np.linalg.qr(rng.standard_normal((v, r)))[0]
@@ -316,10 +321,15 @@ def _grouse_case(v=6000, ell=24, r=24, eta=0.05, seed=77):
     return t_ex, int(np.ceil(eta * v)), r, seed
 
 
-def test_grouse_matches_oracle_numpy_restatement(oracle_mod):
+@pytest.mark.parametrize("solver", ["cg", "chol_fallback"])
+def test_grouse_matches_oracle_numpy_restatement(oracle_mod, solver, monkeypatch):
     """Device GROUSE vs the numpy restatement of lrmc.py:208-268 (pinned to
     the reference's basis in test_oracle_golden): same Omega draws, so the
-    trajectories agree to fp64 solver precision."""
+    trajectories agree to fp64 solver precision -- with the cluster CG, and
+    with every update forced through the gated Cholesky fallback (the path
+    taken when CG does not converge)."""
+    if solver == "chol_fallback":
+        monkeypatch.setenv("RMX_GROUSE_FORCE_FALLBACK", "1")
     t_ex, k, r, seed = _grouse_case()
     res = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=4)
     u, passes, pres, om, conv = oracle_mod.grouse(t_ex, k, r, seed, max_passes=4)
