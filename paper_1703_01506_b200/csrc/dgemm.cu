@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
                                                  const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb,
                                                  double* __restrict__ C, int64_t ldc, int accum) {
+  pdl_wait();
   extern __shared__ __align__(16) double dsm[];
   auto As = [&](int st) { return dsm + (size_t)st * 2 * kTileD; };
   auto Bs = [&](int st) { return dsm + (size_t)st * 2 * kTileD + kTileD; };
@@ -206,6 +207,29 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
   // accumulator (i, j, h): tile row wr + 8 i + lane / 4, column wc + 8 j + 2 (lane % 4) + h
   const int cr = lane >> 2, cc2 = (lane & 3) * 2;
   if (S == 1) {
+    if (!SYRK && accum) {  // C += : all 32 loads in flight before the first store
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t row = m0 + wr + 8 * i + cr;
+            const int c = n0 + wc + 8 * j + cc2 + h;
+            acc[i][j][h] += (row < m && c < n) ? C[row * ldc + c] : 0.0;
+          }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t row = m0 + wr + 8 * i + cr;
+            const int c = n0 + wc + 8 * j + cc2 + h;
+            if (row < m && c < n) C[row * ldc + c] = acc[i][j][h];
+          }
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -267,13 +291,15 @@ cudaError_t launch(dim3 grid, int S, int64_t m, int n, int kk, const double* A, 
   cfg.blockDim = dim3(kT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = S;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_dgemm_rm<SYRK>, m, n, kk, A, lda, B, ldb, C, ldc, accum);
 }
 

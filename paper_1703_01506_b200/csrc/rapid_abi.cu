@@ -1,6 +1,7 @@
 // rapid_abi.cu -- extern "C" RapidPT entry points (include/rmx.h) and the
 // native GROUSE training loop (reference lrmc.py:208-268).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -465,7 +466,12 @@ int rmx_orthonormalize(double* u, int64_t v, int32_t r, int32_t force, double* d
   DevBuf<double> G, dev;
   RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
   RCUDA(dev.alloc(2, s));
-  RCUDA(launch_gram(u, r, r, nullptr, (int)v, nullptr, G.p, 1, s));
+  // U^T U on the fp64 tensor cores, cluster split-K with a fixed reduction
+  // order (deterministic; the atomics of a split-K k_gram were not); row and
+  // column r (the unused right-hand side) stay 0
+  RCUDA(cudaMemsetAsync(G.p, 0, (size_t)(r + 1) * (r + 1) * sizeof(double), s));
+  if (v > INT32_MAX) return rset(st, RMX_E_USAGE, "basis of %lld rows too tall", (long long)v);
+  RCUDA(launch_dsyrk_rm((int)v, r, u, r, G.p, r + 1, s));
   RCUDA(launch_max_dev_identity(G.p, r, dev.p, s));
   double h = 0.0;
   RCUDA(cudaMemcpyAsync(&h, dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -473,7 +479,7 @@ int rmx_orthonormalize(double* u, int64_t v, int32_t r, int32_t force, double* d
   if (drift) *drift = h;
   if (!force && h <= 1e-8) return RMX_OK;
   for (int pass = 0; pass < 2; ++pass) {
-    if (pass > 0) RCUDA(launch_gram(u, r, r, nullptr, (int)v, nullptr, G.p, 1, s));
+    if (pass > 0) RCUDA(launch_dsyrk_rm((int)v, r, u, r, G.p, r + 1, s));
     DevBuf<int32_t> flag;
     RCUDA(flag.alloc(1, s));
     RCUDA(launch_chol_solve(G.p, r, 1, nullptr, flag.p, nullptr, s));
@@ -593,7 +599,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     prof.mark(s);
     const double* trow = t + (int64_t)i * v;
     // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
-    RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, s));
+    RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, sums.p, s));
     prof.mark(s);
     // pending deferred terms <= updates since the last flush (tglob % kDeferCap;
     // a halted update adds none), and the unused columns of X / Y are zero:
@@ -607,8 +613,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
     prof.mark(s);
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
-    RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));
-    RCUDA(cudaMemsetAsync(sums.p, 0, 8 * sizeof(double), s));
+    RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));  // (sums zeroed by the gather)
     prof.mark(s);
     if (use_cg) {
       RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,

@@ -3,8 +3,39 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 namespace rmx {
+
+// Programmatic dependent launch for the GROUSE per-update kernel chain
+// (RMX_PDL=0 turns it off): a kernel launched with the attribute may be
+// scheduled as soon as its predecessor's blocks have exited, and every chain
+// kernel starts with griddepcontrol.wait (pdl_wait, sm100.cuh) before it
+// touches memory, so the dependent-launch latency overlaps the tail of the
+// previous kernel instead of following its completion.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RMX_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
 
 cudaError_t launch_rapid_stats(const double* x, int n, int n1, const int16_t* orders,
                                const int32_t* omegas, int64_t L, int k, double* t_out,
@@ -77,7 +108,8 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
                                    const double* M, const double* cmat, const GrouseState* st,
                                    double* hw, double* mw, double* dots, cudaStream_t s);
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
-                                     int64_t ldo, const double* t, double* vals, cudaStream_t s);
+                                     int64_t ldo, const double* t, double* vals, double* zero8,
+                                     cudaStream_t s);
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
                              double* dots, cudaStream_t s);

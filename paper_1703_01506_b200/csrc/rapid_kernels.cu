@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
   // solve that did not converge, decided on the device)
   // rhs_ext (refinement): G already holds the factor L; solve L L^T d =
   // rhs_ext[b], w_out[b] += d, flag[b] = 1 when |d| > 1e-7 |w| (not converged)
+  pdl_wait();
   if (gate && *gate == 0) return;
   __syncthreads();  // every thread has read the gate before it is overwritten
   extern __shared__ __align__(16) unsigned char chol_smem[];
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
                                                          int32_t* __restrict__ flag,
                                                          double* __restrict__ resid2, double tol,
                                                          double* __restrict__ x0) {
+  pdl_wait();
   extern __shared__ double cs[];
   const int R = (r + NC - 1) / NC;  // rows per CTA
   const uint32_t me = cluster_ctarank();
@@ -973,6 +975,7 @@ constexpr int kHgSplit = 16;
 __global__ void k_h_g_part(int r, const GrouseState* __restrict__ st,
                            const double* __restrict__ ug, int64_t ldu, int k,
                            const double* __restrict__ resid, double* __restrict__ gpart) {
+  pdl_wait();
   if (st->halted || !st->pending) return;
   __shared__ double part[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -997,6 +1000,7 @@ __global__ void k_h_g_fin(const double* __restrict__ hw, int r, const GrouseStat
                           int k, const double* __restrict__ vals, const double* __restrict__ resid,
                           const double* __restrict__ sums, const double* __restrict__ gpart,
                           double* __restrict__ g) {
+  pdl_wait();
   if (st->halted || !st->pending) return;
   const double a = st->pend_a, bb = st->pend_b;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1060,6 +1064,7 @@ __global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
                                const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
                                const double* __restrict__ cmat, const GrouseState* __restrict__ st,
                                int dense) {
+  pdl_wait();
   __shared__ int64_t hit_row[256];
   __shared__ double hit_val[256];
   __shared__ int nhit;
@@ -1161,6 +1166,7 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
                                   const double* __restrict__ cmat,
                                   const GrouseState* __restrict__ st, double* __restrict__ hw,
                                   double* __restrict__ mw, double* __restrict__ dots, int nres) {
+  pdl_wait();
   if ((int)blockIdx.x < nres)
     resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums);
   else
@@ -1172,7 +1178,9 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
 __global__ void k_gather_urows_vals(const double* __restrict__ U, int r,
                                     const int32_t* __restrict__ idx, int k, double* __restrict__ out,
                                     int64_t ldo, const double* __restrict__ t,
-                                    double* __restrict__ vals) {
+                                    double* __restrict__ vals, double* __restrict__ zero8) {
+  pdl_wait();
+  if (zero8 && blockIdx.x == 0 && threadIdx.x < 8) zero8[threadIdx.x] = 0.0;  // the update's sums
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)k * r) return;
   const int i = (int)(e / r), c = (int)(e - (int64_t)i * r);
@@ -1192,6 +1200,7 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
     const double* __restrict__ resid, const double* __restrict__ w, int r,
     int32_t* __restrict__ d_idx, double* __restrict__ d_val, double* __restrict__ cmat,
     double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw) {
+  pdl_wait();
   __shared__ int skip, do_update, slot;
   __shared__ double sb, sinvw, sa, pnorm2;
   __shared__ double part[32];
@@ -1275,6 +1284,7 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
                               const GrouseState* __restrict__ st, const double* __restrict__ mw,
                               const double* __restrict__ dots, const double* __restrict__ b,
                               int r) {
+  pdl_wait();
   if (st->halted || !st->pending) return;
   const int y = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1296,6 +1306,7 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
 }
 
 __global__ void k_defer_count(GrouseState* __restrict__ st) {
+  pdl_wait();
   if (st->halted || !st->pending) return;
   st->nterms += 1;
   st->pending = 0;
@@ -1986,13 +1997,15 @@ cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* fl
   cfg.blockDim = dim3(kCgThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_cg_solve<C>, G, r, w_out, flag, resid2, tol, x0);
 }
 
@@ -2052,9 +2065,11 @@ cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const doubl
   (void)H;
   (void)wn;
   double* gpart = g + r + 1;  // kHgSplit x r scratch after g[0..r]
-  k_h_g_part<<<dim3((unsigned)((r + 31) / 32), kHgSplit), 256, 0, s>>>(r, st, ug, ldu, k, resid, gpart);
-  k_h_g_fin<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(hw, r, st, k, vals, resid, sums, gpart, g);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(k_h_g_part, dim3((unsigned)((r + 31) / 32), kHgSplit), dim3(256), 0, s,
+                             r, st, ug, ldu, k, resid, gpart);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_h_g_fin, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, s, hw, r, st, k,
+                    vals, resid, sums, (const double*)gpart, g);
 }
 
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s) {
@@ -2071,9 +2086,8 @@ cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
 cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
                                 const int32_t* d_idx, const double* d_val, const double* cmat,
                                 const GrouseState* st, int dense, cudaStream_t s) {
-  k_sparse_terms<<<dim3(kDeferCap, (unsigned)((k + 255) / 256)), 256, 0, s>>>(
-      out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
-  return cudaGetLastError();
+  return launch_pdl(k_sparse_terms, dim3(kDeferCap, (unsigned)((k + 255) / 256)), dim3(256), 0, s,
+                    out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
 }
 
 cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
@@ -2102,15 +2116,17 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
                                    double* hw, double* mw, double* dots, cudaStream_t s) {
   const int nres = (k * 32 + 255) / 256;
   const int ndv = (2 * r + kDeferCap + 7) / 8;
-  k_resid_defer_vec<<<(unsigned)(nres + ndv), 256, 0, s>>>(U, ldu, r, k, vals, w, resid, sums, H,
-                                                           M, cmat, st, hw, mw, dots, nres);
-  return cudaGetLastError();
+  return launch_pdl(k_resid_defer_vec, dim3((unsigned)(nres + ndv)), dim3(256), 0, s, U, ldu, r, k,
+                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres);
 }
 
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
-                                     int64_t ldo, const double* t, double* vals, cudaStream_t s) {
+                                     int64_t ldo, const double* t, double* vals, double* zero8,
+                                     cudaStream_t s) {
   const int64_t n = (int64_t)k * r;
-  k_gather_urows_vals<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, ldo, t, vals);
+  cudaError_t e = launch_pdl(k_gather_urows_vals, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                             s, U, r, idx, k, out, ldo, t, vals, zero8);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -2127,18 +2143,17 @@ cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int3
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
                                  const double* hw, cudaStream_t s) {
-  k_grouse_post_m<<<1, 1024, 0, s>>>(st, sums, flag, step, step_index, idx, k, resid, w, r, d_idx,
-                                     d_val, cmat, wn, final_slot, hw);
-  return cudaGetLastError();
+  return launch_pdl(k_grouse_post_m, dim3(1), dim3(1024), 0, s, st, sums, flag, step, step_index,
+                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw);
 }
 
 cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
                                const double* hg, GrouseState* st, const double* mw,
                                const double* dots, const double* wn, int r, cudaStream_t s) {
-  k_defer_apply<<<dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)), 256, 0, s>>>(
-      M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
-  k_defer_count<<<1, 1, 0, s>>>(st);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(k_defer_apply, dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)),
+                             dim3(256), 0, s, M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_defer_count, dim3(1), dim3(1), 0, s, st);
 }
 
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
@@ -2162,8 +2177,8 @@ size_t chol_panel_scratch_doubles(int r) { return (size_t)chol_panel_rows(r) * k
 cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
                                 double* pscratch, cudaStream_t s) {
   const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(double);
-  k_chol_solve<512><<<1, 512, smem, s>>>(G, r, w_out, flag, resid2, flag, nullptr, pscratch);
-  return cudaGetLastError();
+  return launch_pdl(k_chol_solve<512, double>, dim3(1), dim3(512), smem, s, G, r, w_out, flag,
+                    resid2, (const int32_t*)flag, (const double*)nullptr, pscratch);
 }
 
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s) {
