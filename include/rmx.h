@@ -75,6 +75,11 @@ int rmx_abi_version(void);
 
 /* Device capability probe: returns RMX_OK on an sm_100 device, fills SM count. */
 int rmx_device_check(int device, int32_t *sm_count, rmx_status *st);
+/* cudaHostRegister / cudaHostUnregister of caller memory (page-locking the
+ * reference's host arrays in place for the overlapped uploads); 0 = ok.
+ * Through ctypes these calls release the Python GIL. */
+int rmx_host_register(void *ptr, size_t bytes);
+int rmx_host_unregister(void *ptr);
 
 /* ---------------------------------------------------------------- NaivePT
  * Replaces reference naive.py:60-109 run_naive (the _max_block loop 49-57:

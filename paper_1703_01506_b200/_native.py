@@ -70,6 +70,8 @@ class Mat0Info(ctypes.Structure):
 EXPORTS = (
     "rmx_abi_version",
     "rmx_device_check",
+    "rmx_host_register",
+    "rmx_host_unregister",
     "rmx_naive_workspace_bytes",
     "rmx_naive_maxnull",
     "rmx_naive_maxnull_host",
@@ -132,6 +134,8 @@ _NP = ctypes.POINTER(NaiveStats)
 _SIGS = {
     "rmx_abi_version": ([], ctypes.c_int),
     "rmx_device_check": ([ctypes.c_int, ctypes.POINTER(_i32), _SP], ctypes.c_int),
+    "rmx_host_register": ([_vp, _sz], ctypes.c_int),
+    "rmx_host_unregister": ([_vp], ctypes.c_int),
     "rmx_naive_workspace_bytes": ([_i64, _i32, _i64], _sz),
     "rmx_naive_maxnull": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
                           ctypes.c_int),

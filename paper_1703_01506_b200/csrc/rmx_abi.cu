@@ -415,6 +415,15 @@ extern "C" {
 
 int rmx_abi_version(void) { return RMX_ABI_VERSION; }
 
+// Page-lock / unlock host memory in place.  Called through ctypes, which
+// drops the GIL for the call: registering the 839 MB config-4 matrix takes
+// a few hundred ms, during which host threads (the BASIS_INIT normals) keep
+// running -- torch's cudart binding holds the GIL for the whole call.
+int rmx_host_register(void* ptr, size_t bytes) {
+  return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? 0 : 1;
+}
+int rmx_host_unregister(void* ptr) { return cudaHostUnregister(ptr) == cudaSuccess ? 0 : 1; }
+
 int rmx_device_check(int device, int32_t* sm_count, rmx_status* st) {
   clear_status(st);
   int ndev = 0;

@@ -24,13 +24,17 @@ _LOCK = threading.RLock()
 _MIN_REGISTER_BYTES = 64 << 20
 
 
-def _unregister(ptr: int) -> None:
-    import torch
+def _lib():
+    from . import _native
 
+    return _native.load()
+
+
+def _unregister(ptr: int) -> None:
     with _LOCK:
         if _REGISTERED.pop(ptr, None) is not None:
             try:
-                torch.cuda.cudart().cudaHostUnregister(ptr)
+                _lib().rmx_host_unregister(ptr)
             except Exception:  # interpreter shutdown
                 pass
 
@@ -58,14 +62,12 @@ def _owner(arr: np.ndarray) -> np.ndarray:
 def _register(arr: np.ndarray) -> bool:
     """Page-lock a (large, C-contiguous) array's memory in place, once per
     owning array (unregistered when the owner is garbage-collected)."""
-    import torch
-
     owner = _owner(arr)
     ptr = owner.ctypes.data
     with _LOCK:
         if ptr in _REGISTERED and _REGISTERED[ptr][0]() is owner:
             return True
-    rc = torch.cuda.cudart().cudaHostRegister(ptr, owner.nbytes, 0)
+    rc = _lib().rmx_host_register(ptr, owner.nbytes)  # ctypes: the GIL is released
     if int(rc) != 0:
         return False
     with _LOCK:

@@ -324,6 +324,9 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
     block = 1 << 20
     bufs = [pinned_empty((block,), np.float64) for _ in range(2)]
     done = [None, None]
+    import threading
+
+    drawn = threading.Event()  # set when the last block is drawn (other host draws wait for it)
 
     def work():
         torch.cuda.set_device(dev)
@@ -342,6 +345,7 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
                 done[b] = ev
         finally:
             gen.close()
+            drawn.set()
         return out
 
     join = _host_async(work)
@@ -353,6 +357,7 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
         t.record_stream(cur)
         return t
 
+    joined.drawn = drawn
     return joined
 
 
@@ -556,18 +561,54 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
     init = _basis_init_async(cfg.seed, v, rank, dev)    # host, overlapped with the GPU work below
     gap = None
     if cfg.shift_override is None and cfg.shift_estimator != "residual-sup":
-        gap = _to_dev_async(lambda: draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v), dev)
+        # the SHIFT_GAP streams (needed after GROUSE) start once the serial
+        # BASIS_INIT stream (GROUSE's critical path) is drawn: no competition
+        # for host cores with the one stream that cannot be parallelised
+        def gap_draw():
+            init.drawn.wait()
+            return draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v)
+
+        gap = _to_dev_async(gap_draw, dev)
     xd = data_to_device(x, dev)
     od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
     _mark("x_upload+training_columns")
-    pre = None
+    pre, pre_join = None, None
     if prefetch_recovery and ell < plan.count:
-        pre = _RecoverInputs(x, xd, plan, cfg.seed, ell, k, dev)
+        if os.environ.get("RMX_PREFETCH_SERIAL"):
+            pre = _RecoverInputs(x, xd, plan, cfg.seed, ell, k, dev)
+        else:
+            # recovery's basis-independent inputs on a low-priority side
+            # stream from a host thread, concurrently with GROUSE (latency-
+            # bound: most SMs idle) instead of in front of it
+            lo_prio = torch.cuda.Stream(dev, priority=0)  # the lowest priority
+            lo_prio.wait_stream(torch.cuda.current_stream(dev))  # after xd's upload
+
+            def prefetch():
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(lo_prio):
+                    r = _RecoverInputs(x, xd, plan, cfg.seed, ell, k, dev)
+                    done = torch.cuda.Event()
+                    done.record(lo_prio)
+                return r, done
+
+            pre_join = _host_async(prefetch)
         _mark("recovery_prefetch")
-    u, final, passes, conv, _, _, host_u = _train_basis_device(
-        t_dev, v, ell, k, rank, cfg.seed, cfg.max_passes, cfg.tolerance, init,
-        host_basis=prefetch_recovery)
+    hi_prio = torch.cuda.Stream(dev, priority=-100)  # mapped to the highest priority
+    hi_prio.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(hi_prio):
+        u, final, passes, conv, _, _, host_u = _train_basis_device(
+            t_dev, v, ell, k, rank, cfg.seed, cfg.max_passes, cfg.tolerance, init,
+            host_basis=prefetch_recovery)
+    torch.cuda.current_stream(dev).wait_stream(hi_prio)
+    for tnsr in (u, final):
+        tnsr.record_stream(torch.cuda.current_stream(dev))
+    if pre_join is not None:
+        pre, done = pre_join()
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_event(done)
+        for tnsr in (pre.od, pre.omd, pre.t):
+            tnsr.record_stream(cur)
     # fits of the frozen basis on the final pass's observed rows (rapid.py:90-97)
     vals = torch.empty((ell, k), dtype=torch.float64, device=dev)
     nat.call("rmx_gather_rows", nat.ptr(t_dev), v, nat.ptr(final), k, ell, nat.ptr(vals),
