@@ -538,7 +538,7 @@ def main():
     # config, same tensor path); None when there is no capture for it
     traffic, traffic_src = None, None
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                         f"r01_k1_traffic_{cfg.name}.json")
+                         f"r02_k1_traffic_{cfg.name}.json")
     if world == 1 and os.path.exists(tpath):
         try:
             tj = json.load(open(tpath)).get("int8" if i8 else "fp16x2")

@@ -328,24 +328,37 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
 
     drawn = threading.Event()  # set when the last block is drawn (other host draws wait for it)
 
+    trace = os.environ.get("RMX_TRACE_BASIS")
+
     def work():
+        t_start = time.perf_counter()
         torch.cuda.set_device(dev)
         gen = NormalStream(seed, (BASIS_INIT,))
+        t_fill = t_wait = t_copy = 0.0
         try:
             for i, lo in enumerate(range(0, total, block)):
                 n = min(block, total - lo)
                 b = i & 1
+                t0 = time.perf_counter()
                 if done[b] is not None:
                     done[b].synchronize()  # the buffer's previous upload has left it
+                t1 = time.perf_counter()
                 gen.fill(bufs[b][:n])
+                t2 = time.perf_counter()
                 with torch.cuda.stream(side):
                     flat[lo:lo + n].copy_(torch.from_numpy(bufs[b][:n]), non_blocking=True)
                     ev = torch.cuda.Event()
                     ev.record(side)
                 done[b] = ev
+                t_wait += t1 - t0
+                t_fill += t2 - t1
+                t_copy += time.perf_counter() - t2
         finally:
             gen.close()
             drawn.set()
+        if trace:
+            print(f"[basis-init] total {time.perf_counter() - t_start:.3f}s fill {t_fill:.3f}s "
+                  f"wait {t_wait:.3f}s copy-issue {t_copy:.3f}s", flush=True)
         return out
 
     join = _host_async(work)
