@@ -80,6 +80,11 @@ int rmx_device_check(int device, int32_t *sm_count, rmx_status *st);
  * Through ctypes these calls release the Python GIL. */
 int rmx_host_register(void *ptr, size_t bytes);
 int rmx_host_unregister(void *ptr);
+/* bytes of pageable host memory -> dev through the caller's page-locked
+ * ring (two halves: memcpy into one while the other's copy is in flight),
+ * for one-shot uploads; returns after the last copy. */
+int rmx_upload_staged(const void *host, size_t bytes, void *dev, void *ring, size_t ring_bytes,
+                      void *stream, rmx_status *st);
 
 /* ---------------------------------------------------------------- NaivePT
  * Replaces reference naive.py:60-109 run_naive (the _max_block loop 49-57:
@@ -369,6 +374,14 @@ int rmx_normal_stream_open(uint64_t seed, const uint32_t *path, int32_t npath,
                            rmx_normal_stream **out, rmx_status *st);
 int rmx_normal_stream_fill(rmx_normal_stream *h, int64_t count, double *out);
 int rmx_normal_stream_close(rmx_normal_stream *h);
+/* count normals of the stream into device memory (dev_out), drawn through
+ * the caller's page-locked ring (pinned_doubles doubles, two halves) with
+ * each half's upload on `stream` overlapping the next half's draw; returns
+ * after the last copy.  Replaces the init_basis draw + transfer of
+ * lrmc.py:85-93 (the reference draws into host memory). */
+int rmx_normal_stream_fill_device(rmx_normal_stream *h, int64_t count, double *dev_out,
+                                  double *pinned, int64_t pinned_doubles, void *stream,
+                                  rmx_status *st);
 
 /* rmx_lsq_solve with the Gram on the tensor cores (v = rows of U): G~ =
  * [U_Omega | vals]^T [U_Omega | vals] from fp16 hi/lo planes (tcgen05,

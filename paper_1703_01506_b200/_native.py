@@ -72,6 +72,7 @@ EXPORTS = (
     "rmx_device_check",
     "rmx_host_register",
     "rmx_host_unregister",
+    "rmx_upload_staged",
     "rmx_naive_workspace_bytes",
     "rmx_naive_maxnull",
     "rmx_naive_maxnull_host",
@@ -100,6 +101,7 @@ EXPORTS = (
     "rmx_normal_stream_open",
     "rmx_normal_stream_fill",
     "rmx_normal_stream_close",
+    "rmx_normal_stream_fill_device",
     "rmx_complete_max",
     "rmx_to_f32",
     "rmx_row_max",
@@ -136,6 +138,7 @@ _SIGS = {
     "rmx_device_check": ([ctypes.c_int, ctypes.POINTER(_i32), _SP], ctypes.c_int),
     "rmx_host_register": ([_vp, _sz], ctypes.c_int),
     "rmx_host_unregister": ([_vp], ctypes.c_int),
+    "rmx_upload_staged": ([_vp, _sz, _vp, _vp, _sz, _vp, _SP], ctypes.c_int),
     "rmx_naive_workspace_bytes": ([_i64, _i32, _i64], _sz),
     "rmx_naive_maxnull": ([_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp, _SP, _NP],
                           ctypes.c_int),
@@ -197,6 +200,7 @@ _SIGS = {
                                ctypes.c_int),
     "rmx_normal_stream_fill": ([_vp, _i64, _vp], ctypes.c_int),
     "rmx_normal_stream_close": ([_vp], ctypes.c_int),
+    "rmx_normal_stream_fill_device": ([_vp, _i64, _vp, _vp, _i64, _vp, _SP], ctypes.c_int),
     "rmx_complete_max": ([_vp, _i64, _i32, _vp, _i64, _i64, ctypes.c_double, ctypes.c_double,
                           ctypes.c_uint64, _i32, _vp, _vp, _vp, _vp, _SP], ctypes.c_int),
     "rmx_to_f32": ([_vp, _i64, _vp, _vp, _SP], ctypes.c_int),

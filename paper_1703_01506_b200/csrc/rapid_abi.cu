@@ -459,6 +459,50 @@ int rmx_mean_var(const double* a, int64_t n, double* out2, void* stream, rmx_sta
 
 // Orthonormalise U (v x r, in place) by CholeskyQR2.  Returns the
 // orthonormality error max|U^T U - I| measured BEFORE the call in *drift.
+// count normals of an open stream straight into device memory: drawn into
+// one half of the page-locked ring while the other half's copy is in
+// flight, all inside one call (through ctypes, without the GIL: the
+// BASIS_INIT stream is GROUSE's critical path and its Python-side copy
+// loop cost as much as the draw).  Returns after the last copy completed.
+int rmx_normal_stream_fill_device(rmx_normal_stream* h, int64_t count, double* dev_out,
+                                  double* pinned, int64_t pinned_doubles, void* stream,
+                                  rmx_status* st) {
+  rclear(st);
+  if (!h || !dev_out || !pinned || pinned_doubles < 2 || count < 0)
+    return rset(st, RMX_E_USAGE, "bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t half = pinned_doubles / 2;
+  cudaEvent_t ev[2];
+  RCUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  RCUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  int rc = RMX_OK;
+  for (int64_t lo = 0, i = 0; lo < count && rc == RMX_OK; lo += half, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t n = std::min(half, count - lo);
+    double* buf = pinned + (size_t)b * half;
+    if (used[b] && cudaEventSynchronize(ev[b]) != cudaSuccess) {
+      rc = rset(st, RMX_E_CUDA, "normal upload failed");
+      break;
+    }
+    if (rmx_normal_stream_fill(h, n, buf) != 0) {
+      rc = rset(st, RMX_E_USAGE, "normal stream fill failed");
+      break;
+    }
+    if (cudaMemcpyAsync(dev_out + lo, buf, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, s) !=
+            cudaSuccess ||
+        cudaEventRecord(ev[b], s) != cudaSuccess) {
+      rc = rset(st, RMX_E_CUDA, "normal upload failed");
+      break;
+    }
+    used[b] = true;
+  }
+  cudaStreamSynchronize(s);  // the ring is the caller's: no copy may still read it
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return rc;
+}
+
 int rmx_orthonormalize(double* u, int64_t v, int32_t r, int32_t force, double* drift,
                        void* stream, rmx_status* st) {
   rclear(st);

@@ -415,6 +415,46 @@ extern "C" {
 
 int rmx_abi_version(void) { return RMX_ABI_VERSION; }
 
+// Upload of pageable host memory through the caller's page-locked ring
+// (two halves): memcpy into one half while the other half's H2D copy is in
+// flight.  For one-shot uploads (RapidPT's X) this avoids page-locking the
+// caller's array in place, whose cost (0.3-1 s for 839 MB, variable) sat
+// on the critical path before GROUSE.  Returns after the last copy.
+int rmx_upload_staged(const void* host, size_t bytes, void* dev, void* ring, size_t ring_bytes,
+                      void* stream, rmx_status* st) {
+  clear_status(st);
+  if ((!host || !dev || !ring) && bytes) return set_status(st, RMX_E_USAGE, "null buffer");
+  const size_t half = ring_bytes / 2;
+  if (half == 0) return set_status(st, RMX_E_USAGE, "staging ring too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev[2];
+  RMX_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  RMX_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  int rc = RMX_OK;
+  for (size_t off = 0, i = 0; off < bytes; off += half, ++i) {
+    const int b = (int)(i & 1);
+    const size_t n = std::min(half, bytes - off);
+    char* buf = static_cast<char*>(ring) + b * half;
+    if (used[b] && cudaEventSynchronize(ev[b]) != cudaSuccess) {
+      rc = set_status(st, RMX_E_CUDA, "staged upload failed");
+      break;
+    }
+    memcpy(buf, static_cast<const char*>(host) + off, n);
+    if (cudaMemcpyAsync(static_cast<char*>(dev) + off, buf, n, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess ||
+        cudaEventRecord(ev[b], s) != cudaSuccess) {
+      rc = set_status(st, RMX_E_CUDA, "staged upload failed");
+      break;
+    }
+    used[b] = true;
+  }
+  cudaStreamSynchronize(s);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return rc;
+}
+
 // Page-lock / unlock host memory in place.  Called through ctypes, which
 // drops the GIL for the call: registering the 839 MB config-4 matrix takes
 // a few hundred ms, during which host threads (the BASIS_INIT normals) keep
@@ -436,6 +476,17 @@ int rmx_device_check(int device, int32_t* sm_count, rmx_status* st) {
   if (prop.major != 10)
     return set_status(st, RMX_E_USAGE, "librmx is built for sm_100a; device %d is sm_%d%d (%s)",
                       device, prop.major, prop.minor, prop.name);
+  // Host threads that wait for the GPU block instead of spinning (RMX_SYNC_SPIN=1
+  // keeps CUDA's default): a spinning waiter on a hyperthread sibling halves
+  // the speed of the serial BASIS_INIT draw running beside it, which is
+  // GROUSE's critical path.  Applies to the (already active) primary context.
+  const char* spin = getenv("RMX_SYNC_SPIN");
+  if (!(spin && atoi(spin) == 1)) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur == device)
+      cudaSetDeviceFlags(cudaDeviceScheduleBlockingSync);
+    cudaGetLastError();  // best effort: an unchangeable flag is not an error
+  }
   return RMX_OK;
 }
 

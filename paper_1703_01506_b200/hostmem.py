@@ -10,6 +10,7 @@ rate.  Small arrays just go through torch's pinned allocator.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 import warnings
 import weakref
@@ -150,3 +151,35 @@ def wait_inflight() -> None:
     for _, ev in pending:
         ev.synchronize()
     _prune_inflight()
+
+
+_STAGE: dict = {}
+
+
+def upload_staged(arr: np.ndarray, device, stream=None):
+    """One-shot upload of a (large, pageable) array without page-locking it:
+    through a cached 2 x 32 MB page-locked ring (rmx_upload_staged, one
+    native call, the GIL released).  An array that is already registered
+    goes straight through to_device."""
+    import torch
+
+    from . import _native as nat
+
+    arr = np.ascontiguousarray(arr)
+    owner = _owner(arr)
+    with _LOCK:
+        registered = owner.ctypes.data in _REGISTERED
+    if registered or arr.nbytes < _MIN_REGISTER_BYTES:
+        return to_device(arr, device, stream)
+    ring = _STAGE.get("ring")
+    if ring is None:
+        ring = pinned_empty((64 << 20,), np.uint8)
+        _STAGE["ring"] = ring
+    out = torch.empty(arr.shape, dtype=_torch_dtype(arr.dtype), device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    st = nat.Status()
+    rc = nat.load().rmx_upload_staged(arr.ctypes.data, arr.nbytes, out.data_ptr(),
+                                      ring.ctypes.data, ring.nbytes, nat.stream_handle(s),
+                                      ctypes.byref(st))
+    nat.raise_for(rc, st)
+    return out

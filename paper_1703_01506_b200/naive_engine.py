@@ -180,17 +180,20 @@ def upload(x_values: np.ndarray, orders: np.ndarray, device):
     return xd, od
 
 
-def data_to_device(x, device):
+def data_to_device(x, device, one_shot: bool = False):
     """(v, n) float64 device copy of a DataMatrix, uploaded from its float32
-    source when it keeps one (half the bytes; the upcast is exact)."""
+    source when it keeps one (half the bytes; the upcast is exact).
+    one_shot: through a page-locked staging ring instead of page-locking the
+    array in place (cheaper for an array uploaded once, hostmem.upload_staged)."""
     import torch
 
-    from .hostmem import to_device
+    from .hostmem import to_device, upload_staged
 
+    up = upload_staged if one_shot else to_device
     x = as_data_matrix(x)
     if x.float32_values is not None:
-        return to_device(x.float32_values, device).to(dtype=torch.float64)
-    return to_device(x.values, device)
+        return up(x.float32_values, device).to(dtype=torch.float64)
+    return up(x.values, device)
 
 
 def run_naive_ex(x, plan, materialize: bool = False, two_sided: bool = False,

@@ -213,6 +213,16 @@ class NormalStream:
             raise RuntimeError(f"rmx_normal_stream_fill failed ({rc})")
         return out
 
+    def fill_device(self, out, pinned: np.ndarray, stream) -> None:
+        """Draw out.numel() normals straight into the contiguous fp64 CUDA
+        tensor `out` through the page-locked ring `pinned` (one native call,
+        the GIL released; returns when the last copy has landed)."""
+        st = nat.Status()
+        rc = nat.load().rmx_normal_stream_fill_device(
+            self._h, int(out.numel()), out.data_ptr(), pinned.ctypes.data, int(pinned.size),
+            nat.stream_handle(stream), ctypes.byref(st))
+        nat.raise_for(rc, st)
+
     def close(self) -> None:
         if self._h:
             nat.load().rmx_normal_stream_close(self._h)

@@ -319,46 +319,25 @@ def _basis_init_async(seed: int, v: int, rank: int, dev):
 
     side = torch.cuda.Stream(dev)
     out = torch.empty((v, rank), dtype=torch.float64, device=dev)
-    flat = out.view(-1)
-    total = v * rank
-    block = 1 << 20
-    bufs = [pinned_empty((block,), np.float64) for _ in range(2)]
-    done = [None, None]
+    ring = pinned_empty((1 << 21,), np.float64)  # two 8 MB halves
     import threading
 
-    drawn = threading.Event()  # set when the last block is drawn (other host draws wait for it)
-
+    drawn = threading.Event()  # set when the stream is drawn (other host draws wait for it)
     trace = os.environ.get("RMX_TRACE_BASIS")
 
     def work():
         t_start = time.perf_counter()
         torch.cuda.set_device(dev)
         gen = NormalStream(seed, (BASIS_INIT,))
-        t_fill = t_wait = t_copy = 0.0
         try:
-            for i, lo in enumerate(range(0, total, block)):
-                n = min(block, total - lo)
-                b = i & 1
-                t0 = time.perf_counter()
-                if done[b] is not None:
-                    done[b].synchronize()  # the buffer's previous upload has left it
-                t1 = time.perf_counter()
-                gen.fill(bufs[b][:n])
-                t2 = time.perf_counter()
-                with torch.cuda.stream(side):
-                    flat[lo:lo + n].copy_(torch.from_numpy(bufs[b][:n]), non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                done[b] = ev
-                t_wait += t1 - t0
-                t_fill += t2 - t1
-                t_copy += time.perf_counter() - t2
+            # one native call: draw into a ring half while the other half's
+            # upload is in flight (no per-block Python, no GIL)
+            gen.fill_device(out, ring, side)
         finally:
             gen.close()
             drawn.set()
         if trace:
-            print(f"[basis-init] total {time.perf_counter() - t_start:.3f}s fill {t_fill:.3f}s "
-                  f"wait {t_wait:.3f}s copy-issue {t_copy:.3f}s", flush=True)
+            print(f"[basis-init] draw + upload {time.perf_counter() - t_start:.3f}s", flush=True)
         return out
 
     join = _host_async(work)
@@ -582,7 +561,7 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
             return draw_normals(cfg.seed, SHIFT_GAP, 0, ell, v)
 
         gap = _to_dev_async(gap_draw, dev)
-    xd = data_to_device(x, dev)
+    xd = data_to_device(x, dev, one_shot=True)
     od = device_orders(plan.master_seed, 0, ell, x.subjects, dev)
     t_dev = tstat_exact_device(xd, x.n1, od)            # (ell, v), bit-exact columns
     _mark("x_upload+training_columns")
@@ -595,7 +574,9 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
             # stream from a host thread, concurrently with GROUSE (latency-
             # bound: most SMs idle) instead of in front of it
             lo_prio = torch.cuda.Stream(dev, priority=0)  # the lowest priority
-            lo_prio.wait_stream(torch.cuda.current_stream(dev))  # after xd's upload
+            # after the training columns (GROUSE's input): interleaved with
+            # them the prefetch only delayed GROUSE's start
+            lo_prio.wait_stream(torch.cuda.current_stream(dev))
 
             def prefetch():
                 torch.cuda.set_device(dev)
@@ -713,7 +694,7 @@ def recover(x, model: SubspaceModel, plan, cfg, _pre: Optional[_RecoverInputs] =
     if _pre is not None and _pre.key == (int(model.seed), ell, k, L, plan.master_seed):
         xd, od, omd, t, st, rc = _pre.xd, _pre.od, _pre.omd, _pre.t, _pre.st, _pre.rc
     else:
-        xd = data_to_device(x, dev)
+        xd = data_to_device(x, dev, one_shot=True)
         od = device_orders(plan.master_seed, ell, L, x.subjects, dev)
         omd = device_omegas(model.seed, RECOVER_OMEGA, ell, L, v, k, dev)
         t = torch.empty((nrec, k), dtype=torch.float64, device=dev)
