@@ -323,7 +323,7 @@ __global__ void k_gram_planes(const double* __restrict__ U, int64_t ldu, int64_t
 // partial g are summed in shared memory.
 constexpr int kRWarps = 8;
 template <int RL>  // r <= 32 RL
-__global__ void __launch_bounds__(32 * kRWarps) k_lsq_resid(const double* __restrict__ U,
+__global__ void __launch_bounds__(32 * kRWarps, 2) k_lsq_resid(const double* __restrict__ U,
                                                             int64_t ldu, int r,
                                                             const int32_t* __restrict__ idx,
                                                             int k, const double* __restrict__ vals,
@@ -345,7 +345,36 @@ __global__ void __launch_bounds__(32 * kRWarps) k_lsq_resid(const double* __rest
   }
   const int32_t* ib = idx + b * k;
   const double* tb = vals + b * k;
-  for (int kk = warp; kk < k; kk += kRWarps) {
+  // two rows per warp iteration: both rows' loads are in flight together and
+  // their dot-product butterflies interleave (the per-row arithmetic and its
+  // order are unchanged: same bits)
+  int kk = warp;
+  for (; kk + kRWarps < k; kk += 2 * kRWarps) {
+    const double* urow1 = U + (int64_t)ib[kk] * ldu;
+    const double* urow2 = U + (int64_t)ib[kk + kRWarps] * ldu;
+    double u1[RL], u2[RL];
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      const int c = lane + 32 * q;
+      u1[q] = c < r ? __ldg(urow1 + c) : 0.0;
+      u2[q] = c < r ? __ldg(urow2 + c) : 0.0;
+    }
+    double dot1 = 0.0, dot2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      dot1 = fma(u1[q], wr[q], dot1);
+      dot2 = fma(u2[q], wr[q], dot2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dot1 += __shfl_xor_sync(0xffffffffu, dot1, o);
+      dot2 += __shfl_xor_sync(0xffffffffu, dot2, o);
+    }
+    const double e1 = tb[kk] - dot1, e2 = tb[kk + kRWarps] - dot2;
+#pragma unroll
+    for (int q = 0; q < RL; ++q) acc[q] = fma(e2, u2[q], fma(e1, u1[q], acc[q]));
+  }
+  for (; kk < k; kk += kRWarps) {
     const double* urow = U + (int64_t)ib[kk] * ldu;
     double u[RL];
     double dot = 0.0;
@@ -468,6 +497,7 @@ cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t*
   };
   if (r <= 128) return go(k_lsq_resid<4>);
   if (r <= 256) return go(k_lsq_resid<8>);
+  if (r <= 416) return go(k_lsq_resid<13>);
   if (r <= 512) return go(k_lsq_resid<16>);
   return cudaErrorInvalidValue;
 }
