@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
                                                    int32_t* flag, double* __restrict__ resid2,
                                                    const int32_t* gate = nullptr,
                                                    const double* __restrict__ rhs_ext = nullptr,
-                                                   T* __restrict__ pscratch = nullptr) {
+                                                   T* __restrict__ pscratch = nullptr,
+                                                   int lookahead = 1) {
   // pscratch (the gated GROUSE fallback): the panel in global memory, so the
   // launch needs only a few KB of shared memory (its common case is to exit
   // at the gate; a 100+ KB request would reconfigure the SMs every update)
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
   T* rinv = D + kPW * kPS;       // kPW: 1 / L_cc
   T* after = rinv + kPW;
   T* P = pscratch ? pscratch : after;  // chol_panel_rows(r) x kPS panel (factor only)
+  constexpr bool kLookAhead = NT == 256 && sizeof(T) == 4;  // see the factor loop
   T* y = pscratch ? after : (rhs_ext ? P : P + (size_t)chol_panel_rows(r) * kPS);  // r: rhs / solution
   __shared__ int bad;
   __shared__ T dmax;
@@ -285,7 +287,131 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
       D[i * kPS + j] = val;
     }
   };
-  for (int jb = 0; jb < (rhs_ext ? 0 : r); jb += kPW) {
+  // Look-ahead (the batched fp32 factor of the recovery): warp 0 applies the
+  // trailing update to the NEXT diagonal block only and factors it while the
+  // other warps update the rest of the trailing matrix, so the serial
+  // 32-step diagonal factor no longer idles 7 of 8 warps once per panel
+  // (ncu: ~30% of the factor's stall samples were warps waiting for it).
+  // Same arithmetic, same order: same bits.
+  const bool la = kLookAhead && lookahead && !rhs_ext && !pscratch;
+  if (la) {
+    T* Dn = y + r;               // the second diagonal-block buffer
+    T* rn = Dn + kPW * kPS;
+    T* Dc = D;
+    T* rc = rinv;
+    load_block(0, min(kPW, r));
+    __syncthreads();
+    if (wid == 0) chol_block32(Dc, rc, tiny, &bad);
+    __syncthreads();
+    for (int jb = 0; jb < r; jb += kPW) {
+      const int w = min(kPW, r - jb);
+      for (int e = tid; e < w * w; e += NT) {
+        const int i = e / w, j = e % w;
+        if (j <= i) Gb[(int64_t)(jb + i) * ld + jb + j] = Dc[i * kPS + j];
+      }
+      const int rows = r - jb - w;
+      for (int i = tid; i < rows; i += NT) {  // panel rows, as below
+        T* gi = Gb + (int64_t)(jb + w + i) * ld + jb;
+        T pr[kPW];
+#pragma unroll
+        for (int c = 0; c < kPW; ++c) pr[c] = c < w ? gi[c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < kPW; ++c) {
+          T sacc = pr[c];
+#pragma unroll
+          for (int l = 0; l < c; ++l) sacc = fma(-pr[l], Dc[c * kPS + l], sacc);
+          pr[c] = sacc * rc[c];
+        }
+        T* prow = P + (size_t)i * kPS;
+#pragma unroll
+        for (int c = 0; c < kPW; ++c) {
+          prow[c] = pr[c];
+          if (c < w) gi[c] = pr[c];
+        }
+      }
+      __syncthreads();
+      if (rows <= 0) break;
+      const int wn = min(kPW, rows);
+      if (wid == 0) {
+        // next diagonal block = its G entries minus P_i . P_j, row `lane`
+        const int i = lane;
+        const T* pi = P + (size_t)i * kPS;
+        for (int j = 0; j < kPW; ++j) {
+          T val = (i == j) ? 1.0 : 0.0;
+          if (i < wn && j < wn && j <= i) {
+            const T* pj = P + (size_t)j * kPS;
+            T acc = 0.0;
+#pragma unroll 8
+            for (int c = 0; c < kPW; ++c) acc = fma(pi[c], pj[c], acc);
+            val = Gb[(int64_t)(jb + w + i) * ld + jb + w + j] - acc;
+          }
+          Dn[i * kPS + j] = val;
+        }
+        __syncwarp();
+        chol_block32(Dn, rn, tiny, &bad);
+      } else {
+        // the rest of the trailing lower triangle: 4 x 4 tiles whose rows
+        // lie below the next diagonal block (tile rows 4 bi >= wn)
+        const int nb = (rows + 3) / 4;
+        const int t0 = ((wn + 3) / 4) * ((wn + 3) / 4 + 1) / 2;  // tiles inside the block
+        const int ntile = nb * (nb + 1) / 2;
+        for (int t = t0 + tid - 32; t < ntile; t += NT - 32) {
+          int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+          while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+          while (bi * (bi + 1) / 2 > t) --bi;
+          const int bj = t - bi * (bi + 1) / 2;
+          T acc[4][4] = {};
+          const T* pi = P + (size_t)(4 * bi) * kPS;
+          const T* pj = P + (size_t)(4 * bj) * kPS;
+#pragma unroll 4
+          for (int c = 0; c < kPW; ++c) {
+            T a[4], bb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              a[q] = (4 * bi + q < rows) ? pi[q * kPS + c] : 0.0;
+              bb[q] = (4 * bj + q < rows) ? pj[q * kPS + c] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], bb[u], acc[q][u]);
+          }
+          // all 16 loads in flight before the first store (the element-wise
+          // load-subtract-store chain serialised on the L2 latency)
+          T old[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = 4 * bi + q;
+            const T* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * bj + u;
+              old[q][u] = (i < rows && j <= i) ? grow[j] : T(0);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = 4 * bi + q;
+            if (i >= rows) continue;
+            T* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * bj + u;
+              if (j <= i) grow[j] = old[q][u] - acc[q][u];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      T* tD = Dc;
+      Dc = Dn;
+      Dn = tD;
+      T* tr = rc;
+      rc = rn;
+      rn = tr;
+    }
+  }
+  for (int jb = 0; jb < ((rhs_ext || la) ? 0 : r); jb += kPW) {
     const int w = min(kPW, r - jb);
     load_block(jb, w);
     __syncthreads();
@@ -341,6 +467,17 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
 #pragma unroll
           for (int u = 0; u < 4; ++u) acc[q][u] = fma(a[q], bb[u], acc[q][u]);
       }
+      T old[4][4];  // all loads in flight before the first store
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = 4 * bi + q;
+        const T* grow = Gb + (int64_t)(jb + w + i) * ld + jb + w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * bj + u;
+          old[q][u] = (i < rows && j <= i) ? grow[j] : T(0);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = 4 * bi + q;
@@ -349,7 +486,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = 4 * bj + u;
-          if (j <= i) grow[j] -= acc[q][u];
+          if (j <= i) grow[j] = old[q][u] - acc[q][u];
         }
       }
     }
@@ -1521,8 +1658,9 @@ cudaError_t launch_chol_solve(double* G, int r, int64_t B, double* w_out, int32_
 
 cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int32_t* flag,
                                   cudaStream_t s) {
-  const size_t smem =
-      ((size_t)kPW * kPS + kPW + (size_t)chol_panel_rows(r) * kPS + (size_t)r) * sizeof(float);
+  // + the look-ahead's second diagonal-block buffer (NT = 256)
+  const size_t smem = ((size_t)2 * (kPW * kPS + kPW) + (size_t)chol_panel_rows(r) * kPS +
+                       (size_t)r) * sizeof(float);
   // RMX_CHOL_NT=512: one 512-thread CTA per SM (working set of the trailing
   // updates ~148 systems -> L2-resident) instead of three 256-thread CTAs
   const char* ntv = getenv("RMX_CHOL_NT");
@@ -1530,13 +1668,14 @@ cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int
     auto kern = k_chol_solve<512, float>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr);
+    kern<<<(unsigned)B, 512, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr, 0);
     return cudaGetLastError();
   }
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr);
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_out, flag, nullptr, nullptr, nullptr, nullptr,
+                                      getenv("RMX_CHOL_NOLA") ? 0 : 1);
   return cudaGetLastError();
 }
 
@@ -1930,7 +2069,7 @@ cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rh
   auto kern = k_chol_solve<256, float>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs, nullptr);
+  kern<<<(unsigned)B, 256, smem, s>>>(G, r, w_inout, nconv, nullptr, nullptr, rhs, nullptr, 0);
   return cudaGetLastError();
 }
 
@@ -2178,7 +2317,7 @@ cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, 
                                 double* pscratch, cudaStream_t s) {
   const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(double);
   return launch_pdl(k_chol_solve<512, double>, dim3(1), dim3(512), smem, s, G, r, w_out, flag,
-                    resid2, (const int32_t*)flag, (const double*)nullptr, pscratch);
+                    resid2, (const int32_t*)flag, (const double*)nullptr, pscratch, 0);
 }
 
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s) {
