@@ -555,7 +555,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(wn.alloc(r, s));
   RCUDA(vals.alloc(k, s));
   RCUDA(resid.alloc(k, s));
-  RCUDA(sums.alloc(8, s));
+  // + the residual blocks' partials (k_resid_defer_vec -> k_grouse_post_m)
+  RCUDA(sums.alloc(8 + 2 * (size_t)((k * 32 + 255) / 256), s));
   RCUDA(flag.alloc(1, s));
   RCUDA(idxbuf.alloc(k, s));
   // ug rows: [U_Omega row | t_Omega] (the Gram's operand), padded to an even
@@ -605,7 +606,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       RCUDA(launch_dgemm_rm(v, nt, r, ubase, r, Xf.p, kDeferCap, ub2.p, kDeferCap, 0, s));
       RCUDA(launch_dgemm_rm(v, r, nt, ub2.p, kDeferCap, Yf.p, r, ubase, r, 1, s));
     }
-    RCUDA(launch_sparse_terms(ubase, r, r, nullptr, k, didx.p, dval.p, cmat.p, gst.p, 1, s));
+    RCUDA(launch_sparse_terms_dense(ubase, r, r, k, didx.p, dval.p, cmat.p, nt, s));
     RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));
     return RMX_OK;
   };
@@ -654,7 +655,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       RCUDA(launch_dgemm_rm(k, r, ntc, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
     }
     prof.mark(s);
-    RCUDA(launch_sparse_terms(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, 0, s));
+    RCUDA(launch_sparse_terms_rows(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, s));
     prof.mark(s);
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
     RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));  // (sums zeroed by the gather)

@@ -93,6 +93,13 @@ struct GrouseState {
 };
 // M-deferred GROUSE: U = U_base M + sum_s d_s c_s^T (d_s sparse on Omega_s)
 constexpr int kDeferCap = 64;  // terms between flushes (the host flushes every 64 updates)
+// deterministic variants (no atomics): per-update rows / per-term dense flush
+cudaError_t launch_sparse_terms_rows(double* out, int64_t ldo, int r, const int32_t* rows_sorted,
+                                     int k, const int32_t* d_idx, const double* d_val,
+                                     const double* cmat, const GrouseState* st, cudaStream_t s);
+cudaError_t launch_sparse_terms_dense(double* out, int64_t ldo, int r, int k, const int32_t* d_idx,
+                                      const double* d_val, const double* cmat, int nterms,
+                                      cudaStream_t s);
 cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
                                 const int32_t* d_idx, const double* d_val, const double* cmat,
                                 const GrouseState* st, int dense, cudaStream_t s);
@@ -113,7 +120,7 @@ cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx,
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
                              double* dots, cudaStream_t s);
-cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int32_t* flag,
+cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* flag,
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,

@@ -1035,7 +1035,8 @@ __device__ __forceinline__ void resid_block(int bid, const double* __restrict__ 
                                             int r, const int32_t* __restrict__ idx, int k,
                                             const double* __restrict__ vals,
                                             const double* __restrict__ w,
-                                            double* __restrict__ resid, double* __restrict__ sums) {
+                                            double* __restrict__ resid, double* __restrict__ sums,
+                                            double* __restrict__ rpart = nullptr) {
   __shared__ double part[2][8];  // blockDim.x == 256
   const int warp = (bid * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   double ee = 0.0, tt = 0.0;
@@ -1060,8 +1061,13 @@ __device__ __forceinline__ void resid_block(int bid, const double* __restrict__ 
       a += part[0][q];
       b += part[1][q];
     }
-    atomicAdd(&sums[0], a);  // |resid|^2
-    atomicAdd(&sums[2], b);  // |t_Omega|^2
+    if (rpart) {  // per-block partials, reduced in a fixed order by the consumer
+      rpart[2 * bid] = a;
+      rpart[2 * bid + 1] = b;
+    } else {
+      atomicAdd(&sums[0], a);  // |resid|^2
+      atomicAdd(&sums[2], b);  // |t_Omega|^2
+    }
   }
 }
 
@@ -1196,6 +1202,72 @@ __global__ void k_h_identity(double* __restrict__ H, int r) {
 // grid (kDeferCap terms) x (k / 256 pieces of the term's index list): one
 // binary search per thread, so the latency is one search, not k / 256 of
 // them in sequence (expected hits per term: k^2 / v, ~6 at config 5)
+// Deterministic sparse terms on the gathered rows (per-update mode): one
+// warp per observed row q (voxel rows_sorted[q]); its lanes binary-search
+// the voxel in the terms' sorted index lists (lane l: terms l, l + 32), then
+// the hits are added in term order, lanes over the columns -- no atomics, so
+// every run adds the same terms in the same order (the block-per-term
+// version accumulated colliding rows with atomicAdd in arbitrary order).
+__global__ void __launch_bounds__(256) k_sparse_terms_rows(
+    double* __restrict__ out, int64_t ldo, int r, const int32_t* __restrict__ rows_sorted, int k,
+    const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
+    const double* __restrict__ cmat, const GrouseState* __restrict__ st) {
+  pdl_wait();
+  if (st->halted) return;
+  const int nt = st->nterms;
+  if (nt <= 0) return;
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (q >= k) return;
+  const int32_t vox = __ldg(rows_sorted + q);
+  int pos[2] = {-1, -1};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int sterm = lane + 32 * h;
+    if (sterm < nt) {
+      const int32_t* di = d_idx + (int64_t)sterm * k;
+      int lo = 0, hi = k - 1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int32_t x = __ldg(di + mid);
+        if (x == vox) {
+          pos[h] = mid;
+          break;
+        }
+        if (x < vox) lo = mid + 1;
+        else hi = mid - 1;
+      }
+    }
+  }
+  double* o = out + (int64_t)q * ldo;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    unsigned hits = __ballot_sync(0xffffffffu, pos[h] >= 0);
+    while (hits) {  // ascending term order
+      const int src = __ffs(hits) - 1;
+      hits &= hits - 1;
+      const int sterm = src + 32 * h;
+      const int p = __shfl_sync(0xffffffffu, pos[h], src);
+      const double dq = d_val[(int64_t)sterm * k + p];
+      const double* cs = cmat + (int64_t)sterm * r;
+      for (int c = lane; c < r; c += 32) o[c] += dq * cs[c];
+    }
+  }
+}
+
+// Deterministic dense flush of ONE deferred term: U[d_idx[q], :] += d_q c^T.
+// A term's voxels are distinct, so no two threads touch one element; the
+// host launches the terms one after another (term order = update order).
+__global__ void k_sparse_term_dense(double* __restrict__ out, int64_t ldo, int r,
+                                    const int32_t* __restrict__ di, const double* __restrict__ dv,
+                                    const double* __restrict__ cs, int k) {
+  pdl_wait();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * r) return;
+  const int q = (int)(e / r), c = (int)(e - (int64_t)q * r);
+  out[(int64_t)di[q] * ldo + c] += dv[q] * cs[c];
+}
+
 __global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
                                const int32_t* __restrict__ rows_sorted, int k,
                                const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
@@ -1302,10 +1374,11 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
                                   const double* __restrict__ H, const double* __restrict__ M,
                                   const double* __restrict__ cmat,
                                   const GrouseState* __restrict__ st, double* __restrict__ hw,
-                                  double* __restrict__ mw, double* __restrict__ dots, int nres) {
+                                  double* __restrict__ mw, double* __restrict__ dots, int nres,
+                                  double* __restrict__ rpart) {
   pdl_wait();
   if ((int)blockIdx.x < nres)
-    resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums);
+    resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums, rpart);
   else
     defer_vec_block(blockIdx.x - nres, H, M, cmat, w, r, st, hw, mw, dots);
 }
@@ -1332,15 +1405,44 @@ __global__ void k_gather_urows_vals(const double* __restrict__ U, int r,
 
 // decisions as k_grouse_post; the update becomes deferred term nterms
 __global__ void __launch_bounds__(1024) k_grouse_post_m(
-    GrouseState* __restrict__ st, const double* __restrict__ sums, const int32_t* __restrict__ flag,
+    GrouseState* __restrict__ st, double* __restrict__ sums, const int32_t* __restrict__ flag,
     double step, int64_t step_index, const int32_t* __restrict__ idx, int k,
     const double* __restrict__ resid, const double* __restrict__ w, int r,
     int32_t* __restrict__ d_idx, double* __restrict__ d_val, double* __restrict__ cmat,
-    double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw) {
+    double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw,
+    int nres) {
   pdl_wait();
   __shared__ int skip, do_update, slot;
   __shared__ double sb, sinvw, sa, pnorm2;
   __shared__ double part[32];
+  __shared__ double part2[32];
+  {  // |resid|^2 and |t_Omega|^2 from k_resid_defer_vec's per-block partials
+     // (sums + 8), in a fixed order: every run gives the same bits
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nres; i += blockDim.x) {
+      a += sums[8 + 2 * i];
+      b += sums[8 + 2 * i + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      part[threadIdx.x / 32] = a;
+      part2[threadIdx.x / 32] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int i = 0; i < (int)(blockDim.x / 32); ++i) {
+        ta += part[i];
+        tb += part2[i];
+      }
+      sums[0] = ta;
+      sums[2] = tb;
+    }
+    __syncthreads();
+  }
   {  // |p|^2 = |U w|^2 = w^T H w
     double acc = 0.0;
     for (int c = threadIdx.x; c < r; c += blockDim.x) acc = fma(w[c], hw[c], acc);
@@ -2222,6 +2324,26 @@ cudaError_t launch_h_identity(double* H, int r, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_sparse_terms_rows(double* out, int64_t ldo, int r, const int32_t* rows_sorted,
+                                     int k, const int32_t* d_idx, const double* d_val,
+                                     const double* cmat, const GrouseState* st, cudaStream_t s) {
+  return launch_pdl(k_sparse_terms_rows, dim3((unsigned)((k + 7) / 8)), dim3(256), 0, s, out, ldo,
+                    r, rows_sorted, k, d_idx, d_val, cmat, st);
+}
+
+cudaError_t launch_sparse_terms_dense(double* out, int64_t ldo, int r, int k, const int32_t* d_idx,
+                                      const double* d_val, const double* cmat, int nterms,
+                                      cudaStream_t s) {
+  const int64_t n = (int64_t)k * r;
+  for (int t = 0; t < nterms; ++t) {
+    cudaError_t e = launch_pdl(k_sparse_term_dense, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                               s, out, ldo, r, d_idx + (int64_t)t * k, d_val + (int64_t)t * k,
+                               cmat + (int64_t)t * r, k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
                                 const int32_t* d_idx, const double* d_val, const double* cmat,
                                 const GrouseState* st, int dense, cudaStream_t s) {
@@ -2255,8 +2377,10 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
                                    double* hw, double* mw, double* dots, cudaStream_t s) {
   const int nres = (k * 32 + 255) / 256;
   const int ndv = (2 * r + kDeferCap + 7) / 8;
+  // sums[0] / sums[2] (|resid|^2, |t_Omega|^2): per-block partials in
+  // sums + 8.., reduced in a fixed order by k_grouse_post_m (deterministic)
   return launch_pdl(k_resid_defer_vec, dim3((unsigned)(nres + ndv)), dim3(256), 0, s, U, ldu, r, k,
-                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres);
+                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres, sums + 8);
 }
 
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
@@ -2277,13 +2401,14 @@ cudaError_t launch_defer_vec(const double* H, const double* M, const double* cma
   return cudaGetLastError();
 }
 
-cudaError_t launch_grouse_post_m(GrouseState* st, const double* sums, const int32_t* flag,
+cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* flag,
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
                                  const double* hw, cudaStream_t s) {
+  const int nres = (k * 32 + 255) / 256;  // k_resid_defer_vec's residual blocks
   return launch_pdl(k_grouse_post_m, dim3(1), dim3(1024), 0, s, st, sums, flag, step, step_index,
-                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw);
+                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw, nres);
 }
 
 cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,

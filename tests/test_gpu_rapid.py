@@ -354,3 +354,22 @@ def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, monkeypatch):
     assert np.allclose(res.pass_residuals, pres, rtol=1e-9, atol=0)
     assert oracle_mod.principal_cosines(res.basis.matrix, u).min() > 1 - 1e-10
     assert all(np.array_equal(a, b) for a, b in zip(res.final_omegas, om))
+
+
+def test_run_rapid_bit_reproducible():
+    """Two run_rapid calls on the same input give the same bits: GROUSE has no
+    floating-point atomics (deterministic split-K reductions, sparse terms
+    added in term order, residual norms reduced in a fixed order) and the
+    recovery noise is counter-based (reference: results depend only on the
+    seed, rapid.py / streams.py)."""
+    g = np.random.default_rng(5)
+    v, n1, n2 = 8192, 12, 20
+    vals = (g.standard_normal((v, n1 + n2)) * 0.5).astype(np.float32)
+    vals[:200, :n1] += 0.8
+    x = rmx.DataMatrix(vals, n1, n2)
+    rc = rmx.RunConfig(permutations=600, seed=11, engine="rapid", sample_rate=0.05, max_passes=4)
+    a = rmx.run_rapid(x, rc)
+    b = rmx.run_rapid(x, rc)
+    assert np.array_equal(a[1].basis.matrix, b[1].basis.matrix)
+    assert np.array_equal(a[0].maxima, b[0].maxima)
+    assert a[1].residual_std == b[1].residual_std and a[1].max_shift == b[1].max_shift
