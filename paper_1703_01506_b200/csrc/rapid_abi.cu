@@ -583,6 +583,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // each column's CG solution from the previous pass warm-starts its next
   // solve (same stopping rule |G w - b| <= 1e-13 |b|, far fewer iterations
   // once the basis settles)
+  if (getenv("RMX_CG_STATS")) cg_timing(1, nullptr);
   const bool warm = !getenv("RMX_GROUSE_COLD");
   if (warm) {
     RCUDA(wprev.alloc((size_t)ell * r, s));
@@ -806,11 +807,16 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     if (int rc = flush(hs.nterms)) return rc;
   }
   if (getenv("RMX_CG_STATS")) {
-    unsigned long long cs[2] = {0, 0};
+    unsigned long long cs[2] = {0, 0}, ph[6] = {0, 0, 0, 0, 0, 0};
     cudaStreamSynchronize(s);
     cg_stats(cs);
-    fprintf(stderr, "rmx cg: %llu solves, %llu iterations (%.1f per solve)\n", cs[0], cs[1],
-            cs[0] ? (double)cs[1] / (double)cs[0] : 0.0);
+    cg_timing(0, ph);
+    const double it = cs[1] ? (double)cs[1] : 1.0;
+    fprintf(stderr,
+            "rmx cg: %llu solves, %llu iterations (%.1f per solve); CTA 0 cycles per iteration: "
+            "block reduce %.0f, post %.0f, wait for peers %.0f, matvec %.0f\n",
+            cs[0], cs[1], cs[0] ? (double)cs[1] / (double)cs[0] : 0.0, ph[1] / it, ph[2] / it,
+            ph[3] / it, ph[4] / it);
   }
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(ubase, v, r, 0, &drift, stream, st)) return rc;

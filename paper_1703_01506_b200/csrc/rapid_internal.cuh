@@ -142,6 +142,7 @@ cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const doubl
                             cudaStream_t s);
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
+void cg_timing(int on, unsigned long long phase[6]);
 void cg_stats(unsigned long long out[2]);  // k_cg_solve (solves, iterations) so far
 // the gated Cholesky fallback after a non-converged cluster CG; pscratch:
 // chol_panel_scratch_doubles(r) doubles of global scratch for the panel

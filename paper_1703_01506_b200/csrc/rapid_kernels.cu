@@ -640,6 +640,11 @@ __device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank,
 // the recurrence residual; the result is then checked against the true
 // residual b - A x, and flag = 1 (Cholesky fallback) when that check or the
 // iteration cap fails.
+// RMX_CG_STATS phase clocks (CTA 0, thread 0, per iteration): local partial
+// dots, block reduction, post + wait for the peers, matvec, vector updates
+__device__ unsigned long long g_cg_phase[6];
+__device__ int g_cg_timing;
+
 __device__ __forceinline__ void cg_block_reduce3(double a, double b, double c, double* wsum,
                                                  double& A, double& B, double& C) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -671,8 +676,11 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, int
                                             double* wsum, uint64_t* bars, int par, uint32_t& xph,
                                             double& A, double& B, double& C) {
   const uint32_t me = cluster_ctarank();
+  const bool tm = g_cg_timing && me == 0 && threadIdx.x == 0;
+  const long long c0 = tm ? clock64() : 0;
   double ta, tb, tc;
   cg_block_reduce3(a, b, c, wsum, ta, tb, tc);
+  const long long c1 = tm ? clock64() : 0;
   const int tid = threadIdx.x;
   uint64_t* bar = bars + par;
   // this CTA receives every CTA's rows (rtot values when v is posted) and
@@ -691,8 +699,15 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, int
   // a sender can be at most one exchange ahead of this CTA: it needs this
   // CTA's next post before its own next-but-one wait, so the two parity
   // buffers/barriers never see data of two exchanges at once
+  const long long c2 = tm ? clock64() : 0;
   mbar_wait(bar, (xph >> par) & 1u);
   xph ^= 1u << par;
+  if (tm) {
+    const long long c3 = clock64();
+    atomicAdd(&g_cg_phase[1], (unsigned long long)(c1 - c0));  // block reduction
+    atomicAdd(&g_cg_phase[2], (unsigned long long)(c2 - c1));  // posting
+    atomicAdd(&g_cg_phase[3], (unsigned long long)(c3 - c2));  // waiting for the peers
+  }
   // every warp sums the NC partials with the same shuffle tree: the
   // same bits on every CTA (they all take the same convergence decision)
   static_assert(NC <= 32 && (NC & (NC - 1)) == 0, "power-of-2 cluster");
@@ -725,11 +740,17 @@ __device__ __forceinline__ void cg_matvec(const double* Gs, int nr, int r, const
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int i0 = wid; i0 < nr; i0 += 4 * W) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = lane; j < r; j += 32) {
-      const double f = full[j];
+    // warp-uniform trip count (a lane-dependent one left the warp diverged
+    // before the butterflies, which then compiled to the slow collective
+    // shuffle path: ~2,900 cycles per matvec)
+#pragma unroll 4
+    for (int j0 = 0; j0 < r; j0 += 32) {
+      const int j = j0 + lane;
+      const bool in = j < r;
+      const double f = in ? full[j] : 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (i0 + q * W < nr) acc[q] = fma(Gs[(size_t)(i0 + q * W) * r + j], f, acc[q]);
+        if (in && i0 + q * W < nr) acc[q] = fma(Gs[(size_t)(i0 + q * W) * r + j], f, acc[q]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -827,7 +848,10 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       converged = 1;
       break;
     }
+    const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
+    const long long m0 = tm ? clock64() : 0;
     cg_matvec(Gs, nr, r, full + used * r, nv);  // n = A m
+    if (tm) atomicAdd(&g_cg_phase[4], (unsigned long long)(clock64() - m0));
     double alpha, beta;
     if (it == 0) {
       beta = 0.0;
@@ -2434,6 +2458,11 @@ cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s) {
 
 void cg_stats(unsigned long long out[2]) {
   cudaMemcpyFromSymbol(out, g_cg_iters, sizeof(unsigned long long) * 2);
+}
+
+void cg_timing(int on, unsigned long long phase[6]) {
+  if (phase) cudaMemcpyFromSymbol(phase, g_cg_phase, sizeof(unsigned long long) * 6);
+  cudaMemcpyToSymbol(g_cg_timing, &on, sizeof(int));
 }
 
 size_t chol_panel_scratch_doubles(int r) { return (size_t)chol_panel_rows(r) * kPS; }
