@@ -764,9 +764,39 @@ __device__ __forceinline__ void cg_matvec(const double* Gs, int nr, int r, const
   __syncthreads();
 }
 
+// The same product with the CTA's rows of G held in REGISTERS (warp wid owns
+// rows wid + q W, lane l columns l + 32 jj): per iteration only the
+// exchanged vector is read from shared memory (the shared-memory version
+// re-read 25 x 400 doubles per matvec and was bound by shared-memory
+// bandwidth, ~2,600 cycles).  Same per-row order (lane-strided chains, then
+// the butterfly): same bits.
+template <int RL>
+__device__ __forceinline__ void cg_matvec_reg(const double (&g)[4][RL], int nr, int r,
+                                              const double* full, double* out) {
+  constexpr int W = kCgThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int jj = 0; jj < RL; ++jj) {
+    const int j = jj * 32 + lane;
+    const double f = j < r ? full[j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = fma(g[q][jj], f, acc[q]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (wid + q * W < nr) out[wid + q * W] = acc[q];
+  __syncthreads();
+}
+
 __device__ unsigned long long g_cg_iters[2];  // (solves, iterations): RMX_CG_STATS diagnostics
 
-template <int NC>
+template <int NC, int RL = 0>
 __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
                                                          double* __restrict__ w_out,
                                                          int32_t* __restrict__ flag,
@@ -778,7 +808,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   const uint32_t me = cluster_ctarank();
   const int r0 = (int)me * R, nr = max(0, min(R, r - r0));
   double* Gs = cs;                       // nr x r
-  double* full = Gs + (size_t)R * r;     // 2 x r: exchanged vector, by parity
+  double* full = Gs + (RL > 0 ? 0 : (size_t)R * r);  // 2 x r: exchanged vector, by parity
   double* vec = full + 2 * (size_t)r;    // 11 x R local rows
   double *x = vec, *rv = vec + R, *u = vec + 2 * R, *w = vec + 3 * R, *m = vec + 4 * R,
          *nv = vec + 5 * R, *z = vec + 6 * R, *q = vec + 7 * R, *sv = vec + 8 * R,
@@ -794,10 +824,29 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     mbar_init(&xbar[1], 1);
     fence_mbar_init();
   }
-  for (int e = tid; e < nr * r; e += kCgThreads) {
-    const int i = e / r, j = e % r;
-    Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
+  // RL > 0: the CTA's rows of G in registers (r <= 32 RL, at most 4 rows per warp)
+  constexpr int kRL = RL > 0 ? RL : 1;
+  double greg[4][kRL];
+  if constexpr (RL > 0) {
+    constexpr int W = kCgThreads / 32;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+      for (int jj = 0; jj < RL; ++jj) {
+        const int i = wid + qq * W, j = jj * 32 + lane;
+        greg[qq][jj] = (i < nr && j < r) ? G[(int64_t)(r0 + i) * ld + j] : 0.0;
+      }
+  } else {
+    for (int e = tid; e < nr * r; e += kCgThreads) {
+      const int i = e / r, j = e % r;
+      Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
+    }
   }
+  auto matvec = [&](const double* fv, double* outv) {
+    if constexpr (RL > 0) cg_matvec_reg<kRL>(greg, nr, r, fv, outv);
+    else cg_matvec(Gs, nr, r, fv, outv);
+  };
   double pb = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
     const double di = G[(int64_t)(r0 + i) * ld + r0 + i];
@@ -814,7 +863,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   if (x0) {  // r = b - A x0
     cg_exchange<NC>(x, nr, r0, r, full + par * r, pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
                     par, xph, BB, d0, d1);
-    cg_matvec(Gs, nr, r, full + par * r, nv);
+    matvec(full + par * r, nv);
     for (int i = tid; i < nr; i += kCgThreads) rv[i] -= nv[i];
     par ^= 1;
     __syncthreads();
@@ -825,7 +874,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   cg_exchange<NC>(u, nr, r0, r, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
                     par, xph, d0, d1, d1);
   if (!x0) BB = d0;
-  cg_matvec(Gs, nr, r, full + par * r, w);
+  matvec(full + par * r, w);
   par ^= 1;
   const double stop = tol * tol * BB;
   int converged = BB == 0.0;
@@ -850,7 +899,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     }
     const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
     const long long m0 = tm ? clock64() : 0;
-    cg_matvec(Gs, nr, r, full + used * r, nv);  // n = A m
+    matvec(full + used * r, nv);  // n = A m
     if (tm) atomicAdd(&g_cg_phase[4], (unsigned long long)(clock64() - m0));
     double alpha, beta;
     if (it == 0) {
@@ -880,7 +929,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
   cg_exchange<NC>(x, nr, r0, r, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
                     par, xph, d0, d1, d1);
-  cg_matvec(Gs, nr, r, full + par * r, nv);
+  matvec(full + par * r, nv);
   par ^= 1;
   double ptr = 0.0, pw = 0.0, pbw = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
@@ -2246,15 +2295,17 @@ size_t cg_smem_bytes(int r) { return cg_smem_bytes_c(r, cg_ctas()); }
 
 bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
 
-template <int C>
+template <int C, int RL = 0>
 cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* flag,
                               double* resid2, double tol, double* x0, cudaStream_t s) {
-  const size_t smem = cg_smem_bytes_c(r, C);
-  cudaError_t e = cudaFuncSetAttribute(k_cg_solve<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  // the register-resident variant keeps no copy of G in shared memory
+  const size_t smem =
+      cg_smem_bytes_c(r, C) - (RL > 0 ? (size_t)((r + C - 1) / C) * r * sizeof(double) : 0);
+  cudaError_t e = cudaFuncSetAttribute(k_cg_solve<C, RL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
-    e = cudaFuncSetAttribute(k_cg_solve<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cg_solve<C, RL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
@@ -2271,13 +2322,18 @@ cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* fl
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_cg_solve<C>, G, r, w_out, flag, resid2, tol, x0);
+  return cudaLaunchKernelEx(&cfg, k_cg_solve<C, RL>, G, r, w_out, flag, resid2, tol, x0);
 }
 
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
                             double tol, double* x0, cudaStream_t s) {
-  return cg_ctas() == 8 ? launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s)
-                        : launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s);
+  // rows of G in registers when each warp holds at most 4 rows of <= 416
+  // columns (RMX_CG_SMEM=1: the shared-memory variant)
+  const bool reg = r <= 13 * 32 && (r + kCgCtas - 1) / kCgCtas <= 4 * (kCgThreads / 32) &&
+                   !getenv("RMX_CG_SMEM");
+  if (cg_ctas() == 8) return launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s);
+  if (reg) return launch_cg_solve_c<kCgCtas, 13>(G, r, w_out, flag, resid2, tol, x0, s);
+  return launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
