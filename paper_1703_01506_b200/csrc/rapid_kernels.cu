@@ -1293,25 +1293,21 @@ __global__ void __launch_bounds__(256) k_sparse_terms_rows(
   const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (q >= k) return;
   const int32_t vox = __ldg(rows_sorted + q);
+  // branch-free lower-bound searches, the lane's two terms interleaved (a
+  // fixed number of dependent L2 loads instead of two early-exit loops)
   int pos[2] = {-1, -1};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int sterm = lane + 32 * h;
-    if (sterm < nt) {
-      const int32_t* di = d_idx + (int64_t)sterm * k;
-      int lo = 0, hi = k - 1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const int32_t x = __ldg(di + mid);
-        if (x == vox) {
-          pos[h] = mid;
-          break;
-        }
-        if (x < vox) lo = mid + 1;
-        else hi = mid - 1;
-      }
-    }
+  const int32_t* di0 = d_idx + (int64_t)lane * k;
+  const int32_t* di1 = d_idx + (int64_t)(lane + 32) * k;
+  const bool a0 = lane < nt, a1 = lane + 32 < nt;
+  int p0 = 0, p1 = 0;  // largest index with di[p] <= vox (0 if none)
+  int step = 1;
+  while (step * 2 <= k) step *= 2;
+  for (; step > 0; step >>= 1) {
+    if (a0 && p0 + step < k && __ldg(di0 + p0 + step) <= vox) p0 += step;
+    if (a1 && p1 + step < k && __ldg(di1 + p1 + step) <= vox) p1 += step;
   }
+  if (a0 && __ldg(di0 + p0) == vox) pos[0] = p0;
+  if (a1 && __ldg(di1 + p1) == vox) pos[1] = p1;
   double* o = out + (int64_t)q * ldo;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
