@@ -814,9 +814,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const double it = cs[1] ? (double)cs[1] : 1.0;
     fprintf(stderr,
             "rmx cg: %llu solves, %llu iterations (%.1f per solve); CTA 0 cycles per iteration: "
-            "block reduce %.0f, post %.0f, wait for peers %.0f, matvec %.0f\n",
-            cs[0], cs[1], cs[0] ? (double)cs[1] / (double)cs[0] : 0.0, ph[1] / it, ph[2] / it,
-            ph[3] / it, ph[4] / it);
+            "local dots %.0f, block reduce %.0f, post %.0f, wait for peers %.0f, matvec %.0f, "
+            "scalars + vector updates %.0f\n",
+            cs[0], cs[1], cs[0] ? (double)cs[1] / (double)cs[0] : 0.0, ph[0] / it, ph[1] / it,
+            ph[2] / it, ph[3] / it, ph[4] / it, ph[5] / it);
   }
   double drift = 0.0;
   if (int rc = rmx_orthonormalize(ubase, v, r, 0, &drift, stream, st)) return rc;

@@ -731,6 +731,71 @@ __device__ __forceinline__ void cg_exchange(const double* v, int nr, int r0, int
   __syncthreads();  // wsum reusable
 }
 
+// The exchange when all of the CTA's rows live in warp 0 (nr <= 32, the
+// register-resident variant): lane i computed row i, so warp 0 alone reduces
+// the partial dot products (shuffles: no shared memory, no block barrier)
+// and posts its rows and totals; every warp then waits on the parity
+// mbarrier and sums the NC partials as in cg_exchange (same bits: the block
+// reduction added only zeros to warp 0's butterfly).
+template <int NC>
+__device__ __forceinline__ void cg_exchange_w0(const double* v, int nr, int r0, int rtot,
+                                               double* full, double a, double b, double c,
+                                               double* slots, uint64_t* bars, int par,
+                                               uint32_t& xph, double& A, double& B, double& C) {
+  const uint32_t me = cluster_ctarank();
+  const bool tm = g_cg_timing && me == 0 && threadIdx.x == 0;
+  const long long c0 = tm ? clock64() : 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint64_t* bar = bars + par;
+  if (tid < 32) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+  }
+  const long long c1 = tm ? clock64() : 0;
+  if (tid == 0) mbar_expect_tx(bar, (uint32_t)(((v ? rtot : 0) + 3 * NC) * sizeof(double)));
+  if (tid < 32) {
+    if (v && lane < nr) {
+      const double vi = v[lane];
+#pragma unroll 4
+      for (int d = 0; d < NC; ++d) st_async_f64(full + r0 + lane, d, vi, bar);
+    }
+    if (lane < NC) {
+      st_async_f64(slots + 3 * me, lane, a, bar);
+      st_async_f64(slots + 3 * me + 1, lane, b, bar);
+      st_async_f64(slots + 3 * me + 2, lane, c, bar);
+    }
+  }
+  const long long c2 = tm ? clock64() : 0;
+  mbar_wait(bar, (xph >> par) & 1u);
+  xph ^= 1u << par;
+  if (tm) {
+    const long long c3 = clock64();
+    atomicAdd(&g_cg_phase[1], (unsigned long long)(c1 - c0));
+    atomicAdd(&g_cg_phase[2], (unsigned long long)(c2 - c1));
+    atomicAdd(&g_cg_phase[3], (unsigned long long)(c3 - c2));
+  }
+  static_assert(NC <= 32 && (NC & (NC - 1)) == 0, "power-of-2 cluster");
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  if (lane < NC) {
+    sa = slots[3 * lane];
+    sb = slots[3 * lane + 1];
+    sc = slots[3 * lane + 2];
+  }
+#pragma unroll
+  for (int o = NC / 2; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  }
+  A = __shfl_sync(0xffffffffu, sa, 0);
+  B = __shfl_sync(0xffffffffu, sb, 0);
+  C = __shfl_sync(0xffffffffu, sc, 0);
+}
+
 // out[i] = G_rows[i] . full: warp wid owns rows wid + q W (W warps), four
 // rows at a time as independent fma chains (the per-row order -- lane
 // strided, then the butterfly -- is unchanged, so are the bits)
@@ -859,10 +924,18 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   }
   cluster_sync();  // every CTA's exchange barriers are initialised before any st.async
   int par = 0;
+  auto xchg = [&](const double* vv, double pa, double pb2, double pc, double& A, double& B,
+                  double& C) {
+    if constexpr (RL > 0)
+      cg_exchange_w0<NC>(vv, vv ? nr : 0, r0, r, vv ? full + par * r : nullptr, pa, pb2, pc,
+                         slots + par * 3 * NC, xbar, par, xph, A, B, C);
+    else
+      cg_exchange<NC>(vv, vv ? nr : 0, r0, r, vv ? full + par * r : nullptr, pa, pb2, pc,
+                      slots + par * 3 * NC, wsum, xbar, par, xph, A, B, C);
+  };
   double BB, d0, d1;
   if (x0) {  // r = b - A x0
-    cg_exchange<NC>(x, nr, r0, r, full + par * r, pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
-                    par, xph, BB, d0, d1);
+    xchg(x, pb, 0.0, 0.0, BB, d0, d1);
     matvec(full + par * r, nv);
     for (int i = tid; i < nr; i += kCgThreads) rv[i] -= nv[i];
     par ^= 1;
@@ -871,8 +944,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   for (int i = tid; i < nr; i += kCgThreads) u[i] = rv[i] * dinv[i];
   __syncthreads();
   // w = A u (and |b|^2 when not yet reduced)
-  cg_exchange<NC>(u, nr, r0, r, full + par * r, x0 ? 0.0 : pb, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
-                    par, xph, d0, d1, d1);
+  xchg(u, x0 ? 0.0 : pb, 0.0, 0.0, d0, d1, d1);
   if (!x0) BB = d0;
   matvec(full + par * r, w);
   par ^= 1;
@@ -880,7 +952,9 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   int converged = BB == 0.0;
   double gamma_prev = 1.0, alpha_prev = 1.0;
   int it = 0;
+  const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
   for (; it < r && !converged; ++it) {
+    const long long d0 = tm ? clock64() : 0;
     double pg = 0.0, pd = 0.0, pr = 0.0;
     for (int i = tid; i < nr; i += kCgThreads) {
       pg += rv[i] * u[i];
@@ -888,19 +962,17 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       pr += rv[i] * rv[i];
       m[i] = w[i] * dinv[i];
     }
+    if (tm) atomicAdd(&g_cg_phase[0], (unsigned long long)(clock64() - d0));
     double GAM, DEL, RR;
-    cg_exchange<NC>(m, nr, r0, r, full + par * r, pg, pd, pr, slots + par * 3 * NC, wsum, xbar,
-                    par, xph, GAM, DEL, RR);
+    xchg(m, pg, pd, pr, GAM, DEL, RR);
     const int used = par;
     par ^= 1;  // every exchange flips the buffers (also on the way out)
     if (RR <= stop) {
       converged = 1;
       break;
     }
-    const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
-    const long long m0 = tm ? clock64() : 0;
-    matvec(full + used * r, nv);  // n = A m
-    if (tm) atomicAdd(&g_cg_phase[4], (unsigned long long)(clock64() - m0));
+    // the step scalars need only the exchanged sums: computed before the
+    // matvec so their fp64 divisions overlap its loads (same arithmetic)
     double alpha, beta;
     if (it == 0) {
       beta = 0.0;
@@ -913,6 +985,10 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     if (!(alpha == alpha) || alpha == 0.0) break;  // breakdown: not converged
     gamma_prev = GAM;
     alpha_prev = alpha;
+    const long long m0 = tm ? clock64() : 0;
+    matvec(full + used * r, nv);  // n = A m
+    const long long m1 = tm ? clock64() : 0;
+    if (tm) atomicAdd(&g_cg_phase[4], (unsigned long long)(m1 - m0));
     for (int i = tid; i < nr; i += kCgThreads) {
       z[i] = fma(beta, z[i], nv[i]);
       q[i] = fma(beta, q[i], m[i]);
@@ -923,12 +999,12 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
       u[i] = fma(-alpha, q[i], u[i]);
       w[i] = fma(-alpha, z[i], w[i]);
     }
+    if (tm) atomicAdd(&g_cg_phase[5], (unsigned long long)(clock64() - m1));
     // no barrier: the next iteration's partial sums read only this thread's
     // rows, and cg_exchange's block reduction syncs before the rows are posted
   }
   // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
-  cg_exchange<NC>(x, nr, r0, r, full + par * r, 0.0, 0.0, 0.0, slots + par * 3 * NC, wsum, xbar,
-                    par, xph, d0, d1, d1);
+  xchg(x, 0.0, 0.0, 0.0, d0, d1, d1);
   matvec(full + par * r, nv);
   par ^= 1;
   double ptr = 0.0, pw = 0.0, pbw = 0.0;
@@ -942,8 +1018,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     if (x0) x0[r0 + i] = x[i];
   }
   double TR, WW, BW;
-  cg_exchange<NC>(nullptr, 0, r0, r, nullptr, ptr, pw, pbw, slots + par * 3 * NC, wsum, xbar,
-                    par, xph, TR, WW, BW);
+  xchg(nullptr, ptr, pw, pbw, TR, WW, BW);
   if (me == 0 && tid == 0) {
     if (resid2) {
       resid2[0] = G[(int64_t)r * ld + r] - BW;
