@@ -878,22 +878,39 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
       return rc;
     return finish_host();
   }
+  // The pipeline's streams and events persist per host thread and device
+  // (creating 4 streams and ~2 chunks' worth of events cost a noticeable part
+  // of a 35 ms end-to-end call).  Reuse is safe: every call ends with the
+  // caller's stream waiting on all of them and a synchronisation.
   struct Streams {
+    int dev = -1;
     cudaStream_t cp = nullptr, pp = nullptr, k[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
-    ~Streams() {
-      for (cudaEvent_t e : ev) cudaEventDestroy(e);
-      for (cudaStream_t x : {cp, pp, k[0], k[1]})
-        if (x) cudaStreamDestroy(x);
-    }
+    size_t used = 0;
     cudaError_t event(cudaEvent_t* e) {
+      if (used < ev.size()) {
+        *e = ev[used++];
+        return cudaSuccess;
+      }
       cudaError_t r = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
-      if (r == cudaSuccess) ev.push_back(*e);
+      if (r == cudaSuccess) {
+        ev.push_back(*e);
+        ++used;
+      }
       return r;
     }
-  } S;
-  for (cudaStream_t* x : {&S.cp, &S.pp, &S.k[0], &S.k[1]})
-    RMX_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  };
+  static thread_local Streams* tl_streams = nullptr;  // never freed (process lifetime)
+  int cur_dev = 0;
+  RMX_CUDA(cudaGetDevice(&cur_dev));
+  if (!tl_streams || tl_streams->dev != cur_dev) {
+    tl_streams = new Streams();
+    tl_streams->dev = cur_dev;
+    for (cudaStream_t* x : {&tl_streams->cp, &tl_streams->pp, &tl_streams->k[0], &tl_streams->k[1]})
+      RMX_CUDA(cudaStreamCreateWithFlags(x, cudaStreamNonBlocking));
+  }
+  Streams& S = *tl_streams;
+  S.used = 0;
   const int nc = ws.lay.n_chunks;
   cudaEvent_t e0, e_ord, e_pdone, e_k[2];
   RMX_CUDA(S.event(&e0));
