@@ -22,6 +22,7 @@
 // fixed order (deterministic -- no atomics) and writes them.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "rapid_internal.cuh"
 #include "sm100.cuh"
@@ -268,8 +269,12 @@ __global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
 // K split for grids that cannot fill the GPU: up to 8 CTAs per tile while
 // the grid stays within ~4 CTAs per SM and every CTA keeps >= 32 K rows
 int pick_split(int64_t tiles, int kk) {
+  static const int cap = [] {
+    const char* e = getenv("RMX_DGEMM_SPLIT_MAX");  // experiments: cap the cluster split
+    return e ? std::max(1, std::min(8, atoi(e))) : 8;
+  }();
   int S = 1;
-  while (S < 8 && tiles * S * 2 <= 4 * 148 && kk / (2 * S) >= 2 * kBK) S *= 2;
+  while (S < cap && tiles * S * 2 <= 4 * 148 && kk / (2 * S) >= 2 * kBK) S *= 2;
   return S;
 }
 
