@@ -578,8 +578,6 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(mw.alloc(r, s));
   RCUDA(dots.alloc(kDeferCap, s));
   RCUDA(gst.alloc(1, s));
-  DevBuf<double> pscr;  // the gated Cholesky fallback's panel
-  RCUDA(pscr.alloc(chol_panel_scratch_doubles(r), s));
   // each column's CG solution from the previous pass warm-starts its next
   // solve (same stopping rule |G w - b| <= 1e-13 |b|, far fewer iterations
   // once the basis settles)
@@ -637,7 +635,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     prof.ev.resize((size_t)PhaseProf::kPh * PhaseProf::kN);
     for (auto& e : prof.ev) RCUDA(cudaEventCreate(&e));
   }
-  auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob) -> int {
+  // chol: solve with the batched Cholesky (a retry after the cluster CG did
+  // not converge, and the redraws of an ill-conditioned restriction); else
+  // the cluster CG, whose non-convergence halts the update for that retry --
+  // no gated fallback kernel in every update's chain
+  auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob, bool chol) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
     prof.cur = (prof.on && tglob >= PhaseProf::kLo && tglob < PhaseProf::kLo + PhaseProf::kN)
                    ? tglob : -1;
@@ -661,12 +663,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
     RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));  // (sums zeroed by the gather)
     prof.mark(s);
-    if (use_cg) {
+    const bool cg = use_cg && !chol;
+    if (cg) {
       RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,
                             warm ? wprev.p + (int64_t)i * r : nullptr, s));
       prof.mark(s);
       if (force_fallback) RCUDA(cudaMemsetAsync(flag.p, 0x01, 1, s));  // tests: flag = 1
-      RCUDA(launch_chol_if_flag(G.p, r, w.p, flag.p, sums.p + 4, pscr.p, s));
     } else {
       RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
       prof.mark(s);
@@ -677,7 +679,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     prof.mark(s);
     RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
                                didx.p, dval.p, cmat.p, wn.p,
-                               final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p, s));
+                               final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p,
+                               cg ? 1 : 0, s));
     RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, lu, k, vals.p, resid.p, sums.p, hg.p,
                           s));
     RCUDA(launch_defer_apply(M.p, Xf.p, Yf.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r,
@@ -719,7 +722,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
         halt_used[q] = 1;
         RCUDA(launch_force_halt(gst.p, tglob, s));
       }
-    if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob)) return rc;
+    if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob, false)) return rc;
     ++tglob;
     bool stop = false;
     // Process the checkpoint at tglob.  After a halt is resolved by a redraw,
@@ -733,6 +736,22 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       if (hs.overflow)
         return rset(st, RMX_E_CUDA, "GROUSE: more than %d deferred updates between flushes",
                     kDeferCap);
+      if (hs.halted && hs.cg_fail) {
+        // the cluster CG of update h did not converge: the same Omega again
+        // with the Cholesky solve (the updates after h were no-ops)
+        const int64_t h = hs.halt_step;
+        const int hp = (int)(h / ell), hi = (int)(h % ell);
+        GrouseState z{};
+        RCUDA(cudaMemcpyAsync(&gst.p->halted, &z.halted, sizeof(int), cudaMemcpyHostToDevice, s));
+        RCUDA(cudaMemcpyAsync(&gst.p->cg_fail, &z.cg_fail, sizeof(int), cudaMemcpyHostToDevice, s));
+        if (int rc = enqueue(hp, hi, omegas0 + ((int64_t)hp * ell + hi) * k, h, true)) return rc;
+        if (int rc = read_state(&hs)) return rc;
+        if (!hs.halted) {
+          tglob = h + 1;  // replay the skipped updates
+          continue;
+        }
+        // else: the Cholesky solve flagged the restriction -> redraw below
+      }
       if (hs.halted) {
         // ill-conditioned restriction at update h: redraw its Omega from the same
         // stream (lrmc.py:240-250); updates after h were no-ops and are replayed
@@ -745,7 +764,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
           RCUDA(cudaMemcpyAsync(idxbuf.p, host_idx.data(), k * sizeof(int32_t),
                                 cudaMemcpyHostToDevice, s));
           RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(int), s));  // clear `halted`
-          if (int rc = enqueue(hp, hi, idxbuf.p, h)) return rc;
+          if (int rc = enqueue(hp, hi, idxbuf.p, h, true)) return rc;
           if (int rc = read_state(&hs)) return rc;
           if (!hs.halted) {
             ok = true;

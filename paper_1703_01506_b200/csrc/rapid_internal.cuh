@@ -89,7 +89,9 @@ struct GrouseState {
   double pend_b;   // beta of the pending update (d = beta r on Omega)
   double aa;       // |p|^2 = w^T H w of the pending update
   int nterms;      // deferred sparse terms since the last flush (M-deferred GROUSE)
-  int pad2;
+  int cg_fail;     // the halt came from a cluster CG that did not converge (retry: Cholesky)
+  unsigned int hg_done;  // blocks of k_h_g_part finished (last-block reduction)
+  unsigned int da_done;  // blocks of k_defer_apply finished (last block counts the term)
 };
 // M-deferred GROUSE: U = U_base M + sum_s d_s c_s^T (d_s sparse on Omega_s)
 constexpr int kDeferCap = 64;  // terms between flushes (the host flushes every 64 updates)
@@ -124,7 +126,7 @@ cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* f
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
-                                 const double* hw, cudaStream_t s);
+                                 const double* hw, int cg_mode, cudaStream_t s);
 // M += a (M w) b^T, and the same term as factors M = I + X Yt (X: r x
 // kDeferCap, Yt: kDeferCap x r, column / row nterms)
 cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
@@ -144,11 +146,6 @@ cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
 void cg_timing(int on, unsigned long long phase[6]);
 void cg_stats(unsigned long long out[2]);  // k_cg_solve (solves, iterations) so far
-// the gated Cholesky fallback after a non-converged cluster CG; pscratch:
-// chol_panel_scratch_doubles(r) doubles of global scratch for the panel
-size_t chol_panel_scratch_doubles(int r);
-cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                                double* pscratch, cudaStream_t s);
 // K4 on tcgen05: operand preparation and the max decode
 cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
                             cudaStream_t s);

@@ -243,9 +243,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? (sizeof(T) == 4 ? 3 : 2) : 1) 
                                                    const double* __restrict__ rhs_ext = nullptr,
                                                    T* __restrict__ pscratch = nullptr,
                                                    int lookahead = 1) {
-  // pscratch (the gated GROUSE fallback): the panel in global memory, so the
-  // launch needs only a few KB of shared memory (its common case is to exit
-  // at the gate; a 100+ KB request would reconfigure the SMs every update)
+  // pscratch: the panel in global memory, so the launch needs only a few KB
+  // of shared memory
   // gate: run only when *gate != 0 (Cholesky fallback after a cluster-CG
   // solve that did not converge, decided on the device)
   // rhs_ext (refinement): G already holds the factor L; solve L L^T d =
@@ -1263,12 +1262,15 @@ __global__ void k_pred(const double* __restrict__ U, int64_t v, int r, const dou
 // st->aa) in g[r].
 constexpr int kHgSplit = 16;
 
-__global__ void k_h_g_part(int r, const GrouseState* __restrict__ st,
+__global__ void k_h_g_part(int r, GrouseState* __restrict__ st,
                            const double* __restrict__ ug, int64_t ldu, int k,
-                           const double* __restrict__ resid, double* __restrict__ gpart) {
+                           const double* __restrict__ resid, double* __restrict__ gpart,
+                           const double* __restrict__ hw, const double* __restrict__ vals,
+                           const double* __restrict__ sums, double* __restrict__ g) {
   pdl_wait();
   if (st->halted || !st->pending) return;
   __shared__ double part[8][33];
+  __shared__ bool last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + tx;
   const int rows = (k + kHgSplit - 1) / kHgSplit;
@@ -1285,37 +1287,38 @@ __global__ void k_h_g_part(int r, const GrouseState* __restrict__ st,
     for (int q = 0; q < 8; ++q) t += part[q][tx];
     gpart[(int64_t)blockIdx.y * r + c] = t;
   }
-}
-
-__global__ void k_h_g_fin(const double* __restrict__ hw, int r, const GrouseState* __restrict__ st,
-                          int k, const double* __restrict__ vals, const double* __restrict__ resid,
-                          const double* __restrict__ sums, const double* __restrict__ gpart,
-                          double* __restrict__ g) {
-  pdl_wait();
-  if (st->halted || !st->pending) return;
+  // the last block to finish forms g (was k_h_g_fin: one launch fewer)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned total = gridDim.x * gridDim.y;
+    last = atomicAdd(&st->hg_done, 1u) == total - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   const double a = st->pend_a, bb = st->pend_b;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < r) {
+  for (int cc = threadIdx.x; cc < r; cc += blockDim.x) {
     double t = 0.0;
 #pragma unroll
-    for (int q = 0; q < kHgSplit; ++q) t += gpart[(int64_t)q * r + c];
-    g[c] = a * hw[c] + bb * t;
+    for (int q = 0; q < kHgSplit; ++q) t += __ldcg(gpart + (int64_t)q * r + cc);
+    g[cc] = a * hw[cc] + bb * t;
   }
-  if (blockIdx.x == 0) {  // (ug w).resid over the k rows: the whole block (k / 256 loads each)
-    __shared__ double part[32];
-    const int lane = threadIdx.x & 31;
-    double pr = 0.0;
-    for (int i = threadIdx.x; i < k; i += blockDim.x) pr = fma(vals[i] - resid[i], resid[i], pr);
-    for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
-    if (lane == 0) part[threadIdx.x >> 5] = pr;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += part[q];
-      g[r] = a * a * st->aa + 2.0 * a * bb * t + bb * bb * sums[0];
-    }
+  __shared__ double kp[32];
+  const int lane = threadIdx.x & 31;
+  double pr = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) pr = fma(vals[i] - resid[i], resid[i], pr);
+  for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+  if (lane == 0) kp[threadIdx.x >> 5] = pr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += kp[q];
+    g[r] = a * a * st->aa + 2.0 * a * bb * t + bb * bb * sums[0];
+    st->hg_done = 0;  // ready for the next update
   }
 }
+
 
 __global__ void k_h_drift(const double* __restrict__ H, int r, double* __restrict__ out) {
   __shared__ double part[32];
@@ -1554,7 +1557,7 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
     const double* __restrict__ resid, const double* __restrict__ w, int r,
     int32_t* __restrict__ d_idx, double* __restrict__ d_val, double* __restrict__ cmat,
     double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw,
-    int nres) {
+    int nres, int cg_mode) {
   pdl_wait();
   __shared__ int skip, do_update, slot;
   __shared__ double sb, sinvw, sa, pnorm2;
@@ -1610,8 +1613,12 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
       st->halt_step = (int)step_index;
       skip = 1;
     } else if (*flag) {
+      // CG mode: the cluster CG did not converge -> the host re-runs this
+      // update with the Cholesky solve; Cholesky mode: a non-positive pivot
+      // (ill-conditioned restriction) -> the host redraws Omega
       st->halted = 1;
       st->halt_step = (int)step_index;
+      st->cg_fail = cg_mode;
       skip = 1;
     } else {
       const double resid_norm = sqrt(fmax(sums[0], 0.0));
@@ -1664,36 +1671,42 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
 __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
                               double* __restrict__ Yt, double* __restrict__ cmat,
                               double* __restrict__ H, const double* __restrict__ g,
-                              const GrouseState* __restrict__ st, const double* __restrict__ mw,
+                              GrouseState* __restrict__ st, const double* __restrict__ mw,
                               const double* __restrict__ dots, const double* __restrict__ b,
                               int r) {
   pdl_wait();
   if (st->halted || !st->pending) return;
   const int y = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= r) return;
   const double a = st->pend_a;
-  if (y < r) {
-    M[(int64_t)y * r + c] = fma(a * mw[y], b[c], M[(int64_t)y * r + c]);
-    // the same rank-1 term as factors: M = I + X Yt (column / row nterms)
-    const int nt = st->nterms;
-    if (c == 0) X[(int64_t)y * kDeferCap + nt] = a * mw[y];
-    if (y == 0) Yt[(int64_t)nt * r + c] = b[c];
-  } else if (y < 2 * r) {  // H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2)
-    const int i = y - r;
-    H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
-  } else if (y - 2 * r < st->nterms) {
-    const int sterm = y - 2 * r;
-    cmat[(int64_t)sterm * r + c] = fma(a * dots[sterm], b[c], cmat[(int64_t)sterm * r + c]);
+  const int nt = st->nterms;
+  if (c < r) {
+    if (y < r) {
+      M[(int64_t)y * r + c] = fma(a * mw[y], b[c], M[(int64_t)y * r + c]);
+      // the same rank-1 term as factors: M = I + X Yt (column / row nterms)
+      if (c == 0) X[(int64_t)y * kDeferCap + nt] = a * mw[y];
+      if (y == 0) Yt[(int64_t)nt * r + c] = b[c];
+    } else if (y < 2 * r) {  // H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2)
+      const int i = y - r;
+      H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
+    } else if (y - 2 * r < nt) {
+      const int sterm = y - 2 * r;
+      cmat[(int64_t)sterm * r + c] = fma(a * dots[sterm], b[c], cmat[(int64_t)sterm * r + c]);
+    }
+  }
+  // the last block to finish counts the new term (was k_defer_count: one
+  // launch fewer); every block read nterms / pending before its arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned total = gridDim.x * gridDim.y;
+    if (atomicAdd(&st->da_done, 1u) == total - 1) {
+      st->nterms = nt + 1;
+      st->pending = 0;
+      st->da_done = 0;
+    }
   }
 }
 
-__global__ void k_defer_count(GrouseState* __restrict__ st) {
-  pdl_wait();
-  if (st->halted || !st->pending) return;
-  st->nterms += 1;
-  st->pending = 0;
-}
 
 __global__ void k_force_halt(GrouseState* __restrict__ st, int64_t step) {
   if (st->halted) return;
@@ -2457,11 +2470,8 @@ cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const doubl
   (void)H;
   (void)wn;
   double* gpart = g + r + 1;  // kHgSplit x r scratch after g[0..r]
-  cudaError_t e = launch_pdl(k_h_g_part, dim3((unsigned)((r + 31) / 32), kHgSplit), dim3(256), 0, s,
-                             r, st, ug, ldu, k, resid, gpart);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(k_h_g_fin, dim3((unsigned)((r + 255) / 256)), dim3(256), 0, s, hw, r, st, k,
-                    vals, resid, sums, (const double*)gpart, g);
+  return launch_pdl(k_h_g_part, dim3((unsigned)((r + 31) / 32), kHgSplit), dim3(256), 0, s, r,
+                    const_cast<GrouseState*>(st), ug, ldu, k, resid, gpart, hw, vals, sums, g);
 }
 
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s) {
@@ -2556,19 +2566,17 @@ cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* f
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
-                                 const double* hw, cudaStream_t s) {
+                                 const double* hw, int cg_mode, cudaStream_t s) {
   const int nres = (k * 32 + 255) / 256;  // k_resid_defer_vec's residual blocks
   return launch_pdl(k_grouse_post_m, dim3(1), dim3(1024), 0, s, st, sums, flag, step, step_index,
-                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw, nres);
+                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw, nres, cg_mode);
 }
 
 cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
                                const double* hg, GrouseState* st, const double* mw,
                                const double* dots, const double* wn, int r, cudaStream_t s) {
-  cudaError_t e = launch_pdl(k_defer_apply, dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)),
-                             dim3(256), 0, s, M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(k_defer_count, dim3(1), dim3(1), 0, s, st);
+  return launch_pdl(k_defer_apply, dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)),
+                    dim3(256), 0, s, M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
 }
 
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
@@ -2592,14 +2600,6 @@ void cg_timing(int on, unsigned long long phase[6]) {
   cudaMemcpyToSymbol(g_cg_timing, &on, sizeof(int));
 }
 
-size_t chol_panel_scratch_doubles(int r) { return (size_t)chol_panel_rows(r) * kPS; }
-
-cudaError_t launch_chol_if_flag(double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                                double* pscratch, cudaStream_t s) {
-  const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(double);
-  return launch_pdl(k_chol_solve<512, double>, dim3(1), dim3(512), smem, s, G, r, w_out, flag,
-                    resid2, (const int32_t*)flag, (const double*)nullptr, pscratch, 0);
-}
 
 cudaError_t launch_trsm_lt(double* X, int64_t v, int r, const double* L, cudaStream_t s) {
   const int wpb = 4;
