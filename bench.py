@@ -516,14 +516,29 @@ def main():
     bf16_burst = float(pk.get("bf16_tflops", 0.0) or pk.get("bf16_tflops_sustained"))
     bf16_sust = float(pk.get("bf16_tflops_sustained", bf16_burst))
     balanced = 2 * cfg.n1 == n
+    i8_meas = None
     if i8:
-        # u8 x s8 -> s32 MMA over K = 2 kpad (z = 255 h + l digit planes), S only;
-        # B200 dense int8 = 2x dense bf16 (4.5 vs 2.25 P nominal); MEASURED_PEAKS
-        # has no int8 entry, so the peak is 2x its measured bf16 figure
+        # u8 x s8 -> s32 MMA over K = 2 kpad (z = 255 h + l digit planes), S only.
+        # Peak: the larger of 2x the measured bf16 burst (B200 dense int8 =
+        # 2x dense bf16 nominally) and the int8 GEMM measured on the box
+        # (cuBLASLt kind::i8, tools/measure_int8_peak.py ->
+        # profiles/r02_int8_peak.json; MEASURED_PEAKS has no int8 entry)
         kpad = -(-n // 16) * 16  # the [h | l] planes share one K extent 2 kpad (32-byte MMA K step)
         exec_flops = 2.0 * (2 * kpad) * v * local_L
         peak, peak_sust = 2.0 * bf16_burst, 2.0 * bf16_sust
         peak_kind = f"{pk_kind} bf16 dense burst x 2 (int8 dense)"
+        i8_meas = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_int8_peak.json")) as f:
+                pj = json.load(f)
+            i8_meas = {"burst": float(pj["int8_burst_tops"]),
+                       "sustained": float(pj["int8_sustained_tops"]),
+                       "source": "profiles/r02_int8_peak.json (cuBLASLt int8 GEMM on a B200)"}
+            if i8_meas["burst"] > peak:
+                peak, peak_sust = i8_meas["burst"], i8_meas["sustained"]
+                peak_kind = "measured int8 dense burst (cuBLASLt)"
+        except (OSError, KeyError, ValueError):
+            pass
         note = ("n1 == n2: t depends on S = G.Z only; K1 runs it as an exact int8 GEMM "
                 "(2 digit planes: 2 kpad int8 MACs per entry = 4 kpad ops ~ the algorithmic 4n)")
     else:
@@ -556,6 +571,9 @@ def main():
                 "frac_of_sustained": achieved / peak_sust,
                 "executed_tensor_tflops": exec_rate, "executed_frac": exec_rate / peak,
                 "tensor_path": "int8" if i8 else "fp16x2", "note": note}
+    if i8 and i8_meas:
+        roofline["int8_measured"] = dict(i8_meas, frac_of_burst=achieved / i8_meas["burst"],
+                                         frac_of_sustained=achieved / i8_meas["sustained"])
 
     # ---------------- e2e through the public API from host buffers -----------
     e2e = None

@@ -249,12 +249,15 @@ static NaiveLayout naive_layout_compute(int64_t v, int n, int n1, int64_t L, int
   lay.n_chunks = lay.n_ramp + (bulk + lay.tiles_per_chunk - 1) / lay.tiles_per_chunk;
   lay.grid = lay.cg * (int)std::min<int64_t>(n_clusters, (int64_t)lay.n_mtiles * lay.n_chunks);
 
+  lay.mwords = (lay.kpad + 31) / 32;
   size_t off = 0;
   lay.off_planes = off;
   // fp16: [4][v][kpad] halves (z_hi, q_hi, z_lo, q_lo); int8: [v][2 kpad] bytes
   off = align_up(off + (lay.i8 ? (size_t)2 * v * lay.kpad : (size_t)4 * v * lay.kpad * 2), 1024);
   lay.off_scale = off;  // int8: per-voxel dequantisation scale, padded to whole tiles
   off = align_up(off + (lay.i8 ? (size_t)lay.n_vtiles * lay.vt * 4 : 0), 256);
+  lay.off_gmask = off;
+  off = align_up(off + (size_t)lay.n_mtiles * tile_perms * lay.mwords * 4, 256);
   lay.off_cand = off;
   off = align_up(off + (size_t)lay.n_mtiles * tile_perms * lay.n_chunks * lay.groups * 32, 256);
   lay.off_susp = off;
@@ -329,6 +332,7 @@ struct Ws {
   __half* planes() const { return reinterpret_cast<__half*>(base + lay.off_planes); }
   uint8_t* planes8() const { return base + lay.off_planes; }
   float* scale() const { return reinterpret_cast<float*>(base + lay.off_scale); }
+  uint32_t* gmask() const { return reinterpret_cast<uint32_t*>(base + lay.off_gmask); }
   int4* cand() const { return reinterpret_cast<int4*>(base + lay.off_cand); }
   int32_t* susp() const { return reinterpret_cast<int32_t*>(base + lay.off_susp); }
   int32_t* cvox() const { return reinterpret_cast<int32_t*>(base + lay.off_cvox); }
@@ -554,7 +558,7 @@ int prep_rows(const double* x, int64_t v, int32_t n, int32_t n1, const Ws& ws, i
 int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t L,
                int32_t two_sided, float* dbg, void* workspace, size_t workspace_bytes,
                void* stream, rmx_status* st, rmx_naive_stats* stats, int chunk_begin = 0,
-               int chunk_end = -1) {
+               int chunk_end = -1, bool mask_ready = false) {
   clear_status(st);
   if (int rc = check_dims(v, n, n1, L, st)) return rc;
   Ws ws;
@@ -571,8 +575,13 @@ int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t 
   const double beta = -c * (1.0 / (d1 * d1 * (d1 - 1.0)) + 1.0 / (d2 * d2 * (d2 - 1.0)));
   const double gamma = c * T / (d2 * (d2 - 1.0));
   const double bmax = std::fabs(alpha) * T + std::fabs(beta) * d1 * T + gamma;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!mask_ready)
+    RMX_CUDA(launch_group_mask(orders, L, (int64_t)ws.lay.n_mtiles * kTileM * ws.lay.cg, n, n1,
+                               ws.lay.mwords, ws.gmask(), s));
   TfillArgs a{};
-  a.orders = orders;
+  a.gmask = ws.gmask();
+  a.mwords = ws.lay.mwords;
   a.L = L;
   a.v = v;
   a.n = n;
@@ -596,7 +605,7 @@ int tfill_impl(int64_t v, int32_t n, int32_t n1, const int16_t* orders, int64_t 
   a.best_t = ws.best();
   a.counters = ws.counters();
   a.dbg_t = dbg;
-  RMX_CUDA(launch_tfill_tc(ws.lay, a, ws.planes(), two_sided, static_cast<cudaStream_t>(stream)));
+  RMX_CUDA(launch_tfill_tc(ws.lay, a, ws.planes(), two_sided, s));
   if (stats) {
     stats->chunks = ws.lay.n_chunks;
     stats->grid = ws.lay.grid;
@@ -938,7 +947,12 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
     RMX_CUDA(cudaEventRecord(e_ord, S.cp));
   }
   if (int rc = prep_init(ws, n, n1, L, S.pp, st)) return rc;
-  for (cudaStream_t x : {S.k[0], S.k[1]}) RMX_CUDA(cudaStreamWaitEvent(x, e_ord, 0));
+  // the labels' bit rows, once, ahead of every chunk's K1 (both K1 streams)
+  RMX_CUDA(cudaStreamWaitEvent(S.k[0], e_ord, 0));
+  RMX_CUDA(launch_group_mask(orders_dev, L, (int64_t)ws.lay.n_mtiles * kTileM * ws.lay.cg, n, n1,
+                             ws.lay.mwords, ws.gmask(), S.k[0]));
+  RMX_CUDA(cudaEventRecord(e_ord, S.k[0]));
+  RMX_CUDA(cudaStreamWaitEvent(S.k[1], e_ord, 0));
   // chunk c: its rows' copy (after the host read them, for a file), then K0
   // and K1 on them; enqueued chunk by chunk so a file's reads overlap the
   // copies and the engine work of the chunks before
@@ -966,7 +980,7 @@ int naive_host_impl(const double* x_host, const float* x_host32, float* x32_dev,
     cudaStream_t ks = S.k[c & 1];
     RMX_CUDA(cudaStreamWaitEvent(ks, e_prep[c], 0));
     if (int rc = tfill_impl(v, n, n1, orders_dev, L, two_sided, nullptr, workspace,
-                            workspace_bytes, ks, st, stats, c, c + 1))
+                            workspace_bytes, ks, st, stats, c, c + 1, /*mask_ready=*/true))
       return rc;
   }
   RMX_CUDA(launch_const_reduce(x_dev, v, n, n1, ws.cvox(), ws.counters(), ws.cinfo(), S.pp));

@@ -106,8 +106,9 @@ struct NaiveLayout {
   int cg;             // CTAs per MMA tile (tcgen05 cta_group): 1 or 2
   int i8;             // exact int8 MMA on 16-bit fixed-point Z (balanced groups)
   int vt;             // voxels per tile: 256 (S-only, n1 == n2) or 128 (S | Q)
-  size_t off_planes, off_scale, off_cand, off_susp, off_cvox, off_overflow, off_best, off_const,
-      off_counters;
+  int mwords;         // 32-bit words of a group-1 indicator row (kpad bits)
+  size_t off_planes, off_scale, off_gmask, off_cand, off_susp, off_cvox, off_overflow, off_best,
+      off_const, off_counters;
   size_t total;
 };
 
@@ -133,7 +134,12 @@ struct PrepArgs {
 };
 
 struct TfillArgs {
-  const int16_t* orders;  // [L][n]
+  // group-1 indicator of every permutation as a bit row ([n_mtiles * tile][mwords]
+  // u32, bit k of row p = subject k in orders[p, :n1]; zero rows past L):
+  // 52 B per permutation at n = 400 instead of the 800 B order row, so the
+  // labels stay L2-resident across the chunk sweep (launch_group_mask)
+  const uint32_t* gmask;
+  int mwords;
   int64_t L, v;
   int n, n1, kpad, nk16;
   int n_vtiles, n_mtiles, n_chunks, tiles_per_chunk;
@@ -194,6 +200,8 @@ cudaError_t launch_pairs(const double* x, int64_t v, int n, int n1, const int16_
                          int32_t* deg_out, cudaStream_t s);
 
 // tfill_tc.cu
+cudaError_t launch_group_mask(const int16_t* orders, int64_t L, int64_t rows, int n, int n1,
+                              int mwords, uint32_t* gmask, cudaStream_t s);
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
                             int two_sided, cudaStream_t s);
 cudaError_t launch_complete_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,

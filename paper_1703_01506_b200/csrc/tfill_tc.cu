@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], EPI_WARPS * CG);
     }
-    mbar_init(afull, kTileM * CG);
+    mbar_init(afull, kTileM * CG * (MODE == 1 ? 1 : GROUPS));
     fence_mbar_init();
     tma_prefetch(&pmap);
   }
@@ -581,31 +581,48 @@ __global__ void __launch_bounds__(64 + 32 * EPI_WARPS, 1)
       chunk_range(a, chunk, t0, t1);
       const int64_t p = ((int64_t)mtile * CG + rank) * kTileM + row;
       const bool prow = p < a.L;
-      if (grp == 0) {
-        // A row `row`: G[p, k] = 1 for k in orders[p, :n1] (canonical K-major
-        // no-swizzle layout: 8x8 core matrices, LBO = 128 B, SBO = kpad*16 B)
-        // (core matrix = 8 rows x 16 bytes: 8 fp16 or 16 u8 K-elements)
-        // (int8: K runs over [h | l], A row = [255 G | G])
-        constexpr int EPC = 16 / ELT;  // K elements per core-matrix row
+      if (MODE == 1) {
+        if (grp == 0) {  // A row = W[p] (fp16, kpad halves = kpad / 8 core-matrix rows)
+          uint8_t* rbase = a_mem + (row >> 3) * (kext * 8 * ELT) + (row & 7) * 16;
+          const uint4* src = reinterpret_cast<const uint4*>(a.wA + p * (int64_t)a.kpad);
+          for (int kc = 0; kc < a.kpad / 8; ++kc)
+            *reinterpret_cast<uint4*>(rbase + kc * 128) = prow ? src[kc] : make_uint4(0, 0, 0, 0);
+          fence_proxy_async_smem();
+          if (CG == 2) mbar_arrive_cluster(afull, 0);
+          else mbar_arrive(afull);
+        }
+      } else {
+        // A row `row` from the permutation's indicator bits (gmask; zero rows
+        // past L), canonical K-major no-swizzle layout: 8x8 core matrices,
+        // LBO = 128 B, SBO = kext*8*ELT; a core-matrix row is 16 bytes = 16
+        // u8 / 8 fp16 K-elements.  int8: K runs over [h | l], A row =
+        // [255 G | G].  Every epilogue group expands its share of the row's
+        // core-matrix columns (kc = grp, grp + GROUPS, ...).
         uint8_t* rbase = a_mem + (row >> 3) * (kext * 8 * ELT) + (row & 7) * 16;
-        for (int kc = 0; kc < kext / EPC; ++kc)
-          *reinterpret_cast<uint4*>(rbase + kc * 128) = make_uint4(0, 0, 0, 0);
-        if (MODE == 1) {  // A row = W[p] (fp16, kpad halves = kpad / 8 core-matrix rows)
-          if (prow) {
-            const uint4* src = reinterpret_cast<const uint4*>(a.wA + p * (int64_t)a.kpad);
-            for (int kc = 0; kc < a.kpad / 8; ++kc) *reinterpret_cast<uint4*>(rbase + kc * 128) = src[kc];
+        const uint32_t* mrow = a.gmask + p * (int64_t)a.mwords;
+        if (I8) {
+          const int nkc = a.kpad / 16;  // 16 indicator bits per core-matrix row
+          for (int kc = grp; kc < nkc; kc += GROUPS) {
+            const uint32_t bits = (mrow[kc >> 1] >> ((kc & 1) * 16)) & 0xFFFFu;
+            uint32_t e[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)  // 4 bits -> 4 bytes of 0 / 1
+              e[q] = (((bits >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+            *reinterpret_cast<uint4*>(rbase + kc * 128) =
+                make_uint4(e[0] * 255u, e[1] * 255u, e[2] * 255u, e[3] * 255u);
+            *reinterpret_cast<uint4*>(rbase + (nkc + kc) * 128) = make_uint4(e[0], e[1], e[2], e[3]);
           }
-        } else if (prow) {
-          const int16_t* ord = a.orders + p * a.n;
-          for (int i = 0; i < a.n1; ++i) {
-            const int k = ord[i];
-            if (I8) {
-              rbase[(k / EPC) * 128 + (k % EPC)] = 255u;
-              const int k2 = a.kpad + k;
-              rbase[(k2 / EPC) * 128 + (k2 % EPC)] = 1u;
-            } else {
-              *reinterpret_cast<uint16_t*>(rbase + (k / EPC) * 128 + (k % EPC) * 2) = 0x3C00u;
+        } else {
+          const int nkc = a.kpad / 8;  // 8 indicator bits per core-matrix row
+          for (int kc = grp; kc < nkc; kc += GROUPS) {
+            const uint32_t bits = (mrow[kc >> 2] >> ((kc & 3) * 8)) & 0xFFu;
+            uint32_t e[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // 2 bits -> two fp16 0 / 1
+              const uint32_t b2 = (bits >> (2 * q)) & 3u;
+              e[q] = ((b2 & 1u) | ((b2 & 2u) << 15)) * 0x3C00u;
             }
+            *reinterpret_cast<uint4*>(rbase + kc * 128) = make_uint4(e[0], e[1], e[2], e[3]);
           }
         }
         fence_proxy_async_smem();
@@ -957,6 +974,39 @@ cudaError_t launch_complete_tc(const NaiveLayout& lay, const TfillArgs& a, const
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   return two_sided ? dispatch_complete<true>(lay, a, map, s) : dispatch_complete<false>(lay, a, map, s);
+}
+
+// Group-1 indicator bit rows of the labels (K1's A operand source): one warp
+// per permutation row; rows in [L, rows) are zero (the tail of the last
+// permutation tile).  Reads the L x n int16 orders once (80 MB at config 4).
+__global__ void k_group_mask(const int16_t* __restrict__ orders, int64_t L, int64_t rows, int n,
+                             int n1, int mwords, uint32_t* __restrict__ gmask) {
+  __shared__ uint32_t words[8][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* my = words[w];
+  for (int64_t p = (int64_t)blockIdx.x * 8 + w; p < rows; p += (int64_t)gridDim.x * 8) {
+    for (int j = lane; j < mwords; j += 32) my[j] = 0u;
+    __syncwarp();
+    if (p < L) {
+      const int16_t* ord = orders + p * n;
+      for (int i = lane; i < n1; i += 32) {
+        const int k = ord[i];
+        atomicOr(&my[k >> 5], 1u << (k & 31));
+      }
+    }
+    __syncwarp();
+    for (int j = lane; j < mwords; j += 32) gmask[p * mwords + j] = my[j];
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_group_mask(const int16_t* orders, int64_t L, int64_t rows, int n, int n1,
+                              int mwords, uint32_t* gmask, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (mwords > 32) return cudaErrorInvalidValue;  // n > 1024: never a tensor-core tile
+  const int blocks = (int)std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  k_group_mask<<<blocks, 256, 0, s>>>(orders, L, rows, n, n1, mwords, gmask);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tfill_tc(const NaiveLayout& lay, const TfillArgs& a, const __half* planes,
