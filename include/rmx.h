@@ -399,6 +399,18 @@ int rmx_lsq_solve_tc(const double *u, int64_t ldu, int64_t v, int32_t r, const i
                      void *workspace, size_t workspace_bytes, int32_t *stats, void *stream,
                      rmx_status *st);
 
+/* rmx_lsq_solve_tc with an adaptive second refinement step (RapidPT
+ * recovery, rapid.py:198-205): every system takes one fp64 refinement step;
+ * a system whose first correction is within settle_tol |w| is settled (its w
+ * is within ~settle_tol^2 |w| of the normal-equations solution: 1e-8 at the
+ * engine's 1e-4), the others take the second step and, if still unsettled,
+ * the fp64 Gram path.  settle_tol = 0 is rmx_lsq_solve_tc. */
+int rmx_lsq_solve_tc_settle(const double *u, int64_t ldu, int64_t v, int32_t r,
+                            const int32_t *idx, int32_t k, const double *vals, int64_t B,
+                            double *w_out, int32_t *flag_out, void *workspace,
+                            size_t workspace_bytes, int32_t *stats, double settle_tol,
+                            void *stream, rmx_status *st);
+
 /* Completion + residual + max (rapid.py:198-205): for each of B columns,
  *   max_out[b] = max_j op(W[b] . U[j] + sigma * z(perm_base + b, j)) + mu,
  * op = |.| when two_sided.  z is Philox N(0,1) unless znoise (B x v fp32) is

@@ -93,6 +93,7 @@ EXPORTS = (
     "rmx_lsq_workspace_bytes",
     "rmx_lsq_solve",
     "rmx_lsq_solve_tc",
+    "rmx_lsq_solve_tc_settle",
     "rmx_lsq_solve_exact",
     "rmx_track_update",
     "rmx_normal_tables_set",
@@ -186,6 +187,8 @@ _SIGS = {
                              _vp, _SP], ctypes.c_int),
     "rmx_lsq_solve_tc": ([_vp, _i64, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp,
                           _SP], ctypes.c_int),
+    "rmx_lsq_solve_tc_settle": ([_vp, _i64, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _sz,
+                                 _vp, ctypes.c_double, _vp, _SP], ctypes.c_int),
     "rmx_lsq_solve": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp, _SP],
                       ctypes.c_int),
     "rmx_lsq_solve_exact": ([_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _SP],

@@ -328,11 +328,13 @@ __global__ void __launch_bounds__(32 * kRWarps, 2) k_lsq_resid(const double* __r
                                                             const int32_t* __restrict__ idx,
                                                             int k, const double* __restrict__ vals,
                                                             const double* __restrict__ W,
-                                                            double* __restrict__ gout) {
+                                                            double* __restrict__ gout,
+                                                            const int32_t* __restrict__ active) {
   extern __shared__ double rsm[];  // w[r] | part[kRWarps][r]
   double* w = rsm;
   double* part = rsm + r;
   const int64_t b = blockIdx.x;
+  if (active && active[b] == 0) return;  // settled system: no refinement step
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < r; i += blockDim.x) w[i] = W[b * r + i];
   __syncthreads();
@@ -482,7 +484,7 @@ cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t
 
 cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
                              const double* vals, const double* W, int64_t B, double* g,
-                             cudaStream_t s) {
+                             cudaStream_t s, const int32_t* active) {
   const size_t smem = (size_t)(1 + kRWarps) * r * sizeof(double);
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -491,7 +493,8 @@ cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t*
     for (int64_t b0 = 0; b0 < B; b0 += 65535) {
       const int64_t cnt = std::min<int64_t>(65535, B - b0);
       kern<<<(unsigned)cnt, 32 * kRWarps, smem, s>>>(U, ldu, r, idx + b0 * k, k, vals + b0 * k,
-                                                      W + b0 * r, g + b0 * r);
+                                                      W + b0 * r, g + b0 * r,
+                                                      active ? active + b0 : nullptr);
     }
     return cudaGetLastError();
   };

@@ -275,10 +275,13 @@ int rmx_track_update(double* u, int64_t v, int32_t r, const int32_t* idx, int32_
   return RMX_OK;
 }
 
-int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_t* idx,
-                     int32_t k, const double* vals, int64_t B, double* w_out, int32_t* flag_out,
-                     void* workspace, size_t workspace_bytes, int32_t* stats, void* stream,
-                     rmx_status* st) {
+}  // extern "C"
+
+namespace {
+int lsq_tc_impl(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_t* idx, int32_t k,
+                const double* vals, int64_t B, double* w_out, int32_t* flag_out, void* workspace,
+                size_t workspace_bytes, int32_t* stats, double settle_tol, void* stream,
+                rmx_status* st) {
   rclear(st);
   if (r < 1 || k < r || B < 1 || !vals || !w_out || !idx || v < 1)
     return rset(st, RMX_E_USAGE, "%d observed rows cannot determine %d coefficients", k, r);
@@ -291,6 +294,8 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
   // G~ in fp32 (its precision is the tensor cores' anyway): half the bytes,
   // a twice-as-fast factor; RMX_GRAM_CHOL64=1 keeps the factor in fp64
   const bool f32 = !getenv("RMX_GRAM_CHOL64");
+  const char* rs = getenv("RMX_REFINE_STEPS");
+  const bool force2 = settle_tol <= 0.0 || (rs && atoi(rs) >= 2);
   const size_t per = f32 ? gram_bytes(r) / 2 : gram_bytes(r);
   int64_t chunk = (int64_t)((workspace_bytes > 256 ? workspace_bytes - 256 : 0) /
                             (per + 4 * sizeof(double)));
@@ -324,13 +329,33 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
     } else {
       RCUDA(launch_chol_solve(G, r, cnt, wb, flags.p + b0, nrm, s));
     }
-    // two refinement steps with the fp64 residual (contraction ~ cond * 1e-5 each)
-    for (int it = 0; it < 2; ++it) {
+    // fp64 refinement: step 1 on every system.  settle_tol > 0: a first
+    // correction within settle_tol |w| means the fp32 solve's error (and the
+    // step's contraction) is about that size, so the refined w is within
+    // ~settle_tol^2 |w| of the solution and the system is settled; only the
+    // rest take a second step.  settle_tol = 0 (rmx_lsq_solve_tc): two steps
+    // on every system (w to ~1e-12).  RMX_REFINE_STEPS=2 forces two steps.
+    if (f32) {
       RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
-      if (f32)
-        RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0,
-                                      s));
-      else RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s,
+                                    nullptr, force2 ? 0.0 : settle_tol));
+      if (getenv("RMX_LSQ_STATS")) {  // diagnostics: systems taking the second step
+        std::vector<int32_t> h((size_t)cnt);
+        RCUDA(cudaMemcpyAsync(h.data(), nconv.p + b0, (size_t)cnt * 4, cudaMemcpyDeviceToHost, s));
+        RCUDA(cudaStreamSynchronize(s));
+        int64_t c2 = 0;
+        for (int32_t x : h) c2 += x != 0;
+        fprintf(stderr, "[lsq_tc] batch of %lld systems: %lld take a second refinement step\n",
+                (long long)cnt, (long long)c2);
+      }
+      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s, nconv.p + b0));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s,
+                                    nconv.p + b0, 1e-7));
+    } else {
+      for (int it = 0; it < 2; ++it) {
+        RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
+        RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
+      }
     }
   }
   // systems whose fp32 factor was singular or whose refinement has not
@@ -361,6 +386,31 @@ int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const i
   }
   RCUDA(cudaStreamSynchronize(s));
   return RMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rmx_lsq_solve_tc(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_t* idx,
+                     int32_t k, const double* vals, int64_t B, double* w_out, int32_t* flag_out,
+                     void* workspace, size_t workspace_bytes, int32_t* stats, void* stream,
+                     rmx_status* st) {
+  return lsq_tc_impl(u, ldu, v, r, idx, k, vals, B, w_out, flag_out, workspace, workspace_bytes,
+                     stats, 0.0, stream, st);
+}
+
+int rmx_lsq_solve_tc_settle(const double* u, int64_t ldu, int64_t v, int32_t r,
+                            const int32_t* idx, int32_t k, const double* vals, int64_t B,
+                            double* w_out, int32_t* flag_out, void* workspace,
+                            size_t workspace_bytes, int32_t* stats, double settle_tol,
+                            void* stream, rmx_status* st) {
+  if (!(settle_tol >= 0.0 && settle_tol < 1e-2)) {
+    rclear(st);
+    return rset(st, RMX_E_USAGE, "settle_tol %g outside [0, 1e-2)", settle_tol);
+  }
+  return lsq_tc_impl(u, ldu, v, r, idx, k, vals, B, w_out, flag_out, workspace, workspace_bytes,
+                     stats, settle_tol, stream, st);
 }
 
 int rmx_complete_max(const float* u32, int64_t v, int32_t r, const float* w32, int64_t B,

@@ -60,8 +60,11 @@ cudaError_t launch_chol_cluster_f32(float* G, int r, int64_t B, double* rhs_out,
                                     int32_t* flag, cudaStream_t s);
 cudaError_t launch_chol_solve_f32(float* G, int r, int64_t B, double* w_out, int32_t* flag,
                                   cudaStream_t s);
+// w += (L L^T)^-1 rhs; nconv[b] = |correction| > tol |w|.  active (optional):
+// only systems with active[b] != 0 are touched.
 cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,
-                                    double* w_inout, int32_t* nconv, cudaStream_t s);
+                                    double* w_inout, int32_t* nconv, cudaStream_t s,
+                                    const int32_t* active = nullptr, double tol = 1e-7);
 // Tensor-core Gram (gram_tc.cu): G_b ~ [U[idx_b] | vals_b]^T [U[idx_b] | vals_b]
 // (lower triangle, (r+1)^2 each) from fp16 hi/lo planes of U (gram_planes),
 // fp32-accurate; refined to fp64 accuracy by lsq_resid + launch_chol_resolve
@@ -76,7 +79,7 @@ cudaError_t launch_gram_tc(const __half* planes, int64_t v, int r, const int32_t
 // g_b = U_Omega^T (t - U_Omega w_b) in fp64 (one gather of the rows)
 cudaError_t launch_lsq_resid(const double* U, int64_t ldu, int r, const int32_t* idx, int k,
                              const double* vals, const double* W, int64_t B, double* g,
-                             cudaStream_t s);
+                             cudaStream_t s, const int32_t* active = nullptr);
 // GROUSE step state kept on the device, so the update loop runs without a
 // host round trip per update (decisions by k_grouse_post_m).
 struct GrouseState {

@@ -2225,11 +2225,13 @@ constexpr int kTrsvWarps = 4;
 __global__ void __launch_bounds__(32 * kTrsvWarps) k_trsv_warp(const float* __restrict__ G, int r,
                                                                 int64_t B, const double* __restrict__ rhs,
                                                                 double* __restrict__ w_inout,
-                                                                int32_t* __restrict__ nconv) {
+                                                                int32_t* __restrict__ nconv,
+                                                                const int32_t* active, double tol2) {
   extern __shared__ __align__(16) float ty[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * kTrsvWarps + wid;
   if (b >= B) return;
+  if (active && active[b] == 0) return;  // settled earlier: w and nconv[b] stay
   const int ld = r + 1;
   const int rp = (r + 31) / 32 * 32;
   float* y = ty + (size_t)wid * rp;
@@ -2307,11 +2309,12 @@ __global__ void __launch_bounds__(32 * kTrsvWarps) k_trsv_warp(const float* __re
     dd += __shfl_xor_sync(0xffffffffu, dd, o);
     ww += __shfl_xor_sync(0xffffffffu, ww, o);
   }
-  if (lane == 0 && nconv) nconv[b] = (dd > 1e-14 * ww) ? 1 : 0;
+  if (lane == 0 && nconv) nconv[b] = (dd > tol2 * ww) ? 1 : 0;
 }
 
 cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rhs,
-                                    double* w_inout, int32_t* nconv, cudaStream_t s) {
+                                    double* w_inout, int32_t* nconv, cudaStream_t s,
+                                    const int32_t* active, double tol) {
   if (!getenv("RMX_TRSV_CTA")) {  // one warp per system (RMX_TRSV_CTA=1: the CTA version)
     const int rp = (r + 31) / 32 * 32;
     const size_t smem = (size_t)kTrsvWarps * rp * sizeof(float);
@@ -2321,7 +2324,7 @@ cudaError_t launch_chol_resolve_f32(float* G, int r, int64_t B, const double* rh
       if (e != cudaSuccess) return e;
     }
     k_trsv_warp<<<(unsigned)((B + kTrsvWarps - 1) / kTrsvWarps), 32 * kTrsvWarps, smem, s>>>(
-        G, r, B, rhs, w_inout, nconv);
+        G, r, B, rhs, w_inout, nconv, active, tol * tol);
     return cudaGetLastError();
   }
   const size_t smem = ((size_t)kPW * kPS + kPW + (size_t)r) * sizeof(float);

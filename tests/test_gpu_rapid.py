@@ -269,6 +269,36 @@ def test_tensor_core_gram_lsq_matches_fp64(monkeypatch, chol, v, r, k, B):
     assert stats[1] <= 1, stats  # at most the singular system was re-solved in fp64
 
 
+@pytest.mark.parametrize("v,r,k,B", [(20000, 400, 1836, 160), (6000, 100, 700, 300)])
+def test_tensor_core_gram_lsq_settle_mode(v, r, k, B):
+    """rmx_lsq_solve_tc_settle (RapidPT recovery's mode): the second fp64
+    refinement step only where the first correction exceeds 1e-4 |w|; every
+    settled system is within ~1e-8 |w| of the fp64 solution (asserted at 1e-7),
+    flags equal the fp64 path's."""
+    import torch
+
+    from paper_1703_01506_b200 import rapid_engine as re
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(v * 7 + r)
+    u = np.linalg.qr(rng.standard_normal((v, r)))[0]
+    idx = np.stack([np.sort(rng.choice(v, k, replace=False)) for _ in range(B)]).astype(np.int32)
+    vals = rng.standard_normal((B, k)) * 3.0 + (u[idx] @ rng.standard_normal(r)) * 40.0
+    ud = torch.from_numpy(u).to(dev)
+    idd = torch.from_numpy(idx).to(dev)
+    vd = torch.from_numpy(vals).to(dev)
+    W, F, stats = re._lsq_tc(ud, r, idd, k, vd, B, settle=1e-4)
+    W0, F0, _ = re._lsq(ud, r, idd, k, vd, B)
+    torch.cuda.synchronize()
+    W, W0, F, F0 = W.cpu().numpy(), W0.cpu().numpy(), F.cpu().numpy(), F0.cpu().numpy()
+    assert stats[0] == 1 and stats[1] == 0
+    assert np.array_equal(F, F0)
+    err = np.abs(W - W0).max(axis=1) / np.abs(W0).max(axis=1)
+    assert err.max() < 1e-7, err.max()
+    with pytest.raises(Exception):
+        re._lsq_tc(ud, r, idd, k, vd, B, settle=0.5)
+
+
 def test_run_rapid_prefetched_recovery_and_pending_basis():
     """run_rapid computes recovery's basis-independent inputs during training
     and copies the basis to the host behind recovery (rapid_engine.py

@@ -39,26 +39,20 @@ def main():
     for nm in ("_lsq_tc", "_complete_max"):
         if hasattr(re, nm):
             wrap(re, nm)
-    orig_init = re._basis_init_async
-
-    def timed_init(seed, v, rank, dev):
-        t0 = time.perf_counter()
-        j = orig_init(seed, v, rank, dev)
-
-        def join():
-            t1 = time.perf_counter()
-            a = j()
-            acc["basis_init_wait"] = time.perf_counter() - t1
-            acc["basis_init_ready_after"] = time.perf_counter() - t0
-            return a
-        return join
-    re._basis_init_async = timed_init
     cfg0 = CONFIGS[args.config]
     dev = torch.device("cuda", 0)
     x = rmx.DataMatrix(make_data_torch(cfg0, dev).to(torch.float32).cpu().numpy(), cfg0.n1, cfg0.n2)
     rc = rmx.RunConfig(permutations=cfg0.permutations, seed=cfg0.plan_seed, engine="rapid",
                        training_columns=cfg0.training_columns, rank=cfg0.rank,
                        sample_rate=cfg0.sample_rate, max_passes=50)
+    from paper_1703_01506_b200.datagen import scaled
+    cw = scaled(cfg0, (64, 64, 32), 2048)  # warm-up: kernels, allocator
+    xw = rmx.DataMatrix(make_data_torch(cw, dev).to(torch.float32).cpu().numpy(), cw.n1, cw.n2)
+    rmx.run_rapid(xw, rmx.RunConfig(permutations=2048, seed=cw.plan_seed, engine="rapid",
+                                    training_columns=cw.training_columns, rank=cw.rank,
+                                    sample_rate=cw.sample_rate, max_passes=1))
+    acc.clear()
+    torch.cuda.synchronize()
     re._PHASE_LOG = []
     t0 = time.perf_counter()
     null, model, counters = rmx.run_rapid(x, rc)
