@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <vector>
 
 #include "../../include/rmx.h"
@@ -596,14 +597,17 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   if (k > v) return rset(st, RMX_E_USAGE, "observed rows %d exceed voxel count %lld", k, (long long)v);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // sums: 0 |r|^2 1 |p|^2 2 |t|^2 4.. solver (4 resid, 5 |w|^2)
-  DevBuf<double> G, w, vals, resid, sums, wn, ug, ub2, M, cmat, dval, H, hg, hdrift, hw, mw,
-      dots, wprev, Xf, Yf, tk;
+  DevBuf<double> G, w, vals, resid, sums, wn, ug, ualt, M, NT, cmat, ctil, dval, H, hg, hdrift, hw,
+      mw, nw, dots, wprev, ugraw;
   DevBuf<int32_t> flag, idxbuf, didx;
   DevBuf<GrouseState> gst;
-  RCUDA(G.alloc((size_t)(r + 1) * (r + 1), s));
+  // look-ahead (two-stream) mode double-buffers the early chain's outputs
+  // (rows, values, Gram); buffer 0 also serves the serial path
+  const size_t gsz = (size_t)(r + 1) * (r + 1);
+  RCUDA(G.alloc(2 * gsz, s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
-  RCUDA(vals.alloc(k, s));
+  RCUDA(vals.alloc(2 * (size_t)k, s));
   RCUDA(resid.alloc(k, s));
   // + the residual blocks' partials (k_resid_defer_vec -> k_grouse_post_m)
   RCUDA(sums.alloc(8 + 2 * (size_t)((k * 32 + 255) / 256), s));
@@ -612,13 +616,22 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // ug rows: [U_Omega row | t_Omega] (the Gram's operand), padded to an even
   // length (16-byte aligned rows)
   const int64_t lu = (r + 2) / 2 * 2;
-  RCUDA(ug.alloc((size_t)k * lu, s));
-  RCUDA(ub2.alloc((size_t)v * kDeferCap, s));  // T = U_base X (flush)
+  const size_t ugsz = (size_t)k * lu;
+  RCUDA(ug.alloc(2 * ugsz, s));
+  DevBuf<double> lav, lcpart, lcorr;
+  DevBuf<GrouseLook> lookb;
+  RCUDA(lav.alloc(k, s));
+  RCUDA(lcpart.alloc(late_chain_cpart_doubles(r, k), s));
+  RCUDA(lcorr.alloc(2 * (size_t)r + 3, s));
+  RCUDA(lookb.alloc(1, s));
+  RCUDA(cudaMemsetAsync(lookb.p, 0, sizeof(GrouseLook), s));
+  RCUDA(ualt.alloc((size_t)v * r, s));  // the rebase target (U_base M), swapped with U_base
   RCUDA(M.alloc((size_t)r * r, s));
-  RCUDA(Xf.alloc((size_t)r * kDeferCap, s));
-  RCUDA(Yf.alloc((size_t)kDeferCap * r, s));
-  RCUDA(tk.alloc((size_t)k * kDeferCap, s));
+  RCUDA(NT.alloc((size_t)r * r, s));    // (M^-1)^T, tracked for the sparse flush
+  RCUDA(ugraw.alloc(ugsz, s));          // gathered rows of U_base before the product with M
   RCUDA(cmat.alloc((size_t)kDeferCap * r, s));
+  RCUDA(ctil.alloc((size_t)kDeferCap * r, s));
+  RCUDA(nw.alloc(r, s));
   RCUDA(dval.alloc((size_t)kDeferCap * k, s));
   RCUDA(didx.alloc((size_t)kDeferCap * k, s));
   RCUDA(H.alloc((size_t)r * r, s));
@@ -638,25 +651,43 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(cudaMemsetAsync(wprev.p, 0, (size_t)ell * r * sizeof(double), s));
   }
   RCUDA(cudaMemsetAsync(gst.p, 0, sizeof(GrouseState), s));
-  RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));  // M = I, X = Y = 0, no terms
-  RCUDA(launch_h_identity(H.p, r, s));          // the caller hands in an orthonormalised U
+  RCUDA(launch_h_identity(M.p, r, s));   // M = I
+  RCUDA(launch_h_identity(NT.p, r, s));  // M^-1 = I
+  RCUDA(launch_h_identity(H.p, r, s));   // the caller hands in an orthonormalised U
   std::vector<int32_t> host_idx(k);
   const double tau = ell * max_passes / 2.0;
   const bool use_cg = cg_solve_supported(r) && !getenv("RMX_GROUSE_CHOL");
   // tests: every CG solve is treated as not converged (the Cholesky fallback runs)
   const bool force_fallback = getenv("RMX_GROUSE_FORCE_FALLBACK") != nullptr;
-  // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE),
-  // M = I + X Y^T with one column of X / row of Y^T per deferred update
-  // (k_defer_apply): the flush U <- U M + terms is U += (U X) Y^T in place
-  // (4 v r nt flops instead of 2 v r^2), the per-update gather likewise.
+  // U = ubase M + sum_s d_s c_s^T (rapid_kernels.cu, M-deferred GROUSE): the
+  // rotation part of every update folds into the dense r x r matrix M, the
+  // residual part stays a sparse term for at most kDeferCap updates.
+  //  * flush (every kDeferCap updates): only the sparse terms are folded into
+  //    the base, as ubase[Omega_s] += d_s (c_s^T M^-1) -- k rows per term
+  //    instead of two DGEMMs over all v rows (M^-1 is tracked, transposed, by
+  //    the same rank-1 updates as M);
+  //  * rebase (every kRebase updates, before a re-orthonormalisation and at
+  //    the end): ubase <- ubase M out of place (one v x r x r DGEMM, 2 v r^2
+  //    flops), M = M^-1 = I, which also bounds the rounding drift of the
+  //    tracked inverse.
   double* ubase = u;
-  auto flush = [&](int nt) -> int {
-    if (nt > 0) {
-      RCUDA(launch_dgemm_rm(v, nt, r, ubase, r, Xf.p, kDeferCap, ub2.p, kDeferCap, 0, s));
-      RCUDA(launch_dgemm_rm(v, r, nt, ub2.p, kDeferCap, Yf.p, r, ubase, r, 1, s));
-    }
-    RCUDA(launch_sparse_terms_dense(ubase, r, r, k, didx.p, dval.p, cmat.p, nt, s));
-    RCUDA(launch_flush_reset(M.p, Xf.p, Yf.p, r, gst.p, s));
+  double* uother = ualt.p;
+  const int64_t kRebase = [] {
+    const char* e = getenv("RMX_GROUSE_REBASE");
+    const long long q = e ? atoll(e) : 1024;
+    return (int64_t)std::max<long long>(kDeferCap, q / kDeferCap * kDeferCap);
+  }();
+  auto flush = [&](int nt) -> int {  // sparse terms -> ubase (M unchanged)
+    RCUDA(launch_ctil(NT.p, cmat.p, r, nt, ctil.p, s));
+    RCUDA(launch_sparse_terms_dense(ubase, r, r, k, didx.p, dval.p, ctil.p, nt, s));
+    RCUDA(launch_reset_terms(gst.p, s));
+    return RMX_OK;
+  };
+  auto rebase = [&]() -> int {  // ubase <- ubase M (no pending terms), M = M^-1 = I
+    RCUDA(launch_dgemm_rm(v, r, r, ubase, r, M.p, r, uother, r, 0, s));
+    std::swap(ubase, uother);
+    RCUDA(launch_h_identity(M.p, r, s));
+    RCUDA(launch_h_identity(NT.p, r, s));
     return RMX_OK;
   };
   // One update, entirely on the device (lrmc.py:160-193): the Omega rows of
@@ -685,62 +716,114 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     prof.ev.resize((size_t)PhaseProf::kPh * PhaseProf::kN);
     for (auto& e : prof.ev) RCUDA(cudaEventCreate(&e));
   }
+  // early chain of an update (everything before the solve): rows of U on
+  // Omega with the deferred terms, and the Gram, into buffer `b`, on stream
+  // `se`.  `pending` bounds the deferred terms it sees (updates since the flush).
+  bool m_identity = true;  // no update applied since the last rebase (M = I exactly)
+  auto enqueue_early = [&](int i, const int32_t* idx, int pending, int b, cudaStream_t se,
+                           bool marks) -> int {
+    const double* trow = t + (int64_t)i * v;
+    double* ugb = ug.p + (size_t)b * ugsz;
+    // U_Omega = ubase[Omega] M: the raw rows (t[Omega] goes straight into
+    // column r of the product's rows), then one k x r x r DGEMM; right after a
+    // rebase M = I and the rows are gathered in place
+    (void)pending;
+    if (m_identity) {
+      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugb, lu, trow, vals.p + (size_t)b * k,
+                                     marks ? sums.p : nullptr, se));
+      if (marks) prof.mark(se);
+    } else {
+      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugraw.p, lu, trow, vals.p + (size_t)b * k,
+                                     marks ? sums.p : nullptr, se, ugb));
+      if (marks) prof.mark(se);
+      RCUDA(launch_dgemm_rm(k, r, r, ugraw.p, lu, M.p, r, ugb, lu, 0, se));
+    }
+    if (marks) prof.mark(se);
+    RCUDA(launch_sparse_terms_rows(ugb, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, se));
+    if (marks) prof.mark(se);
+    // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
+    RCUDA(launch_dsyrk_rm(k, r + 1, ugb, lu, G.p + (size_t)b * gsz, r + 1, se));
+    if (marks) prof.mark(se);
+    return RMX_OK;
+  };
+  // the rest of the update on the main stream: (late chain,) solve, residual,
+  // decisions, H, M.  corr: the look-ahead correction is applied by the solve.
+  // before_apply (optional): an event the M / term update must wait for (the
+  // next update's early chain reads M's factors and the terms)
+  bool prof_la_mark = false;  // set below: look-ahead profiling marks the late chain's end
+  auto enqueue_main = [&](int i, const int32_t* idx, int64_t tglob, bool chol, int b, bool late,
+                          cudaEvent_t before_apply, cudaStream_t sh = nullptr,
+                          cudaEvent_t h_prev = nullptr, cudaEvent_t post_done = nullptr,
+                          cudaEvent_t h_done = nullptr) -> int {
+    const double step = 1.0 / (1.0 + (double)tglob / tau);
+    double* ugb = ug.p + (size_t)b * ugsz;
+    double* valsb = vals.p + (size_t)b * k;
+    double* Gb = G.p + (size_t)b * gsz;
+    if (late)
+      RCUDA(launch_late_chain(ugb, lu, r, idx, k, w.p, didx.p, dval.p, wn.p, gst.p, lookb.p,
+                              lav.p, lcpart.p, lcorr.p, s));
+    if (prof_la_mark) prof.mark(s);
+    const bool cg = use_cg && !chol;
+    if (cg) {
+      RCUDA(launch_cg_solve(Gb, r, w.p, flag.p, sums.p + 4, 1e-13,
+                            warm ? wprev.p + (int64_t)i * r : nullptr, s,
+                            late ? lcorr.p : nullptr, late ? lookb.p : nullptr));
+      prof.mark(s);
+      if (force_fallback) RCUDA(cudaMemsetAsync(flag.p, 0x01, 1, s));  // tests: flag = 1
+    } else {
+      RCUDA(launch_chol_solve(Gb, r, 1, w.p, flag.p, sums.p + 4, s));
+      prof.mark(s);
+    }
+    prof.mark(s);
+    // sh (look-ahead): the H update runs on its own stream beside the next
+    // update's late chain and solve; H is read again here (hw = H w)
+    if (h_prev) RCUDA(cudaStreamWaitEvent(s, h_prev, 0));
+    RCUDA(launch_resid_defer_vec(ugb, lu, r, k, valsb, w.p, resid.p, sums.p, H.p, M.p, cmat.p,
+                                 gst.p, hw.p, mw.p, dots.p, s, NT.p, nw.p));
+    prof.mark(s);
+    RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
+                               didx.p, dval.p, cmat.p, wn.p,
+                               final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p,
+                               cg ? 1 : 0, s, lookb.p));
+    if (sh) {
+      RCUDA(cudaEventRecord(post_done, s));
+      RCUDA(cudaStreamWaitEvent(sh, post_done, 0));
+    }
+    RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ugb, lu, k, valsb, resid.p, sums.p, hg.p,
+                          sh ? sh : s, lookb.p));
+    if (sh) RCUDA(cudaEventRecord(h_done, sh));
+    if (before_apply) RCUDA(cudaStreamWaitEvent(s, before_apply, 0));
+    RCUDA(launch_defer_apply(M.p, NT.p, cmat.p, gst.p, mw.p, dots.p, wn.p, nw.p, r, s));
+    m_identity = false;
+    prof.mark(s);
+    return RMX_OK;
+  };
   // chol: solve with the batched Cholesky (a retry after the cluster CG did
   // not converge, and the redraws of an ill-conditioned restriction); else
   // the cluster CG, whose non-convergence halts the update for that retry --
   // no gated fallback kernel in every update's chain
   auto enqueue = [&](int p, int i, const int32_t* idx, int64_t tglob, bool chol) -> int {
-    const double step = 1.0 / (1.0 + (double)tglob / tau);
     prof.cur = (prof.on && tglob >= PhaseProf::kLo && tglob < PhaseProf::kLo + PhaseProf::kN)
                    ? tglob : -1;
     prof.slot = 0;
     prof.mark(s);
-    const double* trow = t + (int64_t)i * v;
-    // U_Omega = ubase[Omega] (I + X Y^T): all kDeferCap columns (unused ones are 0)
-    RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ug.p, lu, trow, vals.p, sums.p, s));
-    prof.mark(s);
-    // pending deferred terms <= updates since the last flush (tglob % kDeferCap;
-    // a halted update adds none), and the unused columns of X / Y are zero:
-    // only the first ntc columns take part (none right after a flush)
-    const int ntc = std::min(kDeferCap, ((int)(tglob % kDeferCap) + 15) / 16 * 16);
-    if (ntc > 0) {
-      RCUDA(launch_dgemm_rm(k, ntc, r, ug.p, lu, Xf.p, kDeferCap, tk.p, kDeferCap, 0, s));
-      RCUDA(launch_dgemm_rm(k, r, ntc, tk.p, kDeferCap, Yf.p, r, ug.p, lu, 1, s));
-    }
-    prof.mark(s);
-    RCUDA(launch_sparse_terms_rows(ug.p, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, s));
-    prof.mark(s);
-    // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
-    RCUDA(launch_dsyrk_rm(k, r + 1, ug.p, lu, G.p, r + 1, s));  // (sums zeroed by the gather)
-    prof.mark(s);
-    const bool cg = use_cg && !chol;
-    if (cg) {
-      RCUDA(launch_cg_solve(G.p, r, w.p, flag.p, sums.p + 4, 1e-13,
-                            warm ? wprev.p + (int64_t)i * r : nullptr, s));
-      prof.mark(s);
-      if (force_fallback) RCUDA(cudaMemsetAsync(flag.p, 0x01, 1, s));  // tests: flag = 1
-    } else {
-      RCUDA(launch_chol_solve(G.p, r, 1, w.p, flag.p, sums.p + 4, s));
-      prof.mark(s);
-    }
-    prof.mark(s);
-    RCUDA(launch_resid_defer_vec(ug.p, lu, r, k, vals.p, w.p, resid.p, sums.p, H.p, M.p, cmat.p,
-                                 gst.p, hw.p, mw.p, dots.p, s));
-    prof.mark(s);
-    RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
-                               didx.p, dval.p, cmat.p, wn.p,
-                               final_omegas ? final_omegas + (int64_t)i * k : nullptr, hw.p,
-                               cg ? 1 : 0, s));
-    RCUDA(launch_h_update(H.p, r, gst.p, hw.p, wn.p, ug.p, lu, k, vals.p, resid.p, sums.p, hg.p,
-                          s));
-    RCUDA(launch_defer_apply(M.p, Xf.p, Yf.p, cmat.p, H.p, hg.p, gst.p, mw.p, dots.p, wn.p, r,
-                             s));
-    prof.mark(s);
+    if (int rc = enqueue_early(i, idx, (int)(tglob % kDeferCap), 0, s, true)) return rc;
     (void)p;
-    return RMX_OK;
+    return enqueue_main(i, idx, tglob, chol, 0, false, nullptr);
   };
   double hdrift_host = 0.0;
+  // RMX_GROUSE_HOSTPROF=1 (diagnostics): host time spent enqueueing vs
+  // waiting at the checkpoints (a wait near zero = the host is the bound)
+  const bool hostprof = getenv("RMX_GROUSE_HOSTPROF") != nullptr;
+  double host_wait_s = 0.0;
+  const auto host_t0 = std::chrono::steady_clock::now();
   auto read_state = [&](GrouseState* h) -> int {
+    const auto w0 = std::chrono::steady_clock::now();
+    struct Acc {
+      double& a;
+      std::chrono::steady_clock::time_point t;
+      ~Acc() { a += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
+    } acc{host_wait_s, w0};
     RCUDA(launch_h_drift(H.p, r, hdrift.p, s));
     RCUDA(cudaMemcpyAsync(h, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaMemcpyAsync(&hdrift_host, hdrift.p, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -765,6 +848,67 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     }
   }
   std::vector<char> halt_used(halt_at.size(), 0);
+  // Look-ahead mode (default with the cluster CG; RMX_GROUSE_LOOKAHEAD=0 or
+  // the phase profiler select the serial chain): update h + 1's early chain
+  // runs on a second stream from the state before update h while update h is
+  // solved; its late chain then adds update h's rank-1 term (k_late /
+  // the solve's corr).  Ordering: early(h + 1) starts after update
+  // h - 1 is fully applied (evD) and must finish (evE) before update h's term
+  // is written into M's factors and the term list, which it reads.  The first
+  // update after a checkpoint starts cold (its early chain sees every term).
+  const char* la_env = getenv("RMX_GROUSE_LOOKAHEAD");
+  // RMX_GROUSE_PROFILE=2: marks on the main stream of the look-ahead chain
+  const bool prof_la = prof.on && atoi(getenv("RMX_GROUSE_PROFILE")) == 2;
+  const bool lookahead = use_cg && r <= 510 /* k_late's shared-memory partials */ &&
+                         (!prof.on || prof_la) && !(la_env && atoi(la_env) == 0);
+  struct LookStreams {
+    cudaStream_t s2 = nullptr, s3 = nullptr;
+    cudaEvent_t evE[2] = {nullptr, nullptr}, evD = nullptr, evP = nullptr;
+    cudaEvent_t evH[2] = {nullptr, nullptr};
+    ~LookStreams() {
+      for (cudaEvent_t e : evE)
+        if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : evH)
+        if (e) cudaEventDestroy(e);
+      if (evD) cudaEventDestroy(evD);
+      if (evP) cudaEventDestroy(evP);
+      if (s2) cudaStreamDestroy(s2);
+      if (s3) cudaStreamDestroy(s3);
+    }
+  } ls;
+  if (lookahead) {
+    int prio = 0;
+    RCUDA(cudaStreamGetPriority(s, &prio));
+    // one notch below the main stream: the solve's cluster is placed before
+    // the early chain's pending blocks when SMs free up
+    int plo = 0, phi = 0;
+    RCUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi));  // (least, greatest), numerically plo >= phi
+    RCUDA(cudaStreamCreateWithPriority(&ls.s2, cudaStreamNonBlocking, std::min(plo, prio + 1)));
+    RCUDA(cudaStreamCreateWithPriority(&ls.s3, cudaStreamNonBlocking, std::min(plo, prio + 1)));
+    for (auto& e : ls.evE) RCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ls.evH) RCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    RCUDA(cudaEventCreateWithFlags(&ls.evD, cudaEventDisableTiming));
+    RCUDA(cudaEventCreateWithFlags(&ls.evP, cudaEventDisableTiming));
+  }
+  prof_la_mark = prof_la;
+  bool h_pending[2] = {false, false};  // evH[b] was recorded (an H update read buffer b)
+  int64_t h_last = -1;                 // the last update whose H update went to s3
+  bool have_early = false;  // update tglob's early chain is already in flight on s2
+  auto early_on_s2 = [&](int64_t h) -> int {  // after everything enqueued on s so far
+    const int hp = (int)(h / ell), hi = (int)(h % ell);
+    RCUDA(cudaEventRecord(ls.evD, s));
+    RCUDA(cudaStreamWaitEvent(ls.s2, ls.evD, 0));
+    // buffer h & 1 was last read by update h - 2's H update (stream s3)
+    if (h_pending[h & 1]) RCUDA(cudaStreamWaitEvent(ls.s2, ls.evH[h & 1], 0));
+    // terms from updates before h - 1 inclusive when h follows an update in
+    // flight (its own term comes with the late chain); every term when cold
+    const int pending = (int)((have_early ? h - 1 : h) % kDeferCap);
+    if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending, (int)(h & 1),
+                               ls.s2, false))
+      return rc;
+    RCUDA(cudaEventRecord(ls.evE[h & 1], ls.s2));
+    return RMX_OK;
+  };
   while (tglob < total) {
     const int p = (int)(tglob / ell), i = (int)(tglob % ell);
     for (size_t q = 0; q < halt_at.size(); ++q)
@@ -772,7 +916,33 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
         halt_used[q] = 1;
         RCUDA(launch_force_halt(gst.p, tglob, s));
       }
-    if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob, false)) return rc;
+    if (!lookahead) {
+      if (int rc = enqueue(p, i, omegas0 + ((int64_t)p * ell + i) * k, tglob, false)) return rc;
+    } else {
+      const int64_t h = tglob;
+      const bool cold = !have_early;
+      if (cold)
+        if (int rc = early_on_s2(h)) return rc;
+      RCUDA(cudaStreamWaitEvent(s, ls.evE[h & 1], 0));
+      prof.cur = (prof.on && h >= PhaseProf::kLo && h < PhaseProf::kLo + PhaseProf::kN) ? h : -1;
+      prof.slot = 0;
+      prof.mark(s);
+      // the next update's early chain, unless a checkpoint follows this update
+      const bool next = h + 1 < total && !is_checkpoint(h + 1);
+      if (next) {
+        have_early = true;
+        if (int rc = early_on_s2(h + 1)) return rc;
+      }
+      if (int rc = enqueue_main(i, omegas0 + ((int64_t)p * ell + i) * k, h, false, (int)(h & 1),
+                                !cold, next ? ls.evE[(h + 1) & 1] : nullptr, ls.s3,
+                                h_last >= 0 ? ls.evH[h_last & 1] : nullptr, ls.evP,
+                                ls.evH[h & 1]))
+        return rc;
+      h_pending[h & 1] = true;
+      h_last = h;
+      while (prof.cur >= 0 && prof.slot < PhaseProf::kPh) prof.mark(s);
+      have_early = next;
+    }
     ++tglob;
     bool stop = false;
     // Process the checkpoint at tglob.  After a halt is resolved by a redraw,
@@ -782,7 +952,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // pass end is skipped).
     while (is_checkpoint(tglob)) {
       GrouseState hs;
+      if (lookahead && h_last >= 0) RCUDA(cudaStreamWaitEvent(s, ls.evH[h_last & 1], 0));
       if (int rc = read_state(&hs)) return rc;
+      if (const char* tp = getenv("RMX_GROUSE_TRACE")) {  // one flush block's timeline
+        if (tglob == 2048) grouse_trace(1, nullptr);
+        if (tglob == 2112) grouse_trace(0, tp);
+      }
       if (hs.overflow)
         return rset(st, RMX_E_CUDA, "GROUSE: more than %d deferred updates between flushes",
                     kDeferCap);
@@ -831,7 +1006,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       const int pc = (int)((tglob - 1) / ell);  // pass of the update before the checkpoint
       if (tglob % kDeferCap == 0) {  // at most kDeferCap deferred terms: rewrite U
         if (int rc = flush(hs.nterms)) return rc;
-        if (hdrift_host > 1e-8) {  // lrmc.py:258-259 every 64 updates, from the tracked H
+        const bool reorth = hdrift_host > 1e-8;  // lrmc.py:258-259 every 64 updates, from the tracked H
+        if (reorth || tglob % kRebase == 0) {
+          if (int rc = rebase()) return rc;
+          m_identity = true;
+        }
+        if (reorth) {
           double drift = 0.0;
           if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
           RCUDA(launch_h_identity(H.p, r, s));
@@ -853,9 +1033,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   }
   if (prof.on && tglob >= PhaseProf::kLo + PhaseProf::kN) {
     RCUDA(cudaStreamSynchronize(s));
-    static const char* names[PhaseProf::kPh - 1] = {"gather", "deferred_dgemms", "sparse_terms",
-                                                     "syrk+memset", "cg", "chol_gate",
-                                                     "resid", "post+h_update+defer"};
+    static const char* names_serial[PhaseProf::kPh - 1] = {
+        "gather", "deferred_dgemms", "sparse_terms", "syrk+memset", "cg", "chol_gate", "resid",
+        "post+h_update+defer"};
+    static const char* names_la[PhaseProf::kPh - 1] = {
+        "late_chain", "cg", "gate", "resid", "post+h_update+wait_early+defer", "-", "-", "-"};
+    const char* const* names = lookahead ? names_la : names_serial;
     double tot[PhaseProf::kPh - 1] = {};
     for (int u = 0; u < PhaseProf::kN; ++u)
       for (int q = 0; q + 1 < PhaseProf::kPh; ++q) {
@@ -874,7 +1057,16 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(cudaMemcpyAsync(&hs, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
     if (int rc = flush(hs.nterms)) return rc;
+    if (int rc = rebase()) return rc;
+    if (ubase != u) {  // an odd number of rebases: the result belongs in the caller's buffer
+      RCUDA(cudaMemcpyAsync(u, ubase, (size_t)v * r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      ubase = u;
+    }
   }
+  if (hostprof)
+    fprintf(stderr, "{\"grouse_host\": {\"loop_s\": %.3f, \"checkpoint_wait_s\": %.3f, \"lookahead\": %d}}\n",
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count(),
+            host_wait_s, lookahead ? 1 : 0);
   if (getenv("RMX_CG_STATS")) {
     unsigned long long cs[2] = {0, 0}, ph[6] = {0, 0, 0, 0, 0, 0};
     cudaStreamSynchronize(s);

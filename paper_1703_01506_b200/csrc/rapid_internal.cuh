@@ -95,6 +95,16 @@ struct GrouseState {
   int cg_fail;     // the halt came from a cluster CG that did not converge (retry: Cholesky)
   unsigned int hg_done;  // blocks of k_h_g_part finished (last-block reduction)
   unsigned int da_done;  // blocks of k_defer_apply finished (last block counts the term)
+  double pend_g;   // the pending update's inverse factor: (I + a w b^T)^-1 = I - pend_g w b^T
+};
+// look-ahead GROUSE: what update h decided, for the late chain of update h + 1
+// (written by k_grouse_post_m, read by k_late / k_cg_solve)
+struct GrouseLook {
+  int applied;        // update h added a term (not halted, not degenerate)
+  int slot;           // its deferred-term slot (d_idx / d_val row)
+  unsigned int done;  // blocks of k_late finished (last-block reduction)
+  int pad;
+  double a;           // pend_a of the update
 };
 // M-deferred GROUSE: U = U_base M + sum_s d_s c_s^T (d_s sparse on Omega_s)
 constexpr int kDeferCap = 64;  // terms between flushes (the host flushes every 64 updates)
@@ -118,23 +128,36 @@ cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, d
 cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
-                                   double* hw, double* mw, double* dots, cudaStream_t s);
+                                   double* hw, double* mw, double* dots, cudaStream_t s,
+                                   const double* NT, double* nw);
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
                                      int64_t ldo, const double* t, double* vals, double* zero8,
-                                     cudaStream_t s);
+                                     cudaStream_t s, double* aug = nullptr);
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
-                             double* dots, cudaStream_t s);
+                             double* dots, cudaStream_t s, const double* NT, double* nw);
 cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* flag,
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
-                                 const double* hw, int cg_mode, cudaStream_t s);
-// M += a (M w) b^T, and the same term as factors M = I + X Yt (X: r x
-// kDeferCap, Yt: kDeferCap x r, column / row nterms)
-cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
-                               const double* hg, GrouseState* st, const double* mw,
-                               const double* dots, const double* wn, int r, cudaStream_t s);
+                                 const double* hw, int cg_mode, cudaStream_t s,
+                                 GrouseLook* look = nullptr);
+// late chain of a look-ahead update (rapid_kernels.cu: k_late):
+// A (k x lda: [U_Omega | t]) += av b^T and corr = (c[0..r], b[0..r], |av|^2)
+cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows_sorted, int k,
+                              const double* w, const int32_t* d_idx, const double* d_val,
+                              const double* b, const GrouseState* st, GrouseLook* look,
+                              double* av, double* cpart, double* corr, cudaStream_t s);
+size_t late_chain_cpart_doubles(int r, int k);
+// M += a (M w) b^T, its inverse (transposed, NT) likewise, and the older
+// terms' c_s (H: launch_h_update)
+cudaError_t launch_defer_apply(double* M, double* NT, double* cmat, GrouseState* st,
+                               const double* mw, const double* dots, const double* wn,
+                               const double* nw, int r, cudaStream_t s);
+// sparse flush: ctil[s] = M^-T c_s (the terms expressed against U_base M)
+cudaError_t launch_ctil(const double* NT, const double* cmat, int r, int nterms, double* ctil,
+                        cudaStream_t s);
+cudaError_t launch_reset_terms(GrouseState* st, cudaStream_t s);
 // test hook: mark update `step` as halted (ill-conditioned) before it runs
 cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s);
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
@@ -144,10 +167,12 @@ cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseSt
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
                             const double* wn, const double* ug, int64_t ldu, int k,
                             const double* vals, const double* resid, const double* sums, double* g,
-                            cudaStream_t s);
+                            cudaStream_t s, const GrouseLook* look);
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s);
 cudaError_t launch_h_identity(double* H, int r, cudaStream_t s);
 void cg_timing(int on, unsigned long long phase[6]);
+// diagnostics: start (on = 1) / stop and dump (on = 0) the chain kernels' timeline
+void grouse_trace(int on, const char* dump_path);
 void cg_stats(unsigned long long out[2]);  // k_cg_solve (solves, iterations) so far
 // K4 on tcgen05: operand preparation and the max decode
 cudaError_t launch_u_planes(const float* U, int64_t v, int r, int kpad, __half* planes,
@@ -160,7 +185,8 @@ cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, doubl
 // x0 (optional, in/out): starting point, overwritten with the solution
 bool cg_solve_supported(int r);
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                            double tol, double* x0, cudaStream_t s);
+                            double tol, double* x0, cudaStream_t s, const double* corr = nullptr,
+                            const GrouseLook* look = nullptr);
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
                                 int64_t perm_base, double sigma, double mu, uint64_t seed,
                                 int two_sided, const float* znoise, const double* base,

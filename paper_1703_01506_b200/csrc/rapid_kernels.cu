@@ -21,7 +21,9 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "philox.cuh"
 #include "rapid_internal.cuh"
@@ -641,7 +643,28 @@ __device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank,
 // iteration cap fails.
 // RMX_CG_STATS phase clocks (CTA 0, thread 0, per iteration): local partial
 // dots, block reduction, post + wait for the peers, matvec, vector updates
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// RMX_GROUSE_TRACE (diagnostics): block 0 of each chain kernel stamps its
+// entry, the end of its pdl_wait and its exit with the global timer
+constexpr unsigned kTraceCap = 16384;
+__device__ unsigned long long g_tr[2 * kTraceCap];
+__device__ unsigned int g_tr_n;
+__device__ int g_tr_on;
+__device__ __forceinline__ void tr(int id, int ph) {
+  if (g_tr_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const unsigned i = atomicAdd(&g_tr_n, 1u);
+    if (i < kTraceCap) {
+      g_tr[2 * i] = globaltimer_ns();
+      g_tr[2 * i + 1] = (unsigned long long)(id * 4 + ph);
+    }
+  }
+}
 __device__ unsigned long long g_cg_phase[6];
+__device__ unsigned long long g_cg_wall[4];  // ns: load G, setup to the loop, loop, tail
 __device__ int g_cg_timing;
 
 __device__ __forceinline__ void cg_block_reduce3(double a, double b, double c, double* wsum,
@@ -860,14 +883,49 @@ __device__ __forceinline__ void cg_matvec_reg(const double (&g)[4][RL], int nr, 
 
 __device__ unsigned long long g_cg_iters[2];  // (solves, iterations): RMX_CG_STATS diagnostics
 
+// doubles of the solver's shared-memory layout before the look-ahead
+// correction vector (2 r + 3 doubles): G rows (shared-memory variant only),
+// the exchanged vectors, the local rows, the partial-sum slots, the two mbarriers
+__host__ __device__ inline size_t cg_corr_offset(int r, int C, bool reg) {
+  const size_t R = (size_t)((r + C - 1) / C);
+  return (reg ? 0 : R * (size_t)r) + 2 * (size_t)r + 11 * R + 6 * (size_t)C +
+         3 * (size_t)(kCgThreads / 32) + 2;
+}
+
 template <int NC, int RL = 0>
 __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restrict__ G, int r,
                                                          double* __restrict__ w_out,
                                                          int32_t* __restrict__ flag,
                                                          double* __restrict__ resid2, double tol,
-                                                         double* __restrict__ x0) {
+                                                         double* __restrict__ x0,
+                                                         const double* __restrict__ corr,
+                                                         const GrouseLook* __restrict__ look) {
+  tr(5, 0);
   pdl_wait();
+  tr(5, 1);
+  unsigned long long wall0 = 0;
+  if (g_cg_timing && threadIdx.x == 0 && cluster_ctarank() == 0) wall0 = globaltimer_ns();
   extern __shared__ double cs[];
+  // look-ahead GROUSE: G was formed from the rows before the previous update's
+  // rank-1 term a b^T; that term's contribution is added as the rows are read:
+  // G' = G + c b^T + b c^T + |a|^2 b b^T (c = A^T a incl. the t column, b_r = 0)
+  const bool con = corr != nullptr && look->applied != 0;
+  // staged in shared memory (behind the solver's own buffers, see cg_smem_bytes_c):
+  // read from global per element, the correction made the load of G 6x slower
+  double* corr_s = cs + cg_corr_offset(r, NC, RL > 0);
+  if (con) {
+    for (int e = threadIdx.x; e < 2 * r + 3; e += kCgThreads) corr_s[e] = corr[e];
+    __syncthreads();
+  }
+  const double* cc = corr_s;
+  const double* cb = corr_s + (r + 1);
+  const double csq = con ? corr_s[2 * r + 2] : 0.0;
+  auto gfix = [&](int i, int j, double g) -> double {  // i, j < r
+    if (!con) return g;
+    const double bi = cb[i], bj = cb[j];
+    return g + (cc[i] * bj + bi * cc[j]) + csq * bi * bj;
+  };
+  auto rhsfix = [&](int j, double g) -> double { return con ? fma(cc[r], cb[j], g) : g; };
   const int R = (r + NC - 1) / NC;  // rows per CTA
   const uint32_t me = cluster_ctarank();
   const int r0 = (int)me * R, nr = max(0, min(R, r - r0));
@@ -899,12 +957,12 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
 #pragma unroll
       for (int jj = 0; jj < RL; ++jj) {
         const int i = wid + qq * W, j = jj * 32 + lane;
-        greg[qq][jj] = (i < nr && j < r) ? G[(int64_t)(r0 + i) * ld + j] : 0.0;
+        greg[qq][jj] = (i < nr && j < r) ? gfix(r0 + i, j, G[(int64_t)(r0 + i) * ld + j]) : 0.0;
       }
   } else {
     for (int e = tid; e < nr * r; e += kCgThreads) {
       const int i = e / r, j = e % r;
-      Gs[(size_t)i * r + j] = G[(int64_t)(r0 + i) * ld + j];
+      Gs[(size_t)i * r + j] = gfix(r0 + i, j, G[(int64_t)(r0 + i) * ld + j]);
     }
   }
   auto matvec = [&](const double* fv, double* outv) {
@@ -913,15 +971,17 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   };
   double pb = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
-    const double di = G[(int64_t)(r0 + i) * ld + r0 + i];
+    const double di = gfix(r0 + i, r0 + i, G[(int64_t)(r0 + i) * ld + r0 + i]);
     dinv[i] = di > 0.0 ? 1.0 / di : 1.0;
     x[i] = x0 ? x0[r0 + i] : 0.0;
-    const double bi = G[(int64_t)r * ld + r0 + i];
+    const double bi = rhsfix(r0 + i, G[(int64_t)r * ld + r0 + i]);
     rv[i] = bi;
     pb += bi * bi;
     z[i] = q[i] = sv[i] = p[i] = 0.0;
   }
   cluster_sync();  // every CTA's exchange barriers are initialised before any st.async
+  unsigned long long wall1 = 0;
+  if (wall0) wall1 = globaltimer_ns();
   int par = 0;
   auto xchg = [&](const double* vv, double pa, double pb2, double pc, double& A, double& B,
                   double& C) {
@@ -952,6 +1012,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   double gamma_prev = 1.0, alpha_prev = 1.0;
   int it = 0;
   const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
+  unsigned long long wall2 = 0;
+  if (wall0) wall2 = globaltimer_ns();
   for (; it < r && !converged; ++it) {
     const long long d0 = tm ? clock64() : 0;
     double pg = 0.0, pd = 0.0, pr = 0.0;
@@ -1002,13 +1064,15 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     // no barrier: the next iteration's partial sums read only this thread's
     // rows, and cg_exchange's block reduction syncs before the rows are posted
   }
+  unsigned long long wall3 = 0;
+  if (wall0) wall3 = globaltimer_ns();
   // true residual check: |b - A x|^2 <= 16 stop (else the Cholesky fallback)
   xchg(x, 0.0, 0.0, 0.0, d0, d1, d1);
   matvec(full + par * r, nv);
   par ^= 1;
   double ptr = 0.0, pw = 0.0, pbw = 0.0;
   for (int i = tid; i < nr; i += kCgThreads) {
-    const double bi = G[(int64_t)r * ld + r0 + i];
+    const double bi = rhsfix(r0 + i, G[(int64_t)r * ld + r0 + i]);
     const double ti = bi - nv[i];
     ptr += ti * ti;
     pw += x[i] * x[i];
@@ -1030,6 +1094,13 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     atomicAdd(&g_cg_iters[1], (unsigned long long)it);
   }
   cluster_sync();  // no CTA exits while others may still write into its smem
+  if (wall0) {
+    const unsigned long long wall4 = globaltimer_ns();
+    atomicAdd(&g_cg_wall[0], wall1 - wall0);
+    atomicAdd(&g_cg_wall[1], wall2 - wall1);
+    atomicAdd(&g_cg_wall[2], wall3 - wall2);
+    atomicAdd(&g_cg_wall[3], wall4 - wall3);
+  }
 }
 
 // ------------------------------------------------------------------ K4 (tcgen05 operands)
@@ -1266,9 +1337,14 @@ __global__ void k_h_g_part(int r, GrouseState* __restrict__ st,
                            const double* __restrict__ ug, int64_t ldu, int k,
                            const double* __restrict__ resid, double* __restrict__ gpart,
                            const double* __restrict__ hw, const double* __restrict__ vals,
-                           const double* __restrict__ sums, double* __restrict__ g) {
+                           const double* __restrict__ sums, double* __restrict__ g,
+                           const GrouseLook* __restrict__ look) {
+  tr(8, 0);
   pdl_wait();
-  if (st->halted || !st->pending) return;
+  tr(8, 1);
+  // look->applied, not st->pending: this runs beside k_defer_apply (its own
+  // stream in look-ahead mode), which clears `pending`
+  if (st->halted || !look->applied) return;
   __shared__ double part[8][33];
   __shared__ bool last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1363,7 +1439,9 @@ __global__ void __launch_bounds__(256) k_sparse_terms_rows(
     double* __restrict__ out, int64_t ldo, int r, const int32_t* __restrict__ rows_sorted, int k,
     const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
     const double* __restrict__ cmat, const GrouseState* __restrict__ st) {
+  tr(3, 0);
   pdl_wait();
+  tr(3, 1);
   if (st->halted) return;
   const int nt = st->nterms;
   if (nt <= 0) return;
@@ -1483,7 +1561,9 @@ __device__ __forceinline__ void defer_vec_block(int bid, const double* __restric
                                                 const double* __restrict__ w, int r,
                                                 const GrouseState* __restrict__ st,
                                                 double* __restrict__ hw, double* __restrict__ mw,
-                                                double* __restrict__ dots) {
+                                                double* __restrict__ dots,
+                                                const double* __restrict__ NT,
+                                                double* __restrict__ nw) {
   const int task = bid * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const double* row;
@@ -1494,9 +1574,12 @@ __device__ __forceinline__ void defer_vec_block(int bid, const double* __restric
   } else if (task < 2 * r) {
     row = M + (int64_t)(task - r) * r;
     out = mw + (task - r);
-  } else if (task < 2 * r + st->nterms) {
-    row = cmat + (int64_t)(task - 2 * r) * r;
-    out = dots + (task - 2 * r);
+  } else if (task < 3 * r) {  // nw = M^-T w (NT = (M^-1)^T, tracked for the sparse flush)
+    row = NT + (int64_t)(task - 2 * r) * r;
+    out = nw + (task - 2 * r);
+  } else if (task < 3 * r + st->nterms) {
+    row = cmat + (int64_t)(task - 3 * r) * r;
+    out = dots + (task - 3 * r);
   } else {
     return;
   }
@@ -1509,8 +1592,9 @@ __device__ __forceinline__ void defer_vec_block(int bid, const double* __restric
 __global__ void k_defer_vec(const double* __restrict__ H, const double* __restrict__ M,
                             const double* __restrict__ cmat, const double* __restrict__ w, int r,
                             const GrouseState* __restrict__ st, double* __restrict__ hw,
-                            double* __restrict__ mw, double* __restrict__ dots) {
-  defer_vec_block(blockIdx.x, H, M, cmat, w, r, st, hw, mw, dots);
+                            double* __restrict__ mw, double* __restrict__ dots,
+                            const double* __restrict__ NT, double* __restrict__ nw) {
+  defer_vec_block(blockIdx.x, H, M, cmat, w, r, st, hw, mw, dots, NT, nw);
 }
 
 // one launch for the two independent consumers of the solve: the residual
@@ -1522,12 +1606,15 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
                                   const double* __restrict__ cmat,
                                   const GrouseState* __restrict__ st, double* __restrict__ hw,
                                   double* __restrict__ mw, double* __restrict__ dots, int nres,
-                                  double* __restrict__ rpart) {
+                                  double* __restrict__ rpart, const double* __restrict__ NT,
+                                  double* __restrict__ nw) {
+  tr(6, 0);
   pdl_wait();
+  tr(6, 1);
   if ((int)blockIdx.x < nres)
     resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums, rpart);
   else
-    defer_vec_block(blockIdx.x - nres, H, M, cmat, w, r, st, hw, mw, dots);
+    defer_vec_block(blockIdx.x - nres, H, M, cmat, w, r, st, hw, mw, dots, NT, nw);
 }
 
 // gathered rows of U (k x r at ld ldo) and, from the threads of column 0,
@@ -1535,8 +1622,11 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
 __global__ void k_gather_urows_vals(const double* __restrict__ U, int r,
                                     const int32_t* __restrict__ idx, int k, double* __restrict__ out,
                                     int64_t ldo, const double* __restrict__ t,
-                                    double* __restrict__ vals, double* __restrict__ zero8) {
+                                    double* __restrict__ vals, double* __restrict__ zero8,
+                                    double* __restrict__ aug) {
+  tr(1, 0);
   pdl_wait();
+  tr(1, 1);
   if (zero8 && blockIdx.x == 0 && threadIdx.x < 8) zero8[threadIdx.x] = 0.0;  // the update's sums
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)k * r) return;
@@ -1546,7 +1636,7 @@ __global__ void k_gather_urows_vals(const double* __restrict__ U, int r,
   if (c == 0) {
     const double x = t[row];
     vals[i] = x;
-    out[(int64_t)i * ldo + r] = x;
+    (aug ? aug : out)[(int64_t)i * ldo + r] = x;  // aug: the rows the product with M fills
   }
 }
 
@@ -1557,8 +1647,10 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
     const double* __restrict__ resid, const double* __restrict__ w, int r,
     int32_t* __restrict__ d_idx, double* __restrict__ d_val, double* __restrict__ cmat,
     double* __restrict__ wn, int32_t* __restrict__ final_slot, const double* __restrict__ hw,
-    int nres, int cg_mode) {
+    int nres, int cg_mode, GrouseLook* __restrict__ look) {
+  tr(7, 0);
   pdl_wait();
+  tr(7, 1);
   __shared__ int skip, do_update, slot;
   __shared__ double sb, sinvw, sa, pnorm2;
   __shared__ double part[32];
@@ -1605,6 +1697,9 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
   }
   if (threadIdx.x == 0) {
     skip = 0;
+    do_update = 0;
+    slot = 0;
+    sa = 0.0;
     if (st->halted) {
       skip = 1;
     } else if (st->nterms >= kDeferCap) {  // never with a correct host loop
@@ -1638,9 +1733,16 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
       sa = a;
       sb = bcoef;
       sinvw = upd ? 1.0 / w_norm : 0.0;
+      // (I + a w b^T)^-1 = I - g w b^T, g = a / (1 + a |w|)  (b.w = |w|)
+      st->pend_g = upd ? a / (1.0 + a * w_norm) : 0.0;
       slot = st->nterms;
       st->aa = pnorm2;  // |p|^2 for the H update
       st->rel_sum += t_norm > 0.0 ? resid_norm / t_norm : 0.0;
+    }
+    if (look) {  // what the next update's late chain has to add (k_late)
+      look->applied = (!skip && do_update) ? 1 : 0;
+      look->slot = slot;
+      look->a = sa;
     }
   }
   __syncthreads();
@@ -1668,13 +1770,27 @@ __global__ void __launch_bounds__(1024) k_grouse_post_m(
 // after k_grouse_post_m (+ the H update): M <- M + a (M w) b^T and the older
 // terms c_s <- c_s + a (w . c_s) b; block row y: M row y (y < r) or term
 // y - r; then k_defer_count adds the new term
-__global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
-                              double* __restrict__ Yt, double* __restrict__ cmat,
-                              double* __restrict__ H, const double* __restrict__ g,
+// H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2), after k_h_g_part; off
+// the update's critical path (H is next read by the following update's
+// k_resid_defer_vec, after its solve)
+__global__ void k_h_apply(double* __restrict__ H, const double* __restrict__ g,
+                          const double* __restrict__ b, const GrouseState* __restrict__ st,
+                          const GrouseLook* __restrict__ look, int r) {
+  pdl_wait();
+  if (st->halted || !look->applied) return;
+  const int i = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < r) H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
+}
+
+__global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ NT,
+                              double* __restrict__ cmat,
                               GrouseState* __restrict__ st, const double* __restrict__ mw,
                               const double* __restrict__ dots, const double* __restrict__ b,
-                              int r) {
+                              const double* __restrict__ nw, int r) {
+  tr(9, 0);
   pdl_wait();
+  tr(9, 1);
   if (st->halted || !st->pending) return;
   const int y = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1683,12 +1799,11 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
   if (c < r) {
     if (y < r) {
       M[(int64_t)y * r + c] = fma(a * mw[y], b[c], M[(int64_t)y * r + c]);
-      // the same rank-1 term as factors: M = I + X Yt (column / row nterms)
-      if (c == 0) X[(int64_t)y * kDeferCap + nt] = a * mw[y];
-      if (y == 0) Yt[(int64_t)nt * r + c] = b[c];
-    } else if (y < 2 * r) {  // H <- H + b g^T + g b^T + |a|^2 b b^T (g[r] = |a|^2)
+    } else if (y < 2 * r) {
+      // N = M^-1 <- (I - g w b^T) N (pend_g = a / (1 + a |w|)); stored
+      // transposed: NT[i][c] -= g (b^T N)_i w_c = g nw[i] b[c]  (nw = NT w, b = w / |w|)
       const int i = y - r;
-      H[(int64_t)i * r + c] += b[i] * g[c] + g[i] * b[c] + g[r] * b[i] * b[c];
+      NT[(int64_t)i * r + c] = fma(-st->pend_g * nw[i], b[c], NT[(int64_t)i * r + c]);
     } else if (y - 2 * r < nt) {
       const int sterm = y - 2 * r;
       cmat[(int64_t)sterm * r + c] = fma(a * dots[sterm], b[c], cmat[(int64_t)sterm * r + c]);
@@ -1708,11 +1823,174 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ X,
 }
 
 
+// ---- look-ahead GROUSE: the late chain of update h + 1
+// The early chain (gather, deferred products, sparse terms, Gram) of update
+// h + 1 runs on a second stream while update h is solved, from the state
+// before update h: A = [U_Omega' | t_Omega'] and G = A^T A without update h's
+// term.  Update h is U <- U (I + a w b^T) + d b^T (b = w / |w|, d = pend_b
+// resid on Omega_h), so on the rows Omega' of update h + 1
+//   A' = A + av b^T,  av = a (A w) + d|Omega',
+//   G' = G + c b^T + b c^T + |av|^2 b b^T,  c = A^T av (b_r = 0: the t column).
+// k_late (one launch): per block of rows, av (warp per row; d by a search of
+// Omega_h's sorted list), then the block's partials of c and |av|^2 and the
+// rank-1 term applied to its rows; the last block reduces the partials in a
+// fixed order (deterministic).  The cluster CG adds the correction to G as
+// it loads its rows (corr).
+constexpr int kLateRows = 32;    // rows of A per block (at most)
+constexpr int kLateCluster = 8;  // CTAs whose partials are summed through DSMEM
+
+__device__ __forceinline__ double ld_dsmem_f64(const double* local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+  return v;
+}
+
+__global__ void __cluster_dims__(kLateCluster, 1, 1) __launch_bounds__(256) k_late(
+    double* __restrict__ A, int64_t lda, int r, const int32_t* __restrict__ rows_sorted, int k,
+    const double* __restrict__ w, const int32_t* __restrict__ d_idx,
+    const double* __restrict__ d_val, const double* __restrict__ b,
+    const GrouseState* __restrict__ st, GrouseLook* __restrict__ look,
+    double* __restrict__ cpart, double* __restrict__ corr) {
+  pdl_trigger();  // the solve becomes resident (and claims its cluster's SMs) while this runs
+  tr(4, 0);
+  pdl_wait();
+  tr(4, 1);
+  if (st->halted || !look->applied) return;
+  __shared__ double av_s[kLateRows];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rows = (k + gridDim.x - 1) / gridDim.x;  // <= kLateRows (launcher)
+  const int i0 = blockIdx.x * rows, i1 = min(k, i0 + rows);
+  const int nloc = max(0, i1 - i0);
+  const int slot = look->slot;
+  const double a = look->a;
+  // av = a (A w) + d|Omega': warp per row; the row's voxel is searched in
+  // Omega_h's sorted list by one lane per row, the warp's rows in parallel
+  {
+    constexpr int kPerWarp = kLateRows / 8;
+    double dot[kPerWarp];
+#pragma unroll
+    for (int q = 0; q < kPerWarp; ++q) {
+      const int li = wid + q * 8;
+      double sacc = 0.0;
+      if (li < nloc) {
+        const double* row = A + (int64_t)(i0 + li) * lda;
+        for (int c = lane; c < r; c += 32) sacc = fma(row[c], w[c], sacc);
+      }
+      dot[q] = sacc;
+    }
+#pragma unroll
+    for (int q = 0; q < kPerWarp; ++q)
+      for (int o = 16; o > 0; o >>= 1) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
+    // lane q searches row (wid + 8 q)
+    double mine = 0.0;
+    int li = -1;
+#pragma unroll
+    for (int q = 0; q < kPerWarp; ++q)
+      if (lane == q) {
+        mine = dot[q];
+        li = wid + q * 8;
+      }
+    if (li >= 0 && li < nloc) {
+      const int32_t vox = __ldg(rows_sorted + i0 + li);
+      const int32_t* di = d_idx + (int64_t)slot * k;
+      int p = 0, step = 1;
+      while (step * 2 <= k) step *= 2;
+      for (; step > 0; step >>= 1)
+        if (p + step < k && __ldg(di + p + step) <= vox) p += step;
+      const double d = __ldg(di + p) == vox ? d_val[(int64_t)slot * k + p] : 0.0;
+      av_s[li] = fma(a, mine, d);
+    }
+  }
+  __syncthreads();
+  // c partials over this block's rows (column r is the t column) and the
+  // rank-1 term on the rows: thread per column, every row's load in flight
+  // before the first store
+  __shared__ double cp_s[2 * 256 + 2];  // the block's partial c (r + 1 <= 512) and |av|^2
+  for (int c = threadIdx.x; c <= r; c += blockDim.x) {
+    const double bc = c < r ? b[c] : 0.0;
+    double* pc = A + (int64_t)i0 * lda + c;
+    double x[kLateRows];
+#pragma unroll
+    for (int q = 0; q < kLateRows; ++q) x[q] = q < nloc ? __ldcg(pc + (int64_t)q * lda) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kLateRows; ++q)
+      if (q < nloc) {
+        const double ai = av_s[q];
+        acc = fma(x[q], ai, acc);
+        if (c < r) pc[(int64_t)q * lda] = fma(ai, bc, x[q]);
+      }
+    cp_s[c] = acc;
+  }
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+    for (int i = 0; i < nloc; ++i) ss = fma(av_s[i], av_s[i], ss);
+    cp_s[r + 1] = ss;
+  }
+  // the cluster's kLateCluster partials -> one per cluster (rank q sums a
+  // slice of the columns through DSMEM, CTAs in rank order), so the last
+  // block's serial pass reads gridDim.x / kLateCluster partials, not gridDim.x
+  cluster_sync();
+  {
+    const uint32_t me = cluster_ctarank();
+    const int ncol = r + 2;
+    const int per = (ncol + kLateCluster - 1) / kLateCluster;
+    const int c = (int)me * per + (int)threadIdx.x;
+    if ((int)threadIdx.x < per && c < ncol) {
+      double t = 0.0;
+#pragma unroll
+      for (uint32_t q = 0; q < (uint32_t)kLateCluster; ++q) t += ld_dsmem_f64(&cp_s[c], q);
+      cpart[(int64_t)(blockIdx.x / kLateCluster) * (r + 2) + c] = t;
+    }
+  }
+  __threadfence();
+  cluster_sync();  // no CTA exits while a peer may still read its partials
+  if (threadIdx.x == 0) last = atomicAdd(&look->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // fixed-order reduction of the per-cluster partials (deterministic)
+  const int ncl = gridDim.x / kLateCluster;
+  for (int cc = threadIdx.x; cc <= r + 1; cc += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < ncl; ++q) t += __ldcg(cpart + (int64_t)q * (r + 2) + cc);
+    if (cc <= r) corr[cc] = t;            // c (c_r = t . av)
+    else corr[2 * r + 2] = t;             // |av|^2
+    if (cc < r) corr[r + 1 + cc] = b[cc];
+  }
+  if (threadIdx.x == 0) {
+    corr[2 * r + 1] = 0.0;  // b_r
+    look->done = 0;
+  }
+}
+
 __global__ void k_force_halt(GrouseState* __restrict__ st, int64_t step) {
   if (st->halted) return;
   st->halted = 1;
   st->halt_step = (int)step;
 }
+
+// sparse flush (dense-M GROUSE): the deferred terms fold into the base as
+// U_base += d_s (c_s^T M^-1), so that U_base M keeps representing U; ctil[s] =
+// NT c_s (one warp per output)
+__global__ void k_ctil(const double* __restrict__ NT, const double* __restrict__ cmat, int r,
+                       int nterms, double* __restrict__ ctil) {
+  const int task = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (task >= nterms * r) return;
+  const int sterm = task / r, c = task - sterm * r;
+  const double* row = NT + (int64_t)c * r;
+  const double* cs = cmat + (int64_t)sterm * r;
+  double acc = 0.0;
+  for (int j = lane; j < r; j += 32) acc = fma(row[j], cs[j], acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) ctil[task] = acc;
+}
+
+__global__ void k_reset_terms(GrouseState* __restrict__ st) { st->nterms = 0; }
 
 __global__ void k_flush_reset(double* __restrict__ M, double* __restrict__ X,
                               double* __restrict__ Yt, int r, GrouseState* __restrict__ st) {
@@ -1870,7 +2148,9 @@ cudaError_t launch_gram(const double* U, int64_t ldu, int r, const int32_t* idx,
   const int64_t blocks = (int64_t)ntiles * B;
   if (blocks < 6 * 148) {  // 64-thread CTAs: several per SM
     splits = (int)std::min<int64_t>((6 * 148 + blocks - 1) / blocks, std::max(1, k / 64));
-    splits = std::max(1, std::min(splits, 4096));
+    // at most two partial sums per element: 0 + a + b is the same in either
+    // order, so the atomics stay deterministic (three or more are not)
+    splits = std::max(1, std::min(splits, 2));
   }
   const int rps = ((k + splits - 1) / splits + kGK - 1) / kGK * kGK;
   splits = (k + rps - 1) / rps;
@@ -2372,10 +2652,8 @@ int cg_ctas() {  // cluster size of the GROUSE solve: 16 (default) or 8 (RMX_CG_
   return c;
 }
 
-size_t cg_smem_bytes_c(int r, int C) {
-  const int R = (r + C - 1) / C;
-  return ((size_t)R * r + 2 * (size_t)r + 11 * (size_t)R + 6 * C + 3 * (kCgThreads / 32) + 2) *
-         sizeof(double);  // + the two exchange mbarriers
+size_t cg_smem_bytes_c(int r, int C) {  // the shared-memory variant's full layout
+  return (cg_corr_offset(r, C, false) + 2 * (size_t)r + 3) * sizeof(double);
 }
 
 size_t cg_smem_bytes(int r) { return cg_smem_bytes_c(r, cg_ctas()); }
@@ -2384,7 +2662,8 @@ bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
 
 template <int C, int RL = 0>
 cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* flag,
-                              double* resid2, double tol, double* x0, cudaStream_t s) {
+                              double* resid2, double tol, double* x0, cudaStream_t s,
+                              const double* corr, const GrouseLook* look) {
   // the register-resident variant keeps no copy of G in shared memory
   const size_t smem =
       cg_smem_bytes_c(r, C) - (RL > 0 ? (size_t)((r + C - 1) / C) * r * sizeof(double) : 0);
@@ -2409,18 +2688,21 @@ cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* fl
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_cg_solve<C, RL>, G, r, w_out, flag, resid2, tol, x0);
+  return cudaLaunchKernelEx(&cfg, k_cg_solve<C, RL>, G, r, w_out, flag, resid2, tol, x0, corr,
+                            look);
 }
 
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
-                            double tol, double* x0, cudaStream_t s) {
+                            double tol, double* x0, cudaStream_t s, const double* corr,
+                            const GrouseLook* look) {
   // rows of G in registers when each warp holds at most 4 rows of <= 416
   // columns (RMX_CG_SMEM=1: the shared-memory variant)
   const bool reg = r <= 13 * 32 && (r + kCgCtas - 1) / kCgCtas <= 4 * (kCgThreads / 32) &&
                    !getenv("RMX_CG_SMEM");
-  if (cg_ctas() == 8) return launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s);
-  if (reg) return launch_cg_solve_c<kCgCtas, 13>(G, r, w_out, flag, resid2, tol, x0, s);
-  return launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s);
+  if (cg_ctas() == 8)
+    return launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
+  if (reg) return launch_cg_solve_c<kCgCtas, 13>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
+  return launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
@@ -2469,12 +2751,15 @@ cudaError_t launch_pred(const double* U, int64_t v, int r, const double* w, doub
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,
                             const double* wn, const double* ug, int64_t ldu, int k,
                             const double* vals,
-                            const double* resid, const double* sums, double* g, cudaStream_t s) {
-  (void)H;
-  (void)wn;
+                            const double* resid, const double* sums, double* g, cudaStream_t s,
+                            const GrouseLook* look) {
   double* gpart = g + r + 1;  // kHgSplit x r scratch after g[0..r]
-  return launch_pdl(k_h_g_part, dim3((unsigned)((r + 31) / 32), kHgSplit), dim3(256), 0, s, r,
-                    const_cast<GrouseState*>(st), ug, ldu, k, resid, gpart, hw, vals, sums, g);
+  cudaError_t e = launch_pdl(k_h_g_part, dim3((unsigned)((r + 31) / 32), kHgSplit), dim3(256), 0,
+                             s, r, const_cast<GrouseState*>(st), ug, ldu, k, resid, gpart, hw, vals,
+                             sums, g, look);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_h_apply, dim3((unsigned)((r + 255) / 256), (unsigned)r), dim3(256), 0, s, H,
+                    static_cast<const double*>(g), wn, st, look, r);
 }
 
 cudaError_t launch_h_drift(const double* H, int r, double* out, cudaStream_t s) {
@@ -2538,30 +2823,32 @@ cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, d
 cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
-                                   double* hw, double* mw, double* dots, cudaStream_t s) {
+                                   double* hw, double* mw, double* dots, cudaStream_t s,
+                                   const double* NT, double* nw) {
   const int nres = (k * 32 + 255) / 256;
-  const int ndv = (2 * r + kDeferCap + 7) / 8;
+  const int ndv = (3 * r + kDeferCap + 7) / 8;
   // sums[0] / sums[2] (|resid|^2, |t_Omega|^2): per-block partials in
   // sums + 8.., reduced in a fixed order by k_grouse_post_m (deterministic)
   return launch_pdl(k_resid_defer_vec, dim3((unsigned)(nres + ndv)), dim3(256), 0, s, U, ldu, r, k,
-                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres, sums + 8);
+                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres, sums + 8, NT, nw);
 }
 
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
                                      int64_t ldo, const double* t, double* vals, double* zero8,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, double* aug) {
   const int64_t n = (int64_t)k * r;
   cudaError_t e = launch_pdl(k_gather_urows_vals, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
-                             s, U, r, idx, k, out, ldo, t, vals, zero8);
+                             s, U, r, idx, k, out, ldo, t, vals, zero8, aug);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
                              const double* w, int r, const GrouseState* st, double* hw, double* mw,
-                             double* dots, cudaStream_t s) {
-  const int tasks = 2 * r + kDeferCap;
-  k_defer_vec<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(H, M, cmat, w, r, st, hw, mw, dots);
+                             double* dots, cudaStream_t s, const double* NT, double* nw) {
+  const int tasks = 3 * r + kDeferCap;
+  k_defer_vec<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(H, M, cmat, w, r, st, hw, mw, dots, NT,
+                                                         nw);
   return cudaGetLastError();
 }
 
@@ -2569,18 +2856,49 @@ cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* f
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
-                                 const double* hw, int cg_mode, cudaStream_t s) {
+                                 const double* hw, int cg_mode, cudaStream_t s,
+                                 GrouseLook* look) {
   const int nres = (k * 32 + 255) / 256;  // k_resid_defer_vec's residual blocks
   return launch_pdl(k_grouse_post_m, dim3(1), dim3(1024), 0, s, st, sums, flag, step, step_index,
-                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw, nres, cg_mode);
+                    idx, k, resid, w, r, d_idx, d_val, cmat, wn, final_slot, hw, nres, cg_mode,
+                    look);
 }
 
-cudaError_t launch_defer_apply(double* M, double* X, double* Yt, double* cmat, double* H,
-                               const double* hg, GrouseState* st, const double* mw,
-                               const double* dots, const double* wn, int r, cudaStream_t s) {
+cudaError_t launch_defer_apply(double* M, double* NT, double* cmat, GrouseState* st,
+                               const double* mw, const double* dots, const double* wn,
+                               const double* nw, int r, cudaStream_t s) {
   return launch_pdl(k_defer_apply, dim3((unsigned)((r + 255) / 256), (unsigned)(2 * r + kDeferCap)),
-                    dim3(256), 0, s, M, X, Yt, cmat, H, hg, st, mw, dots, wn, r);
+                    dim3(256), 0, s, M, NT, cmat, st, mw, dots, wn, nw, r);
 }
+
+cudaError_t launch_ctil(const double* NT, const double* cmat, int r, int nterms, double* ctil,
+                        cudaStream_t s) {
+  if (nterms <= 0) return cudaSuccess;
+  const int tasks = nterms * r;
+  k_ctil<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(NT, cmat, r, nterms, ctil);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset_terms(GrouseState* st, cudaStream_t s) {
+  k_reset_terms<<<1, 1, 0, s>>>(st);
+  return cudaGetLastError();
+}
+
+static int late_blocks(int k) {  // a multiple of the cluster size
+  const int b = std::max(96, (k + kLateRows - 1) / kLateRows);
+  return (b + kLateCluster - 1) / kLateCluster * kLateCluster;
+}
+
+cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows_sorted, int k,
+                              const double* w, const int32_t* d_idx, const double* d_val,
+                              const double* b, const GrouseState* st, GrouseLook* look,
+                              double* av, double* cpart, double* corr, cudaStream_t s) {
+  (void)av;
+  return launch_pdl(k_late, dim3((unsigned)late_blocks(k)), dim3(256), 0, s, A, lda, r,
+                    rows_sorted, k, w, d_idx, d_val, b, st, look, cpart, corr);
+}
+
+size_t late_chain_cpart_doubles(int r, int k) { return (size_t)late_blocks(k) * (r + 2); }
 
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
                                cudaStream_t s) {
@@ -2594,12 +2912,39 @@ cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+void grouse_trace(int on, const char* dump_path) {
+  if (!on && dump_path) {
+    unsigned int n = 0;
+    cudaMemcpyFromSymbol(&n, g_tr_n, sizeof(n));
+    if (n > kTraceCap) n = kTraceCap;
+    std::vector<unsigned long long> h(2 * (size_t)n);
+    if (n) cudaMemcpyFromSymbol(h.data(), g_tr, h.size() * sizeof(unsigned long long));
+    if (FILE* f = fopen(dump_path, "w")) {
+      for (unsigned i = 0; i < n; ++i)
+        fprintf(f, "%llu %llu %llu\n", h[2 * i], h[2 * i + 1] / 4, h[2 * i + 1] % 4);
+      fclose(f);
+    }
+  }
+  unsigned int z = 0;
+  if (on) cudaMemcpyToSymbol(g_tr_n, &z, sizeof(z));
+  cudaMemcpyToSymbol(g_tr_on, &on, sizeof(int));
+}
+
 void cg_stats(unsigned long long out[2]) {
   cudaMemcpyFromSymbol(out, g_cg_iters, sizeof(unsigned long long) * 2);
 }
 
 void cg_timing(int on, unsigned long long phase[6]) {
   if (phase) cudaMemcpyFromSymbol(phase, g_cg_phase, sizeof(unsigned long long) * 6);
+  if (phase && !on) {
+    unsigned long long wl[4];
+    cudaMemcpyFromSymbol(wl, g_cg_wall, sizeof(wl));
+    unsigned long long cs2[2];
+    cudaMemcpyFromSymbol(cs2, g_cg_iters, sizeof(cs2));
+    const double n = cs2[0] ? (double)cs2[0] : 1.0;
+    fprintf(stderr, "rmx cg wall (us per solve): load G %.2f, setup %.2f, loop %.2f, tail %.2f\n",
+            wl[0] / n * 1e-3, wl[1] / n * 1e-3, wl[2] / n * 1e-3, wl[3] / n * 1e-3);
+  }
   cudaMemcpyToSymbol(g_cg_timing, &on, sizeof(int));
 }
 

@@ -91,6 +91,12 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
 // stream has completed and its writes are visible (a no-op when this
 // kernel was launched without the PDL attribute).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// lets the next kernel of the stream (launched with programmatic stream
+// serialisation) become resident now; it still waits in its own pdl_wait
+// until this grid has completed and its writes are visible
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

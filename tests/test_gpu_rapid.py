@@ -351,15 +351,20 @@ def _grouse_case(v=6000, ell=24, r=24, eta=0.05, seed=77):
     return t_ex, int(np.ceil(eta * v)), r, seed
 
 
+@pytest.mark.parametrize("chain", ["lookahead", "serial"])
 @pytest.mark.parametrize("solver", ["cg", "chol_fallback"])
-def test_grouse_matches_oracle_numpy_restatement(oracle_mod, solver, monkeypatch):
+def test_grouse_matches_oracle_numpy_restatement(oracle_mod, solver, chain, monkeypatch):
     """Device GROUSE vs the numpy restatement of lrmc.py:208-268 (pinned to
     the reference's basis in test_oracle_golden): same Omega draws, so the
     trajectories agree to fp64 solver precision -- with the cluster CG, and
     with every update forced through the gated Cholesky fallback (the path
-    taken when CG does not converge)."""
+    taken when CG does not converge); with the look-ahead chain (update h + 1's
+    rows and Gram formed before update h's term, which is added as a rank-1
+    correction) and with the serial chain."""
     if solver == "chol_fallback":
         monkeypatch.setenv("RMX_GROUSE_FORCE_FALLBACK", "1")
+    if chain == "serial":
+        monkeypatch.setenv("RMX_GROUSE_LOOKAHEAD", "0")
     t_ex, k, r, seed = _grouse_case()
     res = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=4)
     u, passes, pres, om, conv = oracle_mod.grouse(t_ex, k, r, seed, max_passes=4)
@@ -369,8 +374,9 @@ def test_grouse_matches_oracle_numpy_restatement(oracle_mod, solver, monkeypatch
     assert all(np.array_equal(a, b) for a, b in zip(res.final_omegas, om))
 
 
+@pytest.mark.parametrize("chain", ["lookahead", "serial"])
 @pytest.mark.parametrize("halts", ["63", "71", "95", "63,71,95", "0,40"])
-def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, monkeypatch):
+def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, chain, monkeypatch):
     """An ill-conditioned restriction at update h is redrawn from the same
     stream (lrmc.py:240-250).  h = 63 ends a 64-update flush block, h = 71 a
     pass (ell = 24), h = 95 the whole training: the checkpoint at h + 1 must
@@ -378,6 +384,8 @@ def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, monkeypatch):
     t_ex, k, r, seed = _grouse_case()
     hs = tuple(int(h) for h in halts.split(","))
     monkeypatch.setenv("RMX_GROUSE_TEST_HALT", halts)
+    if chain == "serial":
+        monkeypatch.setenv("RMX_GROUSE_LOOKAHEAD", "0")
     res = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=4)
     u, passes, pres, om, conv = oracle_mod.grouse(t_ex, k, r, seed, max_passes=4, force_halt=hs)
     assert res.passes == passes == 4 and res.updates == 96
