@@ -655,7 +655,7 @@ __device__ unsigned long long g_tr[2 * kTraceCap];
 __device__ unsigned int g_tr_n;
 __device__ int g_tr_on;
 __device__ __forceinline__ void tr(int id, int ph) {
-  if (g_tr_on && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && g_tr_on) {
     const unsigned i = atomicAdd(&g_tr_n, 1u);
     if (i < kTraceCap) {
       g_tr[2 * i] = globaltimer_ns();

@@ -436,14 +436,17 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
     dev = t_dev.device
     if init is None:
         init = _basis_init_async(seed, v, rank, dev)
+    # the observation sets of every pass (stream(seed, TRAIN_OMEGA, i, p), drawn
+    # on the GPU) while the host still draws the BASIS_INIT normals
+    om_dev = torch.empty((max_passes, ell, k), dtype=torch.int32, device=dev)
+    for p in range(max_passes):
+        om_dev[p] = device_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, dev, extra=p)
+    _mark("train_omegas")
     u = init()
     host_u = _host_array_async((v, rank)) if host_basis else None
     _mark("basis_normals_ready")
     _orthonormalize(u, force=True)
     _mark("basis_upload+qr")
-    om_dev = torch.empty((max_passes, ell, k), dtype=torch.int32, device=dev)
-    for p in range(max_passes):  # stream(seed, TRAIN_OMEGA, i, p), drawn on the GPU
-        om_dev[p] = device_omegas(seed, TRAIN_OMEGA, 0, ell, v, k, dev, extra=p)
     final = torch.empty((ell, k), dtype=torch.int32, device=dev)
     pass_resid = (ctypes.c_double * max_passes)()
     passes, conv, updates = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int64(0)
@@ -456,7 +459,6 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
         except Exception:
             return 1
 
-    _mark("train_omegas")
     cbf = nat.OMEGA_CB(cb)
     nat.call("rmx_grouse_train", nat.ptr(t_dev), v, ell, rank, k, nat.ptr(om_dev), max_passes,
              float(tolerance), nat.ptr(u), cbf, None, pass_resid, ctypes.byref(passes),
@@ -488,10 +490,15 @@ def train_basis(t_ex: np.ndarray, k: int, rank: int, seed: int, max_passes: int 
 _PHASE_LOG = None  # tools/rapid_phases.py sets a list: (tag, seconds) marks, device-synchronised
 
 
+_HOST_MARKS = os.environ.get("RMX_RAPID_HOSTMARKS")  # diagnostics: host-side marks, no device sync
+
+
 def _mark(tag: str) -> None:
     if _PHASE_LOG is not None:
         _torch().cuda.synchronize()
         _PHASE_LOG.append((tag, time.perf_counter()))
+    elif _HOST_MARKS:
+        print(f"[host-mark] {time.perf_counter():.3f} {tag}", flush=True)
 
 
 def _host_async(fn):
@@ -583,22 +590,40 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
             # them the prefetch only delayed GROUSE's start
             lo_prio.wait_stream(torch.cuda.current_stream(dev))
 
+            trace_pf = os.environ.get("RMX_TRACE_PREFETCH")
+            pf_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if trace_pf else None
+
             def prefetch():
                 torch.cuda.set_device(dev)
                 with torch.cuda.stream(lo_prio):
+                    if pf_ev:
+                        pf_ev[0].record(lo_prio)
                     r = _RecoverInputs(x, xd, plan, cfg.seed, ell, k, dev)
                     done = torch.cuda.Event()
                     done.record(lo_prio)
+                    if pf_ev:
+                        pf_ev[1].record(lo_prio)
                 return r, done
 
             pre_join = _host_async(prefetch)
         _mark("recovery_prefetch")
+    if os.environ.get("RMX_RAPID_SYNC_BEFORE_GROUSE"):  # diagnostics: no prefetch beside GROUSE
+        torch.cuda.synchronize()
     hi_prio = torch.cuda.Stream(dev, priority=-100)  # mapped to the highest priority
     hi_prio.wait_stream(torch.cuda.current_stream(dev))
     with torch.cuda.stream(hi_prio):
+        if pre_join is not None and pf_ev:
+            pf_ev[2].record(hi_prio)
         u, final, passes, conv, _, _, host_u = _train_basis_device(
             t_dev, v, ell, k, rank, cfg.seed, cfg.max_passes, cfg.tolerance, init,
             host_basis=prefetch_recovery)
+    if pre_join is not None and pf_ev:
+        pf_ev[3].record(hi_prio)
+        torch.cuda.synchronize()
+        print(f"[prefetch-trace] prefetch start -> end {pf_ev[0].elapsed_time(pf_ev[1]):.1f} ms; "
+              f"prefetch start -> basis phase start {pf_ev[0].elapsed_time(pf_ev[2]):.1f} ms; "
+              f"basis phase start -> GROUSE end {pf_ev[2].elapsed_time(pf_ev[3]):.1f} ms",
+              flush=True)
     torch.cuda.current_stream(dev).wait_stream(hi_prio)
     for tnsr in (u, final):
         tnsr.record_stream(torch.cuda.current_stream(dev))
@@ -758,6 +783,7 @@ def run_rapid(x, cfg):
     cfg = cfg.resolve(x)
     plan = cfg.plan_for(x)
     t0 = time.perf_counter()
+    _mark("run_rapid_start")
     model, _, _, pre = _train_device(x, cfg, prefetch_recovery=True)
     t1 = time.perf_counter()
     null, rec = recover(x, model, plan, cfg, _pre=pre)
