@@ -302,29 +302,63 @@ int lsq_tc_impl(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_
                             (per + 4 * sizeof(double)));
   if (chunk < 1) return rset(st, RMX_E_USAGE, "lsq workspace too small");
   chunk = std::min<int64_t>(chunk, B);
-  void* Graw = workspace;
+  // RMX_LSQ_STREAMS=2 (experiment): two batches in flight on two side streams
+  // (each owns half of the workspace), so the tensor-core Gram of one batch
+  // overlaps the latency-bound factor / resolves of the other.  Measured
+  // slower at config 5 (0.70 s vs 0.67 s per 99,600 systems: the factor's
+  // three CTAs per SM leave the Gram no room), so one batch at a time is the
+  // default.
+  const char* ls_env = getenv("RMX_LSQ_STREAMS");
+  const bool two = f32 && B > chunk / 2 && chunk >= 2 && ls_env && atoi(ls_env) == 2;
+  if (two) chunk /= 2;
+  struct Side {
+    cudaStream_t q[2] = {nullptr, nullptr};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    ~Side() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      for (cudaStream_t x : q)
+        if (x) cudaStreamDestroy(x);
+    }
+  } side;
+  void* Gq[2] = {workspace, static_cast<uint8_t*>(workspace) + (two ? chunk * per : 0)};
   double* G = static_cast<double*>(workspace);
-  double* nrm = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) + chunk * per);
+  double* nrm = reinterpret_cast<double*>(static_cast<uint8_t*>(workspace) +
+                                          (two ? 2 : 1) * chunk * per);
   DevBuf<__half> planes;
-  DevBuf<double> g;
+  DevBuf<double> gbuf;
   DevBuf<int32_t> flags, nconv;
   RCUDA(planes.alloc((size_t)2 * v * gram_tc_kpg(r), s));
-  RCUDA(g.alloc((size_t)chunk * r, s));
+  RCUDA(gbuf.alloc((size_t)(two ? 2 : 1) * chunk * r, s));
   RCUDA(flags.alloc((size_t)B, s));
   RCUDA(nconv.alloc((size_t)B, s));
   RCUDA(launch_gram_planes(u, ldu, v, r, planes.p, s));
+  if (two) {
+    int prio = 0;
+    RCUDA(cudaStreamGetPriority(s, &prio));
+    for (auto& x : side.q) RCUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio));
+    for (auto& e : side.ev) RCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    RCUDA(cudaEventRecord(side.ev[2], s));  // planes, scratch and the caller's inputs are ready
+    for (auto& x : side.q) RCUDA(cudaStreamWaitEvent(x, side.ev[2], 0));
+  }
+  cudaStream_t s_caller = s;
   const int sms = device_sm_count();
-  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+  int64_t batch_no = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk, ++batch_no) {
     const int64_t cnt = std::min(chunk, B - b0);
     const int32_t* ib = idx + b0 * k;
     const double* vb = vals + b0 * k;
     double* wb = w_out + b0 * r;
+    const int qi = two ? (int)(batch_no & 1) : 0;
+    cudaStream_t s = two ? side.q[qi] : s_caller;  // this batch's stream (shadows the caller's)
+    void* Graw = Gq[qi];
+    double* gp = gbuf.p + (size_t)qi * chunk * r;
     RCUDA(launch_gram_tc(planes.p, v, r, ib, k, vb, Graw, f32 ? 1 : 0, cnt, sms, s));
     if (f32 && chol_cluster_supported(r)) {
       // factor on chip (4-CTA clusters), then the first solve as a resolve
       // from w = 0 (its convergence flag is overwritten by the refinements)
-      RCUDA(launch_chol_cluster_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, flags.p + b0, s));
-      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s));
+      RCUDA(launch_chol_cluster_f32(static_cast<float*>(Graw), r, cnt, gp, wb, flags.p + b0, s));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, gp, wb, nconv.p + b0, s));
     } else if (f32) {
       RCUDA(launch_chol_solve_f32(static_cast<float*>(Graw), r, cnt, wb, flags.p + b0, s));
     } else {
@@ -337,8 +371,8 @@ int lsq_tc_impl(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_
     // rest take a second step.  settle_tol = 0 (rmx_lsq_solve_tc): two steps
     // on every system (w to ~1e-12).  RMX_REFINE_STEPS=2 forces two steps.
     if (f32) {
-      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
-      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s,
+      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, gp, s));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, gp, wb, nconv.p + b0, s,
                                     nullptr, force2 ? 0.0 : settle_tol));
       if (getenv("RMX_LSQ_STATS")) {  // diagnostics: systems taking the second step
         std::vector<int32_t> h((size_t)cnt);
@@ -349,16 +383,21 @@ int lsq_tc_impl(const double* u, int64_t ldu, int64_t v, int32_t r, const int32_
         fprintf(stderr, "[lsq_tc] batch of %lld systems: %lld take a second refinement step\n",
                 (long long)cnt, (long long)c2);
       }
-      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s, nconv.p + b0));
-      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, g.p, wb, nconv.p + b0, s,
+      RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, gp, s, nconv.p + b0));
+      RCUDA(launch_chol_resolve_f32(static_cast<float*>(Graw), r, cnt, gp, wb, nconv.p + b0, s,
                                     nconv.p + b0, 1e-7));
     } else {
       for (int it = 0; it < 2; ++it) {
-        RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, g.p, s));
-        RCUDA(launch_chol_resolve(G, r, cnt, g.p, wb, nconv.p + b0, s));
+        RCUDA(launch_lsq_resid(u, ldu, r, ib, k, vb, wb, cnt, gp, s));
+        RCUDA(launch_chol_resolve(G, r, cnt, gp, wb, nconv.p + b0, s));
       }
     }
   }
+  if (two)
+    for (int qi = 0; qi < 2; ++qi) {
+      RCUDA(cudaEventRecord(side.ev[qi], side.q[qi]));
+      RCUDA(cudaStreamWaitEvent(s, side.ev[qi], 0));
+    }
   // systems whose fp32 factor was singular or whose refinement has not
   // settled (rare: cond(U_Omega) >~ 1e3): the reference's decision on the
   // fp64 Gram -- exact cond vs 1e12, Cholesky or pivoted LU, w = rhs when
@@ -620,7 +659,9 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(ug.alloc(2 * ugsz, s));
   DevBuf<double> lav, lcpart, lcorr;
   DevBuf<GrouseLook> lookb;
-  RCUDA(lav.alloc(k, s));
+  // k_late's first-level group counters (it leaves them zero)
+  RCUDA(lav.alloc((late_chain_group_counters(k) + 1) / 2 + 1, s));
+  RCUDA(cudaMemsetAsync(lav.p, 0, ((late_chain_group_counters(k) + 1) / 2 + 1) * sizeof(double), s));
   RCUDA(lcpart.alloc(late_chain_cpart_doubles(r, k), s));
   RCUDA(lcorr.alloc(2 * (size_t)r + 3, s));
   RCUDA(lookb.alloc(1, s));

@@ -149,6 +149,7 @@ cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows
                               const double* b, const GrouseState* st, GrouseLook* look,
                               double* av, double* cpart, double* corr, cudaStream_t s);
 size_t late_chain_cpart_doubles(int r, int k);
+size_t late_chain_group_counters(int k);  // unsigned ints behind `av` (zeroed once)
 // M += a (M w) b^T, its inverse (transposed, NT) likewise, and the older
 // terms' c_s (H: launch_h_update)
 cudaError_t launch_defer_apply(double* M, double* NT, double* cmat, GrouseState* st,

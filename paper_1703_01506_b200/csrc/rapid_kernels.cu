@@ -1833,26 +1833,18 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ NT,
 //   G' = G + c b^T + b c^T + |av|^2 b b^T,  c = A^T av (b_r = 0: the t column).
 // k_late (one launch): per block of rows, av (warp per row; d by a search of
 // Omega_h's sorted list), then the block's partials of c and |av|^2 and the
-// rank-1 term applied to its rows; the last block reduces the partials in a
-// fixed order (deterministic).  The cluster CG adds the correction to G as
+// rank-1 term applied to its rows; the partials are reduced in two levels in
+// a fixed order (deterministic).  The cluster CG adds the correction to G as
 // it loads its rows (corr).
 constexpr int kLateRows = 32;    // rows of A per block (at most)
-constexpr int kLateCluster = 8;  // CTAs whose partials are summed through DSMEM
+constexpr int kLateGroup = 8;    // blocks per first-level reduction group
 
-__device__ __forceinline__ double ld_dsmem_f64(const double* local, uint32_t rank) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
-  return v;
-}
-
-__global__ void __cluster_dims__(kLateCluster, 1, 1) __launch_bounds__(256) k_late(
+__global__ void __launch_bounds__(256) k_late(
     double* __restrict__ A, int64_t lda, int r, const int32_t* __restrict__ rows_sorted, int k,
     const double* __restrict__ w, const int32_t* __restrict__ d_idx,
     const double* __restrict__ d_val, const double* __restrict__ b,
     const GrouseState* __restrict__ st, GrouseLook* __restrict__ look,
-    double* __restrict__ cpart, double* __restrict__ corr) {
+    double* __restrict__ cpart, double* __restrict__ corr, unsigned int* __restrict__ gcnt) {
   pdl_trigger();  // the solve becomes resident (and claims its cluster's SMs) while this runs
   tr(4, 0);
   pdl_wait();
@@ -1930,33 +1922,47 @@ __global__ void __cluster_dims__(kLateCluster, 1, 1) __launch_bounds__(256) k_la
     for (int i = 0; i < nloc; ++i) ss = fma(av_s[i], av_s[i], ss);
     cp_s[r + 1] = ss;
   }
-  // the cluster's kLateCluster partials -> one per cluster (rank q sums a
-  // slice of the columns through DSMEM, CTAs in rank order), so the last
-  // block's serial pass reads gridDim.x / kLateCluster partials, not gridDim.x
-  cluster_sync();
+  // two-level fixed-order reduction without a serial pass over every block's
+  // partials: the last block of each group of kLateGroup blocks sums the
+  // group's partials (block order), the last group to finish sums the groups
+  __syncthreads();
   {
-    const uint32_t me = cluster_ctarank();
-    const int ncol = r + 2;
-    const int per = (ncol + kLateCluster - 1) / kLateCluster;
-    const int c = (int)me * per + (int)threadIdx.x;
-    if ((int)threadIdx.x < per && c < ncol) {
-      double t = 0.0;
-#pragma unroll
-      for (uint32_t q = 0; q < (uint32_t)kLateCluster; ++q) t += ld_dsmem_f64(&cp_s[c], q);
-      cpart[(int64_t)(blockIdx.x / kLateCluster) * (r + 2) + c] = t;
-    }
+    double* mine = cpart + (int64_t)blockIdx.x * (r + 2);
+    for (int c = threadIdx.x; c <= r + 1; c += blockDim.x) mine[c] = cp_s[c];
   }
   __threadfence();
-  cluster_sync();  // no CTA exits while a peer may still read its partials
-  if (threadIdx.x == 0) last = atomicAdd(&look->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  const int grp = blockIdx.x / kLateGroup, ngrp = gridDim.x / kLateGroup;
+  if (threadIdx.x == 0) last = atomicAdd(&gcnt[grp], 1u) == kLateGroup - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // fixed-order reduction of the per-cluster partials (deterministic)
-  const int ncl = gridDim.x / kLateCluster;
+  {
+    const double* base = cpart + (int64_t)grp * kLateGroup * (r + 2);
+    double* gout = cpart + (int64_t)(gridDim.x + grp) * (r + 2);
+    for (int c = threadIdx.x; c <= r + 1; c += blockDim.x) {
+      double v[kLateGroup];
+#pragma unroll
+      for (int q = 0; q < kLateGroup; ++q) v[q] = __ldcg(base + (int64_t)q * (r + 2) + c);
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kLateGroup; ++q) t += v[q];
+      gout[c] = t;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gcnt[grp] = 0;
+    last = atomicAdd(&look->done, 1u) == (unsigned)ngrp - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // fixed-order reduction of the group partials (deterministic)
   for (int cc = threadIdx.x; cc <= r + 1; cc += blockDim.x) {
     double t = 0.0;
-    for (int q = 0; q < ncl; ++q) t += __ldcg(cpart + (int64_t)q * (r + 2) + cc);
+    for (int q = 0; q < ngrp; ++q) t += __ldcg(cpart + (int64_t)(gridDim.x + q) * (r + 2) + cc);
     if (cc <= r) corr[cc] = t;            // c (c_r = t . av)
     else corr[2 * r + 2] = t;             // |av|^2
     if (cc < r) corr[r + 1 + cc] = b[cc];
@@ -2884,21 +2890,26 @@ cudaError_t launch_reset_terms(GrouseState* st, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-static int late_blocks(int k) {  // a multiple of the cluster size
+static int late_blocks(int k) {  // a multiple of the group size
   const int b = std::max(96, (k + kLateRows - 1) / kLateRows);
-  return (b + kLateCluster - 1) / kLateCluster * kLateCluster;
+  return (b + kLateGroup - 1) / kLateGroup * kLateGroup;
 }
 
 cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows_sorted, int k,
                               const double* w, const int32_t* d_idx, const double* d_val,
                               const double* b, const GrouseState* st, GrouseLook* look,
                               double* av, double* cpart, double* corr, cudaStream_t s) {
-  (void)av;
+  // av: the group counters (zeroed by the caller once; the kernel leaves them zero)
   return launch_pdl(k_late, dim3((unsigned)late_blocks(k)), dim3(256), 0, s, A, lda, r,
-                    rows_sorted, k, w, d_idx, d_val, b, st, look, cpart, corr);
+                    rows_sorted, k, w, d_idx, d_val, b, st, look, cpart, corr,
+                    reinterpret_cast<unsigned int*>(av));
 }
 
-size_t late_chain_cpart_doubles(int r, int k) { return (size_t)late_blocks(k) * (r + 2); }
+// per-block partials, then per-group partials
+size_t late_chain_cpart_doubles(int r, int k) {
+  return (size_t)(late_blocks(k) + late_blocks(k) / kLateGroup) * (r + 2);
+}
+size_t late_chain_group_counters(int k) { return (size_t)late_blocks(k) / kLateGroup; }
 
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
                                cudaStream_t s) {
