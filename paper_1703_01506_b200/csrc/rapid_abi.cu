@@ -646,7 +646,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(G.alloc(2 * gsz, s));
   RCUDA(w.alloc(r, s));
   RCUDA(wn.alloc(r, s));
-  RCUDA(vals.alloc(2 * (size_t)k, s));
+  RCUDA(vals.alloc(3 * (size_t)k, s));
   RCUDA(resid.alloc(k, s));
   // + the residual blocks' partials (k_resid_defer_vec -> k_grouse_post_m)
   RCUDA(sums.alloc(8 + 2 * (size_t)((k * 32 + 255) / 256), s));
@@ -656,7 +656,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // length (16-byte aligned rows)
   const int64_t lu = (r + 2) / 2 * 2;
   const size_t ugsz = (size_t)k * lu;
-  RCUDA(ug.alloc(2 * ugsz, s));
+  RCUDA(ug.alloc(3 * ugsz, s));
   DevBuf<double> lav, lcpart, lcorr;
   DevBuf<GrouseLook> lookb;
   // k_late's first-level group counters (it leaves them zero)
@@ -764,17 +764,18 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   auto enqueue_early = [&](int i, const int32_t* idx, int pending, int b, cudaStream_t se,
                            bool marks) -> int {
     const double* trow = t + (int64_t)i * v;
-    double* ugb = ug.p + (size_t)b * ugsz;
+    const int bu = b >> 1, bg = b & 1;  // rows / values buffer (of 3), Gram buffer (of 2)
+    double* ugb = ug.p + (size_t)bu * ugsz;
     // U_Omega = ubase[Omega] M: the raw rows (t[Omega] goes straight into
     // column r of the product's rows), then one k x r x r DGEMM; right after a
     // rebase M = I and the rows are gathered in place
     (void)pending;
     if (m_identity) {
-      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugb, lu, trow, vals.p + (size_t)b * k,
+      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugb, lu, trow, vals.p + (size_t)bu * k,
                                      marks ? sums.p : nullptr, se));
       if (marks) prof.mark(se);
     } else {
-      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugraw.p, lu, trow, vals.p + (size_t)b * k,
+      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugraw.p, lu, trow, vals.p + (size_t)bu * k,
                                      marks ? sums.p : nullptr, se, ugb));
       if (marks) prof.mark(se);
       RCUDA(launch_dgemm_rm(k, r, r, ugraw.p, lu, M.p, r, ugb, lu, 0, se));
@@ -783,7 +784,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(launch_sparse_terms_rows(ugb, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, se));
     if (marks) prof.mark(se);
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
-    RCUDA(launch_dsyrk_rm(k, r + 1, ugb, lu, G.p + (size_t)b * gsz, r + 1, se));
+    RCUDA(launch_dsyrk_rm(k, r + 1, ugb, lu, G.p + (size_t)bg * gsz, r + 1, se));
     if (marks) prof.mark(se);
     return RMX_OK;
   };
@@ -797,9 +798,10 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                           cudaEvent_t h_prev = nullptr, cudaEvent_t post_done = nullptr,
                           cudaEvent_t h_done = nullptr) -> int {
     const double step = 1.0 / (1.0 + (double)tglob / tau);
-    double* ugb = ug.p + (size_t)b * ugsz;
-    double* valsb = vals.p + (size_t)b * k;
-    double* Gb = G.p + (size_t)b * gsz;
+    const int bu = b >> 1, bg = b & 1;
+    double* ugb = ug.p + (size_t)bu * ugsz;
+    double* valsb = vals.p + (size_t)bu * k;
+    double* Gb = G.p + (size_t)bg * gsz;
     if (late)
       RCUDA(launch_late_chain(ugb, lu, r, idx, k, w.p, didx.p, dval.p, wn.p, gst.p, lookb.p,
                               lav.p, lcpart.p, lcorr.p, s));
@@ -932,20 +934,20 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     RCUDA(cudaEventCreateWithFlags(&ls.evP, cudaEventDisableTiming));
   }
   prof_la_mark = prof_la;
-  bool h_pending[2] = {false, false};  // evH[b] was recorded (an H update read buffer b)
   int64_t h_last = -1;                 // the last update whose H update went to s3
   bool have_early = false;  // update tglob's early chain is already in flight on s2
   auto early_on_s2 = [&](int64_t h) -> int {  // after everything enqueued on s so far
     const int hp = (int)(h / ell), hi = (int)(h % ell);
     RCUDA(cudaEventRecord(ls.evD, s));
     RCUDA(cudaStreamWaitEvent(ls.s2, ls.evD, 0));
-    // buffer h & 1 was last read by update h - 2's H update (stream s3)
-    if (h_pending[h & 1]) RCUDA(cudaStreamWaitEvent(ls.s2, ls.evH[h & 1], 0));
+    // rows / values are triple-buffered: buffer h % 3 was last read by update
+    // h - 3, whose H update (stream s3) completed before update h - 2's
+    // residual kernel, so only evD orders this chain
     // terms from updates before h - 1 inclusive when h follows an update in
     // flight (its own term comes with the late chain); every term when cold
     const int pending = (int)((have_early ? h - 1 : h) % kDeferCap);
-    if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending, (int)(h & 1),
-                               ls.s2, false))
+    if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending,
+                               (int)((h % 3) * 2 + (h & 1)), ls.s2, false))
       return rc;
     RCUDA(cudaEventRecord(ls.evE[h & 1], ls.s2));
     return RMX_OK;
@@ -974,12 +976,12 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
         have_early = true;
         if (int rc = early_on_s2(h + 1)) return rc;
       }
-      if (int rc = enqueue_main(i, omegas0 + ((int64_t)p * ell + i) * k, h, false, (int)(h & 1),
+      if (int rc = enqueue_main(i, omegas0 + ((int64_t)p * ell + i) * k, h, false,
+                                (int)((h % 3) * 2 + (h & 1)),
                                 !cold, next ? ls.evE[(h + 1) & 1] : nullptr, ls.s3,
                                 h_last >= 0 ? ls.evH[h_last & 1] : nullptr, ls.evP,
                                 ls.evH[h & 1]))
         return rc;
-      h_pending[h & 1] = true;
       h_last = h;
       while (prof.cur >= 0 && prof.slot < PhaseProf::kPh) prof.mark(s);
       have_early = next;

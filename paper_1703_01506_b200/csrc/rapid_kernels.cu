@@ -913,17 +913,16 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   // staged in shared memory (behind the solver's own buffers, see cg_smem_bytes_c):
   // read from global per element, the correction made the load of G 6x slower
   double* corr_s = cs + cg_corr_offset(r, NC, RL > 0);
-  if (con) {
+  if (con && RL == 0) {  // (register variant: staged below, behind the loads of G)
     for (int e = threadIdx.x; e < 2 * r + 3; e += kCgThreads) corr_s[e] = corr[e];
     __syncthreads();
   }
   const double* cc = corr_s;
   const double* cb = corr_s + (r + 1);
-  const double csq = con ? corr_s[2 * r + 2] : 0.0;
   auto gfix = [&](int i, int j, double g) -> double {  // i, j < r
     if (!con) return g;
     const double bi = cb[i], bj = cb[j];
-    return g + (cc[i] * bj + bi * cc[j]) + csq * bi * bj;
+    return g + (cc[i] * bj + bi * cc[j]) + corr_s[2 * r + 2] * bi * bj;
   };
   auto rhsfix = [&](int j, double g) -> double { return con ? fma(cc[r], cb[j], g) : g; };
   const int R = (r + NC - 1) / NC;  // rows per CTA
@@ -957,8 +956,19 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
 #pragma unroll
       for (int jj = 0; jj < RL; ++jj) {
         const int i = wid + qq * W, j = jj * 32 + lane;
-        greg[qq][jj] = (i < nr && j < r) ? gfix(r0 + i, j, G[(int64_t)(r0 + i) * ld + j]) : 0.0;
+        greg[qq][jj] = (i < nr && j < r) ? G[(int64_t)(r0 + i) * ld + j] : 0.0;
       }
+    if (con) {  // the raw rows are in flight while the correction vectors are staged
+      for (int e = threadIdx.x; e < 2 * r + 3; e += kCgThreads) corr_s[e] = corr[e];
+      __syncthreads();
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int jj = 0; jj < RL; ++jj) {
+          const int i = wid + qq * W, j = jj * 32 + lane;
+          if (i < nr && j < r) greg[qq][jj] = gfix(r0 + i, j, greg[qq][jj]);
+        }
+    }
   } else {
     for (int e = tid; e < nr * r; e += kCgThreads) {
       const int i = e / r, j = e % r;
