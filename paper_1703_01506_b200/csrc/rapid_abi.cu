@@ -657,12 +657,13 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   const int64_t lu = (r + 2) / 2 * 2;
   const size_t ugsz = (size_t)k * lu;
   RCUDA(ug.alloc(3 * ugsz, s));
-  DevBuf<double> lav, lcpart, lcorr;
+  DevBuf<double> lav, lcorr;
+  DevBuf<int32_t> ipos, ilist, icount;  // Omega' /\ Omega_h per rows buffer (k_isect)
   DevBuf<GrouseLook> lookb;
-  // k_late's first-level group counters (it leaves them zero)
-  RCUDA(lav.alloc((late_chain_group_counters(k) + 1) / 2 + 1, s));
-  RCUDA(cudaMemsetAsync(lav.p, 0, ((late_chain_group_counters(k) + 1) / 2 + 1) * sizeof(double), s));
-  RCUDA(lcpart.alloc(late_chain_cpart_doubles(r, k), s));
+  RCUDA(lav.alloc(k, s));
+  RCUDA(ipos.alloc(3 * (size_t)k, s));
+  RCUDA(ilist.alloc(3 * (size_t)k, s));
+  RCUDA(icount.alloc(4, s));
   RCUDA(lcorr.alloc(2 * (size_t)r + 3, s));
   RCUDA(lookb.alloc(1, s));
   RCUDA(cudaMemsetAsync(lookb.p, 0, sizeof(GrouseLook), s));
@@ -762,7 +763,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // `se`.  `pending` bounds the deferred terms it sees (updates since the flush).
   bool m_identity = true;  // no update applied since the last rebase (M = I exactly)
   auto enqueue_early = [&](int i, const int32_t* idx, int pending, int b, cudaStream_t se,
-                           bool marks) -> int {
+                           bool marks, const int32_t* idx_prev = nullptr) -> int {
     const double* trow = t + (int64_t)i * v;
     const int bu = b >> 1, bg = b & 1;  // rows / values buffer (of 3), Gram buffer (of 2)
     double* ugb = ug.p + (size_t)bu * ugsz;
@@ -786,6 +787,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // Gram of [U_Omega | t_Omega] (column r of ug is vals): the full (r+1)^2
     RCUDA(launch_dsyrk_rm(k, r + 1, ugb, lu, G.p + (size_t)bg * gsz, r + 1, se));
     if (marks) prof.mark(se);
+    // look-ahead: the rows this update shares with the previous one (the late
+    // chain adds the previous update's sparse term on them)
+    if (idx_prev)
+      RCUDA(launch_isect(idx, idx_prev, k, ipos.p + (size_t)bu * k, ilist.p + (size_t)bu * k,
+                         icount.p + bu, se));
     return RMX_OK;
   };
   // the rest of the update on the main stream: (late chain,) solve, residual,
@@ -802,15 +808,18 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     double* ugb = ug.p + (size_t)bu * ugsz;
     double* valsb = vals.p + (size_t)bu * k;
     double* Gb = G.p + (size_t)bg * gsz;
-    if (late)
-      RCUDA(launch_late_chain(ugb, lu, r, idx, k, w.p, didx.p, dval.p, wn.p, gst.p, lookb.p,
-                              lav.p, lcpart.p, lcorr.p, s));
+    if (late) {
+      RCUDA(launch_late_chain(ugb, lu, r, k, Gb, w.p, dval.p, ipos.p + (size_t)bu * k,
+                              ilist.p + (size_t)bu * k, icount.p + bu, wn.p, gst.p, lookb.p,
+                              lav.p, lcorr.p, s));
+    }
     if (prof_la_mark) prof.mark(s);
     const bool cg = use_cg && !chol;
     if (cg) {
       RCUDA(launch_cg_solve(Gb, r, w.p, flag.p, sums.p + 4, 1e-13,
                             warm ? wprev.p + (int64_t)i * r : nullptr, s,
-                            late ? lcorr.p : nullptr, late ? lookb.p : nullptr));
+                            late ? lcorr.p : nullptr, late ? lookb.p : nullptr,
+                            late ? lav.p : nullptr, late ? k : 0));
       prof.mark(s);
       if (force_fallback) RCUDA(cudaMemsetAsync(flag.p, 0x01, 1, s));  // tests: flag = 1
     } else {
@@ -822,7 +831,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // update's late chain and solve; H is read again here (hw = H w)
     if (h_prev) RCUDA(cudaStreamWaitEvent(s, h_prev, 0));
     RCUDA(launch_resid_defer_vec(ugb, lu, r, k, valsb, w.p, resid.p, sums.p, H.p, M.p, cmat.p,
-                                 gst.p, hw.p, mw.p, dots.p, s, NT.p, nw.p));
+                                 gst.p, hw.p, mw.p, dots.p, s, NT.p, nw.p, late ? lav.p : nullptr,
+                                 wn.p, lookb.p));
     prof.mark(s);
     RCUDA(launch_grouse_post_m(gst.p, sums.p, flag.p, step, tglob, idx, k, resid.p, w.p, r,
                                didx.p, dval.p, cmat.p, wn.p,
@@ -946,8 +956,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // terms from updates before h - 1 inclusive when h follows an update in
     // flight (its own term comes with the late chain); every term when cold
     const int pending = (int)((have_early ? h - 1 : h) % kDeferCap);
+    const int64_t hm = h - 1;  // the update in flight whose term the late chain will add
+    const int32_t* idx_prev =
+        have_early ? omegas0 + ((hm / ell) * ell + hm % ell) * k : nullptr;
     if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending,
-                               (int)((h % 3) * 2 + (h & 1)), ls.s2, false))
+                               (int)((h % 3) * 2 + (h & 1)), ls.s2, false, idx_prev))
       return rc;
     RCUDA(cudaEventRecord(ls.evE[h & 1], ls.s2));
     return RMX_OK;

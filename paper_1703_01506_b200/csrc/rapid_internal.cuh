@@ -102,7 +102,7 @@ struct GrouseState {
 struct GrouseLook {
   int applied;        // update h added a term (not halted, not degenerate)
   int slot;           // its deferred-term slot (d_idx / d_val row)
-  unsigned int done;  // blocks of k_late finished (last-block reduction)
+  unsigned int done;  // (unused)
   int pad;
   double a;           // pend_a of the update
 };
@@ -129,7 +129,8 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
                                    double* hw, double* mw, double* dots, cudaStream_t s,
-                                   const double* NT, double* nw);
+                                   const double* NT, double* nw, const double* av = nullptr,
+                                   const double* b = nullptr, const GrouseLook* look = nullptr);
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
                                      int64_t ldo, const double* t, double* vals, double* zero8,
                                      cudaStream_t s, double* aug = nullptr);
@@ -142,14 +143,16 @@ cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* f
                                  double* d_val, double* cmat, double* wn, int32_t* final_slot,
                                  const double* hw, int cg_mode, cudaStream_t s,
                                  GrouseLook* look = nullptr);
-// late chain of a look-ahead update (rapid_kernels.cu: k_late):
-// A (k x lda: [U_Omega | t]) += av b^T and corr = (c[0..r], b[0..r], |av|^2)
-cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows_sorted, int k,
-                              const double* w, const int32_t* d_idx, const double* d_val,
-                              const double* b, const GrouseState* st, GrouseLook* look,
-                              double* av, double* cpart, double* corr, cudaStream_t s);
-size_t late_chain_cpart_doubles(int r, int k);
-size_t late_chain_group_counters(int k);  // unsigned ints behind `av` (zeroed once)
+// look-ahead update (rapid_kernels.cu): k_isect (early chain: Omega' /\ Omega_h),
+// k_late (av and corr = (c[0..r], b[0..r], -)); the rank-1 term A += av b^T is
+// applied by k_resid_defer_vec's pass over the rows
+cudaError_t launch_isect(const int32_t* rows_next, const int32_t* rows_prev, int k, int32_t* pos,
+                         int32_t* list, int32_t* count, cudaStream_t s);
+cudaError_t launch_late_chain(const double* A, int64_t lda, int r, int k, const double* G,
+                              const double* w, const double* d_val, const int32_t* pos,
+                              const int32_t* list, const int32_t* count, const double* b,
+                              const GrouseState* st, const GrouseLook* look, double* av,
+                              double* corr, cudaStream_t s);
 // M += a (M w) b^T, its inverse (transposed, NT) likewise, and the older
 // terms' c_s (H: launch_h_update)
 cudaError_t launch_defer_apply(double* M, double* NT, double* cmat, GrouseState* st,
@@ -187,7 +190,8 @@ cudaError_t launch_max_finalize(const uint32_t* enc, int64_t B, double mu, doubl
 bool cg_solve_supported(int r);
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
                             double tol, double* x0, cudaStream_t s, const double* corr = nullptr,
-                            const GrouseLook* look = nullptr);
+                            const GrouseLook* look = nullptr, const double* av = nullptr,
+                            int kav = 0);
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
                                 int64_t perm_base, double sigma, double mu, uint64_t seed,
                                 int two_sided, const float* znoise, const double* base,

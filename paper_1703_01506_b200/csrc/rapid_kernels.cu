@@ -899,7 +899,8 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
                                                          double* __restrict__ resid2, double tol,
                                                          double* __restrict__ x0,
                                                          const double* __restrict__ corr,
-                                                         const GrouseLook* __restrict__ look) {
+                                                         const GrouseLook* __restrict__ look,
+                                                         const double* __restrict__ av, int kav) {
   tr(5, 0);
   pdl_wait();
   tr(5, 1);
@@ -913,10 +914,6 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   // staged in shared memory (behind the solver's own buffers, see cg_smem_bytes_c):
   // read from global per element, the correction made the load of G 6x slower
   double* corr_s = cs + cg_corr_offset(r, NC, RL > 0);
-  if (con && RL == 0) {  // (register variant: staged below, behind the loads of G)
-    for (int e = threadIdx.x; e < 2 * r + 3; e += kCgThreads) corr_s[e] = corr[e];
-    __syncthreads();
-  }
   const double* cc = corr_s;
   const double* cb = corr_s + (r + 1);
   auto gfix = [&](int i, int j, double g) -> double {  // i, j < r
@@ -945,6 +942,27 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
     mbar_init(&xbar[1], 1);
     fence_mbar_init();
   }
+  // c and b from k_late, |av|^2 summed here (fixed order: thread strides, xor
+  // tree, warps in order -- every CTA gets the same bits)
+  auto stage_corr = [&]() {
+    double* avp = wsum;  // free until the first exchange
+    for (int e = threadIdx.x; e < 2 * r + 2; e += kCgThreads) corr_s[e] = corr[e];
+    double ps = 0.0;
+    for (int i = threadIdx.x; i < kav; i += kCgThreads) {
+      const double x = av[i];
+      ps = fma(x, x, ps);
+    }
+    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    if ((threadIdx.x & 31) == 0) avp[threadIdx.x >> 5] = ps;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kCgThreads / 32; ++q) t += avp[q];
+      corr_s[2 * r + 2] = t;
+    }
+    __syncthreads();
+  };
+  if (con && RL == 0) stage_corr();  // (register variant: staged below, behind the loads of G)
   // RL > 0: the CTA's rows of G in registers (r <= 32 RL, at most 4 rows per warp)
   constexpr int kRL = RL > 0 ? RL : 1;
   double greg[4][kRL];
@@ -959,8 +977,7 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
         greg[qq][jj] = (i < nr && j < r) ? G[(int64_t)(r0 + i) * ld + j] : 0.0;
       }
     if (con) {  // the raw rows are in flight while the correction vectors are staged
-      for (int e = threadIdx.x; e < 2 * r + 3; e += kCgThreads) corr_s[e] = corr[e];
-      __syncthreads();
+      stage_corr();
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
 #pragma unroll
@@ -1264,13 +1281,26 @@ __device__ __forceinline__ void resid_block(int bid, const double* __restrict__ 
                                             const double* __restrict__ vals,
                                             const double* __restrict__ w,
                                             double* __restrict__ resid, double* __restrict__ sums,
-                                            double* __restrict__ rpart = nullptr) {
+                                            double* __restrict__ rpart = nullptr,
+                                            const double* __restrict__ av = nullptr,
+                                            const double* __restrict__ b = nullptr) {
   __shared__ double part[2][8];  // blockDim.x == 256
   const int warp = (bid * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   double ee = 0.0, tt = 0.0;
   if (warp < k) {
     const double* u = U + (int64_t)(idx ? idx[warp] : warp) * ldu;
     double s = 0.0;
+    if (av) {
+      // look-ahead: the previous update's rank-1 term av b^T goes onto the row
+      // here (the rows were gathered before it; k_h_g_part reads them next)
+      double* um = const_cast<double*>(u);
+      const double a = av[warp];
+      for (int c = lane; c < r; c += 32) {
+        const double x = fma(a, b[c], um[c]);
+        um[c] = x;
+        s += x * w[c];
+      }
+    } else
     for (int c = lane; c < r; c += 32) s += u[c] * w[c];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const double e = vals[warp] - s;
@@ -1617,12 +1647,15 @@ __global__ void k_resid_defer_vec(const double* __restrict__ U, int64_t ldu, int
                                   const GrouseState* __restrict__ st, double* __restrict__ hw,
                                   double* __restrict__ mw, double* __restrict__ dots, int nres,
                                   double* __restrict__ rpart, const double* __restrict__ NT,
-                                  double* __restrict__ nw) {
+                                  double* __restrict__ nw, const double* __restrict__ av,
+                                  const double* __restrict__ b,
+                                  const GrouseLook* __restrict__ look) {
   tr(6, 0);
   pdl_wait();
   tr(6, 1);
   if ((int)blockIdx.x < nres)
-    resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums, rpart);
+    resid_block(blockIdx.x, U, ldu, r, nullptr, k, vals, w, resid, sums, rpart,
+                (av && look->applied && !st->halted) ? av : nullptr, b);
   else
     defer_vec_block(blockIdx.x - nres, H, M, cmat, w, r, st, hw, mw, dots, NT, nw);
 }
@@ -1834,152 +1867,113 @@ __global__ void k_defer_apply(double* __restrict__ M, double* __restrict__ NT,
 
 
 // ---- look-ahead GROUSE: the late chain of update h + 1
-// The early chain (gather, deferred products, sparse terms, Gram) of update
+// The early chain (gather, product with M, sparse terms, Gram) of update
 // h + 1 runs on a second stream while update h is solved, from the state
 // before update h: A = [U_Omega' | t_Omega'] and G = A^T A without update h's
 // term.  Update h is U <- U (I + a w b^T) + d b^T (b = w / |w|, d = pend_b
 // resid on Omega_h), so on the rows Omega' of update h + 1
 //   A' = A + av b^T,  av = a (A w) + d|Omega',
 //   G' = G + c b^T + b c^T + |av|^2 b b^T,  c = A^T av (b_r = 0: the t column).
-// k_late (one launch): per block of rows, av (warp per row; d by a search of
-// Omega_h's sorted list), then the block's partials of c and |av|^2 and the
-// rank-1 term applied to its rows; the partials are reduced in two levels in
-// a fixed order (deterministic).  The cluster CG adds the correction to G as
-// it loads its rows (corr).
-constexpr int kLateRows = 32;    // rows of A per block (at most)
-constexpr int kLateGroup = 8;    // blocks per first-level reduction group
+// Since A^T A = G is already there, c = a (G w) + A^T d|Omega' needs no pass
+// over all rows: d|Omega' is non-zero only on Omega' /\ Omega_h (k^2 / v rows
+// on average), which the early chain lists (k_isect).  On the critical path
+// k_late is one launch without reductions: row warps form av, column warps
+// form c; the solve sums |av|^2 itself and adds the correction to G as it
+// loads its rows (corr); the rank-1 term goes onto the rows in the residual
+// kernel's pass over them (k_resid_defer_vec), before k_h_g_part reads them.
 
+// Early chain: pos[q] = index of Omega'[q] in the sorted Omega_h (or -1) and
+// the ascending list of the q that are present.  One block; ordered compaction.
+__global__ void __launch_bounds__(1024) k_isect(const int32_t* __restrict__ rows_next,
+                                                const int32_t* __restrict__ rows_prev, int k,
+                                                int32_t* __restrict__ pos,
+                                                int32_t* __restrict__ list,
+                                                int32_t* __restrict__ count) {
+  pdl_wait();
+  __shared__ int wcnt[32];
+  __shared__ int base_s;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int top = 1;
+  while (top * 2 <= k) top *= 2;
+  for (int q0 = 0; q0 < k; q0 += blockDim.x) {
+    const int q = q0 + threadIdx.x;
+    int found = -1;
+    if (q < k) {
+      const int32_t vox = __ldg(rows_next + q);
+      int p = 0;
+      for (int step = top; step > 0; step >>= 1)
+        if (p + step < k && __ldg(rows_prev + p + step) <= vox) p += step;
+      if (__ldg(rows_prev + p) == vox) found = p;
+      pos[q] = found;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
+    if (lane == 0) wcnt[wid] = __popc(m);
+    __syncthreads();
+    int before = base_s;
+    for (int ww = 0; ww < wid; ++ww) before += wcnt[ww];
+    if (found >= 0) list[before + __popc(m & ((1u << lane) - 1u))] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) t += wcnt[ww];
+      base_s += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base_s;
+}
+
+// grid: nrb row blocks (8 rows each, warp per row) then column blocks (8
+// columns each, warp per column of [U_Omega' | t], r + 1 columns)
 __global__ void __launch_bounds__(256) k_late(
-    double* __restrict__ A, int64_t lda, int r, const int32_t* __restrict__ rows_sorted, int k,
-    const double* __restrict__ w, const int32_t* __restrict__ d_idx,
-    const double* __restrict__ d_val, const double* __restrict__ b,
-    const GrouseState* __restrict__ st, GrouseLook* __restrict__ look,
-    double* __restrict__ cpart, double* __restrict__ corr, unsigned int* __restrict__ gcnt) {
+    const double* __restrict__ A, int64_t lda, int r, int k, const double* __restrict__ G,
+    const double* __restrict__ w, const double* __restrict__ d_val,
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ list,
+    const int32_t* __restrict__ count, const double* __restrict__ b,
+    const GrouseState* __restrict__ st, const GrouseLook* __restrict__ look,
+    double* __restrict__ av, double* __restrict__ corr, int nrb) {
   pdl_trigger();  // the solve becomes resident (and claims its cluster's SMs) while this runs
   tr(4, 0);
   pdl_wait();
   tr(4, 1);
   if (st->halted || !look->applied) return;
-  __shared__ double av_s[kLateRows];
-  __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int rows = (k + gridDim.x - 1) / gridDim.x;  // <= kLateRows (launcher)
-  const int i0 = blockIdx.x * rows, i1 = min(k, i0 + rows);
-  const int nloc = max(0, i1 - i0);
-  const int slot = look->slot;
   const double a = look->a;
-  // av = a (A w) + d|Omega': warp per row; the row's voxel is searched in
-  // Omega_h's sorted list by one lane per row, the warp's rows in parallel
-  {
-    constexpr int kPerWarp = kLateRows / 8;
-    double dot[kPerWarp];
-#pragma unroll
-    for (int q = 0; q < kPerWarp; ++q) {
-      const int li = wid + q * 8;
-      double sacc = 0.0;
-      if (li < nloc) {
-        const double* row = A + (int64_t)(i0 + li) * lda;
-        for (int c = lane; c < r; c += 32) sacc = fma(row[c], w[c], sacc);
-      }
-      dot[q] = sacc;
+  const double* dv = d_val + (int64_t)look->slot * k;
+  if ((int)blockIdx.x < nrb) {  // av = a (A w) + d|Omega'
+    const int q = blockIdx.x * 8 + wid;
+    if (q >= k) return;
+    const double* row = A + (int64_t)q * lda;
+    double sacc = 0.0;
+    for (int c = lane; c < r; c += 32) sacc = fma(row[c], w[c], sacc);
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) {
+      const int p = pos[q];
+      av[q] = fma(a, sacc, p >= 0 ? dv[p] : 0.0);
     }
-#pragma unroll
-    for (int q = 0; q < kPerWarp; ++q)
-      for (int o = 16; o > 0; o >>= 1) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
-    // lane q searches row (wid + 8 q)
-    double mine = 0.0;
-    int li = -1;
-#pragma unroll
-    for (int q = 0; q < kPerWarp; ++q)
-      if (lane == q) {
-        mine = dot[q];
-        li = wid + q * 8;
-      }
-    if (li >= 0 && li < nloc) {
-      const int32_t vox = __ldg(rows_sorted + i0 + li);
-      const int32_t* di = d_idx + (int64_t)slot * k;
-      int p = 0, step = 1;
-      while (step * 2 <= k) step *= 2;
-      for (; step > 0; step >>= 1)
-        if (p + step < k && __ldg(di + p + step) <= vox) p += step;
-      const double d = __ldg(di + p) == vox ? d_val[(int64_t)slot * k + p] : 0.0;
-      av_s[li] = fma(a, mine, d);
-    }
+    return;
   }
-  __syncthreads();
-  // c partials over this block's rows (column r is the t column) and the
-  // rank-1 term on the rows: thread per column, every row's load in flight
-  // before the first store
-  __shared__ double cp_s[2 * 256 + 2];  // the block's partial c (r + 1 <= 512) and |av|^2
-  for (int c = threadIdx.x; c <= r; c += blockDim.x) {
-    const double bc = c < r ? b[c] : 0.0;
-    double* pc = A + (int64_t)i0 * lda + c;
-    double x[kLateRows];
-#pragma unroll
-    for (int q = 0; q < kLateRows; ++q) x[q] = q < nloc ? __ldcg(pc + (int64_t)q * lda) : 0.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < kLateRows; ++q)
-      if (q < nloc) {
-        const double ai = av_s[q];
-        acc = fma(x[q], ai, acc);
-        if (c < r) pc[(int64_t)q * lda] = fma(ai, bc, x[q]);
-      }
-    cp_s[c] = acc;
+  // c_j = a (G w)_j + sum over the common rows of A[q][j] d_q   (j <= r)
+  const int j = ((int)blockIdx.x - nrb) * 8 + wid;
+  if (j > r) return;
+  const double* grow = G + (int64_t)j * (r + 1);
+  double gacc = 0.0;
+  for (int c = lane; c < r; c += 32) gacc = fma(grow[c], w[c], gacc);
+  for (int o = 16; o > 0; o >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, o);
+  const int n = *count;
+  double sp = 0.0;
+  for (int e = lane; e < n; e += 32) {
+    const int q = list[e];
+    sp = fma(A[(int64_t)q * lda + j], dv[pos[q]], sp);
   }
-  if (threadIdx.x == 0) {
-    double ss = 0.0;
-    for (int i = 0; i < nloc; ++i) ss = fma(av_s[i], av_s[i], ss);
-    cp_s[r + 1] = ss;
-  }
-  // two-level fixed-order reduction without a serial pass over every block's
-  // partials: the last block of each group of kLateGroup blocks sums the
-  // group's partials (block order), the last group to finish sums the groups
-  __syncthreads();
-  {
-    double* mine = cpart + (int64_t)blockIdx.x * (r + 2);
-    for (int c = threadIdx.x; c <= r + 1; c += blockDim.x) mine[c] = cp_s[c];
-  }
-  __threadfence();
-  __syncthreads();
-  const int grp = blockIdx.x / kLateGroup, ngrp = gridDim.x / kLateGroup;
-  if (threadIdx.x == 0) last = atomicAdd(&gcnt[grp], 1u) == kLateGroup - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  {
-    const double* base = cpart + (int64_t)grp * kLateGroup * (r + 2);
-    double* gout = cpart + (int64_t)(gridDim.x + grp) * (r + 2);
-    for (int c = threadIdx.x; c <= r + 1; c += blockDim.x) {
-      double v[kLateGroup];
-#pragma unroll
-      for (int q = 0; q < kLateGroup; ++q) v[q] = __ldcg(base + (int64_t)q * (r + 2) + c);
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < kLateGroup; ++q) t += v[q];
-      gout[c] = t;
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    gcnt[grp] = 0;
-    last = atomicAdd(&look->done, 1u) == (unsigned)ngrp - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // fixed-order reduction of the group partials (deterministic)
-  for (int cc = threadIdx.x; cc <= r + 1; cc += blockDim.x) {
-    double t = 0.0;
-    for (int q = 0; q < ngrp; ++q) t += __ldcg(cpart + (int64_t)(gridDim.x + q) * (r + 2) + cc);
-    if (cc <= r) corr[cc] = t;            // c (c_r = t . av)
-    else corr[2 * r + 2] = t;             // |av|^2
-    if (cc < r) corr[r + 1 + cc] = b[cc];
-  }
-  if (threadIdx.x == 0) {
-    corr[2 * r + 1] = 0.0;  // b_r
-    look->done = 0;
+  // fixed order: lanes hold e = lane, lane + 32, ...; xor tree (deterministic)
+  for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+  if (lane == 0) {
+    corr[j] = fma(a, gacc, sp);
+    if (j < r) corr[r + 1 + j] = b[j];
+    else corr[2 * r + 1] = 0.0;  // b_r
   }
 }
 
@@ -2679,7 +2673,8 @@ bool cg_solve_supported(int r) { return cg_smem_bytes(r) <= 200 * 1024; }
 template <int C, int RL = 0>
 cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* flag,
                               double* resid2, double tol, double* x0, cudaStream_t s,
-                              const double* corr, const GrouseLook* look) {
+                              const double* corr, const GrouseLook* look, const double* av,
+                              int kav) {
   // the register-resident variant keeps no copy of G in shared memory
   const size_t smem =
       cg_smem_bytes_c(r, C) - (RL > 0 ? (size_t)((r + C - 1) / C) * r * sizeof(double) : 0);
@@ -2705,20 +2700,22 @@ cudaError_t launch_cg_solve_c(const double* G, int r, double* w_out, int32_t* fl
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_cg_solve<C, RL>, G, r, w_out, flag, resid2, tol, x0, corr,
-                            look);
+                            look, av, kav);
 }
 
 cudaError_t launch_cg_solve(const double* G, int r, double* w_out, int32_t* flag, double* resid2,
                             double tol, double* x0, cudaStream_t s, const double* corr,
-                            const GrouseLook* look) {
+                            const GrouseLook* look, const double* av, int kav) {
   // rows of G in registers when each warp holds at most 4 rows of <= 416
   // columns (RMX_CG_SMEM=1: the shared-memory variant)
   const bool reg = r <= 13 * 32 && (r + kCgCtas - 1) / kCgCtas <= 4 * (kCgThreads / 32) &&
                    !getenv("RMX_CG_SMEM");
   if (cg_ctas() == 8)
-    return launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
-  if (reg) return launch_cg_solve_c<kCgCtas, 13>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
-  return launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s, corr, look);
+    return launch_cg_solve_c<8>(G, r, w_out, flag, resid2, tol, x0, s, corr, look, av, kav);
+  if (reg)
+    return launch_cg_solve_c<kCgCtas, 13>(G, r, w_out, flag, resid2, tol, x0, s, corr, look, av,
+                                          kav);
+  return launch_cg_solve_c<kCgCtas>(G, r, w_out, flag, resid2, tol, x0, s, corr, look, av, kav);
 }
 
 cudaError_t launch_complete_max(const float* U, int64_t v, int r, const float* W, int64_t B,
@@ -2840,13 +2837,15 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
                                    double* hw, double* mw, double* dots, cudaStream_t s,
-                                   const double* NT, double* nw) {
+                                   const double* NT, double* nw, const double* av,
+                                   const double* b, const GrouseLook* look) {
   const int nres = (k * 32 + 255) / 256;
   const int ndv = (3 * r + kDeferCap + 7) / 8;
   // sums[0] / sums[2] (|resid|^2, |t_Omega|^2): per-block partials in
   // sums + 8.., reduced in a fixed order by k_grouse_post_m (deterministic)
   return launch_pdl(k_resid_defer_vec, dim3((unsigned)(nres + ndv)), dim3(256), 0, s, U, ldu, r, k,
-                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres, sums + 8, NT, nw);
+                    vals, w, resid, sums, H, M, cmat, st, hw, mw, dots, nres, sums + 8, NT, nw, av,
+                    b, look);
 }
 
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
@@ -2900,26 +2899,20 @@ cudaError_t launch_reset_terms(GrouseState* st, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-static int late_blocks(int k) {  // a multiple of the group size
-  const int b = std::max(96, (k + kLateRows - 1) / kLateRows);
-  return (b + kLateGroup - 1) / kLateGroup * kLateGroup;
+cudaError_t launch_isect(const int32_t* rows_next, const int32_t* rows_prev, int k, int32_t* pos,
+                         int32_t* list, int32_t* count, cudaStream_t s) {
+  return launch_pdl(k_isect, dim3(1), dim3(1024), 0, s, rows_next, rows_prev, k, pos, list, count);
 }
 
-cudaError_t launch_late_chain(double* A, int64_t lda, int r, const int32_t* rows_sorted, int k,
-                              const double* w, const int32_t* d_idx, const double* d_val,
-                              const double* b, const GrouseState* st, GrouseLook* look,
-                              double* av, double* cpart, double* corr, cudaStream_t s) {
-  // av: the group counters (zeroed by the caller once; the kernel leaves them zero)
-  return launch_pdl(k_late, dim3((unsigned)late_blocks(k)), dim3(256), 0, s, A, lda, r,
-                    rows_sorted, k, w, d_idx, d_val, b, st, look, cpart, corr,
-                    reinterpret_cast<unsigned int*>(av));
+cudaError_t launch_late_chain(const double* A, int64_t lda, int r, int k, const double* G,
+                              const double* w, const double* d_val, const int32_t* pos,
+                              const int32_t* list, const int32_t* count, const double* b,
+                              const GrouseState* st, const GrouseLook* look, double* av,
+                              double* corr, cudaStream_t s) {
+  const int nrb = (k + 7) / 8, ncb = (r + 1 + 7) / 8;
+  return launch_pdl(k_late, dim3((unsigned)(nrb + ncb)), dim3(256), 0, s, A, lda, r, k, G, w,
+                    d_val, pos, list, count, b, st, look, av, corr, nrb);
 }
-
-// per-block partials, then per-group partials
-size_t late_chain_cpart_doubles(int r, int k) {
-  return (size_t)(late_blocks(k) + late_blocks(k) / kLateGroup) * (r + 2);
-}
-size_t late_chain_group_counters(int k) { return (size_t)late_blocks(k) / kLateGroup; }
 
 cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
                                cudaStream_t s) {
