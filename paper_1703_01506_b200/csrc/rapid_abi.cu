@@ -670,7 +670,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   RCUDA(ualt.alloc((size_t)v * r, s));  // the rebase target (U_base M), swapped with U_base
   RCUDA(M.alloc((size_t)r * r, s));
   RCUDA(NT.alloc((size_t)r * r, s));    // (M^-1)^T, tracked for the sparse flush
-  RCUDA(ugraw.alloc(ugsz, s));          // gathered rows of U_base before the product with M
+  RCUDA(ugraw.alloc(2 * ugsz, s));      // gathered rows of U_base before the product with M (x2)
   RCUDA(cmat.alloc((size_t)kDeferCap * r, s));
   RCUDA(ctil.alloc((size_t)kDeferCap * r, s));
   RCUDA(nw.alloc(r, s));
@@ -762,24 +762,35 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // Omega with the deferred terms, and the Gram, into buffer `b`, on stream
   // `se`.  `pending` bounds the deferred terms it sees (updates since the flush).
   bool m_identity = true;  // no update applied since the last rebase (M = I exactly)
+  // the raw rows of U_base on Omega (and t[Omega] into column r of the product's
+  // rows): depends only on U_base, so the look-ahead loop issues it one update
+  // further ahead than the rest of the early chain
+  auto enqueue_gather = [&](int i, const int32_t* idx, int b, cudaStream_t se, bool marks) -> int {
+    const double* trow = t + (int64_t)i * v;
+    const int bu = b >> 1, bg = b & 1;
+    RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugraw.p + (size_t)bg * ugsz, lu, trow,
+                                   vals.p + (size_t)bu * k, marks ? sums.p : nullptr, se,
+                                   ug.p + (size_t)bu * ugsz));
+    return RMX_OK;
+  };
   auto enqueue_early = [&](int i, const int32_t* idx, int pending, int b, cudaStream_t se,
-                           bool marks, const int32_t* idx_prev = nullptr) -> int {
+                           bool marks, const int32_t* idx_prev = nullptr,
+                           bool gathered = false) -> int {
     const double* trow = t + (int64_t)i * v;
     const int bu = b >> 1, bg = b & 1;  // rows / values buffer (of 3), Gram buffer (of 2)
     double* ugb = ug.p + (size_t)bu * ugsz;
-    // U_Omega = ubase[Omega] M: the raw rows (t[Omega] goes straight into
-    // column r of the product's rows), then one k x r x r DGEMM; right after a
-    // rebase M = I and the rows are gathered in place
+    // U_Omega = ubase[Omega] M: the raw rows, then one k x r x r DGEMM; right
+    // after a rebase M = I and the rows are gathered in place
     (void)pending;
-    if (m_identity) {
+    if (m_identity && !gathered) {
       RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugb, lu, trow, vals.p + (size_t)bu * k,
                                      marks ? sums.p : nullptr, se));
       if (marks) prof.mark(se);
     } else {
-      RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugraw.p, lu, trow, vals.p + (size_t)bu * k,
-                                     marks ? sums.p : nullptr, se, ugb));
+      if (!gathered)
+        if (int rc = enqueue_gather(i, idx, b, se, marks)) return rc;
       if (marks) prof.mark(se);
-      RCUDA(launch_dgemm_rm(k, r, r, ugraw.p, lu, M.p, r, ugb, lu, 0, se));
+      RCUDA(launch_dgemm_rm(k, r, r, ugraw.p + (size_t)bg * ugsz, lu, M.p, r, ugb, lu, 0, se));
     }
     if (marks) prof.mark(se);
     RCUDA(launch_sparse_terms_rows(ugb, lu, r, idx, k, didx.p, dval.p, cmat.p, gst.p, se));
@@ -945,6 +956,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   }
   prof_la_mark = prof_la;
   int64_t h_last = -1;                 // the last update whose H update went to s3
+  int64_t pregathered = -1;            // update whose raw rows are already gathered (s2)
   bool have_early = false;  // update tglob's early chain is already in flight on s2
   auto early_on_s2 = [&](int64_t h) -> int {  // after everything enqueued on s so far
     const int hp = (int)(h / ell), hi = (int)(h % ell);
@@ -959,10 +971,25 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     const int64_t hm = h - 1;  // the update in flight whose term the late chain will add
     const int32_t* idx_prev =
         have_early ? omegas0 + ((hm / ell) * ell + hm % ell) * k : nullptr;
+    const bool gathered = pregathered == h;
+    if (!have_early) pregathered = -1;  // cold start: nothing issued ahead survives
     if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending,
-                               (int)((h % 3) * 2 + (h & 1)), ls.s2, false, idx_prev))
+                               (int)((h % 3) * 2 + (h & 1)), ls.s2, false, idx_prev,
+                               have_early && gathered))
       return rc;
     RCUDA(cudaEventRecord(ls.evE[h & 1], ls.s2));
+    // the gather of update h + 1 behind this chain (it only needs U_base, which
+    // changes at checkpoints), so it runs beside the current solve's iterations
+    // instead of beside the next solve's load of G.  Its buffers (h + 1) % 3
+    // were last read by update h - 2, H update included (evH).
+    const int64_t g = h + 1;
+    if (have_early && g < total && !is_checkpoint(g) && h_last >= 0 && h_last == h - 2) {
+      RCUDA(cudaStreamWaitEvent(ls.s2, ls.evH[h_last & 1], 0));
+      if (int rc = enqueue_gather((int)(g % ell), omegas0 + g * k, (int)((g % 3) * 2 + (g & 1)),
+                                  ls.s2, false))
+        return rc;
+      pregathered = g;
+    }
     return RMX_OK;
   };
   while (tglob < total) {
