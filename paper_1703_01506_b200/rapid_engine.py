@@ -429,7 +429,8 @@ def _d2h_async(t, dest):
 
 
 def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
-                        max_passes: int, tolerance: float, init=None, host_basis: bool = False):
+                        max_passes: int, tolerance: float, init=None, host_basis: bool = False,
+                        before_grouse=None):
     """GROUSE on device.  t_dev: (ell, v) fp64 training statistics; init: a
     joiner from _basis_init_async (else the normals are drawn here)."""
     torch = _torch()
@@ -460,6 +461,8 @@ def _train_basis_device(t_dev, v: int, ell: int, k: int, rank: int, seed: int,
             return 1
 
     cbf = nat.OMEGA_CB(cb)
+    if before_grouse is not None:
+        before_grouse()
     nat.call("rmx_grouse_train", nat.ptr(t_dev), v, ell, rank, k, nat.ptr(om_dev), max_passes,
              float(tolerance), nat.ptr(u), cbf, None, pass_resid, ctypes.byref(passes),
              ctypes.byref(conv), ctypes.byref(updates), nat.ptr(final), _stream(dev))
@@ -611,12 +614,24 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
         torch.cuda.synchronize()
     hi_prio = torch.cuda.Stream(dev, priority=-100)  # mapped to the highest priority
     hi_prio.wait_stream(torch.cuda.current_stream(dev))
+    pre_box = {}
+
+    def prefetch_first():
+        # GROUSE's three-stream chain is latency-bound end to end: resident
+        # blocks of the prefetch's kernels beside it cost it more than their own
+        # duration (config 5: +1.0 s for 0.6 s of prefetch), so the prefetch --
+        # which has had the GPU to itself while the host drew the BASIS_INIT
+        # normals -- finishes before the first update starts
+        if pre_join is not None and not os.environ.get("RMX_PREFETCH_BESIDE_GROUSE"):
+            pre_box["r"] = pre_join()
+            torch.cuda.current_stream(dev).wait_event(pre_box["r"][1])
+
     with torch.cuda.stream(hi_prio):
         if pre_join is not None and pf_ev:
             pf_ev[2].record(hi_prio)
         u, final, passes, conv, _, _, host_u = _train_basis_device(
             t_dev, v, ell, k, rank, cfg.seed, cfg.max_passes, cfg.tolerance, init,
-            host_basis=prefetch_recovery)
+            host_basis=prefetch_recovery, before_grouse=prefetch_first)
     if pre_join is not None and pf_ev:
         pf_ev[3].record(hi_prio)
         torch.cuda.synchronize()
@@ -628,7 +643,7 @@ def _train_device(x, cfg, prefetch_recovery: bool = False):
     for tnsr in (u, final):
         tnsr.record_stream(torch.cuda.current_stream(dev))
     if pre_join is not None:
-        pre, done = pre_join()
+        pre, done = pre_box["r"] if "r" in pre_box else pre_join()
         cur = torch.cuda.current_stream(dev)
         cur.wait_event(done)
         for tnsr in (pre.od, pre.omd, pre.t):
