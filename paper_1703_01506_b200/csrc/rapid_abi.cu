@@ -880,6 +880,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   // waiting at the checkpoints (a wait near zero = the host is the bound)
   const bool hostprof = getenv("RMX_GROUSE_HOSTPROF") != nullptr;
   double host_wait_s = 0.0;
+  int reorth_count = 0;
   const auto host_t0 = std::chrono::steady_clock::now();
   auto read_state = [&](GrouseState* h) -> int {
     const auto w0 = std::chrono::steady_clock::now();
@@ -1095,6 +1096,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
           m_identity = true;
         }
         if (reorth) {
+          ++reorth_count;
           double drift = 0.0;
           if (int rc = rmx_orthonormalize(ubase, v, r, 1, &drift, stream, st)) return rc;
           RCUDA(launch_h_identity(H.p, r, s));
@@ -1147,9 +1149,11 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     }
   }
   if (hostprof)
-    fprintf(stderr, "{\"grouse_host\": {\"loop_s\": %.3f, \"checkpoint_wait_s\": %.3f, \"lookahead\": %d}}\n",
+    fprintf(stderr,
+            "{\"grouse_host\": {\"loop_s\": %.3f, \"checkpoint_wait_s\": %.3f, \"lookahead\": %d, "
+            "\"reorthonormalisations\": %d}}\n",
             std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count(),
-            host_wait_s, lookahead ? 1 : 0);
+            host_wait_s, lookahead ? 1 : 0, reorth_count);
   if (getenv("RMX_CG_STATS")) {
     unsigned long long cs[2] = {0, 0}, ph[6] = {0, 0, 0, 0, 0, 0};
     cudaStreamSynchronize(s);

@@ -115,16 +115,6 @@ cudaError_t launch_sparse_terms_rows(double* out, int64_t ldo, int r, const int3
 cudaError_t launch_sparse_terms_dense(double* out, int64_t ldo, int r, int k, const int32_t* d_idx,
                                       const double* d_val, const double* cmat, int nterms,
                                       cudaStream_t s);
-cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
-                                const int32_t* d_idx, const double* d_val, const double* cmat,
-                                const GrouseState* st, int dense, cudaStream_t s);
-cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
-                                cudaStream_t s);
-cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, int k, double* out,
-                                   int64_t ldo, cudaStream_t s);
-// vals[i] = t[idx[i]] and aug[i * ldaug] = the same (the Gram's extra column)
-cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
-                                   double* aug, int64_t ldaug, cudaStream_t s);
 cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
@@ -134,9 +124,6 @@ cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, c
 cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx, int k, double* out,
                                      int64_t ldo, const double* t, double* vals, double* zero8,
                                      cudaStream_t s, double* aug = nullptr);
-cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
-                             const double* w, int r, const GrouseState* st, double* hw, double* mw,
-                             double* dots, cudaStream_t s, const double* NT, double* nw);
 cudaError_t launch_grouse_post_m(GrouseState* st, double* sums, const int32_t* flag,
                                  double step, int64_t step_index, const int32_t* idx, int k,
                                  const double* resid, const double* w, int r, int32_t* d_idx,
@@ -164,8 +151,6 @@ cudaError_t launch_ctil(const double* NT, const double* cmat, int r, int nterms,
 cudaError_t launch_reset_terms(GrouseState* st, cudaStream_t s);
 // test hook: mark update `step` as halted (ill-conditioned) before it runs
 cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s);
-cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
-                               cudaStream_t s);
 // H = U^T U tracked through the rank-1 updates (the every-64-updates drift
 // check of lrmc.py:258-259 without a 168 GFLOP Gram)
 cudaError_t launch_h_update(double* H, int r, const GrouseState* st, const double* hw,

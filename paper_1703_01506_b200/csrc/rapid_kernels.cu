@@ -623,11 +623,6 @@ __device__ __forceinline__ void st_async_f64(double* local_ptr, uint32_t rank, d
                : "memory");
 }
 
-__device__ __forceinline__ void st_cluster_f64(double* local_ptr, uint32_t rank, double v) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_ptr)), "r"(rank));
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
-}
 
 
 // Pipelined preconditioned CG (Ghysels & Vanroose, p-PCG): besides x, r,
@@ -1533,65 +1528,6 @@ __global__ void k_sparse_term_dense(double* __restrict__ out, int64_t ldo, int r
   out[(int64_t)di[q] * ldo + c] += dv[q] * cs[c];
 }
 
-__global__ void k_sparse_terms(double* __restrict__ out, int64_t ldo, int r,
-                               const int32_t* __restrict__ rows_sorted, int k,
-                               const int32_t* __restrict__ d_idx, const double* __restrict__ d_val,
-                               const double* __restrict__ cmat, const GrouseState* __restrict__ st,
-                               int dense) {
-  pdl_wait();
-  __shared__ int64_t hit_row[256];
-  __shared__ double hit_val[256];
-  __shared__ int nhit;
-  const int sterm = blockIdx.x;
-  if (st->halted || sterm >= st->nterms) return;
-  const int32_t* di = d_idx + (int64_t)sterm * k;
-  const double* dv = d_val + (int64_t)sterm * k;
-  const double* cs = cmat + (int64_t)sterm * r;
-  if (threadIdx.x == 0) nhit = 0;
-  __syncthreads();
-  const int q = blockIdx.y * 256 + threadIdx.x;
-  if (q < k) {
-    const int32_t vox = di[q];
-    int64_t row = -1;
-    if (dense) {
-      row = vox;
-    } else {  // position of vox in the sorted Omega, if present
-      int lo = 0, hi = k - 1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const int32_t x = __ldg(rows_sorted + mid);
-        if (x == vox) {
-          row = mid;
-          break;
-        }
-        if (x < vox) lo = mid + 1;
-        else hi = mid - 1;
-      }
-    }
-    if (row >= 0) {
-      const int slot = atomicAdd(&nhit, 1);
-      hit_row[slot] = row;
-      hit_val[slot] = dv[q];
-    }
-  }
-  __syncthreads();
-  const int n = nhit;
-  for (int h = 0; h < n; ++h) {  // the block adds d_q c_s^T to the hit rows
-    double* o = out + hit_row[h] * ldo;
-    const double dq = hit_val[h];
-    for (int c = threadIdx.x; c < r; c += blockDim.x) atomicAdd(o + c, dq * cs[c]);
-  }
-}
-
-// gathered rows of U (k x r, row-major) for the cuBLAS product with M
-__global__ void k_gather_urows(const double* __restrict__ U, int r, const int32_t* __restrict__ idx,
-                               int k, double* __restrict__ out, int64_t ldo) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)k * r) return;
-  const int i = (int)(e / r), c = (int)(e - (int64_t)i * r);
-  out[(int64_t)i * ldo + c] = U[(int64_t)idx[i] * r + c];
-}
-
 // Per-update matrix-vector products, one warp per output (coalesced rows):
 // hw = H w (for |p|^2 = w.hw and the H update), mw = M w (the M update) and
 // dots[s] = w . c_s for the live terms.
@@ -1627,14 +1563,6 @@ __device__ __forceinline__ void defer_vec_block(int bid, const double* __restric
   for (int j = lane; j < r; j += 32) acc = fma(row[j], w[j], acc);
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) *out = acc;
-}
-
-__global__ void k_defer_vec(const double* __restrict__ H, const double* __restrict__ M,
-                            const double* __restrict__ cmat, const double* __restrict__ w, int r,
-                            const GrouseState* __restrict__ st, double* __restrict__ hw,
-                            double* __restrict__ mw, double* __restrict__ dots,
-                            const double* __restrict__ NT, double* __restrict__ nw) {
-  defer_vec_block(blockIdx.x, H, M, cmat, w, r, st, hw, mw, dots, NT, nw);
 }
 
 // one launch for the two independent consumers of the solve: the residual
@@ -2002,17 +1930,6 @@ __global__ void k_ctil(const double* __restrict__ NT, const double* __restrict__
 
 __global__ void k_reset_terms(GrouseState* __restrict__ st) { st->nterms = 0; }
 
-__global__ void k_flush_reset(double* __restrict__ M, double* __restrict__ X,
-                              double* __restrict__ Yt, int r, GrouseState* __restrict__ st) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < (int64_t)r * r) M[e] = (e / r == e % r) ? 1.0 : 0.0;
-  if (e < (int64_t)r * kDeferCap) {
-    X[e] = 0.0;
-    Yt[e] = 0.0;
-  }
-  if (e == 0) st->nterms = 0;
-}
-
 // X <- X L^{-T} for the lower Cholesky factor L stored in G (ld = r + 1):
 // row i solves y L^T = x, i.e. L y^T = x^T (forward substitution).  One
 // warp per row, lanes split the dot products.
@@ -2033,15 +1950,6 @@ __global__ void k_trsm_lt(double* __restrict__ X, int64_t v, int r, const double
     __syncwarp();
   }
   for (int c = lane; c < r; c += 32) X[i * r + c] = y[c];
-}
-
-__global__ void k_gather_vals(const double* __restrict__ t, const int32_t* __restrict__ idx, int k,
-                              double* __restrict__ vals, double* __restrict__ aug, int64_t ldaug) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= k) return;
-  const double x = t[idx[i]];
-  vals[i] = x;
-  if (aug) aug[(int64_t)i * ldaug] = x;
 }
 
 // out = max |G[i][j] - delta_ij| over the leading r x r block (ld = r + 1)
@@ -2806,33 +2714,6 @@ cudaError_t launch_sparse_terms_dense(double* out, int64_t ldo, int r, int k, co
   return cudaSuccess;
 }
 
-cudaError_t launch_sparse_terms(double* out, int64_t ldo, int r, const int32_t* rows_sorted, int k,
-                                const int32_t* d_idx, const double* d_val, const double* cmat,
-                                const GrouseState* st, int dense, cudaStream_t s) {
-  return launch_pdl(k_sparse_terms, dim3(kDeferCap, (unsigned)((k + 255) / 256)), dim3(256), 0, s,
-                    out, ldo, r, rows_sorted, k, d_idx, d_val, cmat, st, dense);
-}
-
-cudaError_t launch_gather_urows(const double* U, int r, const int32_t* idx, int k, double* out,
-                                cudaStream_t s) {
-  const int64_t n = (int64_t)k * r;
-  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, r);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_urows_ld(const double* U, int r, const int32_t* idx, int k, double* out,
-                                   int64_t ldo, cudaStream_t s) {
-  const int64_t n = (int64_t)k * r;
-  k_gather_urows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U, r, idx, k, out, ldo);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_vals_aug(const double* t, const int32_t* idx, int k, double* vals,
-                                   double* aug, int64_t ldaug, cudaStream_t s) {
-  k_gather_vals<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(t, idx, k, vals, aug, ldaug);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_resid_defer_vec(const double* U, int64_t ldu, int r, int k, const double* vals,
                                    const double* w, double* resid, double* sums, const double* H,
                                    const double* M, const double* cmat, const GrouseState* st,
@@ -2855,15 +2736,6 @@ cudaError_t launch_gather_urows_vals(const double* U, int r, const int32_t* idx,
   cudaError_t e = launch_pdl(k_gather_urows_vals, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
                              s, U, r, idx, k, out, ldo, t, vals, zero8, aug);
   if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_defer_vec(const double* H, const double* M, const double* cmat,
-                             const double* w, int r, const GrouseState* st, double* hw, double* mw,
-                             double* dots, cudaStream_t s, const double* NT, double* nw) {
-  const int tasks = 3 * r + kDeferCap;
-  k_defer_vec<<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(H, M, cmat, w, r, st, hw, mw, dots, NT,
-                                                         nw);
   return cudaGetLastError();
 }
 
@@ -2912,13 +2784,6 @@ cudaError_t launch_late_chain(const double* A, int64_t lda, int r, int k, const 
   const int nrb = (k + 7) / 8, ncb = (r + 1 + 7) / 8;
   return launch_pdl(k_late, dim3((unsigned)(nrb + ncb)), dim3(256), 0, s, A, lda, r, k, G, w,
                     d_val, pos, list, count, b, st, look, av, corr, nrb);
-}
-
-cudaError_t launch_flush_reset(double* M, double* X, double* Yt, int r, GrouseState* st,
-                               cudaStream_t s) {
-  const int64_t n = (int64_t)r * std::max(r, kDeferCap);
-  k_flush_reset<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(M, X, Yt, r, st);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_force_halt(GrouseState* st, int64_t step, cudaStream_t s) {
