@@ -80,8 +80,7 @@ int rmx_rapid_stats(const double* x, int64_t v, int32_t n, int32_t n1, const int
   RCUDA(cudaMemsetAsync(key.p, 0xff, sizeof(unsigned long long), s));
   RCUDA(launch_rapid_stats(x, n, n1, orders, omegas, L, k, t_out, key.p, s));
   unsigned long long hk = 0;
-  RCUDA(cudaMemcpyAsync(&hk, key.p, sizeof(hk), cudaMemcpyDeviceToHost, s));
-  RCUDA(cudaStreamSynchronize(s));
+  RCUDA(read_small_sync(&hk, key.p, sizeof(hk), s));
   if (hk != ~0ull) {
     st->perm = (int64_t)(hk >> 32);
     st->voxel = (int64_t)(hk & 0xffffffffu);  // index into the permutation's Omega
@@ -567,18 +566,27 @@ int rmx_normal_stream_fill_device(rmx_normal_stream* h, int64_t count, double* d
   RCUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   bool used[2] = {false, false};
   int rc = RMX_OK;
+  const bool trace = getenv("RMX_TRACE_BASIS") != nullptr;  // diagnostics: where the time goes
+  double t_wait = 0.0, t_draw = 0.0, t_issue = 0.0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
   for (int64_t lo = 0, i = 0; lo < count && rc == RMX_OK; lo += half, ++i) {
     const int b = (int)(i & 1);
     const int64_t n = std::min(half, count - lo);
     double* buf = pinned + (size_t)b * half;
+    const auto t0 = now();
     if (used[b] && cudaEventSynchronize(ev[b]) != cudaSuccess) {
       rc = rset(st, RMX_E_CUDA, "normal upload failed");
       break;
     }
+    const auto t1 = now();
     if (rmx_normal_stream_fill(h, n, buf) != 0) {
       rc = rset(st, RMX_E_USAGE, "normal stream fill failed");
       break;
     }
+    const auto t2 = now();
     if (cudaMemcpyAsync(dev_out + lo, buf, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, s) !=
             cudaSuccess ||
         cudaEventRecord(ev[b], s) != cudaSuccess) {
@@ -586,7 +594,19 @@ int rmx_normal_stream_fill_device(rmx_normal_stream* h, int64_t count, double* d
       break;
     }
     used[b] = true;
+    if (trace) {
+      const double di = secs(t2, now());
+      t_wait += secs(t0, t1);
+      t_draw += secs(t1, t2);
+      t_issue += di;
+      if (di > 0.005)
+        fprintf(stderr, "[basis-init] block %lld: copy issue took %.1f ms (draw %.1f ms)\n",
+                (long long)i, 1e3 * di, 1e3 * secs(t1, t2));
+    }
   }
+  if (trace)
+    fprintf(stderr, "[basis-init] ring waits %.3f s, draws %.3f s, copy issue %.3f s\n", t_wait,
+            t_draw, t_issue);
   cudaStreamSynchronize(s);  // the ring is the caller's: no copy may still read it
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
@@ -608,8 +628,7 @@ int rmx_orthonormalize(double* u, int64_t v, int32_t r, int32_t force, double* d
   RCUDA(launch_dsyrk_rm((int)v, r, u, r, G.p, r + 1, s));
   RCUDA(launch_max_dev_identity(G.p, r, dev.p, s));
   double h = 0.0;
-  RCUDA(cudaMemcpyAsync(&h, dev.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-  RCUDA(cudaStreamSynchronize(s));
+  RCUDA(read_small_sync(&h, dev.p, sizeof(double), s));
   if (drift) *drift = h;
   if (!force && h <= 1e-8) return RMX_OK;
   for (int pass = 0; pass < 2; ++pass) {
@@ -890,9 +909,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       ~Acc() { a += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
     } acc{host_wait_s, w0};
     RCUDA(launch_h_drift(H.p, r, hdrift.p, s));
-    RCUDA(cudaMemcpyAsync(h, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
-    RCUDA(cudaMemcpyAsync(&hdrift_host, hdrift.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-    RCUDA(cudaStreamSynchronize(s));
+    RCUDA(read_small_sync(h, gst.p, sizeof(GrouseState), s));
+    RCUDA(read_small_sync(&hdrift_host, hdrift.p, sizeof(double), s));
     return RMX_OK;
   };
   int passes = 0, converged = 0;
@@ -1139,8 +1157,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   }
   {
     GrouseState hs;
-    RCUDA(cudaMemcpyAsync(&hs, gst.p, sizeof(GrouseState), cudaMemcpyDeviceToHost, s));
-    RCUDA(cudaStreamSynchronize(s));
+    RCUDA(read_small_sync(&hs, gst.p, sizeof(GrouseState), s));
     if (int rc = flush(hs.nterms)) return rc;
     if (int rc = rebase()) return rc;
     if (ubase != u) {  // an odd number of rebases: the result belongs in the caller's buffer

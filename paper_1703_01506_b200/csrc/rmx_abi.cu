@@ -683,8 +683,7 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
   ra.argmax_out = argmax_out;
   RMX_CUDA(launch_refine(ra, s));
   NaiveCounters hc;
-  RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
-  RMX_CUDA(cudaStreamSynchronize(s));
+  RMX_CUDA(read_small_sync(&hc, ws.counters(), sizeof(hc), s));
   int64_t overflow_perms = 0;
   if (hc.susp_count > (unsigned)kSuspectCap) {
     // too many near-degenerate entries to list: exact fp64 evaluation of everything
@@ -699,8 +698,7 @@ int rmx_naive_finish(const double* x, int64_t v, int32_t n, int32_t n1, const in
     overflow_perms = hc.overflow_count;
   }
   if (overflow_perms > 0) {
-    RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
-    RMX_CUDA(cudaStreamSynchronize(s));
+    RMX_CUDA(read_small_sync(&hc, ws.counters(), sizeof(hc), s));
   }
   if (stats) {
     stats->suspects = hc.susp_count;
@@ -734,8 +732,7 @@ int rmx_naive_maxnull(const double* x, int64_t v, int32_t n, int32_t n1, const i
                                 ws.counters(), s, st))
       return rc;
     NaiveCounters hc;
-    RMX_CUDA(cudaMemcpyAsync(&hc, ws.counters(), sizeof(hc), cudaMemcpyDeviceToHost, s));
-    RMX_CUDA(cudaStreamSynchronize(s));
+    RMX_CUDA(read_small_sync(&hc, ws.counters(), sizeof(hc), s));
     if (stats) {
       memset(stats, 0, sizeof(*stats));
       stats->overflow_perms = L;
@@ -1213,8 +1210,7 @@ int rmx_tstat_exact(const double* x, int64_t v, int32_t n, int32_t n1, const int
   RMX_CUDA(launch_exact_rows(xt, v, n, n1, orders, nullptr, L, 0, t_out, ld, nullptr, nullptr, nvb,
                              c, s));
   NaiveCounters hc;
-  RMX_CUDA(cudaMemcpyAsync(&hc, c, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  RMX_CUDA(cudaStreamSynchronize(s));
+  RMX_CUDA(read_small_sync(&hc, c, sizeof(hc), s));
   cudaFreeAsync(xt, s);
   cudaFreeAsync(c, s);
   return report_degenerate(x, v, n, n1, orders, hc.deg_key, s, st);

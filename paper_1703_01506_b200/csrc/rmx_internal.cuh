@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 
 namespace rmx {
 
@@ -217,5 +218,35 @@ cudaError_t launch_plan_orders(uint64_t seed, int64_t lo, int64_t count, int n, 
 cudaError_t launch_omega_draws(uint64_t seed, uint32_t domain, int64_t lo, int64_t count,
                                int has_extra, uint32_t extra, uint32_t v, int k, int32_t* out,
                                cudaStream_t s);
+
+// A small device-to-host read followed by a stream synchronisation, through a
+// page-locked bounce buffer.  cudaMemcpyAsync into pageable memory (a stack
+// variable) returns only once the copy is done and holds the context lock
+// while it waits for the stream's earlier work, which stalls every other
+// thread's CUDA calls for that long (measured: the BASIS_INIT normal stream's
+// upload thread blocked for the 284 ms of the training-column kernel).  With a
+// page-locked destination the copy is enqueued at once and the wait happens in
+// cudaStreamSynchronize, which does not hold the lock.
+inline cudaError_t read_small_sync(void* dst, const void* dev, size_t bytes, cudaStream_t s) {
+  constexpr size_t kCap = 4096;
+  static thread_local void* bounce = nullptr;
+  if (bytes > kCap) {
+    cudaError_t e = cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, s);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+  }
+  if (!bounce) {
+    cudaError_t e = cudaHostAlloc(&bounce, kCap, cudaHostAllocDefault);  // once per host thread
+    if (e != cudaSuccess) {
+      bounce = nullptr;
+      return e;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(bounce, dev, bytes, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  std::memcpy(dst, bounce, bytes);
+  return cudaSuccess;
+}
 
 }  // namespace rmx

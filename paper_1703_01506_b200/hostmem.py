@@ -154,6 +154,7 @@ def wait_inflight() -> None:
 
 
 _STAGE: dict = {}
+_STAGE_LOCK = threading.Lock()
 
 
 def upload_staged(arr: np.ndarray, device, stream=None):
@@ -171,15 +172,16 @@ def upload_staged(arr: np.ndarray, device, stream=None):
         registered = owner.ctypes.data in _REGISTERED
     if registered or arr.nbytes < _MIN_REGISTER_BYTES:
         return to_device(arr, device, stream)
-    ring = _STAGE.get("ring")
-    if ring is None:
-        ring = pinned_empty((64 << 20,), np.uint8)
-        _STAGE["ring"] = ring
     out = torch.empty(arr.shape, dtype=_torch_dtype(arr.dtype), device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
     st = nat.Status()
-    rc = nat.load().rmx_upload_staged(arr.ctypes.data, arr.nbytes, out.data_ptr(),
-                                      ring.ctypes.data, ring.nbytes, nat.stream_handle(s),
-                                      ctypes.byref(st))
+    with _STAGE_LOCK:  # one ring: uploads from different host threads take turns
+        ring = _STAGE.get("ring")
+        if ring is None:
+            ring = pinned_empty((64 << 20,), np.uint8)
+            _STAGE["ring"] = ring
+        rc = nat.load().rmx_upload_staged(arr.ctypes.data, arr.nbytes, out.data_ptr(),
+                                          ring.ctypes.data, ring.nbytes, nat.stream_handle(s),
+                                          ctypes.byref(st))
     nat.raise_for(rc, st)
     return out

@@ -367,8 +367,13 @@ def _to_dev_async(draw, dev):
 
     def work():
         a = draw()
+        # through the page-locked staging ring: a pageable copy of this size
+        # (1.7 GB of SHIFT_GAP normals at config 5) holds the CUDA context lock
+        # while the driver stages it, stalling the GROUSE launch thread
+        from .hostmem import upload_staged
+
         with torch.cuda.stream(side):
-            return _to_dev(a, dev)
+            return upload_staged(np.ascontiguousarray(a), dev, side)
 
     join = _host_async(work)
 
