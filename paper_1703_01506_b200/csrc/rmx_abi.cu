@@ -491,6 +491,20 @@ int rmx_device_check(int device, int32_t* sm_count, rmx_status* st) {
       cudaSetDeviceFlags(cudaDeviceScheduleBlockingSync);
     cudaGetLastError();  // best effort: an unchangeable flag is not an error
   }
+  // The engine's scratch comes from the stream-ordered pool (cudaMallocAsync).
+  // By default the pool returns unused memory to the driver at every
+  // synchronisation, so each call would map its GB-sized buffers again
+  // (physical allocation: tens to hundreds of ms, and variable); keep it
+  // cached instead (RMX_POOL_TRIM=1 restores the default).
+  const char* trim = getenv("RMX_POOL_TRIM");
+  if (!(trim && atoi(trim) == 1)) {
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   return RMX_OK;
 }
 
