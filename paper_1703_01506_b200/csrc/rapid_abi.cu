@@ -942,8 +942,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
   const char* la_env = getenv("RMX_GROUSE_LOOKAHEAD");
   // RMX_GROUSE_PROFILE=2: marks on the main stream of the look-ahead chain
   const bool prof_la = prof.on && atoi(getenv("RMX_GROUSE_PROFILE")) == 2;
-  const bool lookahead = use_cg && r <= 510 /* k_late's shared-memory partials */ &&
-                         (!prof.on || prof_la) && !(la_env && atoi(la_env) == 0);
+  const bool lookahead = use_cg && (!prof.on || prof_la) && !(la_env && atoi(la_env) == 0);
   struct LookStreams {
     cudaStream_t s2 = nullptr, s3 = nullptr;
     cudaEvent_t evE[2] = {nullptr, nullptr}, evD = nullptr, evP = nullptr;

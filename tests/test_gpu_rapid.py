@@ -394,6 +394,24 @@ def test_grouse_halt_redraw_at_checkpoints(oracle_mod, halts, chain, monkeypatch
     assert all(np.array_equal(a, b) for a, b in zip(res.final_omegas, om))
 
 
+@pytest.mark.parametrize("v,ell,r,eta", [(40000, 100, 100, 0.02), (3000, 40, 40, 1.0)])
+def test_grouse_lookahead_matches_serial_chain(oracle_mod, v, ell, r, eta, monkeypatch):
+    """The look-ahead chain (update h + 1's rows and Gram formed before update
+    h's term; the term enters as a rank-1 correction built from G w and the
+    rows shared with the previous Omega) against the serial chain on the same
+    draws: several flush blocks and pass ends at r = 100, and the exact regime
+    (eta = 1: every row is shared with the previous update)."""
+    t_ex, k, r, seed = _grouse_case(v=v, ell=ell, r=r, eta=eta, seed=123)
+    res_la = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=3)
+    monkeypatch.setenv("RMX_GROUSE_LOOKAHEAD", "0")
+    res_se = rmx.train_basis(t_ex, k=k, rank=r, seed=seed, max_passes=3)
+    assert res_la.passes == res_se.passes == 3 and res_la.updates == res_se.updates == 3 * ell
+    assert np.allclose(res_la.pass_residuals, res_se.pass_residuals, rtol=1e-9, atol=0)
+    cos = oracle_mod.principal_cosines(res_la.basis.matrix, res_se.basis.matrix)
+    assert cos.min() > 1 - 1e-10
+    assert all(np.array_equal(a, b) for a, b in zip(res_la.final_omegas, res_se.final_omegas))
+
+
 def test_run_rapid_bit_reproducible():
     """Two run_rapid calls on the same input give the same bits: GROUSE has no
     floating-point atomics (deterministic split-K reductions, sparse terms
