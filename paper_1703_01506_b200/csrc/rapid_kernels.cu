@@ -758,7 +758,8 @@ template <int NC>
 __device__ __forceinline__ void cg_exchange_w0(const double* v, int nr, int r0, int rtot,
                                                double* full, double a, double b, double c,
                                                double* slots, uint64_t* bars, int par,
-                                               uint32_t& xph, double& A, double& B, double& C) {
+                                               uint32_t& xph, double& A, double& B, double& C,
+                                               double vreg = 0.0, bool from_reg = false) {
   const uint32_t me = cluster_ctarank();
   const bool tm = g_cg_timing && me == 0 && threadIdx.x == 0;
   const long long c0 = tm ? clock64() : 0;
@@ -776,7 +777,7 @@ __device__ __forceinline__ void cg_exchange_w0(const double* v, int nr, int r0, 
   if (tid == 0) mbar_expect_tx(bar, (uint32_t)(((v ? rtot : 0) + 3 * NC) * sizeof(double)));
   if (tid < 32) {
     if (v && lane < nr) {
-      const double vi = v[lane];
+      const double vi = from_reg ? vreg : v[lane];  // the lane's row: register or shared memory
 #pragma unroll 4
       for (int d = 0; d < NC; ++d) st_async_f64(full + r0 + lane, d, vi, bar);
     }
@@ -1036,6 +1037,69 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_solve(const double* __restric
   const bool tm = g_cg_timing && cluster_ctarank() == 0 && tid == 0;
   unsigned long long wall2 = 0;
   if (wall0) wall2 = globaltimer_ns();
+  if constexpr (RL > 0) {
+    // Register variant: nr <= 32, so the CTA's rows of every iteration vector
+    // live in warp 0's lanes -- kept in registers across the loop (the shared-
+    // memory copies cost ~850 of ~4,000 cycles per iteration in loads, stores
+    // and their latencies); only the matvec's output passes through shared
+    // memory.  Same recurrences; x is written back for the final check.
+    const bool act = tid < nr;
+    double xr = 0.0, rr = 0.0, ur = 0.0, wr = 0.0, zr = 0.0, qr = 0.0, sr = 0.0, pp = 0.0,
+           dr = 0.0;
+    if (act) {
+      xr = x[tid];
+      rr = rv[tid];
+      ur = u[tid];
+      wr = w[tid];
+      zr = z[tid];
+      qr = q[tid];
+      sr = sv[tid];
+      pp = p[tid];
+      dr = dinv[tid];
+    }
+    for (; it < r && !converged; ++it) {
+      const double mr = wr * dr;
+      double GAM, DEL, RR;
+      cg_exchange_w0<NC>(m, nr, r0, r, full + par * r, rr * ur, wr * ur, rr * rr,
+                         slots + par * 3 * NC, xbar, par, xph, GAM, DEL, RR, mr, true);
+      const int used = par;
+      par ^= 1;
+      if (RR <= stop) {
+        converged = 1;
+        break;
+      }
+      double alpha, beta;
+      if (it == 0) {
+        beta = 0.0;
+        alpha = DEL != 0.0 ? GAM / DEL : 0.0;
+      } else {
+        beta = GAM / gamma_prev;
+        const double den = DEL - beta * GAM / alpha_prev;
+        alpha = den != 0.0 ? GAM / den : 0.0;
+      }
+      if (!(alpha == alpha) || alpha == 0.0) break;  // breakdown: not converged
+      gamma_prev = GAM;
+      alpha_prev = alpha;
+      const long long m0 = tm ? clock64() : 0;
+      matvec(full + used * r, nv);  // n = A m (ends with a block barrier)
+      if (tm) atomicAdd(&g_cg_phase[4], (unsigned long long)(clock64() - m0));
+      if (act) {
+        const double nvr = nv[tid];
+        zr = fma(beta, zr, nvr);
+        qr = fma(beta, qr, mr);
+        sr = fma(beta, sr, wr);
+        pp = fma(beta, pp, ur);
+        xr = fma(alpha, pp, xr);
+        rr = fma(-alpha, sr, rr);
+        ur = fma(-alpha, qr, ur);
+        wr = fma(-alpha, zr, wr);
+      }
+      // the next matvec overwrites nv only after every peer's rows have
+      // arrived, this CTA's included, and warp 0 posts them after this read
+    }
+    if (act) x[tid] = xr;
+    __syncthreads();
+  } else
   for (; it < r && !converged; ++it) {
     const long long d0 = tm ? clock64() : 0;
     double pg = 0.0, pd = 0.0, pr = 0.0;
