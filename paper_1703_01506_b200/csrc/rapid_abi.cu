@@ -777,10 +777,8 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     prof.ev.resize((size_t)PhaseProf::kPh * PhaseProf::kN);
     for (auto& e : prof.ev) RCUDA(cudaEventCreate(&e));
   }
-  // early chain of an update (everything before the solve): rows of U on
-  // Omega with the deferred terms, and the Gram, into buffer `b`, on stream
-  // `se`.  `pending` bounds the deferred terms it sees (updates since the flush).
   bool m_identity = true;  // no update applied since the last rebase (M = I exactly)
+  // b encodes the buffers of an update: rows / values b >> 1 (of 3), Gram b & 1.
   // the raw rows of U_base on Omega (and t[Omega] into column r of the product's
   // rows): depends only on U_base, so the look-ahead loop issues it one update
   // further ahead than the rest of the early chain
@@ -792,15 +790,17 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                                    ug.p + (size_t)bu * ugsz));
     return RMX_OK;
   };
-  auto enqueue_early = [&](int i, const int32_t* idx, int pending, int b, cudaStream_t se,
-                           bool marks, const int32_t* idx_prev = nullptr,
-                           bool gathered = false) -> int {
+  // early chain of an update (everything before the solve) on stream `se`: the
+  // rows of U on Omega (product with M, deferred sparse terms) and their Gram;
+  // idx_prev (look-ahead): the previous update's Omega, for k_isect; gathered:
+  // the raw rows were issued ahead (enqueue_gather)
+  auto enqueue_early = [&](int i, const int32_t* idx, int b, cudaStream_t se, bool marks,
+                           const int32_t* idx_prev = nullptr, bool gathered = false) -> int {
     const double* trow = t + (int64_t)i * v;
     const int bu = b >> 1, bg = b & 1;  // rows / values buffer (of 3), Gram buffer (of 2)
     double* ugb = ug.p + (size_t)bu * ugsz;
     // U_Omega = ubase[Omega] M: the raw rows, then one k x r x r DGEMM; right
     // after a rebase M = I and the rows are gathered in place
-    (void)pending;
     if (m_identity && !gathered) {
       RCUDA(launch_gather_urows_vals(ubase, r, idx, k, ugb, lu, trow, vals.p + (size_t)bu * k,
                                      marks ? sums.p : nullptr, se));
@@ -890,7 +890,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
                    ? tglob : -1;
     prof.slot = 0;
     prof.mark(s);
-    if (int rc = enqueue_early(i, idx, (int)(tglob % kDeferCap), 0, s, true)) return rc;
+    if (int rc = enqueue_early(i, idx, 0, s, true)) return rc;
     (void)p;
     return enqueue_main(i, idx, tglob, chol, 0, false, nullptr);
   };
@@ -983,15 +983,14 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     // rows / values are triple-buffered: buffer h % 3 was last read by update
     // h - 3, whose H update (stream s3) completed before update h - 2's
     // residual kernel, so only evD orders this chain
-    // terms from updates before h - 1 inclusive when h follows an update in
-    // flight (its own term comes with the late chain); every term when cold
-    const int pending = (int)((have_early ? h - 1 : h) % kDeferCap);
+    // the chain sees the terms of the updates applied so far: all but update
+    // h - 1's when that update is in flight (its term comes with the late
+    // chain), every term when cold
     const int64_t hm = h - 1;  // the update in flight whose term the late chain will add
-    const int32_t* idx_prev =
-        have_early ? omegas0 + ((hm / ell) * ell + hm % ell) * k : nullptr;
+    const int32_t* idx_prev = have_early ? omegas0 + hm * k : nullptr;
     const bool gathered = pregathered == h;
     if (!have_early) pregathered = -1;  // cold start: nothing issued ahead survives
-    if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k, pending,
+    if (int rc = enqueue_early(hi, omegas0 + ((int64_t)hp * ell + hi) * k,
                                (int)((h % 3) * 2 + (h & 1)), ls.s2, false, idx_prev,
                                have_early && gathered))
       return rc;
