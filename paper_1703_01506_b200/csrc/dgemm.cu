@@ -273,8 +273,12 @@ int pick_split(int64_t tiles, int kk) {
     const char* e = getenv("RMX_DGEMM_SPLIT_MAX");  // experiments: cap the cluster split
     return e ? std::max(1, std::min(8, atoi(e))) : 8;
   }();
+  static const int64_t lim = [] {
+    const char* e = getenv("RMX_DGEMM_SPLIT_CTAS");  // experiments: CTA budget of the split
+    return e ? (int64_t)std::max(148, atoi(e)) : (int64_t)4 * 148;
+  }();
   int S = 1;
-  while (S < cap && tiles * S * 2 <= 4 * 148 && kk / (2 * S) >= 2 * kBK) S *= 2;
+  while (S < cap && tiles * S * 2 <= lim && kk / (2 * S) >= 2 * kBK) S *= 2;
   return S;
 }
 

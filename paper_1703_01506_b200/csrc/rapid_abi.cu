@@ -819,7 +819,7 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
     if (marks) prof.mark(se);
     // look-ahead: the rows this update shares with the previous one (the late
     // chain adds the previous update's sparse term on them)
-    if (idx_prev)
+    if (idx_prev && !gathered)  // (issued with the rows when they were gathered ahead)
       RCUDA(launch_isect(idx, idx_prev, k, ipos.p + (size_t)bu * k, ilist.p + (size_t)bu * k,
                          icount.p + bu, se));
     return RMX_OK;
@@ -1005,6 +1005,9 @@ int rmx_grouse_train(const double* t, int64_t v, int32_t ell, int32_t r, int32_t
       if (int rc = enqueue_gather((int)(g % ell), omegas0 + g * k, (int)((g % 3) * 2 + (g & 1)),
                                   ls.s2, false))
         return rc;
+      // and the rows it shares with update h (static Omega lists): off both chains
+      RCUDA(launch_isect(omegas0 + g * k, omegas0 + h * k, k, ipos.p + (size_t)(g % 3) * k,
+                         ilist.p + (size_t)(g % 3) * k, icount.p + (g % 3), ls.s2));
       pregathered = g;
     }
     return RMX_OK;
