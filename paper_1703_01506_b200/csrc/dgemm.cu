@@ -32,7 +32,11 @@ namespace {
 
 constexpr int kBM = 64, kBN = 64, kBK = 16, kT = 128;
 constexpr int kLd = 72;                                      // smem row stride (doubles)
-constexpr int kStages = 4;                                   // cp.async ring depth
+// three stages (54 KB) and <= 128 registers: four CTAs per SM.  The k x r x r
+// product of a GROUSE update has 406 CTAs and shares the GPU with the solve's
+// 16-SM cluster; at three CTAs per SM (four stages, 162 registers) ten of them
+// fell into a second wave (68 us in situ against 47 us alone; now 56 us)
+constexpr int kStages = 3;                                   // cp.async ring depth
 constexpr int kTileD = kBK * kLd;                            // doubles per operand tile
 constexpr int kStage = kStages * 2 * kTileD;                 // doubles: the A + B ring
 constexpr int kPart = kBM * (kBN + 1);                       // doubles: the CTA's partial tile
@@ -65,7 +69,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 // SYRK = true:  C (n x n, symmetric, both halves written) = A^T A with A
 //               (kk x n) row-major; blockIdx.x enumerates the lower tiles.
 template <bool SYRK>
-__global__ void __launch_bounds__(kT) k_dgemm_rm(int64_t m, int n, int kk,
+__global__ void __launch_bounds__(kT, 4) k_dgemm_rm(int64_t m, int n, int kk,
                                                  const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb,
                                                  double* __restrict__ C, int64_t ldc, int accum) {
