@@ -82,16 +82,25 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run_nvml(self) -> bool:
-        """Poll NVML every 10 ms (the timed region of a step is ~35 ms)."""
+    def _init_nvml(self):
+        """NVML is initialised before the timed region starts (the first
+        nvmlInit of a process can take longer than the whole region, which
+        left a run unsampled)."""
         try:
             import pynvml
 
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            return pynvml, h, mx
         except Exception:
+            return None
+
+    def _run_nvml(self) -> bool:
+        """Poll NVML every 10 ms (the timed region of a step is ~35 ms)."""
+        if self._nvml is None:
             return False
+        pynvml, h, mx = self._nvml
         get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
         bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
@@ -122,6 +131,7 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        self._nvml = self._init_nvml()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
