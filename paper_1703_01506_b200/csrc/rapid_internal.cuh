@@ -96,6 +96,7 @@ struct GrouseState {
   unsigned int hg_done;  // blocks of k_h_g_part finished (last-block reduction)
   unsigned int da_done;  // blocks of k_defer_apply finished (last block counts the term)
   double pend_g;   // the pending update's inverse factor: (I + a w b^T)^-1 = I - pend_g w b^T
+  double hdrift;   // max |H - I| (k_h_drift at a checkpoint; read with the rest of the state)
 };
 // look-ahead GROUSE: what update h decided, for the late chain of update h + 1
 // (written by k_grouse_post_m, read by k_late / k_cg_solve)

@@ -249,4 +249,39 @@ inline cudaError_t read_small_sync(void* dst, const void* dev, size_t bytes, cud
   return cudaSuccess;
 }
 
+// The same read, but the host polls an event instead of sleeping in
+// cudaStreamSynchronize: with cudaDeviceScheduleBlockingSync (set so waiting
+// threads do not spin beside the serial BASIS_INIT draw) every wake-up costs
+// ~50-100 us, which a latency-critical loop (GROUSE's checkpoints, ~360 per
+// training) should not pay.
+inline cudaError_t read_small_spin(void* dst, const void* dev, size_t bytes, cudaStream_t s) {
+  constexpr size_t kCap = 4096;
+  static thread_local void* bounce = nullptr;
+  static thread_local cudaEvent_t ev = nullptr;
+  if (bytes > kCap) return read_small_sync(dst, dev, bytes, s);
+  if (!bounce) {
+    cudaError_t e = cudaHostAlloc(&bounce, kCap, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      bounce = nullptr;
+      return e;
+    }
+  }
+  if (!ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      ev = nullptr;
+      return e;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(bounce, dev, bytes, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(ev, s);
+  if (e != cudaSuccess) return e;
+  while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+  }
+  if (e != cudaSuccess) return e;
+  std::memcpy(dst, bounce, bytes);
+  return cudaSuccess;
+}
+
 }  // namespace rmx
