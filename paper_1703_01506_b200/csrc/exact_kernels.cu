@@ -672,6 +672,47 @@ __global__ void k_exact_rows(const double* __restrict__ xt, int64_t v, int n, in
   }
 }
 
+// Many permutations x all voxels with the statistics written out (the
+// training columns of RapidPT, a materialised T): thread per voxel like
+// k_exact_rows, but a block first stages its kVsVox voxels' rows in shared
+// memory ([subject][voxel]: conflict-free for a common subject index) and then
+// walks a chunk of permutations over them, so X is read once per chunk of
+// permutations instead of once per permutation (k_exact_rows<true> re-read all
+// of X^T, 1.7 GB at config 5, for each of the 400 training permutations: 672 GB).
+// Same welch_exact arithmetic, so the same bits.  grid (voxel blocks, chunks).
+constexpr int kVsVox = 64;
+
+__global__ void __launch_bounds__(kVsVox) k_exact_rows_vstage(
+    const double* __restrict__ x, int64_t v, int n, int n1, const int16_t* __restrict__ orders,
+    int64_t nperm, int perms_per_chunk, double* __restrict__ t_out, int64_t ld,
+    NaiveCounters* counters) {
+  extern __shared__ __align__(16) unsigned char vsm[];
+  double* xs = reinterpret_cast<double*>(vsm);                         // [n][kVsVox]
+  int16_t* ord = reinterpret_cast<int16_t*>(xs + (size_t)n * kVsVox);  // [n]
+  const int64_t j0 = (int64_t)blockIdx.x * kVsVox;
+  const int nv = (int)min((int64_t)kVsVox, v - j0);
+  const int t = threadIdx.x;
+  for (int e = t; e < nv * n; e += kVsVox) {  // rows are contiguous in X: coalesced reads
+    const int jj = e / n, k = e - jj * n;
+    xs[(size_t)k * kVsVox + jj] = x[(j0 + jj) * n + k];
+  }
+  const int64_t p0 = (int64_t)blockIdx.y * perms_per_chunk;
+  const int64_t p1 = min(nperm, p0 + perms_per_chunk);
+  for (int64_t p = p0; p < p1; ++p) {
+    __syncthreads();  // the rows are staged / the previous labelling is done with
+    for (int k = t; k < n; k += kVsVox) ord[k] = orders[p * n + k];
+    __syncthreads();
+    if (t < nv) {
+      const WelchExact r = welch_exact(xs + t, kVsVox, ord, n1, n - n1);
+      if (r.degenerate) {
+        if (counters) note_degenerate(counters, p, j0 + t);
+      } else {
+        t_out[p * ld + j0 + t] = r.t;
+      }
+    }
+  }
+}
+
 __global__ void k_exact_reduce(const double* part_val, const int32_t* part_idx, int nvb,
                                const int32_t* perm_list, int64_t nperm, double* max_out,
                                int32_t* argmax_out) {
@@ -774,6 +815,29 @@ cudaError_t launch_transpose(const double* x, int64_t v, int n, double* xt, cuda
   dim3 grid((unsigned)((v + 31) / 32), (unsigned)((n + 31) / 32));
   k_transpose<<<grid, dim3(32, 8), 0, s>>>(x, v, n, xt);
   return cudaGetLastError();
+}
+
+cudaError_t launch_exact_rows_vstage(const double* x, int64_t v, int n, int n1,
+                                     const int16_t* orders, int64_t nperm, double* t_out,
+                                     int64_t ld, NaiveCounters* counters, cudaStream_t s) {
+  if (nperm <= 0) return cudaSuccess;
+  const size_t smem = (size_t)n * kVsVox * sizeof(double) + (size_t)n * sizeof(int16_t);
+  cudaError_t e = cudaFuncSetAttribute(k_exact_rows_vstage,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t vblocks = (v + kVsVox - 1) / kVsVox;
+  // enough chunks to fill the GPU a few times over, at least 16 permutations each
+  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((nperm + 15) / 16, (8 * 148 + vblocks - 1) / vblocks));
+  chunks = std::min(chunks, 65535);
+  const int ppc = (int)((nperm + chunks - 1) / chunks);
+  chunks = (int)((nperm + ppc - 1) / ppc);
+  k_exact_rows_vstage<<<dim3((unsigned)vblocks, (unsigned)chunks), kVsVox, smem, s>>>(
+      x, v, n, n1, orders, nperm, ppc, t_out, ld, counters);
+  return cudaGetLastError();
+}
+
+bool exact_rows_vstage_supported(int n) {
+  return (size_t)n * kVsVox * sizeof(double) + (size_t)n * sizeof(int16_t) <= 200 * 1024;
 }
 
 cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1, const int16_t* orders,

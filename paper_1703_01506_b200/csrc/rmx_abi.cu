@@ -1215,6 +1215,19 @@ int rmx_tstat_exact(const double* x, int64_t v, int32_t n, int32_t n1, const int
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* xt = nullptr;
   NaiveCounters* c = nullptr;
+  // many labellings: the voxel-staged kernel reads X once per chunk of
+  // labellings (RMX_EXACT_VSTAGE=0: the thread-per-voxel kernel over X^T)
+  const char* vs_env = getenv("RMX_EXACT_VSTAGE");
+  if (L >= 16 && exact_rows_vstage_supported(n) && !(vs_env && atoi(vs_env) == 0)) {
+    RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(NaiveCounters), s));
+    RMX_CUDA(cudaMemsetAsync(c, 0, sizeof(NaiveCounters), s));
+    RMX_CUDA(cudaMemsetAsync(&c->deg_key, 0xff, sizeof(unsigned long long), s));
+    RMX_CUDA(launch_exact_rows_vstage(x, v, n, n1, orders, L, t_out, ld, c, s));
+    NaiveCounters hv;
+    RMX_CUDA(read_small_sync(&hv, c, sizeof(hv), s));
+    cudaFreeAsync(c, s);
+    return report_degenerate(x, v, n, n1, orders, hv.deg_key, s, st);
+  }
   RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xt), (size_t)v * n * sizeof(double), s));
   RMX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(NaiveCounters), s));
   RMX_CUDA(cudaMemsetAsync(c, 0, sizeof(NaiveCounters), s));

@@ -188,6 +188,12 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t s);
 cudaError_t launch_transpose(const double* x, int64_t v, int n, double* xt, cudaStream_t s);
 // exact statistic for perms `perm_list` (or all when null) x all voxels;
 // writes T (perm-major, ld) and/or per-perm max/argmax; reports degenerate.
+// every statistic of nperm labellings written to t_out (perm-major, ld), rows
+// staged per block of voxels (exact_kernels.cu: k_exact_rows_vstage); x row-major
+bool exact_rows_vstage_supported(int n);
+cudaError_t launch_exact_rows_vstage(const double* x, int64_t v, int n, int n1,
+                                     const int16_t* orders, int64_t nperm, double* t_out,
+                                     int64_t ld, NaiveCounters* counters, cudaStream_t s);
 cudaError_t launch_exact_rows(const double* xt, int64_t v, int n, int n1,
                              const int16_t* orders, const int32_t* perm_list, int64_t nperm,
                              int two_sided, double* t_out, int64_t ld, double* part_val,
